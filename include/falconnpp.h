@@ -1,0 +1,160 @@
+/*
+ * falconnpp.h -- C ABI of the B200-native Falconn++ hot path (libfalconnpp_b200.so).
+ *
+ * Drop-in boundary for the reference's index/query API.  The reference
+ * (/root/reference) ships only rotation.{hpp,cpp}, dataset.{hpp,cpp} and
+ * common.hpp; the index/query layer exists only as SPEC operations and as
+ * CMake entries for missing files (proj/CMakeLists.txt:27-31).
+ * Each entry point below names the reference interface it replaces.
+ *
+ * Conventions: plain pointers and sizes, no torch/CUDA types.  Every function
+ * returns FPP_OK or one FPP_ERR_* class; fpp_last_error() gives the message of
+ * the last failure on the calling thread (the reference throws
+ * std::invalid_argument with the same messages, e.g. dataset.cpp:10-18).
+ * Host buffers are read/written synchronously before return.  The library owns
+ * all device memory behind the opaque fpp_index.  A built index is immutable;
+ * concurrent fpp_query calls on one index are allowed.
+ * There is no CPU fallback: without a CUDA device every compute entry point
+ * returns FPP_ERR_CUDA.
+ */
+#ifndef FALCONNPP_H
+#define FALCONNPP_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPP_ABI_VERSION 1
+
+/* error classes ("one exit code per error class") */
+#define FPP_OK 0
+#define FPP_ERR_INVALID_ARGUMENT 1 /* invalid config: SPEC.md:234-236,249; rotation.cpp:42-49 */
+#define FPP_ERR_EMPTY_DATASET 2    /* SPEC.md:249; dataset.cpp:10-11 */
+#define FPP_ERR_DIMENSION 3        /* dimension mismatch: SPEC.md:325; dataset.cpp:62-65 */
+#define FPP_ERR_OUT_OF_RANGE 4     /* iProbes>NB, qProbes not in [L,L*NB] (:195-197), k>n (:325) */
+#define FPP_ERR_NON_FINITE 5       /* dataset.cpp:15-18 */
+#define FPP_ERR_ZERO_NORM 6        /* dataset.cpp:32 */
+#define FPP_ERR_CUDA 7             /* no device / CUDA runtime failure */
+#define FPP_ERR_OUT_OF_MEMORY 8
+#define FPP_ERR_UNSUPPORTED 9      /* valid per SPEC but outside the GPU path's envelope */
+
+/* IndexConfig, SPEC.md:233-236 (mode = falconnpp, centering off). */
+typedef struct fpp_params {
+  uint32_t L;        /* tables >= 1 */
+  uint32_t K;        /* concatenated cross-polytope hashes per table: 1 or 2 (SPEC l) */
+  uint32_t D;        /* projections per function, power of two, D <= d_pad (one block) */
+  uint32_t iprobes;  /* indexing probes, 1 <= iprobes <= NB */
+  uint32_t kappa;    /* limit-scaling floor, default 20 */
+  float alpha;       /* scaling factor, 0 < alpha <= 1 */
+  uint64_t seed;     /* master seed; stack (t,f) uses derive_seed(seed,t,f,0) */
+  int32_t device;    /* CUDA device ordinal (-1 = current) */
+  uint32_t id_offset;/* global id of local row 0 (sharded builds) */
+  uint64_t scratch_bytes; /* build scratch budget per pass (0 = auto) */
+} fpp_params;
+
+/* SearchResult.stats */
+typedef struct fpp_query_stats {
+  uint64_t probes;     /* P_q: buckets probed */
+  uint64_t entries;    /* E_q: kept entries walked in the probed buckets */
+  uint64_t candidates; /* U_q: unique ids scored (exact inner products) */
+} fpp_query_stats;
+
+/* per-kernel device time accumulated since the last reset (CUDA events) */
+typedef struct fpp_timings {
+  double hash_ms;     /* build: K1 hashing + histogram */
+  double sort_ms;     /* build: scans + scatter + segmented select/sort into CSR */
+  double qhash_ms;    /* query: K1 hashing + ranked lists */
+  double probe_ms;    /* query: probe selection + directory reads */
+  double collect_ms;  /* query: bucket walk + dedup */
+  double score_ms;    /* query: row gather + fp64 dot + top-k (K3+K4) */
+  uint64_t launches;  /* kernels launched */
+  uint64_t score_rows;/* rows gathered by the score kernel */
+  uint64_t entries;   /* bucket entries walked */
+  uint64_t probes;    /* probes */
+} fpp_timings;
+
+typedef struct fpp_index fpp_index;
+
+int fpp_abi_version(void);
+const char* fpp_last_error(void);
+void fpp_default_params(fpp_params* p);
+int fpp_device_count(void);
+
+/*
+ * Index::build (north star build(X,L,K,D,iProbes,alpha)).
+ * X: host, row-major n x d fp32, already normalized (dataset.cpp:24-38) --
+ * the library never re-normalizes.
+ */
+int fpp_build(const float* X, uint64_t n, uint32_t d, const fpp_params* p, fpp_index** out);
+/* same, X already in device memory of p->device (copied into the index) */
+int fpp_build_device(const float* X_dev, uint64_t n, uint32_t d, const fpp_params* p,
+                     fpp_index** out);
+void fpp_free(fpp_index* idx);
+
+/*
+ * Index::query (north star query(Q,k,qProbes)).
+ * Q host nq x d; ids [nq*k] (0xFFFFFFFF past min(k,U_q)); scores [nq*k] fp64
+ * inner products (-inf past min(k,U_q)), descending, ties by lower id;
+ * stats optional [nq].  ids are global (local + id_offset).
+ */
+int fpp_query(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uint32_t qprobes,
+              uint32_t* ids, double* scores, fpp_query_stats* stats);
+/* device-resident variant: Q_dev, ids_dev, scores_dev, stats_dev on the index device;
+   stream is a cudaStream_t (NULL = library stream), asynchronous w.r.t. the host
+   except for one small readback per query chunk. */
+int fpp_query_device(const fpp_index* idx, const float* Q_dev, uint64_t nq, uint32_t k,
+                     uint32_t qprobes, uint32_t* ids_dev, double* scores_dev,
+                     fpp_query_stats* stats_dev, void* stream);
+
+/* ------------------------------------------------------ introspection / parity */
+typedef struct fpp_index_info {
+  uint64_t n;
+  uint32_t d, d_pad, L, K, D, iprobes, kappa;
+  float alpha;
+  uint64_t seed;
+  uint64_t num_buckets;   /* NB per table = (2D)^K */
+  uint64_t kept_total;    /* entries kept over all tables */
+  uint64_t prefilter_total; /* n*L*iprobes */
+  uint64_t device_bytes;  /* resident index bytes */
+  uint32_t max_bucket;    /* largest kept bucket */
+  uint32_t id_offset;
+} fpp_index_info;
+
+int fpp_index_info_get(const fpp_index* idx, fpp_index_info* info);
+uint64_t fpp_table_size(const fpp_index* idx, uint32_t t);
+/* CSR of table t (SPEC.md:237-242 FalconnPPIndex): offsets [NB+1] (relative), ids, scores */
+int fpp_table_csr(const fpp_index* idx, uint32_t t, uint32_t* offsets, uint32_t* ids,
+                  float* scores);
+/* GPU projections of host rows X[n][d] through stack (t,f): out [n][D] (rotation.cpp:70-100) */
+int fpp_project(const fpp_index* idx, const float* X, uint64_t n, uint32_t t, uint32_t f,
+                float* out);
+/* GPU index probes (bucket, score) of host rows for table t: [n][iprobes] */
+int fpp_index_probes(const fpp_index* idx, const float* X, uint64_t n, uint32_t t,
+                     uint32_t* buckets, float* scores);
+/* ranked per-function query lists [nq][L][K][s] (value, code), s = fpp_query_cap */
+uint32_t fpp_query_cap(const fpp_index* idx, uint32_t qprobes);
+uint64_t fpp_query_probes(const fpp_index* idx, uint32_t qprobes);
+int fpp_query_lists(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t qprobes,
+                    float* vals, uint32_t* codes);
+/* one query's probe set (t*NB+bucket, ascending) and candidate set (local ids, ascending) */
+int fpp_query_debug(const fpp_index* idx, const float* q, uint32_t qprobes, uint64_t* probes,
+                    uint64_t* n_probes, uint32_t* cands, uint64_t* n_cands);
+
+int fpp_timings_get(const fpp_index* idx, fpp_timings* t);
+int fpp_timings_reset(const fpp_index* idx);
+
+/* -------------------------------------------------------------- host helpers */
+/* normalize(Dataset) in place (dataset.cpp:24-38); FPP_ERR_ZERO_NORM names the row */
+int fpp_normalize(float* X, uint64_t n, uint32_t d);
+/* seeded synthetic data: clusters=0 -> i.i.d. N(0,1);
+   else mixture of `clusters` isotropic Gaussians (centers N(0,I), std sigma).
+   stream selects independent draws (0 = data, 1 = queries); rows NOT normalized. */
+int fpp_synth(float* X, uint64_t n, uint32_t d, uint32_t clusters, float sigma, uint64_t seed,
+              uint32_t stream, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

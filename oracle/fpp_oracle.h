@@ -1,0 +1,109 @@
+/*
+ * fpp_oracle.h -- CPU restatement of the Falconn++ hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This is the parity checker for the CUDA path in
+ * paper_2206_01382_b200/ and the CPU-baseline arm of bench.py.  Only tests/,
+ * __graft_entry__.smoke() and bench.py (cpu_baseline / --impl reference) may
+ * load it.  The product library never links or calls anything in oracle/.
+ *
+ * Parity pinning: the rotation + dataset parts restate
+ * /root/reference/proj/src/rotation.cpp and dataset.cpp and are pinned against
+ * (a) the unmodified reference compiled into oracle/_ref/ (oracle/Makefile) and
+ * (b) the fingerprints of SURVEY.md section 8(c) (tests/golden/).  The hashing,
+ * index and query parts have NO reference code; they
+ * restate SPEC.md with the pinned choices of SURVEY.md section 8(c) and
+ * DESIGN.md section 3.  Those parts are pinned by the SPEC worked examples and
+ * the SPEC acceptance criterion #4 (exhaustive probing == brute force).
+ */
+#ifndef FPP_ORACLE_H
+#define FPP_ORACLE_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  uint32_t L;        /* tables */
+  uint32_t K;        /* concatenated hashes per table, 1 or 2 (SPEC l) */
+  uint32_t D;        /* projections per function (power of two) */
+  uint32_t iprobes;  /* indexing probes */
+  uint32_t kappa;    /* limit-scaling floor (default 20) */
+  float alpha;       /* scaling factor (0,1] */
+  uint64_t seed;     /* master seed */
+} orc_params;
+
+typedef struct {
+  uint64_t probes;      /* P_q: probes visited */
+  uint64_t entries;     /* E_q: kept bucket entries walked */
+  uint64_t candidates;  /* U_q: unique ids scored */
+} orc_stats;
+
+typedef struct orc_index orc_index;
+
+/* common.hpp:18-58 */
+uint64_t orc_mix64(uint64_t z);
+uint64_t orc_derive_seed(uint64_t master, uint64_t a, uint64_t b, uint64_t c);
+uint64_t orc_fnv1a64(const void* data, size_t len, uint64_t h);
+
+/* rotation.cpp */
+uint32_t orc_pad_dimension(uint32_t d);
+void orc_fht(float* v, uint32_t n);
+/* signs for one SpinnerStack: blocks*3*P floats (+1/-1), rotation.hpp:56 */
+void orc_signs(uint64_t seed, uint32_t P, uint32_t blocks, float* out);
+/* project one row x[d] with stack (d, D, seed): out[D] */
+void orc_project(uint32_t d, uint32_t D, uint64_t seed, const float* x, float* out);
+
+/* batch forms (OpenMP over rows) */
+void orc_project_rows(uint32_t d, uint32_t D, uint64_t seed, const float* X, uint64_t n,
+                      float* out, int threads);
+void orc_cp_hash_rows(const float* proj, uint64_t n, uint32_t D, uint32_t* out);
+/* index probes of rows X for table t of an index */
+void orc_index_probes_rows(const orc_index* idx, const float* X, uint64_t n, uint32_t t,
+                           uint32_t* buckets, float* scores);
+
+/* dataset.cpp */
+int64_t orc_normalize(float* X, uint64_t n, uint32_t d);   /* -1 ok, else zero row idx */
+double orc_inner_product(const float* a, const float* b, uint32_t d);
+
+/* hashing */
+uint32_t orc_cp_hash(const float* p, uint32_t D);
+/* ranked signed list of one function: r entries (value, code) */
+void orc_rank(const float* p, uint32_t D, uint32_t r, float* vals, uint32_t* codes);
+/* index probes of one point in one table, given its K projections [K][D] */
+void orc_index_probes(const float* proj, uint32_t K, uint32_t D, uint32_t iprobes,
+                      uint32_t* buckets, float* scores);
+
+/* index build */
+orc_index* orc_build(const float* X, uint64_t n, uint32_t d, const orc_params* prm,
+                     int threads, uint32_t t_begin, uint32_t t_end);
+void orc_free(orc_index* idx);
+uint64_t orc_num_buckets(const orc_index* idx);
+/* CSR of one table (tables [t_begin,t_end) only) */
+uint64_t orc_table_size(const orc_index* idx, uint32_t t);
+void orc_table(const orc_index* idx, uint32_t t, uint32_t* offsets /*NB+1*/,
+               uint32_t* ids, float* scores);
+
+/* query */
+uint32_t orc_query_cap(const orc_index* idx, uint32_t qprobes);     /* s */
+uint64_t orc_query_probes(const orc_index* idx, uint32_t qprobes);  /* P_eff */
+int orc_query(const orc_index* idx, const float* Q, uint64_t nq, uint32_t k,
+              uint32_t qprobes, uint32_t* ids, double* scores, orc_stats* stats,
+              int threads);
+/* per-query intermediates; probes as t*NB+bucket, sorted asc; cands sorted asc.
+   returns 0; sizes written to *np / *nc (buffers must hold P_eff / n). */
+int orc_query_debug(const orc_index* idx, const float* q, uint32_t qprobes,
+                    uint64_t* probes, uint64_t* np, uint32_t* cands, uint64_t* nc);
+/* query projections ranked lists [L][K][s] */
+void orc_query_lists(const orc_index* idx, const float* q, uint32_t s, float* vals,
+                     uint32_t* codes);
+
+/* brute force top-k */
+void orc_brute_force(const float* X, uint64_t n, uint32_t d, const float* Q, uint64_t nq,
+                     uint32_t k, uint32_t* ids, double* scores, int threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

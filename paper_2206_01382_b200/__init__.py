@@ -1,0 +1,331 @@
+"""paper_2206_01382_b200 -- B200-native Falconn++ hot path (index build + batched query).
+
+Python mirror of the reference's index/query API (SPEC.md:245-253 build,
+SPEC.md:321-329 search; north star ``build(X, L, K, D, iProbes, alpha)`` /
+``query(Q, k, qProbes)``) over the C ABI in include/falconnpp.h.  All compute
+runs in libfalconnpp_b200.so (hand-written sm_100a CUDA); there is no CPU
+fallback -- without the library this package fails to import, and without a
+GPU every compute call raises ``FppCudaError``.
+
+Errors mirror the reference's ``std::invalid_argument`` (dataset.cpp:10-18,
+rotation.cpp:18-20,42-49): configuration / range / dimension errors raise
+``ValueError`` subclasses carrying the library's message.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import _build
+
+__all__ = ["Index", "normalize", "synth", "device_count", "FppError", "FppInvalidArgument",
+           "FppEmptyDataset", "FppDimensionError", "FppOutOfRange", "FppNonFinite",
+           "FppZeroNorm", "FppCudaError", "FppOutOfMemory", "FppUnsupported", "lib",
+           "LIB_PATH", "Params", "QueryStats", "Timings"]
+
+LIB_PATH = _build.LIB
+
+FPP_OK = 0
+ERRORS = {1: "INVALID_ARGUMENT", 2: "EMPTY_DATASET", 3: "DIMENSION", 4: "OUT_OF_RANGE",
+          5: "NON_FINITE", 6: "ZERO_NORM", 7: "CUDA", 8: "OUT_OF_MEMORY", 9: "UNSUPPORTED"}
+
+
+class FppError(Exception):
+    code = -1
+
+
+class FppInvalidArgument(FppError, ValueError):
+    code = 1
+
+
+class FppEmptyDataset(FppError, ValueError):
+    code = 2
+
+
+class FppDimensionError(FppError, ValueError):
+    code = 3
+
+
+class FppOutOfRange(FppError, ValueError):
+    code = 4
+
+
+class FppNonFinite(FppError, ValueError):
+    code = 5
+
+
+class FppZeroNorm(FppError, ValueError):
+    code = 6
+
+
+class FppCudaError(FppError, RuntimeError):
+    code = 7
+
+
+class FppOutOfMemory(FppError, MemoryError):
+    code = 8
+
+
+class FppUnsupported(FppError, NotImplementedError):
+    code = 9
+
+
+_EXC = {c.code: c for c in (FppInvalidArgument, FppEmptyDataset, FppDimensionError, FppOutOfRange,
+                            FppNonFinite, FppZeroNorm, FppCudaError, FppOutOfMemory,
+                            FppUnsupported)}
+
+
+class Params(C.Structure):
+    _fields_ = [("L", C.c_uint32), ("K", C.c_uint32), ("D", C.c_uint32),
+                ("iprobes", C.c_uint32), ("kappa", C.c_uint32), ("alpha", C.c_float),
+                ("seed", C.c_uint64), ("device", C.c_int32), ("id_offset", C.c_uint32),
+                ("scratch_bytes", C.c_uint64)]
+
+
+class QueryStats(C.Structure):
+    _fields_ = [("probes", C.c_uint64), ("entries", C.c_uint64), ("candidates", C.c_uint64)]
+
+
+class Timings(C.Structure):
+    _fields_ = [("hash_ms", C.c_double), ("sort_ms", C.c_double), ("qhash_ms", C.c_double),
+                ("probe_ms", C.c_double), ("collect_ms", C.c_double), ("score_ms", C.c_double),
+                ("launches", C.c_uint64), ("score_rows", C.c_uint64), ("entries", C.c_uint64),
+                ("probes", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class IndexInfo(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("d", C.c_uint32), ("d_pad", C.c_uint32), ("L", C.c_uint32),
+                ("K", C.c_uint32), ("D", C.c_uint32), ("iprobes", C.c_uint32),
+                ("kappa", C.c_uint32), ("alpha", C.c_float), ("seed", C.c_uint64),
+                ("num_buckets", C.c_uint64), ("kept_total", C.c_uint64),
+                ("prefilter_total", C.c_uint64), ("device_bytes", C.c_uint64),
+                ("max_bucket", C.c_uint32), ("id_offset", C.c_uint32)]
+
+
+vp = C.c_void_p
+u32, u64, f32, i32 = C.c_uint32, C.c_uint64, C.c_float, C.c_int
+
+# (name, restype, argtypes) -- every symbol declared in include/falconnpp.h
+SIGNATURES = [
+    ("fpp_abi_version", C.c_int, []),
+    ("fpp_last_error", C.c_char_p, []),
+    ("fpp_default_params", None, [C.POINTER(Params)]),
+    ("fpp_device_count", C.c_int, []),
+    ("fpp_build", C.c_int, [vp, u64, u32, C.POINTER(Params), C.POINTER(vp)]),
+    ("fpp_build_device", C.c_int, [vp, u64, u32, C.POINTER(Params), C.POINTER(vp)]),
+    ("fpp_free", None, [vp]),
+    ("fpp_query", C.c_int, [vp, vp, u64, u32, u32, vp, vp, vp]),
+    ("fpp_query_device", C.c_int, [vp, vp, u64, u32, u32, vp, vp, vp, vp]),
+    ("fpp_index_info_get", C.c_int, [vp, C.POINTER(IndexInfo)]),
+    ("fpp_table_size", u64, [vp, u32]),
+    ("fpp_table_csr", C.c_int, [vp, u32, vp, vp, vp]),
+    ("fpp_project", C.c_int, [vp, vp, u64, u32, u32, vp]),
+    ("fpp_index_probes", C.c_int, [vp, vp, u64, u32, vp, vp]),
+    ("fpp_query_cap", u32, [vp, u32]),
+    ("fpp_query_probes", u64, [vp, u32]),
+    ("fpp_query_lists", C.c_int, [vp, vp, u64, u32, vp, vp]),
+    ("fpp_query_debug", C.c_int, [vp, vp, u32, vp, C.POINTER(u64), vp, C.POINTER(u64)]),
+    ("fpp_timings_get", C.c_int, [vp, C.POINTER(Timings)]),
+    ("fpp_timings_reset", C.c_int, [vp]),
+    ("fpp_normalize", C.c_int, [vp, u64, u32]),
+    ("fpp_synth", C.c_int, [vp, u64, u32, u32, f32, u64, u32, i32]),
+]
+
+_lib = None
+
+
+def lib():
+    """Load libfalconnpp_b200.so (building it with nvcc if absent)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            _build.build()
+        L = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != FPP_OK:
+        msg = lib().fpp_last_error().decode(errors="replace")
+        raise _EXC.get(rc, FppError)(f"[{ERRORS.get(rc, rc)}] {msg}")
+
+
+def _ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+def _f32(X) -> np.ndarray:
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    if X.ndim == 1:
+        X = X.reshape(1, -1)
+    return X
+
+
+def device_count() -> int:
+    return lib().fpp_device_count()
+
+
+def normalize(X: np.ndarray) -> np.ndarray:
+    """normalize(Dataset) (dataset.cpp:24-38); returns a normalized copy."""
+    X = np.array(_f32(X), copy=True)
+    _check(lib().fpp_normalize(_ptr(X), X.shape[0], X.shape[1]))
+    return X
+
+
+def synth(n: int, d: int, clusters: int = 0, sigma: float = 0.0, seed: int = 1, stream: int = 0,
+          threads: int = 0) -> np.ndarray:
+    """Pinned synthetic data; rows are NOT normalized."""
+    X = np.empty((n, d), np.float32)
+    _check(lib().fpp_synth(_ptr(X), n, d, clusters, sigma, seed, stream, threads))
+    return X
+
+
+class Index:
+    """A built Falconn++ index resident on one GPU (SPEC.md:237-242 FalconnPPIndex)."""
+
+    def __init__(self, handle, params: Params, n: int, d: int, X_ref=None):
+        self._h = handle
+        self.params = params
+        self.n, self.d = n, d
+        self._X_ref = X_ref
+
+    # --------------------------------------------------------------- build
+    @classmethod
+    def build(cls, X, L: int, K: int, D: int, iProbes: int, alpha: float, kappa: int = 20,
+              seed: int = 1, device: int = -1, id_offset: int = 0, scratch_bytes: int = 0):
+        """Index::build(X, L, K, D, iProbes, alpha) -- SPEC.md:245-253.
+
+        X is host (numpy) n x d fp32, already normalized, or a CUDA torch tensor.
+        """
+        p = Params(L, K, D, iProbes, kappa, alpha, seed, device, id_offset, scratch_bytes)
+        h = C.c_void_p()
+        if _is_torch_cuda(X):
+            X = X.contiguous()
+            if X.dtype.__str__() != "torch.float32":
+                raise FppInvalidArgument("build: X must be float32")
+            n, d = X.shape
+            if device < 0:
+                p.device = X.device.index or 0
+            _check(lib().fpp_build_device(C.c_void_p(X.data_ptr()), n, d, C.byref(p), C.byref(h)))
+        else:
+            X = _f32(X)
+            n, d = X.shape
+            _check(lib().fpp_build(_ptr(X), n, d, C.byref(p), C.byref(h)))
+        return cls(h, p, n, d)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.fpp_free(h)
+            self._h = None
+
+    def close(self):
+        self.__del__()
+
+    # --------------------------------------------------------------- query
+    def query(self, Q, k: int, qProbes: int, return_stats: bool = False):
+        """Index::query(Q, k, qProbes) -- SPEC.md:321-329, batch over rows of Q.
+
+        Returns ids [nq,k] uint32 (0xFFFFFFFF past min(k,U)), scores [nq,k] fp64
+        (-inf past min(k,U)) and optionally stats [nq,3] (probes, entries,
+        candidates).
+        """
+        Q = _f32(Q)
+        if Q.shape[1] != self.d:
+            raise FppDimensionError(f"search: query dim {Q.shape[1]} != index dim {self.d}")
+        nq = Q.shape[0]
+        ids = np.empty((nq, k), np.uint32)
+        sc = np.empty((nq, k), np.float64)
+        st = (QueryStats * max(nq, 1))() if return_stats else None
+        _check(lib().fpp_query(self._h, _ptr(Q), nq, k, qProbes, _ptr(ids), _ptr(sc),
+                               C.cast(st, C.c_void_p) if st is not None else None))
+        if return_stats:
+            stats = np.array([(s.probes, s.entries, s.candidates) for s in st[:nq]],
+                             dtype=np.uint64).reshape(nq, 3)
+            return ids, sc, stats
+        return ids, sc
+
+    def query_device(self, Q, ids, scores, k: int, qProbes: int, stats=None, stream=None):
+        """Device-resident batch query on torch CUDA tensors (no host copies)."""
+        if Q.shape[1] != self.d:
+            raise FppDimensionError("search: dimension mismatch")
+        _check(lib().fpp_query_device(self._h, C.c_void_p(Q.data_ptr()), Q.shape[0], k, qProbes,
+                                      C.c_void_p(ids.data_ptr()), C.c_void_p(scores.data_ptr()),
+                                      C.c_void_p(stats.data_ptr()) if stats is not None else None,
+                                      C.c_void_p(stream) if stream else None))
+
+    # ------------------------------------------------------- introspection
+    def info(self) -> dict:
+        inf = IndexInfo()
+        _check(lib().fpp_index_info_get(self._h, C.byref(inf)))
+        return {k: getattr(inf, k) for k, _ in inf._fields_}
+
+    def table(self, t: int):
+        NB = self.info()["num_buckets"]
+        tot = lib().fpp_table_size(self._h, t)
+        off = np.empty(NB + 1, np.uint32)
+        ids = np.empty(max(tot, 1), np.uint32)
+        sc = np.empty(max(tot, 1), np.float32)
+        _check(lib().fpp_table_csr(self._h, t, _ptr(off), _ptr(ids), _ptr(sc)))
+        return off, ids[:tot], sc[:tot]
+
+    def project(self, X, t: int, f: int) -> np.ndarray:
+        X = _f32(X)
+        out = np.empty((X.shape[0], self.params.D), np.float32)
+        _check(lib().fpp_project(self._h, _ptr(X), X.shape[0], t, f, _ptr(out)))
+        return out
+
+    def index_probes(self, X, t: int):
+        X = _f32(X)
+        ip = self.params.iprobes
+        b = np.empty((X.shape[0], ip), np.uint32)
+        s = np.empty((X.shape[0], ip), np.float32)
+        _check(lib().fpp_index_probes(self._h, _ptr(X), X.shape[0], t, _ptr(b), _ptr(s)))
+        return b, s
+
+    def cap(self, qProbes: int) -> int:
+        return lib().fpp_query_cap(self._h, qProbes)
+
+    def peff(self, qProbes: int) -> int:
+        return lib().fpp_query_probes(self._h, qProbes)
+
+    def query_lists(self, Q, qProbes: int):
+        Q = _f32(Q)
+        s = self.cap(qProbes)
+        L, K = self.params.L, self.params.K
+        v = np.empty((Q.shape[0], L, K, s), np.float32)
+        c = np.empty((Q.shape[0], L, K, s), np.uint32)
+        _check(lib().fpp_query_lists(self._h, _ptr(Q), Q.shape[0], qProbes, _ptr(v), _ptr(c)))
+        return v, c
+
+    def query_debug(self, q, qProbes: int):
+        q = _f32(q)
+        pe = self.peff(qProbes)
+        probes = np.empty(pe, np.uint64)
+        cands = np.empty(self.n, np.uint32)
+        npr, nc = u64(), u64()
+        _check(lib().fpp_query_debug(self._h, _ptr(q), qProbes, _ptr(probes), C.byref(npr),
+                                     _ptr(cands), C.byref(nc)))
+        return probes[:npr.value].copy(), cands[:nc.value].copy()
+
+    def timings(self) -> dict:
+        t = Timings()
+        _check(lib().fpp_timings_get(self._h, C.byref(t)))
+        return t.as_dict()
+
+    def reset_timings(self) -> None:
+        _check(lib().fpp_timings_reset(self._h))
+
+
+def _is_torch_cuda(x) -> bool:
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)

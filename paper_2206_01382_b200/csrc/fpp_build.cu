@@ -1,0 +1,589 @@
+// fpp_build.cu -- index build: K1 (cross-polytope hashing + index probes) and
+// K2 (bucketing, alpha/kappa limit-scaling filter, CSR).
+//
+// Reference semantics: SPEC.md:245-262 build / filter_bucket
+// (Algorithm 1), PAPER.md:336-339 (limit scaling), rotation.cpp:70-100
+// (projection).  Pinned choices: DESIGN.md section 3.  Oracle: oracle/fpp_oracle.c
+// orc_build().
+//
+// Pipeline per chunk of T tables:
+//   k_hash_build   one lane-group per point: x stays in registers, for every
+//                  table/function run the spinner stack (3 x signs+FHT), rank
+//                  top-R coordinates, pick top-iProbes pairs, emit
+//                  (bucket, score) and bump the bucket histogram
+//   k_scan_*       per-table exclusive scans: histogram -> pre-filter starts,
+//                  keep(B) -> kept CSR offsets
+//   k_scatter      (score desc, id asc) 64-bit keys into bucket segments
+//   k_classify     B=1 written directly; B<=32 -> warp list; B>32 -> CTA list
+//   k_sort_small   warp bitonic sort, keep prefix -> CSR
+//   k_sort_large   CTA smem bitonic (B<=4096) or radix-select + chunked sort
+#include <algorithm>
+#include <cstdio>
+
+#include "fpp_device.cuh"
+#include "fpp_internal.h"
+
+namespace fpp {
+
+// ------------------------------------------------------------------ K1 build
+template <int P, int R>
+__global__ void __launch_bounds__(256)
+k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, uint32_t K,
+             const uint32_t* __restrict__ signs, uint32_t t0, uint32_t T, uint32_t ip,
+             uint2* __restrict__ ent, uint32_t* __restrict__ counts, uint64_t NB) {
+  using S = FhtShape<P>;
+  const int lane = threadIdx.x & 31;
+  const int g = lane % S::G;
+  const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
+  const bool active = gid < n;
+  const uint64_t i = active ? gid : n - 1;  // inactive groups shadow a real row
+  float x[S::EPT];
+  load_row<P>(X + i * d, d, g, x);
+  const uint32_t r = ip < D ? ip : D;  // ranks needed per function (host ensures <= R)
+  const uint32_t twoD = 2 * D;
+  for (uint32_t tt = 0; tt < T; ++tt) {
+    const uint32_t t = t0 + tt;
+    uint64_t top0[R], top1[R];
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      if (f >= (int)K) break;
+      float v[S::EPT];
+#pragma unroll
+      for (int e = 0; e < S::EPT; ++e) v[e] = x[e];
+      spinner_project<P>(v, signs + ((uint64_t)t * K + f) * 3 * S::W, g);
+      uint64_t tk[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) tk[q] = ~0ull;
+#pragma unroll
+      for (int e = 0; e < S::EPT; ++e) {
+        const uint32_t j = (uint32_t)g * S::EPT + e;
+        if (j < D) topr_insert<R>(tk, rank_key(v[e], j));
+      }
+      topr_group_merge<R, S::G>(tk);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (f == 0) top0[q] = tk[q];
+        else top1[q] = tk[q];
+      }
+    }
+    if (g != 0 || !active) continue;
+    uint2* out = ent + ((uint64_t)tt * n + i) * ip;
+    uint32_t* cnt = counts ? counts + (uint64_t)tt * NB : nullptr;
+    if (K == 1) {
+      // SPEC.md:184-192 with l=1: the top-iProbes signed vectors themselves
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if ((uint32_t)q < ip) {
+          const uint32_t b = rank_code(top0[q], D);
+          out[q] = make_uint2(b, __float_as_uint(rank_val(top0[q])));
+          if (cnt) atomicAdd(cnt + b, 1u);
+        }
+      }
+    } else {
+      // top-iProbes pairs by (fl(v1+v2) desc, r1 asc, r2 asc): successive
+      // selection of the best pair strictly after the previous one.
+      float ps = 0.0f;
+      int pa = -1, pb = -1;
+      for (uint32_t sel = 0; sel < ip; ++sel) {
+        float bs = 0.0f;
+        int ba = -1, bb = -1;
+        uint32_t bc1 = 0, bc2 = 0;
+#pragma unroll
+        for (int a = 0; a < R; ++a) {
+          if ((uint32_t)a >= r) break;
+          const float va = rank_val(top0[a]);
+          const uint32_t ca = rank_code(top0[a], D);
+#pragma unroll
+          for (int b = 0; b < R; ++b) {
+            if ((uint32_t)b >= r) break;
+            const float s = va + rank_val(top1[b]);
+            const bool after = pa < 0 || ps > s || (ps == s && (pa < a || (pa == a && pb < b)));
+            if (!after) continue;
+            const bool better = ba < 0 || s > bs || (s == bs && (a < ba || (a == ba && b < bb)));
+            if (better) {
+              bs = s; ba = a; bb = b; bc1 = ca; bc2 = rank_code(top1[b], D);
+            }
+          }
+        }
+        const uint32_t bucket = bc1 * twoD + bc2;
+        out[sel] = make_uint2(bucket, __float_as_uint(bs));
+        if (cnt) atomicAdd(cnt + bucket, 1u);
+        ps = bs; pa = ba; pb = bb;
+      }
+    }
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(256)
+k_project(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D,
+          const uint32_t* __restrict__ sw, float* __restrict__ out) {
+  using S = FhtShape<P>;
+  const int lane = threadIdx.x & 31;
+  const int g = lane % S::G;
+  const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
+  const bool active = gid < n;
+  const uint64_t i = active ? gid : n - 1;
+  float v[S::EPT];
+  load_row<P>(X + i * d, d, g, v);
+  spinner_project<P>(v, sw, g);
+  if (!active) return;
+#pragma unroll
+  for (int e = 0; e < S::EPT; ++e) {
+    const uint32_t j = (uint32_t)g * S::EPT + e;
+    if (j < D) out[i * D + j] = v[e];
+  }
+}
+
+// ------------------------------------------------------------- per-table scan
+constexpr int SCAN_THREADS = 512;
+constexpr int SCAN_PER_THREAD = 8;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_PER_THREAD;
+
+struct KeepXform {
+  int mode;  // 0 identity, 1 keep(B)
+  float alpha;
+  uint32_t ip, kappa;
+  __device__ __forceinline__ uint32_t operator()(uint32_t B) const {
+    return mode ? keep_count(B, alpha, ip, kappa) : B;
+  }
+};
+
+__global__ void __launch_bounds__(SCAN_THREADS)
+k_scan_reduce(const uint32_t* __restrict__ in, uint64_t NB, uint32_t ntiles, KeepXform xf,
+              uint32_t* __restrict__ tile_sums) {
+  __shared__ uint32_t sh[32];
+  const uint32_t tile = blockIdx.x, t = blockIdx.y;
+  const uint32_t* src = in + (uint64_t)t * NB;
+  uint32_t s = 0;
+  const uint64_t base = (uint64_t)tile * SCAN_TILE + threadIdx.x * SCAN_PER_THREAD;
+#pragma unroll
+  for (int k = 0; k < SCAN_PER_THREAD; ++k)
+    if (base + k < NB) s += xf(src[base + k]);
+  uint32_t tot;
+  block_excl_scan_u32(s, sh, &tot);
+  if (threadIdx.x == 0) tile_sums[(uint64_t)t * ntiles + tile] = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS)
+k_scan_tiles(uint32_t* __restrict__ tile_sums, uint32_t ntiles, uint32_t* __restrict__ totals) {
+  __shared__ uint32_t sh[32];
+  uint32_t* ts = tile_sums + (uint64_t)blockIdx.x * ntiles;
+  uint32_t carry = 0;
+  for (uint32_t b = 0; b < ntiles; b += blockDim.x) {
+    const uint32_t i = b + threadIdx.x;
+    const uint32_t v = i < ntiles ? ts[i] : 0;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan_u32(v, sh, &tot);
+    if (i < ntiles) ts[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS)
+k_scan_apply(const uint32_t* __restrict__ in, uint64_t NB, uint32_t ntiles, KeepXform xf,
+             const uint32_t* __restrict__ tile_sums, const uint32_t* __restrict__ totals,
+             uint32_t* __restrict__ out /* [T][NB+1] */) {
+  __shared__ uint32_t sh[32];
+  const uint32_t tile = blockIdx.x, t = blockIdx.y;
+  const uint32_t* src = in + (uint64_t)t * NB;
+  uint32_t* dst = out + (uint64_t)t * (NB + 1);
+  const uint64_t base = (uint64_t)tile * SCAN_TILE + threadIdx.x * SCAN_PER_THREAD;
+  uint32_t v[SCAN_PER_THREAD];
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_PER_THREAD; ++k) {
+    v[k] = base + k < NB ? xf(src[base + k]) : 0;
+    s += v[k];
+  }
+  uint32_t run = tile_sums[(uint64_t)t * ntiles + tile] + block_excl_scan_u32(s, sh, nullptr);
+#pragma unroll
+  for (int k = 0; k < SCAN_PER_THREAD; ++k) {
+    if (base + k < NB) dst[base + k] = run;
+    run += v[k];
+  }
+  if (tile == 0 && threadIdx.x == 0) dst[NB] = totals[t];
+}
+
+// in [T][NB] -> out [T][NB+1] exclusive, totals [T]
+static void scan_tables(const uint32_t* in, uint64_t NB, uint32_t T, KeepXform xf, uint32_t* out,
+                        uint32_t* totals, DBuf<uint32_t>& tile_buf, cudaStream_t s) {
+  const uint32_t ntiles = (uint32_t)((NB + SCAN_TILE - 1) / SCAN_TILE);
+  tile_buf.ensure((size_t)ntiles * T);
+  dim3 grid(ntiles, T);
+  k_scan_reduce<<<grid, SCAN_THREADS, 0, s>>>(in, NB, ntiles, xf, tile_buf.p);
+  FPP_LAUNCH();
+  k_scan_tiles<<<T, SCAN_THREADS, 0, s>>>(tile_buf.p, ntiles, totals);
+  FPP_LAUNCH();
+  k_scan_apply<<<grid, SCAN_THREADS, 0, s>>>(in, NB, ntiles, xf, tile_buf.p, totals, out);
+  FPP_LAUNCH();
+}
+
+// ------------------------------------------------------------------ scatter
+__global__ void __launch_bounds__(256)
+k_scatter(const uint2* __restrict__ ent, uint64_t nip, uint32_t ip, uint32_t T, uint64_t NB,
+          const uint32_t* __restrict__ starts, uint32_t* __restrict__ cursor,
+          uint64_t* __restrict__ keys) {
+  const uint64_t total = nip * T;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t tt = (uint32_t)(e / nip);
+    const uint64_t rem = e - (uint64_t)tt * nip;
+    const uint32_t i = (uint32_t)(rem / ip);
+    const uint2 en = ent[e];
+    const uint32_t pos = starts[(uint64_t)tt * (NB + 1) + en.x] +
+                         atomicAdd(cursor + (uint64_t)tt * NB + en.x, 1u);
+    keys[(uint64_t)tt * nip + pos] = desc_score_key(__uint_as_float(en.y), i);
+  }
+}
+
+struct CsrOut {
+  const uint32_t* offs;     // [T][NB+1] kept offsets of this chunk's tables
+  const uint64_t* base;     // [T] table bases (global positions)
+  uint32_t* ids;
+  float* scores;
+};
+
+__device__ __forceinline__ void csr_put(const CsrOut& o, uint32_t tt, uint64_t NB, uint32_t b,
+                                        uint32_t j, uint64_t key) {
+  const uint64_t pos = o.base[tt] + o.offs[(uint64_t)tt * (NB + 1) + b] + j;
+  o.ids[pos] = (uint32_t)(key & 0xffffffffu);
+  o.scores[pos] = desc_score_val(key);
+}
+
+constexpr uint32_t SMALL_MAX = 32;
+constexpr uint32_t LARGE_CAP = 4096;
+
+__global__ void __launch_bounds__(256)
+k_classify(const uint32_t* __restrict__ starts, const uint64_t* __restrict__ keys, uint64_t nip,
+           uint32_t T, uint64_t NB, CsrOut o, uint32_t* __restrict__ small_list,
+           uint32_t* __restrict__ large_list, uint32_t* __restrict__ ctr) {
+  const uint64_t total = NB * T;
+  uint32_t local_max = 0;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t tt = (uint32_t)(x / NB);
+    const uint32_t b = (uint32_t)(x - (uint64_t)tt * NB);
+    const uint32_t* st = starts + (uint64_t)tt * (NB + 1);
+    const uint32_t B = st[b + 1] - st[b];
+    if (B == 0) continue;
+    const uint32_t* of = o.offs + (uint64_t)tt * (NB + 1);
+    const uint32_t k = of[b + 1] - of[b];
+    local_max = max(local_max, k);
+    if (k == 0) continue;
+    if (B == 1) {
+      csr_put(o, tt, NB, b, 0, keys[(uint64_t)tt * nip + st[b]]);
+    } else if (B <= SMALL_MAX) {
+      small_list[atomicAdd(ctr + 0, 1u)] = (uint32_t)x;
+    } else {
+      large_list[atomicAdd(ctr + 1, 1u)] = (uint32_t)x;
+    }
+  }
+  // block max, one atomic per block
+  for (int o2 = 16; o2 > 0; o2 >>= 1) local_max = max(local_max, __shfl_xor_sync(FULL, local_max, o2));
+  if ((threadIdx.x & 31) == 0 && local_max) atomicMax(ctr + 2, local_max);
+}
+
+__global__ void __launch_bounds__(256)
+k_sort_small(const uint32_t* __restrict__ starts, const uint64_t* __restrict__ keys, uint64_t nip,
+             uint64_t NB, CsrOut o, const uint32_t* __restrict__ list,
+             const uint32_t* __restrict__ ctr) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t count = ctr[0];
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < count; it += nwarps) {
+    const uint32_t x = list[it];
+    const uint32_t tt = (uint32_t)(x / NB), b = (uint32_t)(x - (uint64_t)tt * NB);
+    const uint32_t* st = starts + (uint64_t)tt * (NB + 1);
+    const uint32_t B = st[b + 1] - st[b];
+    const uint32_t* of = o.offs + (uint64_t)tt * (NB + 1);
+    const uint32_t k = of[b + 1] - of[b];
+    uint64_t key = lane < (int)B ? keys[(uint64_t)tt * nip + st[b] + lane] : ~0ull;
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const uint64_t other = __shfl_xor_sync(FULL, key, j);
+        const bool up = (lane & kk) == 0;
+        const bool lower = (lane & j) == 0;
+        const uint64_t mn = key < other ? key : other, mx = key < other ? other : key;
+        key = (lower == up) ? mn : mx;
+      }
+    }
+    if ((uint32_t)lane < k) csr_put(o, tt, NB, b, lane, key);
+  }
+}
+
+__device__ void block_bitonic(uint64_t* s, uint32_t N) {
+  for (uint32_t k = 2; k <= N; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t a = s[i], b = s[ixj];
+          const bool asc = (i & k) == 0;
+          if ((a > b) == asc) {
+            s[i] = b;
+            s[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// key of 0-based rank `rank` (ascending) among seg[0..B), keys unique
+__device__ uint64_t block_radix_select(const uint64_t* __restrict__ seg, uint32_t B, uint32_t rank,
+                                       uint32_t* hist, uint64_t* sh_prefix, uint32_t* sh_rank) {
+  uint64_t prefix = 0, mask = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
+      const uint64_t k = seg[i];
+      if ((k & mask) == prefix) atomicAdd(hist + ((k >> shift) & 255u), 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t cum = 0, dg = 0;
+      for (; dg < 256; ++dg) {
+        if (cum + hist[dg] > rank) break;
+        cum += hist[dg];
+      }
+      rank -= cum;
+      *sh_prefix = prefix | ((uint64_t)dg << shift);
+      *sh_rank = rank;
+    }
+    __syncthreads();
+    prefix = *sh_prefix;
+    rank = *sh_rank;
+    mask |= 255ull << shift;
+    __syncthreads();
+  }
+  return prefix;
+}
+
+__global__ void __launch_bounds__(256)
+k_sort_large(const uint32_t* __restrict__ starts, const uint64_t* __restrict__ keys, uint64_t nip,
+             uint64_t NB, CsrOut o, const uint32_t* __restrict__ list,
+             const uint32_t* __restrict__ ctr) {
+  __shared__ uint64_t s[LARGE_CAP];
+  __shared__ uint32_t hist[256];
+  __shared__ uint64_t sh_prefix;
+  __shared__ uint32_t sh_rank, sh_cnt;
+  const uint32_t count = ctr[1];
+  for (uint32_t it = blockIdx.x; it < count; it += gridDim.x) {
+    const uint32_t x = list[it];
+    const uint32_t tt = (uint32_t)(x / NB), b = (uint32_t)(x - (uint64_t)tt * NB);
+    const uint32_t* st = starts + (uint64_t)tt * (NB + 1);
+    const uint32_t B = st[b + 1] - st[b];
+    const uint32_t* of = o.offs + (uint64_t)tt * (NB + 1);
+    const uint32_t k = of[b + 1] - of[b];
+    const uint64_t* seg = keys + (uint64_t)tt * nip + st[b];
+    if (B <= LARGE_CAP) {
+      uint32_t N = 1;
+      while (N < B) N <<= 1;
+      for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) s[i] = i < B ? seg[i] : ~0ull;
+      __syncthreads();
+      block_bitonic(s, N);
+      for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) csr_put(o, tt, NB, b, j, s[j]);
+      __syncthreads();
+      continue;
+    }
+    // radix-select the cut of each CAP-sized chunk of the kept prefix, sort the chunk
+    uint64_t lo = 0;
+    bool have_lo = false;
+    for (uint32_t c0 = 0; c0 < k; c0 += LARGE_CAP) {
+      const uint32_t cnt = min(LARGE_CAP, k - c0);
+      const uint64_t hi = block_radix_select(seg, B, c0 + cnt - 1, hist, &sh_prefix, &sh_rank);
+      if (threadIdx.x == 0) sh_cnt = 0;
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
+        const uint64_t kk = seg[i];
+        if (kk <= hi && (!have_lo || kk > lo)) s[atomicAdd(&sh_cnt, 1u)] = kk;
+      }
+      __syncthreads();
+      uint32_t N = 1;
+      while (N < cnt) N <<= 1;
+      for (uint32_t i = cnt + threadIdx.x; i < N; i += blockDim.x) s[i] = ~0ull;
+      __syncthreads();
+      block_bitonic(s, N);
+      for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) csr_put(o, tt, NB, b, c0 + j, s[j]);
+      __syncthreads();
+      lo = hi;
+      have_lo = true;
+    }
+  }
+}
+
+// ------------------------------------------------------------ host dispatch
+template <int R>
+static void launch_hash_R(const Index& ix, const float* X, uint64_t n, uint32_t t0, uint32_t T,
+                          uint2* ent, uint32_t* counts, cudaStream_t s) {
+  const uint32_t P = ix.P;
+  uint32_t G = P < 32 ? 1 : P / 32;
+  const uint64_t threads = n * G;
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  const uint32_t K = ix.prm.K, D = ix.prm.D, ip = ix.prm.iprobes;
+#define FPP_HASH_CASE(PP)                                                                      \
+  case PP:                                                                                     \
+    k_hash_build<PP, R><<<blocks, 256, 0, s>>>(X, n, ix.d, D, K, ix.signs, t0, T, ip, ent,     \
+                                               counts, ix.NB);                                 \
+    break;
+  switch (P) {
+    FPP_HASH_CASE(2) FPP_HASH_CASE(4) FPP_HASH_CASE(8) FPP_HASH_CASE(16) FPP_HASH_CASE(32)
+    FPP_HASH_CASE(64) FPP_HASH_CASE(128) FPP_HASH_CASE(256) FPP_HASH_CASE(512)
+    FPP_HASH_CASE(1024)
+    default: fail(FPP_ERR_UNSUPPORTED, "build: padded dimension > 1024 not supported on GPU");
+  }
+#undef FPP_HASH_CASE
+  FPP_LAUNCH();
+}
+
+static void launch_hash(const Index& ix, const float* X, uint64_t n, uint32_t t0, uint32_t T,
+                        uint2* ent, uint32_t* counts, cudaStream_t s) {
+  const uint32_t r = std::min(ix.prm.iprobes, ix.prm.D);
+  if (r <= 4) launch_hash_R<4>(ix, X, n, t0, T, ent, counts, s);
+  else if (r <= 8) launch_hash_R<8>(ix, X, n, t0, T, ent, counts, s);
+  else launch_hash_R<16>(ix, X, n, t0, T, ent, counts, s);
+}
+
+void launch_index_probes(const Index& ix, const float* Xd, uint64_t n, uint32_t t, uint2* out,
+                         cudaStream_t s) {
+  launch_hash(ix, Xd, n, t, 1, out, nullptr, s);
+}
+
+void launch_project(const Index& ix, const float* Xd, uint64_t n, uint32_t t, uint32_t f,
+                    float* out, cudaStream_t s) {
+  const uint32_t P = ix.P;
+  uint32_t G = P < 32 ? 1 : P / 32;
+  const unsigned blocks = (unsigned)((n * G + 255) / 256);
+  const uint32_t* sw = ix.signs + ((uint64_t)t * ix.prm.K + f) * 3 * ix.W;
+#define FPP_PROJ_CASE(PP)                                                                       \
+  case PP:                                                                                      \
+    k_project<PP><<<blocks, 256, 0, s>>>(Xd, n, ix.d, ix.prm.D, sw, out);                      \
+    break;
+  switch (P) {
+    FPP_PROJ_CASE(2) FPP_PROJ_CASE(4) FPP_PROJ_CASE(8) FPP_PROJ_CASE(16) FPP_PROJ_CASE(32)
+    FPP_PROJ_CASE(64) FPP_PROJ_CASE(128) FPP_PROJ_CASE(256) FPP_PROJ_CASE(512)
+    FPP_PROJ_CASE(1024)
+    default: fail(FPP_ERR_UNSUPPORTED, "project: padded dimension > 1024 not supported on GPU");
+  }
+#undef FPP_PROJ_CASE
+  FPP_LAUNCH();
+}
+
+void build_tables(Index& ix) {
+  const uint32_t L = ix.prm.L, ip = ix.prm.iprobes;
+  const uint64_t n = ix.n, NB = ix.NB, nip = n * ip;
+  cudaStream_t s = ix.stream;
+  if (nip >= (1ull << 32)) fail(FPP_ERR_UNSUPPORTED, "build: n*iProbes must be < 2^32 per shard");
+  // scratch per table in one pass
+  const uint64_t per_table = nip * (8 + 8) + NB * 4 * 2 + (NB + 1) * 4 + (nip / 2 + 1) * 4 +
+                             (nip / (SMALL_MAX + 1) + 1) * 4;
+  uint64_t budget = ix.prm.scratch_bytes;
+  if (!budget) {
+    size_t fr = 0, tot = 0;
+    FPP_CUDA(cudaMemGetInfo(&fr, &tot));
+    budget = std::min<uint64_t>((uint64_t)(fr * 0.6), 48ull << 30);
+  }
+  uint32_t T = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(L, budget / per_table));
+  while ((uint64_t)T * NB >= (1ull << 32) && T > 1) --T;
+  if ((uint64_t)T * NB >= (1ull << 32)) fail(FPP_ERR_UNSUPPORTED, "build: NB too large");
+
+  DBuf<uint2> ent((size_t)T * nip);
+  DBuf<uint64_t> keys((size_t)T * nip);
+  DBuf<uint32_t> counts((size_t)T * NB);
+  DBuf<uint32_t> starts((size_t)T * (NB + 1));
+  DBuf<uint32_t> small_list((size_t)T * (nip / 2 + 1));
+  DBuf<uint32_t> large_list((size_t)T * (nip / (SMALL_MAX + 1) + 1));
+  DBuf<uint32_t> tiles, totals(T), ctr(4);
+  DBuf<uint64_t> base_d(T);
+
+  ix.offsets = static_cast<uint32_t*>(dmalloc((size_t)L * (NB + 1) * sizeof(uint32_t)));
+  ix.table_base = static_cast<uint64_t*>(dmalloc((size_t)(L + 1) * sizeof(uint64_t)));
+  ix.table_base_h.assign(L + 1, 0);
+  uint64_t cap = 0;
+  std::vector<uint32_t> tot_h(T);
+  const int sms = sm_count();
+  KeepXform ident{0, 0.f, 1, 0};
+  KeepXform keepx{1, ix.prm.alpha, ip, ix.prm.kappa};
+  uint32_t max_keep = 0;
+
+  for (uint32_t t0 = 0; t0 < L; t0 += T) {
+    const uint32_t Tc = std::min(T, L - t0);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ix.timer.begin(PH_HASH, s, &e0);
+    FPP_CUDA(cudaMemsetAsync(counts.p, 0, (size_t)Tc * NB * sizeof(uint32_t), s));
+    launch_hash(ix, ix.X, n, t0, Tc, ent.p, counts.p, s);
+    ix.timer.end(PH_HASH, e0, s);
+    ix.timer.begin(PH_SORT, s, &e1);
+    uint32_t* offs = ix.offsets + (uint64_t)t0 * (NB + 1);
+    scan_tables(counts.p, NB, Tc, ident, starts.p, totals.p, tiles, s);
+    scan_tables(counts.p, NB, Tc, keepx, offs, totals.p, tiles, s);
+    FPP_CUDA(cudaMemcpyAsync(tot_h.data(), totals.p, Tc * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, s));
+    FPP_CUDA(cudaStreamSynchronize(s));
+    for (uint32_t tt = 0; tt < Tc; ++tt)
+      ix.table_base_h[t0 + tt + 1] = ix.table_base_h[t0 + tt] + tot_h[tt];
+    const uint64_t need = ix.table_base_h[t0 + Tc];
+    if (need > cap) {  // grow the contiguous CSR arrays, keep built tables
+      uint64_t ncap = std::max<uint64_t>(need + need / 2,
+                                         need + (uint64_t)(L - t0 - Tc) * tot_h[0]);
+      if (t0 + Tc == L) ncap = need;
+      uint32_t* nids = static_cast<uint32_t*>(dmalloc((ncap + 1) * sizeof(uint32_t)));
+      float* nsc = static_cast<float*>(dmalloc((ncap + 1) * sizeof(float)));
+      const uint64_t have = ix.table_base_h[t0];
+      if (have) {
+        FPP_CUDA(cudaMemcpyAsync(nids, ix.ids, have * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        FPP_CUDA(cudaMemcpyAsync(nsc, ix.scores, have * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        FPP_CUDA(cudaStreamSynchronize(s));
+      }
+      if (ix.ids) dfree(ix.ids);
+      if (ix.scores) dfree(ix.scores);
+      ix.ids = nids;
+      ix.scores = nsc;
+      cap = ncap;
+    }
+    FPP_CUDA(cudaMemcpyAsync(base_d.p, ix.table_base_h.data() + t0, Tc * sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, s));
+    FPP_CUDA(cudaMemsetAsync(counts.p, 0, (size_t)Tc * NB * sizeof(uint32_t), s));
+    FPP_CUDA(cudaMemsetAsync(ctr.p, 0, 4 * sizeof(uint32_t), s));
+    {
+      const uint64_t tot = nip * Tc;
+      const unsigned blocks = (unsigned)std::min<uint64_t>((tot + 255) / 256, (uint64_t)sms * 32);
+      k_scatter<<<blocks, 256, 0, s>>>(ent.p, nip, ip, Tc, NB, starts.p, counts.p, keys.p);
+      FPP_LAUNCH();
+    }
+    CsrOut o{offs, base_d.p, ix.ids, ix.scores};
+    {
+      const uint64_t tot = NB * Tc;
+      const unsigned blocks = (unsigned)std::min<uint64_t>((tot + 255) / 256, (uint64_t)sms * 32);
+      k_classify<<<blocks, 256, 0, s>>>(starts.p, keys.p, nip, Tc, NB, o, small_list.p,
+                                        large_list.p, ctr.p);
+      FPP_LAUNCH();
+    }
+    k_sort_small<<<sms * 8, 256, 0, s>>>(starts.p, keys.p, nip, NB, o, small_list.p, ctr.p);
+    FPP_LAUNCH();
+    k_sort_large<<<sms * 4, 256, 0, s>>>(starts.p, keys.p, nip, NB, o, large_list.p, ctr.p);
+    FPP_LAUNCH();
+    uint32_t mk = 0;
+    FPP_CUDA(cudaMemcpyAsync(&mk, ctr.p + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    ix.timer.end(PH_SORT, e1, s);
+    FPP_CUDA(cudaStreamSynchronize(s));
+    max_keep = std::max(max_keep, mk);
+  }
+  ix.kept_total = ix.table_base_h[L];
+  ix.max_bucket = max_keep;
+  if (!ix.ids) {
+    ix.ids = static_cast<uint32_t*>(dmalloc(sizeof(uint32_t)));
+    ix.scores = static_cast<float*>(dmalloc(sizeof(float)));
+  }
+  FPP_CUDA(cudaMemcpyAsync(ix.table_base, ix.table_base_h.data(), (L + 1) * sizeof(uint64_t),
+                           cudaMemcpyHostToDevice, s));
+  FPP_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace fpp

@@ -1,0 +1,604 @@
+// fpp_capi.cu -- the C ABI (include/falconnpp.h): validation with the
+// reference's error classes, device ownership, host<->device staging, and the
+// host helpers (normalize, synthetic data).  No CPU compute fallback: every
+// compute entry point runs the CUDA kernels or fails with FPP_ERR_CUDA.
+#include <cuda_runtime.h>
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "fpp_internal.h"
+
+namespace fpp {
+
+static thread_local std::string g_err;
+
+void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();
+  const int code = e == cudaErrorMemoryAllocation ? FPP_ERR_OUT_OF_MEMORY : FPP_ERR_CUDA;
+  fail(code, std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + what + " (" + file +
+                 ":" + std::to_string(line) + ")");
+}
+
+void* dmalloc(size_t bytes) {
+  void* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, bytes ? bytes : 1);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? FPP_ERR_OUT_OF_MEMORY : FPP_ERR_CUDA,
+         "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  }
+  return p;
+}
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+cudaEvent_t PhaseTimer::get() {
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  FPP_CUDA(cudaEventCreate(&e));
+  return e;
+}
+void PhaseTimer::begin(int, cudaStream_t s, cudaEvent_t* out) {
+  *out = get();
+  FPP_CUDA(cudaEventRecord(*out, s));
+}
+void PhaseTimer::end(int ph, cudaEvent_t start, cudaStream_t s) {
+  cudaEvent_t e = get();
+  FPP_CUDA(cudaEventRecord(e, s));
+  open.push_back({ph, {start, e}});
+}
+void PhaseTimer::collect(double* ms) {
+  for (auto& o : open) {
+    cudaEventSynchronize(o.second.second);
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, o.second.first, o.second.second) == cudaSuccess) ms[o.first] += t;
+    pool.push_back(o.second.first);
+    pool.push_back(o.second.second);
+  }
+  open.clear();
+}
+PhaseTimer::~PhaseTimer() {
+  for (auto& o : open) {
+    cudaEventDestroy(o.second.first);
+    cudaEventDestroy(o.second.second);
+  }
+  for (auto e : pool) cudaEventDestroy(e);
+}
+
+Index::~Index() {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  dfree(X);
+  dfree(signs);
+  dfree(offsets);
+  dfree(table_base);
+  dfree(ids);
+  dfree(scores);
+  q_vals.release(); q_codes.release(); q_ppos.release(); q_plen.release(); q_eq.release();
+  q_coff.release(); q_uq.release(); q_cands.release(); q_bitmap.release(); q_in.release();
+  q_ids.release(); q_scores.release(); q_stats.release(); q_counter.release();
+  if (h_pinned) cudaFreeHost(h_pinned);
+  if (stream) cudaStreamDestroy(stream);
+  cudaSetDevice(cur);
+}
+
+uint64_t host_mix64(uint64_t z) {  // common.hpp:18-23
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+uint64_t host_derive_seed(uint64_t m, uint64_t a, uint64_t b, uint64_t c) {  // common.hpp:27-34
+  uint64_t h = host_mix64(m);
+  h = host_mix64(h ^ (a * 0xff51afd7ed558ccdULL));
+  h = host_mix64(h ^ (b * 0xc4ceb9fe1a85ec53ULL));
+  h = host_mix64(h ^ (c * 0xd6e8feb86659fd93ULL));
+  return h;
+}
+
+// Sign bitmasks [L][K][3][W]: bit e of word w of stage s is sign index
+// s*P + 32w + e of the stack's stream (rotation.cpp:55-67; bit = 1 -> +1).
+void pack_signs(const fpp_params& p, uint32_t P, std::vector<uint32_t>& words) {
+  const uint32_t W = P < 32 ? 1 : P / 32;
+  words.assign((size_t)p.L * p.K * 3 * W, 0u);
+  std::vector<uint8_t> bits(3 * (size_t)P);
+  for (uint32_t t = 0; t < p.L; ++t)
+    for (uint32_t f = 0; f < p.K; ++f) {
+      uint64_t state = host_derive_seed(p.seed, t, f, 0), word = 0;
+      int left = 0;
+      for (size_t i = 0; i < bits.size(); ++i) {
+        if (left == 0) { word = host_mix64(state++); left = 64; }
+        bits[i] = (uint8_t)(word & 1u);
+        word >>= 1;
+        --left;
+      }
+      uint32_t* out = words.data() + ((size_t)t * p.K + f) * 3 * W;
+      for (uint32_t s = 0; s < 3; ++s)
+        for (uint32_t j = 0; j < P; ++j)
+          if (bits[(size_t)s * P + j]) out[s * W + j / 32] |= 1u << (j % 32);
+    }
+}
+
+static uint32_t isqrt_ceil(uint64_t q) {
+  uint64_t r = (uint64_t)std::sqrt((double)q);
+  while (r * r > q) --r;
+  while (r * r < q) ++r;
+  return (uint32_t)r;
+}
+
+// SPEC.md:211 per-function cap; K=1 uses min(2D, qProbes)
+uint32_t query_cap(const Index& ix, uint32_t qprobes) {
+  const uint64_t D2 = 2ull * ix.prm.D;
+  const uint64_t s = ix.prm.K == 2 ? 2ull * isqrt_ceil(qprobes) : qprobes;
+  return (uint32_t)std::min(s, D2);
+}
+uint64_t query_probes(const Index& ix, uint32_t qprobes) {
+  const uint64_t s = query_cap(ix, qprobes);
+  const uint64_t avail = (uint64_t)ix.prm.L * (ix.prm.K == 2 ? s * s : s);
+  return std::min<uint64_t>(qprobes, avail);
+}
+
+int sm_count() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+  }
+  return v;
+}
+
+__global__ void k_check_finite(const float* __restrict__ X, uint64_t cnt, unsigned long long* bad) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (!isfinite(X[i])) atomicMin(bad, (unsigned long long)i);
+}
+
+static void set_device(int dev) {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    fail(FPP_ERR_CUDA, "no CUDA device available (the GPU path has no CPU fallback)");
+  }
+  if (dev >= count) fail(FPP_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+  if (dev >= 0) FPP_CUDA(cudaSetDevice(dev));
+}
+
+static void validate_params(const fpp_params& p, uint64_t n, uint32_t d) {
+  if (n == 0) fail(FPP_ERR_EMPTY_DATASET, "dataset: need at least one point");
+  if (d == 0) fail(FPP_ERR_INVALID_ARGUMENT, "dataset: dim must be >= 1");
+  if (p.L == 0) fail(FPP_ERR_INVALID_ARGUMENT, "build: L must be >= 1");
+  if (p.K != 1 && p.K != 2) fail(FPP_ERR_INVALID_ARGUMENT, "build: K (concatenation l) must be 1 or 2");
+  if (p.D == 0 || (p.D & (p.D - 1)))
+    fail(FPP_ERR_INVALID_ARGUMENT, "SpinnerStack: D must be a power of two, got " + std::to_string(p.D));
+  if (!(p.alpha > 0.0f && p.alpha <= 1.0f)) fail(FPP_ERR_INVALID_ARGUMENT, "build: alpha must be in (0,1]");
+  if (p.iprobes == 0) fail(FPP_ERR_INVALID_ARGUMENT, "build: iProbes must be >= 1");
+  uint32_t P = 1;
+  while (P < d) P <<= 1;
+  if (p.D > P && p.D % P) fail(FPP_ERR_INVALID_ARGUMENT, "SpinnerStack: D must be a multiple of padded dim");
+  const uint64_t NB = p.K == 2 ? 4ull * p.D * p.D : 2ull * p.D;
+  if (p.iprobes > NB) fail(FPP_ERR_OUT_OF_RANGE, "index_probe_sequence: iProbes > number of buckets");
+  if (p.D > P) fail(FPP_ERR_UNSUPPORTED, "GPU path: D > d_pad (multi-block stacks) not supported");
+  if (P > 1024) fail(FPP_ERR_UNSUPPORTED, "GPU path: d_pad > 1024 not supported");
+  if (p.iprobes > std::min<uint32_t>(p.D, 16))
+    fail(FPP_ERR_UNSUPPORTED, "GPU path: iProbes must be <= min(D,16)");
+  if (n >= (1ull << 32) || n * p.iprobes >= (1ull << 32))
+    fail(FPP_ERR_UNSUPPORTED, "GPU path: n*iProbes must be < 2^32 per shard");
+}
+
+static fpp_index* build_common(const float* X, bool on_device, uint64_t n, uint32_t d,
+                               const fpp_params* pp) {
+  if (!pp) fail(FPP_ERR_INVALID_ARGUMENT, "build: params is NULL");
+  if (!X && n) fail(FPP_ERR_INVALID_ARGUMENT, "build: X is NULL");
+  const fpp_params p = *pp;
+  validate_params(p, n, d);
+  set_device(p.device);
+  if (!on_device) {  // dataset.cpp:15-18 finite check
+    int64_t bad = -1;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+    for (int64_t i = 0; i < (int64_t)(n * d); ++i)
+      if (!std::isfinite(X[i]) && bad < 0) bad = i;
+    if (bad >= 0)
+      fail(FPP_ERR_NON_FINITE, "dataset: non-finite coordinate in row " + std::to_string(bad / d));
+  }
+  auto* ix = new Index();
+  try {
+    ix->prm = p;
+    ix->n = n;
+    ix->d = d;
+    uint32_t P = 1;
+    while (P < d) P <<= 1;
+    ix->P = P;
+    ix->W = P < 32 ? 1 : P / 32;
+    ix->NB = p.K == 2 ? 4ull * p.D * p.D : 2ull * p.D;
+    FPP_CUDA(cudaGetDevice(&ix->device));
+    FPP_CUDA(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
+    FPP_CUDA(cudaMallocHost(&ix->h_pinned, 64));
+    ix->X = static_cast<float*>(dmalloc(n * d * sizeof(float)));
+    FPP_CUDA(cudaMemcpyAsync(ix->X, X, n * d * sizeof(float),
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                             ix->stream));
+    if (on_device) {
+      DBuf<unsigned long long> bad(1);
+      const unsigned long long init = ~0ull;
+      FPP_CUDA(cudaMemcpyAsync(bad.p, &init, 8, cudaMemcpyHostToDevice, ix->stream));
+      k_check_finite<<<sm_count() * 4, 256, 0, ix->stream>>>(ix->X, n * d, bad.p);
+      FPP_LAUNCH();
+      unsigned long long b = 0;
+      FPP_CUDA(cudaMemcpyAsync(&b, bad.p, 8, cudaMemcpyDeviceToHost, ix->stream));
+      FPP_CUDA(cudaStreamSynchronize(ix->stream));
+      if (b != ~0ull)
+        fail(FPP_ERR_NON_FINITE, "dataset: non-finite coordinate in row " + std::to_string(b / d));
+    }
+    std::vector<uint32_t> words;
+    pack_signs(p, P, words);
+    ix->signs = static_cast<uint32_t*>(dmalloc(words.size() * 4));
+    FPP_CUDA(cudaMemcpyAsync(ix->signs, words.data(), words.size() * 4, cudaMemcpyHostToDevice,
+                             ix->stream));
+    FPP_CUDA(cudaStreamSynchronize(ix->stream));
+    build_tables(*ix);
+    ix->device_bytes = n * d * 4 + words.size() * 4 + (uint64_t)p.L * (ix->NB + 1) * 4 +
+                       (p.L + 1) * 8 + ix->kept_total * 8;
+    double ms[PH_COUNT] = {0};
+    ix->timer.collect(ms);
+    ix->acc.hash_ms += ms[PH_HASH];
+    ix->acc.sort_ms += ms[PH_SORT];
+  } catch (...) {
+    delete ix;
+    throw;
+  }
+  return reinterpret_cast<fpp_index*>(ix);
+}
+
+static const Index& IX(const fpp_index* p) {
+  if (!p) fail(FPP_ERR_INVALID_ARGUMENT, "index is NULL");
+  return *reinterpret_cast<const Index*>(p);
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    FPP_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+static void validate_query(const Index& ix, uint64_t nq, uint32_t k, uint32_t qprobes,
+                           const void* Q, const void* ids, const void* scores) {
+  if (k == 0) fail(FPP_ERR_INVALID_ARGUMENT, "search: k must be >= 1");
+  if (k > ix.n) fail(FPP_ERR_OUT_OF_RANGE, "search: k > n");
+  if (k > 32) fail(FPP_ERR_UNSUPPORTED, "GPU path: k must be <= 32");
+  if (qprobes < ix.prm.L || (uint64_t)qprobes > (uint64_t)ix.prm.L * ix.NB)
+    fail(FPP_ERR_OUT_OF_RANGE, "query_probe_sequence: qProbes must be in [L, L*NB]");
+  if (nq && (!Q || !ids || !scores)) fail(FPP_ERR_INVALID_ARGUMENT, "search: NULL buffer");
+}
+
+static void collect_timings(const Index& ix) {
+  double ms[PH_COUNT] = {0};
+  ix.timer.collect(ms);
+  ix.acc.hash_ms += ms[PH_HASH];
+  ix.acc.sort_ms += ms[PH_SORT];
+  ix.acc.qhash_ms += ms[PH_QHASH];
+  ix.acc.probe_ms += ms[PH_PROBE];
+  ix.acc.collect_ms += ms[PH_COLLECT];
+  ix.acc.score_ms += ms[PH_SCORE];
+}
+
+}  // namespace fpp
+
+using namespace fpp;
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return FPP_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host out of memory";
+    return FPP_ERR_OUT_OF_MEMORY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FPP_ERR_CUDA;
+  }
+}
+
+extern "C" {
+
+int fpp_abi_version(void) { return FPP_ABI_VERSION; }
+const char* fpp_last_error(void) { return g_err.c_str(); }
+
+void fpp_default_params(fpp_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->L = 50;
+  p->K = 2;
+  p->D = 128;
+  p->iprobes = 3;
+  p->kappa = 20;
+  p->alpha = 0.1f;
+  p->seed = 1;
+  p->device = -1;
+}
+
+int fpp_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return c;
+}
+
+int fpp_build(const float* X, uint64_t n, uint32_t d, const fpp_params* p, fpp_index** out) {
+  return guarded([&] {
+    if (!out) fail(FPP_ERR_INVALID_ARGUMENT, "build: out is NULL");
+    *out = build_common(X, false, n, d, p);
+  });
+}
+
+int fpp_build_device(const float* X, uint64_t n, uint32_t d, const fpp_params* p, fpp_index** out) {
+  return guarded([&] {
+    if (!out) fail(FPP_ERR_INVALID_ARGUMENT, "build: out is NULL");
+    *out = build_common(X, true, n, d, p);
+  });
+}
+
+void fpp_free(fpp_index* idx) { delete reinterpret_cast<Index*>(idx); }
+
+int fpp_query(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uint32_t qprobes,
+              uint32_t* ids, double* scores, fpp_query_stats* stats) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    validate_query(ix, nq, k, qprobes, Q, ids, scores);
+    if (!nq) return;
+    DeviceGuard dg(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    cudaStream_t s = ix.stream;
+    ix.q_in.ensure(nq * ix.d);
+    ix.q_ids.ensure(nq * k);
+    ix.q_scores.ensure(nq * k);
+    if (stats) ix.q_stats.ensure(nq);
+    FPP_CUDA(cudaMemcpyAsync(ix.q_in.p, Q, nq * ix.d * 4, cudaMemcpyHostToDevice, s));
+    run_query(ix, ix.q_in.p, nq, k, qprobes, ix.q_ids.p, ix.q_scores.p, stats ? ix.q_stats.p : nullptr, s);
+    FPP_CUDA(cudaMemcpyAsync(ids, ix.q_ids.p, nq * k * 4, cudaMemcpyDeviceToHost, s));
+    FPP_CUDA(cudaMemcpyAsync(scores, ix.q_scores.p, nq * k * 8, cudaMemcpyDeviceToHost, s));
+    if (stats)
+      FPP_CUDA(cudaMemcpyAsync(stats, ix.q_stats.p, nq * sizeof(fpp_query_stats), cudaMemcpyDeviceToHost, s));
+    FPP_CUDA(cudaStreamSynchronize(s));
+    collect_timings(ix);
+  });
+}
+
+int fpp_query_device(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uint32_t qprobes,
+                     uint32_t* ids, double* scores, fpp_query_stats* stats, void* stream) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    validate_query(ix, nq, k, qprobes, Q, ids, scores);
+    if (!nq) return;
+    DeviceGuard dg(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ix.stream;
+    run_query(ix, Q, nq, k, qprobes, ids, scores, stats, s);
+  });
+}
+
+int fpp_index_info_get(const fpp_index* idx, fpp_index_info* info) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    if (!info) fail(FPP_ERR_INVALID_ARGUMENT, "info is NULL");
+    info->n = ix.n;
+    info->d = ix.d;
+    info->d_pad = ix.P;
+    info->L = ix.prm.L;
+    info->K = ix.prm.K;
+    info->D = ix.prm.D;
+    info->iprobes = ix.prm.iprobes;
+    info->kappa = ix.prm.kappa;
+    info->alpha = ix.prm.alpha;
+    info->seed = ix.prm.seed;
+    info->num_buckets = ix.NB;
+    info->kept_total = ix.kept_total;
+    info->prefilter_total = ix.n * ix.prm.L * ix.prm.iprobes;
+    info->device_bytes = ix.device_bytes;
+    info->max_bucket = ix.max_bucket;
+    info->id_offset = ix.prm.id_offset;
+  });
+}
+
+uint64_t fpp_table_size(const fpp_index* idx, uint32_t t) {
+  if (!idx) return 0;
+  const Index& ix = *reinterpret_cast<const Index*>(idx);
+  if (t >= ix.prm.L) return 0;
+  return ix.table_base_h[t + 1] - ix.table_base_h[t];
+}
+
+int fpp_table_csr(const fpp_index* idx, uint32_t t, uint32_t* offsets, uint32_t* ids, float* scores) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    if (t >= ix.prm.L) fail(FPP_ERR_OUT_OF_RANGE, "table index out of range");
+    DeviceGuard dg(ix.device);
+    const uint64_t b0 = ix.table_base_h[t], cnt = ix.table_base_h[t + 1] - b0;
+    if (offsets)
+      FPP_CUDA(cudaMemcpy(offsets, ix.offsets + (uint64_t)t * (ix.NB + 1), (ix.NB + 1) * 4,
+                          cudaMemcpyDeviceToHost));
+    if (ids && cnt) FPP_CUDA(cudaMemcpy(ids, ix.ids + b0, cnt * 4, cudaMemcpyDeviceToHost));
+    if (scores && cnt) FPP_CUDA(cudaMemcpy(scores, ix.scores + b0, cnt * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int fpp_project(const fpp_index* idx, const float* X, uint64_t n, uint32_t t, uint32_t f, float* out) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    if (t >= ix.prm.L || f >= ix.prm.K) fail(FPP_ERR_OUT_OF_RANGE, "project: (t,f) out of range");
+    if (!n) return;
+    DeviceGuard dg(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    DBuf<float> xd(n * ix.d), od(n * ix.prm.D);
+    FPP_CUDA(cudaMemcpy(xd.p, X, n * ix.d * 4, cudaMemcpyHostToDevice));
+    launch_project(ix, xd.p, n, t, f, od.p, ix.stream);
+    FPP_CUDA(cudaStreamSynchronize(ix.stream));
+    FPP_CUDA(cudaMemcpy(out, od.p, n * ix.prm.D * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int fpp_index_probes(const fpp_index* idx, const float* X, uint64_t n, uint32_t t, uint32_t* buckets,
+                     float* scores) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    if (t >= ix.prm.L) fail(FPP_ERR_OUT_OF_RANGE, "index_probes: table out of range");
+    if (!n) return;
+    DeviceGuard dg(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    const uint32_t ip = ix.prm.iprobes;
+    DBuf<float> xd(n * ix.d);
+    DBuf<uint2> od(n * ip);
+    FPP_CUDA(cudaMemcpy(xd.p, X, n * ix.d * 4, cudaMemcpyHostToDevice));
+    launch_index_probes(ix, xd.p, n, t, od.p, ix.stream);
+    FPP_CUDA(cudaStreamSynchronize(ix.stream));
+    std::vector<uint2> h(n * ip);
+    FPP_CUDA(cudaMemcpy(h.data(), od.p, n * ip * 8, cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < n * ip; ++i) {
+      buckets[i] = h[i].x;
+      std::memcpy(scores + i, &h[i].y, 4);
+    }
+  });
+}
+
+uint32_t fpp_query_cap(const fpp_index* idx, uint32_t qprobes) {
+  return idx ? query_cap(*reinterpret_cast<const Index*>(idx), qprobes) : 0;
+}
+uint64_t fpp_query_probes(const fpp_index* idx, uint32_t qprobes) {
+  return idx ? query_probes(*reinterpret_cast<const Index*>(idx), qprobes) : 0;
+}
+
+int fpp_query_lists(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t qprobes, float* vals,
+                    uint32_t* codes) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    if (!nq) return;
+    DeviceGuard dg(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    const uint32_t s = query_cap(ix, qprobes);
+    const uint64_t tot = nq * ix.prm.L * ix.prm.K * s;
+    DBuf<float> qd(nq * ix.d), vd(tot);
+    DBuf<uint32_t> cd(tot);
+    FPP_CUDA(cudaMemcpy(qd.p, Q, nq * ix.d * 4, cudaMemcpyHostToDevice));
+    launch_query_lists(ix, qd.p, nq, s, vd.p, cd.p, ix.stream);
+    FPP_CUDA(cudaStreamSynchronize(ix.stream));
+    FPP_CUDA(cudaMemcpy(vals, vd.p, tot * 4, cudaMemcpyDeviceToHost));
+    FPP_CUDA(cudaMemcpy(codes, cd.p, tot * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int fpp_query_debug(const fpp_index* idx, const float* q, uint32_t qprobes, uint64_t* probes,
+                    uint64_t* n_probes, uint32_t* cands, uint64_t* n_cands) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    validate_query(ix, 1, 1, qprobes, q, probes, cands);
+    DeviceGuard dg(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    DBuf<float> qd(ix.d);
+    FPP_CUDA(cudaMemcpy(qd.p, q, ix.d * 4, cudaMemcpyHostToDevice));
+    std::vector<uint64_t> pv;
+    std::vector<uint32_t> cv;
+    query_debug(ix, qd.p, qprobes, pv, cv);
+    std::memcpy(probes, pv.data(), pv.size() * 8);
+    std::memcpy(cands, cv.data(), cv.size() * 4);
+    *n_probes = pv.size();
+    *n_cands = cv.size();
+    collect_timings(ix);
+  });
+}
+
+int fpp_timings_get(const fpp_index* idx, fpp_timings* t) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    collect_timings(ix);
+    if (t) *t = ix.acc;
+  });
+}
+
+int fpp_timings_reset(const fpp_index* idx) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    collect_timings(ix);
+    ix.acc = fpp_timings{};
+  });
+}
+
+// dataset.cpp:24-38, parallel over rows (per-row arithmetic is the reference's)
+int fpp_normalize(float* X, uint64_t n, uint32_t d) {
+  return guarded([&] {
+    if (!X || !n || !d) fail(FPP_ERR_EMPTY_DATASET, "dataset: need at least one point");
+    int64_t bad = -1;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+    for (int64_t i = 0; i < (int64_t)n; ++i) {
+      float* row = X + (uint64_t)i * d;
+      double sq = 0.0;
+      for (uint32_t j = 0; j < d; ++j) sq += double(row[j]) * double(row[j]);
+      if (sq == 0.0) {
+        if (bad < 0) bad = i;
+        continue;
+      }
+      const float inv = float(1.0 / std::sqrt(sq));
+      for (uint32_t j = 0; j < d; ++j) row[j] *= inv;
+    }
+    if (bad >= 0) fail(FPP_ERR_ZERO_NORM, "normalize: zero-norm row " + std::to_string(bad));
+  });
+}
+
+// pinned synthetic generator
+static inline double synth_u(uint64_t seed, uint64_t stream, uint64_t k) {
+  return ((double)(host_mix64(host_derive_seed(seed, stream, k, 0)) >> 11) + 0.5) * 0x1.0p-53;
+}
+static inline double synth_normal(uint64_t seed, uint64_t stream, uint64_t k) {
+  const double u1 = synth_u(seed, stream, 2 * k), u2 = synth_u(seed, stream, 2 * k + 1);
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+}
+
+int fpp_synth(float* X, uint64_t n, uint32_t d, uint32_t clusters, float sigma, uint64_t seed,
+              uint32_t stream, int threads) {
+  return guarded([&] {
+    if (!X || !n || !d) fail(FPP_ERR_EMPTY_DATASET, "synth: empty");
+    if (threads <= 0) threads = omp_get_max_threads();
+    const uint64_t s_noise = 3 + 100ull * stream, s_assign = 2 + 100ull * stream;
+#pragma omp parallel for schedule(static) num_threads(threads)
+    for (int64_t i = 0; i < (int64_t)n; ++i) {
+      float* row = X + (uint64_t)i * d;
+      if (clusters == 0) {
+        for (uint32_t j = 0; j < d; ++j) row[j] = (float)synth_normal(seed, s_noise, (uint64_t)i * d + j);
+      } else {
+        const uint64_t c = host_mix64(host_derive_seed(seed, s_assign, (uint64_t)i, 0)) % clusters;
+        for (uint32_t j = 0; j < d; ++j) {
+          const double ctr = synth_normal(seed, 1, c * d + j);
+          const double z = synth_normal(seed, s_noise, (uint64_t)i * d + j);
+          row[j] = (float)(ctr + (double)sigma * z);
+        }
+      }
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,219 @@
+// fpp_device.cuh -- device primitives shared by the build and query kernels.
+//
+// * order-preserving float keys (total orders of DESIGN.md section 3)
+// * the warp-group Fast Hadamard Transform with the reference butterfly graph
+//   (rotation.cpp:16-32: len ascending, a[j]=x+y, a[j+len]=x-y), which is what
+//   makes GPU projections bit-identical to SpinnerStack::project
+// * group-wide top-R selection of (|p| desc, index asc) keys
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fpp {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// Monotone map float -> uint32 (ascending).  -0.0 is canonicalised to +0.0 so
+// that key equality coincides with float equality (ties compare equal).
+__device__ __forceinline__ uint32_t ord_key(float f) {
+  uint32_t u = __float_as_uint(f + 0.0f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord_inv(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// ---------------------------------------------------------------- FHT group
+// A group of G = P/EPT consecutive lanes holds one length-P vector, lane g
+// owning elements j = g*EPT + e (e in [0,EPT)).  Stages with len < EPT are
+// in-register; len >= EPT exchange with lane g ^ (len/EPT) through shfl.xor.
+// The stage ORDER is the reference's (len ascending), and each output element
+// is computed with the same operand order (x+y for the lower, x-y for the upper
+// element), so every intermediate is bit-identical to rotation.cpp:22-31.
+template <int P>
+struct FhtShape {
+  static constexpr int EPT = P < 32 ? P : 32;
+  static constexpr int G = P / EPT;    // lanes per vector
+  static constexpr int GPW = 32 / G;   // vectors per warp
+  static constexpr int W = P < 32 ? 1 : P / 32;  // 32-bit sign words per stage
+};
+
+template <int P, int EPT>
+__device__ __forceinline__ void fht_group(float (&v)[EPT], int g) {
+#pragma unroll
+  for (int len = 1; len < EPT; len <<= 1) {
+#pragma unroll
+    for (int i = 0; i < EPT; i += 2 * len) {
+#pragma unroll
+      for (int j = i; j < i + len; ++j) {
+        const float x = v[j], y = v[j + len];
+        v[j] = x + y;
+        v[j + len] = x - y;
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 1; m < P / EPT; m <<= 1) {
+    const bool upper = (g & m) != 0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const float o = __shfl_xor_sync(FULL, v[e], m);
+      v[e] = upper ? (o - v[e]) : (v[e] + o);
+    }
+  }
+}
+
+// Multiply by the +/-1 diagonal of one stage: bit e of `w` set -> +1, clear -> -1
+// (rotation.cpp:55-67,93).  Done as a sign-bit XOR, bit-identical to x * (+/-1.0f).
+template <int EPT>
+__device__ __forceinline__ void apply_signs(float (&v)[EPT], uint32_t w) {
+#pragma unroll
+  for (int e = 0; e < EPT; ++e)
+    v[e] = __uint_as_float(__float_as_uint(v[e]) ^ (((~w >> e) & 1u) << 31));
+}
+
+// Full SpinnerStack::project of one block (rotation.cpp:81-98): 3 x (signs, FHT),
+// then the exact power-of-two scale 1/P.  `sw` points at this stack's
+// [3][W] sign words.
+template <int P>
+__device__ __forceinline__ void spinner_project(float (&v)[FhtShape<P>::EPT], const uint32_t* sw,
+                                                int g) {
+  using S = FhtShape<P>;
+#pragma unroll
+  for (int stage = 0; stage < 3; ++stage) {
+    const uint32_t w = __ldg(sw + stage * S::W + (S::G > 1 ? g : 0));
+    apply_signs<S::EPT>(v, w);
+    fht_group<P, S::EPT>(v, g);
+  }
+  const float scale = 1.0f / (float)P;
+#pragma unroll
+  for (int e = 0; e < S::EPT; ++e) v[e] = v[e] * scale;
+}
+
+// Load row x[0..d) into the group layout, zero-padded to P (rotation.cpp:88-89).
+template <int P>
+__device__ __forceinline__ void load_row(const float* __restrict__ x, uint32_t d, int g,
+                                         float (&v)[FhtShape<P>::EPT]) {
+  constexpr int EPT = FhtShape<P>::EPT;
+  const uint32_t base = (uint32_t)g * EPT;
+  if ((d & 3u) == 0 && (EPT % 4) == 0) {
+#pragma unroll
+    for (int e = 0; e < EPT; e += 4) {
+      if (base + e < d) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(x + base + e));
+        v[e] = q.x; v[e + 1] = q.y; v[e + 2] = q.z; v[e + 3] = q.w;
+      } else {
+        v[e] = v[e + 1] = v[e + 2] = v[e + 3] = 0.0f;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) v[e] = (base + e < d) ? __ldg(x + base + e) : 0.0f;
+  }
+}
+
+// -------------------------------------------------------- top-R rank keys
+// key = (~ord(|p|)) << 32 | (j << 1) | (p < 0): ascending key order is
+// (|p| desc, j asc) -- the natural ranked list of DESIGN.md section 3; the low
+// bit carries the sign so the code (j or D+j) can be recovered.
+__device__ __forceinline__ uint64_t rank_key(float p, uint32_t j) {
+  const uint32_t hi = ~ord_key(fabsf(p));
+  return ((uint64_t)hi << 32) | ((uint64_t)j << 1) | (p < 0.0f ? 1u : 0u);
+}
+__device__ __forceinline__ float rank_val(uint64_t k) { return ord_inv(~(uint32_t)(k >> 32)); }
+__device__ __forceinline__ uint32_t rank_code(uint64_t k, uint32_t D) {
+  const uint32_t j = (uint32_t)(k & 0xffffffffu) >> 1;
+  return (k & 1u) ? D + j : j;
+}
+
+template <int R>
+__device__ __forceinline__ void topr_insert(uint64_t (&t)[R], uint64_t key) {
+  if (key >= t[R - 1]) return;
+  t[R - 1] = key;
+#pragma unroll
+  for (int i = R - 1; i > 0; --i) {
+    if (t[i] < t[i - 1]) {
+      const uint64_t a = t[i];
+      t[i] = t[i - 1];
+      t[i - 1] = a;
+    }
+  }
+}
+
+// merge sorted lists across the G lanes of a group (butterfly; every lane ends
+// with the group's R smallest keys, ascending).  Bitonic merge per step.
+template <int R, int G>
+__device__ __forceinline__ void topr_group_merge(uint64_t (&t)[R]) {
+#pragma unroll
+  for (int m = 1; m < G; m <<= 1) {
+    uint64_t o[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) o[i] = __shfl_xor_sync(FULL, t[i], m);
+    // t ascending, o ascending: min(t[i], o[R-1-i]) is bitonic and holds the R smallest
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const uint64_t b = o[R - 1 - i];
+      t[i] = t[i] < b ? t[i] : b;
+    }
+#pragma unroll
+    for (int k = R / 2; k > 0; k >>= 1) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int p = i ^ k;
+        if (p > i) {
+          const uint64_t a = t[i], b = t[p];
+          t[i] = a < b ? a : b;
+          t[p] = a < b ? b : a;
+        }
+      }
+    }
+  }
+}
+
+// exclusive block-wide scan (all threads must call); sh >= 32 words
+__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sh, uint32_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    uint32_t s = lane < nw ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) sh[lane] = s;
+  }
+  __syncthreads();
+  const uint32_t wbase = w ? sh[w - 1] : 0;
+  if (total) *total = sh[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return wbase + x - v;
+}
+
+// ------------------------------------------------------------ misc helpers
+__device__ __forceinline__ uint64_t desc_score_key(float s, uint32_t id) {
+  return ((uint64_t)(~ord_key(s)) << 32) | id;  // ascending = (score desc, id asc)
+}
+__device__ __forceinline__ float desc_score_val(uint64_t k) {
+  return ord_inv(~(uint32_t)(k >> 32));
+}
+
+// exact keep count, SPEC.md:257 / SURVEY 8(c): min(B, max(kappa, floor(double(alpha)*B/iP)))
+__device__ __host__ __forceinline__ uint32_t keep_count(uint32_t B, float alpha, uint32_t ip,
+                                                        uint32_t kappa) {
+  const double f = floor((double)alpha * (double)B / (double)ip);
+  uint64_t k = (uint64_t)f;
+  if (k < kappa) k = kappa;
+  if (k > B) k = B;
+  return (uint32_t)k;
+}
+
+}  // namespace fpp

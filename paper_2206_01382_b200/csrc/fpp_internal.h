@@ -1,0 +1,135 @@
+// fpp_internal.h -- host-side index object and kernel entry points shared by
+// fpp_capi.cu, fpp_build.cu and fpp_query.cu.  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/falconnpp.h"
+
+namespace fpp {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define FPP_CUDA(x) ::fpp::cuda_check((x), #x, __FILE__, __LINE__)
+#define FPP_LAUNCH() ::fpp::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// device allocation with OOM -> FPP_ERR_OUT_OF_MEMORY
+void* dmalloc(size_t bytes);
+void dfree(void* p);
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    if (count) p = static_cast<T*>(dmalloc(count * sizeof(T)));
+    n = count;
+  }
+  // grow without preserving contents
+  void ensure(size_t count) {
+    if (count > n) alloc(count + count / 4);
+  }
+  void release() {
+    if (p) dfree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// Phase timer: CUDA events recorded on the launching stream around each phase.
+enum Phase { PH_HASH = 0, PH_SORT, PH_QHASH, PH_PROBE, PH_COLLECT, PH_SCORE, PH_COUNT };
+struct PhaseTimer {
+  bool enabled = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> open;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get();
+  void begin(int ph, cudaStream_t s, cudaEvent_t* out_start);
+  void end(int ph, cudaEvent_t start, cudaStream_t s);
+  void collect(double* ms_by_phase);  // after stream sync
+  ~PhaseTimer();
+};
+
+struct Index {
+  fpp_params prm{};
+  uint64_t n = 0;
+  uint32_t d = 0, P = 0;  // P = d_pad = FHT length
+  uint64_t NB = 0;        // buckets per table
+  int device = 0;
+  cudaStream_t stream = nullptr;
+
+  float* X = nullptr;         // [n][d] device, owned
+  uint32_t* signs = nullptr;  // [L][K][3][W] device
+  uint32_t W = 1;
+  uint32_t* offsets = nullptr;  // [L][NB+1] kept offsets, relative to table base
+  uint64_t* table_base = nullptr;  // [L+1] device
+  std::vector<uint64_t> table_base_h;
+  uint32_t* ids = nullptr;   // [kept_total] local ids
+  float* scores = nullptr;   // [kept_total]
+  uint64_t kept_total = 0;
+  uint32_t max_bucket = 0;
+  uint64_t device_bytes = 0;
+
+  // query scratch (guarded by mu; concurrent queries serialize on it)
+  mutable std::mutex mu;
+  mutable DBuf<float> q_vals;
+  mutable DBuf<uint32_t> q_codes;
+  mutable DBuf<uint64_t> q_ppos;
+  mutable DBuf<uint32_t> q_plen;
+  mutable DBuf<uint32_t> q_eq;
+  mutable DBuf<uint64_t> q_coff;
+  mutable DBuf<uint32_t> q_uq;
+  mutable DBuf<uint32_t> q_cands;
+  mutable DBuf<uint32_t> q_bitmap;
+  mutable DBuf<float> q_in;
+  mutable DBuf<uint32_t> q_ids;
+  mutable DBuf<double> q_scores;
+  mutable DBuf<fpp_query_stats> q_stats;
+  mutable DBuf<uint32_t> q_counter;
+  uint64_t* h_pinned = nullptr;  // small pinned readback
+
+  mutable PhaseTimer timer;
+  mutable fpp_timings acc{};
+
+  ~Index();
+};
+
+// host helpers (fpp_capi.cu)
+uint64_t host_mix64(uint64_t z);
+uint64_t host_derive_seed(uint64_t m, uint64_t a, uint64_t b, uint64_t c);
+void pack_signs(const fpp_params& p, uint32_t P, std::vector<uint32_t>& words);
+uint32_t query_cap(const Index& ix, uint32_t qprobes);
+uint64_t query_probes(const Index& ix, uint32_t qprobes);
+int sm_count();
+
+// build (fpp_build.cu)
+void build_tables(Index& ix);
+void launch_project(const Index& ix, const float* Xd, uint64_t n, uint32_t t, uint32_t f,
+                    float* out, cudaStream_t s);
+void launch_index_probes(const Index& ix, const float* Xd, uint64_t n, uint32_t t,
+                         uint2* out, cudaStream_t s);
+
+// query (fpp_query.cu)
+void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t qprobes,
+               uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s);
+void launch_query_lists(const Index& ix, const float* Qd, uint64_t nq, uint32_t s_cap,
+                        float* vals, uint32_t* codes, cudaStream_t s);
+// probes (t*NB+b) and candidates of query 0 of Qd (debug/parity)
+void query_debug(const Index& ix, const float* qd, uint32_t qprobes,
+                 std::vector<uint64_t>& probes, std::vector<uint32_t>& cands);
+
+}  // namespace fpp

@@ -1,0 +1,196 @@
+"""GPU parity: every intermediate of the CUDA path against the CPU oracle.
+
+Bar (BASELINE.json north star): projections, hash codes,
+index probes, kept-bucket CSR (ids + scores), ranked query lists, probe sets and
+candidate sets are bit-exact; top-k ids identical (ties by lower id); scores are
+asserted bit-exact too (the score kernel accumulates in the reference's
+sequential fp64 order) -- the north-star tolerance would be 1e-5 relative.
+All calls go through the C ABI (paper_2206_01382_b200 -> libfalconnpp_b200.so).
+"""
+import numpy as np
+import pytest
+
+from tests.conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+SCORE_RTOL = 1e-5  # north-star tolerance; the GPU path is in fact bit-exact
+
+
+def data(fpp, n, d, clusters=0, sigma=0.0, seed=1, stream=0):
+    return fpp.normalize(fpp.synth(n, d, clusters, sigma, seed=seed, stream=stream))
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+@pytest.mark.parametrize("d", [2, 5, 17, 32, 100, 128, 256, 300, 960])
+def test_projection_bitexact(fpp, orc, d):
+    X = data(fpp, 257, d)
+    P = orc.lib().orc_pad_dimension(d)
+    ix = fpp.Index.build(X, L=3, K=2, D=P, iProbes=1, alpha=1.0)
+    for t in range(3):
+        for f in range(2):
+            seed = orc.lib().orc_derive_seed(1, t, f, 0)
+            ref = orc.project_rows(X, P, seed)
+            got = ix.project(X, t, f)
+            assert np.array_equal(bits(got), bits(ref)), (d, t, f)
+            assert np.array_equal(orc.cp_hash_rows(got), orc.cp_hash_rows(ref))
+
+
+def test_projection_truncated_D(fpp, orc):
+    X = data(fpp, 100, 200)  # d_pad 256, D = 64 < d_pad (rotation.cpp:51-53,96-98)
+    ix = fpp.Index.build(X, L=2, K=2, D=64, iProbes=2, alpha=0.5)
+    for t in range(2):
+        for f in range(2):
+            seed = orc.lib().orc_derive_seed(1, t, f, 0)
+            assert np.array_equal(bits(ix.project(X, t, f)), bits(orc.project_rows(X, 64, seed)))
+
+
+@pytest.mark.parametrize("K,D,ip,d", [(2, 128, 3, 128), (2, 512, 3, 300), (2, 1024, 3, 960),
+                                      (2, 256, 5, 256), (1, 128, 3, 128), (2, 64, 1, 100),
+                                      (2, 32, 16, 32), (1, 16, 9, 16), (2, 64, 7, 200)])
+def test_index_probes_bitexact(fpp, orc, K, D, ip, d):
+    X = data(fpp, 500, d, clusters=7, sigma=0.3)
+    ix = fpp.Index.build(X, L=2, K=K, D=D, iProbes=ip, alpha=0.5)
+    ox = orc.Index(X, L=2, K=K, D=D, iprobes=ip, alpha=0.5)
+    for t in range(2):
+        gb, gs = ix.index_probes(X, t)
+        ob, os_ = ox.index_probes(X, t)
+        assert np.array_equal(gb, ob), (K, D, ip, t)
+        assert np.array_equal(bits(gs), bits(os_)), (K, D, ip, t)
+
+
+CSR_CASES = [
+    # name, n, d, clusters, sigma, L, K, D, ip, alpha, kappa
+    ("c1_small", 20000, 128, 0, 0.0, 3, 2, 128, 3, 0.1, 20),
+    ("clustered", 20000, 64, 20, 0.25, 3, 2, 64, 3, 0.05, 20),
+    ("one_cluster_big_buckets", 30000, 64, 1, 0.05, 2, 2, 64, 3, 0.1, 20),
+    ("alpha1_full_sort", 30000, 32, 1, 0.05, 2, 2, 32, 2, 1.0, 0),
+    ("kappa0_stress", 20000, 128, 10, 0.3, 2, 2, 128, 3, 0.01, 0),
+    ("K1", 10000, 64, 0, 0.0, 3, 1, 64, 3, 0.3, 5),
+    ("d300", 8000, 300, 50, 0.3, 2, 2, 512, 3, 0.05, 20),
+]
+
+
+@pytest.mark.parametrize("case", CSR_CASES, ids=[c[0] for c in CSR_CASES])
+def test_csr_bitexact(fpp, orc, case):
+    _, n, d, C, sg, L, K, D, ip, al, ka = case
+    X = data(fpp, n, d, C, sg)
+    ix = fpp.Index.build(X, L=L, K=K, D=D, iProbes=ip, alpha=al, kappa=ka)
+    ox = orc.Index(X, L=L, K=K, D=D, iprobes=ip, alpha=al, kappa=ka)
+    tot = 0
+    for t in range(L):
+        go, gi, gs = ix.table(t)
+        oo, oi, os_ = ox.table(t)
+        assert np.array_equal(go, oo), t
+        assert np.array_equal(gi, oi), t
+        assert np.array_equal(gs, os_), t  # float == (canonical +-0)
+        tot += len(oi)
+    info = ix.info()
+    assert info["kept_total"] == tot
+    assert info["prefilter_total"] == n * L * ip
+
+
+@pytest.mark.parametrize("qp", [50, 137, 1000, 5000, 40000])
+def test_query_lists_bitexact(fpp, orc, qp):
+    X = data(fpp, 3000, 100, 10, 0.3)
+    Q = data(fpp, 9, 100, 10, 0.3, stream=1)
+    L = 5
+    ix = fpp.Index.build(X, L=L, K=2, D=128, iProbes=3, alpha=0.1)  # s > D for qp >= 5000
+    ox = orc.Index(X, L=L, K=2, D=128, iprobes=3, alpha=0.1)
+    s = ix.cap(qp)
+    assert s == ox.cap(qp)
+    gv, gc = ix.query_lists(Q, qp)
+    for i in range(len(Q)):
+        ov, oc = ox.query_lists(Q[i], s)
+        assert np.array_equal(bits(gv[i]), bits(ov)), (qp, i)
+        assert np.array_equal(gc[i], oc), (qp, i)
+
+
+QUERY_CASES = [
+    # name, n, d, clusters, sigma, L, K, D, ip, alpha, kappa, qprobes list
+    ("c1_like", 20000, 128, 0, 0.0, 10, 2, 128, 3, 0.1, 20, [10, 100, 1000, 3000]),
+    ("c2_like", 12000, 300, 100, 0.3, 8, 2, 512, 3, 0.05, 20, [8, 800, 2000, 20000]),
+    ("c4_like_s_gt_D", 20000, 128, 100, 0.25, 6, 2, 128, 3, 0.01, 20, [5000, 100000]),
+    ("K1", 5000, 64, 0, 0.0, 6, 1, 64, 2, 0.5, 10, [6, 60, 768]),
+    ("wide_c3_like", 4000, 960, 20, 0.2, 4, 2, 1024, 3, 0.02, 20, [1000, 10000]),
+]
+
+
+@pytest.mark.parametrize("case", QUERY_CASES, ids=[c[0] for c in QUERY_CASES])
+def test_query_parity(fpp, orc, case):
+    _, n, d, C, sg, L, K, D, ip, al, ka, qps = case
+    X = data(fpp, n, d, C, sg)
+    Q = data(fpp, 64, d, C, sg, stream=1)
+    ix = fpp.Index.build(X, L=L, K=K, D=D, iProbes=ip, alpha=al, kappa=ka)
+    ox = orc.Index(X, L=L, K=K, D=D, iprobes=ip, alpha=al, kappa=ka)
+    k = 20
+    for qp in qps:
+        gi, gs, gst = ix.query(Q, k, qp, return_stats=True)
+        oi, os_, ost = ox.query(Q, k, qp)
+        assert np.array_equal(gst, ost), qp
+        assert np.array_equal(gi, oi), qp
+        ok = np.isfinite(os_)
+        assert np.array_equal(np.isfinite(gs), ok)
+        np.testing.assert_allclose(gs[ok], os_[ok], rtol=SCORE_RTOL, atol=0)
+        assert np.array_equal(gs[ok], os_[ok]), "scores expected bit-exact"
+        for qi in (0, 7, 31):
+            gp, gc = ix.query_debug(Q[qi], qp)
+            op, oc = ox.query_debug(Q[qi], qp)
+            assert np.array_equal(gp, op), (qp, qi)
+            assert np.array_equal(gc, oc), (qp, qi)
+
+
+def test_acceptance4_exhaustive_equals_bruteforce(fpp, orc):
+    # alpha=1, iProbes=1, qProbes=L*4D^2 must equal brute force
+    X = data(fpp, 2000, 32, seed=3)
+    Q = data(fpp, 100, 32, seed=3, stream=1)
+    L, D = 2, 32
+    ix = fpp.Index.build(X, L=L, K=2, D=D, iProbes=1, alpha=1.0, kappa=0)
+    gi, gs = ix.query(Q, 20, L * 4 * D * D)
+    bi, bs = orc.brute_force(X, Q, 20)
+    assert np.array_equal(gi, bi)
+    assert np.array_equal(gs, bs)
+
+
+def test_duplicates_tie_lower_id(fpp, orc):
+    X = data(fpp, 1000, 64, seed=5)
+    X[500:510] = X[3]  # exact duplicates: equal scores, lower id first
+    Q = X[3:4].copy()
+    ix = fpp.Index.build(X, L=4, K=2, D=64, iProbes=3, alpha=1.0, kappa=0)
+    ox = orc.Index(X, L=4, K=2, D=64, iprobes=3, alpha=1.0, kappa=0)
+    gi, gs = ix.query(Q, 20, 400)
+    oi, os_, _ = ox.query(Q, 20, 400)
+    assert np.array_equal(gi, oi)
+    assert list(gi[0][:11]) == [3] + list(range(500, 510))
+
+
+def test_fewer_candidates_than_k(fpp, orc):
+    X = data(fpp, 5000, 64, seed=9)
+    Q = data(fpp, 8, 64, seed=9, stream=1)
+    ix = fpp.Index.build(X, L=1, K=2, D=64, iProbes=1, alpha=0.01, kappa=1)
+    ox = orc.Index(X, L=1, K=2, D=64, iprobes=1, alpha=0.01, kappa=1)
+    gi, gs, gst = ix.query(Q, 32, 1, return_stats=True)
+    oi, os_, ost = ox.query(Q, 32, 1)
+    assert np.array_equal(gi, oi) and np.array_equal(gst, ost)
+    assert (gi == 0xFFFFFFFF).any() and np.isneginf(gs[gi == 0xFFFFFFFF]).all()
+
+
+def test_empty_batch_and_errors(fpp):
+    X = data(fpp, 100, 16)
+    ix = fpp.Index.build(X, L=2, K=2, D=16, iProbes=1, alpha=1.0)
+    ids, sc = ix.query(np.zeros((0, 16), np.float32), 5, 4)
+    assert ids.shape == (0, 5)
+    with pytest.raises(fpp.FppOutOfRange):
+        ix.query(X[:2], 5, 1)  # qProbes < L
+    with pytest.raises(fpp.FppOutOfRange):
+        ix.query(X[:2], 101, 4)  # k > n
+    with pytest.raises(fpp.FppDimensionError):
+        ix.query(np.zeros((1, 15), np.float32), 5, 4)
+    bad = X.copy()
+    bad[7, 3] = np.nan
+    with pytest.raises(fpp.FppNonFinite):
+        fpp.Index.build(bad, L=2, K=2, D=16, iProbes=1, alpha=1.0)
