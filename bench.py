@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""bench.py -- Falconn++ hot path on B200: batched query throughput (+ build points/s).
+
+Default (N=1): BASELINE.json configs[1] ("c2"): n=1.2M d=300 1000-cluster mixture
+(sigma 0.3) normalized, L=100 K=2 D=512 iProbes=3 alpha=0.05 kappa=20, 10,000
+queries, k=20, headline qProbes=10,000 (the 1k-20k sweep is reported beside it).
+A step = one batched query of all nq queries through the hot path (hash ->
+probe select -> bucket walk/dedup -> row gather + fp64 dot + top-k).
+
+  python bench.py [--gpus N --steps K --warmup W --config c2 --qprobes 10000]
+  python bench.py --impl reference ...   # CPU oracle port on the host cores
+
+Multi-GPU (torchrun, one rank per GPU): rank g indexes ids [g*n/G,(g+1)*n/G),
+queries are replicated, per-rank top-k lists are merged after an NCCL
+all-gather; value = nq*K / (max over ranks of the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: n, d, clusters, sigma, L, K, D, iprobes, alpha, nq, qprobes(headline), sweep
+    "c1": dict(n=100_000, d=128, clusters=0, sigma=0.0, L=50, K=2, D=128, iprobes=3, alpha=0.1,
+               nq=1000, qprobes=1000, sweep=[50, 200, 1000]),
+    "c2": dict(n=1_200_000, d=300, clusters=1000, sigma=0.3, L=100, K=2, D=512, iprobes=3,
+               alpha=0.05, nq=10_000, qprobes=10_000, sweep=[1000, 2000, 5000, 10_000, 20_000]),
+    "c3": dict(n=1_000_000, d=960, clusters=500, sigma=0.2, L=100, K=2, D=1024, iprobes=3,
+               alpha=0.02, nq=1000, qprobes=10_000, sweep=[10_000]),
+    "c4": dict(n=10_000_000, d=128, clusters=10_000, sigma=0.25, L=50, K=2, D=128, iprobes=3,
+               alpha=0.01, nq=100_000, qprobes=5000, sweep=[5000]),
+}
+K_TOP = 20
+KAPPA = 20
+SEED = 1
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_data(cfg, lo, hi, gen):
+    """Rows [lo,hi) of the pinned synthetic dataset + all queries, normalized once."""
+    X = gen.synth(hi, cfg["d"], cfg["clusters"], cfg["sigma"], seed=SEED, stream=0)[lo:hi]
+    X = gen.normalize(X)
+    Q = gen.normalize(gen.synth(cfg["nq"], cfg["d"], cfg["clusters"], cfg["sigma"], seed=SEED,
+                                stream=1))
+    return np.ascontiguousarray(X), Q
+
+
+def cpu_baseline(cfg, X, Q, ix, qprobes, budget_s=20.0):
+    """Oracle port on this host: query sample over the GPU-built (bit-exact) CSR, and one
+    table of the build extrapolated linearly in L."""
+    from oracle import oracle as orc
+    threads = os.cpu_count() or 1
+    L = cfg["L"]
+    info = ix.info()
+    offs, ids, scs, tb = [], [], [], [0]
+    for t in range(L):
+        o, i, s = ix.table(t)
+        offs.append(o)
+        ids.append(i)
+        scs.append(s)
+        tb.append(tb[-1] + len(i))
+    csr = (np.stack(offs), np.concatenate(ids), np.concatenate(scs), np.array(tb, np.uint64))
+    ox = orc.Index(X, L=L, K=cfg["K"], D=cfg["D"], iprobes=cfg["iprobes"], alpha=cfg["alpha"],
+                   kappa=KAPPA, seed=SEED, csr=csr)
+    del csr, offs, ids, scs
+    # calibrate then run a bounded sample of queries with all host threads
+    m = min(len(Q), threads)
+    t0 = time.perf_counter()
+    ox.query(Q[:m], K_TOP, qprobes, threads=threads)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    ns = int(min(len(Q), max(m, m * budget_s * 0.6 / dt)))
+    t0 = time.perf_counter()
+    ox.query(Q[:ns], K_TOP, qprobes, threads=threads)
+    tq = time.perf_counter() - t0
+    qps = ns / tq
+    # build: one table, all threads, extrapolated to L tables
+    t0 = time.perf_counter()
+    ob = orc.Index(X, L=L, K=cfg["K"], D=cfg["D"], iprobes=cfg["iprobes"], alpha=cfg["alpha"],
+                   kappa=KAPPA, seed=SEED, threads=threads, t_begin=0, t_end=1)
+    tb1 = time.perf_counter() - t0
+    del ob
+    build_pps = len(X) / (tb1 * L)
+    return {"value": qps, "unit": "queries/s", "cores": threads, "kind": "port",
+            "sample": f"{ns} of {len(Q)} queries at qProbes={qprobes} over the full "
+                      f"{L}-table index (CSR imported from the GPU build, bit-exact); "
+                      f"{threads} OpenMP threads",
+            "build_points_per_s": build_pps,
+            "build_sample": f"1 of {L} tables on all {len(X)} points, extrapolated linearly in L",
+            "kept_total": info["kept_total"]}
+
+
+def run_reference(args, cfg, qprobes):
+    """--impl reference: the CPU oracle port (the reference ships no hashing/index/query
+    code) on the host cores, same config/metric/unit."""
+    from oracle import oracle as orc
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n = cfg["n"]
+    X, Q = make_data(cfg, 0, n, orc)
+    log(f"[reference] oracle build of {cfg['L']} tables on {threads} threads ...")
+    t0 = time.perf_counter()
+    ox = orc.Index(X, L=cfg["L"], K=cfg["K"], D=cfg["D"], iprobes=cfg["iprobes"],
+                   alpha=cfg["alpha"], kappa=KAPPA, seed=SEED, threads=threads)
+    tbuild = time.perf_counter() - t0
+    log(f"[reference] build {tbuild:.1f}s")
+    m = min(len(Q), threads)
+    t0 = time.perf_counter()
+    ox.query(Q[:m], K_TOP, qprobes, threads=threads)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    ns = int(min(len(Q), max(m, m * 8.0 / dt)))  # ~8 s per step
+    for w in range(args.warmup):
+        ox.query(Q[:m], K_TOP, qprobes, threads=threads)
+    times = []
+    for s in range(args.steps):
+        t0 = time.perf_counter()
+        ox.query(Q[:ns], K_TOP, qprobes, threads=threads)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    qps = ns * args.steps / tot
+    line = {
+        "metric": "queries/s (k=20)", "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64",
+        "data": "synthetic (pinned seeded generator, DESIGN.md section 6)", "impl": "reference",
+        "config": {"workload": args.config, "n": n, "d": cfg["d"], "L": cfg["L"], "K": cfg["K"],
+                   "D": cfg["D"], "iProbes": cfg["iprobes"], "alpha": cfg["alpha"],
+                   "kappa": KAPPA, "qProbes": qprobes, "k": K_TOP, "nq_per_step": ns},
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "port",
+                         "sample": f"{ns} of {cfg['nq']} queries per step, full {cfg['L']}-table "
+                                   f"oracle index built on CPU"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "build_points_per_s": n / tbuild,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--qprobes", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-recall", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    qprobes = args.qprobes or cfg["qprobes"]
+    if args.impl == "reference":
+        return run_reference(args, cfg, qprobes)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2206_01382_b200 as fpp
+    from paper_2206_01382_b200 import dist as fdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, d, nq = cfg["n"], cfg["d"], cfg["nq"]
+    lo, hi = fdist.shard_range(n, world, rank)
+    t0 = time.perf_counter()
+    X, Q = make_data(cfg, lo, hi, fpp)
+    log(f"[rank {rank}] data {time.perf_counter() - t0:.1f}s shard [{lo},{hi})")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---------------------------------------------------------------- build
+    Xd = torch.from_numpy(X).cuda()
+    barrier()
+    torch.cuda.synchronize()
+    tb0 = time.perf_counter()
+    ix = fpp.Index.build(Xd, L=cfg["L"], K=cfg["K"], D=cfg["D"], iProbes=cfg["iprobes"],
+                         alpha=cfg["alpha"], kappa=KAPPA, seed=SEED, device=local, id_offset=lo)
+    torch.cuda.synchronize()
+    tbuild = time.perf_counter() - tb0
+    tim = ix.timings()
+    build_dev_ms = tim["hash_ms"] + tim["sort_ms"]
+    tb_t = torch.tensor([tbuild, build_dev_ms / 1e3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tb_t, op=dist.ReduceOp.MAX)
+    tbuild_max, tbuild_dev_max = tb_t.tolist()
+    info = ix.info()
+    log(f"[rank {rank}] build {tbuild:.3f}s (device {build_dev_ms:.1f} ms: hash "
+        f"{tim['hash_ms']:.1f} sort {tim['sort_ms']:.1f}) kept {info['kept_total']}")
+    del Xd
+
+    # ---------------------------------------------------------------- query
+    Qd = torch.from_numpy(Q).cuda()
+    ids_d = torch.empty((nq, K_TOP), dtype=torch.int32, device="cuda")
+    sc_d = torch.empty((nq, K_TOP), dtype=torch.float64, device="cuda")
+    st_d = torch.empty((nq, 3), dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def step(qp, stats=None):
+        ix.query_device(Qd, ids_d, sc_d, K_TOP, qp, stats=stats, stream=stream)
+        if world > 1:
+            fdist.allgather_merge(sc_d, ids_d.view(torch.int32).to(torch.int64) & 0xFFFFFFFF,
+                                  K_TOP)
+
+    step(qprobes, st_d)
+    torch.cuda.synchronize()
+    st = st_d.cpu().numpy().astype(np.uint64)
+    P_sum, E_sum, U_sum = (int(x) for x in st.sum(axis=0))
+    for _ in range(args.warmup - 1):
+        step(qprobes)
+    ix.reset_timings()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            step(qprobes)
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    tim = ix.timings()
+    qps = nq * args.steps / (t_ms / 1e3)
+
+    # roofline of the dominant kernel (k_score): algorithmic bytes per launch / launch time
+    hbm, peak_kind = peaks()
+    score_bytes_step = 4 * d * U_sum + 4 * U_sum + 4 * d * nq + 12 * K_TOP * nq
+    path_bytes_step = 8 * P_sum + 4 * E_sum + 4 * d * U_sum + 4 * d * nq + 12 * K_TOP * nq
+    score_ms = tim["score_ms"] / args.steps
+    achieved = score_bytes_step / (score_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "score_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tj = json.load(f)
+            if tj.get("config") == args.config and tj.get("qprobes") == qprobes:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    launches_per_step = tim["launches"] / args.steps
+
+    # --------------------------------------------------------- e2e (host API)
+    import torch as _t
+    Qh = _t.empty((nq, d), dtype=_t.float32).pin_memory().numpy()
+    Qh[:] = Q
+    ix.query(Qh, K_TOP, qprobes)
+    barrier()
+    te0 = time.perf_counter()
+    for _ in range(args.steps):
+        ids_h, sc_h = ix.query(Qh, K_TOP, qprobes)
+        if world > 1:
+            s_t = torch.from_numpy(sc_h).cuda()
+            i_t = torch.from_numpy(ids_h.astype(np.int64)).cuda()
+            ms, mi = fdist.allgather_merge(s_t, i_t, K_TOP)
+            mi.cpu()
+    te = time.perf_counter() - te0
+    tet = torch.tensor([te], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tet, op=dist.ReduceOp.MAX)
+    e2e_qps = nq * args.steps / float(tet.item())
+
+    # ---------------------------------------------- qProbes sweep (+ recall)
+    sweep = []
+    if not args.no_sweep and world == 1:
+        gt = None
+        if not args.no_recall:
+            nr = min(nq, 1000)
+            Xall = torch.from_numpy(X).cuda().double()
+            S = Qd[:nr].double() @ Xall.T
+            # ties by lower id: topk on score then stable by id is overkill at fp64; use topk
+            gt = torch.topk(S, K_TOP, dim=1).indices.cpu().numpy()
+            del Xall, S
+        for qp in cfg["sweep"]:
+            ix.reset_timings()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            step(qp)
+            torch.cuda.synchronize()
+            e0.record()
+            step(qp)
+            e1.record()
+            torch.cuda.synchronize()
+            row = {"qprobes": qp, "queries_per_s": nq / (e0.elapsed_time(e1) / 1e3)}
+            if gt is not None:
+                got = ids_d[:len(gt)].cpu().numpy().view(np.uint32)
+                rec = np.mean([len(set(got[i]) & set(gt[i])) / K_TOP for i in range(len(gt))])
+                row["recall_at_20"] = float(rec)
+            sweep.append(row)
+
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(cfg, X, Q, ix, qprobes)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "error": repr(e)}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": "queries/s (k=20)", "value": qps, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f32 (FHT, pair scores) / f64 (inner products)",
+            "data": "synthetic (pinned seeded generator, DESIGN.md section 6; stands in for the "
+                    "paper's corpora)",
+            "config": {"workload": args.config, "n": n, "d": d, "clusters": cfg["clusters"],
+                       "sigma": cfg["sigma"], "L": cfg["L"], "K": cfg["K"], "D": cfg["D"],
+                       "iProbes": cfg["iprobes"], "alpha": cfg["alpha"], "kappa": KAPPA,
+                       "qProbes": qprobes, "k": K_TOP, "nq": nq,
+                       "parallelism": f"shard{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (X %.2f GB gathered at random)" % (
+                           n * d * 4 / 1e9)},
+            "roofline": {"kernel": "k_score", "bound": "hbm", "achieved": achieved,
+                         "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "algorithmic_bytes_per_step": score_bytes_step,
+                         "launches_per_step": launches_per_step,
+                         "kernel_ms_per_step": score_ms,
+                         "share_of_step": score_ms / (t_ms / args.steps)},
+            "path": {"algorithmic_bytes_per_step": path_bytes_step,
+                     "achieved_gbs": path_bytes_step / (t_ms / args.steps / 1e3) / 1e9,
+                     "frac_of_hbm": path_bytes_step / (t_ms / args.steps / 1e3) / 1e9 / hbm,
+                     "mean_probes": P_sum / nq, "mean_entries": E_sum / nq,
+                     "mean_candidates": U_sum / nq,
+                     "phase_ms_per_step": {k: tim[k] / args.steps for k in
+                                           ("qhash_ms", "probe_ms", "collect_ms", "score_ms")}},
+            "build": {"points_per_s": n / tbuild_max, "device_points_per_s": n / tbuild_dev_max,
+                      "wall_s": tbuild_max, "device_s": tbuild_dev_max,
+                      "kept_total": info["kept_total"],
+                      "prefilter_total": info["prefilter_total"]},
+            "e2e": {"value": e2e_qps, "unit": "queries/s",
+                    "h2d_bytes_per_step": nq * d * 4,
+                    "d2h_bytes_per_step": nq * K_TOP * (4 + 8)},
+            "gpu_launches": int(tim["launches"]),
+            "cpu_baseline": cpu,
+            "sweep": sweep,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -426,6 +426,40 @@ void orc_index_probes_rows(const orc_index* idx, const float* X, uint64_t n, uin
   free(buf);
 }
 
+orc_index* orc_index_from_csr(const float* X, uint64_t n, uint32_t d, const orc_params* prm,
+                              const uint32_t* offsets, const uint32_t* ids, const float* scores,
+                              const uint64_t* table_base) {
+  orc_index* idx = (orc_index*)calloc(1, sizeof(orc_index));
+  idx->p = *prm;
+  idx->n = n;
+  idx->d = d;
+  idx->P = orc_pad_dimension(d);
+  idx->NB = prm->K == 2 ? 4u * prm->D * prm->D : 2u * prm->D;
+  idx->X = X;
+  idx->t_begin = 0;
+  idx->t_end = prm->L;
+  const uint32_t K = prm->K, D = prm->D, P = idx->P, NB = idx->NB;
+  const uint64_t per = (uint64_t)blocks_of(P, D) * 3u * P;
+  idx->signs = (float*)malloc((size_t)prm->L * K * per * sizeof(float));
+  for (uint32_t t = 0; t < prm->L; ++t)
+    for (uint32_t f = 0; f < K; ++f)
+      orc_signs(orc_derive_seed(prm->seed, t, f, 0), P, blocks_of(P, D),
+                idx->signs + ((uint64_t)t * K + f) * per);
+  idx->offsets = (uint32_t**)calloc(prm->L, sizeof(void*));
+  idx->ids = (uint32_t**)calloc(prm->L, sizeof(void*));
+  idx->scores = (float**)calloc(prm->L, sizeof(void*));
+  for (uint32_t t = 0; t < prm->L; ++t) {
+    const uint64_t cnt = table_base[t + 1] - table_base[t];
+    idx->offsets[t] = (uint32_t*)malloc(((size_t)NB + 1) * sizeof(uint32_t));
+    memcpy(idx->offsets[t], offsets + (uint64_t)t * (NB + 1), ((size_t)NB + 1) * sizeof(uint32_t));
+    idx->ids[t] = (uint32_t*)malloc((cnt + 1) * sizeof(uint32_t));
+    idx->scores[t] = (float*)malloc((cnt + 1) * sizeof(float));
+    memcpy(idx->ids[t], ids + table_base[t], cnt * sizeof(uint32_t));
+    memcpy(idx->scores[t], scores + table_base[t], cnt * sizeof(float));
+  }
+  return idx;
+}
+
 void orc_free(orc_index* idx) {
   if (!idx) return;
   for (uint32_t t = 0; t < idx->t_end - idx->t_begin; ++t) {
@@ -720,5 +754,36 @@ void orc_brute_force(const float* X, uint64_t n, uint32_t d, const float* Q, uin
       }
     }
     free(top);
+  }
+}
+
+/* ------------------------------------------------------------- synthetic */
+/* u(s,k) = ((mix64(derive_seed(seed,s,k,0))>>11)+0.5)*2^-53,
+   N(0,1) by Box-Muller in double; centers stream 1, assignment stream 2+100*stream,
+   noise stream 3+100*stream. */
+static double synth_u(uint64_t seed, uint64_t stream, uint64_t k) {
+  return ((double)(orc_mix64(orc_derive_seed(seed, stream, k, 0)) >> 11) + 0.5) * 0x1.0p-53;
+}
+static double synth_normal(uint64_t seed, uint64_t stream, uint64_t k) {
+  const double u1 = synth_u(seed, stream, 2 * k), u2 = synth_u(seed, stream, 2 * k + 1);
+  return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+}
+void orc_synth(float* X, uint64_t n, uint32_t d, uint32_t clusters, float sigma, uint64_t seed,
+               uint32_t stream, int threads) {
+  const uint64_t s_noise = 3 + 100ull * stream, s_assign = 2 + 100ull * stream;
+  if (threads <= 0) threads = 1;
+#pragma omp parallel for schedule(static) num_threads(threads)
+  for (int64_t i = 0; i < (int64_t)n; ++i) {
+    float* row = X + (uint64_t)i * d;
+    if (clusters == 0) {
+      for (uint32_t j = 0; j < d; ++j) row[j] = (float)synth_normal(seed, s_noise, (uint64_t)i * d + j);
+    } else {
+      const uint64_t c = orc_mix64(orc_derive_seed(seed, s_assign, (uint64_t)i, 0)) % clusters;
+      for (uint32_t j = 0; j < d; ++j) {
+        const double ctr = synth_normal(seed, 1, c * d + j);
+        const double z = synth_normal(seed, s_noise, (uint64_t)i * d + j);
+        row[j] = (float)(ctr + (double)sigma * z);
+      }
+    }
   }
 }

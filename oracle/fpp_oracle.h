@@ -79,6 +79,11 @@ void orc_index_probes(const float* proj, uint32_t K, uint32_t D, uint32_t iprobe
 orc_index* orc_build(const float* X, uint64_t n, uint32_t d, const orc_params* prm,
                      int threads, uint32_t t_begin, uint32_t t_end);
 void orc_free(orc_index* idx);
+/* wrap an already-built CSR (e.g. the GPU's, verified bit-exact) for CPU query timing:
+   offsets [L][NB+1], ids/scores [table_base[L]], table_base [L+1] */
+orc_index* orc_index_from_csr(const float* X, uint64_t n, uint32_t d, const orc_params* prm,
+                              const uint32_t* offsets, const uint32_t* ids, const float* scores,
+                              const uint64_t* table_base);
 uint64_t orc_num_buckets(const orc_index* idx);
 /* CSR of one table (tables [t_begin,t_end) only) */
 uint64_t orc_table_size(const orc_index* idx, uint32_t t);
@@ -98,6 +103,10 @@ int orc_query_debug(const orc_index* idx, const float* q, uint32_t qprobes,
 /* query projections ranked lists [L][K][s] */
 void orc_query_lists(const orc_index* idx, const float* q, uint32_t s, float* vals,
                      uint32_t* codes);
+
+/* the pinned synthetic generator, restated for the CPU arm */
+void orc_synth(float* X, uint64_t n, uint32_t d, uint32_t clusters, float sigma, uint64_t seed,
+               uint32_t stream, int threads);
 
 /* brute force top-k */
 void orc_brute_force(const float* X, uint64_t n, uint32_t d, const float* Q, uint64_t nq,

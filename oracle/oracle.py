@@ -65,6 +65,11 @@ def lib():
         L.orc_cp_hash_rows.argtypes = [f32p, C.c_uint64, C.c_uint32, u32p]
         L.orc_index_probes_rows.argtypes = [C.c_void_p, f32p, C.c_uint64, C.c_uint32, u32p,
                                             f32p]
+        L.orc_index_from_csr.restype = C.c_void_p
+        L.orc_index_from_csr.argtypes = [f32p, C.c_uint64, C.c_uint32, C.POINTER(Params), u32p,
+                                         u32p, f32p, u64p]
+        L.orc_synth.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_float, C.c_uint64,
+                                C.c_uint32, C.c_int]
         L.orc_normalize.restype = C.c_int64
         L.orc_normalize.argtypes = [f32p, C.c_uint64, C.c_uint32]
         L.orc_inner_product.restype = C.c_double
@@ -153,6 +158,13 @@ def cp_hash_rows(Pm: np.ndarray) -> np.ndarray:
     return out
 
 
+def synth(n: int, d: int, clusters: int = 0, sigma: float = 0.0, seed: int = 1,
+          stream: int = 0, threads: int = 0) -> np.ndarray:
+    X = np.empty((n, d), np.float32)
+    lib().orc_synth(X.reshape(-1), n, d, clusters, sigma, seed, stream, threads or os.cpu_count())
+    return X
+
+
 def normalize(X: np.ndarray) -> np.ndarray:
     X = np.array(X, dtype=np.float32, order="C", copy=True)
     r = lib().orc_normalize(X.reshape(-1), X.shape[0], X.shape[1])
@@ -166,14 +178,19 @@ class Index:
 
     def __init__(self, X: np.ndarray, L: int, K: int, D: int, iprobes: int, alpha: float,
                  kappa: int = 20, seed: int = 1, threads: int = 0,
-                 t_begin: int = 0, t_end: int = 0):
+                 t_begin: int = 0, t_end: int = 0, csr=None):
         self.X = np.ascontiguousarray(X, dtype=np.float32)
         self.n, self.d = self.X.shape
         self.prm = Params(L, K, D, iprobes, kappa, alpha, seed)
         self.L, self.K, self.D = L, K, D
         self.t_begin, self.t_end = t_begin, (t_end or L)
-        self.h = lib().orc_build(self.X.reshape(-1), self.n, self.d, C.byref(self.prm),
-                                 threads, t_begin, t_end)
+        if csr is not None:  # (offsets [L][NB+1], ids, scores, table_base [L+1])
+            off, ids, sc, tb = (np.ascontiguousarray(a) for a in csr)
+            self.h = lib().orc_index_from_csr(self.X.reshape(-1), self.n, self.d,
+                                              C.byref(self.prm), off.reshape(-1), ids, sc, tb)
+        else:
+            self.h = lib().orc_build(self.X.reshape(-1), self.n, self.d, C.byref(self.prm),
+                                     threads, t_begin, t_end)
         if not self.h:
             raise ValueError("oracle build: invalid configuration")
         self.NB = lib().orc_num_buckets(self.h)

@@ -726,7 +726,7 @@ static void run_chunk(const Index& ix, const float* Qd, uint32_t nqc, uint32_t k
   k_score<<<nqc, SC_WARPS * 32, sc_smem, s>>>(sa);
   FPP_LAUNCH();
   ix.timer.end(PH_SCORE, e0, s);
-  ix.acc.launches += 6;
+  ix.acc.launches += 5;  // lists, probe_select, scan_eq, collect, score
   ix.acc.probes += peff * nqc;
 }
 

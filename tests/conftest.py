@@ -13,14 +13,6 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
-def gpu_available() -> bool:
-    try:
-        import paper_2206_01382_b200 as fpp
-        return fpp.device_count() > 0
-    except Exception:
-        return False
-
-
 @pytest.fixture(scope="session")
 def fpp():
     import paper_2206_01382_b200 as m

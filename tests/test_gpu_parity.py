@@ -10,7 +10,7 @@ All calls go through the C ABI (paper_2206_01382_b200 -> libfalconnpp_b200.so).
 import numpy as np
 import pytest
 
-from tests.conftest import gpu_available
+from fpp_testutil import gpu_available
 
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
@@ -160,8 +160,9 @@ def test_duplicates_tie_lower_id(fpp, orc):
     X = data(fpp, 1000, 64, seed=5)
     X[500:510] = X[3]  # exact duplicates: equal scores, lower id first
     Q = X[3:4].copy()
-    ix = fpp.Index.build(X, L=4, K=2, D=64, iProbes=3, alpha=1.0, kappa=0)
-    ox = orc.Index(X, L=4, K=2, D=64, iprobes=3, alpha=1.0, kappa=0)
+    # iProbes=1, alpha=1: keep = floor(B/1) = B, so every duplicate survives the filter
+    ix = fpp.Index.build(X, L=4, K=2, D=64, iProbes=1, alpha=1.0, kappa=0)
+    ox = orc.Index(X, L=4, K=2, D=64, iprobes=1, alpha=1.0, kappa=0)
     gi, gs = ix.query(Q, 20, 400)
     oi, os_, _ = ox.query(Q, 20, 400)
     assert np.array_equal(gi, oi)
