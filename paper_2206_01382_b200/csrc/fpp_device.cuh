@@ -170,6 +170,47 @@ __device__ __forceinline__ void topr_group_merge(uint64_t (&t)[R]) {
   }
 }
 
+// Bitonic sort (ascending) of the P = G*EPT keys held by a lane group, element
+// index i = g*EPT + e.  In-register compare-exchanges for strides < EPT,
+// shfl.xor for strides >= EPT.  Fully unrolled (P, EPT compile-time).
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  const uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)v, m);
+  const uint32_t hi = __shfl_xor_sync(FULL, (uint32_t)(v >> 32), m);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+template <int P, int EPT>
+__device__ __forceinline__ void group_bitonic_sort(uint64_t (&k)[EPT], int g) {
+#pragma unroll
+  for (int size = 2; size <= P; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= EPT) {
+        const int m = stride / EPT;
+        const bool lower = (g & m) == 0;
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          const uint64_t o = shfl_xor_u64(k[e], m);
+          const bool asc = (((g * EPT + e) & size) == 0);
+          const uint64_t mn = k[e] < o ? k[e] : o, mx = k[e] < o ? o : k[e];
+          k[e] = (lower == asc) ? mn : mx;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          if (e & stride) continue;
+          const int e2 = e | stride;
+          const bool asc = (((g * EPT + e) & size) == 0);
+          const uint64_t a = k[e], b = k[e2];
+          const uint64_t mn = a < b ? a : b, mx = a < b ? b : a;
+          k[e] = asc ? mn : mx;
+          k[e2] = asc ? mx : mn;
+        }
+      }
+    }
+  }
+}
+
 // exclusive block-wide scan (all threads must call); sh >= 32 words
 __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sh, uint32_t* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

@@ -31,85 +31,83 @@
 namespace fpp {
 
 // ---------------------------------------------------------------- K1 query
+// One lane group (G = P/EPT lanes) per (query, table, function): spinner
+// projections in registers, register bitonic sort of the (|p| desc, j asc) rank
+// keys, the first min(s,D) written out; when s > D a second sort of the
+// (|p| asc, j asc) keys supplies the opposite-signed tail.
 template <int P>
-__global__ void __launch_bounds__(256)
-k_query_lists(const float* __restrict__ Q, uint32_t d, uint32_t D, uint32_t K,
+__global__ void __launch_bounds__(128)
+k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, uint32_t K,
               const uint32_t* __restrict__ signs, uint32_t L, uint32_t s,
               float* __restrict__ vals, uint32_t* __restrict__ codes) {
   using S = FhtShape<P>;
-  __shared__ float pv[2][P];
-  __shared__ uint64_t keys[P];
-  const uint32_t q = blockIdx.x, t = blockIdx.y;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int grp = threadIdx.x / S::G;
+  constexpr int EPT = S::EPT;
+  const int lane = threadIdx.x & 31;
   const int g = lane % S::G;
-  if (warp * S::GPW < (int)K) {  // warps that host a function's FHT group
-    const int f = grp < (int)K ? grp : (int)K - 1;
-    float v[S::EPT];
-    load_row<P>(Q + (uint64_t)q * d, d, g, v);
-    spinner_project<P>(v, signs + ((uint64_t)t * K + f) * 3 * S::W, g);
-    if (grp < (int)K) {
+  const uint64_t gg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
+  const uint64_t total = nq * L * K;
+  const bool active = gg < total;
+  const uint64_t gid = active ? gg : total - 1;
+  const uint32_t f = (uint32_t)(gid % K);
+  const uint32_t t = (uint32_t)((gid / K) % L);
+  const uint64_t q = gid / ((uint64_t)K * L);
+  float v[EPT];
+  load_row<P>(Q + q * d, d, g, v);
+  spinner_project<P>(v, signs + ((uint64_t)t * K + f) * 3 * S::W, g);
+  uint64_t key[EPT];
 #pragma unroll
-      for (int e = 0; e < S::EPT; ++e) pv[f][g * S::EPT + e] = v[e];
+  for (int e = 0; e < EPT; ++e) {
+    const uint32_t j = (uint32_t)g * EPT + e;
+    key[e] = j < D ? rank_key(v[e], j) : ~0ull;
+  }
+  group_bitonic_sort<P, EPT>(key, g);
+  const uint64_t ob = gid * s;
+  const uint32_t nat = s < D ? s : D;
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t r = (uint32_t)g * EPT + e;
+      if (r < nat) {
+        vals[ob + r] = rank_val(key[e]);
+        codes[ob + r] = rank_code(key[e], D);
+      }
     }
   }
-  __syncthreads();
-  const uint32_t nat = s < D ? s : D;
-  for (uint32_t f = 0; f < K; ++f) {
-    const uint64_t ob = (((uint64_t)q * L + t) * K + f) * s;
-    for (uint32_t j = threadIdx.x; j < P; j += blockDim.x)
-      keys[j] = j < D ? rank_key(pv[f][j], j) : ~0ull;
-    __syncthreads();
-    for (uint32_t k = 2; k <= P; k <<= 1)
-      for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-        for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-          const uint32_t ixj = i ^ jj;
-          if (ixj > i) {
-            const uint64_t a = keys[i], b = keys[ixj];
-            if ((a > b) == ((i & k) == 0)) { keys[i] = b; keys[ixj] = a; }
-          }
-        }
-        __syncthreads();
-      }
-    for (uint32_t r = threadIdx.x; r < nat; r += blockDim.x) {
-      vals[ob + r] = rank_val(keys[r]);
-      codes[ob + r] = rank_code(keys[r], D);
+  if (s > D) {  // opposite signed vectors: (|p| asc, j asc), value -|p|
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t j = (uint32_t)g * EPT + e;
+      key[e] = j < D ? (((uint64_t)ord_key(fabsf(v[e])) << 32) | ((uint64_t)j << 1) |
+                        (v[e] < 0.0f ? 1u : 0u))
+                     : ~0ull;
     }
-    __syncthreads();
-    if (s > D) {  // opposite signed vectors: (|p| asc, j asc), value -|p|
-      for (uint32_t j = threadIdx.x; j < P; j += blockDim.x) {
-        if (j < D) {
-          const float p = pv[f][j];
-          keys[j] = ((uint64_t)ord_key(fabsf(p)) << 32) | ((uint64_t)j << 1) | (p < 0.0f ? 1u : 0u);
-        } else {
-          keys[j] = ~0ull;
+    group_bitonic_sort<P, EPT>(key, g);
+    if (active) {
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const uint32_t r = (uint32_t)g * EPT + e;
+        if (r < s - D) {
+          const uint64_t kk = key[e];
+          const uint32_t j = (uint32_t)(kk & 0xffffffffu) >> 1;
+          vals[ob + D + r] = -ord_inv((uint32_t)(kk >> 32));
+          codes[ob + D + r] = (kk & 1u) ? j : D + j;
         }
       }
-      __syncthreads();
-      for (uint32_t k = 2; k <= P; k <<= 1)
-        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-          for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-            const uint32_t ixj = i ^ jj;
-            if (ixj > i) {
-              const uint64_t a = keys[i], b = keys[ixj];
-              if ((a > b) == ((i & k) == 0)) { keys[i] = b; keys[ixj] = a; }
-            }
-          }
-          __syncthreads();
-        }
-      for (uint32_t r = threadIdx.x; r < s - D; r += blockDim.x) {
-        const uint64_t kk = keys[r];
-        const uint32_t j = (uint32_t)(kk & 0xffffffffu) >> 1;
-        vals[ob + D + r] = -ord_inv((uint32_t)(kk >> 32));
-        codes[ob + D + r] = (kk & 1u) ? j : D + j;
-      }
-      __syncthreads();
     }
   }
 }
 
 // ------------------------------------------------------------ probe select
-constexpr int PS_THREADS = 512;
+// CTA per query, one thread per table.  The probe set is {true bucket of each
+// table} U the M = P_eff - L best remaining (t, r1, r2) under
+// (fl(v1[r1]+v2[r2]) desc, r1, r2, t).  fp32 rounding is
+// monotone, so in every table the pairs scoring >= T form a staircase that a
+// two-pointer walk counts in O(active r1 + active r2).  T* (the M-th best
+// score) is found by a galloping + binary search on the ordered-key space, the
+// walks touching only the active prefixes of the ranked lists (L1-resident).
+// Ties at T* are resolved exactly in (r1, r2, t) order.
+constexpr int PS_THREADS = 128;
+constexpr int PS_TIE_CAP = 1024;
 
 struct ProbeArgs {
   const float* vals;      // [nq][L][K][s]
@@ -123,19 +121,7 @@ struct ProbeArgs {
   uint32_t* plen;         // [nq][peff]
   uint32_t* eq;           // [nq]
   uint64_t* dbg;          // optional [nq][peff] t*NB+b
-  int use_smem;
 };
-
-__device__ __forceinline__ uint32_t prefix_ge(float v1, const float* __restrict__ v2, uint32_t n2,
-                                              uint32_t T) {
-  uint32_t lo = 0, hi = n2;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (ord_key(v1 + v2[mid]) >= T) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
 
 __device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t* sh) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
@@ -148,123 +134,207 @@ __device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t* sh) {
   __syncthreads();
   return t;
 }
+__device__ __forceinline__ uint32_t block_max_u32(uint32_t v, uint32_t* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  uint32_t t = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = max(t, sh[i]);
+  __syncthreads();
+  return t;
+}
+
+__device__ const float g_zero_row[1] = {0.0f};
+
+struct TableLists {
+  const float* v1;  // [s]
+  const float* v2;  // [S2] (a zero row when K == 1)
+  uint32_t s1, S2;
+};
+
+// number of non-forced pairs with key >= T (two-pointer staircase walk)
+__device__ __forceinline__ uint32_t walk_count(const TableLists& tl, uint32_t T) {
+  uint32_t p = 0;
+  const float x0 = __ldg(tl.v1);
+  while (p < tl.S2 && ord_key(x0 + __ldg(tl.v2 + p)) >= T) ++p;
+  uint32_t c = p > 0 ? p - 1 : 0;  // exclude the forced (0,0)
+  for (uint32_t r1 = 1; r1 < tl.s1 && p > 0; ++r1) {
+    const float x = __ldg(tl.v1 + r1);
+    while (p > 0 && ord_key(x + __ldg(tl.v2 + p - 1)) < T) --p;
+    c += p;
+  }
+  return c;
+}
+
+// visit (r1, pa, pb): prefixes at Ta > Tb (pa <= pb), r1 ascending while pb > 0
+template <class F>
+__device__ __forceinline__ void walk2(const TableLists& tl, uint32_t Ta, uint32_t Tb, F&& visit) {
+  uint32_t pb = 0;
+  const float x0 = __ldg(tl.v1);
+  while (pb < tl.S2 && ord_key(x0 + __ldg(tl.v2 + pb)) >= Tb) ++pb;
+  uint32_t pa = 0;
+  while (pa < pb && ord_key(x0 + __ldg(tl.v2 + pa)) >= Ta) ++pa;
+  visit(0u, pa, pb);
+  for (uint32_t r1 = 1; r1 < tl.s1 && pb > 0; ++r1) {
+    const float x = __ldg(tl.v1 + r1);
+    while (pb > 0 && ord_key(x + __ldg(tl.v2 + pb - 1)) < Tb) --pb;
+    while (pa > 0 && ord_key(x + __ldg(tl.v2 + pa - 1)) < Ta) --pa;
+    if (pa > pb) pa = pb;
+    visit(r1, pa, pb);
+  }
+}
 
 __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
-  extern __shared__ float sv[];  // [L][K][s] values when they fit
   __shared__ uint64_t red[32];
-  __shared__ uint64_t scan_sh[32];
-  __shared__ float zero_row[1];
+  __shared__ uint32_t redu[32];
+  __shared__ uint64_t ties[PS_TIE_CAP];
+  __shared__ uint32_t n_ties;
   const uint32_t q = blockIdx.x;
   const uint32_t L = a.L, K = a.K, s = a.s;
   const uint32_t S2 = K == 2 ? s : 1;
   const uint64_t LKs = (uint64_t)L * K * s;
   const float* V = a.vals + (uint64_t)q * LKs;
-  const uint32_t* C = a.codes + (uint64_t)q * LKs;
-  if (a.use_smem) {
-    for (uint64_t i = threadIdx.x; i < LKs; i += blockDim.x) sv[i] = V[i];
-    V = sv;
-  }
-  if (threadIdx.x == 0) zero_row[0] = 0.0f;
+  const uint32_t* Cq = a.codes + (uint64_t)q * LKs;
+  if (threadIdx.x == 0) n_ties = 0;
   __syncthreads();
+  auto lists = [&](uint32_t t) {
+    TableLists tl;
+    tl.v1 = V + (uint64_t)t * K * s;
+    tl.v2 = K == 2 ? tl.v1 + s : g_zero_row;
+    tl.s1 = s;
+    tl.S2 = S2;
+    return tl;
+  };
   const uint64_t M = a.peff - L;  // non-forced probes
-  const uint32_t items = L * s;   // item = (t, r1), t-major
-  // contiguous item range per thread (for the emission scan)
-  const uint32_t per = (items + blockDim.x - 1) / blockDim.x;
-  const uint32_t it0 = min(items, threadIdx.x * per), it1 = min(items, it0 + per);
-#define V1(t, r) V[((uint64_t)(t) * K) * s + (r)]
-#define V2ROW(t) (K == 2 ? V + ((uint64_t)(t) * K + 1) * s : zero_row)
-  // raw prefix count for item, excluding the forced (0,0)
-  auto cnt_item = [&](uint32_t it, uint32_t T) -> uint32_t {
-    const uint32_t t = it / s, r1 = it - t * s;
-    uint32_t c = prefix_ge(V1(t, r1), V2ROW(t), S2, T);
-    if (r1 == 0 && c > 0) c -= 1;
-    return c;
+  auto count = [&](uint32_t T) -> uint64_t {
+    uint64_t c = 0;
+    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) c += walk_count(lists(t), T);
+    return block_sum_u64(c, red);
   };
   uint32_t Tstar = 0;
-  uint64_t cgt = 0;
   if (M > 0) {
-    // largest key T with c_ge(T) >= M  (M-th best non-forced pair score)
-    for (int bit = 31; bit >= 0; --bit) {
-      const uint32_t cand = Tstar | (1u << bit);
-      uint64_t c = 0;
-      for (uint32_t it = it0; it < it1; ++it) c += cnt_item(it, cand);
-      c = block_sum_u64(c, red);
-      if (c >= M) Tstar = cand;
+    // best non-forced key over all tables: max(v1[0]+v2[1], v1[1]+v2[0])
+    uint32_t hi = 0;
+    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
+      const TableLists tl = lists(t);
+      const float x0 = __ldg(tl.v1);
+      if (S2 > 1) hi = max(hi, ord_key(x0 + __ldg(tl.v2 + 1)));
+      if (s > 1) hi = max(hi, ord_key(__ldg(tl.v1 + 1) + __ldg(tl.v2)));
     }
-    if (Tstar != 0xffffffffu) {
-      uint64_t c = 0;
-      for (uint32_t it = it0; it < it1; ++it) c += cnt_item(it, Tstar + 1);
-      cgt = block_sum_u64(c, red);
+    hi = block_max_u32(hi, redu);
+    // gallop down from hi until count >= M, then bisect: Tstar = max T with count(T) >= M
+    uint32_t bad = 0xffffffffu;  // count(bad) < M (or sentinel)
+    uint32_t T = hi, step = 1;
+    bool have_bad = false;
+    for (;;) {
+      if (count(T) >= M) break;
+      bad = T;
+      have_bad = true;
+      T = T > step ? T - step : 0;
+      step <<= 1;
+      if (T == 0) break;  // count(0) counts every pair >= M
+    }
+    uint32_t lo = T;
+    if (have_bad) {
+      while (bad - lo > 1) {
+        const uint32_t mid = lo + (bad - lo) / 2;
+        if (count(mid) >= M) lo = mid;
+        else bad = mid;
+      }
+    } else {
+      // count(hi) >= M already: search upward is impossible (hi is the max key)
+    }
+    Tstar = lo;
+  }
+  const uint32_t Ta = Tstar == 0xffffffffu ? 0xffffffffu : Tstar + 1;  // strictly above T*
+  // per-thread gt / tie counts
+  uint64_t my_gt = 0, my_tie = 0;
+  if (M > 0) {
+    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
+      walk2(lists(t), Ta, Tstar, [&](uint32_t r1, uint32_t pa, uint32_t pb) {
+        const uint32_t st = r1 == 0 ? 1 : 0;
+        const uint32_t ga = max(st, pa), gb = max(st, pb);
+        my_gt += ga - st;
+        my_tie += gb - ga;
+      });
     }
   }
-  // ranges: gt = [st, ga), ties = [ga, gb) in r2, st = (r1==0)
-  auto ranges = [&](uint32_t it, uint32_t& st, uint32_t& ga, uint32_t& gb) {
-    const uint32_t t = it / s, r1 = it - t * s;
-    st = r1 == 0 ? 1 : 0;
-    const float v1 = V1(t, r1);
-    const float* v2 = V2ROW(t);
-    const uint32_t pa = (M == 0 || Tstar == 0xffffffffu) ? 0 : prefix_ge(v1, v2, S2, Tstar + 1);
-    const uint32_t pb = M == 0 ? 0 : prefix_ge(v1, v2, S2, Tstar);
-    ga = max(st, pa);
-    gb = max(st, pb);
-  };
-  const uint64_t m = M - cgt;  // ties to take at T*
-  uint64_t ties_total = 0;
-  if (M > 0) {
-    uint64_t c = 0;
-    for (uint32_t it = it0; it < it1; ++it) {
-      uint32_t st, ga, gb;
-      ranges(it, st, ga, gb);
-      c += gb - ga;
-    }
-    ties_total = block_sum_u64(c, red);
-  }
-  // partial ties: smallest composite key Kc with count_lt(Kc) >= m,
-  // composite = (r1*S2 + r2)*L + t  -> order (r1, r2, t)
+  const uint64_t cgt = block_sum_u64(my_gt, red);
+  const uint64_t ties_total = block_sum_u64(my_tie, red);
+  const uint64_t m = M > cgt ? M - cgt : 0;  // ties to take
+  // composite tie key (r1*S2 + r2)*L + t: order (r1, r2, t); take keys < Kstar
   uint64_t Kstar = ~0ull;
   if (M > 0 && ties_total > m) {
-    auto count_lt = [&](uint64_t Kc) -> uint64_t {
-      const uint64_t kr1 = Kc / ((uint64_t)S2 * L);
-      const uint64_t rem = Kc - kr1 * S2 * L;
-      const uint64_t kr2 = rem / L, kt = rem - kr2 * L;
-      uint64_t c = 0;
-      for (uint32_t it = it0; it < it1; ++it) {
-        const uint32_t t = it / s, r1 = it - t * s;
-        if (r1 > kr1) continue;
-        uint32_t st, ga, gb;
-        ranges(it, st, ga, gb);
-        if (ga == gb) continue;
-        if (r1 < kr1) { c += gb - ga; continue; }
-        if (kr2 > ga) c += (kr2 < gb ? kr2 : (uint64_t)gb) - ga;
-        if (kr2 >= ga && kr2 < gb && t < kt) c += 1;
+    if (ties_total <= PS_TIE_CAP) {
+      for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
+        walk2(lists(t), Ta, Tstar, [&](uint32_t r1, uint32_t pa, uint32_t pb) {
+          const uint32_t st = r1 == 0 ? 1 : 0;
+          for (uint32_t r2 = max(st, pa); r2 < max(st, pb); ++r2)
+            ties[atomicAdd(&n_ties, 1u)] = ((uint64_t)r1 * S2 + r2) * L + t;
+        });
       }
-      return block_sum_u64(c, red);
-    };
-    uint64_t lo = 0, hi = (uint64_t)s * S2 * L;  // count_lt(hi) = ties_total >= m
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (count_lt(mid) >= m) hi = mid;
-      else lo = mid + 1;
+      __syncthreads();
+      uint32_t N = 1;
+      while (N < ties_total) N <<= 1;
+      for (uint32_t i = ties_total + threadIdx.x; i < N; i += blockDim.x) ties[i] = ~0ull;
+      __syncthreads();
+      for (uint32_t kk = 2; kk <= N; kk <<= 1)
+        for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+            const uint32_t ixj = i ^ jj;
+            if (ixj > i) {
+              const uint64_t x = ties[i], y = ties[ixj];
+              if ((x > y) == ((i & kk) == 0)) { ties[i] = y; ties[ixj] = x; }
+            }
+          }
+          __syncthreads();
+        }
+      Kstar = ties[m];  // keys < ties[m] are the m smallest
+      __syncthreads();
+    } else {
+      // many ties: bisect the composite key with counting walks
+      auto count_lt = [&](uint64_t Kc) -> uint64_t {
+        const uint64_t kr1 = Kc / ((uint64_t)S2 * L);
+        const uint64_t rem = Kc - kr1 * S2 * L;
+        const uint64_t kr2 = rem / L, kt = rem - kr2 * L;
+        uint64_t c = 0;
+        for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
+          walk2(lists(t), Ta, Tstar, [&](uint32_t r1, uint32_t pa, uint32_t pb) {
+            const uint32_t st = r1 == 0 ? 1 : 0;
+            const uint64_t ga = max(st, pa), gb = max(st, pb);
+            if (ga == gb || r1 > kr1) return;
+            if (r1 < kr1) { c += gb - ga; return; }
+            if (kr2 > ga) c += (kr2 < gb ? kr2 : gb) - ga;
+            if (kr2 >= ga && kr2 < gb && t < kt) c += 1;
+          });
+        }
+        return block_sum_u64(c, red);
+      };
+      uint64_t lo = 0, hi = (uint64_t)s * S2 * L;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (count_lt(mid) >= m) hi = mid;
+        else lo = mid + 1;
+      }
+      Kstar = lo;
     }
-    Kstar = lo;
   }
-  auto take_tie = [&](uint32_t t, uint32_t r1, uint32_t r2) -> bool {
-    if (Kstar == ~0ull) return true;
-    return (((uint64_t)r1 * S2 + r2) * L + t) < Kstar;
-  };
-  // emission counts per thread
+  // emission counts, exclusive scan over threads
   uint64_t mine = 0;
-  for (uint32_t it = it0; it < it1; ++it) {
-    if (M == 0) break;
-    uint32_t st, ga, gb;
-    ranges(it, st, ga, gb);
-    const uint32_t t = it / s, r1 = it - t * s;
-    mine += ga - st;
-    if (Kstar == ~0ull) mine += gb - ga;
-    else
-      for (uint32_t r2 = ga; r2 < gb; ++r2) mine += take_tie(t, r1, r2);
+  if (M > 0) {
+    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
+      walk2(lists(t), Ta, Tstar, [&](uint32_t r1, uint32_t pa, uint32_t pb) {
+        const uint32_t st = r1 == 0 ? 1 : 0;
+        const uint32_t ga = max(st, pa), gb = max(st, pb);
+        mine += ga - st;
+        if (Kstar == ~0ull) mine += gb - ga;
+        else
+          for (uint32_t r2 = ga; r2 < gb; ++r2) mine += (((uint64_t)r1 * S2 + r2) * L + t) < Kstar;
+      });
+    }
   }
-  // exclusive block scan of `mine`
   uint64_t x = mine;
   {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -272,10 +342,10 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       const uint64_t y = __shfl_up_sync(FULL, x, o);
       if (lane >= o) x += y;
     }
-    if (lane == 31) scan_sh[w] = x;
+    if (lane == 31) red[w] = x;
     __syncthreads();
     uint64_t wb = 0;
-    for (int i = 0; i < w; ++i) wb += scan_sh[i];
+    for (int i = 0; i < w; ++i) wb += red[i];
     x = wb + x - mine;
     __syncthreads();
   }
@@ -286,32 +356,35 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
   uint64_t esum = 0;
   auto emit = [&](uint64_t slot, uint32_t t, uint32_t b) {
     const uint32_t* of = a.offs + (uint64_t)t * (a.NB + 1);
-    const uint32_t o0 = of[b], o1 = of[b + 1];
-    ppos[slot] = a.tbase[t] + o0;
+    const uint32_t o0 = __ldg(of + b), o1 = __ldg(of + b + 1);
+    ppos[slot] = __ldg(a.tbase + t) + o0;
     plen[slot] = o1 - o0;
     esum += o1 - o0;
     if (dbg) dbg[slot] = (uint64_t)t * a.NB + b;
   };
-  const uint32_t* Cq = C;
-  auto bucket_of = [&](uint32_t t, uint32_t r1, uint32_t r2) -> uint32_t {
-    const uint32_t c1 = Cq[((uint64_t)t * K) * s + r1];
-    return K == 2 ? c1 * twoD + Cq[((uint64_t)t * K + 1) * s + r2] : c1;
-  };
-  for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) emit(t, t, bucket_of(t, 0, 0));
-  uint64_t slot = L + x;
-  for (uint32_t it = it0; it < it1; ++it) {
-    if (M == 0) break;
-    uint32_t st, ga, gb;
-    ranges(it, st, ga, gb);
-    const uint32_t t = it / s, r1 = it - t * s;
-    for (uint32_t r2 = st; r2 < ga; ++r2) emit(slot++, t, bucket_of(t, r1, r2));
-    for (uint32_t r2 = ga; r2 < gb; ++r2)
-      if (take_tie(t, r1, r2)) emit(slot++, t, bucket_of(t, r1, r2));
+  for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
+    const uint32_t* c1 = Cq + (uint64_t)t * K * s;
+    const uint32_t* c2 = c1 + s;
+    emit(t, t, K == 2 ? __ldg(c1) * twoD + __ldg(c2) : __ldg(c1));
+  }
+  if (M > 0) {
+    uint64_t slot = L + x;
+    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
+      const uint32_t* c1 = Cq + (uint64_t)t * K * s;
+      const uint32_t* c2 = c1 + s;
+      walk2(lists(t), Ta, Tstar, [&](uint32_t r1, uint32_t pa, uint32_t pb) {
+        const uint32_t st = r1 == 0 ? 1 : 0;
+        const uint32_t ga = max(st, pa), gb = max(st, pb);
+        const uint32_t h1 = __ldg(c1 + r1);
+        for (uint32_t r2 = st; r2 < gb; ++r2) {
+          if (r2 >= ga && Kstar != ~0ull && (((uint64_t)r1 * S2 + r2) * L + t) >= Kstar) continue;
+          emit(slot++, t, K == 2 ? h1 * twoD + __ldg(c2 + r2) : h1);
+        }
+      });
+    }
   }
   esum = block_sum_u64(esum, red);
   if (threadIdx.x == 0) a.eq[q] = (uint32_t)esum;
-#undef V1
-#undef V2ROW
 }
 
 // exclusive scan of eq[nq] -> coff[nq+1] (single CTA)
@@ -497,6 +570,12 @@ __device__ __forceinline__ void topk_insert(double& bs, uint32_t& bi, uint32_t k
   }
 }
 
+// Per warp: 32-candidate batches; every batch streams its rows as 32-float
+// column slices through a SC_STAGES-deep cp.async ring.  Lane l copies the 16 B
+// chunk (l & 7) of rows (l >> 3) + 4*it, it = 0..7, with row addresses resolved
+// once per batch, so a slice costs 8 cp.async per lane.  Lane r then folds row
+// r's slice into its fp64 accumulator in the reference's sequential order.
+template <bool VEC>
 __global__ void __launch_bounds__(SC_WARPS * 32, 2) k_score(ScoreArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const uint32_t d = a.d;
@@ -516,60 +595,69 @@ __global__ void __launch_bounds__(SC_WARPS * 32, 2) k_score(ScoreArgs a) {
   uint32_t bi = 0xffffffffu;
   float* wring = ring + (size_t)w * SC_STAGES * SC_STAGE_FLOATS;
   const uint32_t nb = (U + 31) / 32;
-  const uint32_t my_nb = nb > (uint32_t)w ? (nb - w + SC_WARPS - 1) / SC_WARPS : 0;
   const uint32_t nsl = (d + SC_SLICE - 1) / SC_SLICE;
-  const uint64_t S = (uint64_t)my_nb * nsl;
-  const bool vec = (d & 3u) == 0;
-  uint32_t iss_id = 0;
-  uint32_t iss_b = 0xffffffffu;
-  auto issue = [&](uint64_t step) {
-    if (step < S) {
-      const uint32_t bl = (uint32_t)(step / nsl), c = (uint32_t)(step - (uint64_t)bl * nsl);
-      const uint32_t bidx = w + bl * SC_WARPS;
-      if (bidx != iss_b) {
-        iss_b = bidx;
-        const uint32_t ci = bidx * 32 + lane;
-        iss_id = ci < U ? __ldg(cand + ci) : 0xffffffffu;
+  const float* X = a.X;
+  // issue cursor
+  uint32_t ib = w, ic = 0, nissued = 0;
+  const float* rp[8];
+  uint32_t my_id = 0xffffffffu;
+  const int kk = lane & 7, rbase = lane >> 3;
+  auto load_batch = [&](uint32_t bidx) {
+    const uint32_t ci = bidx * 32 + lane;
+    my_id = ci < U ? __ldg(cand + ci) : 0xffffffffu;
+    if (VEC) {
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const uint32_t idr = __shfl_sync(FULL, my_id, rbase + 4 * it);
+        rp[it] = idr != 0xffffffffu ? X + (uint64_t)idr * d : nullptr;
       }
-      float* buf = wring + (size_t)(step % SC_STAGES) * SC_STAGE_FLOATS;
-      const uint32_t col0 = c * SC_SLICE;
+    }
+  };
+  auto issue = [&]() {
+    if (ib < nb) {
+      float* buf = wring + (size_t)(nissued % SC_STAGES) * SC_STAGE_FLOATS;
+      const uint32_t col0 = ic * SC_SLICE;
       const uint32_t len = min((uint32_t)SC_SLICE, d - col0);
-      if (vec) {
-        const uint32_t npc = len >> 2;  // 16 B pieces per row
-        for (uint32_t it = 0; it < npc; ++it) {
-          const uint32_t p = lane + 32 * it;
-          const uint32_t r = p / npc, kk = p - r * npc;
-          const uint32_t id = __shfl_sync(FULL, iss_id, r);
-          if (id != 0xffffffffu)
-            cp_async16(buf + r * SC_ROWPAD + kk * 4, a.X + (uint64_t)id * d + col0 + kk * 4);
+      if (VEC) {
+        if ((uint32_t)kk < (len >> 2)) {
+#pragma unroll
+          for (int it = 0; it < 8; ++it)
+            if (rp[it]) cp_async16(buf + (rbase + 4 * it) * SC_ROWPAD + kk * 4, rp[it] + col0 + kk * 4);
         }
       } else {
-        for (uint32_t it = 0; it < len; ++it) {
-          const uint32_t p = lane + 32 * it;
-          const uint32_t r = p / len, kk = p - r * len;
-          const uint32_t id = __shfl_sync(FULL, iss_id, r);
-          if (id != 0xffffffffu) cp_async4(buf + r * SC_ROWPAD + kk, a.X + (uint64_t)id * d + col0 + kk);
+        for (int r = 0; r < 32; ++r) {
+          const uint32_t idr = __shfl_sync(FULL, my_id, r);
+          if (idr != 0xffffffffu && (uint32_t)lane < len)
+            cp_async4(buf + r * SC_ROWPAD + lane, X + (uint64_t)idr * d + col0 + lane);
         }
+      }
+      if (++ic == nsl) {
+        ic = 0;
+        ib += SC_WARPS;
+        if (ib < nb) load_batch(ib);
       }
     }
     cp_commit();
+    ++nissued;
   };
+  if ((uint32_t)w < nb) load_batch(w);
 #pragma unroll
-  for (int st = 0; st < SC_STAGES - 1; ++st) issue(st);
+  for (int st = 0; st < SC_STAGES - 1; ++st) issue();
   double acc = 0.0;
-  for (uint64_t step = 0; step < S; ++step) {
-    issue(step + SC_STAGES - 1);
+  uint32_t cb = w, cc = 0, ncomp = 0;
+  while (cb < nb) {
+    issue();
     cp_wait<SC_STAGES - 1>();
     __syncwarp();
-    const uint32_t bl = (uint32_t)(step / nsl), c = (uint32_t)(step - (uint64_t)bl * nsl);
-    const float* row = wring + (size_t)(step % SC_STAGES) * SC_STAGE_FLOATS + lane * SC_ROWPAD;
-    const uint32_t col0 = c * SC_SLICE;
+    const float* row = wring + (size_t)(ncomp % SC_STAGES) * SC_STAGE_FLOATS + lane * SC_ROWPAD;
+    const uint32_t col0 = cc * SC_SLICE;
     const uint32_t len = min((uint32_t)SC_SLICE, d - col0);
     const double* qq = qd + col0;
-    if (vec) {
-      for (uint32_t j = 0; j < len; j += 4) {
+    // dataset.cpp:67 acc += double(a[i]) * double(b[i]), sequential i (exact products)
+    if (VEC && len == SC_SLICE) {
+#pragma unroll
+      for (int j = 0; j < SC_SLICE; j += 4) {
         const float4 xv = *reinterpret_cast<const float4*>(row + j);
-        // dataset.cpp:67 acc += double(a[i]) * double(b[i]), sequential i
         acc = fma((double)xv.x, qq[j], acc);
         acc = fma((double)xv.y, qq[j + 1], acc);
         acc = fma((double)xv.z, qq[j + 2], acc);
@@ -579,12 +667,15 @@ __global__ void __launch_bounds__(SC_WARPS * 32, 2) k_score(ScoreArgs a) {
       for (uint32_t j = 0; j < len; ++j) acc = fma((double)row[j], qq[j], acc);
     }
     __syncwarp();
-    if (c == nsl - 1) {
-      const uint32_t ci = (w + bl * SC_WARPS) * 32 + lane;
+    ++ncomp;
+    if (++cc == nsl) {
+      const uint32_t ci = cb * 32 + lane;
       const bool valid = ci < U;
       const uint32_t id = valid ? __ldg(cand + ci) : 0xffffffffu;
       topk_insert(bs, bi, k, acc, id, valid);
       acc = 0.0;
+      cc = 0;
+      cb += SC_WARPS;
     }
   }
   cp_wait<0>();
@@ -618,11 +709,12 @@ static size_t score_smem(uint32_t d) {
 void launch_query_lists(const Index& ix, const float* Qd, uint64_t nq, uint32_t s_cap,
                         float* vals, uint32_t* codes, cudaStream_t s) {
   if (nq == 0) return;
-  dim3 grid((unsigned)nq, ix.prm.L);
   const uint32_t d = ix.d, D = ix.prm.D, K = ix.prm.K, L = ix.prm.L;
+  const uint32_t G = ix.P < 32 ? 1 : ix.P / 32;
+  const unsigned grid = (unsigned)((nq * L * K * G + 127) / 128);
 #define FPP_QL_CASE(PP)                                                                      \
   case PP:                                                                                   \
-    k_query_lists<PP><<<grid, 256, 0, s>>>(Qd, d, D, K, ix.signs, L, s_cap, vals, codes);    \
+    k_query_lists<PP><<<grid, 128, 0, s>>>(Qd, nq, d, D, K, ix.signs, L, s_cap, vals, codes); \
     break;
   switch (ix.P) {
     FPP_QL_CASE(2) FPP_QL_CASE(4) FPP_QL_CASE(8) FPP_QL_CASE(16) FPP_QL_CASE(32)
@@ -668,17 +760,8 @@ static void run_chunk(const Index& ix, const float* Qd, uint32_t nqc, uint32_t k
 
   ix.timer.begin(PH_PROBE, s, &e0);
   ProbeArgs pa{ix.q_vals.p, ix.q_codes.p, L, K, scap, ix.prm.D, ix.NB, peff, ix.offsets,
-               ix.table_base, ix.q_ppos.p, ix.q_plen.p, ix.q_eq.p, dbg_probes, 0};
-  size_t ps_smem = LKs * sizeof(float);
-  const int smax = co_smem_max() - 4096;
-  if ((int)ps_smem <= smax) {
-    pa.use_smem = 1;
-    FPP_CUDA(cudaFuncSetAttribute(k_probe_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)ps_smem));
-  } else {
-    ps_smem = 0;
-  }
-  k_probe_select<<<nqc, PS_THREADS, ps_smem, s>>>(pa);
+               ix.table_base, ix.q_ppos.p, ix.q_plen.p, ix.q_eq.p, dbg_probes};
+  k_probe_select<<<nqc, PS_THREADS, 0, s>>>(pa);
   FPP_LAUNCH();
   k_scan_eq<<<1, 1024, 0, s>>>(ix.q_eq.p, nqc, ix.q_coff.p);
   FPP_LAUNCH();
@@ -722,8 +805,15 @@ static void run_chunk(const Index& ix, const float* Qd, uint32_t nqc, uint32_t k
   ScoreArgs sa{ix.X, ix.d, Qd, ix.q_coff.p, ix.q_cands.p, ix.q_uq.p, ix.q_eq.p, peff, k,
                ix.prm.id_offset, ids_d, scores_d, stats_d};
   const size_t sc_smem = score_smem(ix.d);
-  FPP_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem));
-  k_score<<<nqc, SC_WARPS * 32, sc_smem, s>>>(sa);
+  if ((ix.d & 3u) == 0) {
+    FPP_CUDA(cudaFuncSetAttribute(k_score<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sc_smem));
+    k_score<true><<<nqc, SC_WARPS * 32, sc_smem, s>>>(sa);
+  } else {
+    FPP_CUDA(cudaFuncSetAttribute(k_score<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sc_smem));
+    k_score<false><<<nqc, SC_WARPS * 32, sc_smem, s>>>(sa);
+  }
   FPP_LAUNCH();
   ix.timer.end(PH_SCORE, e0, s);
   ix.acc.launches += 5;  // lists, probe_select, scan_eq, collect, score
