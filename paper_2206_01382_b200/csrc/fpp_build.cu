@@ -44,21 +44,38 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
   for (uint32_t tt = 0; tt < T; ++tt) {
     const uint32_t t = t0 + tt;
     uint64_t top0[R], top1[R];
-#pragma unroll
-    for (int f = 0; f < 2; ++f) {
-      if (f >= (int)K) break;
+#pragma unroll 1
+    for (int f = 0; f < (int)K; ++f) {
       float v[S::EPT];
 #pragma unroll
       for (int e = 0; e < S::EPT; ++e) v[e] = x[e];
       spinner_project<P>(v, signs + ((uint64_t)t * K + f) * 3 * S::W, g);
-      uint64_t tk[R];
+      // lane-local top-R by (|p| desc, j asc): strict '>' keeps the lower j on ties
+      float tp[R];
+      uint32_t tj[R];
 #pragma unroll
-      for (int q = 0; q < R; ++q) tk[q] = ~0ull;
+      for (int q = 0; q < R; ++q) { tp[q] = 0.0f; tj[q] = 0xffffffffu; }
+      float thr = -1.0f;
 #pragma unroll
       for (int e = 0; e < S::EPT; ++e) {
         const uint32_t j = (uint32_t)g * S::EPT + e;
-        if (j < D) topr_insert<R>(tk, rank_key(v[e], j));
+        const float a = fabsf(v[e]);
+        if (j < D && a > thr) {
+          float cp = v[e];
+          uint32_t cj = j;
+#pragma unroll
+          for (int q = 0; q < R; ++q) {  // insert, shifting the tail down
+            const bool ins = tj[q] == 0xffffffffu || fabsf(cp) > fabsf(tp[q]);
+            const float op = tp[q];
+            const uint32_t oj = tj[q];
+            if (ins) { tp[q] = cp; tj[q] = cj; cp = op; cj = oj; }
+          }
+          thr = tj[R - 1] == 0xffffffffu ? -1.0f : fabsf(tp[R - 1]);
+        }
       }
+      uint64_t tk[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) tk[q] = tj[q] == 0xffffffffu ? ~0ull : rank_key(tp[q], tj[q]);
       topr_group_merge<R, S::G>(tk);
 #pragma unroll
       for (int q = 0; q < R; ++q) {

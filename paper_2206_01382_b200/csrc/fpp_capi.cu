@@ -90,7 +90,7 @@ Index::~Index() {
   dfree(table_base);
   dfree(ids);
   dfree(scores);
-  q_vals.release(); q_codes.release(); q_ppos.release(); q_plen.release(); q_eq.release();
+  q_vals.release(); q_codes.release(); q_ppos.release(); q_plen.release(); q_gbuf.release(); q_ckey.release(); q_cpair.release(); q_eq.release();
   q_coff.release(); q_uq.release(); q_cands.release(); q_bitmap.release(); q_in.release();
   q_ids.release(); q_scores.release(); q_stats.release(); q_counter.release();
   if (h_pinned) cudaFreeHost(h_pinned);
@@ -197,6 +197,9 @@ static void validate_params(const fpp_params& p, uint64_t n, uint32_t d) {
   const uint64_t NB = p.K == 2 ? 4ull * p.D * p.D : 2ull * p.D;
   if (p.iprobes > NB) fail(FPP_ERR_OUT_OF_RANGE, "index_probe_sequence: iProbes > number of buckets");
   if (p.D > P) fail(FPP_ERR_UNSUPPORTED, "GPU path: D > d_pad (multi-block stacks) not supported");
+  if (p.L > 1024) fail(FPP_ERR_UNSUPPORTED, "GPU path: L must be <= 1024");
+  if ((uint64_t)p.L * NB >= (1ull << 32))
+    fail(FPP_ERR_UNSUPPORTED, "GPU path: L*NB must be < 2^32 (32-bit global bucket ids)");
   if (P > 1024) fail(FPP_ERR_UNSUPPORTED, "GPU path: d_pad > 1024 not supported");
   if (p.iprobes > std::min<uint32_t>(p.D, 16))
     fail(FPP_ERR_UNSUPPORTED, "GPU path: iProbes must be <= min(D,16)");

@@ -90,6 +90,10 @@ struct Index {
   mutable DBuf<uint32_t> q_codes;
   mutable DBuf<uint64_t> q_ppos;
   mutable DBuf<uint32_t> q_plen;
+  mutable DBuf<uint32_t> q_gbuf;
+  mutable DBuf<uint32_t> q_ckey;
+  mutable DBuf<uint32_t> q_cpair;
+  mutable DBuf<uint64_t> q_dbgclk;
   mutable DBuf<uint32_t> q_eq;
   mutable DBuf<uint64_t> q_coff;
   mutable DBuf<uint32_t> q_uq;
@@ -127,7 +131,7 @@ void launch_index_probes(const Index& ix, const float* Xd, uint64_t n, uint32_t 
 void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t qprobes,
                uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s);
 void launch_query_lists(const Index& ix, const float* Qd, uint64_t nq, uint32_t s_cap,
-                        float* vals, uint32_t* codes, cudaStream_t s);
+                        float* vals, uint32_t* codes, cudaStream_t s, uint64_t lstride = 0);
 // probes (t*NB+b) and candidates of query 0 of Qd (debug/parity)
 void query_debug(const Index& ix, const float* qd, uint32_t qprobes,
                  std::vector<uint64_t>& probes, std::vector<uint32_t>& cands);

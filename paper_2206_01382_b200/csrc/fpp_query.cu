@@ -24,6 +24,7 @@
 //                   register top-k, CTA merge
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "fpp_device.cuh"
 #include "fpp_internal.h"
@@ -32,18 +33,66 @@ namespace fpp {
 
 // ---------------------------------------------------------------- K1 query
 // One lane group (G = P/EPT lanes) per (query, table, function): spinner
-// projections in registers, register bitonic sort of the (|p| desc, j asc) rank
-// keys, the first min(s,D) written out; when s > D a second sort of the
-// (|p| asc, j asc) keys supplies the opposite-signed tail.
+// projections in registers, then the ranked list.  Sorting uses 32-bit keys
+// (22-bit truncated rank value | 10-bit index) -- half the shuffles and a third
+// of the ALU work of 64-bit keys -- followed by an exact fix-up of the rare runs
+// whose truncated values collide, so the emitted order is exactly
+// (|p| desc, j asc) (then, when s > D, the opposite tail (|p| asc, j asc)).
+template <bool NAT>
+__device__ __forceinline__ bool rank_before(float pa, uint32_t ja, float pb, uint32_t jb) {
+  const float a = fabsf(pa), b = fabsf(pb);
+  if (a != b) return NAT ? a > b : a < b;
+  return ja < jb;
+}
+
+// sort the group's keys, store to sk, fix equal-prefix runs exactly (one lane per run)
+template <int P, int EPT, bool NAT>
+__device__ __forceinline__ void rank_sort_exact(uint32_t (&kk)[EPT], int g, uint32_t* sk,
+                                                const float* pv) {
+  group_bitonic_sort_u32<P, EPT>(kk, g);
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) sk[g * EPT + e] = kk[e];
+  __syncwarp();
+#pragma unroll 1
+  for (int e = 0; e < EPT; ++e) {
+    const int i = g * EPT + e;
+    const uint32_t x = sk[i];
+    if (x == 0xffffffffu || i + 1 >= P) continue;
+    const uint32_t pf = x >> 10;
+    if ((sk[i + 1] >> 10) != pf || sk[i + 1] == 0xffffffffu) continue;
+    if (i > 0 && (sk[i - 1] >> 10) == pf) continue;  // not the run start
+    int end = i + 1;
+    while (end < P && sk[end] != 0xffffffffu && (sk[end] >> 10) == pf) ++end;
+    for (int u = i + 1; u < end; ++u) {  // insertion sort by the exact order
+      const uint32_t y = sk[u];
+      const uint32_t jy = y & 1023u;
+      const float py = pv[jy];
+      int w = u - 1;
+      while (w >= i && rank_before<NAT>(py, jy, pv[sk[w] & 1023u], sk[w] & 1023u)) {
+        sk[w + 1] = sk[w];
+        --w;
+      }
+      sk[w + 1] = y;
+    }
+  }
+  __syncwarp();
+}
+
 template <int P>
 __global__ void __launch_bounds__(128)
 k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, uint32_t K,
-              const uint32_t* __restrict__ signs, uint32_t L, uint32_t s,
+              const uint32_t* __restrict__ signs, uint32_t L, uint32_t s, uint64_t lstride,
               float* __restrict__ vals, uint32_t* __restrict__ codes) {
   using S = FhtShape<P>;
   constexpr int EPT = S::EPT;
+  constexpr int GPB = 128 / S::G;
+  __shared__ float pv_all[GPB][P];
+  __shared__ uint32_t sk_all[GPB][P];
   const int lane = threadIdx.x & 31;
   const int g = lane % S::G;
+  const int gl = threadIdx.x / S::G;
+  float* pv = pv_all[gl];
+  uint32_t* sk = sk_all[gl];
   const uint64_t gg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
   const uint64_t total = nq * L * K;
   const bool active = gg < total;
@@ -54,64 +103,59 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
   float v[EPT];
   load_row<P>(Q + q * d, d, g, v);
   spinner_project<P>(v, signs + ((uint64_t)t * K + f) * 3 * S::W, g);
-  uint64_t key[EPT];
+  uint32_t kk[EPT];
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     const uint32_t j = (uint32_t)g * EPT + e;
-    key[e] = j < D ? rank_key(v[e], j) : ~0ull;
+    pv[j] = v[e];
+    kk[e] = j < D ? (((~ord_key(fabsf(v[e]))) & 0xfffffc00u) | j) : 0xffffffffu;
   }
-  group_bitonic_sort<P, EPT>(key, g);
-  const uint64_t ob = gid * s;
+  rank_sort_exact<P, EPT, true>(kk, g, sk, pv);
+  const uint64_t ob = q * lstride + (uint64_t)(t * K + f) * s;
   const uint32_t nat = s < D ? s : D;
   if (active) {
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const uint32_t r = (uint32_t)g * EPT + e;
-      if (r < nat) {
-        vals[ob + r] = rank_val(key[e]);
-        codes[ob + r] = rank_code(key[e], D);
-      }
+    for (uint32_t r = g; r < nat; r += S::G) {
+      const uint32_t j = sk[r] & 1023u;
+      const float p = pv[j];
+      vals[ob + r] = fabsf(p);
+      codes[ob + r] = p < 0.0f ? D + j : j;
     }
   }
   if (s > D) {  // opposite signed vectors: (|p| asc, j asc), value -|p|
+    __syncwarp();
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       const uint32_t j = (uint32_t)g * EPT + e;
-      key[e] = j < D ? (((uint64_t)ord_key(fabsf(v[e])) << 32) | ((uint64_t)j << 1) |
-                        (v[e] < 0.0f ? 1u : 0u))
-                     : ~0ull;
+      kk[e] = j < D ? ((ord_key(fabsf(v[e])) & 0xfffffc00u) | j) : 0xffffffffu;
     }
-    group_bitonic_sort<P, EPT>(key, g);
+    rank_sort_exact<P, EPT, false>(kk, g, sk, pv);
     if (active) {
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        const uint32_t r = (uint32_t)g * EPT + e;
-        if (r < s - D) {
-          const uint64_t kk = key[e];
-          const uint32_t j = (uint32_t)(kk & 0xffffffffu) >> 1;
-          vals[ob + D + r] = -ord_inv((uint32_t)(kk >> 32));
-          codes[ob + D + r] = (kk & 1u) ? j : D + j;
-        }
+      for (uint32_t r = g; r < s - D; r += S::G) {
+        const uint32_t j = sk[r] & 1023u;
+        const float p = pv[j];
+        vals[ob + D + r] = -fabsf(p);
+        codes[ob + D + r] = p < 0.0f ? j : D + j;
       }
     }
   }
 }
 
 // ------------------------------------------------------------ probe select
-// CTA per query, one thread per table.  The probe set is {true bucket of each
-// table} U the M = P_eff - L best remaining (t, r1, r2) under
+// One warp per query, lanes over tables.  The probe set is {true bucket of
+// each table} U the M = P_eff - L best remaining (t, r1, r2) under
 // (fl(v1[r1]+v2[r2]) desc, r1, r2, t).  fp32 rounding is
-// monotone, so in every table the pairs scoring >= T form a staircase that a
-// two-pointer walk counts in O(active r1 + active r2).  T* (the M-th best
-// score) is found by a galloping + binary search on the ordered-key space, the
-// walks touching only the active prefixes of the ranked lists (L1-resident).
-// Ties at T* are resolved exactly in (r1, r2, t) order.
-constexpr int PS_THREADS = 128;
-constexpr int PS_TIE_CAP = 1024;
+// monotone, so the pairs of a table scoring >= T form a staircase; a walk over
+// r1 with a binary-searched r2 boundary counts it.  T* (the M-th best score)
+// is bracketed in ordered-key space and found by a safeguarded interpolation
+// search on the count (exact: the loop keeps count(lo) >= M > count(hi) and
+// stops at hi = lo + 1).  Ties at T* are resolved exactly in (r1, r2, t) order.
+constexpr int PS_THREADS = 256;
+constexpr int PS_TIE_CAP = 512;
 
 struct ProbeArgs {
   const float* vals;      // [nq][L][K][s]
   const uint32_t* codes;  // [nq][L][K][s]
+  uint32_t nq;
   uint32_t L, K, s, D;
   uint64_t NB;
   uint64_t peff;          // probes per query (incl. the L forced)
@@ -121,30 +165,13 @@ struct ProbeArgs {
   uint32_t* plen;         // [nq][peff]
   uint32_t* eq;           // [nq]
   uint64_t* dbg;          // optional [nq][peff] t*NB+b
+  uint32_t* gbuf;         // [nq][peff] bucket-id scratch when not in shared memory
+  uint64_t lstride;       // per-query list stride (L*K*s rounded up to 4 floats)
+  long long* dbg_clk;     // optional [nq][8]: phase clocks + search iterations
+  uint32_t* ckey;         // [nq][ccap] candidate pair keys (scratch)
+  uint32_t* cpair;        // [nq][ccap] candidate pairs (t<<22 | r1<<11 | r2)
+  uint32_t ccap;
 };
-
-__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t* sh) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) sh[w] = v;
-  __syncthreads();
-  uint64_t t = 0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh[i];
-  __syncthreads();
-  return t;
-}
-__device__ __forceinline__ uint32_t block_max_u32(uint32_t v, uint32_t* sh) {
-  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) sh[w] = v;
-  __syncthreads();
-  uint32_t t = 0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t = max(t, sh[i]);
-  __syncthreads();
-  return t;
-}
 
 __device__ const float g_zero_row[1] = {0.0f};
 
@@ -154,162 +181,336 @@ struct TableLists {
   uint32_t s1, S2;
 };
 
-// number of non-forced pairs with key >= T (two-pointer staircase walk)
-__device__ __forceinline__ uint32_t walk_count(const TableLists& tl, uint32_t T) {
-  uint32_t p = 0;
-  const float x0 = __ldg(tl.v1);
-  while (p < tl.S2 && ord_key(x0 + __ldg(tl.v2 + p)) >= T) ++p;
-  uint32_t c = p > 0 ? p - 1 : 0;  // exclude the forced (0,0)
-  for (uint32_t r1 = 1; r1 < tl.s1 && p > 0; ++r1) {
-    const float x = __ldg(tl.v1 + r1);
-    while (p > 0 && ord_key(x + __ldg(tl.v2 + p - 1)) < T) --p;
-    c += p;
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// (lists may live in shared or global memory: generic loads)
+// number of r2 in [0, hi) with key(x + v2[r2]) >= T (a prefix: v2 non-increasing)
+__device__ __forceinline__ uint32_t prefix_bs(float x, const float* v2, uint32_t hi,
+                                              uint32_t T) {
+  uint32_t lo = 0;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (ord_key(x + v2[mid]) >= T) lo = mid + 1;
+    else hi = mid;
   }
-  return c;
+  return lo;
+}
+
+// first row in [lo, hi) with key(v1[row] + y) < T (rows satisfying it form a prefix)
+__device__ __forceinline__ uint32_t first_fail_row(const float* v1, float y, uint32_t lo,
+                                                   uint32_t hi, uint32_t T) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (ord_key(v1[mid] + y) >= T) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// non-forced pairs with key >= T.  Walks the staircase corner to corner: the
+// rows sharing a boundary p are found by one binary search over r1 and the
+// next boundary by one over r2, so the cost is O(corners * log s) whether the
+// staircase is long in r1, in r2, or both.
+__device__ __forceinline__ uint32_t walk_count(const TableLists& tl, uint32_t T) {
+  uint32_t p = prefix_bs(tl.v1[0], tl.v2, tl.S2, T);
+  if (p == 0) return 0;
+  uint32_t c = 0, r1 = 0;
+  for (;;) {
+    const uint32_t e = first_fail_row(tl.v1, tl.v2[p - 1], r1 + 1, tl.s1, T);
+    c += p * (e - r1);
+    if (e >= tl.s1) break;
+    p = prefix_bs(tl.v1[e], tl.v2, p - 1, T);
+    if (p == 0) break;
+    r1 = e;
+  }
+  return c - 1;  // exclude the forced (0,0)
 }
 
 // visit (r1, pa, pb): prefixes at Ta > Tb (pa <= pb), r1 ascending while pb > 0
 template <class F>
 __device__ __forceinline__ void walk2(const TableLists& tl, uint32_t Ta, uint32_t Tb, F&& visit) {
-  uint32_t pb = 0;
-  const float x0 = __ldg(tl.v1);
-  while (pb < tl.S2 && ord_key(x0 + __ldg(tl.v2 + pb)) >= Tb) ++pb;
-  uint32_t pa = 0;
-  while (pa < pb && ord_key(x0 + __ldg(tl.v2 + pa)) >= Ta) ++pa;
+  const float x0 = tl.v1[0];
+  uint32_t pb = prefix_bs(x0, tl.v2, tl.S2, Tb);
+  uint32_t pa = prefix_bs(x0, tl.v2, pb, Ta);
   visit(0u, pa, pb);
   for (uint32_t r1 = 1; r1 < tl.s1 && pb > 0; ++r1) {
-    const float x = __ldg(tl.v1 + r1);
-    while (pb > 0 && ord_key(x + __ldg(tl.v2 + pb - 1)) < Tb) --pb;
-    while (pa > 0 && ord_key(x + __ldg(tl.v2 + pa - 1)) < Ta) --pa;
+    const float x = tl.v1[r1];
+    if (ord_key(x + tl.v2[pb - 1]) < Tb) pb = prefix_bs(x, tl.v2, pb - 1, Tb);
     if (pa > pb) pa = pb;
+    if (pa > 0 && ord_key(x + tl.v2[pa - 1]) < Ta) pa = prefix_bs(x, tl.v2, pa - 1, Ta);
     visit(r1, pa, pb);
   }
 }
 
+__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t* sh) {
+  v = warp_sum_u64(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  uint64_t t = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sh[i];
+  return t;
+}
+
+// CTA per query, thread per table.  The query's value lists are staged in
+// shared memory (when they fit) so the repeated staircase walks never leave the
+// SM; the emitted bucket ids are collected in shared memory and resolved
+// against the CSR directory by a flat, unrolled loop (8 independent loads in
+// flight per thread).
+// non-forced pairs >= T among rows [rb, re) (corner walk on a row block)
+__device__ __forceinline__ uint32_t walk_count_rows(const float* v1, const float* v2, uint32_t S2,
+                                                    uint32_t rb, uint32_t re, uint32_t T) {
+  if (rb >= re) return 0;
+  uint32_t p = prefix_bs(v1[rb], v2, S2, T);
+  if (p == 0) return 0;
+  uint32_t c = 0, r1 = rb;
+  for (;;) {
+    const uint32_t e = first_fail_row(v1, v2[p - 1], r1 + 1, re, T);
+    c += p * (e - r1);
+    if (e >= re) break;
+    p = prefix_bs(v1[e], v2, p - 1, T);
+    if (p == 0) break;
+    r1 = e;
+  }
+  return rb == 0 ? c - 1 : c;  // exclude the forced (0,0)
+}
+
+// visit (r1, pa, pb) for rows [rb, re) while pb > 0 (prefixes at Ta > Tb)
+template <class F>
+__device__ __forceinline__ void walk2_rows(const float* v1, const float* v2, uint32_t S2,
+                                           uint32_t rb, uint32_t re, uint32_t Ta, uint32_t Tb,
+                                           F&& visit) {
+  if (rb >= re) return;
+  const float x0 = v1[rb];
+  uint32_t pb = prefix_bs(x0, v2, S2, Tb);
+  if (pb == 0) return;
+  uint32_t pa = Ta == 0xffffffffu ? 0 : prefix_bs(x0, v2, pb, Ta);
+  visit(rb, pa, pb);
+  for (uint32_t r1 = rb + 1; r1 < re; ++r1) {
+    const float x = v1[r1];
+    if (ord_key(x + v2[pb - 1]) < Tb) pb = prefix_bs(x, v2, pb - 1, Tb);
+    if (pb == 0) return;
+    if (pa > pb) pa = pb;
+    if (pa > 0 && ord_key(x + v2[pa - 1]) < Ta) pa = prefix_bs(x, v2, pa - 1, Ta);
+    visit(r1, pa, pb);
+  }
+}
+
+// CTA per query (PS_THREADS threads, ~13 KB shared memory, so several query
+// CTAs share an SM and hide each other's latency).
+//  1. radix-select the M-th best key among the L-shape "arm" pairs (row 0 and
+//     column 0 of every table): a subset, so that key T_lo <= T*;
+//  2. one staircase walk materialises every non-forced pair >= T_lo (key +
+//     packed (t, r1, r2)) into per-query global scratch;
+//  3. radix-select T* over that flat array (balanced, coalesced passes);
+//  4. count / collect ties at T*, pick the (r1, r2, t)-smallest ones;
+//  5. compact the selected pairs into bucket ids, resolve them against the CSR
+//     directory with 8 independent loads per thread in flight.
+// If the candidate set overflows the scratch, every pass re-walks instead.
 __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
-  __shared__ uint64_t red[32];
-  __shared__ uint32_t redu[32];
+  __shared__ uint64_t red[PS_THREADS / 32];
   __shared__ uint64_t ties[PS_TIE_CAP];
-  __shared__ uint32_t n_ties;
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t n_ties, n_cand, sel_prefix, sel_rem;
+  long long ck[8];
+  ck[0] = clock64();
   const uint32_t q = blockIdx.x;
   const uint32_t L = a.L, K = a.K, s = a.s;
   const uint32_t S2 = K == 2 ? s : 1;
-  const uint64_t LKs = (uint64_t)L * K * s;
-  const float* V = a.vals + (uint64_t)q * LKs;
-  const uint32_t* Cq = a.codes + (uint64_t)q * LKs;
-  if (threadIdx.x == 0) n_ties = 0;
+  const float* V = a.vals + (uint64_t)q * a.lstride;
+  const uint32_t* Cq = a.codes + (uint64_t)q * a.lstride;
+  uint32_t* ckey = a.ckey + (uint64_t)q * a.ccap;
+  uint32_t* cpair = a.cpair + (uint64_t)q * a.ccap;
+  if (threadIdx.x == 0) {
+    n_ties = 0;
+    n_cand = 0;
+  }
   __syncthreads();
-  auto lists = [&](uint32_t t) {
-    TableLists tl;
-    tl.v1 = V + (uint64_t)t * K * s;
-    tl.v2 = K == 2 ? tl.v1 + s : g_zero_row;
-    tl.s1 = s;
-    tl.S2 = S2;
-    return tl;
+  ck[1] = clock64();
+  auto V1 = [&](uint32_t t) { return V + (uint64_t)t * K * s; };
+  auto V2 = [&](uint32_t t) { return K == 2 ? V + (uint64_t)t * K * s + s : g_zero_row; };
+  const uint32_t TPT = L < blockDim.x ? blockDim.x / L : 1;
+  const uint32_t RB = (s + TPT - 1) / TPT;
+  const uint32_t units = L * TPT;
+  auto unit = [&](uint32_t u, uint32_t& t, uint32_t& rb, uint32_t& re) {
+    t = u / TPT;
+    const uint32_t part = u - t * TPT;
+    rb = min(s, part * RB);
+    re = min(s, rb + RB);
   };
   const uint64_t M = a.peff - L;  // non-forced probes
-  auto count = [&](uint32_t T) -> uint64_t {
-    uint64_t c = 0;
-    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) c += walk_count(lists(t), T);
-    return block_sum_u64(c, red);
-  };
-  uint32_t Tstar = 0;
-  if (M > 0) {
-    // best non-forced key over all tables: max(v1[0]+v2[1], v1[1]+v2[0])
-    uint32_t hi = 0;
-    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
-      const TableLists tl = lists(t);
-      const float x0 = __ldg(tl.v1);
-      if (S2 > 1) hi = max(hi, ord_key(x0 + __ldg(tl.v2 + 1)));
-      if (s > 1) hi = max(hi, ord_key(__ldg(tl.v1 + 1) + __ldg(tl.v2)));
-    }
-    hi = block_max_u32(hi, redu);
-    // gallop down from hi until count >= M, then bisect: Tstar = max T with count(T) >= M
-    uint32_t bad = 0xffffffffu;  // count(bad) < M (or sentinel)
-    uint32_t T = hi, step = 1;
-    bool have_bad = false;
-    for (;;) {
-      if (count(T) >= M) break;
-      bad = T;
-      have_bad = true;
-      T = T > step ? T - step : 0;
-      step <<= 1;
-      if (T == 0) break;  // count(0) counts every pair >= M
-    }
-    uint32_t lo = T;
-    if (have_bad) {
-      while (bad - lo > 1) {
-        const uint32_t mid = lo + (bad - lo) / 2;
-        if (count(mid) >= M) lo = mid;
-        else bad = mid;
+  // rank-th largest key (1-based) among enumerated keys in [base, base + 2^nbits)
+  auto radix_select = [&](uint64_t rank, uint32_t base, int nbits, auto&& enumerate) -> uint32_t {
+    uint32_t prefix = 0, mask = 0, rem = (uint32_t)rank;
+    int hb = nbits;
+    while (hb > 0) {
+      const int w = hb < 11 ? hb : 11, sh = hb - w, nb = 1 << w;
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      enumerate([&](uint32_t key, uint32_t) {
+        const uint32_t off = key - base;
+        if ((off & mask) == prefix) atomicAdd(&hist[(off >> sh) & (nb - 1)], 1u);
+      });
+      __syncthreads();
+      // descending scan over the bins, 8 bins per thread
+      uint32_t hv[8], hs = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int bin = nb - 1 - (int)(threadIdx.x * 8 + j);
+        hv[j] = bin >= 0 ? hist[bin] : 0;
+        hs += hv[j];
       }
-    } else {
-      // count(hi) >= M already: search upward is impossible (hi is the max key)
+      uint32_t tot;
+      uint32_t above = block_excl_scan_u32(hs, (uint32_t*)red, &tot);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int bin = nb - 1 - (int)(threadIdx.x * 8 + j);
+        if (bin >= 0 && above < rem && rem <= above + hv[j]) {
+          sel_prefix = prefix | ((uint32_t)bin << sh);
+          sel_rem = rem - above;
+        }
+        above += hv[j];
+      }
+      __syncthreads();
+      prefix = sel_prefix;
+      rem = sel_rem;
+      mask |= (uint32_t)(nb - 1) << sh;
+      hb = sh;
+      __syncthreads();
     }
-    Tstar = lo;
-  }
-  const uint32_t Ta = Tstar == 0xffffffffu ? 0xffffffffu : Tstar + 1;  // strictly above T*
-  // per-thread gt / tie counts
-  uint64_t my_gt = 0, my_tie = 0;
-  if (M > 0) {
-    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
-      walk2(lists(t), Ta, Tstar, [&](uint32_t r1, uint32_t pa, uint32_t pb) {
-        const uint32_t st = r1 == 0 ? 1 : 0;
-        const uint32_t ga = max(st, pa), gb = max(st, pb);
-        my_gt += ga - st;
-        my_tie += gb - ga;
+    return base + prefix;
+  };
+  auto bitlen = [](uint32_t x) { return x ? 32 - __clz(x) : 0; };
+  auto pack = [](uint32_t t, uint32_t r1, uint32_t r2) { return (t << 22) | (r1 << 11) | r2; };
+  uint32_t Tstar = 0, Tlo = 0;
+  bool flat = false;
+  uint32_t C = 0;
+  // walk-based enumeration of the non-forced pairs >= Tlo
+  auto enum_stair = [&](auto&& visit) {
+    for (uint32_t u = threadIdx.x; u < units; u += blockDim.x) {
+      uint32_t t, rb, re;
+      unit(u, t, rb, re);
+      const float* v1 = V1(t);
+      const float* v2 = V2(t);
+      walk2_rows(v1, v2, S2, rb, re, 0xffffffffu, Tlo, [&](uint32_t r1, uint32_t, uint32_t pb) {
+        const float x = v1[r1];
+        for (uint32_t r2 = r1 == 0 ? 1 : 0; r2 < pb; ++r2) visit(ord_key(x + v2[r2]), pack(t, r1, r2));
       });
     }
+  };
+  auto enum_cand = [&](auto&& visit) {
+    if (flat) {
+      for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) visit(__ldcg(ckey + i), __ldcg(cpair + i));
+    } else {
+      enum_stair(visit);
+    }
+  };
+  if (M > 0) {
+    const uint32_t arm_len = (S2 - 1) + (s - 1);
+    const uint32_t apt = (arm_len + TPT - 1) / TPT;
+    auto enum_arms = [&](auto&& visit) {
+      for (uint32_t u = threadIdx.x; u < units; u += blockDim.x) {
+        const uint32_t t = u / TPT, part = u - t * TPT;
+        const float* v1 = V1(t);
+        const float* v2 = V2(t);
+        const uint32_t i0 = min(arm_len, part * apt), i1 = min(arm_len, i0 + apt);
+        for (uint32_t i = i0; i < i1; ++i) {
+          const float sc = i < S2 - 1 ? v1[0] + v2[i + 1] : v1[i - (S2 - 1) + 1] + v2[0];
+          visit(ord_key(sc), 0u);
+        }
+      }
+    };
+    uint32_t amax = 0, amin = 0xffffffffu;
+    enum_arms([&](uint32_t k, uint32_t) { amax = max(amax, k); amin = min(amin, k); });
+    uint64_t pk = ((uint64_t)amax << 32) | (0xffffffffu - amin);
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t y = ((uint64_t)__shfl_xor_sync(FULL, (uint32_t)(pk >> 32), o) << 32) |
+                         __shfl_xor_sync(FULL, (uint32_t)pk, o);
+      pk = (max(pk >> 32, y >> 32) << 32) | max(pk & 0xffffffffu, y & 0xffffffffu);
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pk;
+    __syncthreads();
+    uint64_t mx = 0, nl = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      mx = max(mx, red[i] >> 32);
+      nl = max(nl, red[i] & 0xffffffffu);
+    }
+    amax = (uint32_t)mx;
+    amin = 0xffffffffu - (uint32_t)nl;
+    __syncthreads();
+    if ((uint64_t)arm_len * L >= M) Tlo = radix_select(M, amin, bitlen(amax - amin), enum_arms);
+    // materialise every non-forced pair >= Tlo (one atomic per row run)
+    for (uint32_t u = threadIdx.x; u < units; u += blockDim.x) {
+      uint32_t t, rb, re;
+      unit(u, t, rb, re);
+      const float* v1 = V1(t);
+      const float* v2 = V2(t);
+      walk2_rows(v1, v2, S2, rb, re, 0xffffffffu, Tlo, [&](uint32_t r1, uint32_t, uint32_t pb) {
+        const uint32_t st = r1 == 0 ? 1 : 0;
+        if (pb <= st) return;
+        const uint32_t base = atomicAdd(&n_cand, pb - st);
+        if (base + (pb - st) > a.ccap) return;
+        const float x = v1[r1];
+        for (uint32_t r2 = st; r2 < pb; ++r2) {
+          ckey[base + r2 - st] = ord_key(x + v2[r2]);
+          cpair[base + r2 - st] = pack(t, r1, r2);
+        }
+      });
+    }
+    __syncthreads();
+    C = n_cand;
+    flat = C <= a.ccap;
+    // every pair >= Tlo has key <= amax (the best non-forced pair lies on an arm)
+    Tstar = radix_select(M, Tlo, bitlen(amax - Tlo), enum_cand);
   }
+  ck[2] = clock64();
+  // counts above / at T* (pairs below Tlo are below T* and never matter)
+  uint64_t my_gt = 0, my_ge = 0;
+  if (M > 0)
+    enum_cand([&](uint32_t key, uint32_t) {
+      my_gt += key > Tstar;
+      my_ge += key >= Tstar;
+    });
   const uint64_t cgt = block_sum_u64(my_gt, red);
-  const uint64_t ties_total = block_sum_u64(my_tie, red);
+  const uint64_t ties_total = block_sum_u64(my_ge, red) - cgt;
   const uint64_t m = M > cgt ? M - cgt : 0;  // ties to take
-  // composite tie key (r1*S2 + r2)*L + t: order (r1, r2, t); take keys < Kstar
+  auto comp = [&](uint32_t pr) {  // (r1, r2, t) composite order
+    const uint32_t t = pr >> 22, r1 = (pr >> 11) & 2047u, r2 = pr & 2047u;
+    return ((uint64_t)r1 * S2 + r2) * L + t;
+  };
   uint64_t Kstar = ~0ull;
   if (M > 0 && ties_total > m) {
     if (ties_total <= PS_TIE_CAP) {
-      for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
-        walk2(lists(t), Ta, Tstar, [&](uint32_t r1, uint32_t pa, uint32_t pb) {
-          const uint32_t st = r1 == 0 ? 1 : 0;
-          for (uint32_t r2 = max(st, pa); r2 < max(st, pb); ++r2)
-            ties[atomicAdd(&n_ties, 1u)] = ((uint64_t)r1 * S2 + r2) * L + t;
-        });
+      enum_cand([&](uint32_t key, uint32_t pr) {
+        if (key == Tstar) ties[atomicAdd(&n_ties, 1u)] = comp(pr);
+      });
+      __syncthreads();
+      uint64_t found = ~0ull;
+      for (uint32_t i = threadIdx.x; i < ties_total; i += blockDim.x) {
+        const uint64_t xk = ties[i];
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < ties_total; ++j) rank += ties[j] < xk;
+        if (rank == m) found = xk;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t y = ((uint64_t)__shfl_xor_sync(FULL, (uint32_t)(found >> 32), o) << 32) |
+                           __shfl_xor_sync(FULL, (uint32_t)found, o);
+        found = y < found ? y : found;
       }
       __syncthreads();
-      uint32_t N = 1;
-      while (N < ties_total) N <<= 1;
-      for (uint32_t i = ties_total + threadIdx.x; i < N; i += blockDim.x) ties[i] = ~0ull;
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = found;
       __syncthreads();
-      for (uint32_t kk = 2; kk <= N; kk <<= 1)
-        for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
-          for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
-            const uint32_t ixj = i ^ jj;
-            if (ixj > i) {
-              const uint64_t x = ties[i], y = ties[ixj];
-              if ((x > y) == ((i & kk) == 0)) { ties[i] = y; ties[ixj] = x; }
-            }
-          }
-          __syncthreads();
-        }
-      Kstar = ties[m];  // keys < ties[m] are the m smallest
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) Kstar = red[i] < Kstar ? red[i] : Kstar;
       __syncthreads();
     } else {
-      // many ties: bisect the composite key with counting walks
       auto count_lt = [&](uint64_t Kc) -> uint64_t {
-        const uint64_t kr1 = Kc / ((uint64_t)S2 * L);
-        const uint64_t rem = Kc - kr1 * S2 * L;
-        const uint64_t kr2 = rem / L, kt = rem - kr2 * L;
         uint64_t c = 0;
-        for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
-          walk2(lists(t), Ta, Tstar, [&](uint32_t r1, uint32_t pa, uint32_t pb) {
-            const uint32_t st = r1 == 0 ? 1 : 0;
-            const uint64_t ga = max(st, pa), gb = max(st, pb);
-            if (ga == gb || r1 > kr1) return;
-            if (r1 < kr1) { c += gb - ga; return; }
-            if (kr2 > ga) c += (kr2 < gb ? kr2 : gb) - ga;
-            if (kr2 >= ga && kr2 < gb && t < kt) c += 1;
-          });
-        }
+        enum_cand([&](uint32_t key, uint32_t pr) { c += key == Tstar && comp(pr) < Kc; });
         return block_sum_u64(c, red);
       };
       uint64_t lo = 0, hi = (uint64_t)s * S2 * L;
@@ -321,70 +522,102 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       Kstar = lo;
     }
   }
-  // emission counts, exclusive scan over threads
-  uint64_t mine = 0;
+  ck[3] = clock64();
+  auto selected = [&](uint32_t key, uint32_t pr) {
+    return key > Tstar || (key == Tstar && (Kstar == ~0ull || comp(pr) < Kstar));
+  };
+  uint32_t* gb_out = a.gbuf + (uint64_t)q * a.peff;
+  const uint32_t twoD = 2 * a.D;
+  const uint32_t NB = (uint32_t)a.NB;
+  auto bucket = [&](uint32_t pr) {
+    const uint32_t t = pr >> 22, r1 = (pr >> 11) & 2047u, r2 = pr & 2047u;
+    const uint32_t* c1 = Cq + (uint64_t)t * K * s;
+    return t * NB + (K == 2 ? __ldg(c1 + r1) * twoD + __ldg(c1 + s + r2) : __ldg(c1 + r1));
+  };
+  for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) gb_out[t] = bucket(t << 22);
   if (M > 0) {
-    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
-      walk2(lists(t), Ta, Tstar, [&](uint32_t r1, uint32_t pa, uint32_t pb) {
-        const uint32_t st = r1 == 0 ? 1 : 0;
-        const uint32_t ga = max(st, pa), gb = max(st, pb);
-        mine += ga - st;
-        if (Kstar == ~0ull) mine += gb - ga;
-        else
-          for (uint32_t r2 = ga; r2 < gb; ++r2) mine += (((uint64_t)r1 * S2 + r2) * L + t) < Kstar;
+    // compaction of the selected pairs: per-thread counts, exclusive scan, write
+    uint64_t mine = 0;
+    uint32_t i_beg = 0, i_end = 0;
+    if (flat) {
+      const uint32_t per = (C + blockDim.x - 1) / blockDim.x;
+      i_beg = min(C, threadIdx.x * per);
+      i_end = min(C, i_beg + per);
+      for (uint32_t i = i_beg; i < i_end; ++i) mine += selected(__ldcg(ckey + i), __ldcg(cpair + i));
+    } else {
+      enum_stair([&](uint32_t key, uint32_t pr) { mine += selected(key, pr); });
+    }
+    uint64_t x = mine;
+    {
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = ((uint64_t)__shfl_up_sync(FULL, (uint32_t)(x >> 32), o) << 32) |
+                           __shfl_up_sync(FULL, (uint32_t)x, o);
+        if (lane >= o) x += y;
+      }
+      __syncthreads();
+      if (lane == 31) red[w] = x;
+      __syncthreads();
+      uint64_t wb = 0;
+      for (int i = 0; i < w; ++i) wb += red[i];
+      x = wb + x - mine;
+    }
+    uint64_t slot = L + x;
+    if (flat) {
+      for (uint32_t i = i_beg; i < i_end; ++i) {
+        const uint32_t pr = __ldcg(cpair + i);
+        if (selected(__ldcg(ckey + i), pr)) gb_out[slot++] = bucket(pr);
+      }
+    } else {
+      enum_stair([&](uint32_t key, uint32_t pr) {
+        if (selected(key, pr)) gb_out[slot++] = bucket(pr);
       });
     }
   }
-  uint64_t x = mine;
-  {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t y = __shfl_up_sync(FULL, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) red[w] = x;
-    __syncthreads();
-    uint64_t wb = 0;
-    for (int i = 0; i < w; ++i) wb += red[i];
-    x = wb + x - mine;
-    __syncthreads();
-  }
+  __syncthreads();
+  ck[4] = clock64();
+  // resolve probes against the directory: 8 probes (16 loads) in flight per thread
   uint64_t* ppos = a.ppos + (uint64_t)q * a.peff;
   uint32_t* plen = a.plen + (uint64_t)q * a.peff;
   uint64_t* dbg = a.dbg ? a.dbg + (uint64_t)q * a.peff : nullptr;
-  const uint32_t twoD = 2 * a.D;
   uint64_t esum = 0;
-  auto emit = [&](uint64_t slot, uint32_t t, uint32_t b) {
-    const uint32_t* of = a.offs + (uint64_t)t * (a.NB + 1);
-    const uint32_t o0 = __ldg(of + b), o1 = __ldg(of + b + 1);
-    ppos[slot] = __ldg(a.tbase + t) + o0;
-    plen[slot] = o1 - o0;
-    esum += o1 - o0;
-    if (dbg) dbg[slot] = (uint64_t)t * a.NB + b;
-  };
-  for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
-    const uint32_t* c1 = Cq + (uint64_t)t * K * s;
-    const uint32_t* c2 = c1 + s;
-    emit(t, t, K == 2 ? __ldg(c1) * twoD + __ldg(c2) : __ldg(c1));
-  }
-  if (M > 0) {
-    uint64_t slot = L + x;
-    for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) {
-      const uint32_t* c1 = Cq + (uint64_t)t * K * s;
-      const uint32_t* c2 = c1 + s;
-      walk2(lists(t), Ta, Tstar, [&](uint32_t r1, uint32_t pa, uint32_t pb) {
-        const uint32_t st = r1 == 0 ? 1 : 0;
-        const uint32_t ga = max(st, pa), gb = max(st, pb);
-        const uint32_t h1 = __ldg(c1 + r1);
-        for (uint32_t r2 = st; r2 < gb; ++r2) {
-          if (r2 >= ga && Kstar != ~0ull && (((uint64_t)r1 * S2 + r2) * L + t) >= Kstar) continue;
-          emit(slot++, t, K == 2 ? h1 * twoD + __ldg(c2 + r2) : h1);
-        }
-      });
+  const uint32_t P = (uint32_t)a.peff;
+  constexpr int UR = 8;
+  for (uint32_t p0 = threadIdx.x; p0 < P; p0 += UR * blockDim.x) {
+    uint32_t gbk[UR], o0[UR], o1[UR], tt[UR];
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      const uint32_t pp = p0 + u * blockDim.x;
+      gbk[u] = pp < P ? __ldcg(gb_out + pp) : 0;
+      tt[u] = gbk[u] / NB;
+    }
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      const uint32_t* of = a.offs + (uint64_t)tt[u] * (NB + 1) + (gbk[u] - tt[u] * NB);
+      o0[u] = __ldg(of);
+      o1[u] = __ldg(of + 1);
+    }
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      const uint32_t pp = p0 + u * blockDim.x;
+      if (pp < P) {
+        ppos[pp] = __ldg(a.tbase + tt[u]) + o0[u];
+        plen[pp] = o1[u] - o0[u];
+        esum += o1[u] - o0[u];
+        if (dbg) dbg[pp] = (uint64_t)tt[u] * a.NB + (gbk[u] - tt[u] * NB);
+      }
     }
   }
   esum = block_sum_u64(esum, red);
-  if (threadIdx.x == 0) a.eq[q] = (uint32_t)esum;
+  if (threadIdx.x == 0) {
+    a.eq[q] = (uint32_t)esum;
+    if (a.dbg_clk) {
+      ck[5] = clock64();
+      ck[6] = flat;
+      ck[7] = C;
+      for (int i = 0; i < 8; ++i) a.dbg_clk[(uint64_t)q * 8 + i] = ck[i];
+    }
+  }
 }
 
 // exclusive scan of eq[nq] -> coff[nq+1] (single CTA)
@@ -473,28 +706,51 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
       if (threadIdx.x * 2 + 1 < np) pref[threadIdx.x * 2 + 1] = ex + v[0];
       if (threadIdx.x == 0) pref[np] = tot;
       __syncthreads();
-      for (uint32_t e = threadIdx.x; e < tot; e += blockDim.x) {
-        // probe containing entry e: last p with pref[p] <= e
+      // thread-contiguous entry ranges: one binary search per thread, then a
+      // forward walk with 4 independent id loads in flight
+      const uint32_t per = (tot + blockDim.x - 1) / blockDim.x;
+      uint32_t e = min(tot, threadIdx.x * per);
+      const uint32_t e_end = min(tot, e + per);
+      uint32_t p = 0;
+      {
         uint32_t lo = 0, hi = np;
         while (hi - lo > 1) {
           const uint32_t mid = (lo + hi) >> 1;
           if (pref[mid] <= e) lo = mid;
           else hi = mid;
         }
-        const uint32_t id = __ldg(a.ids + tpos[lo] + (e - pref[lo]));
-        const uint32_t bit = 1u << (id & 31);
-        const uint32_t old = atomicOr(bm + (id >> 5), bit);
-        const bool isnew = !(old & bit);
-        const unsigned act = __activemask();
-        const unsigned bal = __ballot_sync(act, isnew);
-        if (bal) {
-          const int lane = threadIdx.x & 31;
-          const int leader = __ffs(act) - 1;
-          uint32_t base = 0;
-          if (lane == leader) base = atomicAdd(&ucount, __popc(bal));
-          base = __shfl_sync(act, base, leader);
-          if (isnew) out[base + __popc(bal & ((1u << lane) - 1))] = id;
+        p = lo;
+      }
+      while (e < e_end) {
+        uint32_t idv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          idv[u] = 0xffffffffu;
+          if (e + u < e_end) {
+            while (pref[p + 1] <= e + u) ++p;
+            idv[u] = __ldg(a.ids + tpos[p] + (e + u - pref[p]));
+          }
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t id = idv[u];
+          bool isnew = false;
+          if (id != 0xffffffffu) {
+            const uint32_t bit = 1u << (id & 31);
+            isnew = !(atomicOr(bm + (id >> 5), bit) & bit);
+          }
+          const unsigned act = __activemask();
+          const unsigned bal = __ballot_sync(act, isnew);
+          if (bal) {
+            const int lane = threadIdx.x & 31;
+            const int leader = __ffs(act) - 1;
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(&ucount, __popc(bal));
+            base = __shfl_sync(act, base, leader);
+            if (isnew) out[base + __popc(bal & ((1u << lane) - 1))] = id;
+          }
+        }
+        e += 4;
       }
       __syncthreads();
     }
@@ -707,14 +963,15 @@ static size_t score_smem(uint32_t d) {
 
 // ------------------------------------------------------------ host driver
 void launch_query_lists(const Index& ix, const float* Qd, uint64_t nq, uint32_t s_cap,
-                        float* vals, uint32_t* codes, cudaStream_t s) {
+                        float* vals, uint32_t* codes, cudaStream_t s, uint64_t lstride) {
+  if (!lstride) lstride = (uint64_t)ix.prm.L * ix.prm.K * s_cap;
   if (nq == 0) return;
   const uint32_t d = ix.d, D = ix.prm.D, K = ix.prm.K, L = ix.prm.L;
   const uint32_t G = ix.P < 32 ? 1 : ix.P / 32;
   const unsigned grid = (unsigned)((nq * L * K * G + 127) / 128);
 #define FPP_QL_CASE(PP)                                                                      \
   case PP:                                                                                   \
-    k_query_lists<PP><<<grid, 128, 0, s>>>(Qd, nq, d, D, K, ix.signs, L, s_cap, vals, codes); \
+    k_query_lists<PP><<<grid, 128, 0, s>>>(Qd, nq, d, D, K, ix.signs, L, s_cap, lstride, vals, codes); \
     break;
   switch (ix.P) {
     FPP_QL_CASE(2) FPP_QL_CASE(4) FPP_QL_CASE(8) FPP_QL_CASE(16) FPP_QL_CASE(32)
@@ -744,8 +1001,9 @@ static void run_chunk(const Index& ix, const float* Qd, uint32_t nqc, uint32_t k
   const uint32_t scap = query_cap(ix, qprobes);
   const uint64_t peff = query_probes(ix, qprobes);
   const uint64_t LKs = (uint64_t)L * K * scap;
-  ix.q_vals.ensure((size_t)nqc * LKs);
-  ix.q_codes.ensure((size_t)nqc * LKs);
+  const uint64_t lstride = (LKs + 3) & ~3ull;  // 16-byte aligned per-query blocks (TMA)
+  ix.q_vals.ensure((size_t)nqc * lstride);
+  ix.q_codes.ensure((size_t)nqc * lstride);
   ix.q_ppos.ensure((size_t)nqc * peff);
   ix.q_plen.ensure((size_t)nqc * peff);
   ix.q_eq.ensure(nqc);
@@ -755,13 +1013,44 @@ static void run_chunk(const Index& ix, const float* Qd, uint32_t nqc, uint32_t k
 
   cudaEvent_t e0;
   ix.timer.begin(PH_QHASH, s, &e0);
-  launch_query_lists(ix, Qd, nqc, scap, ix.q_vals.p, ix.q_codes.p, s);
+  launch_query_lists(ix, Qd, nqc, scap, ix.q_vals.p, ix.q_codes.p, s, lstride);
   ix.timer.end(PH_QHASH, e0, s);
 
   ix.timer.begin(PH_PROBE, s, &e0);
-  ProbeArgs pa{ix.q_vals.p, ix.q_codes.p, L, K, scap, ix.prm.D, ix.NB, peff, ix.offsets,
-               ix.table_base, ix.q_ppos.p, ix.q_plen.p, ix.q_eq.p, dbg_probes};
-  k_probe_select<<<nqc, PS_THREADS, 0, s>>>(pa);
+  ProbeArgs pa{ix.q_vals.p, ix.q_codes.p, nqc, L, K, scap, ix.prm.D, ix.NB, peff, ix.offsets,
+               ix.table_base, ix.q_ppos.p, ix.q_plen.p, ix.q_eq.p, dbg_probes, nullptr, lstride, nullptr,
+               nullptr, nullptr, 0};
+  static const bool dbg_probe = getenv("FPP_DEBUG_PROBE") != nullptr;
+  if (dbg_probe) {
+    ix.q_dbgclk.ensure((size_t)nqc * 8);
+    pa.dbg_clk = reinterpret_cast<long long*>(ix.q_dbgclk.p);
+  }
+  {
+    const uint32_t ccap = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(4 * peff + 4096, 16384),
+                                                       (uint64_t)L * K * scap * scap);
+    ix.q_ckey.ensure((size_t)nqc * ccap);
+    ix.q_cpair.ensure((size_t)nqc * ccap);
+    pa.ckey = ix.q_ckey.p;
+    pa.cpair = ix.q_cpair.p;
+    pa.ccap = ccap;
+    ix.q_gbuf.ensure((size_t)nqc * peff);
+    pa.gbuf = ix.q_gbuf.p;
+    k_probe_select<<<nqc, PS_THREADS, 0, s>>>(pa);
+  }
+  if (dbg_probe) {
+    std::vector<long long> h((size_t)nqc * 8);
+    FPP_CUDA(cudaMemcpyAsync(h.data(), pa.dbg_clk, h.size() * 8, cudaMemcpyDeviceToHost, s));
+    FPP_CUDA(cudaStreamSynchronize(s));
+    double acc[6] = {0}, it = 0, ti = 0;
+    for (uint32_t i = 0; i < nqc; ++i) {
+      for (int j = 0; j < 5; ++j) acc[j] += (double)(h[i * 8 + j + 1] - h[i * 8 + j]);
+      it += (double)h[i * 8 + 6];
+      ti += (double)h[i * 8 + 7];
+    }
+    fprintf(stderr, "[probe dbg] per query cycles: stage %.0f search %.0f ties %.0f emitcount %.0f "
+            "resolve %.0f | flat %.2f candidates %.1f\n", acc[0] / nqc, acc[1] / nqc, acc[2] / nqc,
+            acc[3] / nqc, acc[4] / nqc, it / nqc, ti / nqc);
+  }
   FPP_LAUNCH();
   k_scan_eq<<<1, 1024, 0, s>>>(ix.q_eq.p, nqc, ix.q_coff.p);
   FPP_LAUNCH();
@@ -822,7 +1111,8 @@ static void run_chunk(const Index& ix, const float* Qd, uint32_t nqc, uint32_t k
 
 static uint32_t chunk_size(const Index& ix, uint32_t qprobes, uint64_t nq) {
   const uint64_t LKs = (uint64_t)ix.prm.L * ix.prm.K * query_cap(ix, qprobes);
-  const uint64_t per_q = LKs * 8 + query_probes(ix, qprobes) * 12 + 64;
+  const uint64_t pe = query_probes(ix, qprobes);
+  const uint64_t per_q = LKs * 8 + pe * 16 + (4 * pe + 16384) * 8 + 64;
   uint64_t c = (1ull << 31) / per_q;  // ~2 GB of per-chunk scratch
   c = std::max<uint64_t>(1, std::min<uint64_t>(c, 16384));
   return (uint32_t)std::min<uint64_t>(c, nq);
