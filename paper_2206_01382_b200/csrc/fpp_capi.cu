@@ -90,12 +90,30 @@ Index::~Index() {
   dfree(table_base);
   dfree(ids);
   dfree(scores);
-  q_vals.release(); q_codes.release(); q_ppos.release(); q_plen.release(); q_gbuf.release(); q_ckey.release(); q_cpair.release(); q_eq.release();
-  q_coff.release(); q_uq.release(); q_cands.release(); q_bitmap.release(); q_in.release();
-  q_ids.release(); q_scores.release(); q_stats.release(); q_counter.release();
+  for (auto& sl : slot) sl.release();
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (ev_join2) cudaEventDestroy(ev_join2);
+  if (sA) cudaStreamDestroy(sA);
+  if (sB) cudaStreamDestroy(sB);
+  q_in.release(); q_ids.release(); q_scores.release(); q_stats.release();
   if (h_pinned) cudaFreeHost(h_pinned);
   if (stream) cudaStreamDestroy(stream);
   cudaSetDevice(cur);
+}
+
+void Index::QSlot::release() {
+  vals.release(); codes.release(); ppos.release(); plen.release(); gbuf.release();
+  ckey.release(); cpair.release(); dbgclk.release(); eq.release(); coff.release();
+  uq.release(); cands.release(); bitmap.release(); counter.release();
+  if (pinned) cudaFreeHost(pinned);
+  if (ev_probe) cudaEventDestroy(ev_probe);
+  if (ev_bdone) cudaEventDestroy(ev_bdone);
+  ev_bdone = nullptr;
+  if (stream) cudaStreamDestroy(stream);
+  pinned = nullptr;
+  ev_probe = nullptr;
+  stream = nullptr;
 }
 
 uint64_t host_mix64(uint64_t z) {  // common.hpp:18-23

@@ -84,26 +84,37 @@ struct Index {
   uint32_t max_bucket = 0;
   uint64_t device_bytes = 0;
 
-  // query scratch (guarded by mu; concurrent queries serialize on it)
+  // query scratch (guarded by mu; concurrent queries serialize on it).  Two
+  // slots double-buffer query chunks across two streams.
+  struct QSlot {
+    DBuf<float> vals;
+    DBuf<uint32_t> codes;
+    DBuf<uint64_t> ppos;
+    DBuf<uint32_t> plen;
+    DBuf<uint32_t> gbuf;
+    DBuf<uint32_t> ckey;
+    DBuf<uint32_t> cpair;
+    DBuf<uint64_t> dbgclk;
+    DBuf<uint32_t> eq;
+    DBuf<uint64_t> coff;
+    DBuf<uint32_t> uq;
+    DBuf<uint32_t> cands;
+    DBuf<uint32_t> bitmap;
+    DBuf<uint32_t> counter;
+    uint64_t* pinned = nullptr;     // etot readback
+    cudaEvent_t ev_probe = nullptr; // stage A (hash + probe select) done
+    cudaEvent_t ev_bdone = nullptr; // stage B (collect + score) done
+    cudaStream_t stream = nullptr;  // unused (streams live on the index)
+    void release();
+  };
   mutable std::mutex mu;
-  mutable DBuf<float> q_vals;
-  mutable DBuf<uint32_t> q_codes;
-  mutable DBuf<uint64_t> q_ppos;
-  mutable DBuf<uint32_t> q_plen;
-  mutable DBuf<uint32_t> q_gbuf;
-  mutable DBuf<uint32_t> q_ckey;
-  mutable DBuf<uint32_t> q_cpair;
-  mutable DBuf<uint64_t> q_dbgclk;
-  mutable DBuf<uint32_t> q_eq;
-  mutable DBuf<uint64_t> q_coff;
-  mutable DBuf<uint32_t> q_uq;
-  mutable DBuf<uint32_t> q_cands;
-  mutable DBuf<uint32_t> q_bitmap;
+  mutable QSlot slot[2];
+  mutable cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+  mutable cudaStream_t sA = nullptr, sB = nullptr;  // pipeline streams (low / high priority)
   mutable DBuf<float> q_in;
   mutable DBuf<uint32_t> q_ids;
   mutable DBuf<double> q_scores;
   mutable DBuf<fpp_query_stats> q_stats;
-  mutable DBuf<uint32_t> q_counter;
   uint64_t* h_pinned = nullptr;  // small pinned readback
 
   mutable PhaseTimer timer;

@@ -993,54 +993,75 @@ static int co_smem_max() {
   return v;
 }
 
-// run one chunk; dbg_probes optional
-static void run_chunk(const Index& ix, const float* Qd, uint32_t nqc, uint32_t k, uint32_t qprobes,
-                      uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s,
-                      uint64_t* dbg_probes) {
+// Stage A of one chunk on stream `st`: query hashing, probe selection,
+// candidate offsets; the total candidate count is copied to the slot's pinned
+// word and ev_probe recorded.
+static uint32_t cand_cap(const Index& ix, uint32_t qprobes) {
+  const uint64_t peff = query_probes(ix, qprobes);
+  const uint64_t scap = query_cap(ix, qprobes);
+  return (uint32_t)std::min<uint64_t>(std::max<uint64_t>(4 * peff + 4096, 16384),
+                                      (uint64_t)ix.prm.L * ix.prm.K * scap * scap);
+}
+
+// size a slot's chunk buffers for up to nqc queries (before any launch uses it)
+static void prepare_slot(const Index& ix, Index::QSlot& sl, uint32_t nqc, uint32_t qprobes) {
+  const uint64_t LKs = (uint64_t)ix.prm.L * ix.prm.K * query_cap(ix, qprobes);
+  const uint64_t lstride = (LKs + 3) & ~3ull;
+  const uint64_t peff = query_probes(ix, qprobes);
+  const uint32_t ccap = cand_cap(ix, qprobes);
+  sl.vals.ensure((size_t)nqc * lstride);
+  sl.codes.ensure((size_t)nqc * lstride);
+  sl.ppos.ensure((size_t)nqc * peff);
+  sl.plen.ensure((size_t)nqc * peff);
+  sl.gbuf.ensure((size_t)nqc * peff);
+  sl.ckey.ensure((size_t)nqc * ccap);
+  sl.cpair.ensure((size_t)nqc * ccap);
+  sl.eq.ensure(nqc);
+  sl.uq.ensure(nqc);
+  sl.coff.ensure((size_t)nqc + 1);
+  sl.counter.ensure(4);
+}
+
+static void stage_a(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t nqc,
+                    uint32_t qprobes, cudaStream_t st, uint64_t* dbg_probes) {
   const uint32_t L = ix.prm.L, K = ix.prm.K;
   const uint32_t scap = query_cap(ix, qprobes);
   const uint64_t peff = query_probes(ix, qprobes);
   const uint64_t LKs = (uint64_t)L * K * scap;
-  const uint64_t lstride = (LKs + 3) & ~3ull;  // 16-byte aligned per-query blocks (TMA)
-  ix.q_vals.ensure((size_t)nqc * lstride);
-  ix.q_codes.ensure((size_t)nqc * lstride);
-  ix.q_ppos.ensure((size_t)nqc * peff);
-  ix.q_plen.ensure((size_t)nqc * peff);
-  ix.q_eq.ensure(nqc);
-  ix.q_uq.ensure(nqc);
-  ix.q_coff.ensure((size_t)nqc + 1);
-  ix.q_counter.ensure(4);
+  const uint64_t lstride = (LKs + 3) & ~3ull;  // 16-byte aligned per-query blocks
+  prepare_slot(ix, sl, nqc, qprobes);
+  sl.vals.ensure((size_t)nqc * lstride);
+  sl.codes.ensure((size_t)nqc * lstride);
+  sl.ppos.ensure((size_t)nqc * peff);
+  sl.plen.ensure((size_t)nqc * peff);
+  sl.eq.ensure(nqc);
+  sl.uq.ensure(nqc);
+  sl.coff.ensure((size_t)nqc + 1);
+  sl.counter.ensure(4);
+  if (!sl.pinned) FPP_CUDA(cudaMallocHost(&sl.pinned, 64));
+  if (!sl.ev_probe) FPP_CUDA(cudaEventCreateWithFlags(&sl.ev_probe, cudaEventDisableTiming));
 
   cudaEvent_t e0;
-  ix.timer.begin(PH_QHASH, s, &e0);
-  launch_query_lists(ix, Qd, nqc, scap, ix.q_vals.p, ix.q_codes.p, s, lstride);
-  ix.timer.end(PH_QHASH, e0, s);
+  ix.timer.begin(PH_QHASH, st, &e0);
+  launch_query_lists(ix, Qd, nqc, scap, sl.vals.p, sl.codes.p, st, lstride);
+  ix.timer.end(PH_QHASH, e0, st);
 
-  ix.timer.begin(PH_PROBE, s, &e0);
-  ProbeArgs pa{ix.q_vals.p, ix.q_codes.p, nqc, L, K, scap, ix.prm.D, ix.NB, peff, ix.offsets,
-               ix.table_base, ix.q_ppos.p, ix.q_plen.p, ix.q_eq.p, dbg_probes, nullptr, lstride, nullptr,
-               nullptr, nullptr, 0};
+  ix.timer.begin(PH_PROBE, st, &e0);
+  const uint32_t ccap = cand_cap(ix, qprobes);
+  ProbeArgs pa{sl.vals.p, sl.codes.p, nqc, L, K, scap, ix.prm.D, ix.NB, peff, ix.offsets,
+               ix.table_base, sl.ppos.p, sl.plen.p, sl.eq.p, dbg_probes, sl.gbuf.p, lstride,
+               nullptr, sl.ckey.p, sl.cpair.p, ccap};
   static const bool dbg_probe = getenv("FPP_DEBUG_PROBE") != nullptr;
   if (dbg_probe) {
-    ix.q_dbgclk.ensure((size_t)nqc * 8);
-    pa.dbg_clk = reinterpret_cast<long long*>(ix.q_dbgclk.p);
+    sl.dbgclk.ensure((size_t)nqc * 8);
+    pa.dbg_clk = reinterpret_cast<long long*>(sl.dbgclk.p);
   }
-  {
-    const uint32_t ccap = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(4 * peff + 4096, 16384),
-                                                       (uint64_t)L * K * scap * scap);
-    ix.q_ckey.ensure((size_t)nqc * ccap);
-    ix.q_cpair.ensure((size_t)nqc * ccap);
-    pa.ckey = ix.q_ckey.p;
-    pa.cpair = ix.q_cpair.p;
-    pa.ccap = ccap;
-    ix.q_gbuf.ensure((size_t)nqc * peff);
-    pa.gbuf = ix.q_gbuf.p;
-    k_probe_select<<<nqc, PS_THREADS, 0, s>>>(pa);
-  }
+  k_probe_select<<<nqc, PS_THREADS, 0, st>>>(pa);
+  FPP_LAUNCH();
   if (dbg_probe) {
     std::vector<long long> h((size_t)nqc * 8);
-    FPP_CUDA(cudaMemcpyAsync(h.data(), pa.dbg_clk, h.size() * 8, cudaMemcpyDeviceToHost, s));
-    FPP_CUDA(cudaStreamSynchronize(s));
+    FPP_CUDA(cudaMemcpyAsync(h.data(), pa.dbg_clk, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    FPP_CUDA(cudaStreamSynchronize(st));
     double acc[6] = {0}, it = 0, ti = 0;
     for (uint32_t i = 0; i < nqc; ++i) {
       for (int j = 0; j < 5; ++j) acc[j] += (double)(h[i * 8 + j + 1] - h[i * 8 + j]);
@@ -1051,20 +1072,26 @@ static void run_chunk(const Index& ix, const float* Qd, uint32_t nqc, uint32_t k
             "resolve %.0f | flat %.2f candidates %.1f\n", acc[0] / nqc, acc[1] / nqc, acc[2] / nqc,
             acc[3] / nqc, acc[4] / nqc, it / nqc, ti / nqc);
   }
+  k_scan_eq<<<1, 1024, 0, st>>>(sl.eq.p, nqc, sl.coff.p);
   FPP_LAUNCH();
-  k_scan_eq<<<1, 1024, 0, s>>>(ix.q_eq.p, nqc, ix.q_coff.p);
-  FPP_LAUNCH();
-  FPP_CUDA(cudaMemcpyAsync(ix.h_pinned, ix.q_coff.p + nqc, sizeof(uint64_t),
-                           cudaMemcpyDeviceToHost, s));
-  ix.timer.end(PH_PROBE, e0, s);
-  FPP_CUDA(cudaStreamSynchronize(s));
-  const uint64_t etot = ix.h_pinned[0];
-  ix.q_cands.ensure(etot + 1);
+  FPP_CUDA(cudaMemcpyAsync(sl.pinned, sl.coff.p + nqc, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  ix.timer.end(PH_PROBE, e0, st);
+  FPP_CUDA(cudaEventRecord(sl.ev_probe, st));
+}
 
-  ix.timer.begin(PH_COLLECT, s, &e0);
+// Stage B on stream `st` (after the host has read the slot's candidate total):
+// bucket walk + dedup, then row gather + fp64 dot + top-k.
+static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t nqc, uint32_t k,
+                    uint32_t qprobes, uint32_t* ids_d, double* scores_d,
+                    fpp_query_stats* stats_d, cudaStream_t st) {
+  const uint64_t peff = query_probes(ix, qprobes);
+  const uint64_t etot = sl.pinned[0];
+  sl.cands.ensure(etot + 1);
+  cudaEvent_t e0;
+  ix.timer.begin(PH_COLLECT, st, &e0);
   const uint32_t nwords = (uint32_t)((ix.n + 31) / 32);
-  CollectArgs ca{ix.q_ppos.p, ix.q_plen.p, peff, ix.ids, ix.q_coff.p, ix.q_cands.p, ix.q_uq.p,
-                 nqc, nwords, nullptr, ix.q_counter.p};
+  CollectArgs ca{sl.ppos.p, sl.plen.p, peff, ix.ids, sl.coff.p, sl.cands.p, sl.uq.p,
+                 nqc, nwords, nullptr, sl.counter.p};
   const size_t static_co = (CO_TILE + 1) * 4 + CO_TILE * 8 + 32 * 4 + 16;
   size_t co_smem = (size_t)nwords * 4;
   unsigned co_grid;
@@ -1079,32 +1106,32 @@ static void run_chunk(const Index& ix, const float* Qd, uint32_t nqc, uint32_t k
     co_smem = 0;
     co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * 2);
     const size_t need = (size_t)co_grid * nwords;
-    if (ix.q_bitmap.n < need) {
-      ix.q_bitmap.alloc(need);
-      FPP_CUDA(cudaMemsetAsync(ix.q_bitmap.p, 0, need * 4, s));
+    if (sl.bitmap.n < need) {
+      sl.bitmap.alloc(need);
+      FPP_CUDA(cudaMemsetAsync(sl.bitmap.p, 0, need * 4, st));
     }
-    ca.gbitmap = ix.q_bitmap.p;
+    ca.gbitmap = sl.bitmap.p;
   }
-  FPP_CUDA(cudaMemsetAsync(ix.q_counter.p, 0, sizeof(uint32_t), s));
-  k_collect<<<co_grid, CO_THREADS, co_smem, s>>>(ca);
+  FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
+  k_collect<<<co_grid, CO_THREADS, co_smem, st>>>(ca);
   FPP_LAUNCH();
-  ix.timer.end(PH_COLLECT, e0, s);
+  ix.timer.end(PH_COLLECT, e0, st);
 
-  ix.timer.begin(PH_SCORE, s, &e0);
-  ScoreArgs sa{ix.X, ix.d, Qd, ix.q_coff.p, ix.q_cands.p, ix.q_uq.p, ix.q_eq.p, peff, k,
+  ix.timer.begin(PH_SCORE, st, &e0);
+  ScoreArgs sa{ix.X, ix.d, Qd, sl.coff.p, sl.cands.p, sl.uq.p, sl.eq.p, peff, k,
                ix.prm.id_offset, ids_d, scores_d, stats_d};
   const size_t sc_smem = score_smem(ix.d);
   if ((ix.d & 3u) == 0) {
     FPP_CUDA(cudaFuncSetAttribute(k_score<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sc_smem));
-    k_score<true><<<nqc, SC_WARPS * 32, sc_smem, s>>>(sa);
+    k_score<true><<<nqc, SC_WARPS * 32, sc_smem, st>>>(sa);
   } else {
     FPP_CUDA(cudaFuncSetAttribute(k_score<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sc_smem));
-    k_score<false><<<nqc, SC_WARPS * 32, sc_smem, s>>>(sa);
+    k_score<false><<<nqc, SC_WARPS * 32, sc_smem, st>>>(sa);
   }
   FPP_LAUNCH();
-  ix.timer.end(PH_SCORE, e0, s);
+  ix.timer.end(PH_SCORE, e0, st);
   ix.acc.launches += 5;  // lists, probe_select, scan_eq, collect, score
   ix.acc.probes += peff * nqc;
 }
@@ -1113,19 +1140,74 @@ static uint32_t chunk_size(const Index& ix, uint32_t qprobes, uint64_t nq) {
   const uint64_t LKs = (uint64_t)ix.prm.L * ix.prm.K * query_cap(ix, qprobes);
   const uint64_t pe = query_probes(ix, qprobes);
   const uint64_t per_q = LKs * 8 + pe * 16 + (4 * pe + 16384) * 8 + 64;
-  uint64_t c = (1ull << 31) / per_q;  // ~2 GB of per-chunk scratch
-  c = std::max<uint64_t>(1, std::min<uint64_t>(c, 16384));
+  uint64_t c = (1ull << 30) / per_q;  // ~1 GB of per-chunk scratch per slot
+  c = std::max<uint64_t>(1, std::min<uint64_t>(c, 8192));
+  // at least 4 chunks when the batch allows, so the two-stream pipeline overlaps
+  const uint64_t quarter = (nq + 3) / 4;
+  if (quarter >= 512) c = std::min(c, quarter);
   return (uint32_t)std::min<uint64_t>(c, nq);
 }
 
+// Two-stream software pipeline over query chunks: stage A (ALU/latency bound:
+// hashing + probe selection) runs on a low-priority stream, stage B (HBM bound:
+// collect + gather/score) on a high-priority one, so the scheduler hands freed
+// SM slots to the bandwidth-bound kernel first and fills the rest with stage A
+// of the next chunk.  Slots alternate; events order slot reuse.
 void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t qprobes,
                uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s) {
   const uint32_t cs = chunk_size(ix, qprobes, nq);
-  for (uint64_t q0 = 0; q0 < nq; q0 += cs) {
-    const uint32_t nqc = (uint32_t)std::min<uint64_t>(cs, nq - q0);
-    run_chunk(ix, Qd + q0 * ix.d, nqc, k, qprobes, ids_d + q0 * k, scores_d + q0 * k,
-              stats_d ? stats_d + q0 : nullptr, s, nullptr);
+  const uint64_t nch = (nq + cs - 1) / cs;
+  static const bool serial = getenv("FPP_SERIAL") != nullptr;
+  if (serial) {  // single-stream order (per-kernel timing without overlap)
+    for (uint64_t c = 0; c < nch; ++c) {
+      const uint64_t q0 = c * cs;
+      const uint32_t n = (uint32_t)std::min<uint64_t>(cs, nq - q0);
+      stage_a(ix, ix.slot[0], Qd + q0 * ix.d, n, qprobes, s, nullptr);
+      FPP_CUDA(cudaEventSynchronize(ix.slot[0].ev_probe));
+      stage_b(ix, ix.slot[0], Qd + q0 * ix.d, n, k, qprobes, ids_d + q0 * k, scores_d + q0 * k,
+              stats_d ? stats_d + q0 : nullptr, s);
+    }
+    return;
   }
+  if (!ix.sA) {
+    int lo = 0, hi = 0;
+    FPP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sA, cudaStreamNonBlocking, lo));
+    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sB, cudaStreamNonBlocking, hi));
+    FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_fork, cudaEventDisableTiming));
+    FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_join, cudaEventDisableTiming));
+    FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_join2, cudaEventDisableTiming));
+    for (auto& sl : ix.slot) FPP_CUDA(cudaEventCreateWithFlags(&sl.ev_bdone, cudaEventDisableTiming));
+  }
+  prepare_slot(ix, ix.slot[0], cs, qprobes);
+  prepare_slot(ix, ix.slot[1], cs, qprobes);
+  FPP_CUDA(cudaEventRecord(ix.ev_fork, s));
+  FPP_CUDA(cudaStreamWaitEvent(ix.sA, ix.ev_fork, 0));
+  FPP_CUDA(cudaStreamWaitEvent(ix.sB, ix.ev_fork, 0));
+  auto issue_a = [&](uint64_t c) {
+    Index::QSlot& sl = ix.slot[c & 1];
+    if (c >= 2) FPP_CUDA(cudaStreamWaitEvent(ix.sA, sl.ev_bdone, 0));  // slot free again
+    const uint64_t q0 = c * cs;
+    const uint32_t n = (uint32_t)std::min<uint64_t>(cs, nq - q0);
+    stage_a(ix, sl, Qd + q0 * ix.d, n, qprobes, ix.sA, nullptr);
+  };
+  issue_a(0);
+  if (nch > 1) issue_a(1);
+  for (uint64_t c = 0; c < nch; ++c) {
+    Index::QSlot& sl = ix.slot[c & 1];
+    FPP_CUDA(cudaEventSynchronize(sl.ev_probe));
+    FPP_CUDA(cudaStreamWaitEvent(ix.sB, sl.ev_probe, 0));
+    const uint64_t q0 = c * cs;
+    const uint32_t n = (uint32_t)std::min<uint64_t>(cs, nq - q0);
+    stage_b(ix, sl, Qd + q0 * ix.d, n, k, qprobes, ids_d + q0 * k, scores_d + q0 * k,
+            stats_d ? stats_d + q0 : nullptr, ix.sB);
+    FPP_CUDA(cudaEventRecord(sl.ev_bdone, ix.sB));
+    if (c + 2 < nch) issue_a(c + 2);
+  }
+  FPP_CUDA(cudaEventRecord(ix.ev_join, ix.sA));
+  FPP_CUDA(cudaEventRecord(ix.ev_join2, ix.sB));
+  FPP_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
+  FPP_CUDA(cudaStreamWaitEvent(s, ix.ev_join2, 0));
 }
 
 void query_debug(const Index& ix, const float* qd, uint32_t qprobes, std::vector<uint64_t>& probes,
@@ -1135,16 +1217,19 @@ void query_debug(const Index& ix, const float* qd, uint32_t qprobes, std::vector
   DBuf<uint64_t> dbg(peff);
   DBuf<uint32_t> ids(32);
   DBuf<double> sc(32);
-  run_chunk(ix, qd, 1, 1, qprobes, ids.p, sc.p, nullptr, s, dbg.p);
+  Index::QSlot& sl = ix.slot[0];
+  stage_a(ix, sl, qd, 1, qprobes, s, dbg.p);
+  FPP_CUDA(cudaEventSynchronize(sl.ev_probe));
+  stage_b(ix, sl, qd, 1, 1, qprobes, ids.p, sc.p, nullptr, s);
   FPP_CUDA(cudaStreamSynchronize(s));
   probes.resize(peff);
   FPP_CUDA(cudaMemcpy(probes.data(), dbg.p, peff * 8, cudaMemcpyDeviceToHost));
   uint32_t U = 0;
   uint64_t off = 0;
-  FPP_CUDA(cudaMemcpy(&U, ix.q_uq.p, 4, cudaMemcpyDeviceToHost));
-  FPP_CUDA(cudaMemcpy(&off, ix.q_coff.p, 8, cudaMemcpyDeviceToHost));
+  FPP_CUDA(cudaMemcpy(&U, sl.uq.p, 4, cudaMemcpyDeviceToHost));
+  FPP_CUDA(cudaMemcpy(&off, sl.coff.p, 8, cudaMemcpyDeviceToHost));
   cands.resize(U);
-  if (U) FPP_CUDA(cudaMemcpy(cands.data(), ix.q_cands.p + off, (size_t)U * 4, cudaMemcpyDeviceToHost));
+  if (U) FPP_CUDA(cudaMemcpy(cands.data(), sl.cands.p + off, (size_t)U * 4, cudaMemcpyDeviceToHost));
   std::sort(probes.begin(), probes.end());
   std::sort(cands.begin(), cands.end());
 }
