@@ -185,11 +185,11 @@ static int cmp_opp(const void* x, const void* y) {  /* |p| asc, i asc */
 
 /*
  * Ranked signed list of one cross-polytope function (SPEC.md:184-201 with the
- * DESIGN.md section 3 pin): the D "natural" signed vectors sign(p_i) r_i in
- * (|p| desc, i asc) order with value +|p_i|, followed by the D opposite
- * vectors -sign(p_i) r_i in (|p| asc, i asc) order with value -|p_i|.  The
- * list is non-increasing in value; entry 0 is cross_polytope_hash.  Only the
- * first r <= 2D entries are produced.
+ * DESIGN.md section 3 pin): the D "natural" signed vectors sign(p_i) r_i
+ * (closest / furthest) in (|p| desc, i asc) order, value
+ * |p_i|, followed -- only when r > D -- by the opposite-signed vectors
+ * -sign(p_i) r_i in the same order and with the same value |p_i|.  Entry 0 is
+ * cross_polytope_hash.  Ranks D.. are the opposite part.
  */
 void orc_rank(const float* p, uint32_t D, uint32_t r, float* vals, uint32_t* codes) {
   const uint32_t rn = r < D ? r : D;
@@ -218,20 +218,19 @@ void orc_rank(const float* p, uint32_t D, uint32_t r, float* vals, uint32_t* cod
     vals[k] = tmp[k].a;
     codes[k] = p[i] >= 0.0f ? i : D + i;
   }
-  if (r > D) {
-    qsort(tmp, D, sizeof(absidx), cmp_opp);
+  if (r > D) {  /* opposite-signed vectors: same (|p| desc, i asc) order, flipped code */
     for (uint32_t k = 0; k < r - D; ++k) {
       const uint32_t i = tmp[k].i;
-      vals[D + k] = -fabsf(p[i]);
+      vals[D + k] = tmp[k].a;
       codes[D + k] = p[i] >= 0.0f ? D + i : i;
     }
   }
   free(tmp);
 }
 
-typedef struct { float s; uint32_t r1, r2, t; } pairkey;
+typedef struct { float s; uint32_t r1, r2, t, g, a, b; } pairkey;
 
-/* pair total order: score desc, r1 asc, r2 asc, t asc */
+/* pair order within a class: score desc, r1 asc, r2 asc, t asc */
 static int pair_better(const pairkey* a, const pairkey* b) {
   if (a->s != b->s) return a->s > b->s;
   if (a->r1 != b->r1) return a->r1 < b->r1;
@@ -239,44 +238,147 @@ static int pair_better(const pairkey* a, const pairkey* b) {
   return a->t < b->t;
 }
 
+/* binary max-heap on pair_better */
+static void heap_push(pairkey* h, uint64_t* n, pairkey k) {
+  uint64_t i = (*n)++;
+  while (i > 0) {
+    uint64_t p = (i - 1) / 2;
+    if (!pair_better(&k, &h[p])) break;
+    h[i] = h[p];
+    i = p;
+  }
+  h[i] = k;
+}
+static pairkey heap_pop(pairkey* h, uint64_t* n) {
+  pairkey top = h[0], last = h[--(*n)];
+  uint64_t i = 0;
+  for (;;) {
+    uint64_t c = 2 * i + 1;
+    if (c >= *n) break;
+    if (c + 1 < *n && pair_better(&h[c + 1], &h[c])) ++c;
+    if (!pair_better(&h[c], &last)) break;
+    h[i] = h[c];
+    i = c;
+  }
+  if (*n) h[i] = last;
+  return top;
+}
+
+static const float k_zero_val[1] = {0.0f};
+static const uint32_t k_zero_code[1] = {0u};
+
+typedef struct {
+  const float* va; const float* vb;
+  const uint32_t* ca; const uint32_t* cb;
+  uint32_t na, nb, oa, ob, t;
+} grid;
+
 /*
- * SPEC.md:184-192 index_probe_sequence: top-iProbes pairs of the two ranked
- * lists by fl(v1+v2).  Pairs beyond rank iProbes in either list can never
- * enter the top iProbes (the key is monotone in both ranks), so r=min(ip,2D).
+ * Class-ordered enumeration of (t, r1, r2) pairs of L tables' ranked lists
+ * vals/codes [L][K][s]:
+ *   class 0: natural x natural, class 1: exactly one opposite-signed entry,
+ *   class 2: both opposite; inside a class (fl(v1+v2) desc, r1, r2, t).
+ * Each (table, part-combination) is a grid sorted in both ranks, so a
+ * best-first heap over the grids' frontiers yields the exact order.  Emits up
+ * to `limit` pairs (bucket t*NB + b, score); skip_forced drops every table's
+ * class-0 (0,0) (the true bucket, handled by the caller).
+ */
+static uint64_t enum_pairs(const float* vals, const uint32_t* codes, uint32_t L, uint32_t K,
+                           uint32_t D, uint32_t s, uint64_t NB, uint64_t limit, int skip_forced,
+                           uint64_t* out_b, float* out_s) {
+  const uint32_t n = s < D ? s : D, o = s > D ? s - D : 0;
+  grid* G = (grid*)malloc((size_t)L * 2 * sizeof(grid));
+  pairkey* heap = (pairkey*)malloc((size_t)(2 * limit + 4 * L + 4) * sizeof(pairkey));
+  uint64_t emitted = 0;
+  const int ncls = K == 2 ? 3 : 2;
+  for (int cls = 0; cls < ncls && emitted < limit; ++cls) {
+    uint32_t ng = 0;
+    for (uint32_t t = 0; t < L; ++t) {
+      const float* v1 = vals + ((uint64_t)t * K) * s;
+      const uint32_t* c1 = codes + ((uint64_t)t * K) * s;
+      const float* v2 = K == 2 ? v1 + s : k_zero_val;
+      const uint32_t* c2 = K == 2 ? c1 + s : k_zero_code;
+      const uint32_t n2 = K == 2 ? n : 1, o2 = K == 2 ? o : 0;
+      /* parts: (start, len, rank offset) natural = (0, n, 0), opposite = (D, o, D) */
+      uint32_t pa[2][3] = {{0, n, 0}, {D, o, D}};
+      uint32_t pb[2][3] = {{0, n2, 0}, {D, o2, D}};
+      int combos[2][2];
+      int nc = 0;
+      if (cls == 0) { combos[nc][0] = 0; combos[nc][1] = 0; ++nc; }
+      if (cls == 1) {
+        combos[nc][0] = 0; combos[nc][1] = 1; ++nc;
+        combos[nc][0] = 1; combos[nc][1] = 0; ++nc;
+      }
+      if (cls == 2) { combos[nc][0] = 1; combos[nc][1] = 1; ++nc; }
+      for (int ci = 0; ci < nc; ++ci) {
+        const int A = combos[ci][0], B = combos[ci][1];
+        if (K == 1 && B == 1) continue;
+        grid g;
+        g.va = v1 + pa[A][0]; g.ca = c1 + pa[A][0]; g.na = pa[A][1]; g.oa = pa[A][2];
+        g.vb = v2 + (K == 2 ? pb[B][0] : 0); g.cb = c2 + (K == 2 ? pb[B][0] : 0);
+        g.nb = pb[B][1]; g.ob = K == 2 ? pb[B][2] : 0; g.t = t;
+        if (g.na == 0 || g.nb == 0) continue;
+        G[ng++] = g;
+      }
+    }
+    uint64_t hn = 0;
+    for (uint32_t gi = 0; gi < ng; ++gi) {
+      const grid* g = &G[gi];
+      if (cls == 0 && skip_forced) {
+        if (g->nb > 1) {
+          pairkey k = {g->va[0] + g->vb[1], g->oa, g->ob + 1, g->t, gi, 0, 1};
+          heap_push(heap, &hn, k);
+        }
+        if (g->na > 1) {
+          pairkey k = {g->va[1] + g->vb[0], g->oa + 1, g->ob, g->t, gi, 1, 0};
+          heap_push(heap, &hn, k);
+        }
+      } else {
+        pairkey k = {g->va[0] + g->vb[0], g->oa, g->ob, g->t, gi, 0, 0};
+        heap_push(heap, &hn, k);
+      }
+    }
+    while (emitted < limit && hn) {
+      const pairkey k = heap_pop(heap, &hn);
+      const grid* g = &G[k.g];
+      const uint32_t b = K == 2 ? g->ca[k.a] * (2 * D) + g->cb[k.b] : g->ca[k.a];
+      out_b[emitted] = (uint64_t)g->t * NB + b;
+      if (out_s) out_s[emitted] = k.s;
+      ++emitted;
+      if (k.b + 1 < g->nb) {
+        pairkey c = {g->va[k.a] + g->vb[k.b + 1], g->oa + k.a, g->ob + k.b + 1, g->t, k.g, k.a, k.b + 1};
+        heap_push(heap, &hn, c);
+      }
+      if (k.b == 0 && k.a + 1 < g->na) {
+        pairkey c = {g->va[k.a + 1] + g->vb[0], g->oa + k.a + 1, g->ob, g->t, k.g, k.a + 1, 0};
+        heap_push(heap, &hn, c);
+      }
+    }
+  }
+  free(G);
+  free(heap);
+  return emitted;
+}
+
+/*
+ * SPEC.md:184-192 index_probe_sequence: the top-iProbes pairs of the point's
+ * ranked lists in the class-ordered total order (the first is the true bucket).
+ * Top pairs of a sorted grid lie within the first iProbes ranks, so lists of
+ * r = min(iProbes, 2D) entries suffice.
  */
 void orc_index_probes(const float* proj, uint32_t K, uint32_t D, uint32_t iprobes,
                       uint32_t* buckets, float* scores) {
   const uint32_t r = iprobes < 2 * D ? iprobes : 2 * D;
-  float v1[64], v2[64];
-  uint32_t c1[64], c2[64];
-  float* V1 = r <= 64 ? v1 : (float*)malloc(r * sizeof(float));
-  uint32_t* C1 = r <= 64 ? c1 : (uint32_t*)malloc(r * sizeof(uint32_t));
-  orc_rank(proj, D, r, V1, C1);
-  if (K == 1) {
-    for (uint32_t k = 0; k < iprobes; ++k) { buckets[k] = C1[k]; scores[k] = V1[k]; }
-  } else {
-    float* V2 = r <= 64 ? v2 : (float*)malloc(r * sizeof(float));
-    uint32_t* C2 = r <= 64 ? c2 : (uint32_t*)malloc(r * sizeof(uint32_t));
-    orc_rank(proj + D, D, r, V2, C2);
-    /* selection of the top iprobes of r*r pairs */
-    pairkey* best = (pairkey*)malloc((size_t)iprobes * sizeof(pairkey));
-    uint32_t cnt = 0;
-    for (uint32_t a = 0; a < r; ++a)
-      for (uint32_t b = 0; b < r; ++b) {
-        pairkey k = {V1[a] + V2[b], a, b, 0};
-        if (cnt == iprobes && !pair_better(&k, &best[iprobes - 1])) continue;
-        uint32_t pos = cnt < iprobes ? cnt++ : iprobes - 1;
-        while (pos > 0 && pair_better(&k, &best[pos - 1])) { best[pos] = best[pos - 1]; --pos; }
-        best[pos] = k;
-      }
-    for (uint32_t k = 0; k < iprobes; ++k) {
-      buckets[k] = C1[best[k].r1] * (2 * D) + C2[best[k].r2];
-      scores[k] = best[k].s;
-    }
-    free(best);
-    if (V2 != v2) { free(V2); free(C2); }
-  }
-  if (V1 != v1) { free(V1); free(C1); }
+  float* V = (float*)malloc((size_t)K * r * sizeof(float));
+  uint32_t* Cc = (uint32_t*)malloc((size_t)K * r * sizeof(uint32_t));
+  uint64_t* ob = (uint64_t*)malloc((size_t)iprobes * sizeof(uint64_t));
+  for (uint32_t f = 0; f < K; ++f) orc_rank(proj + (uint64_t)f * D, D, r, V + f * r, Cc + f * r);
+  const uint64_t NB = K == 2 ? 4ull * D * D : 2ull * D;
+  enum_pairs(V, Cc, 1, K, D, r, NB, iprobes, 0, ob, scores);
+  for (uint32_t k = 0; k < iprobes; ++k) buckets[k] = (uint32_t)ob[k];
+  free(V);
+  free(Cc);
+  free(ob);
 }
 
 void orc_cp_hash_rows(const float* proj, uint64_t n, uint32_t D, uint32_t* out) {
@@ -312,7 +414,11 @@ static int cmp_entry(const void* x, const void* y) {  /* score desc, id asc */
 }
 
 /* SPEC.md:257 + SURVEY 8(c): min(B, max(kappa, floor(double(alpha)*B/iProbes))) */
+uint32_t orc_keep_count(uint32_t B, float alpha, uint32_t iprobes, uint32_t kappa);
 static uint32_t keep_count(uint32_t B, float alpha, uint32_t iprobes, uint32_t kappa) {
+  return orc_keep_count(B, alpha, iprobes, kappa);
+}
+uint32_t orc_keep_count(uint32_t B, float alpha, uint32_t iprobes, uint32_t kappa) {
   double f = floor((double)alpha * (double)B / (double)iprobes);
   uint64_t k = (uint64_t)f;
   if (k < kappa) k = kappa;
@@ -519,83 +625,32 @@ void orc_query_lists(const orc_index* idx, const float* q, uint32_t s, float* va
   free(buf);
 }
 
-/* binary max-heap on pair_better */
-static void heap_push(pairkey* h, uint64_t* n, pairkey k) {
-  uint64_t i = (*n)++;
-  while (i > 0) {
-    uint64_t p = (i - 1) / 2;
-    if (!pair_better(&k, &h[p])) break;
-    h[i] = h[p];
-    i = p;
-  }
-  h[i] = k;
-}
-static pairkey heap_pop(pairkey* h, uint64_t* n) {
-  pairkey top = h[0], last = h[--(*n)];
-  uint64_t i = 0;
-  for (;;) {
-    uint64_t c = 2 * i + 1;
-    if (c >= *n) break;
-    if (c + 1 < *n && pair_better(&h[c + 1], &h[c])) ++c;
-    if (!pair_better(&h[c], &last)) break;
-    h[i] = h[c];
-    i = c;
-  }
-  if (*n) h[i] = last;
-  return top;
-}
-
 /*
  * SPEC.md:193-201 query_probe_sequence (DESIGN.md section 3 pin): the L true
- * buckets, then the best P_eff-L remaining (t,r1,r2) by (fl(v1+v2) desc, r1,
- * r2, t), enumerated best-first over the per-table sorted grids.
- * Writes probes as t*NB+bucket (unsorted), returns count.
+ * buckets, then the best P_eff - L remaining pairs in the class-ordered total
+ * order.  Writes probes as t*NB+bucket (unsorted), returns the count.
  */
 static uint64_t probe_set(const orc_index* idx, const float* vals, const uint32_t* codes,
-                          uint32_t s, uint64_t peff, uint64_t* probes, pairkey* heap) {
+                          uint32_t s, uint64_t peff, uint64_t* probes, pairkey* heap_unused) {
+  (void)heap_unused;
   const uint32_t L = idx->p.L, K = idx->p.K, D = idx->p.D;
   const uint64_t NB = idx->NB;
-  uint64_t np = 0, hn = 0;
-#define V(t, f, r) vals[((uint64_t)(t) * K + (f)) * s + (r)]
-#define C(t, f, r) codes[((uint64_t)(t) * K + (f)) * s + (r)]
   for (uint32_t t = 0; t < L; ++t) {
-    probes[np++] = t * NB + (K == 2 ? (uint64_t)C(t, 0, 0) * 2 * D + C(t, 1, 0) : C(t, 0, 0));
-    if (K == 2) {
-      if (s > 1) {
-        pairkey a = {V(t, 0, 0) + V(t, 1, 1), 0, 1, t};
-        pairkey b = {V(t, 0, 1) + V(t, 1, 0), 1, 0, t};
-        heap_push(heap, &hn, a);
-        heap_push(heap, &hn, b);
-      }
-    } else if (s > 1) {
-      pairkey a = {V(t, 0, 1), 1, 0, t};
-      heap_push(heap, &hn, a);
-    }
+    const uint32_t* c1 = codes + ((uint64_t)t * K) * s;
+    probes[t] = t * NB + (K == 2 ? (uint64_t)c1[0] * 2 * D + c1[s] : c1[0]);
   }
-  while (np < peff && hn) {
-    pairkey k = heap_pop(heap, &hn);
-    const uint32_t t = k.t;
-    if (K == 2) {
-      probes[np++] = t * NB + (uint64_t)C(t, 0, k.r1) * 2 * D + C(t, 1, k.r2);
-      if (k.r2 + 1 < s) {
-        pairkey c = {V(t, 0, k.r1) + V(t, 1, k.r2 + 1), k.r1, k.r2 + 1, t};
-        heap_push(heap, &hn, c);
-      }
-      if (k.r2 == 0 && k.r1 + 1 < s) {
-        pairkey c = {V(t, 0, k.r1 + 1) + V(t, 1, 0), k.r1 + 1, 0, t};
-        heap_push(heap, &hn, c);
-      }
-    } else {
-      probes[np++] = t * NB + C(t, 0, k.r1);
-      if (k.r1 + 1 < s) {
-        pairkey c = {V(t, 0, k.r1 + 1), k.r1 + 1, 0, t};
-        heap_push(heap, &hn, c);
-      }
-    }
-  }
-#undef V
-#undef C
-  return np;
+  return L + enum_pairs(vals, codes, L, K, D, s, NB, peff - L, 1, probes + L, NULL);
+}
+
+uint64_t orc_probe_set_lists(const float* vals, const uint32_t* codes, uint32_t L, uint32_t K,
+                             uint32_t D, uint32_t s, uint64_t peff, uint64_t* probes) {
+  orc_index tmp;
+  memset(&tmp, 0, sizeof(tmp));
+  tmp.p.L = L;
+  tmp.p.K = K;
+  tmp.p.D = D;
+  tmp.NB = K == 2 ? 4u * D * D : 2u * D;
+  return probe_set(&tmp, vals, codes, s, peff, probes, NULL);
 }
 
 typedef struct { double s; uint32_t id; } scored;

@@ -75,6 +75,12 @@ void orc_rank(const float* p, uint32_t D, uint32_t r, float* vals, uint32_t* cod
 void orc_index_probes(const float* proj, uint32_t K, uint32_t D, uint32_t iprobes,
                       uint32_t* buckets, float* scores);
 
+/* SPEC.md:257 keep count of a bucket of pre-filter size B */
+uint32_t orc_keep_count(uint32_t B, float alpha, uint32_t iprobes, uint32_t kappa);
+/* probe set (t*NB + bucket, unsorted) from explicit ranked lists [L][K][s] */
+uint64_t orc_probe_set_lists(const float* vals, const uint32_t* codes, uint32_t L, uint32_t K,
+                             uint32_t D, uint32_t s, uint64_t peff, uint64_t* probes);
+
 /* index build */
 orc_index* orc_build(const float* X, uint64_t n, uint32_t d, const orc_params* prm,
                      int threads, uint32_t t_begin, uint32_t t_end);

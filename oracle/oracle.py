@@ -70,6 +70,11 @@ def lib():
                                          u32p, f32p, u64p]
         L.orc_synth.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_float, C.c_uint64,
                                 C.c_uint32, C.c_int]
+        L.orc_keep_count.restype = C.c_uint32
+        L.orc_keep_count.argtypes = [C.c_uint32, C.c_float, C.c_uint32, C.c_uint32]
+        L.orc_probe_set_lists.restype = C.c_uint64
+        L.orc_probe_set_lists.argtypes = [f32p, u32p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          C.c_uint32, C.c_uint64, u64p]
         L.orc_normalize.restype = C.c_int64
         L.orc_normalize.argtypes = [f32p, C.c_uint64, C.c_uint32]
         L.orc_inner_product.restype = C.c_double
@@ -251,6 +256,20 @@ class Index:
         codes = np.empty(self.L * self.K * s, np.uint32)
         lib().orc_query_lists(self.h, q, s, vals, codes)
         return vals.reshape(self.L, self.K, s), codes.reshape(self.L, self.K, s)
+
+
+def keep_count(B: int, alpha: float, iprobes: int, kappa: int) -> int:
+    return lib().orc_keep_count(B, alpha, iprobes, kappa)
+
+
+def probe_set_lists(vals: np.ndarray, codes: np.ndarray, D: int, peff: int) -> np.ndarray:
+    """vals/codes [L][K][s] -> probe ids t*NB + bucket (sorted)."""
+    vals = np.ascontiguousarray(vals, dtype=np.float32)
+    codes = np.ascontiguousarray(codes, dtype=np.uint32)
+    L, K, s = vals.shape
+    out = np.empty(peff + L, np.uint64)
+    n = lib().orc_probe_set_lists(vals.reshape(-1), codes.reshape(-1), L, K, D, s, peff, out)
+    return np.sort(out[:n])
 
 
 def brute_force(X: np.ndarray, Q: np.ndarray, k: int, threads: int = 0):

@@ -37,7 +37,8 @@ namespace fpp {
 // (22-bit truncated rank value | 10-bit index) -- half the shuffles and a third
 // of the ALU work of 64-bit keys -- followed by an exact fix-up of the rare runs
 // whose truncated values collide, so the emitted order is exactly
-// (|p| desc, j asc) (then, when s > D, the opposite tail (|p| asc, j asc)).
+// (|p| desc, j asc).  When s > D the opposite-signed vectors follow in the same
+// order with flipped codes.
 template <bool NAT>
 __device__ __forceinline__ bool rank_before(float pa, uint32_t ja, float pb, uint32_t jb) {
   const float a = fabsf(pa), b = fabsf(pb);
@@ -121,21 +122,12 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
       codes[ob + r] = p < 0.0f ? D + j : j;
     }
   }
-  if (s > D) {  // opposite signed vectors: (|p| asc, j asc), value -|p|
-    __syncwarp();
-#pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const uint32_t j = (uint32_t)g * EPT + e;
-      kk[e] = j < D ? ((ord_key(fabsf(v[e])) & 0xfffffc00u) | j) : 0xffffffffu;
-    }
-    rank_sort_exact<P, EPT, false>(kk, g, sk, pv);
-    if (active) {
-      for (uint32_t r = g; r < s - D; r += S::G) {
-        const uint32_t j = sk[r] & 1023u;
-        const float p = pv[j];
-        vals[ob + D + r] = -fabsf(p);
-        codes[ob + D + r] = p < 0.0f ? j : D + j;
-      }
+  if (s > D && active) {  // opposite-signed vectors: same order, value |p|, flipped code
+    for (uint32_t r = g; r < s - D; r += S::G) {
+      const uint32_t j = sk[r] & 1023u;
+      const float p = pv[j];
+      vals[ob + D + r] = fabsf(p);
+      codes[ob + D + r] = p < 0.0f ? j : D + j;
     }
   }
 }
@@ -261,9 +253,11 @@ __device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t* sh) {
 // SM; the emitted bucket ids are collected in shared memory and resolved
 // against the CSR directory by a flat, unrolled loop (8 independent loads in
 // flight per thread).
-// non-forced pairs >= T among rows [rb, re) (corner walk on a row block)
+// pairs >= T among rows [rb, re) of a grid (corner walk on a row block);
+// `forced` grids exclude their (0,0) (the true bucket, emitted separately)
 __device__ __forceinline__ uint32_t walk_count_rows(const float* v1, const float* v2, uint32_t S2,
-                                                    uint32_t rb, uint32_t re, uint32_t T) {
+                                                    uint32_t rb, uint32_t re, uint32_t T,
+                                                    bool forced = true) {
   if (rb >= re) return 0;
   uint32_t p = prefix_bs(v1[rb], v2, S2, T);
   if (p == 0) return 0;
@@ -276,7 +270,7 @@ __device__ __forceinline__ uint32_t walk_count_rows(const float* v1, const float
     if (p == 0) break;
     r1 = e;
   }
-  return rb == 0 ? c - 1 : c;  // exclude the forced (0,0)
+  return (rb == 0 && forced) ? c - 1 : c;
 }
 
 // visit (r1, pa, pb) for rows [rb, re) while pb > 0 (prefixes at Ta > Tb)
@@ -300,16 +294,30 @@ __device__ __forceinline__ void walk2_rows(const float* v1, const float* v2, uin
   }
 }
 
+// A "grid" is one (table, list-part x list-part) block of pairs, sorted in
+// both ranks: class 0 = natural x natural (one per table, its (0,0) is the
+// forced true bucket), class 1 = natural x opposite and opposite x natural,
+// class 2 = opposite x opposite.  Classes are taken in
+// order; only the last needed class goes through selection.
+struct GridRef {
+  const float* va;
+  const float* vb;
+  uint32_t na, nb;   // extents
+  uint32_t oa, ob;   // rank offsets (0 natural, D opposite)
+  uint32_t t;
+  bool forced;
+};
+
 // CTA per query (PS_THREADS threads, ~13 KB shared memory, so several query
-// CTAs share an SM and hide each other's latency).
-//  1. radix-select the M-th best key among the L-shape "arm" pairs (row 0 and
-//     column 0 of every table): a subset, so that key T_lo <= T*;
-//  2. one staircase walk materialises every non-forced pair >= T_lo (key +
-//     packed (t, r1, r2)) into per-query global scratch;
+// CTAs share an SM and hide each other's latency).  For the selection class:
+//  1. radix-select the m-th best key among the "arm" pairs (row 0 and column 0
+//     of every grid): a subset, so that key T_lo <= T*;
+//  2. one staircase walk materialises every pair >= T_lo (key + packed
+//     (t, r1, r2)) into per-query global scratch;
 //  3. radix-select T* over that flat array (balanced, coalesced passes);
 //  4. count / collect ties at T*, pick the (r1, r2, t)-smallest ones;
-//  5. compact the selected pairs into bucket ids, resolve them against the CSR
-//     directory with 8 independent loads per thread in flight.
+//  5. compact the selected pairs into bucket ids, then resolve every probe
+//     against the CSR directory with 8 independent loads per thread in flight.
 // If the candidate set overflows the scratch, every pass re-walks instead.
 __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
   __shared__ uint64_t red[PS_THREADS / 32];
@@ -319,8 +327,8 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
   long long ck[8];
   ck[0] = clock64();
   const uint32_t q = blockIdx.x;
-  const uint32_t L = a.L, K = a.K, s = a.s;
-  const uint32_t S2 = K == 2 ? s : 1;
+  const uint32_t L = a.L, K = a.K, s = a.s, D = a.D;
+  const uint32_t n = s < D ? s : D, o = s > D ? s - D : 0;
   const float* V = a.vals + (uint64_t)q * a.lstride;
   const uint32_t* Cq = a.codes + (uint64_t)q * a.lstride;
   uint32_t* ckey = a.ckey + (uint64_t)q * a.ccap;
@@ -331,18 +339,49 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
   }
   __syncthreads();
   ck[1] = clock64();
-  auto V1 = [&](uint32_t t) { return V + (uint64_t)t * K * s; };
-  auto V2 = [&](uint32_t t) { return K == 2 ? V + (uint64_t)t * K * s + s : g_zero_row; };
-  const uint32_t TPT = L < blockDim.x ? blockDim.x / L : 1;
-  const uint32_t RB = (s + TPT - 1) / TPT;
-  const uint32_t units = L * TPT;
-  auto unit = [&](uint32_t u, uint32_t& t, uint32_t& rb, uint32_t& re) {
-    t = u / TPT;
-    const uint32_t part = u - t * TPT;
-    rb = min(s, part * RB);
-    re = min(s, rb + RB);
+  auto ngrids = [&](uint32_t cls) -> uint32_t { return (K == 2 && cls == 1) ? 2 * L : L; };
+  auto grid = [&](uint32_t cls, uint32_t gi) -> GridRef {
+    GridRef g;
+    const uint32_t t = (K == 2 && cls == 1) ? gi >> 1 : gi;
+    const float* v1 = V + (uint64_t)t * K * s;
+    const float* v2 = K == 2 ? v1 + s : g_zero_row;
+    const uint32_t n2 = K == 2 ? n : 1;
+    g.t = t;
+    g.forced = cls == 0;
+    bool a_opp = false, b_opp = false;
+    if (cls == 1) {
+      if (K == 2) { a_opp = gi & 1; b_opp = !a_opp; }
+      else a_opp = true;
+    }
+    if (cls == 2) a_opp = b_opp = true;
+    g.va = v1 + (a_opp ? D : 0);
+    g.na = a_opp ? o : n;
+    g.oa = a_opp ? D : 0;
+    g.vb = v2 + (b_opp ? D : 0);
+    g.nb = b_opp ? o : n2;
+    g.ob = b_opp ? D : 0;
+    return g;
   };
   const uint64_t M = a.peff - L;  // non-forced probes
+  // class sizes (non-forced pairs) and the class needing selection
+  const uint64_t nn2 = K == 2 ? n : 1, oo2 = K == 2 ? o : 0;
+  const uint64_t Ccls[3] = {(uint64_t)L * (n * nn2 - 1),
+                            K == 2 ? 2ull * L * n * o : (uint64_t)L * o,
+                            (uint64_t)L * o * oo2};
+  uint32_t sel = 0;
+  uint64_t m_sel = M;
+  while (sel < 2 && m_sel > Ccls[sel]) { m_sel -= Ccls[sel]; ++sel; }
+  // work partition of the selection class: (grid, row block)
+  const uint32_t NG = ngrids(sel);
+  const uint32_t TPT = NG < blockDim.x ? blockDim.x / NG : 1;
+  const uint32_t units = NG * TPT;
+  auto unit = [&](uint32_t u, GridRef& g, uint32_t& rb, uint32_t& re) {
+    const uint32_t gi = u / TPT, part = u - gi * TPT;
+    g = grid(sel, gi);
+    const uint32_t RB = (g.na + TPT - 1) / TPT;
+    rb = min(g.na, part * RB);
+    re = min(g.na, rb + RB);
+  };
   // rank-th largest key (1-based) among enumerated keys in [base, base + 2^nbits)
   auto radix_select = [&](uint64_t rank, uint32_t base, int nbits, auto&& enumerate) -> uint32_t {
     uint32_t prefix = 0, mask = 0, rem = (uint32_t)rank;
@@ -356,7 +395,6 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
         if ((off & mask) == prefix) atomicAdd(&hist[(off >> sh) & (nb - 1)], 1u);
       });
       __syncthreads();
-      // descending scan over the bins, 8 bins per thread
       uint32_t hv[8], hs = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -389,16 +427,15 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
   uint32_t Tstar = 0, Tlo = 0;
   bool flat = false;
   uint32_t C = 0;
-  // walk-based enumeration of the non-forced pairs >= Tlo
-  auto enum_stair = [&](auto&& visit) {
+  auto enum_stair = [&](auto&& visit) {  // pairs >= Tlo of the selection class
     for (uint32_t u = threadIdx.x; u < units; u += blockDim.x) {
-      uint32_t t, rb, re;
-      unit(u, t, rb, re);
-      const float* v1 = V1(t);
-      const float* v2 = V2(t);
-      walk2_rows(v1, v2, S2, rb, re, 0xffffffffu, Tlo, [&](uint32_t r1, uint32_t, uint32_t pb) {
-        const float x = v1[r1];
-        for (uint32_t r2 = r1 == 0 ? 1 : 0; r2 < pb; ++r2) visit(ord_key(x + v2[r2]), pack(t, r1, r2));
+      GridRef g;
+      uint32_t rb, re;
+      unit(u, g, rb, re);
+      walk2_rows(g.va, g.vb, g.nb, rb, re, 0xffffffffu, Tlo, [&](uint32_t r1, uint32_t, uint32_t pb) {
+        const float x = g.va[r1];
+        for (uint32_t r2 = (r1 == 0 && g.forced) ? 1 : 0; r2 < pb; ++r2)
+          visit(ord_key(x + g.vb[r2]), pack(g.t, g.oa + r1, g.ob + r2));
       });
     }
   };
@@ -409,27 +446,29 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       enum_stair(visit);
     }
   };
-  if (M > 0) {
-    const uint32_t arm_len = (S2 - 1) + (s - 1);
-    const uint32_t apt = (arm_len + TPT - 1) / TPT;
-    auto enum_arms = [&](auto&& visit) {
-      for (uint32_t u = threadIdx.x; u < units; u += blockDim.x) {
-        const uint32_t t = u / TPT, part = u - t * TPT;
-        const float* v1 = V1(t);
-        const float* v2 = V2(t);
-        const uint32_t i0 = min(arm_len, part * apt), i1 = min(arm_len, i0 + apt);
+  if (m_sel > 0) {
+    auto enum_arms = [&](auto&& visit) {  // row 0 and column 0 of every grid
+      for (uint32_t gi = threadIdx.x / 1; gi < NG * TPT; gi += blockDim.x) {
+        const uint32_t g0 = gi / TPT, part = gi - g0 * TPT;
+        const GridRef g = grid(sel, g0);
+        const uint32_t r0 = g.forced ? 1 : 0;
+        const uint32_t arm = (g.nb - r0) + (g.na - 1);
+        const uint32_t apt = (arm + TPT - 1) / TPT;
+        const uint32_t i0 = min(arm, part * apt), i1 = min(arm, i0 + apt);
         for (uint32_t i = i0; i < i1; ++i) {
-          const float sc = i < S2 - 1 ? v1[0] + v2[i + 1] : v1[i - (S2 - 1) + 1] + v2[0];
+          const uint32_t nrow = g.nb - r0;
+          const float sc = i < nrow ? g.va[0] + g.vb[r0 + i] : g.va[i - nrow + 1] + g.vb[0];
           visit(ord_key(sc), 0u);
         }
       }
     };
     uint32_t amax = 0, amin = 0xffffffffu;
-    enum_arms([&](uint32_t k, uint32_t) { amax = max(amax, k); amin = min(amin, k); });
+    uint64_t an = 0;
+    enum_arms([&](uint32_t k, uint32_t) { amax = max(amax, k); amin = min(amin, k); ++an; });
     uint64_t pk = ((uint64_t)amax << 32) | (0xffffffffu - amin);
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t y = ((uint64_t)__shfl_xor_sync(FULL, (uint32_t)(pk >> 32), o) << 32) |
-                         __shfl_xor_sync(FULL, (uint32_t)pk, o);
+    for (int sft = 16; sft > 0; sft >>= 1) {
+      const uint64_t y = ((uint64_t)__shfl_xor_sync(FULL, (uint32_t)(pk >> 32), sft) << 32) |
+                         __shfl_xor_sync(FULL, (uint32_t)pk, sft);
       pk = (max(pk >> 32, y >> 32) << 32) | max(pk & 0xffffffffu, y & 0xffffffffu);
     }
     __syncthreads();
@@ -442,49 +481,47 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
     }
     amax = (uint32_t)mx;
     amin = 0xffffffffu - (uint32_t)nl;
-    __syncthreads();
-    if ((uint64_t)arm_len * L >= M) Tlo = radix_select(M, amin, bitlen(amax - amin), enum_arms);
-    // materialise every non-forced pair >= Tlo (one atomic per row run)
+    an = block_sum_u64(an, red);
+    if (an >= m_sel) Tlo = radix_select(m_sel, amin, bitlen(amax - amin), enum_arms);
+    // materialise every selection-class pair >= Tlo (one atomic per row run)
     for (uint32_t u = threadIdx.x; u < units; u += blockDim.x) {
-      uint32_t t, rb, re;
-      unit(u, t, rb, re);
-      const float* v1 = V1(t);
-      const float* v2 = V2(t);
-      walk2_rows(v1, v2, S2, rb, re, 0xffffffffu, Tlo, [&](uint32_t r1, uint32_t, uint32_t pb) {
-        const uint32_t st = r1 == 0 ? 1 : 0;
+      GridRef g;
+      uint32_t rb, re;
+      unit(u, g, rb, re);
+      walk2_rows(g.va, g.vb, g.nb, rb, re, 0xffffffffu, Tlo, [&](uint32_t r1, uint32_t, uint32_t pb) {
+        const uint32_t st = (r1 == 0 && g.forced) ? 1 : 0;
         if (pb <= st) return;
         const uint32_t base = atomicAdd(&n_cand, pb - st);
         if (base + (pb - st) > a.ccap) return;
-        const float x = v1[r1];
+        const float x = g.va[r1];
         for (uint32_t r2 = st; r2 < pb; ++r2) {
-          ckey[base + r2 - st] = ord_key(x + v2[r2]);
-          cpair[base + r2 - st] = pack(t, r1, r2);
+          ckey[base + r2 - st] = ord_key(x + g.vb[r2]);
+          cpair[base + r2 - st] = pack(g.t, g.oa + r1, g.ob + r2);
         }
       });
     }
     __syncthreads();
     C = n_cand;
     flat = C <= a.ccap;
-    // every pair >= Tlo has key <= amax (the best non-forced pair lies on an arm)
-    Tstar = radix_select(M, Tlo, bitlen(amax - Tlo), enum_cand);
+    // every arm pair is >= every other pair of its row / column, so amax bounds all keys
+    Tstar = radix_select(m_sel, Tlo, bitlen(amax - Tlo), enum_cand);
   }
   ck[2] = clock64();
-  // counts above / at T* (pairs below Tlo are below T* and never matter)
   uint64_t my_gt = 0, my_ge = 0;
-  if (M > 0)
+  if (m_sel > 0)
     enum_cand([&](uint32_t key, uint32_t) {
       my_gt += key > Tstar;
       my_ge += key >= Tstar;
     });
   const uint64_t cgt = block_sum_u64(my_gt, red);
   const uint64_t ties_total = block_sum_u64(my_ge, red) - cgt;
-  const uint64_t m = M > cgt ? M - cgt : 0;  // ties to take
-  auto comp = [&](uint32_t pr) {  // (r1, r2, t) composite order
+  const uint64_t m = m_sel > cgt ? m_sel - cgt : 0;  // ties to take
+  auto comp = [&](uint32_t pr) {  // (r1, r2, t) order on global ranks
     const uint32_t t = pr >> 22, r1 = (pr >> 11) & 2047u, r2 = pr & 2047u;
-    return ((uint64_t)r1 * S2 + r2) * L + t;
+    return ((uint64_t)r1 * 2048u + r2) * L + t;
   };
   uint64_t Kstar = ~0ull;
-  if (M > 0 && ties_total > m) {
+  if (m_sel > 0 && ties_total > m) {
     if (ties_total <= PS_TIE_CAP) {
       enum_cand([&](uint32_t key, uint32_t pr) {
         if (key == Tstar) ties[atomicAdd(&n_ties, 1u)] = comp(pr);
@@ -497,9 +534,9 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
         for (uint32_t j = 0; j < ties_total; ++j) rank += ties[j] < xk;
         if (rank == m) found = xk;
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t y = ((uint64_t)__shfl_xor_sync(FULL, (uint32_t)(found >> 32), o) << 32) |
-                           __shfl_xor_sync(FULL, (uint32_t)found, o);
+      for (int sft = 16; sft > 0; sft >>= 1) {
+        const uint64_t y = ((uint64_t)__shfl_xor_sync(FULL, (uint32_t)(found >> 32), sft) << 32) |
+                           __shfl_xor_sync(FULL, (uint32_t)found, sft);
         found = y < found ? y : found;
       }
       __syncthreads();
@@ -513,7 +550,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
         enum_cand([&](uint32_t key, uint32_t pr) { c += key == Tstar && comp(pr) < Kc; });
         return block_sum_u64(c, red);
       };
-      uint64_t lo = 0, hi = (uint64_t)s * S2 * L;
+      uint64_t lo = 0, hi = (uint64_t)2048 * 2048 * L;
       while (lo < hi) {
         const uint64_t mid = (lo + hi) >> 1;
         if (count_lt(mid) >= m) hi = mid;
@@ -527,7 +564,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
     return key > Tstar || (key == Tstar && (Kstar == ~0ull || comp(pr) < Kstar));
   };
   uint32_t* gb_out = a.gbuf + (uint64_t)q * a.peff;
-  const uint32_t twoD = 2 * a.D;
+  const uint32_t twoD = 2 * D;
   const uint32_t NB = (uint32_t)a.NB;
   auto bucket = [&](uint32_t pr) {
     const uint32_t t = pr >> 22, r1 = (pr >> 11) & 2047u, r2 = pr & 2047u;
@@ -535,7 +572,41 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
     return t * NB + (K == 2 ? __ldg(c1 + r1) * twoD + __ldg(c1 + s + r2) : __ldg(c1 + r1));
   };
   for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) gb_out[t] = bucket(t << 22);
-  if (M > 0) {
+  uint64_t slot0 = L;
+  // whole classes before the selection class: every pair, via per-thread counts + scan
+  for (uint32_t cls = 0; cls < sel; ++cls) {
+    const uint32_t ng = ngrids(cls);
+    uint64_t mine = 0;
+    for (uint32_t gi = threadIdx.x; gi < ng; gi += blockDim.x) {
+      const GridRef g = grid(cls, gi);
+      mine += (uint64_t)g.na * g.nb - (g.forced ? 1 : 0);
+    }
+    uint64_t x = mine;
+    {
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+      for (int sft = 1; sft < 32; sft <<= 1) {
+        const uint64_t y = ((uint64_t)__shfl_up_sync(FULL, (uint32_t)(x >> 32), sft) << 32) |
+                           __shfl_up_sync(FULL, (uint32_t)x, sft);
+        if (lane >= sft) x += y;
+      }
+      __syncthreads();
+      if (lane == 31) red[w] = x;
+      __syncthreads();
+      uint64_t wb = 0;
+      for (int i = 0; i < w; ++i) wb += red[i];
+      x = wb + x - mine;
+    }
+    uint64_t slot = slot0 + x;
+    for (uint32_t gi = threadIdx.x; gi < ng; gi += blockDim.x) {
+      const GridRef g = grid(cls, gi);
+      for (uint32_t r1 = 0; r1 < g.na; ++r1)
+        for (uint32_t r2 = (r1 == 0 && g.forced) ? 1 : 0; r2 < g.nb; ++r2)
+          gb_out[slot++] = bucket(pack(g.t, g.oa + r1, g.ob + r2));
+    }
+    slot0 += Ccls[cls];
+    __syncthreads();
+  }
+  if (m_sel > 0) {
     // compaction of the selected pairs: per-thread counts, exclusive scan, write
     uint64_t mine = 0;
     uint32_t i_beg = 0, i_end = 0;
@@ -550,10 +621,10 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
     uint64_t x = mine;
     {
       const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t y = ((uint64_t)__shfl_up_sync(FULL, (uint32_t)(x >> 32), o) << 32) |
-                           __shfl_up_sync(FULL, (uint32_t)x, o);
-        if (lane >= o) x += y;
+      for (int sft = 1; sft < 32; sft <<= 1) {
+        const uint64_t y = ((uint64_t)__shfl_up_sync(FULL, (uint32_t)(x >> 32), sft) << 32) |
+                           __shfl_up_sync(FULL, (uint32_t)x, sft);
+        if (lane >= sft) x += y;
       }
       __syncthreads();
       if (lane == 31) red[w] = x;
@@ -562,7 +633,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       for (int i = 0; i < w; ++i) wb += red[i];
       x = wb + x - mine;
     }
-    uint64_t slot = L + x;
+    uint64_t slot = slot0 + x;
     if (flat) {
       for (uint32_t i = i_beg; i < i_end; ++i) {
         const uint32_t pr = __ldcg(cpair + i);
