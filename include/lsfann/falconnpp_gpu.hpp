@@ -1,0 +1,92 @@
+// lsfann/falconnpp_gpu.hpp -- header-only C++ host API over the C ABI
+// (include/falconnpp.h), mirroring the reference's namespace (common.hpp:12)
+// and its SPEC operations: Index::build and Index::query
+// (SPEC.md:321-329).  Errors are rethrown as the reference does:
+// std::invalid_argument for configuration / range / data errors
+// (dataset.cpp:10-18, rotation.cpp:18-20,42-49), std::runtime_error for CUDA.
+#pragma once
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "falconnpp.h"
+
+namespace lsfann::gpu {
+
+inline void check(int rc) {
+  if (rc == FPP_OK) return;
+  const std::string msg = fpp_last_error();
+  switch (rc) {
+    case FPP_ERR_INVALID_ARGUMENT:
+    case FPP_ERR_EMPTY_DATASET:
+    case FPP_ERR_DIMENSION:
+    case FPP_ERR_OUT_OF_RANGE:
+    case FPP_ERR_NON_FINITE:
+    case FPP_ERR_ZERO_NORM:
+      throw std::invalid_argument(msg);
+    case FPP_ERR_OUT_OF_MEMORY:
+      throw std::bad_alloc();
+    default:
+      throw std::runtime_error(msg);
+  }
+}
+
+struct QueryResult {
+  std::vector<uint32_t> ids;   // [nq][k], 0xFFFFFFFF past min(k, candidates)
+  std::vector<double> scores;  // [nq][k], -inf past min(k, candidates)
+  std::vector<fpp_query_stats> stats;
+};
+
+class Index {
+ public:
+  // build(X, L, K, D, iProbes, alpha) -- X row-major n x d, already normalized
+  static Index build(std::span<const float> X, std::size_t n, std::size_t d, uint32_t L,
+                     uint32_t K, uint32_t D, uint32_t iProbes, float alpha, uint32_t kappa = 20,
+                     uint64_t seed = 1, int device = -1, uint32_t id_offset = 0) {
+    if (X.size() != n * d) throw std::invalid_argument("build: X.size() != n*d");
+    fpp_params p;
+    fpp_default_params(&p);
+    p.L = L; p.K = K; p.D = D; p.iprobes = iProbes; p.alpha = alpha; p.kappa = kappa;
+    p.seed = seed; p.device = device; p.id_offset = id_offset;
+    fpp_index* h = nullptr;
+    check(fpp_build(X.data(), n, static_cast<uint32_t>(d), &p, &h));
+    return Index(h);
+  }
+
+  // query(Q, k, qProbes) -- batch over the rows of Q
+  QueryResult query(std::span<const float> Q, std::size_t nq, uint32_t k, uint32_t qProbes,
+                    bool with_stats = false) const {
+    QueryResult r;
+    r.ids.resize(nq * k);
+    r.scores.resize(nq * k);
+    if (with_stats) r.stats.resize(nq);
+    check(fpp_query(h_, Q.data(), nq, k, qProbes, r.ids.data(), r.scores.data(),
+                    with_stats ? r.stats.data() : nullptr));
+    return r;
+  }
+
+  fpp_index_info info() const {
+    fpp_index_info i;
+    check(fpp_index_info_get(h_, &i));
+    return i;
+  }
+
+  Index(Index&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  Index& operator=(Index&& o) noexcept {
+    if (this != &o) { fpp_free(h_); h_ = std::exchange(o.h_, nullptr); }
+    return *this;
+  }
+  Index(const Index&) = delete;
+  Index& operator=(const Index&) = delete;
+  ~Index() { fpp_free(h_); }
+  const fpp_index* handle() const { return h_; }
+
+ private:
+  explicit Index(fpp_index* h) : h_(h) {}
+  fpp_index* h_ = nullptr;
+};
+
+}  // namespace lsfann::gpu

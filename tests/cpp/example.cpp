@@ -1,0 +1,29 @@
+// Smoke program for the C++ host API (include/lsfann/falconnpp_gpu.hpp).
+// Built by tests/test_capi.py; run by the GPU test.  Exit 0 on success,
+// 2 if no GPU is present (the build step still validates the API).
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "lsfann/falconnpp_gpu.hpp"
+
+int main() {
+  const std::size_t n = 2000, d = 32, nq = 8;
+  std::vector<float> X(n * d), Q(nq * d);
+  if (fpp_synth(X.data(), n, d, 4, 0.3f, 1, 0, 0) || fpp_normalize(X.data(), n, d)) return 1;
+  if (fpp_synth(Q.data(), nq, d, 4, 0.3f, 1, 1, 0) || fpp_normalize(Q.data(), nq, d)) return 1;
+  try {  // configuration errors surface as std::invalid_argument, like the reference
+    lsfann::gpu::Index::build(X, n, d, 4, 3, 32, 3, 0.1f);
+    return 1;
+  } catch (const std::invalid_argument&) {
+  }
+  if (fpp_device_count() == 0) return 2;
+  auto ix = lsfann::gpu::Index::build(X, n, d, 4, 2, 32, 3, 0.1f);
+  auto r = ix.query(Q, nq, 10, 64, true);
+  for (std::size_t i = 0; i < nq; ++i)
+    for (int j = 0; j + 1 < 10; ++j)
+      if (r.ids[i * 10 + j + 1] != 0xFFFFFFFFu && r.scores[i * 10 + j] < r.scores[i * 10 + j + 1])
+        return 1;
+  std::printf("cpp ok: kept %llu\n", (unsigned long long)ix.info().kept_total);
+  return 0;
+}
