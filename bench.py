@@ -39,6 +39,9 @@ CONFIGS = {
                alpha=0.02, nq=1000, qprobes=10_000, sweep=[10_000]),
     "c4": dict(n=10_000_000, d=128, clusters=10_000, sigma=0.25, L=50, K=2, D=128, iprobes=3,
                alpha=0.01, nq=100_000, qprobes=5000, sweep=[5000]),
+    # index-build throughput config (BASELINE.json configs[4]); build-only
+    "c5": dict(n=50_000_000, d=256, clusters=0, sigma=0.0, L=64, K=2, D=256, iprobes=5,
+               alpha=0.005, nq=0, qprobes=0, sweep=[]),
 }
 K_TOP = 20
 KAPPA = 20
@@ -215,6 +218,137 @@ def run_reference(args, cfg, qprobes):
     print(json.dumps(line), flush=True)
 
 
+def build_cpu_sample(cfg, npts, threads):
+    """Oracle build of one table over a same-distribution sample, as points/s for all L."""
+    from oracle import oracle as orc
+    Xs = orc.normalize(orc.synth(npts, cfg["d"], cfg["clusters"], cfg["sigma"], seed=SEED))
+    t0 = time.perf_counter()
+    ob = orc.Index(Xs, L=cfg["L"], K=cfg["K"], D=cfg["D"], iprobes=cfg["iprobes"],
+                   alpha=cfg["alpha"], kappa=KAPPA, seed=SEED, threads=threads, t_begin=0, t_end=1)
+    dt = time.perf_counter() - t0
+    del ob
+    return npts / (dt * cfg["L"])
+
+
+def run_reference_build(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    npts = 200_000
+    vals = [build_cpu_sample(cfg, npts, threads) for _ in range(max(1, args.steps))]
+    v = float(np.median(vals))
+    print(json.dumps({
+        "metric": "index-build points/s", "value": v, "unit": "points/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "impl": "reference",
+        "data": "synthetic i.i.d. N(0,1) normalized", "config": {"workload": args.config, **cfg},
+        "cpu_baseline": {"value": v, "unit": "points/s", "cores": threads, "kind": "port",
+                         "sample": f"{npts} points x 1 of {cfg['L']} tables per step, "
+                                   f"extrapolated linearly in L"},
+        "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_build(args, cfg):
+    """Build-only throughput (config c5): points/s of the full index build (K1 + K2)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2206_01382_b200 as fpp
+    from paper_2206_01382_b200 import dist as fdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, d = cfg["n"], cfg["d"]
+    lo, hi = fdist.shard_range(n, world, rank)
+    # i.i.d. N(0,1) rows generated on the device (torch Philox, seed 1 + shard offset),
+    # normalized on the device: same distribution as the host generator, not the same bytes
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(SEED * 1_000_003 + lo)
+    X = torch.empty((hi - lo, d), dtype=torch.float32, device="cuda")
+    for a in range(0, hi - lo, 1 << 22):
+        b = min(hi - lo, a + (1 << 22))
+        blk = torch.randn((b - a, d), generator=gen, device="cuda", dtype=torch.float32)
+        X[a:b] = blk / blk.double().norm(dim=1, keepdim=True).float()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def one_build():
+        ix = fpp.Index.build(X, L=cfg["L"], K=cfg["K"], D=cfg["D"], iProbes=cfg["iprobes"],
+                             alpha=cfg["alpha"], kappa=KAPPA, seed=SEED, device=local,
+                             id_offset=lo)
+        return ix
+
+    for _ in range(args.warmup):
+        ix = one_build()
+        info = ix.info()
+        del ix
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    dev_ms = []
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            ix = one_build()
+            t = ix.timings()
+            dev_ms.append((t["hash_ms"], t["sort_ms"]))
+            del ix
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    pps = n * args.steps / (t_ms / 1e3)
+    hash_ms = float(np.mean([a for a, _ in dev_ms]))
+    sort_ms = float(np.mean([b for _, b in dev_ms]))
+    flops = (hi - lo) * cfg["L"] * cfg["K"] * 3 * cfg["D"] * int(np.log2(cfg["D"]))
+    bytes_build = (4 * (hi - lo) * d + 24 * (hi - lo) * cfg["L"] * cfg["iprobes"]
+                   + 8 * info["kept_total"])
+    hbm, peak_kind = peaks()
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        cpu = {"value": build_cpu_sample(cfg, 200_000, threads), "unit": "points/s",
+               "cores": threads, "kind": "port",
+               "sample": f"oracle build of 1 of {cfg['L']} tables over 200000 points of the same "
+                         f"distribution, extrapolated linearly in L"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": "index-build points/s", "value": pps, "unit": "points/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic i.i.d. N(0,1) rows normalized, generated on device (torch Philox)",
+            "config": {"workload": args.config, "n": n, "d": d, "L": cfg["L"], "K": cfg["K"],
+                       "D": cfg["D"], "iProbes": cfg["iprobes"], "alpha": cfg["alpha"],
+                       "kappa": KAPPA, "parallelism": f"shard{world}" if world > 1 else "single"},
+            "roofline": {"kernel": "k_hash_build", "bound": "fp32 (FHT butterflies)",
+                         "fht_adds_per_s": flops / (hash_ms / 1e3),
+                         "hbm_achieved_gbs": bytes_build / ((hash_ms + sort_ms) / 1e3) / 1e9,
+                         "hbm_peak": hbm, "peak_kind": peak_kind,
+                         "hbm_frac": bytes_build / ((hash_ms + sort_ms) / 1e3) / 1e9 / hbm,
+                         "hash_ms": hash_ms, "sort_ms": sort_ms},
+            "build": {"kept_total": info["kept_total"], "prefilter_total": info["prefilter_total"]},
+            "e2e": {"value": pps, "unit": "points/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0,
+                    "note": "inputs device-resident (device-generated); build via fpp_build_device"},
+            "gpu_launches": None, "cpu_baseline": cpu, "clocks": clk.summary(),
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -226,12 +360,19 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-recall", action="store_true")
+    ap.add_argument("--mode", default="", choices=["", "query", "build"],
+                    help="query (default for c1-c4) or build-only throughput (default for c5)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
     qprobes = args.qprobes or cfg["qprobes"]
+    mode = args.mode or ("build" if args.config == "c5" else "query")
     if args.impl == "reference":
+        if mode == "build":
+            return run_reference_build(args, cfg)
         return run_reference(args, cfg, qprobes)
+    if mode == "build":
+        return run_build(args, cfg)
 
     import torch
     import torch.distributed as dist
@@ -330,6 +471,7 @@ def main():
         except Exception:
             traffic = None
     launches_per_step = tim["launches"] / args.steps
+    score_launches_per_step = max(1.0, launches_per_step / 5.0)  # 5 kernels per query chunk
 
     # --------------------------------------------------------- e2e (host API)
     import torch as _t
@@ -404,6 +546,7 @@ def main():
             "roofline": {"kernel": "k_score", "bound": "hbm", "achieved": achieved,
                          "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": score_bytes_step / score_launches_per_step,
                          "algorithmic_bytes_per_step": score_bytes_step,
                          "launches_per_step": launches_per_step,
                          "kernel_ms_per_step": score_ms,

@@ -1211,7 +1211,7 @@ static uint32_t chunk_size(const Index& ix, uint32_t qprobes, uint64_t nq) {
   const uint64_t LKs = (uint64_t)ix.prm.L * ix.prm.K * query_cap(ix, qprobes);
   const uint64_t pe = query_probes(ix, qprobes);
   const uint64_t per_q = LKs * 8 + pe * 16 + (4 * pe + 16384) * 8 + 64;
-  uint64_t c = (1ull << 30) / per_q;  // ~1 GB of per-chunk scratch per slot
+  uint64_t c = (4ull << 30) / per_q;  // ~4 GB of per-chunk scratch per slot
   c = std::max<uint64_t>(1, std::min<uint64_t>(c, 8192));
   // at least 4 chunks when the batch allows, so the two-stream pipeline overlaps
   const uint64_t quarter = (nq + 3) / 4;
