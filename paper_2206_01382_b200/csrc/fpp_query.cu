@@ -25,9 +25,14 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+
+#include <cooperative_groups.h>
 
 #include "fpp_device.cuh"
 #include "fpp_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace fpp {
 
@@ -835,6 +840,101 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
   }
 }
 
+// Large shards (n bits > one SM's shared memory): one thread-block cluster of
+// CO_CLUSTER CTAs per query, the visited bitmap split into per-CTA slices of
+// shared memory and tested-and-set through DSMEM atomics on the owning CTA
+// (cluster.map_shared_rank); the per-query candidate counter lives in CTA 0.
+constexpr int CO_CLUSTER = 8;
+
+__global__ void __cluster_dims__(CO_CLUSTER, 1, 1) __launch_bounds__(CO_THREADS, 1)
+k_collect_cluster(CollectArgs a, uint32_t slice_words) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const uint32_t rank = cluster.block_rank();
+  const uint32_t cid = blockIdx.x / CO_CLUSTER, ncl = gridDim.x / CO_CLUSTER;
+  extern __shared__ uint32_t sbm[];
+  __shared__ uint32_t pref[CO_TILE + 1];
+  __shared__ uint64_t tpos[CO_TILE];
+  __shared__ uint32_t sh[32];
+  __shared__ uint32_t ucount;
+  uint32_t* ucount0 = cluster.map_shared_rank(&ucount, 0);
+  const uint32_t slice_bits = slice_words * 32;
+  for (uint32_t q = cid; q < a.nq; q += ncl) {
+    for (uint32_t w = threadIdx.x; w < slice_words; w += blockDim.x) sbm[w] = 0;
+    if (rank == 0 && threadIdx.x == 0) ucount = 0;
+    cluster.sync();
+    uint32_t* out = a.cands + a.coff[q];
+    const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
+    const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
+    for (uint64_t p0 = (uint64_t)rank * CO_TILE; p0 < a.peff; p0 += (uint64_t)CO_CLUSTER * CO_TILE) {
+      const uint32_t np = (uint32_t)(a.peff - p0 < (uint64_t)CO_TILE ? a.peff - p0 : (uint64_t)CO_TILE);
+      uint32_t v[2] = {0, 0};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const uint32_t i = threadIdx.x * 2 + k;
+        if (i < np) {
+          v[k] = pl[p0 + i];
+          tpos[i] = pp[p0 + i];
+        }
+      }
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan_u32(v[0] + v[1], sh, &tot);
+      if (threadIdx.x * 2 < np) pref[threadIdx.x * 2] = ex;
+      if (threadIdx.x * 2 + 1 < np) pref[threadIdx.x * 2 + 1] = ex + v[0];
+      if (threadIdx.x == 0) pref[np] = tot;
+      __syncthreads();
+      const uint32_t per = (tot + blockDim.x - 1) / blockDim.x;
+      uint32_t e = min(tot, threadIdx.x * per);
+      const uint32_t e_end = min(tot, e + per);
+      uint32_t p = 0;
+      {
+        uint32_t lo = 0, hi = np;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (pref[mid] <= e) lo = mid;
+          else hi = mid;
+        }
+        p = lo;
+      }
+      while (e < e_end) {
+        uint32_t idv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          idv[u] = 0xffffffffu;
+          if (e + u < e_end) {
+            while (pref[p + 1] <= e + u) ++p;
+            idv[u] = __ldg(a.ids + tpos[p] + (e + u - pref[p]));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t id = idv[u];
+          bool isnew = false;
+          if (id != 0xffffffffu) {
+            const uint32_t owner = id / slice_bits, lb = id - owner * slice_bits;
+            uint32_t* rb = cluster.map_shared_rank(sbm, owner);
+            const uint32_t bit = 1u << (lb & 31);
+            isnew = !(atomicOr(rb + (lb >> 5), bit) & bit);
+          }
+          const unsigned act = __activemask();
+          const unsigned bal = __ballot_sync(act, isnew);
+          if (bal) {
+            const int lane = threadIdx.x & 31;
+            const int leader = __ffs(act) - 1;
+            uint32_t base = 0;
+            if (lane == leader) base = atomicAdd(ucount0, __popc(bal));
+            base = __shfl_sync(act, base, leader);
+            if (isnew) out[base + __popc(bal & ((1u << lane) - 1))] = id;
+          }
+        }
+        e += 4;
+      }
+      __syncthreads();
+    }
+    cluster.sync();
+    if (rank == 0 && threadIdx.x == 0) a.uq[q] = ucount;
+  }
+}
+
 // ------------------------------------------------------------------- score
 constexpr int SC_WARPS = 4;
 constexpr int SC_SLICE = 32;              // floats per row slice
@@ -1167,12 +1267,32 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   size_t co_smem = (size_t)nwords * 4;
   unsigned co_grid;
   const int sms = sm_count();
-  if ((int)(co_smem + static_co) <= co_smem_max()) {
+  const uint32_t slice_words = (nwords + CO_CLUSTER - 1) / CO_CLUSTER;
+  // FPP_FORCE_COLLECT=cluster|global selects a large-shard path at any n (tests)
+  const char* force = getenv("FPP_FORCE_COLLECT");
+  const bool f_cluster = force && !strcmp(force, "cluster"), f_global = force && !strcmp(force, "global");
+  if (!f_cluster && !f_global && (int)(co_smem + static_co) <= co_smem_max()) {
     FPP_CUDA(cudaFuncSetAttribute(k_collect, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)co_smem));
     int occ = 1;
     FPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collect, CO_THREADS, co_smem));
     co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * std::max(occ, 1));
+    FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
+    k_collect<<<co_grid, CO_THREADS, co_smem, st>>>(ca);
+  } else if (!f_global && (int)((size_t)slice_words * 4 + static_co) <= co_smem_max()) {
+    // bitmap split over a CO_CLUSTER-CTA cluster (DSMEM)
+    const size_t sm = (size_t)slice_words * 4;
+    FPP_CUDA(cudaFuncSetAttribute(k_collect_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sm));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CO_CLUSTER);
+    cfg.blockDim = dim3(CO_THREADS);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    int ncl = 0;
+    FPP_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k_collect_cluster, &cfg));
+    ncl = std::max(1, std::min<int>(ncl, (int)nqc));
+    k_collect_cluster<<<ncl * CO_CLUSTER, CO_THREADS, sm, st>>>(ca, slice_words);
   } else {
     co_smem = 0;
     co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * 2);
@@ -1182,9 +1302,9 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
       FPP_CUDA(cudaMemsetAsync(sl.bitmap.p, 0, need * 4, st));
     }
     ca.gbitmap = sl.bitmap.p;
+    FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
+    k_collect<<<co_grid, CO_THREADS, co_smem, st>>>(ca);
   }
-  FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
-  k_collect<<<co_grid, CO_THREADS, co_smem, st>>>(ca);
   FPP_LAUNCH();
   ix.timer.end(PH_COLLECT, e0, st);
 

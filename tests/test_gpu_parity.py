@@ -195,3 +195,31 @@ def test_empty_batch_and_errors(fpp):
     bad[7, 3] = np.nan
     with pytest.raises(fpp.FppNonFinite):
         fpp.Index.build(bad, L=2, K=2, D=16, iProbes=1, alpha=1.0)
+
+
+@pytest.mark.parametrize("path", ["cluster", "global"])
+def test_large_shard_collect_paths(fpp, orc, path, monkeypatch):
+    # the DSMEM-cluster bitmap (n > one SM's shared memory) and the global-memory
+    # bitmap fallback, forced at small n, must give the oracle's candidates/top-k
+    monkeypatch.setenv("FPP_FORCE_COLLECT", path)
+    X = data(fpp, 20000, 64, 20, 0.3)
+    Q = data(fpp, 40, 64, 20, 0.3, stream=1)
+    ix = fpp.Index.build(X, L=6, K=2, D=64, iProbes=3, alpha=0.1)
+    ox = orc.Index(X, L=6, K=2, D=64, iprobes=3, alpha=0.1)
+    gi, gs, gst = ix.query(Q, 20, 600, return_stats=True)
+    oi, os_, ost = ox.query(Q, 20, 600)
+    assert np.array_equal(gst, ost) and np.array_equal(gi, oi) and np.array_equal(gs, os_)
+    gp, gc = ix.query_debug(Q[3], 600)
+    op, oc = ox.query_debug(Q[3], 600)
+    assert np.array_equal(gc, oc)
+
+
+def test_cluster_collect_natural_large_n(fpp, orc):
+    # n = 2.2M points > the single-CTA bitmap limit (~1.7M) -> cluster path for real
+    X = data(fpp, 2_200_000, 16, 50, 0.2)
+    Q = data(fpp, 16, 16, 50, 0.2, stream=1)
+    ix = fpp.Index.build(X, L=2, K=2, D=16, iProbes=2, alpha=0.05, kappa=10)
+    ox = orc.Index(X, L=2, K=2, D=16, iprobes=2, alpha=0.05, kappa=10)
+    gi, gs, gst = ix.query(Q, 20, 100, return_stats=True)
+    oi, os_, ost = ox.query(Q, 20, 100)
+    assert np.array_equal(gst, ost) and np.array_equal(gi, oi) and np.array_equal(gs, os_)
