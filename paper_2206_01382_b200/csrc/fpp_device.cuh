@@ -257,6 +257,64 @@ __device__ __forceinline__ void group_bitonic_sort_u32(uint32_t (&k)[EPT], int g
   }
 }
 
+
+// Bitonic sort v2 (ascending, 32-bit keys, index i = g*EPT + e).  Sizes below
+// EPT have compile-time directions; for sizes >= EPT every lane's elements share
+// one direction, so descending blocks are complemented (~k) and all stages run
+// as plain ascending min/max (the complement reverses the order exactly).
+template <int S, int EPT>
+__device__ __forceinline__ void ce_up_u32(uint32_t (&k)[EPT]) {
+  if (S >= EPT) return;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    if (e & S) continue;
+    const uint32_t a = k[e], b = k[e | S];
+    k[e] = min(a, b);
+    k[e | S] = max(a, b);
+  }
+}
+
+template <int P, int EPT>
+__device__ __forceinline__ void group_sort_u32_v2(uint32_t (&k)[EPT], int g) {
+#pragma unroll
+  for (int size = 2; size < EPT; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        if (e & stride) continue;
+        const uint32_t a = k[e], b = k[e | stride];
+        const bool asc = (e & size) == 0;  // compile-time per element
+        k[e] = asc ? min(a, b) : max(a, b);
+        k[e | stride] = asc ? max(a, b) : min(a, b);
+      }
+    }
+  }
+#pragma unroll 1
+  for (int size = EPT; size <= P; size <<= 1) {
+    const uint32_t flip = ((g * EPT) & size) ? 0xffffffffu : 0u;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) k[e] ^= flip;
+#pragma unroll 1
+    for (int stride = size >> 1; stride >= EPT; stride >>= 1) {
+      const int m = stride / EPT;
+      const bool lower = (g & m) == 0;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const uint32_t o = __shfl_xor_sync(FULL, k[e], m);
+        k[e] = lower ? min(k[e], o) : max(k[e], o);
+      }
+    }
+    ce_up_u32<16, EPT>(k);
+    ce_up_u32<8, EPT>(k);
+    ce_up_u32<4, EPT>(k);
+    ce_up_u32<2, EPT>(k);
+    ce_up_u32<1, EPT>(k);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) k[e] ^= flip;
+  }
+}
+
 // exclusive block-wide scan (all threads must call); sh >= 32 words
 __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sh, uint32_t* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

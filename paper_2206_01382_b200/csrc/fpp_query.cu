@@ -51,11 +51,61 @@ __device__ __forceinline__ bool rank_before(float pa, uint32_t ja, float pb, uin
   return ja < jb;
 }
 
-// sort the group's keys, store to sk, fix equal-prefix runs exactly (one lane per run)
+// Sort the group's keys; neighbouring keys with equal quantised prefixes are
+// put in the exact order by odd-even transposition passes in registers (values
+// gathered from pv), falling back to a shared-memory insertion fix-up when a
+// run is long (degenerate inputs).
 template <int P, int EPT, bool NAT>
 __device__ __forceinline__ void rank_sort_exact(uint32_t (&kk)[EPT], int g, uint32_t* sk,
                                                 const float* pv) {
-  group_bitonic_sort_u32<P, EPT>(kk, g);
+  constexpr int G = P / EPT;
+  group_sort_u32_v2<P, EPT>(kk, g);
+  auto same = [](uint32_t x, uint32_t y) {
+    return x != 0xffffffffu && y != 0xffffffffu && (x >> 10) == (y >> 10);
+  };
+  auto before = [&](uint32_t y, uint32_t x) {  // exact: y strictly before x
+    return rank_before<NAT>(pv[y & 1023u], y & 1023u, pv[x & 1023u], x & 1023u);
+  };
+  bool done = false;
+#pragma unroll 1
+  for (int round = 0; round < 4; ++round) {
+    bool swapped = false;
+#pragma unroll
+    for (int e = 0; e + 1 < EPT; e += 2) {  // even pairs (in-lane)
+      if (same(kk[e], kk[e + 1]) && before(kk[e + 1], kk[e])) {
+        const uint32_t tmp = kk[e];
+        kk[e] = kk[e + 1];
+        kk[e + 1] = tmp;
+        swapped = true;
+      }
+    }
+#pragma unroll
+    for (int e = 1; e + 1 < EPT; e += 2) {  // odd pairs (in-lane)
+      if (same(kk[e], kk[e + 1]) && before(kk[e + 1], kk[e])) {
+        const uint32_t tmp = kk[e];
+        kk[e] = kk[e + 1];
+        kk[e + 1] = tmp;
+        swapped = true;
+      }
+    }
+    if (G > 1) {  // odd pair across the lane boundary: (last of g, first of g+1)
+      const uint32_t nxt = __shfl_down_sync(FULL, kk[0], 1);
+      const uint32_t prv = __shfl_up_sync(FULL, kk[EPT - 1], 1);
+      if (g + 1 < G && same(kk[EPT - 1], nxt) && before(nxt, kk[EPT - 1])) {
+        kk[EPT - 1] = nxt;
+        swapped = true;
+      }
+      if (g > 0 && same(prv, kk[0]) && before(kk[0], prv)) {
+        kk[0] = prv;
+        swapped = true;
+      }
+    }
+    if (!__any_sync(FULL, swapped)) {
+      done = true;
+      break;
+    }
+  }
+  if (done) return;
 #pragma unroll
   for (int e = 0; e < EPT; ++e) sk[g * EPT + e] = kk[e];
   __syncwarp();
@@ -81,6 +131,9 @@ __device__ __forceinline__ void rank_sort_exact(uint32_t (&kk)[EPT], int g, uint
       sk[w + 1] = y;
     }
   }
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) kk[e] = sk[g * EPT + e];
   __syncwarp();
 }
 
@@ -109,30 +162,43 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
   float v[EPT];
   load_row<P>(Q + q * d, d, g, v);
   spinner_project<P>(v, signs + ((uint64_t)t * K + f) * 3 * S::W, g);
+  // 22-bit key = |p| quantised against the group maximum (monotone: fp32
+  // multiply and floor are monotone), | 10-bit index; descending |p| -> ascending key
+  float amax = 0.0f;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) amax = fmaxf(amax, fabsf(v[e]));
+#pragma unroll
+  for (int m = 1; m < S::G; m <<= 1) amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, m));
+  const float qs = amax > 0.0f ? 4194303.0f / amax : 0.0f;
   uint32_t kk[EPT];
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     const uint32_t j = (uint32_t)g * EPT + e;
     pv[j] = v[e];
-    kk[e] = j < D ? (((~ord_key(fabsf(v[e]))) & 0xfffffc00u) | j) : 0xffffffffu;
+    const uint32_t qv = min((uint32_t)(fabsf(v[e]) * qs), 4194303u);
+    kk[e] = j < D ? (((4194303u - qv) << 10) | j) : 0xffffffffu;
   }
+  __syncwarp();
   rank_sort_exact<P, EPT, true>(kk, g, sk, pv);
   const uint64_t ob = q * lstride + (uint64_t)(t * K + f) * s;
   const uint32_t nat = s < D ? s : D;
   if (active) {
-    for (uint32_t r = g; r < nat; r += S::G) {
-      const uint32_t j = sk[r] & 1023u;
-      const float p = pv[j];
-      vals[ob + r] = fabsf(p);
-      codes[ob + r] = p < 0.0f ? D + j : j;
-    }
-  }
-  if (s > D && active) {  // opposite-signed vectors: same order, value |p|, flipped code
-    for (uint32_t r = g; r < s - D; r += S::G) {
-      const uint32_t j = sk[r] & 1023u;
-      const float p = pv[j];
-      vals[ob + D + r] = fabsf(p);
-      codes[ob + D + r] = p < 0.0f ? j : D + j;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t r = (uint32_t)g * EPT + e;
+      if (r < nat) {
+        const uint32_t j = kk[e] & 1023u;
+        const float p = pv[j];
+        vals[ob + r] = fabsf(p);
+        codes[ob + r] = p < 0.0f ? D + j : j;
+      }
+      // opposite-signed vectors: same order, value |p|, flipped code
+      if (r + D < s) {
+        const uint32_t j = kk[e] & 1023u;
+        const float p = pv[j];
+        vals[ob + D + r] = fabsf(p);
+        codes[ob + D + r] = p < 0.0f ? j : D + j;
+      }
     }
   }
 }
