@@ -26,14 +26,27 @@
 namespace fpp {
 
 // ------------------------------------------------------------------ K1 build
+// value / code of rank slot `a` of a sorted top-R key list (static select)
+template <int R>
+__device__ __forceinline__ uint64_t pick(const uint64_t (&t)[R], uint32_t a) {
+  uint64_t k = ~0ull;
+#pragma unroll
+  for (int i = 0; i < R; ++i) k = (uint32_t)i == a ? t[i] : k;
+  return k;
+}
+
 template <int P, int R>
 __global__ void __launch_bounds__(256)
 k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, uint32_t K,
              const uint32_t* __restrict__ signs, uint32_t t0, uint32_t T, uint32_t ip,
              uint2* __restrict__ ent, uint32_t* __restrict__ counts, uint64_t NB) {
   using S = FhtShape<P>;
+  constexpr bool TR = P >= 64;  // transpose FHT (cross-lane stages in registers)
+  constexpr int TS = TR ? TransposeShape<P>::STRIDE : 4;
+  __shared__ __align__(16) float tbuf[(256 / S::G) * TS];
   const int lane = threadIdx.x & 31;
   const int g = lane % S::G;
+  float* buf = tbuf + (threadIdx.x / S::G) * TS;
   const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
   const bool active = gid < n;
   const uint64_t i = active ? gid : n - 1;  // inactive groups shadow a real row
@@ -41,6 +54,8 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
   load_row<P>(X + i * d, d, g, x);
   const uint32_t r = ip < D ? ip : D;  // ranks needed per function (host ensures <= R)
   const uint32_t twoD = 2 * D;
+  // pairs this lane evaluates in the group-parallel top-iProbes selection
+  constexpr int NPL = (R * R + S::G - 1) / S::G;
   for (uint32_t tt = 0; tt < T; ++tt) {
     const uint32_t t = t0 + tt;
     uint64_t top0[R], top1[R];
@@ -49,8 +64,10 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
       float v[S::EPT];
 #pragma unroll
       for (int e = 0; e < S::EPT; ++e) v[e] = x[e];
-      spinner_project<P>(v, signs + ((uint64_t)t * K + f) * 3 * S::W, g);
-      // lane-local top-R by (|p| desc, j asc): strict '>' keeps the lower j on ties
+      const uint32_t* sw = signs + ((uint64_t)t * K + f) * 3 * S::W;
+      if constexpr (TR) spinner_project_T<P>(v, sw, g, buf);  // layout B: j = e*G + g
+      else spinner_project<P>(v, sw, g);                      // layout A: j = g*EPT + e
+      // lane-local top-R by (|p| desc, j asc): j increases with e in both layouts
       float tp[R];
       uint32_t tj[R];
 #pragma unroll
@@ -58,7 +75,7 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
       float thr = -1.0f;
 #pragma unroll
       for (int e = 0; e < S::EPT; ++e) {
-        const uint32_t j = (uint32_t)g * S::EPT + e;
+        const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * S::EPT + e;
         const float a = fabsf(v[e]);
         if (j < D && a > thr) {
           float cp = v[e];
@@ -83,49 +100,53 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
         else top1[q] = tk[q];
       }
     }
-    if (g != 0 || !active) continue;
-    uint2* out = ent + ((uint64_t)tt * n + i) * ip;
     uint32_t* cnt = counts ? counts + (uint64_t)tt * NB : nullptr;
+    uint2* out = ent + ((uint64_t)tt * n + i) * ip;
     if (K == 1) {
       // SPEC.md:184-192 with l=1: the top-iProbes signed vectors themselves
+      if (g == 0 && active) {
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
-        if ((uint32_t)q < ip) {
-          const uint32_t b = rank_code(top0[q], D);
-          out[q] = make_uint2(b, __float_as_uint(rank_val(top0[q])));
-          if (cnt) atomicAdd(cnt + b, 1u);
-        }
-      }
-    } else {
-      // top-iProbes pairs by (fl(v1+v2) desc, r1 asc, r2 asc): successive
-      // selection of the best pair strictly after the previous one.
-      float ps = 0.0f;
-      int pa = -1, pb = -1;
-      for (uint32_t sel = 0; sel < ip; ++sel) {
-        float bs = 0.0f;
-        int ba = -1, bb = -1;
-        uint32_t bc1 = 0, bc2 = 0;
-#pragma unroll
-        for (int a = 0; a < R; ++a) {
-          if ((uint32_t)a >= r) break;
-          const float va = rank_val(top0[a]);
-          const uint32_t ca = rank_code(top0[a], D);
-#pragma unroll
-          for (int b = 0; b < R; ++b) {
-            if ((uint32_t)b >= r) break;
-            const float s = va + rank_val(top1[b]);
-            const bool after = pa < 0 || ps > s || (ps == s && (pa < a || (pa == a && pb < b)));
-            if (!after) continue;
-            const bool better = ba < 0 || s > bs || (s == bs && (a < ba || (a == ba && b < bb)));
-            if (better) {
-              bs = s; ba = a; bb = b; bc1 = ca; bc2 = rank_code(top1[b], D);
-            }
+        for (int q = 0; q < R; ++q) {
+          if ((uint32_t)q < ip) {
+            const uint32_t b = rank_code(top0[q], D);
+            out[q] = make_uint2(b, __float_as_uint(rank_val(top0[q])));
+            if (cnt) atomicAdd(cnt + b, 1u);
           }
         }
-        const uint32_t bucket = bc1 * twoD + bc2;
-        out[sel] = make_uint2(bucket, __float_as_uint(bs));
+      }
+      continue;
+    }
+    // top-iProbes pairs by (fl(v1+v2) desc, r1 asc, r2 asc), group-parallel:
+    // composite max-key (ord(score), 0xFFFF-r1, 0xFFFF-r2); each round takes the
+    // group maximum strictly below the previous selection.
+    uint64_t pk[NPL];
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+      const uint32_t pi = (uint32_t)g + (uint32_t)k * S::G;
+      const uint32_t a = pi / R, b = pi % R;
+      pk[k] = 0;
+      if (pi < (uint32_t)(R * R) && a < r && b < r) {
+        const float sc = rank_val(pick<R>(top0, a)) + rank_val(pick<R>(top1, b));
+        pk[k] = ((uint64_t)ord_key(sc) << 32) | ((uint64_t)(0xffffu - a) << 16) | (0xffffu - b);
+      }
+    }
+    uint64_t prev = ~0ull;
+    for (uint32_t sel = 0; sel < ip; ++sel) {
+      uint64_t best = 0;
+#pragma unroll
+      for (int k = 0; k < NPL; ++k) best = (pk[k] < prev && pk[k] > best) ? pk[k] : best;
+#pragma unroll
+      for (int m = 1; m < S::G; m <<= 1) {
+        const uint64_t o = shfl_xor_u64(best, m);
+        best = o > best ? o : best;
+      }
+      prev = best;
+      if (g == 0 && active) {
+        const uint32_t a = 0xffffu - (uint32_t)((best >> 16) & 0xffffu);
+        const uint32_t b = 0xffffu - (uint32_t)(best & 0xffffu);
+        const uint32_t bucket = rank_code(pick<R>(top0, a), D) * twoD + rank_code(pick<R>(top1, b), D);
+        out[sel] = make_uint2(bucket, __float_as_uint(ord_inv((uint32_t)(best >> 32))));
         if (cnt) atomicAdd(cnt + bucket, 1u);
-        ps = bs; pa = ba; pb = bb;
       }
     }
   }
@@ -136,18 +157,23 @@ __global__ void __launch_bounds__(256)
 k_project(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D,
           const uint32_t* __restrict__ sw, float* __restrict__ out) {
   using S = FhtShape<P>;
+  constexpr bool TR = P >= 64;
+  constexpr int TS = TR ? TransposeShape<P>::STRIDE : 4;
+  __shared__ __align__(16) float tbuf[(256 / S::G) * TS];
   const int lane = threadIdx.x & 31;
   const int g = lane % S::G;
+  float* buf = tbuf + (threadIdx.x / S::G) * TS;
   const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
   const bool active = gid < n;
   const uint64_t i = active ? gid : n - 1;
   float v[S::EPT];
   load_row<P>(X + i * d, d, g, v);
-  spinner_project<P>(v, sw, g);
+  if constexpr (TR) spinner_project_T<P>(v, sw, g, buf);
+  else spinner_project<P>(v, sw, g);
   if (!active) return;
 #pragma unroll
   for (int e = 0; e < S::EPT; ++e) {
-    const uint32_t j = (uint32_t)g * S::EPT + e;
+    const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * S::EPT + e;
     if (j < D) out[i * D + j] = v[e];
   }
 }

@@ -92,6 +92,98 @@ __device__ __forceinline__ void spinner_project(float (&v)[FhtShape<P>::EPT], co
   for (int e = 0; e < S::EPT; ++e) v[e] = v[e] * scale;
 }
 
+// ------------------------------------------------ transpose FHT (P >= 64)
+// Same butterfly graph as fht_group, but the cross-lane stages run in
+// registers after one shared-memory transpose per round instead of log2(G)
+// shuffle stages:
+//   layout A: lane g holds j = g*32 + e  (bits 0..4 in registers)
+//   layout B: lane g holds j = e*G + g   (bits lgG..lgG+4 in registers)
+// Per-group scratch: TransposeShape<P>::STRIDE floats (16-byte aligned), padded
+// (4 floats per 32) so the vectorised A writes and the strided B reads are free
+// of bank conflicts, and group regions are offset to different banks.
+template <int P>
+struct TransposeShape {
+  static constexpr int G = P / 32;
+  static constexpr int STRIDE = P / 32 * 36 + (G < 4 ? 4 : (G % 32));
+};
+__device__ __forceinline__ int tpad(int j) { return j + ((j >> 5) << 2); }
+
+// in-register butterflies of layout B: register bit k <-> index bit lgG + k;
+// run the stages of index bits 5 .. 5+lgG-1 (register strides 32/G .. 16)
+template <int P>
+__device__ __forceinline__ void fht_regs_B(float (&v)[32]) {
+  constexpr int G = P / 32;
+#pragma unroll
+  for (int len = 32 / G; len < 32; len <<= 1) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 2 * len) {
+#pragma unroll
+      for (int j = i; j < i + len; ++j) {
+        const float x = v[j], y = v[j + len];
+        v[j] = x + y;
+        v[j + len] = x - y;
+      }
+    }
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void transpose_A_to_B(float (&v)[32], int g, float* buf) {
+  constexpr int G = P / 32;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    *reinterpret_cast<float4*>(buf + tpad(g * 32 + 4 * k)) =
+        make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < 32; ++e) v[e] = buf[tpad(e * G + g)];
+  __syncwarp();
+}
+
+template <int P>
+__device__ __forceinline__ void transpose_B_to_A(float (&v)[32], int g, float* buf) {
+  constexpr int G = P / 32;
+#pragma unroll
+  for (int e = 0; e < 32; ++e) buf[tpad(e * G + g)] = v[e];
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float4 q = *reinterpret_cast<const float4*>(buf + tpad(g * 32 + 4 * k));
+    v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+  }
+  __syncwarp();
+}
+
+// SpinnerStack::project with transpose FHTs: input in layout A, output in
+// layout B (element e of lane g is index e*G + g), scaled by 1/P.
+template <int P>
+__device__ __forceinline__ void spinner_project_T(float (&v)[32], const uint32_t* sw, int g,
+                                                  float* buf) {
+  constexpr int G = P / 32;
+#pragma unroll 1
+  for (int stage = 0; stage < 3; ++stage) {
+    if (stage) transpose_B_to_A<P>(v, g, buf);
+    apply_signs<32>(v, __ldg(sw + stage * G + g));
+#pragma unroll
+    for (int len = 1; len < 32; len <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 2 * len) {
+#pragma unroll
+        for (int j = i; j < i + len; ++j) {
+          const float x = v[j], y = v[j + len];
+          v[j] = x + y;
+          v[j + len] = x - y;
+        }
+      }
+    }
+    transpose_A_to_B<P>(v, g, buf);
+    fht_regs_B<P>(v);
+  }
+  const float scale = 1.0f / (float)P;
+#pragma unroll
+  for (int e = 0; e < 32; ++e) v[e] = v[e] * scale;
+}
+
 // Load row x[0..d) into the group layout, zero-padded to P (rotation.cpp:88-89).
 template <int P>
 __device__ __forceinline__ void load_row(const float* __restrict__ x, uint32_t d, int g,

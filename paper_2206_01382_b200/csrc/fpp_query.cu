@@ -145,13 +145,17 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
   using S = FhtShape<P>;
   constexpr int EPT = S::EPT;
   constexpr int GPB = 128 / S::G;
-  __shared__ float pv_all[GPB][P];
+  constexpr bool TR = P >= 64;  // transpose FHT (cross-lane stages in registers)
+  constexpr int TS = TR ? TransposeShape<P>::STRIDE : 4;
+  constexpr int PVS = TS > P ? TS : P;  // the transpose buffer doubles as pv after the FHT
   __shared__ uint32_t sk_all[GPB][P];
+  __shared__ __align__(16) float tb_all[GPB * PVS];
   const int lane = threadIdx.x & 31;
   const int g = lane % S::G;
   const int gl = threadIdx.x / S::G;
-  float* pv = pv_all[gl];
   uint32_t* sk = sk_all[gl];
+  float* tbuf = tb_all + gl * PVS;
+  float* pv = tbuf;
   const uint64_t gg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
   const uint64_t total = nq * L * K;
   const bool active = gg < total;
@@ -161,7 +165,9 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
   const uint64_t q = gid / ((uint64_t)K * L);
   float v[EPT];
   load_row<P>(Q + q * d, d, g, v);
-  spinner_project<P>(v, signs + ((uint64_t)t * K + f) * 3 * S::W, g);
+  if constexpr (TR) spinner_project_T<P>(v, signs + ((uint64_t)t * K + f) * 3 * S::W, g, tbuf);
+  else spinner_project<P>(v, signs + ((uint64_t)t * K + f) * 3 * S::W, g);
+  __syncwarp();  // transpose buffer is reused as pv below
   // 22-bit key = |p| quantised against the group maximum (monotone: fp32
   // multiply and floor are monotone), | 10-bit index; descending |p| -> ascending key
   float amax = 0.0f;
@@ -173,7 +179,7 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
   uint32_t kk[EPT];
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
-    const uint32_t j = (uint32_t)g * EPT + e;
+    const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * EPT + e;  // layout B / A
     pv[j] = v[e];
     const uint32_t qv = min((uint32_t)(fabsf(v[e]) * qs), 4194303u);
     kk[e] = j < D ? (((4194303u - qv) << 10) | j) : 0xffffffffu;
