@@ -10,9 +10,11 @@ probe select -> bucket walk/dedup -> row gather + fp64 dot + top-k).
   python bench.py [--gpus N --steps K --warmup W --config c2 --qprobes 10000]
   python bench.py --impl reference ...   # CPU oracle port on the host cores
 
-Multi-GPU (torchrun, one rank per GPU): rank g indexes ids [g*n/G,(g+1)*n/G),
-queries are replicated, per-rank top-k lists are merged after an NCCL
-all-gather; value = nq*K / (max over ranks of the timed region).
+Multi-GPU (torchrun, one rank per GPU): rank g indexes ids [g*n/G,(g+1)*n/G)
+with the global filter (NCCL all-reduce of bucket histograms + all-gather of
+bucket prefixes: the shards hold exactly the 1-GPU index), queries are
+replicated, per-rank top-k lists are merged after an NCCL all-gather;
+value = nq*K / (max over ranks of the timed region).
 """
 from __future__ import annotations
 
@@ -282,10 +284,11 @@ def run_build(args, cfg):
             dist.barrier()
 
     def one_build():
-        ix = fpp.Index.build(X, L=cfg["L"], K=cfg["K"], D=cfg["D"], iProbes=cfg["iprobes"],
-                             alpha=cfg["alpha"], kappa=KAPPA, seed=SEED, device=local,
-                             id_offset=lo)
-        return ix
+        prm = dict(L=cfg["L"], K=cfg["K"], D=cfg["D"], iProbes=cfg["iprobes"], alpha=cfg["alpha"],
+                   kappa=KAPPA, seed=SEED, device=local)
+        if world > 1:  # global filter over NCCL
+            return fdist.build_global_filter(fdist.GpuShardEngine(X, lo, **prm))
+        return fpp.Index.build(X, id_offset=lo, **prm)
 
     for _ in range(args.warmup):
         ix = one_build()
@@ -401,8 +404,12 @@ def main():
     barrier()
     torch.cuda.synchronize()
     tb0 = time.perf_counter()
-    ix = fpp.Index.build(Xd, L=cfg["L"], K=cfg["K"], D=cfg["D"], iProbes=cfg["iprobes"],
-                         alpha=cfg["alpha"], kappa=KAPPA, seed=SEED, device=local, id_offset=lo)
+    prm = dict(L=cfg["L"], K=cfg["K"], D=cfg["D"], iProbes=cfg["iprobes"], alpha=cfg["alpha"],
+               kappa=KAPPA, seed=SEED, device=local)
+    if world > 1:  # global filter: the shards together hold exactly the 1-GPU index
+        ix = fdist.build_global_filter(fdist.GpuShardEngine(Xd, lo, **prm))
+    else:
+        ix = fpp.Index.build(Xd, id_offset=lo, **prm)
     torch.cuda.synchronize()
     tbuild = time.perf_counter() - tb0
     tim = ix.timings()

@@ -145,6 +145,26 @@ int fpp_query_debug(const fpp_index* idx, const float* q, uint32_t qprobes, uint
 int fpp_timings_get(const fpp_index* idx, fpp_timings* t);
 int fpp_timings_reset(const fpp_index* idx);
 
+/* ------------------------------------- sharded build, global filter
+ * Rank g of G builds ids [id_offset, id_offset + n) of the global dataset so that
+ * the union of the G shard indexes equals the 1-GPU index exactly:
+ *   fpp_shard_begin        hash every table, local per-(table,bucket) histogram
+ *   fpp_shard_hist         copy it to a device buffer [L*NB] -> caller all-reduces (sum)
+ *   fpp_shard_slots        number of exchange slots (sum over buckets of keep(B_global))
+ *   fpp_shard_prefix       this rank's sorted bucket prefixes in those slots (~0 padded)
+ *                          -> caller all-gathers [G][slots]
+ *   fpp_shard_finish       per-bucket global cut, keep local entries <= cut -> queryable
+ * Device pointers must live on the index's device. */
+int fpp_shard_begin(const float* X, uint64_t n, uint32_t d, const fpp_params* p, fpp_index** out);
+int fpp_shard_begin_device(const float* X_dev, uint64_t n, uint32_t d, const fpp_params* p,
+                           fpp_index** out);
+uint64_t fpp_shard_hist_len(const fpp_index* idx);
+int fpp_shard_hist(const fpp_index* idx, uint32_t* hist_dev);
+int fpp_shard_slots(fpp_index* idx, const uint32_t* global_hist_dev, uint64_t* slots);
+int fpp_shard_prefix(fpp_index* idx, const uint32_t* global_hist_dev, uint64_t* prefix_dev);
+int fpp_shard_finish(fpp_index* idx, const uint32_t* global_hist_dev,
+                     const uint64_t* all_prefix_dev, uint32_t world);
+
 /* -------------------------------------------------------------- host helpers */
 /* normalize(Dataset) in place (dataset.cpp:24-38); FPP_ERR_ZERO_NORM names the row */
 int fpp_normalize(float* X, uint64_t n, uint32_t d);

@@ -132,6 +132,13 @@ SIGNATURES = [
     ("fpp_query_debug", C.c_int, [vp, vp, u32, vp, C.POINTER(u64), vp, C.POINTER(u64)]),
     ("fpp_timings_get", C.c_int, [vp, C.POINTER(Timings)]),
     ("fpp_timings_reset", C.c_int, [vp]),
+    ("fpp_shard_begin", C.c_int, [vp, u64, u32, C.POINTER(Params), C.POINTER(vp)]),
+    ("fpp_shard_begin_device", C.c_int, [vp, u64, u32, C.POINTER(Params), C.POINTER(vp)]),
+    ("fpp_shard_hist_len", u64, [vp]),
+    ("fpp_shard_hist", C.c_int, [vp, vp]),
+    ("fpp_shard_slots", C.c_int, [vp, vp, C.POINTER(u64)]),
+    ("fpp_shard_prefix", C.c_int, [vp, vp, vp]),
+    ("fpp_shard_finish", C.c_int, [vp, vp, vp, u32]),
     ("fpp_normalize", C.c_int, [vp, u64, u32]),
     ("fpp_synth", C.c_int, [vp, u64, u32, u32, f32, u64, u32, i32]),
 ]
@@ -222,6 +229,43 @@ class Index:
             n, d = X.shape
             _check(lib().fpp_build(_ptr(X), n, d, C.byref(p), C.byref(h)))
         return cls(h, p, n, d)
+
+    @classmethod
+    def shard_begin(cls, X, L: int, K: int, D: int, iProbes: int, alpha: float, kappa: int = 20,
+                    seed: int = 1, device: int = -1, id_offset: int = 0):
+        """Phase 1 of the global-filter sharded build (see paper_2206_01382_b200.dist)."""
+        p = Params(L, K, D, iProbes, kappa, alpha, seed, device, id_offset, 0)
+        h = C.c_void_p()
+        if _is_torch_cuda(X):
+            X = X.contiguous()
+            n, d = X.shape
+            if device < 0:
+                p.device = X.device.index or 0
+            _check(lib().fpp_shard_begin_device(C.c_void_p(X.data_ptr()), n, d, C.byref(p),
+                                                C.byref(h)))
+        else:
+            X = _f32(X)
+            n, d = X.shape
+            _check(lib().fpp_shard_begin(_ptr(X), n, d, C.byref(p), C.byref(h)))
+        return cls(h, p, n, d)
+
+    def shard_hist_len(self) -> int:
+        return lib().fpp_shard_hist_len(self._h)
+
+    def shard_hist(self, out_dev_ptr: int) -> None:
+        _check(lib().fpp_shard_hist(self._h, C.c_void_p(out_dev_ptr)))
+
+    def shard_slots(self, global_hist_ptr: int) -> int:
+        v = u64()
+        _check(lib().fpp_shard_slots(self._h, C.c_void_p(global_hist_ptr), C.byref(v)))
+        return v.value
+
+    def shard_prefix(self, global_hist_ptr: int, prefix_ptr: int) -> None:
+        _check(lib().fpp_shard_prefix(self._h, C.c_void_p(global_hist_ptr), C.c_void_p(prefix_ptr)))
+
+    def shard_finish(self, global_hist_ptr: int, all_prefix_ptr: int, world: int) -> None:
+        _check(lib().fpp_shard_finish(self._h, C.c_void_p(global_hist_ptr),
+                                      C.c_void_p(all_prefix_ptr), world))
 
     def __del__(self):
         h = getattr(self, "_h", None)

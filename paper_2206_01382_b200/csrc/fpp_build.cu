@@ -73,11 +73,12 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
 #pragma unroll
       for (int q = 0; q < R; ++q) { tp[q] = 0.0f; tj[q] = 0xffffffffu; }
       float thr = -1.0f;
+      const bool full = D >= (uint32_t)P;  // no truncation: skip the j < D test
 #pragma unroll
       for (int e = 0; e < S::EPT; ++e) {
         const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * S::EPT + e;
         const float a = fabsf(v[e]);
-        if (j < D && a > thr) {
+        if ((full || j < D) && a > thr) {
           float cp = v[e];
           uint32_t cj = j;
 #pragma unroll
@@ -267,7 +268,7 @@ static void scan_tables(const uint32_t* in, uint64_t NB, uint32_t T, KeepXform x
 __global__ void __launch_bounds__(256)
 k_scatter(const uint2* __restrict__ ent, uint64_t nip, uint32_t ip, uint32_t T, uint64_t NB,
           const uint32_t* __restrict__ starts, uint32_t* __restrict__ cursor,
-          uint64_t* __restrict__ keys) {
+          uint64_t* __restrict__ keys, uint32_t id_add = 0) {
   const uint64_t total = nip * T;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (uint64_t)gridDim.x * blockDim.x) {
@@ -277,7 +278,7 @@ k_scatter(const uint2* __restrict__ ent, uint64_t nip, uint32_t ip, uint32_t T, 
     const uint2 en = ent[e];
     const uint32_t pos = starts[(uint64_t)tt * (NB + 1) + en.x] +
                          atomicAdd(cursor + (uint64_t)tt * NB + en.x, 1u);
-    keys[(uint64_t)tt * nip + pos] = desc_score_key(__uint_as_float(en.y), i);
+    keys[(uint64_t)tt * nip + pos] = desc_score_key(__uint_as_float(en.y), i + id_add);
   }
 }
 
@@ -286,11 +287,16 @@ struct CsrOut {
   const uint64_t* base;     // [T] table bases (global positions)
   uint32_t* ids;
   float* scores;
+  uint64_t* keys_out;       // sharded build: sorted keys instead of (ids, scores)
 };
 
 __device__ __forceinline__ void csr_put(const CsrOut& o, uint32_t tt, uint64_t NB, uint32_t b,
                                         uint32_t j, uint64_t key) {
   const uint64_t pos = o.base[tt] + o.offs[(uint64_t)tt * (NB + 1) + b] + j;
+  if (o.keys_out) {
+    o.keys_out[pos] = key;
+    return;
+  }
   o.ids[pos] = (uint32_t)(key & 0xffffffffu);
   o.scores[pos] = desc_score_val(key);
 }
@@ -600,7 +606,7 @@ void build_tables(Index& ix) {
       k_scatter<<<blocks, 256, 0, s>>>(ent.p, nip, ip, Tc, NB, starts.p, counts.p, keys.p);
       FPP_LAUNCH();
     }
-    CsrOut o{offs, base_d.p, ix.ids, ix.scores};
+    CsrOut o{offs, base_d.p, ix.ids, ix.scores, nullptr};
     {
       const uint64_t tot = NB * Tc;
       const unsigned blocks = (unsigned)std::min<uint64_t>((tot + 255) / 256, (uint64_t)sms * 32);
@@ -627,6 +633,243 @@ void build_tables(Index& ix) {
   FPP_CUDA(cudaMemcpyAsync(ix.table_base, ix.table_base_h.data(), (L + 1) * sizeof(uint64_t),
                            cudaMemcpyHostToDevice, s));
   FPP_CUDA(cudaStreamSynchronize(s));
+}
+
+
+// ------------------------------------------------------ sharded build (8(e) B)
+// Global-filter sharding: every shard keeps exactly its part of the 1-GPU
+// index.  begin: hash every table, local histogram, every bucket fully sorted
+// by (score desc, GLOBAL id asc).  prefix: given the all-reduced histogram,
+// export min(keep_g, B_local) sorted keys per bucket into globally agreed
+// slots (Sum keep_g, padded with ~0).  finish: from all ranks' slots, the
+// bucket's cut = keep_g-th smallest key; keep the local keys <= cut as CSR.
+struct ShardState {
+  DBuf<uint64_t> sorted;     // [L][nip] bucket segments, sorted
+  DBuf<uint32_t> starts;     // [L][NB+1]
+  DBuf<uint32_t> hist;       // [L][NB] local
+  DBuf<uint32_t> slot_off;   // [L][NB+1] keep_g offsets within a table's slots
+  DBuf<uint64_t> slot_base;  // [L]
+  std::vector<uint64_t> slot_base_h;
+  uint64_t slots = 0;
+};
+
+void shard_begin(Index& ix) {
+  const uint32_t L = ix.prm.L, ip = ix.prm.iprobes;
+  const uint64_t n = ix.n, NB = ix.NB, nip = n * ip;
+  cudaStream_t s = ix.stream;
+  if (nip >= (1ull << 32)) fail(FPP_ERR_UNSUPPORTED, "build: n*iProbes must be < 2^32 per shard");
+  if ((uint64_t)L * NB >= (1ull << 32)) fail(FPP_ERR_UNSUPPORTED, "build: L*NB too large");
+  auto* st = new ShardState();
+  ix.shard = st;
+  DBuf<uint2> ent((size_t)L * nip);
+  DBuf<uint64_t> keys((size_t)L * nip);
+  st->sorted.alloc((size_t)L * nip);
+  st->hist.alloc((size_t)L * NB);
+  st->starts.alloc((size_t)L * (NB + 1));
+  DBuf<uint32_t> tiles, totals(L), ctr(4), cursor((size_t)L * NB);
+  DBuf<uint32_t> small_list((size_t)L * (nip / 2 + 1)), large_list((size_t)L * (nip / (SMALL_MAX + 1) + 1));
+  cudaEvent_t e0;
+  ix.timer.begin(PH_HASH, s, &e0);
+  FPP_CUDA(cudaMemsetAsync(st->hist.p, 0, (size_t)L * NB * 4, s));
+  launch_hash(ix, ix.X, n, 0, L, ent.p, st->hist.p, s);
+  ix.timer.end(PH_HASH, e0, s);
+  ix.timer.begin(PH_SORT, s, &e0);
+  KeepXform ident{0, 0.f, 1, 0};
+  scan_tables(st->hist.p, NB, L, ident, st->starts.p, totals.p, tiles, s);
+  FPP_CUDA(cudaMemsetAsync(cursor.p, 0, (size_t)L * NB * 4, s));
+  FPP_CUDA(cudaMemsetAsync(ctr.p, 0, 16, s));
+  const int sms = sm_count();
+  {
+    const uint64_t tot = nip * L;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((tot + 255) / 256, (uint64_t)sms * 32);
+    k_scatter<<<blocks, 256, 0, s>>>(ent.p, nip, ip, L, NB, st->starts.p, cursor.p, keys.p,
+                                     ix.prm.id_offset);
+    FPP_LAUNCH();
+  }
+  std::vector<uint64_t> tb(L);
+  for (uint32_t t = 0; t < L; ++t) tb[t] = (uint64_t)t * nip;
+  DBuf<uint64_t> tbd(L);
+  FPP_CUDA(cudaMemcpyAsync(tbd.p, tb.data(), L * 8, cudaMemcpyHostToDevice, s));
+  CsrOut o{st->starts.p, tbd.p, nullptr, nullptr, st->sorted.p};  // keep = B: full sort
+  {
+    const uint64_t tot = NB * L;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((tot + 255) / 256, (uint64_t)sms * 32);
+    k_classify<<<blocks, 256, 0, s>>>(st->starts.p, keys.p, nip, L, NB, o, small_list.p,
+                                      large_list.p, ctr.p);
+    FPP_LAUNCH();
+  }
+  k_sort_small<<<sms * 8, 256, 0, s>>>(st->starts.p, keys.p, nip, NB, o, small_list.p, ctr.p);
+  FPP_LAUNCH();
+  k_sort_large<<<sms * 4, 256, 0, s>>>(st->starts.p, keys.p, nip, NB, o, large_list.p, ctr.p);
+  FPP_LAUNCH();
+  ix.timer.end(PH_SORT, e0, s);
+  FPP_CUDA(cudaStreamSynchronize(s));
+}
+
+__global__ void k_shard_prefix(const uint32_t* __restrict__ ghist, const uint32_t* __restrict__ lhist,
+                               const uint32_t* __restrict__ starts, const uint64_t* __restrict__ sorted,
+                               const uint32_t* __restrict__ slot_off,
+                               const uint64_t* __restrict__ slot_base, uint32_t L, uint64_t NB,
+                               uint64_t nip, KeepXform kx, uint64_t* __restrict__ prefix) {
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < NB * L;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = (uint32_t)(x / NB), b = (uint32_t)(x - (uint64_t)t * NB);
+    const uint32_t kg = kx(ghist[x]);
+    if (!kg) continue;
+    const uint32_t bl = lhist[x];
+    const uint64_t dst = slot_base[t] + slot_off[(uint64_t)t * (NB + 1) + b];
+    const uint64_t src = (uint64_t)t * nip + starts[(uint64_t)t * (NB + 1) + b];
+    for (uint32_t j = 0; j < kg; ++j) prefix[dst + j] = j < bl ? sorted[src + j] : ~0ull;
+  }
+}
+
+// cut = kg-th smallest over `world` sorted runs of kg keys; local kept = #keys <= cut
+__global__ void k_shard_cut(const uint32_t* __restrict__ ghist, const uint32_t* __restrict__ lhist,
+                            const uint32_t* __restrict__ starts, const uint64_t* __restrict__ sorted,
+                            const uint32_t* __restrict__ slot_off,
+                            const uint64_t* __restrict__ slot_base, uint64_t slots,
+                            const uint64_t* __restrict__ all_prefix, uint32_t world, uint32_t L,
+                            uint64_t NB, uint64_t nip, KeepXform kx, uint32_t* __restrict__ kept,
+                            uint64_t* __restrict__ cuts) {
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < NB * L;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = (uint32_t)(x / NB), b = (uint32_t)(x - (uint64_t)t * NB);
+    const uint32_t Bg = ghist[x], kg = kx(Bg), bl = lhist[x];
+    uint64_t cut;
+    if (kg == 0) cut = 0;
+    else if (kg >= Bg) cut = ~0ull;
+    else {
+      const uint64_t off = slot_base[t] + slot_off[(uint64_t)t * (NB + 1) + b];
+      uint32_t ptr[16];
+      for (uint32_t r = 0; r < world; ++r) ptr[r] = 0;
+      cut = ~0ull;
+      for (uint32_t k = 0; k < kg; ++k) {  // k-way merge up to the kg-th key
+        uint32_t br = 0;
+        uint64_t bk = ~0ull;
+        for (uint32_t r = 0; r < world; ++r) {
+          const uint64_t v = ptr[r] < kg ? all_prefix[(uint64_t)r * slots + off + ptr[r]] : ~0ull;
+          if (v < bk) { bk = v; br = r; }
+        }
+        ++ptr[br];
+        cut = bk;
+      }
+    }
+    cuts[x] = cut;
+    // local keys <= cut form a prefix of the sorted local segment
+    const uint64_t src = (uint64_t)t * nip + starts[(uint64_t)t * (NB + 1) + b];
+    uint32_t lo = 0, hi = bl;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (sorted[src + mid] <= cut) lo = mid + 1;
+      else hi = mid;
+    }
+    kept[x] = kg == 0 ? 0 : lo;
+  }
+}
+
+__global__ void k_shard_write(const uint32_t* __restrict__ starts, const uint64_t* __restrict__ sorted,
+                              const uint32_t* __restrict__ offs, const uint64_t* __restrict__ tbase,
+                              uint32_t L, uint64_t NB, uint64_t nip, uint32_t id_sub,
+                              uint32_t* __restrict__ ids, float* __restrict__ scores,
+                              uint32_t* __restrict__ maxk) {
+  uint32_t lm = 0;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < NB * L;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = (uint32_t)(x / NB), b = (uint32_t)(x - (uint64_t)t * NB);
+    const uint32_t* of = offs + (uint64_t)t * (NB + 1);
+    const uint32_t k = of[b + 1] - of[b];
+    lm = max(lm, k);
+    const uint64_t src = (uint64_t)t * nip + starts[(uint64_t)t * (NB + 1) + b];
+    const uint64_t dst = tbase[t] + of[b];
+    for (uint32_t j = 0; j < k; ++j) {
+      const uint64_t key = sorted[src + j];
+      ids[dst + j] = (uint32_t)(key & 0xffffffffu) - id_sub;
+      scores[dst + j] = desc_score_val(key);
+    }
+  }
+  for (int o2 = 16; o2 > 0; o2 >>= 1) lm = max(lm, __shfl_xor_sync(FULL, lm, o2));
+  if ((threadIdx.x & 31) == 0 && lm) atomicMax(maxk, lm);
+}
+
+uint64_t shard_slots(Index& ix, const uint32_t* ghist) {
+  ShardState* st = ix.shard;
+  if (!st) fail(FPP_ERR_INVALID_ARGUMENT, "shard: fpp_shard_begin was not called");
+  const uint32_t L = ix.prm.L;
+  const uint64_t NB = ix.NB;
+  cudaStream_t s = ix.stream;
+  KeepXform kx{1, ix.prm.alpha, ix.prm.iprobes, ix.prm.kappa};
+  st->slot_off.ensure((size_t)L * (NB + 1));
+  DBuf<uint32_t> tiles, totals(L);
+  scan_tables(ghist, NB, L, kx, st->slot_off.p, totals.p, tiles, s);
+  std::vector<uint32_t> th(L);
+  FPP_CUDA(cudaMemcpyAsync(th.data(), totals.p, L * 4, cudaMemcpyDeviceToHost, s));
+  FPP_CUDA(cudaStreamSynchronize(s));
+  st->slot_base_h.assign(L + 1, 0);
+  for (uint32_t t = 0; t < L; ++t) st->slot_base_h[t + 1] = st->slot_base_h[t] + th[t];
+  st->slot_base.ensure(L + 1);
+  FPP_CUDA(cudaMemcpy(st->slot_base.p, st->slot_base_h.data(), (L + 1) * 8, cudaMemcpyHostToDevice));
+  st->slots = st->slot_base_h[L];
+  return st->slots;
+}
+
+void shard_prefix(Index& ix, const uint32_t* ghist, uint64_t* prefix) {
+  ShardState* st = ix.shard;
+  if (!st || !st->slot_off.p) fail(FPP_ERR_INVALID_ARGUMENT, "shard: call fpp_shard_slots first");
+  const uint32_t L = ix.prm.L;
+  KeepXform kx{1, ix.prm.alpha, ix.prm.iprobes, ix.prm.kappa};
+  const unsigned blocks = (unsigned)std::min<uint64_t>((ix.NB * L + 255) / 256, (uint64_t)sm_count() * 32);
+  k_shard_prefix<<<blocks, 256, 0, ix.stream>>>(ghist, st->hist.p, st->starts.p, st->sorted.p,
+                                                st->slot_off.p, st->slot_base.p, L, ix.NB,
+                                                ix.n * ix.prm.iprobes, kx, prefix);
+  FPP_LAUNCH();
+  FPP_CUDA(cudaStreamSynchronize(ix.stream));
+}
+
+void shard_finish(Index& ix, const uint32_t* ghist, const uint64_t* all_prefix, uint32_t world) {
+  ShardState* st = ix.shard;
+  if (!st || !st->slot_off.p) fail(FPP_ERR_INVALID_ARGUMENT, "shard: call fpp_shard_slots first");
+  if (world == 0 || world > 16) fail(FPP_ERR_UNSUPPORTED, "shard: world size must be 1..16");
+  const uint32_t L = ix.prm.L;
+  const uint64_t NB = ix.NB, nip = ix.n * ix.prm.iprobes;
+  cudaStream_t s = ix.stream;
+  KeepXform kx{1, ix.prm.alpha, ix.prm.iprobes, ix.prm.kappa};
+  KeepXform ident{0, 0.f, 1, 0};
+  DBuf<uint32_t> kept((size_t)L * NB), tiles, totals(L), mk(1);
+  DBuf<uint64_t> cuts((size_t)L * NB);
+  const unsigned blocks = (unsigned)std::min<uint64_t>((NB * L + 255) / 256, (uint64_t)sm_count() * 32);
+  k_shard_cut<<<blocks, 256, 0, s>>>(ghist, st->hist.p, st->starts.p, st->sorted.p, st->slot_off.p,
+                                     st->slot_base.p, st->slots, all_prefix, world, L, NB, nip, kx,
+                                     kept.p, cuts.p);
+  FPP_LAUNCH();
+  ix.offsets = static_cast<uint32_t*>(dmalloc((size_t)L * (NB + 1) * sizeof(uint32_t)));
+  scan_tables(kept.p, NB, L, ident, ix.offsets, totals.p, tiles, s);
+  std::vector<uint32_t> th(L);
+  FPP_CUDA(cudaMemcpyAsync(th.data(), totals.p, L * 4, cudaMemcpyDeviceToHost, s));
+  FPP_CUDA(cudaStreamSynchronize(s));
+  ix.table_base_h.assign(L + 1, 0);
+  for (uint32_t t = 0; t < L; ++t) ix.table_base_h[t + 1] = ix.table_base_h[t] + th[t];
+  ix.kept_total = ix.table_base_h[L];
+  ix.table_base = static_cast<uint64_t*>(dmalloc((size_t)(L + 1) * sizeof(uint64_t)));
+  FPP_CUDA(cudaMemcpy(ix.table_base, ix.table_base_h.data(), (L + 1) * 8, cudaMemcpyHostToDevice));
+  ix.ids = static_cast<uint32_t*>(dmalloc((ix.kept_total + 1) * sizeof(uint32_t)));
+  ix.scores = static_cast<float*>(dmalloc((ix.kept_total + 1) * sizeof(float)));
+  FPP_CUDA(cudaMemsetAsync(mk.p, 0, 4, s));
+  k_shard_write<<<blocks, 256, 0, s>>>(st->starts.p, st->sorted.p, ix.offsets, ix.table_base, L, NB,
+                                       nip, ix.prm.id_offset, ix.ids, ix.scores, mk.p);
+  FPP_LAUNCH();
+  uint32_t mx = 0;
+  FPP_CUDA(cudaMemcpyAsync(&mx, mk.p, 4, cudaMemcpyDeviceToHost, s));
+  FPP_CUDA(cudaStreamSynchronize(s));
+  ix.max_bucket = mx;
+  delete st;
+  ix.shard = nullptr;
+}
+
+const uint32_t* shard_hist_ptr(const Index& ix) { return ix.shard->hist.p; }
+
+void shard_release(Index& ix) {
+  delete ix.shard;
+  ix.shard = nullptr;
 }
 
 }  // namespace fpp

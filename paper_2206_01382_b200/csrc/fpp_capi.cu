@@ -90,6 +90,7 @@ Index::~Index() {
   dfree(table_base);
   dfree(ids);
   dfree(scores);
+  if (shard) shard_release(*this);
   for (auto& sl : slot) sl.release();
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
@@ -226,7 +227,7 @@ static void validate_params(const fpp_params& p, uint64_t n, uint32_t d) {
 }
 
 static fpp_index* build_common(const float* X, bool on_device, uint64_t n, uint32_t d,
-                               const fpp_params* pp) {
+                               const fpp_params* pp, bool sharded = false) {
   if (!pp) fail(FPP_ERR_INVALID_ARGUMENT, "build: params is NULL");
   if (!X && n) fail(FPP_ERR_INVALID_ARGUMENT, "build: X is NULL");
   const fpp_params p = *pp;
@@ -275,7 +276,8 @@ static fpp_index* build_common(const float* X, bool on_device, uint64_t n, uint3
     FPP_CUDA(cudaMemcpyAsync(ix->signs, words.data(), words.size() * 4, cudaMemcpyHostToDevice,
                              ix->stream));
     FPP_CUDA(cudaStreamSynchronize(ix->stream));
-    build_tables(*ix);
+    if (sharded) shard_begin(*ix);
+    else build_tables(*ix);
     ix->device_bytes = n * d * 4 + words.size() * 4 + (uint64_t)p.L * (ix->NB + 1) * 4 +
                        (p.L + 1) * 8 + ix->kept_total * 8;
     double ms[PH_COUNT] = {0};
@@ -305,6 +307,7 @@ struct DeviceGuard {
 
 static void validate_query(const Index& ix, uint64_t nq, uint32_t k, uint32_t qprobes,
                            const void* Q, const void* ids, const void* scores) {
+  if (!ix.offsets) fail(FPP_ERR_INVALID_ARGUMENT, "search: sharded build not finished (fpp_shard_finish)");
   if (k == 0) fail(FPP_ERR_INVALID_ARGUMENT, "search: k must be >= 1");
   if (k > ix.n) fail(FPP_ERR_OUT_OF_RANGE, "search: k > n");
   if (k > 32) fail(FPP_ERR_UNSUPPORTED, "GPU path: k must be <= 32");
@@ -422,6 +425,67 @@ int fpp_query_device(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t
     std::lock_guard<std::mutex> lk(ix.mu);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ix.stream;
     run_query(ix, Q, nq, k, qprobes, ids, scores, stats, s);
+  });
+}
+
+int fpp_shard_begin(const float* X, uint64_t n, uint32_t d, const fpp_params* p, fpp_index** out) {
+  return guarded([&] {
+    if (!out) fail(FPP_ERR_INVALID_ARGUMENT, "build: out is NULL");
+    *out = build_common(X, false, n, d, p, true);
+  });
+}
+
+int fpp_shard_begin_device(const float* X, uint64_t n, uint32_t d, const fpp_params* p,
+                           fpp_index** out) {
+  return guarded([&] {
+    if (!out) fail(FPP_ERR_INVALID_ARGUMENT, "build: out is NULL");
+    *out = build_common(X, true, n, d, p, true);
+  });
+}
+
+uint64_t fpp_shard_hist_len(const fpp_index* idx) {
+  if (!idx) return 0;
+  const Index& ix = *reinterpret_cast<const Index*>(idx);
+  return (uint64_t)ix.prm.L * ix.NB;
+}
+
+int fpp_shard_hist(const fpp_index* idx, uint32_t* hist_dev) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    if (!ix.shard) fail(FPP_ERR_INVALID_ARGUMENT, "shard: not a sharded build in progress");
+    DeviceGuard dg(ix.device);
+    FPP_CUDA(cudaMemcpy(hist_dev, shard_hist_ptr(ix), (uint64_t)ix.prm.L * ix.NB * 4,
+                        cudaMemcpyDeviceToDevice));
+  });
+}
+
+int fpp_shard_slots(fpp_index* idx, const uint32_t* global_hist_dev, uint64_t* slots) {
+  return guarded([&] {
+    Index& ix = *reinterpret_cast<Index*>(const_cast<fpp_index*>(idx));
+    DeviceGuard dg(ix.device);
+    *slots = shard_slots(ix, global_hist_dev);
+  });
+}
+
+int fpp_shard_prefix(fpp_index* idx, const uint32_t* global_hist_dev, uint64_t* prefix_dev) {
+  return guarded([&] {
+    Index& ix = *reinterpret_cast<Index*>(idx);
+    DeviceGuard dg(ix.device);
+    shard_prefix(ix, global_hist_dev, prefix_dev);
+  });
+}
+
+int fpp_shard_finish(fpp_index* idx, const uint32_t* global_hist_dev, const uint64_t* all_prefix_dev,
+                     uint32_t world) {
+  return guarded([&] {
+    Index& ix = *reinterpret_cast<Index*>(idx);
+    DeviceGuard dg(ix.device);
+    shard_finish(ix, global_hist_dev, all_prefix_dev, world);
+    ix.device_bytes = ix.n * ix.d * 4 + (uint64_t)ix.prm.L * (ix.NB + 1) * 4 + ix.kept_total * 8;
+    double ms[PH_COUNT] = {0};
+    ix.timer.collect(ms);
+    ix.acc.hash_ms += ms[PH_HASH];
+    ix.acc.sort_ms += ms[PH_SORT];
   });
 }
 

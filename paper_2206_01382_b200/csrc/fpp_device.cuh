@@ -127,28 +127,38 @@ __device__ __forceinline__ void fht_regs_B(float (&v)[32]) {
   }
 }
 
+// e*G + g stays in the 32-block of e*G (G | 32, g < G), so tpad(e*G + g) =
+// C(e) + g with C(e) = e*G + 4*((e*G) >> 5) a compile-time offset; the A rows
+// start at 36*g.  Every access is base register + immediate.
+template <int G>
+__host__ __device__ constexpr int tB(int e) { return e * G + 4 * ((e * G) >> 5); }
+
 template <int P>
 __device__ __forceinline__ void transpose_A_to_B(float (&v)[32], int g, float* buf) {
   constexpr int G = P / 32;
+  float* ra = buf + 36 * g;
+  float* rb = buf + g;
 #pragma unroll
   for (int k = 0; k < 8; ++k)
-    *reinterpret_cast<float4*>(buf + tpad(g * 32 + 4 * k)) =
+    *reinterpret_cast<float4*>(ra + 4 * k) =
         make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
   __syncwarp();
 #pragma unroll
-  for (int e = 0; e < 32; ++e) v[e] = buf[tpad(e * G + g)];
+  for (int e = 0; e < 32; ++e) v[e] = rb[tB<G>(e)];
   __syncwarp();
 }
 
 template <int P>
 __device__ __forceinline__ void transpose_B_to_A(float (&v)[32], int g, float* buf) {
   constexpr int G = P / 32;
+  float* ra = buf + 36 * g;
+  float* rb = buf + g;
 #pragma unroll
-  for (int e = 0; e < 32; ++e) buf[tpad(e * G + g)] = v[e];
+  for (int e = 0; e < 32; ++e) rb[tB<G>(e)] = v[e];
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const float4 q = *reinterpret_cast<const float4*>(buf + tpad(g * 32 + 4 * k));
+    const float4 q = *reinterpret_cast<const float4*>(ra + 4 * k);
     v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
   }
   __syncwarp();

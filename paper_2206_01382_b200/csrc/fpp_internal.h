@@ -64,6 +64,8 @@ struct PhaseTimer {
   ~PhaseTimer();
 };
 
+struct ShardState;
+
 struct Index {
   fpp_params prm{};
   uint64_t n = 0;
@@ -83,6 +85,7 @@ struct Index {
   uint64_t kept_total = 0;
   uint32_t max_bucket = 0;
   uint64_t device_bytes = 0;
+  ShardState* shard = nullptr;  // global-filter sharded build in progress
 
   // query scratch (guarded by mu; concurrent queries serialize on it).  Two
   // slots double-buffer query chunks across two streams.
@@ -137,6 +140,15 @@ void launch_project(const Index& ix, const float* Xd, uint64_t n, uint32_t t, ui
                     float* out, cudaStream_t s);
 void launch_index_probes(const Index& ix, const float* Xd, uint64_t n, uint32_t t,
                          uint2* out, cudaStream_t s);
+
+// global-filter sharded build (fpp_build.cu)
+void shard_begin(Index& ix);
+uint64_t shard_slots(Index& ix, const uint32_t* global_hist);
+void shard_prefix(Index& ix, const uint32_t* global_hist, uint64_t* prefix);
+void shard_finish(Index& ix, const uint32_t* global_hist, const uint64_t* all_prefix,
+                  uint32_t world);
+void shard_release(Index& ix);
+const uint32_t* shard_hist_ptr(const Index& ix);
 
 // query (fpp_query.cu)
 void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t qprobes,

@@ -53,3 +53,59 @@ def allgather_merge(scores: torch.Tensor, ids: torch.Tensor, k: int, group=None)
     dist.all_gather(s_all, scores.contiguous(), group=group)
     dist.all_gather(i_all, ids64.contiguous(), group=group)
     return merge_topk(torch.cat(s_all, dim=1), torch.cat(i_all, dim=1), k)
+
+
+# ---------------------------------------------------------------------------
+# Global-filter sharded build (SURVEY.md 8(e) option B): the union of the
+# shard indexes equals the 1-GPU index exactly, for every G.
+#   1. every rank hashes its shard and histograms (table, bucket) sizes;
+#   2. all-reduce(sum) of the histograms -> the global bucket sizes B_g;
+#   3. each rank writes min(keep(B_g), B_local) of its sorted bucket prefix
+#      into globally agreed slots (sum_b keep(B_g), padded) -> all-gather;
+#   4. per bucket the global cut = keep(B_g)-th smallest (score desc, id asc)
+#      key of the gathered prefixes; each rank keeps its entries <= cut.
+# The engine is the GPU library (GpuShardEngine) or, in the CPU tests, the
+# oracle (tests/test_dist_gloo.py::OracleShardEngine).
+# ---------------------------------------------------------------------------
+
+
+class GpuShardEngine:
+    """Phases of fpp_shard_* on the rank's GPU; tensors are CUDA torch tensors."""
+
+    def __init__(self, X, id_offset: int, **params):
+        import paper_2206_01382_b200 as fpp
+        self.ix = fpp.Index.shard_begin(X, id_offset=id_offset, **params)
+        self.device = X.device if getattr(X, "is_cuda", False) else torch.device("cuda", max(params.get("device", 0), 0))
+
+    def hist(self) -> torch.Tensor:
+        h = torch.empty(self.ix.shard_hist_len(), dtype=torch.int32, device=self.device)
+        self.ix.shard_hist(h.data_ptr())
+        return h
+
+    def slots(self, ghist: torch.Tensor) -> int:
+        return self.ix.shard_slots(ghist.data_ptr())
+
+    def prefix(self, ghist: torch.Tensor, slots: int) -> torch.Tensor:
+        p = torch.empty(max(slots, 1), dtype=torch.int64, device=self.device)
+        self.ix.shard_prefix(ghist.data_ptr(), p.data_ptr())
+        return p[:slots]
+
+    def finish(self, ghist: torch.Tensor, all_prefix: torch.Tensor, world: int):
+        self.ix.shard_finish(ghist.data_ptr(), all_prefix.data_ptr(), world)
+        return self.ix
+
+
+def build_global_filter(engine, group=None):
+    """Run the exchange protocol over torch.distributed; returns engine.finish()."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    h = engine.hist()
+    if world > 1:
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+    slots = engine.slots(h)
+    pre = engine.prefix(h, slots)
+    if world > 1:
+        allp = torch.empty(world * slots, dtype=pre.dtype, device=pre.device)
+        dist.all_gather_into_tensor(allp, pre.contiguous(), group=group)
+    else:
+        allp = pre
+    return engine.finish(h, allp, world)

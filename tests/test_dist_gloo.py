@@ -102,3 +102,54 @@ def test_merge_topk_ties_and_empty():
     ms, mi = fdist.merge_topk(s, i, 4)
     assert mi.tolist() == [[4, 9, 8, 3]]
     assert ms.tolist() == [[1.0, 1.0, 0.7, 0.5]]
+
+
+# --------------------------------------------- global-filter sharded build (8(e) B)
+GF = dict(L=3, K=2, D=16, iProbes=3, alpha=0.2, kappa=4, seed=1)
+
+
+def gf_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from shard_engine import OracleShardEngine
+    n = 3001
+    X, _ = make(n, 16, 1)
+    lo, hi = fdist.shard_range(n, world, rank)
+    kept = fdist.build_global_filter(OracleShardEngine(X[lo:hi], lo, **GF))
+    allk = [None] * world
+    dist.all_gather_object(allk, {k: v.tolist() for k, v in kept.items()})
+    if rank == 0:
+        import pickle
+        with open(out, "wb") as f:
+            pickle.dump(allk, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_global_filter_equals_single_index(tmp_path, world):
+    import pickle
+    out = str(tmp_path / "gf.pkl")
+    mp.spawn(gf_worker, args=(world, free_port(), out), nprocs=world, join=True)
+    allk = pickle.load(open(out, "rb"))
+    from oracle import oracle as orc
+    from shard_engine import ord_key
+    n = 3001
+    X, _ = make(n, 16, 1)
+    ox = orc.Index(X, L=GF["L"], K=GF["K"], D=GF["D"], iprobes=GF["iProbes"], alpha=GF["alpha"],
+                   kappa=GF["kappa"], seed=GF["seed"])
+    union = {}
+    for part in allk:
+        for k, v in part.items():
+            union.setdefault(k, []).extend(v)
+    total = 0
+    for t in range(GF["L"]):
+        off, ids, sc = ox.table(t)
+        for b in np.nonzero(np.diff(off))[0]:
+            keys = (((~ord_key(sc[off[b]:off[b + 1]])) & np.uint64(0xFFFFFFFF)) << np.uint64(32)) \
+                | ids[off[b]:off[b + 1]].astype(np.uint64)
+            got = np.sort(np.array(union.pop((t, int(b)), []), dtype=np.uint64))
+            assert np.array_equal(got, np.sort(keys)), (t, b)
+            total += len(keys)
+    assert not union  # no bucket kept by the shards that the single index drops
+    assert total == sum(len(ox.table(t)[1]) for t in range(GF["L"]))

@@ -223,3 +223,42 @@ def test_cluster_collect_natural_large_n(fpp, orc):
     gi, gs, gst = ix.query(Q, 20, 100, return_stats=True)
     oi, os_, ost = ox.query(Q, 20, 100)
     assert np.array_equal(gst, ost) and np.array_equal(gi, oi) and np.array_equal(gs, os_)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_global_filter_equals_single_gpu_index(fpp, orc, world):
+    # SURVEY 8(e) option B on one GPU: `world` shards built with fpp_shard_*, the
+    # all-reduce / all-gather done in-process; the union of the shard indexes
+    # must equal the 1-GPU index bucket for bucket, and the merged top-k must
+    # equal the 1-GPU top-k bit for bit.
+    import torch
+    from paper_2206_01382_b200 import dist as fdist
+    X = data(fpp, 30011, 64, 40, 0.3)
+    Q = data(fpp, 48, 64, 40, 0.3, stream=1)
+    prm = dict(L=3, K=2, D=64, iProbes=3, alpha=0.1, kappa=20)
+    n = len(X)
+    ranges = [fdist.shard_range(n, world, r) for r in range(world)]
+    engines = [fdist.GpuShardEngine(X[lo:hi], lo, device=0, **prm) for lo, hi in ranges]
+    gh = sum(e.hist() for e in engines)
+    slots = [e.slots(gh) for e in engines]
+    assert len(set(slots)) == 1
+    allp = torch.cat([e.prefix(gh, slots[0]) for e in engines])
+    shards = [e.finish(gh, allp, world) for e in engines]
+    full = fpp.Index.build(X, **prm)
+    for t in range(prm["L"]):
+        fo, fi, fs = full.table(t)
+        parts = [ix.table(t) for ix in shards]
+        for b in np.nonzero(np.diff(fo))[0][:3000]:
+            want = sorted(zip(fi[fo[b]:fo[b + 1]].tolist(), fs[fo[b]:fo[b + 1]].tolist()))
+            got = []
+            for (lo, _), (po, pi, ps) in zip(ranges, parts):
+                got += [(int(i) + lo, s) for i, s in zip(pi[po[b]:po[b + 1]], ps[po[b]:po[b + 1]])]
+            assert sorted(got) == want, (t, b)
+        assert sum(len(p[1]) for p in parts) == len(fi)
+    k, qp = 20, 400
+    fi, fsc = full.query(Q, k, qp)
+    outs = [ix.query(Q, k, qp) for ix in shards]
+    ms, mi = fdist.merge_topk(torch.from_numpy(np.concatenate([o[1] for o in outs], 1)),
+                              torch.from_numpy(np.concatenate([o[0].astype(np.int64) for o in outs], 1)), k)
+    assert np.array_equal(mi.numpy(), fi.astype(np.int64))
+    assert np.array_equal(ms.numpy(), fsc)
