@@ -236,7 +236,7 @@ struct ProbeArgs {
   uint64_t* dbg;          // optional [nq][peff] t*NB+b
   uint32_t* gbuf;         // [nq][peff] bucket-id scratch when not in shared memory
   uint64_t lstride;       // per-query list stride (L*K*s rounded up to 4 floats)
-  long long* dbg_clk;     // optional [nq][8]: phase clocks + search iterations
+  long long* dbg_clk;     // optional [nq][16]: phase clocks + search iterations
   uint32_t* ckey;         // [nq][ccap] candidate pair keys (scratch)
   uint32_t* cpair;        // [nq][ccap] candidate pairs (t<<22 | r1<<11 | r2)
   uint32_t ccap;
@@ -385,27 +385,34 @@ struct GridRef {
   bool forced;
 };
 
-// CTA per query (PS_THREADS threads, ~13 KB shared memory, so several query
+// CTA per query (PS_THREADS threads, ~22 KB shared memory, so several query
 // CTAs share an SM and hide each other's latency).  For the selection class:
-//  1. radix-select the m-th best key among the "arm" pairs (row 0 and column 0
-//     of every grid): a subset, so that key T_lo <= T*;
+//  1. T_lo: the grid corners bound the "arm" keys (row 0 and column 0 of every
+//     grid, each a sorted run); one 4096-bin histogram pass over the arms gives
+//     a bin edge with >= m arm keys above it, so T_lo <= T*;
 //  2. one staircase walk materialises every pair >= T_lo (key + packed
 //     (t, r1, r2)) into per-query global scratch;
-//  3. radix-select T* over that flat array (balanced, coalesced passes);
-//  4. count / collect ties at T*, pick the (r1, r2, t)-smallest ones;
-//  5. compact the selected pairs into bucket ids, then resolve every probe
-//     against the CSR directory with 8 independent loads per thread in flight.
+//  3. radix-select T* over that flat array (balanced, coalesced passes); the
+//     last digit's bin also yields the tie count and the ties to take;
+//  4. ties at T* (rare) are resolved in (r1, r2, t) order;
+//  5. the selected pairs are compacted (warp ballots, one pass), then every
+//     probe's codes -> bucket -> CSR directory entry is resolved with 8 probes
+//     per thread in flight.
 // If the candidate set overflows the scratch, every pass re-walks instead.
+// The emission order of the selection class is not canonical: the probe set
+// (and so the candidate set and the top-k) is.
+constexpr int PS_RBITS = 12;  // radix digit
 __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
   __shared__ uint64_t red[PS_THREADS / 32];
   __shared__ uint64_t ties[PS_TIE_CAP];
-  __shared__ uint32_t hist[2048];
-  __shared__ uint32_t n_ties, n_cand, sel_prefix, sel_rem;
+  __shared__ uint32_t hist[1 << PS_RBITS];
+  __shared__ uint32_t n_ties, n_cand, n_emit, sel_bin, sel_rem, sel_cnt;
   long long ck[8];
   ck[0] = clock64();
   const uint32_t q = blockIdx.x;
   const uint32_t L = a.L, K = a.K, s = a.s, D = a.D;
   const uint32_t n = s < D ? s : D, o = s > D ? s - D : 0;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const float* V = a.vals + (uint64_t)q * a.lstride;
   const uint32_t* Cq = a.codes + (uint64_t)q * a.lstride;
   uint32_t* ckey = a.ckey + (uint64_t)q * a.ccap;
@@ -413,9 +420,8 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
   if (threadIdx.x == 0) {
     n_ties = 0;
     n_cand = 0;
+    n_emit = 0;
   }
-  __syncthreads();
-  ck[1] = clock64();
   auto ngrids = [&](uint32_t cls) -> uint32_t { return (K == 2 && cls == 1) ? 2 * L : L; };
   auto grid = [&](uint32_t cls, uint32_t gi) -> GridRef {
     GridRef g;
@@ -459,44 +465,55 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
     rb = min(g.na, part * RB);
     re = min(g.na, rb + RB);
   };
-  // rank-th largest key (1-based) among enumerated keys in [base, base + 2^nbits)
-  auto radix_select = [&](uint64_t rank, uint32_t base, int nbits, auto&& enumerate) -> uint32_t {
+  // the bin of hist[0, nb) holding the rem-th largest key (1-based, counting
+  // from the top bin): sets sel_bin, sel_rem (rank inside the bin), sel_cnt
+  auto pick_bin = [&](int nb, uint32_t rem) {
+    constexpr int PER = (1 << PS_RBITS) / PS_THREADS;
+    uint32_t hv[PER], hs = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int bin = nb - 1 - (int)(threadIdx.x * PER + j);
+      hv[j] = bin >= 0 ? hist[bin] : 0;
+      hs += hv[j];
+    }
+    uint32_t tot;
+    uint32_t above = block_excl_scan_u32(hs, (uint32_t*)red, &tot);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int bin = nb - 1 - (int)(threadIdx.x * PER + j);
+      if (bin >= 0 && above < rem && rem <= above + hv[j]) {
+        sel_bin = (uint32_t)bin;
+        sel_rem = rem - above;
+        sel_cnt = hv[j];
+      }
+      above += hv[j];
+    }
+    __syncthreads();
+  };
+  // rank-th largest key (1-based) among enumerated keys in [base, base + 2^nbits);
+  // *eqc = how many keys equal it, *eqr = its rank among them
+  auto radix_select = [&](uint64_t rank, uint32_t base, int nbits, auto&& enumerate,
+                          uint32_t* eqc, uint32_t* eqr) -> uint32_t {
     uint32_t prefix = 0, mask = 0, rem = (uint32_t)rank;
-    int hb = nbits;
+    int hb = nbits < 1 ? 1 : nbits;
     while (hb > 0) {
-      const int w = hb < 11 ? hb : 11, sh = hb - w, nb = 1 << w;
+      const int w = hb < PS_RBITS ? hb : PS_RBITS, sh = hb - w, nb = 1 << w;
       for (int i = threadIdx.x; i < nb; i += blockDim.x) hist[i] = 0;
       __syncthreads();
-      enumerate([&](uint32_t key, uint32_t) {
+      enumerate([&](uint32_t key) {
         const uint32_t off = key - base;
         if ((off & mask) == prefix) atomicAdd(&hist[(off >> sh) & (nb - 1)], 1u);
       });
       __syncthreads();
-      uint32_t hv[8], hs = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int bin = nb - 1 - (int)(threadIdx.x * 8 + j);
-        hv[j] = bin >= 0 ? hist[bin] : 0;
-        hs += hv[j];
-      }
-      uint32_t tot;
-      uint32_t above = block_excl_scan_u32(hs, (uint32_t*)red, &tot);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int bin = nb - 1 - (int)(threadIdx.x * 8 + j);
-        if (bin >= 0 && above < rem && rem <= above + hv[j]) {
-          sel_prefix = prefix | ((uint32_t)bin << sh);
-          sel_rem = rem - above;
-        }
-        above += hv[j];
-      }
-      __syncthreads();
-      prefix = sel_prefix;
+      pick_bin(nb, rem);
+      prefix |= sel_bin << sh;
       rem = sel_rem;
+      *eqc = sel_cnt;
       mask |= (uint32_t)(nb - 1) << sh;
       hb = sh;
       __syncthreads();
     }
+    *eqr = rem;
     return base + prefix;
   };
   auto bitlen = [](uint32_t x) { return x ? 32 - __clz(x) : 0; };
@@ -516,6 +533,24 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       });
     }
   };
+  constexpr int EU = 4;  // flat passes: loads of EU elements issued before use
+  auto enum_keys = [&](auto&& visit) {
+    if (flat) {
+      for (uint32_t i0 = threadIdx.x; i0 < C; i0 += EU * blockDim.x) {
+        uint32_t kk[EU];
+#pragma unroll
+        for (int u = 0; u < EU; ++u) {
+          const uint32_t i = i0 + u * blockDim.x;
+          kk[u] = i < C ? __ldcg(ckey + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < EU; ++u)
+          if (i0 + u * blockDim.x < C) visit(kk[u]);
+      }
+    } else {
+      enum_stair([&](uint32_t key, uint32_t) { visit(key); });
+    }
+  };
   auto enum_cand = [&](auto&& visit) {
     if (flat) {
       for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) visit(__ldcg(ckey + i), __ldcg(cpair + i));
@@ -523,76 +558,147 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       enum_stair(visit);
     }
   };
+  __syncthreads();
+  uint32_t ties_total = 0, m = 0;  // keys == T*, and how many of them to take
   if (m_sel > 0) {
-    auto enum_arms = [&](auto&& visit) {  // row 0 and column 0 of every grid
-      for (uint32_t gi = threadIdx.x / 1; gi < NG * TPT; gi += blockDim.x) {
-        const uint32_t g0 = gi / TPT, part = gi - g0 * TPT;
-        const GridRef g = grid(sel, g0);
-        const uint32_t r0 = g.forced ? 1 : 0;
-        const uint32_t arm = (g.nb - r0) + (g.na - 1);
-        const uint32_t apt = (arm + TPT - 1) / TPT;
-        const uint32_t i0 = min(arm, part * apt), i1 = min(arm, i0 + apt);
-        for (uint32_t i = i0; i < i1; ++i) {
-          const uint32_t nrow = g.nb - r0;
-          const float sc = i < nrow ? g.va[0] + g.vb[r0 + i] : g.va[i - nrow + 1] + g.vb[0];
-          visit(ord_key(sc), 0u);
-        }
-      }
-    };
+    // ---- 1. T_lo from the arms (all grids of a class have the same arm length)
+    const GridRef g0 = grid(sel, 0);
+    const uint32_t A = (g0.nb - (g0.forced ? 1 : 0)) + (g0.na - 1);
     uint32_t amax = 0, amin = 0xffffffffu;
-    uint64_t an = 0;
-    enum_arms([&](uint32_t k, uint32_t) { amax = max(amax, k); amin = min(amin, k); ++an; });
+    for (uint32_t gi = threadIdx.x; gi < NG; gi += blockDim.x) {  // runs are sorted: corners
+      const GridRef g = grid(sel, gi);
+      const uint32_t r0 = g.forced ? 1 : 0;
+      if (g.nb > r0) {
+        amax = max(amax, ord_key(g.va[0] + g.vb[r0]));
+        amin = min(amin, ord_key(g.va[0] + g.vb[g.nb - 1]));
+      }
+      if (g.na > 1) {
+        amax = max(amax, ord_key(g.va[1] + g.vb[0]));
+        amin = min(amin, ord_key(g.va[g.na - 1] + g.vb[0]));
+      }
+    }
     uint64_t pk = ((uint64_t)amax << 32) | (0xffffffffu - amin);
     for (int sft = 16; sft > 0; sft >>= 1) {
       const uint64_t y = ((uint64_t)__shfl_xor_sync(FULL, (uint32_t)(pk >> 32), sft) << 32) |
                          __shfl_xor_sync(FULL, (uint32_t)pk, sft);
       pk = (max(pk >> 32, y >> 32) << 32) | max(pk & 0xffffffffu, y & 0xffffffffu);
     }
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = pk;
+    if (lane == 0) red[wp] = pk;
     __syncthreads();
     uint64_t mx = 0, nl = 0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+    for (int i = 0; i < nw; ++i) {
       mx = max(mx, red[i] >> 32);
       nl = max(nl, red[i] & 0xffffffffu);
     }
     amax = (uint32_t)mx;
     amin = 0xffffffffu - (uint32_t)nl;
-    an = block_sum_u64(an, red);
-    if (an >= m_sel) Tlo = radix_select(m_sel, amin, bitlen(amax - amin), enum_arms);
-    // materialise every selection-class pair >= Tlo (one atomic per row run)
-    for (uint32_t u = threadIdx.x; u < units; u += blockDim.x) {
-      GridRef g;
-      uint32_t rb, re;
-      unit(u, g, rb, re);
-      walk2_rows(g.va, g.vb, g.nb, rb, re, 0xffffffffu, Tlo, [&](uint32_t r1, uint32_t, uint32_t pb) {
-        const uint32_t st = (r1 == 0 && g.forced) ? 1 : 0;
-        if (pb <= st) return;
-        const uint32_t base = atomicAdd(&n_cand, pb - st);
-        if (base + (pb - st) > a.ccap) return;
-        const float x = g.va[r1];
-        for (uint32_t r2 = st; r2 < pb; ++r2) {
-          ckey[base + r2 - st] = ord_key(x + g.vb[r2]);
-          cpair[base + r2 - st] = pack(g.t, g.oa + r1, g.ob + r2);
+    __syncthreads();
+    if ((uint64_t)NG * A >= m_sel) {
+      const int nbits = bitlen(amax - amin);
+      const int sh = nbits > PS_RBITS ? nbits - PS_RBITS : 0, nb = 1 << (nbits - sh);
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      // warp per grid: the row arm vb[r0, nb) and the column arm va[1, na), lanes
+      // strided (coalesced), 8 loads per lane in flight
+      constexpr int AU = 8;
+      for (uint32_t gi = wp; gi < NG; gi += nw) {
+        const GridRef g = grid(sel, gi);
+        const uint32_t nrow = g.nb - (g.forced ? 1 : 0);
+        const float x0 = g.va[0], y0 = g.vb[0];
+        for (uint32_t i0 = lane; i0 < A; i0 += 32 * AU) {
+          float v[AU];
+#pragma unroll
+          for (int u = 0; u < AU; ++u) {
+            const uint32_t i = i0 + 32 * u;
+            v[u] = i < A ? (i < nrow ? g.vb[g.nb - nrow + i] : g.va[i - nrow + 1]) : 0.0f;
+          }
+#pragma unroll
+          for (int u = 0; u < AU; ++u) {
+            const uint32_t i = i0 + 32 * u;
+            if (i < A) {
+              const float sc = i < nrow ? x0 + v[u] : v[u] + y0;
+              atomicAdd(&hist[(ord_key(sc) - amin) >> sh], 1u);
+            }
+          }
         }
-      });
+      }
+      __syncthreads();
+      pick_bin(nb, (uint32_t)m_sel);
+      Tlo = amin + (sel_bin << sh);
+    }
+    ck[1] = clock64();
+    // ---- 2. materialise every selection-class pair >= Tlo.  Warp per grid.  The
+    // pairs >= Tlo of row r1 are a prefix [0, pb(r1)) and pb is non-increasing
+    // in r1.  Wide rows (pb > 32): lanes across r2, each row scanning only the
+    // previous row's prefix; ballots give the coalesced writes and the next
+    // bound.  Thin tail (pb <= 32): lanes across 32 rows, columns ascending
+    // until every lane's prefix has ended.
+    auto emit = [&](bool take, uint32_t key, uint32_t pr) {
+      const uint32_t tb = __ballot_sync(FULL, take);
+      if (tb) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&n_cand, __popc(tb));
+        base = __shfl_sync(FULL, base, 0);
+        if (take && base + __popc(tb) <= a.ccap) {
+          const uint32_t at = base + __popc(tb & ((1u << lane) - 1));
+          ckey[at] = key;
+          cpair[at] = pr;
+        }
+      }
+    };
+    for (uint32_t gi = wp; gi < NG; gi += nw) {
+      const GridRef g = grid(sel, gi);
+      uint32_t pb = g.nb, r1 = 0;
+      for (; r1 < g.na && pb > 32; ++r1) {
+        const float x = g.va[r1];
+        uint32_t npb = 0;
+        for (uint32_t c0 = 0; c0 < pb; c0 += 32) {
+          const uint32_t r2 = c0 + lane;
+          const uint32_t key = r2 < pb ? ord_key(x + g.vb[r2]) : 0;
+          const bool ge = r2 < pb && key >= Tlo;
+          const uint32_t bal = __ballot_sync(FULL, ge);
+          npb += __popc(bal);
+          emit(ge && !(g.forced && r1 == 0 && r2 == 0), key, pack(g.t, g.oa + r1, g.ob + r2));
+          if (bal != FULL) break;  // the prefix ended inside this chunk
+        }
+        pb = npb;
+      }
+      for (; r1 < g.na && pb > 0; r1 += 32) {
+        const uint32_t my = r1 + lane;
+        bool alive = my < g.na;
+        const float x = alive ? g.va[my] : 0.0f;
+        uint32_t cnt = 0;
+        for (uint32_t c0 = 0; c0 < pb; c0 += 4) {
+          float y[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) y[u] = c0 + u < pb ? g.vb[c0 + u] : 0.0f;
+          uint32_t any = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t c = c0 + u;
+            const uint32_t key = ord_key(x + y[u]);
+            alive = alive && c < pb && key >= Tlo;
+            cnt += alive;
+            any |= __ballot_sync(FULL, alive);
+            emit(alive && !(g.forced && my == 0 && c == 0), key, pack(g.t, g.oa + my, g.ob + c));
+          }
+          if (!any) break;
+        }
+        pb = __shfl_sync(FULL, cnt, 31);  // the next block's rows lie below row r1 + 31
+      }
     }
     __syncthreads();
     C = n_cand;
     flat = C <= a.ccap;
-    // every arm pair is >= every other pair of its row / column, so amax bounds all keys
-    Tstar = radix_select(m_sel, Tlo, bitlen(amax - Tlo), enum_cand);
+    ck[2] = clock64();
+    // ---- 3. T* (every arm pair is >= every other pair of its row / column, so
+    // amax bounds all keys)
+    Tstar = radix_select(m_sel, Tlo, bitlen(amax - Tlo), enum_keys, &ties_total, &m);
+  } else {
+    ck[1] = ck[2] = clock64();
   }
-  ck[2] = clock64();
-  uint64_t my_gt = 0, my_ge = 0;
-  if (m_sel > 0)
-    enum_cand([&](uint32_t key, uint32_t) {
-      my_gt += key > Tstar;
-      my_ge += key >= Tstar;
-    });
-  const uint64_t cgt = block_sum_u64(my_gt, red);
-  const uint64_t ties_total = block_sum_u64(my_ge, red) - cgt;
-  const uint64_t m = m_sel > cgt ? m_sel - cgt : 0;  // ties to take
+  ck[3] = clock64();
+  // ---- 4. ties at T*: take the m smallest in (r1, r2, t) order
   auto comp = [&](uint32_t pr) {  // (r1, r2, t) order on global ranks
     const uint32_t t = pr >> 22, r1 = (pr >> 11) & 2047u, r2 = pr & 2047u;
     return ((uint64_t)r1 * 2048u + r2) * L + t;
@@ -617,9 +723,9 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
         found = y < found ? y : found;
       }
       __syncthreads();
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = found;
+      if (lane == 0) red[wp] = found;
       __syncthreads();
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) Kstar = red[i] < Kstar ? red[i] : Kstar;
+      for (int i = 0; i < nw; ++i) Kstar = red[i] < Kstar ? red[i] : Kstar;
       __syncthreads();
     } else {
       auto count_lt = [&](uint64_t Kc) -> uint64_t {
@@ -636,19 +742,13 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       Kstar = lo;
     }
   }
-  ck[3] = clock64();
+  ck[4] = clock64();
+  // ---- 5. emission of packed pairs: forced buckets, whole classes, selection
   auto selected = [&](uint32_t key, uint32_t pr) {
     return key > Tstar || (key == Tstar && (Kstar == ~0ull || comp(pr) < Kstar));
   };
   uint32_t* gb_out = a.gbuf + (uint64_t)q * a.peff;
-  const uint32_t twoD = 2 * D;
-  const uint32_t NB = (uint32_t)a.NB;
-  auto bucket = [&](uint32_t pr) {
-    const uint32_t t = pr >> 22, r1 = (pr >> 11) & 2047u, r2 = pr & 2047u;
-    const uint32_t* c1 = Cq + (uint64_t)t * K * s;
-    return t * NB + (K == 2 ? __ldg(c1 + r1) * twoD + __ldg(c1 + s + r2) : __ldg(c1 + r1));
-  };
-  for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) gb_out[t] = bucket(t << 22);
+  for (uint32_t t = threadIdx.x; t < L; t += blockDim.x) gb_out[t] = pack(t, 0, 0);
   uint64_t slot0 = L;
   // whole classes before the selection class: every pair, via per-thread counts + scan
   for (uint32_t cls = 0; cls < sel; ++cls) {
@@ -659,89 +759,89 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       mine += (uint64_t)g.na * g.nb - (g.forced ? 1 : 0);
     }
     uint64_t x = mine;
-    {
-      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-      for (int sft = 1; sft < 32; sft <<= 1) {
-        const uint64_t y = ((uint64_t)__shfl_up_sync(FULL, (uint32_t)(x >> 32), sft) << 32) |
-                           __shfl_up_sync(FULL, (uint32_t)x, sft);
-        if (lane >= sft) x += y;
-      }
-      __syncthreads();
-      if (lane == 31) red[w] = x;
-      __syncthreads();
-      uint64_t wb = 0;
-      for (int i = 0; i < w; ++i) wb += red[i];
-      x = wb + x - mine;
+    for (int sft = 1; sft < 32; sft <<= 1) {
+      const uint64_t y = ((uint64_t)__shfl_up_sync(FULL, (uint32_t)(x >> 32), sft) << 32) |
+                         __shfl_up_sync(FULL, (uint32_t)x, sft);
+      if (lane >= sft) x += y;
     }
-    uint64_t slot = slot0 + x;
+    __syncthreads();
+    if (lane == 31) red[wp] = x;
+    __syncthreads();
+    uint64_t wb = 0;
+    for (int i = 0; i < wp; ++i) wb += red[i];
+    uint64_t slot = slot0 + wb + x - mine;
     for (uint32_t gi = threadIdx.x; gi < ng; gi += blockDim.x) {
       const GridRef g = grid(cls, gi);
       for (uint32_t r1 = 0; r1 < g.na; ++r1)
         for (uint32_t r2 = (r1 == 0 && g.forced) ? 1 : 0; r2 < g.nb; ++r2)
-          gb_out[slot++] = bucket(pack(g.t, g.oa + r1, g.ob + r2));
+          gb_out[slot++] = pack(g.t, g.oa + r1, g.ob + r2);
     }
     slot0 += Ccls[cls];
     __syncthreads();
   }
   if (m_sel > 0) {
-    // compaction of the selected pairs: per-thread counts, exclusive scan, write
-    uint64_t mine = 0;
-    uint32_t i_beg = 0, i_end = 0;
+    uint32_t* out = gb_out + slot0;
     if (flat) {
-      const uint32_t per = (C + blockDim.x - 1) / blockDim.x;
-      i_beg = min(C, threadIdx.x * per);
-      i_end = min(C, i_beg + per);
-      for (uint32_t i = i_beg; i < i_end; ++i) mine += selected(__ldcg(ckey + i), __ldcg(cpair + i));
-    } else {
-      enum_stair([&](uint32_t key, uint32_t pr) { mine += selected(key, pr); });
-    }
-    uint64_t x = mine;
-    {
-      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-      for (int sft = 1; sft < 32; sft <<= 1) {
-        const uint64_t y = ((uint64_t)__shfl_up_sync(FULL, (uint32_t)(x >> 32), sft) << 32) |
-                           __shfl_up_sync(FULL, (uint32_t)x, sft);
-        if (lane >= sft) x += y;
-      }
-      __syncthreads();
-      if (lane == 31) red[w] = x;
-      __syncthreads();
-      uint64_t wb = 0;
-      for (int i = 0; i < w; ++i) wb += red[i];
-      x = wb + x - mine;
-    }
-    uint64_t slot = slot0 + x;
-    if (flat) {
-      for (uint32_t i = i_beg; i < i_end; ++i) {
-        const uint32_t pr = __ldcg(cpair + i);
-        if (selected(__ldcg(ckey + i), pr)) gb_out[slot++] = bucket(pr);
+      // warp-aggregated compaction; the warp-uniform bound keeps ballots full
+      const uint32_t Cr = (C + 31) & ~31u;
+      for (uint32_t i0 = threadIdx.x; i0 < Cr; i0 += EU * blockDim.x) {
+        uint32_t kk[EU], pp[EU];
+#pragma unroll
+        for (int u = 0; u < EU; ++u) {
+          const uint32_t i = i0 + u * blockDim.x;
+          kk[u] = i < C ? __ldcg(ckey + i) : 0;
+          pp[u] = i < C ? __ldcg(cpair + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < EU; ++u) {
+          const uint32_t i = i0 + u * blockDim.x;
+          if (i0 + u * blockDim.x - lane < Cr) {  // warp-uniform
+            const bool take = i < C && selected(kk[u], pp[u]);
+            const uint32_t bal = __ballot_sync(FULL, take);
+            uint32_t base = 0;
+            if (lane == 0 && bal) base = atomicAdd(&n_emit, __popc(bal));
+            base = __shfl_sync(FULL, base, 0);
+            if (take) out[base + __popc(bal & ((1u << lane) - 1))] = pp[u];
+          }
+        }
       }
     } else {
       enum_stair([&](uint32_t key, uint32_t pr) {
-        if (selected(key, pr)) gb_out[slot++] = bucket(pr);
+        if (selected(key, pr)) out[atomicAdd(&n_emit, 1u)] = pr;
       });
     }
   }
   __syncthreads();
-  ck[4] = clock64();
-  // resolve probes against the directory: 8 probes (16 loads) in flight per thread
+  ck[5] = clock64();
+  // ---- 6. resolve probes: pair -> codes -> bucket -> CSR directory entry,
+  // 8 probes per thread in flight
   uint64_t* ppos = a.ppos + (uint64_t)q * a.peff;
   uint32_t* plen = a.plen + (uint64_t)q * a.peff;
   uint64_t* dbg = a.dbg ? a.dbg + (uint64_t)q * a.peff : nullptr;
   uint64_t esum = 0;
   const uint32_t P = (uint32_t)a.peff;
+  const uint32_t twoD = 2 * D;
+  const uint32_t NB = (uint32_t)a.NB;
   constexpr int UR = 8;
   for (uint32_t p0 = threadIdx.x; p0 < P; p0 += UR * blockDim.x) {
-    uint32_t gbk[UR], o0[UR], o1[UR], tt[UR];
+    uint32_t pr[UR], c1[UR], c2[UR], o0[UR], o1[UR];
 #pragma unroll
     for (int u = 0; u < UR; ++u) {
       const uint32_t pp = p0 + u * blockDim.x;
-      gbk[u] = pp < P ? __ldcg(gb_out + pp) : 0;
-      tt[u] = gbk[u] / NB;
+      pr[u] = pp < P ? __ldcg(gb_out + pp) : 0;
     }
 #pragma unroll
     for (int u = 0; u < UR; ++u) {
-      const uint32_t* of = a.offs + (uint64_t)tt[u] * (NB + 1) + (gbk[u] - tt[u] * NB);
+      const uint32_t t = pr[u] >> 22;
+      const uint32_t* cq = Cq + (uint64_t)t * K * s;
+      c1[u] = __ldg(cq + ((pr[u] >> 11) & 2047u));
+      c2[u] = K == 2 ? __ldg(cq + s + (pr[u] & 2047u)) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      const uint32_t t = pr[u] >> 22;
+      c1[u] = K == 2 ? c1[u] * twoD + c2[u] : c1[u];  // bucket within table t
+      const uint32_t* of = a.offs + (uint64_t)t * (NB + 1) + c1[u];
       o0[u] = __ldg(of);
       o1[u] = __ldg(of + 1);
     }
@@ -749,10 +849,11 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
     for (int u = 0; u < UR; ++u) {
       const uint32_t pp = p0 + u * blockDim.x;
       if (pp < P) {
-        ppos[pp] = __ldg(a.tbase + tt[u]) + o0[u];
+        const uint32_t t = pr[u] >> 22;
+        ppos[pp] = __ldg(a.tbase + t) + o0[u];
         plen[pp] = o1[u] - o0[u];
         esum += o1[u] - o0[u];
-        if (dbg) dbg[pp] = (uint64_t)tt[u] * a.NB + (gbk[u] - tt[u] * NB);
+        if (dbg) dbg[pp] = (uint64_t)t * a.NB + c1[u];
       }
     }
   }
@@ -760,10 +861,12 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
   if (threadIdx.x == 0) {
     a.eq[q] = (uint32_t)esum;
     if (a.dbg_clk) {
-      ck[5] = clock64();
-      ck[6] = flat;
-      ck[7] = C;
-      for (int i = 0; i < 8; ++i) a.dbg_clk[(uint64_t)q * 8 + i] = ck[i];
+      ck[6] = clock64();
+      long long* d = a.dbg_clk + (uint64_t)q * 16;
+      for (int i = 0; i < 7; ++i) d[i] = ck[i];
+      d[8] = flat;
+      d[9] = C;
+      d[10] = ties_total;
     }
   }
 }
@@ -797,8 +900,8 @@ __global__ void __launch_bounds__(1024) k_scan_eq(const uint32_t* __restrict__ e
 }
 
 // ----------------------------------------------------------------- collect
-constexpr int CO_THREADS = 512;
-constexpr int CO_TILE = 1024;
+constexpr int CO_THREADS = 1024;
+constexpr int CO_TILE = 2 * CO_THREADS;
 
 struct CollectArgs {
   const uint64_t* ppos;
@@ -1296,24 +1399,26 @@ static void stage_a(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
                nullptr, sl.ckey.p, sl.cpair.p, ccap};
   static const bool dbg_probe = getenv("FPP_DEBUG_PROBE") != nullptr;
   if (dbg_probe) {
-    sl.dbgclk.ensure((size_t)nqc * 8);
+    sl.dbgclk.ensure((size_t)nqc * 16);
     pa.dbg_clk = reinterpret_cast<long long*>(sl.dbgclk.p);
   }
   k_probe_select<<<nqc, PS_THREADS, 0, st>>>(pa);
   FPP_LAUNCH();
   if (dbg_probe) {
-    std::vector<long long> h((size_t)nqc * 8);
+    std::vector<long long> h((size_t)nqc * 16);
     FPP_CUDA(cudaMemcpyAsync(h.data(), pa.dbg_clk, h.size() * 8, cudaMemcpyDeviceToHost, st));
     FPP_CUDA(cudaStreamSynchronize(st));
-    double acc[6] = {0}, it = 0, ti = 0;
+    double acc[6] = {0}, fl = 0, cn = 0, ti = 0;
     for (uint32_t i = 0; i < nqc; ++i) {
-      for (int j = 0; j < 5; ++j) acc[j] += (double)(h[i * 8 + j + 1] - h[i * 8 + j]);
-      it += (double)h[i * 8 + 6];
-      ti += (double)h[i * 8 + 7];
+      for (int j = 0; j < 6; ++j) acc[j] += (double)(h[i * 16 + j + 1] - h[i * 16 + j]);
+      fl += (double)h[i * 16 + 8];
+      cn += (double)h[i * 16 + 9];
+      ti += (double)h[i * 16 + 10];
     }
-    fprintf(stderr, "[probe dbg] per query cycles: stage %.0f search %.0f ties %.0f emitcount %.0f "
-            "resolve %.0f | flat %.2f candidates %.1f\n", acc[0] / nqc, acc[1] / nqc, acc[2] / nqc,
-            acc[3] / nqc, acc[4] / nqc, it / nqc, ti / nqc);
+    fprintf(stderr, "[probe dbg] per query cycles: arms %.0f materialise %.0f radix %.0f ties %.0f "
+            "emit %.0f resolve %.0f | flat %.2f candidates %.1f ties %.2f\n", acc[0] / nqc,
+            acc[1] / nqc, acc[2] / nqc, acc[3] / nqc, acc[4] / nqc, acc[5] / nqc, fl / nqc,
+            cn / nqc, ti / nqc);
   }
   k_scan_eq<<<1, 1024, 0, st>>>(sl.eq.p, nqc, sl.coff.p);
   FPP_LAUNCH();
