@@ -137,7 +137,14 @@ __device__ __forceinline__ void rank_sort_exact(uint32_t (&kk)[EPT], int g, uint
   __syncwarp();
 }
 
-template <int P>
+// NS > 0: exact preselection.  Only the top nat = min(s, D) entries of the
+// ranked order are emitted, so a threshold Tq on the quantised value (found by
+// a few bisection steps on the group count) keeps c in [nat, NS] entries; they
+// are compacted and only NS keys are sorted.  Quantisation is monotone, so
+// every entry ranked before a kept one is kept too and the top nat of the kept
+// set are the top nat overall.  A warp whose groups do
+// not find such a threshold (heavy quantisation ties) sorts all P keys.
+template <int P, int NS>
 __global__ void __launch_bounds__(128)
 k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, uint32_t K,
               const uint32_t* __restrict__ signs, uint32_t L, uint32_t s, uint64_t lstride,
@@ -185,27 +192,81 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
     kk[e] = j < D ? (((4194303u - qv) << 10) | j) : 0xffffffffu;
   }
   __syncwarp();
-  rank_sort_exact<P, EPT, true>(kk, g, sk, pv);
   const uint64_t ob = q * lstride + (uint64_t)(t * K + f) * s;
   const uint32_t nat = s < D ? s : D;
-  if (active) {
+  // ranked entry r of the list (blocked layout r = g*E + e of a sorted key array)
+  auto emit = [&](uint32_t r, uint32_t key) {
+    if (!active) return;
+    if (r < nat) {
+      const uint32_t j = key & 1023u;
+      const float p = pv[j];
+      vals[ob + r] = fabsf(p);
+      codes[ob + r] = p < 0.0f ? D + j : j;
+    }
+    // opposite-signed vectors: same order, value |p|, flipped code
+    if (r + D < s) {
+      const uint32_t j = key & 1023u;
+      const float p = pv[j];
+      vals[ob + D + r] = fabsf(p);
+      codes[ob + D + r] = p < 0.0f ? j : D + j;
+    }
+  };
+  bool fast = false;
+  if constexpr (NS > 0) {
+    constexpr int E2 = NS / S::G;
+    uint32_t lo = 0, hi = 4194302u, tq = 0;
+    bool ok = false, fail = false;
+#pragma unroll 1
+    for (int it = 0; it < 24; ++it) {
+      if (__all_sync(FULL, ok || fail)) break;
+      const uint32_t mid = (lo + hi) >> 1;
+      uint32_t c = 0;
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const uint32_t r = (uint32_t)g * EPT + e;
-      if (r < nat) {
-        const uint32_t j = kk[e] & 1023u;
-        const float p = pv[j];
-        vals[ob + r] = fabsf(p);
-        codes[ob + r] = p < 0.0f ? D + j : j;
-      }
-      // opposite-signed vectors: same order, value |p|, flipped code
-      if (r + D < s) {
-        const uint32_t j = kk[e] & 1023u;
-        const float p = pv[j];
-        vals[ob + D + r] = fabsf(p);
-        codes[ob + D + r] = p < 0.0f ? j : D + j;
+      for (int e = 0; e < EPT; ++e) c += (kk[e] >> 10) <= mid;  // sentinels: 4194303 > mid
+#pragma unroll
+      for (int m = 1; m < S::G; m <<= 1) c += __shfl_xor_sync(FULL, c, m);
+      if (!ok && !fail) {
+        if (c >= nat) {
+          if (c <= (uint32_t)NS) { ok = true; tq = mid; }
+          else if (lo >= mid) fail = true;
+          else hi = mid;
+        } else {
+          lo = mid + 1;
+          if (lo > hi) fail = true;
+        }
       }
     }
+    fast = __all_sync(FULL, ok);
+    if (fast) {
+      uint32_t cl = 0;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) cl += (kk[e] >> 10) <= tq;
+      uint32_t x = cl;  // inclusive scan over the group's lanes
+#pragma unroll
+      for (int o = 1; o < S::G; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, x, o);
+        if (g >= o) x += y;
+      }
+      const uint32_t ctot = __shfl_sync(FULL, x, (lane / S::G) * S::G + S::G - 1);
+      uint32_t pos = x - cl;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e)
+        if ((kk[e] >> 10) <= tq) sk[pos++] = kk[e];
+      for (uint32_t i = ctot + g; i < (uint32_t)NS; i += S::G) sk[i] = 0xffffffffu;
+      __syncwarp();
+      uint32_t k2[E2];
+#pragma unroll
+      for (int e = 0; e < E2; ++e) k2[e] = sk[g * E2 + e];
+      __syncwarp();
+      rank_sort_exact<NS, E2, true>(k2, g, sk, pv);
+#pragma unroll
+      for (int e = 0; e < E2; ++e) emit((uint32_t)g * E2 + e, k2[e]);
+    }
+  }
+  if (!fast) {
+    rank_sort_exact<P, EPT, true>(kk, g, sk, pv);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) emit((uint32_t)g * EPT + e, kk[e]);
   }
 }
 
@@ -1315,15 +1376,29 @@ void launch_query_lists(const Index& ix, const float* Qd, uint64_t nq, uint32_t 
   const uint32_t d = ix.d, D = ix.prm.D, K = ix.prm.K, L = ix.prm.L;
   const uint32_t G = ix.P < 32 ? 1 : ix.P / 32;
   const unsigned grid = (unsigned)((nq * L * K * G + 127) / 128);
-#define FPP_QL_CASE(PP)                                                                      \
-  case PP:                                                                                   \
-    k_query_lists<PP><<<grid, 128, 0, s>>>(Qd, nq, d, D, K, ix.signs, L, s_cap, lstride, vals, codes); \
+  // preselection width: the smallest of P/4, P/2 leaving a margin of P/16 above
+  // nat = min(s, D) (0 = sort all P keys)
+  const uint32_t nat = std::min(s_cap, D), P = ix.P;
+  const int ns = P < 256 ? 0 : (nat + P / 16 <= P / 4 ? 4 : (nat + P / 16 <= P / 2 ? 2 : 0));
+#define FPP_QL_LAUNCH(PP, NSV) \
+  k_query_lists<PP, NSV><<<grid, 128, 0, s>>>(Qd, nq, d, D, K, ix.signs, L, s_cap, lstride, vals, codes)
+#define FPP_QL_CASE(PP)         \
+  case PP:                      \
+    FPP_QL_LAUNCH(PP, 0);       \
+    break;
+#define FPP_QL_CASE_NS(PP)                         \
+  case PP:                                         \
+    if (ns == 4) FPP_QL_LAUNCH(PP, PP / 4);        \
+    else if (ns == 2) FPP_QL_LAUNCH(PP, PP / 2);   \
+    else FPP_QL_LAUNCH(PP, 0);                     \
     break;
   switch (ix.P) {
     FPP_QL_CASE(2) FPP_QL_CASE(4) FPP_QL_CASE(8) FPP_QL_CASE(16) FPP_QL_CASE(32)
-    FPP_QL_CASE(64) FPP_QL_CASE(128) FPP_QL_CASE(256) FPP_QL_CASE(512) FPP_QL_CASE(1024)
+    FPP_QL_CASE(64) FPP_QL_CASE(128) FPP_QL_CASE_NS(256) FPP_QL_CASE_NS(512) FPP_QL_CASE_NS(1024)
     default: fail(FPP_ERR_UNSUPPORTED, "query: padded dimension > 1024 not supported on GPU");
   }
+#undef FPP_QL_CASE_NS
+#undef FPP_QL_LAUNCH
 #undef FPP_QL_CASE
   FPP_LAUNCH();
 }

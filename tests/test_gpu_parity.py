@@ -110,6 +110,29 @@ def test_query_lists_bitexact(fpp, orc, qp):
         assert np.array_equal(gc[i], oc), (qp, i)
 
 
+@pytest.mark.parametrize("K,D,d,qps", [
+    (2, 512, 300, [1000, 5000, 10000, 20000]),  # d padded 300 -> 512
+    (2, 512, 400, [2000, 4000]),
+    (2, 1024, 960, [1000, 10000, 40000]),
+    (2, 256, 200, [500, 3000, 9000]),
+    (1, 512, 500, [100, 200, 700]),
+])
+def test_query_lists_preselect(fpp, orc, K, D, d, qps):
+    # P >= 256 lists are built from a threshold-preselected subset (NS = P/4 or
+    # P/2 keys sorted instead of P); s near and past the NS margins, K = 1
+    X = data(fpp, 2000, d, 10, 0.3)
+    Q = data(fpp, 12, d, 10, 0.3, stream=1)
+    ix = fpp.Index.build(X, L=3, K=K, D=D, iProbes=2, alpha=0.1)
+    ox = orc.Index(X, L=3, K=K, D=D, iprobes=2, alpha=0.1)
+    for qp in qps:
+        s = ix.cap(qp)
+        gv, gc = ix.query_lists(Q, qp)
+        for i in range(len(Q)):
+            ov, oc = ox.query_lists(Q[i], s)
+            assert np.array_equal(bits(gv[i]), bits(ov)), (qp, i)
+            assert np.array_equal(gc[i], oc), (qp, i)
+
+
 QUERY_CASES = [
     # name, n, d, clusters, sigma, L, K, D, ip, alpha, kappa, qprobes list
     ("c1_like", 20000, 128, 0, 0.0, 10, 2, 128, 3, 0.1, 20, [10, 100, 1000, 3000]),
