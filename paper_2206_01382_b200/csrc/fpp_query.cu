@@ -962,7 +962,6 @@ __global__ void __launch_bounds__(1024) k_scan_eq(const uint32_t* __restrict__ e
 
 // ----------------------------------------------------------------- collect
 constexpr int CO_THREADS = 1024;
-constexpr int CO_TILE = 2 * CO_THREADS;
 
 struct CollectArgs {
   const uint64_t* ppos;
@@ -978,100 +977,103 @@ struct CollectArgs {
   uint32_t* counter;     // dynamic query fetch
 };
 
-__global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
-  extern __shared__ uint32_t sbm[];
-  __shared__ uint32_t pref[CO_TILE + 1];
-  __shared__ uint64_t tpos[CO_TILE];
-  __shared__ uint32_t sh[32];
-  __shared__ uint32_t ucount;
-  __shared__ uint32_t qsh;
-  uint32_t* bm = a.gbitmap ? a.gbitmap + (uint64_t)blockIdx.x * a.nwords : sbm;
-  if (a.gbitmap) {  // global bitmaps start zeroed and are cleared by candidate list
+// Warp-cooperative walk over one query's probes.  A warp takes 32 probes at a
+// time (lane i: probe i's (pos, len), coalesced), scans the lengths in
+// registers, and then covers the chunk's entries 32 at a time: lane l takes
+// entry e = e0 + l and finds its probe by a 5-step shuffle binary search over
+// the exclusive offsets, so consecutive lanes read consecutive ids of a bucket.
+// CO_UNROLL rounds issue their id loads before any is consumed.  `tas(id)`
+// tests-and-sets the visited bit and returns whether the id is new; new ids are
+// appended to `out` with one counter atomic per warp round.
+constexpr int CO_UNROLL = 4;
+template <class NextChunk, class TAS>
+__device__ __forceinline__ void collect_walk(const uint64_t* pp, const uint32_t* pl, uint32_t P,
+                                             const uint32_t* __restrict__ ids, uint32_t* out,
+                                             uint32_t* ucount, NextChunk&& next_chunk, TAS&& tas) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t c = next_chunk(); c * 32 < P; c = next_chunk()) {
+    const uint32_t i = c * 32 + lane;
+    const uint32_t len = i < P ? pl[i] : 0;
+    const uint64_t pos = i < P ? pp[i] : 0;
+    uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t T = __shfl_sync(FULL, incl, 31);
+    const uint32_t excl = incl - len;
+    for (uint32_t e0 = 0; e0 < T; e0 += 32 * CO_UNROLL) {
+      uint32_t idv[CO_UNROLL];
+#pragma unroll
+      for (int u = 0; u < CO_UNROLL; ++u) {
+        const uint32_t e = e0 + 32 * u + lane;
+        uint32_t lo = 0;  // largest lane with excl <= e (it has len > 0 when e < T)
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+          const uint32_t cnd = lo + st;
+          if (__shfl_sync(FULL, excl, cnd) <= e) lo = cnd;
+        }
+        const uint32_t plo = __shfl_sync(FULL, (uint32_t)pos, lo);
+        const uint32_t phi = __shfl_sync(FULL, (uint32_t)(pos >> 32), lo);
+        const uint32_t ex = __shfl_sync(FULL, excl, lo);
+        idv[u] = e < T ? __ldg(ids + ((((uint64_t)phi << 32) | plo) + (e - ex))) : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < CO_UNROLL; ++u) {
+        const bool isnew = idv[u] != 0xffffffffu && tas(idv[u]);
+        const uint32_t bal = __ballot_sync(FULL, isnew);
+        if (bal) {
+          uint32_t base = 0;
+          if (lane == 0) base = atomicAdd(ucount, __popc(bal));
+          base = __shfl_sync(FULL, base, 0);
+          if (isnew) out[base + __popc(bal & ((1u << lane) - 1))] = idv[u];
+        }
+      }
+    }
   }
+}
+
+// CTA per query (persistent CTAs fetch queries dynamically); the visited
+// bitmap lives in shared memory (n bits) or, for large shards, in a per-CTA
+// global-memory region that is cleared again through the candidate list.
+__global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
+  extern __shared__ __align__(16) uint32_t sbm[];
+  __shared__ uint32_t ucount, qsh, nextc;
+  uint32_t* bm = a.gbitmap ? a.gbitmap + (uint64_t)blockIdx.x * a.nwords : sbm;
   for (;;) {
-    if (threadIdx.x == 0) qsh = atomicAdd(a.counter, 1u);
+    if (threadIdx.x == 0) {
+      qsh = atomicAdd(a.counter, 1u);
+      ucount = 0;
+      nextc = 0;
+    }
+    if (!a.gbitmap) {
+      const uint32_t n4 = a.nwords >> 2;
+      uint4* b4 = reinterpret_cast<uint4*>(sbm);
+      for (uint32_t w = threadIdx.x; w < n4; w += blockDim.x) b4[w] = make_uint4(0, 0, 0, 0);
+      for (uint32_t w = n4 * 4 + threadIdx.x; w < a.nwords; w += blockDim.x) sbm[w] = 0;
+    }
     __syncthreads();
     const uint32_t q = qsh;
     if (q >= a.nq) break;
-    if (!a.gbitmap) {
-      for (uint32_t w = threadIdx.x; w < a.nwords; w += blockDim.x) bm[w] = 0;
-    }
-    if (threadIdx.x == 0) ucount = 0;
-    __syncthreads();
     uint32_t* out = a.cands + a.coff[q];
-    const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
-    const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
-    for (uint64_t p0 = 0; p0 < a.peff; p0 += CO_TILE) {
-      const uint32_t np = (uint32_t)(a.peff - p0 < (uint64_t)CO_TILE ? a.peff - p0 : (uint64_t)CO_TILE);
-      uint32_t v[2] = {0, 0};
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const uint32_t i = threadIdx.x * 2 + k;
-        if (i < np) {
-          v[k] = pl[p0 + i];
-          tpos[i] = pp[p0 + i];
-        }
-      }
-      uint32_t tot;
-      const uint32_t ex = block_excl_scan_u32(v[0] + v[1], sh, &tot);
-      if (threadIdx.x * 2 < np) pref[threadIdx.x * 2] = ex;
-      if (threadIdx.x * 2 + 1 < np) pref[threadIdx.x * 2 + 1] = ex + v[0];
-      if (threadIdx.x == 0) pref[np] = tot;
-      __syncthreads();
-      // thread-contiguous entry ranges: one binary search per thread, then a
-      // forward walk with 4 independent id loads in flight
-      const uint32_t per = (tot + blockDim.x - 1) / blockDim.x;
-      uint32_t e = min(tot, threadIdx.x * per);
-      const uint32_t e_end = min(tot, e + per);
-      uint32_t p = 0;
-      {
-        uint32_t lo = 0, hi = np;
-        while (hi - lo > 1) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (pref[mid] <= e) lo = mid;
-          else hi = mid;
-        }
-        p = lo;
-      }
-      while (e < e_end) {
-        uint32_t idv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          idv[u] = 0xffffffffu;
-          if (e + u < e_end) {
-            while (pref[p + 1] <= e + u) ++p;
-            idv[u] = __ldg(a.ids + tpos[p] + (e + u - pref[p]));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t id = idv[u];
-          bool isnew = false;
-          if (id != 0xffffffffu) {
-            const uint32_t bit = 1u << (id & 31);
-            isnew = !(atomicOr(bm + (id >> 5), bit) & bit);
-          }
-          const unsigned act = __activemask();
-          const unsigned bal = __ballot_sync(act, isnew);
-          if (bal) {
-            const int lane = threadIdx.x & 31;
-            const int leader = __ffs(act) - 1;
-            uint32_t base = 0;
-            if (lane == leader) base = atomicAdd(&ucount, __popc(bal));
-            base = __shfl_sync(act, base, leader);
-            if (isnew) out[base + __popc(bal & ((1u << lane) - 1))] = id;
-          }
-        }
-        e += 4;
-      }
-      __syncthreads();
-    }
+    const uint32_t P = (uint32_t)a.peff;
+    collect_walk(a.ppos + (uint64_t)q * a.peff, a.plen + (uint64_t)q * a.peff, P, a.ids, out,
+                 &ucount,
+                 [&]() {
+                   uint32_t c = 0;
+                   if ((threadIdx.x & 31) == 0) c = atomicAdd(&nextc, 1u);
+                   return __shfl_sync(FULL, c, 0);
+                 },
+                 [&](uint32_t id) {
+                   const uint32_t bit = 1u << (id & 31);
+                   return !(atomicOr(bm + (id >> 5), bit) & bit);
+                 });
+    __syncthreads();
     const uint32_t U = ucount;
     if (threadIdx.x == 0) a.uq[q] = U;
-    if (a.gbitmap) {
-      __syncthreads();
+    if (a.gbitmap)
       for (uint32_t c = threadIdx.x; c < U; c += blockDim.x) bm[out[c] >> 5] = 0;
-    }
     __syncthreads();
   }
 }
@@ -1079,7 +1081,8 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
 // Large shards (n bits > one SM's shared memory): one thread-block cluster of
 // CO_CLUSTER CTAs per query, the visited bitmap split into per-CTA slices of
 // shared memory and tested-and-set through DSMEM atomics on the owning CTA
-// (cluster.map_shared_rank); the per-query candidate counter lives in CTA 0.
+// (cluster.map_shared_rank); the per-query candidate counter lives in CTA 0,
+// and the probe chunks are dealt round-robin over the cluster's CTAs.
 constexpr int CO_CLUSTER = 8;
 
 __global__ void __cluster_dims__(CO_CLUSTER, 1, 1) __launch_bounds__(CO_THREADS, 1)
@@ -1087,85 +1090,32 @@ k_collect_cluster(CollectArgs a, uint32_t slice_words) {
   cg::cluster_group cluster = cg::this_cluster();
   const uint32_t rank = cluster.block_rank();
   const uint32_t cid = blockIdx.x / CO_CLUSTER, ncl = gridDim.x / CO_CLUSTER;
-  extern __shared__ uint32_t sbm[];
-  __shared__ uint32_t pref[CO_TILE + 1];
-  __shared__ uint64_t tpos[CO_TILE];
-  __shared__ uint32_t sh[32];
-  __shared__ uint32_t ucount;
+  extern __shared__ __align__(16) uint32_t sbm[];
+  __shared__ uint32_t ucount, nextc;
   uint32_t* ucount0 = cluster.map_shared_rank(&ucount, 0);
   const uint32_t slice_bits = slice_words * 32;
   for (uint32_t q = cid; q < a.nq; q += ncl) {
     for (uint32_t w = threadIdx.x; w < slice_words; w += blockDim.x) sbm[w] = 0;
-    if (rank == 0 && threadIdx.x == 0) ucount = 0;
+    if (threadIdx.x == 0) {
+      ucount = 0;
+      nextc = 0;
+    }
     cluster.sync();
     uint32_t* out = a.cands + a.coff[q];
-    const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
-    const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
-    for (uint64_t p0 = (uint64_t)rank * CO_TILE; p0 < a.peff; p0 += (uint64_t)CO_CLUSTER * CO_TILE) {
-      const uint32_t np = (uint32_t)(a.peff - p0 < (uint64_t)CO_TILE ? a.peff - p0 : (uint64_t)CO_TILE);
-      uint32_t v[2] = {0, 0};
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const uint32_t i = threadIdx.x * 2 + k;
-        if (i < np) {
-          v[k] = pl[p0 + i];
-          tpos[i] = pp[p0 + i];
-        }
-      }
-      uint32_t tot;
-      const uint32_t ex = block_excl_scan_u32(v[0] + v[1], sh, &tot);
-      if (threadIdx.x * 2 < np) pref[threadIdx.x * 2] = ex;
-      if (threadIdx.x * 2 + 1 < np) pref[threadIdx.x * 2 + 1] = ex + v[0];
-      if (threadIdx.x == 0) pref[np] = tot;
-      __syncthreads();
-      const uint32_t per = (tot + blockDim.x - 1) / blockDim.x;
-      uint32_t e = min(tot, threadIdx.x * per);
-      const uint32_t e_end = min(tot, e + per);
-      uint32_t p = 0;
-      {
-        uint32_t lo = 0, hi = np;
-        while (hi - lo > 1) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (pref[mid] <= e) lo = mid;
-          else hi = mid;
-        }
-        p = lo;
-      }
-      while (e < e_end) {
-        uint32_t idv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          idv[u] = 0xffffffffu;
-          if (e + u < e_end) {
-            while (pref[p + 1] <= e + u) ++p;
-            idv[u] = __ldg(a.ids + tpos[p] + (e + u - pref[p]));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t id = idv[u];
-          bool isnew = false;
-          if (id != 0xffffffffu) {
-            const uint32_t owner = id / slice_bits, lb = id - owner * slice_bits;
-            uint32_t* rb = cluster.map_shared_rank(sbm, owner);
-            const uint32_t bit = 1u << (lb & 31);
-            isnew = !(atomicOr(rb + (lb >> 5), bit) & bit);
-          }
-          const unsigned act = __activemask();
-          const unsigned bal = __ballot_sync(act, isnew);
-          if (bal) {
-            const int lane = threadIdx.x & 31;
-            const int leader = __ffs(act) - 1;
-            uint32_t base = 0;
-            if (lane == leader) base = atomicAdd(ucount0, __popc(bal));
-            base = __shfl_sync(act, base, leader);
-            if (isnew) out[base + __popc(bal & ((1u << lane) - 1))] = id;
-          }
-        }
-        e += 4;
-      }
-      __syncthreads();
-    }
+    const uint32_t P = (uint32_t)a.peff;
+    collect_walk(a.ppos + (uint64_t)q * a.peff, a.plen + (uint64_t)q * a.peff, P, a.ids, out,
+                 ucount0,
+                 [&]() {
+                   uint32_t c = 0;
+                   if ((threadIdx.x & 31) == 0) c = atomicAdd(&nextc, 1u);
+                   return __shfl_sync(FULL, c, 0) * CO_CLUSTER + rank;
+                 },
+                 [&](uint32_t id) {
+                   const uint32_t owner = id / slice_bits, lb = id - owner * slice_bits;
+                   uint32_t* rb = cluster.map_shared_rank(sbm, owner);
+                   const uint32_t bit = 1u << (lb & 31);
+                   return !(atomicOr(rb + (lb >> 5), bit) & bit);
+                 });
     cluster.sync();
     if (rank == 0 && threadIdx.x == 0) a.uq[q] = ucount;
   }
@@ -1515,7 +1465,7 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   const uint32_t nwords = (uint32_t)((ix.n + 31) / 32);
   CollectArgs ca{sl.ppos.p, sl.plen.p, peff, ix.ids, sl.coff.p, sl.cands.p, sl.uq.p,
                  nqc, nwords, nullptr, sl.counter.p};
-  const size_t static_co = (CO_TILE + 1) * 4 + CO_TILE * 8 + 32 * 4 + 16;
+  const size_t static_co = 64;
   size_t co_smem = (size_t)nwords * 4;
   unsigned co_grid;
   const int sms = sm_count();
@@ -1615,8 +1565,10 @@ void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32
   if (!ix.sA) {
     int lo = 0, hi = 0;
     FPP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sA, cudaStreamNonBlocking, lo));
-    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sB, cudaStreamNonBlocking, hi));
+    const char* pe = getenv("FPP_PRIO");  // experiment knob: 0 equal, 2 = A high
+    const int pm = pe ? atoi(pe) : 1;
+    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sA, cudaStreamNonBlocking, pm == 2 ? hi : lo));
+    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sB, cudaStreamNonBlocking, pm == 1 ? hi : lo));
     FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_fork, cudaEventDisableTiming));
     FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_join, cudaEventDisableTiming));
     FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_join2, cudaEventDisableTiming));
