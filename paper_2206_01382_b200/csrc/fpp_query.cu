@@ -1122,11 +1122,19 @@ k_collect_cluster(CollectArgs a, uint32_t slice_words) {
 }
 
 // ------------------------------------------------------------------- score
-constexpr int SC_WARPS = 4;
-constexpr int SC_SLICE = 32;              // floats per row slice
-constexpr int SC_STAGES = 4;              // cp.async ring depth per warp
-constexpr int SC_ROWPAD = SC_SLICE + 4;   // odd number of 16 B units: conflict-free LDS.128
-constexpr int SC_STAGE_FLOATS = 32 * SC_ROWPAD;
+#ifndef FPP_SC_WARPS
+#define FPP_SC_WARPS 4
+#endif
+constexpr int SC_WARPS = FPP_SC_WARPS;
+// Ring geometry <SL, ST>: SL floats per row slice (a multiple of 32), ST stages
+// per warp.  Wide rows use 96-float slices x 2 stages (longer contiguous runs
+// per row per request, measurably better DRAM efficiency on random row
+// gathers); narrow rows (d < 192) use 32 x 4, whose slice matches the row.
+template <int SL>
+struct ScRing {
+  static constexpr int ROWPAD = SL + 4;  // odd number of 16 B units: conflict-free LDS.128
+  static constexpr int STAGE_FLOATS = 32 * ROWPAD;
+};
 
 struct ScoreArgs {
   const float* X;
@@ -1188,8 +1196,10 @@ __device__ __forceinline__ void topk_insert(double& bs, uint32_t& bi, uint32_t k
 // chunk (l & 7) of rows (l >> 3) + 4*it, it = 0..7, with row addresses resolved
 // once per batch, so a slice costs 8 cp.async per lane.  Lane r then folds row
 // r's slice into its fp64 accumulator in the reference's sequential order.
-template <bool VEC>
+template <bool VEC, int SC_SLICE, int SC_STAGES>
 __global__ void __launch_bounds__(SC_WARPS * 32, 2) k_score(ScoreArgs a) {
+  constexpr int SC_ROWPAD = ScRing<SC_SLICE>::ROWPAD;
+  constexpr int SC_STAGE_FLOATS = ScRing<SC_SLICE>::STAGE_FLOATS;
   extern __shared__ __align__(16) unsigned char smraw[];
   const uint32_t d = a.d;
   double* qd = reinterpret_cast<double*>(smraw);
@@ -1232,16 +1242,21 @@ __global__ void __launch_bounds__(SC_WARPS * 32, 2) k_score(ScoreArgs a) {
       const uint32_t col0 = ic * SC_SLICE;
       const uint32_t len = min((uint32_t)SC_SLICE, d - col0);
       if (VEC) {
-        if ((uint32_t)kk < (len >> 2)) {
 #pragma unroll
-          for (int it = 0; it < 8; ++it)
-            if (rp[it]) cp_async16(buf + (rbase + 4 * it) * SC_ROWPAD + kk * 4, rp[it] + col0 + kk * 4);
+        for (int h = 0; h < SC_SLICE / 32; ++h) {  // 16 B chunks kk + 8h of each row
+          const uint32_t ch = kk + 8 * h;
+          if (ch < (len >> 2)) {
+#pragma unroll
+            for (int it = 0; it < 8; ++it)
+              if (rp[it]) cp_async16(buf + (rbase + 4 * it) * SC_ROWPAD + ch * 4, rp[it] + col0 + ch * 4);
+          }
         }
       } else {
         for (int r = 0; r < 32; ++r) {
           const uint32_t idr = __shfl_sync(FULL, my_id, r);
-          if (idr != 0xffffffffu && (uint32_t)lane < len)
-            cp_async4(buf + r * SC_ROWPAD + lane, X + (uint64_t)idr * d + col0 + lane);
+          if (idr != 0xffffffffu)
+            for (uint32_t c = lane; c < len; c += 32)
+              cp_async4(buf + r * SC_ROWPAD + c, X + (uint64_t)idr * d + col0 + c);
         }
       }
       if (++ic == nsl) {
@@ -1314,8 +1329,8 @@ __global__ void __launch_bounds__(SC_WARPS * 32, 2) k_score(ScoreArgs a) {
   }
 }
 
-static size_t score_smem(uint32_t d) {
-  return ((d * 8 + 127) / 128) * 128 + (size_t)SC_WARPS * SC_STAGES * SC_STAGE_FLOATS * 4;
+static size_t score_smem(uint32_t d, int sl, int st) {
+  return ((d * 8 + 127) / 128) * 128 + (size_t)SC_WARPS * st * 32 * (sl + 4) * 4;
 }
 
 // ------------------------------------------------------------ host driver
@@ -1513,15 +1528,18 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   ix.timer.begin(PH_SCORE, st, &e0);
   ScoreArgs sa{ix.X, ix.d, Qd, sl.coff.p, sl.cands.p, sl.uq.p, sl.eq.p, peff, k,
                ix.prm.id_offset, ids_d, scores_d, stats_d};
-  const size_t sc_smem = score_smem(ix.d);
+  auto launch_score = [&](auto kern, int sl, int stg) {
+    const size_t sm = score_smem(ix.d, sl, stg);
+    FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kern<<<nqc, SC_WARPS * 32, sm, st>>>(sa);
+  };
+  const bool wide = ix.d >= 192;
   if ((ix.d & 3u) == 0) {
-    FPP_CUDA(cudaFuncSetAttribute(k_score<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sc_smem));
-    k_score<true><<<nqc, SC_WARPS * 32, sc_smem, st>>>(sa);
+    if (wide) launch_score(k_score<true, 96, 2>, 96, 2);
+    else launch_score(k_score<true, 32, 4>, 32, 4);
   } else {
-    FPP_CUDA(cudaFuncSetAttribute(k_score<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sc_smem));
-    k_score<false><<<nqc, SC_WARPS * 32, sc_smem, st>>>(sa);
+    if (wide) launch_score(k_score<false, 96, 2>, 96, 2);
+    else launch_score(k_score<false, 32, 4>, 32, 4);
   }
   FPP_LAUNCH();
   ix.timer.end(PH_SCORE, e0, st);

@@ -140,6 +140,9 @@ QUERY_CASES = [
     ("c4_like_s_gt_D", 20000, 128, 100, 0.25, 6, 2, 128, 3, 0.01, 20, [5000, 100000]),
     ("K1", 5000, 64, 0, 0.0, 6, 1, 64, 2, 0.5, 10, [6, 60, 768]),
     ("wide_c3_like", 4000, 960, 20, 0.2, 4, 2, 1024, 3, 0.02, 20, [1000, 10000]),
+    # d % 4 != 0: the scalar cp.async score path, narrow (32-float slices) and wide (96)
+    ("odd_d_narrow", 6000, 17, 10, 0.3, 5, 2, 32, 3, 0.2, 10, [40, 400]),
+    ("odd_d_wide", 6000, 250, 10, 0.3, 5, 2, 256, 3, 0.1, 10, [500, 3000]),
 ]
 
 
