@@ -194,18 +194,22 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
   __syncwarp();
   const uint64_t ob = q * lstride + (uint64_t)(t * K + f) * s;
   const uint32_t nat = s < D ? s : D;
-  // ranked entry r of the list (blocked layout r = g*E + e of a sorted key array)
-  auto emit = [&](uint32_t r, uint32_t key) {
+  // the group's sorted keys go to sk (blocked layout r = g*E + e), then a rolled
+  // loop writes ranks r = g, g+G, ... (coalesced stores, small code)
+  auto emit_all = [&]() {
+    __syncwarp();
     if (!active) return;
-    if (r < nat) {
-      const uint32_t j = key & 1023u;
+#pragma unroll 1
+    for (uint32_t r = g; r < nat; r += S::G) {
+      const uint32_t j = sk[r] & 1023u;
       const float p = pv[j];
       vals[ob + r] = fabsf(p);
       codes[ob + r] = p < 0.0f ? D + j : j;
     }
     // opposite-signed vectors: same order, value |p|, flipped code
-    if (r + D < s) {
-      const uint32_t j = key & 1023u;
+#pragma unroll 1
+    for (uint32_t r = g; r + D < s; r += S::G) {
+      const uint32_t j = sk[r] & 1023u;
       const float p = pv[j];
       vals[ob + D + r] = fabsf(p);
       codes[ob + D + r] = p < 0.0f ? j : D + j;
@@ -260,13 +264,15 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
       __syncwarp();
       rank_sort_exact<NS, E2, true>(k2, g, sk, pv);
 #pragma unroll
-      for (int e = 0; e < E2; ++e) emit((uint32_t)g * E2 + e, k2[e]);
+      for (int e = 0; e < E2; ++e) sk[g * E2 + e] = k2[e];
+      emit_all();
     }
   }
   if (!fast) {
     rank_sort_exact<P, EPT, true>(kk, g, sk, pv);
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) emit((uint32_t)g * EPT + e, kk[e]);
+    for (int e = 0; e < EPT; ++e) sk[g * EPT + e] = kk[e];
+    emit_all();
   }
 }
 
