@@ -392,7 +392,7 @@ __device__ uint64_t block_radix_select(const uint64_t* __restrict__ seg, uint32_
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) {
       const uint64_t k = seg[i];
-      if ((k & mask) == prefix) atomicAdd(hist + ((k >> shift) & 255u), 1u);
+      if ((k & mask) == prefix) smem_inc(hist + ((k >> shift) & 255u));
     }
     __syncthreads();
     if (threadIdx.x == 0) {

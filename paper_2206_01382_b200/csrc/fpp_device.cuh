@@ -417,6 +417,23 @@ __device__ __forceinline__ void group_sort_u32_v2(uint32_t (&k)[EPT], int g) {
   }
 }
 
+// Shared-memory increment without a result (red.shared): plain atomicAdd on a
+// data-dependent address gets a compiler-generated warp-aggregation sequence
+// (vote / find-leader / popc loop) that costs ~10 instructions per call.
+__device__ __forceinline__ void smem_inc(uint32_t* p) {
+  asm volatile("red.shared.add.u32 [%0], 1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+}
+
+// Shared-memory fetch-add issued by one lane (same reason as smem_inc).
+__device__ __forceinline__ uint32_t smem_fetch_add(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;\n"
+               : "=r"(old)
+               : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v)
+               : "memory");
+  return old;
+}
+
 // exclusive block-wide scan (all threads must call); sh >= 32 words
 __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sh, uint32_t* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

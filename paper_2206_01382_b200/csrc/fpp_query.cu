@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       __syncthreads();
       enumerate([&](uint32_t key) {
         const uint32_t off = key - base;
-        if ((off & mask) == prefix) atomicAdd(&hist[(off >> sh) & (nb - 1)], 1u);
+        if ((off & mask) == prefix) smem_inc(&hist[(off >> sh) & (nb - 1)]);
       });
       __syncthreads();
       pick_bin(nb, rem);
@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
             const uint32_t i = i0 + 32 * u;
             if (i < A) {
               const float sc = i < nrow ? x0 + v[u] : v[u] + y0;
-              atomicAdd(&hist[(ord_key(sc) - amin) >> sh], 1u);
+              smem_inc(&hist[(ord_key(sc) - amin) >> sh]);
             }
           }
         }
@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       const uint32_t tb = __ballot_sync(FULL, take);
       if (tb) {
         uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&n_cand, __popc(tb));
+        if (lane == 0) base = smem_fetch_add(&n_cand, __popc(tb));
         base = __shfl_sync(FULL, base, 0);
         if (take && base + __popc(tb) <= a.ccap) {
           const uint32_t at = base + __popc(tb & ((1u << lane) - 1));
@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
             const bool take = i < C && selected(kk[u], pp[u]);
             const uint32_t bal = __ballot_sync(FULL, take);
             uint32_t base = 0;
-            if (lane == 0 && bal) base = atomicAdd(&n_emit, __popc(bal));
+            if (lane == 0 && bal) base = smem_fetch_add(&n_emit, __popc(bal));
             base = __shfl_sync(FULL, base, 0);
             if (take) out[base + __popc(bal & ((1u << lane) - 1))] = pp[u];
           }
@@ -1068,7 +1068,7 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
                  &ucount,
                  [&]() {
                    uint32_t c = 0;
-                   if ((threadIdx.x & 31) == 0) c = atomicAdd(&nextc, 1u);
+                   if ((threadIdx.x & 31) == 0) c = smem_fetch_add(&nextc, 1u);
                    return __shfl_sync(FULL, c, 0);
                  },
                  [&](uint32_t id) {
@@ -1113,7 +1113,7 @@ k_collect_cluster(CollectArgs a, uint32_t slice_words) {
                  ucount0,
                  [&]() {
                    uint32_t c = 0;
-                   if ((threadIdx.x & 31) == 0) c = atomicAdd(&nextc, 1u);
+                   if ((threadIdx.x & 31) == 0) c = smem_fetch_add(&nextc, 1u);
                    return __shfl_sync(FULL, c, 0) * CO_CLUSTER + rank;
                  },
                  [&](uint32_t id) {
