@@ -20,9 +20,12 @@ for r in rows[1:]:
     a[0] += 1
     a[1] += v
 tot = sum(v for _, v in agg.values())
-lines = ["| kernel | launches | total ms | share |", "|---|---|---|---|"]
+QUERY = ("k_query_lists", "k_probe_select", "k_scan_eq", "k_collect", "k_collect_cluster", "k_score")
+qtot = sum(v for k, (_, v) in agg.items() if k in QUERY) or 1
+lines = ["| kernel | launches | total ms | share of all | share of query |", "|---|---|---|---|---|"]
 for k, (c, v) in agg.items():
-    lines.append(f"| {k} | {c} | {v / 1e6:.2f} | {100 * v / tot:.1f}% |")
+    qs = f"{100 * v / qtot:.1f}%" if k in QUERY else "-"
+    lines.append(f"| {k} | {c} | {v / 1e6:.2f} | {100 * v / tot:.1f}% | {qs} |")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
 rr = list(csv.reader(raw.splitlines()))
