@@ -26,27 +26,143 @@
 namespace fpp {
 
 // ------------------------------------------------------------------ K1 build
-// value / code of rank slot `a` of a sorted top-R key list (static select)
-template <int R>
-__device__ __forceinline__ uint64_t pick(const uint64_t (&t)[R], uint32_t a) {
-  uint64_t k = ~0ull;
+// k_hash_build shared memory: NGRP transpose buffers (each >= HB_SEL u64 when
+// P >= 64, 16 B multiples) + NGRP * 2 * R u64 top lists
+template <int P>
+__host__ __device__ constexpr int hb_tbuf_bytes() {
+  return (256 / (P < 32 ? 1 : P / 32)) * (P >= 64 ? TransposeShape<P>::STRIDE : 4) * 4;
+}
+template <int P, int R>
+constexpr int hb_smem_bytes() { return hb_tbuf_bytes<P>() + (256 / (P < 32 ? 1 : P / 32)) * 2 * R * 8; }
+
+// Top-r selection of one projection (r = min(iProbes, D) <= R), exact order
+// (|p| desc, j asc) as 64-bit rank keys, written sorted to sel[0..R).
+//  * P >= 64 (fast path): bisect a threshold T in [0, amax] until the group
+//    count of |p| >= T lies in [r, HB_SEL]; every entry ranked before a kept one
+//    is kept too (|p| is compared exactly), so the top r of the kept set are the
+//    top r overall.  The <= HB_SEL kept keys are compacted and bitonic-sorted.
+//  * otherwise, or when some group of the warp finds no such T (ties at the
+//    threshold): lane-local top-R insertion + butterfly merge of the group.
+constexpr int HB_SEL = 32;
+template <int P, int R>
+__device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], int g, uint32_t D,
+                                          uint32_t r, uint64_t* scratch, uint64_t* sel) {
+  using S = FhtShape<P>;
+  constexpr bool TR = P >= 64;
+  const bool full = D >= (uint32_t)P;  // no truncation: skip the j < D test
+  auto jof = [&](int e) -> uint32_t { return TR ? (uint32_t)e * S::G + g : (uint32_t)g * S::EPT + e; };
+  bool fast = false;
+  if constexpr (TR) {
+    float amax = 0.0f;
 #pragma unroll
-  for (int i = 0; i < R; ++i) k = (uint32_t)i == a ? t[i] : k;
-  return k;
+    for (int e = 0; e < S::EPT; ++e)
+      if (full || jof(e) < D) amax = fmaxf(amax, fabsf(v[e]));
+#pragma unroll
+    for (int m = 1; m < S::G; m <<= 1) amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, m));
+    float lo = 0.0f, hi = 1.0f, tq = 0.0f;
+    bool ok = false, fail = !(amax > 0.0f);
+#pragma unroll 1
+    for (int it = 0; it < 24; ++it) {
+      if (__all_sync(FULL, ok || fail)) break;
+      const float mid = it == 0 ? 0.625f : 0.5f * (lo + hi);  // typical band for r ~ 5
+      const float T = amax * mid;
+      uint32_t c = 0;
+#pragma unroll
+      for (int e = 0; e < S::EPT; ++e) c += ((full || jof(e) < D) && fabsf(v[e]) >= T) ? 1u : 0u;
+#pragma unroll
+      for (int m = 1; m < S::G; m <<= 1) c += __shfl_xor_sync(FULL, c, m);
+      if (!ok && !fail) {
+        if (c > (uint32_t)HB_SEL) lo = mid;
+        else if (c < r) hi = mid;
+        else { ok = true; tq = T; }
+        if (!(hi - lo > 1e-7f)) fail = !ok;
+      }
+    }
+    fast = __all_sync(FULL, ok);
+    if (fast) {
+      uint32_t cl = 0;
+#pragma unroll
+      for (int e = 0; e < S::EPT; ++e) cl += ((full || jof(e) < D) && fabsf(v[e]) >= tq) ? 1u : 0u;
+      uint32_t x = cl;
+#pragma unroll
+      for (int o = 1; o < S::G; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, x, o);
+        if (g >= o) x += y;
+      }
+      const int lane = threadIdx.x & 31;
+      const uint32_t ctot = __shfl_sync(FULL, x, (lane / S::G) * S::G + S::G - 1);
+      uint32_t pos = x - cl;
+#pragma unroll
+      for (int e = 0; e < S::EPT; ++e)
+        if ((full || jof(e) < D) && fabsf(v[e]) >= tq) scratch[pos++] = rank_key(v[e], jof(e));
+      for (uint32_t i = ctot + g; i < (uint32_t)HB_SEL; i += S::G) scratch[i] = ~0ull;
+      __syncwarp();
+      constexpr int E = HB_SEL / S::G;
+      uint64_t k[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) k[e] = scratch[g * E + e];
+      group_bitonic_sort<HB_SEL, E>(k, g);
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (g * E + e < R) sel[g * E + e] = k[e];
+      __syncwarp();
+    }
+  }
+  if (!fast) {
+    float tp[R];
+    uint32_t tj[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) { tp[q] = 0.0f; tj[q] = 0xffffffffu; }
+    float thr = -1.0f;
+#pragma unroll
+    for (int e = 0; e < S::EPT; ++e) {
+      const uint32_t j = jof(e);  // j increases with e in both layouts
+      const float a = fabsf(v[e]);
+      if ((full || j < D) && a > thr) {
+        float cp = v[e];
+        uint32_t cj = j;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {  // insert, shifting the tail down
+          const bool ins = tj[q] == 0xffffffffu || fabsf(cp) > fabsf(tp[q]);
+          const float op = tp[q];
+          const uint32_t oj = tj[q];
+          if (ins) { tp[q] = cp; tj[q] = cj; cp = op; cj = oj; }
+        }
+        thr = tj[R - 1] == 0xffffffffu ? -1.0f : fabsf(tp[R - 1]);
+      }
+    }
+    uint64_t tk[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) tk[q] = tj[q] == 0xffffffffu ? ~0ull : rank_key(tp[q], tj[q]);
+    topr_group_merge<R, S::G>(tk);
+    if (g == 0) {
+#pragma unroll
+      for (int q = 0; q < R; ++q) sel[q] = tk[q];
+    }
+    __syncwarp();
+  }
 }
 
 template <int P, int R>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, uint32_t K,
              const uint32_t* __restrict__ signs, uint32_t t0, uint32_t T, uint32_t ip,
              uint2* __restrict__ ent, uint32_t* __restrict__ counts, uint64_t NB) {
   using S = FhtShape<P>;
   constexpr bool TR = P >= 64;  // transpose FHT (cross-lane stages in registers)
   constexpr int TS = TR ? TransposeShape<P>::STRIDE : 4;
-  __shared__ __align__(16) float tbuf[(256 / S::G) * TS];
+  // dynamic shared memory (hb_smem_bytes): per group a transpose buffer of TS
+  // floats (reused as the 32-key sort scratch once the FHT is done), then per
+  // group the sorted top-R lists of the K functions
+  extern __shared__ __align__(16) unsigned char hb_smem[];
+  constexpr int NGRP = 256 / S::G;
   const int lane = threadIdx.x & 31;
   const int g = lane % S::G;
-  float* buf = tbuf + (threadIdx.x / S::G) * TS;
+  const int grp = threadIdx.x / S::G;
+  float* buf = reinterpret_cast<float*>(hb_smem) + grp * TS;
+  uint64_t* scratch = reinterpret_cast<uint64_t*>(buf);
+  uint64_t* sel0 = reinterpret_cast<uint64_t*>(hb_smem + hb_tbuf_bytes<P>()) + grp * 2 * R;
+  uint64_t* sel1 = sel0 + R;
   const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
   const bool active = gid < n;
   const uint64_t i = active ? gid : n - 1;  // inactive groups shadow a real row
@@ -54,11 +170,11 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
   load_row<P>(X + i * d, d, g, x);
   const uint32_t r = ip < D ? ip : D;  // ranks needed per function (host ensures <= R)
   const uint32_t twoD = 2 * D;
-  // pairs this lane evaluates in the group-parallel top-iProbes selection
+  // candidate pairs: (a+1)(b+1) <= ip (every pair with a' <= a, b' <= b strictly
+  // precedes (a, b), so no other pair can be among the top ip)
   constexpr int NPL = (R * R + S::G - 1) / S::G;
   for (uint32_t tt = 0; tt < T; ++tt) {
     const uint32_t t = t0 + tt;
-    uint64_t top0[R], top1[R];
 #pragma unroll 1
     for (int f = 0; f < (int)K; ++f) {
       float v[S::EPT];
@@ -67,54 +183,21 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
       const uint32_t* sw = signs + ((uint64_t)t * K + f) * 3 * S::W;
       if constexpr (TR) spinner_project_T<P>(v, sw, g, buf);  // layout B: j = e*G + g
       else spinner_project<P>(v, sw, g);                      // layout A: j = g*EPT + e
-      // lane-local top-R by (|p| desc, j asc): j increases with e in both layouts
-      float tp[R];
-      uint32_t tj[R];
-#pragma unroll
-      for (int q = 0; q < R; ++q) { tp[q] = 0.0f; tj[q] = 0xffffffffu; }
-      float thr = -1.0f;
-      const bool full = D >= (uint32_t)P;  // no truncation: skip the j < D test
-#pragma unroll
-      for (int e = 0; e < S::EPT; ++e) {
-        const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * S::EPT + e;
-        const float a = fabsf(v[e]);
-        if ((full || j < D) && a > thr) {
-          float cp = v[e];
-          uint32_t cj = j;
-#pragma unroll
-          for (int q = 0; q < R; ++q) {  // insert, shifting the tail down
-            const bool ins = tj[q] == 0xffffffffu || fabsf(cp) > fabsf(tp[q]);
-            const float op = tp[q];
-            const uint32_t oj = tj[q];
-            if (ins) { tp[q] = cp; tj[q] = cj; cp = op; cj = oj; }
-          }
-          thr = tj[R - 1] == 0xffffffffu ? -1.0f : fabsf(tp[R - 1]);
-        }
-      }
-      uint64_t tk[R];
-#pragma unroll
-      for (int q = 0; q < R; ++q) tk[q] = tj[q] == 0xffffffffu ? ~0ull : rank_key(tp[q], tj[q]);
-      topr_group_merge<R, S::G>(tk);
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        if (f == 0) top0[q] = tk[q];
-        else top1[q] = tk[q];
-      }
+      hb_select<P, R>(v, g, D, r, scratch, f == 0 ? sel0 : sel1);
+      __syncwarp();  // scratch aliases the next projection's transpose buffer
     }
     uint32_t* cnt = counts ? counts + (uint64_t)tt * NB : nullptr;
     uint2* out = ent + ((uint64_t)tt * n + i) * ip;
     if (K == 1) {
       // SPEC.md:184-192 with l=1: the top-iProbes signed vectors themselves
       if (g == 0 && active) {
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-          if ((uint32_t)q < ip) {
-            const uint32_t b = rank_code(top0[q], D);
-            out[q] = make_uint2(b, __float_as_uint(rank_val(top0[q])));
-            if (cnt) atomicAdd(cnt + b, 1u);
-          }
+        for (uint32_t q = 0; q < ip; ++q) {
+          const uint32_t b = rank_code(sel0[q], D);
+          out[q] = make_uint2(b, __float_as_uint(rank_val(sel0[q])));
+          if (cnt) atomicAdd(cnt + b, 1u);
         }
       }
+      __syncwarp();
       continue;
     }
     // top-iProbes pairs by (fl(v1+v2) desc, r1 asc, r2 asc), group-parallel:
@@ -126,13 +209,13 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
       const uint32_t pi = (uint32_t)g + (uint32_t)k * S::G;
       const uint32_t a = pi / R, b = pi % R;
       pk[k] = 0;
-      if (pi < (uint32_t)(R * R) && a < r && b < r) {
-        const float sc = rank_val(pick<R>(top0, a)) + rank_val(pick<R>(top1, b));
+      if (pi < (uint32_t)(R * R) && a < r && b < r && (a + 1) * (b + 1) <= ip) {
+        const float sc = rank_val(sel0[a]) + rank_val(sel1[b]);
         pk[k] = ((uint64_t)ord_key(sc) << 32) | ((uint64_t)(0xffffu - a) << 16) | (0xffffu - b);
       }
     }
     uint64_t prev = ~0ull;
-    for (uint32_t sel = 0; sel < ip; ++sel) {
+    for (uint32_t sl = 0; sl < ip; ++sl) {
       uint64_t best = 0;
 #pragma unroll
       for (int k = 0; k < NPL; ++k) best = (pk[k] < prev && pk[k] > best) ? pk[k] : best;
@@ -145,11 +228,12 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
       if (g == 0 && active) {
         const uint32_t a = 0xffffu - (uint32_t)((best >> 16) & 0xffffu);
         const uint32_t b = 0xffffu - (uint32_t)(best & 0xffffu);
-        const uint32_t bucket = rank_code(pick<R>(top0, a), D) * twoD + rank_code(pick<R>(top1, b), D);
-        out[sel] = make_uint2(bucket, __float_as_uint(ord_inv((uint32_t)(best >> 32))));
+        const uint32_t bucket = rank_code(sel0[a], D) * twoD + rank_code(sel1[b], D);
+        out[sl] = make_uint2(bucket, __float_as_uint(ord_inv((uint32_t)(best >> 32))));
         if (cnt) atomicAdd(cnt + bucket, 1u);
       }
     }
+    __syncwarp();
   }
 }
 
@@ -477,10 +561,15 @@ static void launch_hash_R(const Index& ix, const float* X, uint64_t n, uint32_t 
   const unsigned blocks = (unsigned)((threads + 255) / 256);
   const uint32_t K = ix.prm.K, D = ix.prm.D, ip = ix.prm.iprobes;
 #define FPP_HASH_CASE(PP)                                                                      \
-  case PP:                                                                                     \
-    k_hash_build<PP, R><<<blocks, 256, 0, s>>>(X, n, ix.d, D, K, ix.signs, t0, T, ip, ent,     \
-                                               counts, ix.NB);                                 \
-    break;
+  case PP: {                                                                                   \
+    constexpr int sm = hb_smem_bytes<PP, R>();                                                 \
+    if (sm > 48 * 1024)                                                                        \
+      FPP_CUDA(cudaFuncSetAttribute(k_hash_build<PP, R>,                                       \
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sm));         \
+    k_hash_build<PP, R><<<blocks, 256, sm, s>>>(X, n, ix.d, D, K, ix.signs, t0, T, ip, ent,    \
+                                                counts, ix.NB);                                \
+    break;                                                                                     \
+  }
   switch (P) {
     FPP_HASH_CASE(2) FPP_HASH_CASE(4) FPP_HASH_CASE(8) FPP_HASH_CASE(16) FPP_HASH_CASE(32)
     FPP_HASH_CASE(64) FPP_HASH_CASE(128) FPP_HASH_CASE(256) FPP_HASH_CASE(512)
