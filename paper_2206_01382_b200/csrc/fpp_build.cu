@@ -26,14 +26,19 @@
 namespace fpp {
 
 // ------------------------------------------------------------------ K1 build
-// k_hash_build shared memory: NGRP transpose buffers (each >= HB_SEL u64 when
-// P >= 64, 16 B multiples) + NGRP * 2 * R u64 top lists
+constexpr int HB_SEL = 32;  // keys sorted after the threshold preselection
+
+// k_hash_build shared memory: NGRP transpose buffers (TS >= P floats, reused
+// for the v dump of the preselection) + per group HB_SEL scratch keys and the
+// two sorted top-R lists
 template <int P>
 __host__ __device__ constexpr int hb_tbuf_bytes() {
   return (256 / (P < 32 ? 1 : P / 32)) * (P >= 64 ? TransposeShape<P>::STRIDE : 4) * 4;
 }
 template <int P, int R>
-constexpr int hb_smem_bytes() { return hb_tbuf_bytes<P>() + (256 / (P < 32 ? 1 : P / 32)) * 2 * R * 8; }
+constexpr int hb_smem_bytes() {
+  return hb_tbuf_bytes<P>() + (256 / (P < 32 ? 1 : P / 32)) * (HB_SEL + 2 * R) * 8;
+}
 
 // Top-r selection of one projection (r = min(iProbes, D) <= R), exact order
 // (|p| desc, j asc) as 64-bit rank keys, written sorted to sel[0..R).
@@ -43,10 +48,9 @@ constexpr int hb_smem_bytes() { return hb_tbuf_bytes<P>() + (256 / (P < 32 ? 1 :
 //    top r overall.  The <= HB_SEL kept keys are compacted and bitonic-sorted.
 //  * otherwise, or when some group of the warp finds no such T (ties at the
 //    threshold): lane-local top-R insertion + butterfly merge of the group.
-constexpr int HB_SEL = 32;
 template <int P, int R>
 __device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], int g, uint32_t D,
-                                          uint32_t r, uint64_t* scratch, uint64_t* sel) {
+                                          uint32_t r, float* vbuf, uint64_t* scratch, uint64_t* sel) {
   using S = FhtShape<P>;
   constexpr bool TR = P >= 64;
   const bool full = D >= (uint32_t)P;  // no truncation: skip the j < D test
@@ -59,30 +63,35 @@ __device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], in
       if (full || jof(e) < D) amax = fmaxf(amax, fabsf(v[e]));
 #pragma unroll
     for (int m = 1; m < S::G; m <<= 1) amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, m));
-    float lo = 0.0f, hi = 1.0f, tq = 0.0f;
+    float lo = 0.0f, hi = 1.0f;
+    uint32_t macc = 0;  // this lane's kept elements at the accepted threshold
     bool ok = false, fail = !(amax > 0.0f);
 #pragma unroll 1
     for (int it = 0; it < 24; ++it) {
       if (__all_sync(FULL, ok || fail)) break;
       const float mid = it == 0 ? 0.625f : 0.5f * (lo + hi);  // typical band for r ~ 5
       const float T = amax * mid;
-      uint32_t c = 0;
+      uint32_t m = 0;
 #pragma unroll
-      for (int e = 0; e < S::EPT; ++e) c += ((full || jof(e) < D) && fabsf(v[e]) >= T) ? 1u : 0u;
+      for (int e = 0; e < S::EPT; ++e)
+        m |= (((full || jof(e) < D) && fabsf(v[e]) >= T) ? 1u : 0u) << e;
+      uint32_t c = __popc(m);
 #pragma unroll
-      for (int m = 1; m < S::G; m <<= 1) c += __shfl_xor_sync(FULL, c, m);
+      for (int k = 1; k < S::G; k <<= 1) c += __shfl_xor_sync(FULL, c, k);
       if (!ok && !fail) {
         if (c > (uint32_t)HB_SEL) lo = mid;
         else if (c < r) hi = mid;
-        else { ok = true; tq = T; }
+        else { ok = true; macc = m; }
         if (!(hi - lo > 1e-7f)) fail = !ok;
       }
     }
     fast = __all_sync(FULL, ok);
     if (fast) {
-      uint32_t cl = 0;
+      // v -> shared memory in natural order (the lane reads back only its own
+      // entries), then each lane appends its kept keys at its exclusive offset
 #pragma unroll
-      for (int e = 0; e < S::EPT; ++e) cl += ((full || jof(e) < D) && fabsf(v[e]) >= tq) ? 1u : 0u;
+      for (int e = 0; e < S::EPT; ++e) vbuf[jof(e)] = v[e];
+      const uint32_t cl = __popc(macc);
       uint32_t x = cl;
 #pragma unroll
       for (int o = 1; o < S::G; o <<= 1) {
@@ -92,9 +101,10 @@ __device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], in
       const int lane = threadIdx.x & 31;
       const uint32_t ctot = __shfl_sync(FULL, x, (lane / S::G) * S::G + S::G - 1);
       uint32_t pos = x - cl;
-#pragma unroll
-      for (int e = 0; e < S::EPT; ++e)
-        if ((full || jof(e) < D) && fabsf(v[e]) >= tq) scratch[pos++] = rank_key(v[e], jof(e));
+      for (uint32_t mm = macc; mm; mm &= mm - 1) {
+        const uint32_t j = jof(__ffs(mm) - 1);
+        scratch[pos++] = rank_key(vbuf[j], j);
+      }
       for (uint32_t i = ctot + g; i < (uint32_t)HB_SEL; i += S::G) scratch[i] = ~0ull;
       __syncwarp();
       constexpr int E = HB_SEL / S::G;
@@ -144,7 +154,7 @@ __device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], in
 }
 
 template <int P, int R>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, 3)
 k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, uint32_t K,
              const uint32_t* __restrict__ signs, uint32_t t0, uint32_t T, uint32_t ip,
              uint2* __restrict__ ent, uint32_t* __restrict__ counts, uint64_t NB) {
@@ -159,9 +169,9 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
   const int lane = threadIdx.x & 31;
   const int g = lane % S::G;
   const int grp = threadIdx.x / S::G;
-  float* buf = reinterpret_cast<float*>(hb_smem) + grp * TS;
-  uint64_t* scratch = reinterpret_cast<uint64_t*>(buf);
-  uint64_t* sel0 = reinterpret_cast<uint64_t*>(hb_smem + hb_tbuf_bytes<P>()) + grp * 2 * R;
+  float* buf = reinterpret_cast<float*>(hb_smem) + grp * TS;  // also the v dump (P <= TS)
+  uint64_t* scratch = reinterpret_cast<uint64_t*>(hb_smem + hb_tbuf_bytes<P>()) + grp * (HB_SEL + 2 * R);
+  uint64_t* sel0 = scratch + HB_SEL;
   uint64_t* sel1 = sel0 + R;
   const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
   const bool active = gid < n;
@@ -183,8 +193,8 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
       const uint32_t* sw = signs + ((uint64_t)t * K + f) * 3 * S::W;
       if constexpr (TR) spinner_project_T<P>(v, sw, g, buf);  // layout B: j = e*G + g
       else spinner_project<P>(v, sw, g);                      // layout A: j = g*EPT + e
-      hb_select<P, R>(v, g, D, r, scratch, f == 0 ? sel0 : sel1);
-      __syncwarp();  // scratch aliases the next projection's transpose buffer
+      hb_select<P, R>(v, g, D, r, buf, scratch, f == 0 ? sel0 : sel1);
+      __syncwarp();  // the v dump aliases the next projection's transpose buffer
     }
     uint32_t* cnt = counts ? counts + (uint64_t)tt * NB : nullptr;
     uint2* out = ent + ((uint64_t)tt * n + i) * ip;
