@@ -14,8 +14,10 @@
 //   k_scan_*       per-table exclusive scans: histogram -> pre-filter starts,
 //                  keep(B) -> kept CSR offsets
 //   k_scatter      (score desc, id asc) 64-bit keys into bucket segments
-//   k_classify     B=1 written directly; B<=32 -> warp list; B>32 -> CTA list
+//   k_classify     B=1 written directly; B<=32 -> warp list; B>32 with keep<=32 ->
+//                  warp top-k list; other B>32 -> CTA list
 //   k_sort_small   warp bitonic sort, keep prefix -> CSR
+//   k_sort_topk    warp streams the bucket, keeps the sorted top-keep in registers
 //   k_sort_large   CTA smem bitonic (B<=4096) or radix-select + chunked sort
 #include <algorithm>
 #include <cstdio>
@@ -359,20 +361,35 @@ static void scan_tables(const uint32_t* in, uint64_t NB, uint32_t T, KeepXform x
 }
 
 // ------------------------------------------------------------------ scatter
+// Thread per (point, table): the point's iProbes entries are read together
+// (coalesced across the warp) and their bucket-cursor atomics issued before
+// any result is used.  Order inside a bucket is irrelevant (sorted afterwards).
+constexpr int SCATTER_UNROLL = 4;
 __global__ void __launch_bounds__(256)
-k_scatter(const uint2* __restrict__ ent, uint64_t nip, uint32_t ip, uint32_t T, uint64_t NB,
+k_scatter(const uint2* __restrict__ ent, uint32_t n, uint32_t ip, uint64_t NB,
           const uint32_t* __restrict__ starts, uint32_t* __restrict__ cursor,
           uint64_t* __restrict__ keys, uint32_t id_add = 0) {
-  const uint64_t total = nip * T;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t tt = (uint32_t)(e / nip);
-    const uint64_t rem = e - (uint64_t)tt * nip;
-    const uint32_t i = (uint32_t)(rem / ip);
-    const uint2 en = ent[e];
-    const uint32_t pos = starts[(uint64_t)tt * (NB + 1) + en.x] +
-                         atomicAdd(cursor + (uint64_t)tt * NB + en.x, 1u);
-    keys[(uint64_t)tt * nip + pos] = desc_score_key(__uint_as_float(en.y), i + id_add);
+  const uint32_t tt = blockIdx.y;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t nip = (uint64_t)n * ip;
+  const uint2* e = ent + (uint64_t)tt * nip + (uint64_t)i * ip;
+  const uint32_t* st = starts + (uint64_t)tt * (NB + 1);
+  uint32_t* cur = cursor + (uint64_t)tt * NB;
+  uint64_t* kout = keys + (uint64_t)tt * nip;
+  for (uint32_t q0 = 0; q0 < ip; q0 += SCATTER_UNROLL) {
+    uint2 en[SCATTER_UNROLL];
+    uint32_t pos[SCATTER_UNROLL];
+#pragma unroll
+    for (int u = 0; u < SCATTER_UNROLL; ++u)
+      if (q0 + u < ip) en[u] = e[q0 + u];
+#pragma unroll
+    for (int u = 0; u < SCATTER_UNROLL; ++u)
+      if (q0 + u < ip) pos[u] = atomicAdd(cur + en[u].x, 1u);
+#pragma unroll
+    for (int u = 0; u < SCATTER_UNROLL; ++u)
+      if (q0 + u < ip)
+        kout[st[en[u].x] + pos[u]] = desc_score_key(__uint_as_float(en[u].y), i + id_add);
   }
 }
 
@@ -397,11 +414,12 @@ __device__ __forceinline__ void csr_put(const CsrOut& o, uint32_t tt, uint64_t N
 
 constexpr uint32_t SMALL_MAX = 32;
 constexpr uint32_t LARGE_CAP = 4096;
+constexpr uint32_t TOPK_MAX = 32;  // B > 32 with keep <= 32 -> k_sort_topk
 
 __global__ void __launch_bounds__(256)
 k_classify(const uint32_t* __restrict__ starts, const uint64_t* __restrict__ keys, uint64_t nip,
            uint32_t T, uint64_t NB, CsrOut o, uint32_t* __restrict__ small_list,
-           uint32_t* __restrict__ large_list, uint32_t* __restrict__ ctr) {
+           uint32_t* __restrict__ large_list, uint32_t* __restrict__ ctr, uint64_t large_cap) {
   const uint64_t total = NB * T;
   uint32_t local_max = 0;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
@@ -419,6 +437,8 @@ k_classify(const uint32_t* __restrict__ starts, const uint64_t* __restrict__ key
       csr_put(o, tt, NB, b, 0, keys[(uint64_t)tt * nip + st[b]]);
     } else if (B <= SMALL_MAX) {
       small_list[atomicAdd(ctr + 0, 1u)] = (uint32_t)x;
+    } else if (k <= TOPK_MAX && !o.keys_out) {  // keep << B: warp streaming top-k
+      large_list[large_cap - 1 - atomicAdd(ctr + 3, 1u)] = (uint32_t)x;
     } else {
       large_list[atomicAdd(ctr + 1, 1u)] = (uint32_t)x;
     }
@@ -455,6 +475,57 @@ k_sort_small(const uint32_t* __restrict__ starts, const uint64_t* __restrict__ k
       }
     }
     if ((uint32_t)lane < k) csr_put(o, tt, NB, b, lane, key);
+  }
+}
+
+// Warp per bucket with B > 32 and keep <= 32: the first 32 keys are bitonic
+// sorted across the lanes (lane i = i-th smallest), then every later key below
+// the current keep-th smallest is inserted (ballot rank + shift up).  Keys are
+// unique (id in the low bits), so the result equals the sorted prefix.
+__global__ void __launch_bounds__(256)
+k_sort_topk(const uint32_t* __restrict__ starts, const uint64_t* __restrict__ keys, uint64_t nip,
+            uint64_t NB, CsrOut o, const uint32_t* __restrict__ list,
+            const uint32_t* __restrict__ ctr, uint64_t large_cap) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t count = ctr[3];
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t it = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < count; it += nwarps) {
+    const uint32_t x = list[large_cap - 1 - it];
+    const uint32_t tt = (uint32_t)(x / NB), b = (uint32_t)(x - (uint64_t)tt * NB);
+    const uint32_t* st = starts + (uint64_t)tt * (NB + 1);
+    const uint32_t B = st[b + 1] - st[b];
+    const uint32_t* of = o.offs + (uint64_t)tt * (NB + 1);
+    const uint32_t k = of[b + 1] - of[b];
+    const uint64_t* seg = keys + (uint64_t)tt * nip + st[b];
+    uint64_t top = seg[lane];  // B > 32
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const uint64_t other = __shfl_xor_sync(FULL, top, j);
+        const bool up = (lane & kk) == 0;
+        const bool lower = (lane & j) == 0;
+        const uint64_t mn = top < other ? top : other, mx = top < other ? other : top;
+        top = (lower == up) ? mn : mx;
+      }
+    }
+    uint64_t thr = __shfl_sync(FULL, top, k - 1);
+    for (uint32_t c0 = 32; c0 < B; c0 += 32) {
+      const uint64_t key = c0 + lane < B ? seg[c0 + lane] : ~0ull;
+      uint32_t m = __ballot_sync(FULL, key < thr);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const uint64_t v = __shfl_sync(FULL, key, src);
+        if (v >= thr) continue;  // thr only decreases (warp-uniform)
+        const int pos = __popc(__ballot_sync(FULL, top < v));
+        const uint64_t upv = __shfl_up_sync(FULL, top, 1);
+        if (lane > pos) top = upv;
+        if (lane == pos) top = v;
+        thr = __shfl_sync(FULL, top, k - 1);
+      }
+    }
+    if ((uint32_t)lane < k) csr_put(o, tt, NB, b, lane, top);
   }
 }
 
@@ -700,9 +771,8 @@ void build_tables(Index& ix) {
     FPP_CUDA(cudaMemsetAsync(counts.p, 0, (size_t)Tc * NB * sizeof(uint32_t), s));
     FPP_CUDA(cudaMemsetAsync(ctr.p, 0, 4 * sizeof(uint32_t), s));
     {
-      const uint64_t tot = nip * Tc;
-      const unsigned blocks = (unsigned)std::min<uint64_t>((tot + 255) / 256, (uint64_t)sms * 32);
-      k_scatter<<<blocks, 256, 0, s>>>(ent.p, nip, ip, Tc, NB, starts.p, counts.p, keys.p);
+      const dim3 grid((unsigned)((n + 255) / 256), Tc);
+      k_scatter<<<grid, 256, 0, s>>>(ent.p, (uint32_t)n, ip, NB, starts.p, counts.p, keys.p);
       FPP_LAUNCH();
     }
     CsrOut o{offs, base_d.p, ix.ids, ix.scores, nullptr};
@@ -710,10 +780,13 @@ void build_tables(Index& ix) {
       const uint64_t tot = NB * Tc;
       const unsigned blocks = (unsigned)std::min<uint64_t>((tot + 255) / 256, (uint64_t)sms * 32);
       k_classify<<<blocks, 256, 0, s>>>(starts.p, keys.p, nip, Tc, NB, o, small_list.p,
-                                        large_list.p, ctr.p);
+                                        large_list.p, ctr.p, large_list.n);
       FPP_LAUNCH();
     }
     k_sort_small<<<sms * 8, 256, 0, s>>>(starts.p, keys.p, nip, NB, o, small_list.p, ctr.p);
+    FPP_LAUNCH();
+    k_sort_topk<<<sms * 8, 256, 0, s>>>(starts.p, keys.p, nip, NB, o, large_list.p, ctr.p,
+                                        large_list.n);
     FPP_LAUNCH();
     k_sort_large<<<sms * 4, 256, 0, s>>>(starts.p, keys.p, nip, NB, o, large_list.p, ctr.p);
     FPP_LAUNCH();
@@ -779,10 +852,9 @@ void shard_begin(Index& ix) {
   FPP_CUDA(cudaMemsetAsync(ctr.p, 0, 16, s));
   const int sms = sm_count();
   {
-    const uint64_t tot = nip * L;
-    const unsigned blocks = (unsigned)std::min<uint64_t>((tot + 255) / 256, (uint64_t)sms * 32);
-    k_scatter<<<blocks, 256, 0, s>>>(ent.p, nip, ip, L, NB, st->starts.p, cursor.p, keys.p,
-                                     ix.prm.id_offset);
+    const dim3 grid((unsigned)((n + 255) / 256), L);
+    k_scatter<<<grid, 256, 0, s>>>(ent.p, (uint32_t)n, ip, NB, st->starts.p, cursor.p, keys.p,
+                                   ix.prm.id_offset);
     FPP_LAUNCH();
   }
   std::vector<uint64_t> tb(L);
@@ -794,7 +866,7 @@ void shard_begin(Index& ix) {
     const uint64_t tot = NB * L;
     const unsigned blocks = (unsigned)std::min<uint64_t>((tot + 255) / 256, (uint64_t)sms * 32);
     k_classify<<<blocks, 256, 0, s>>>(st->starts.p, keys.p, nip, L, NB, o, small_list.p,
-                                      large_list.p, ctr.p);
+                                      large_list.p, ctr.p, large_list.n);
     FPP_LAUNCH();
   }
   k_sort_small<<<sms * 8, 256, 0, s>>>(st->starts.p, keys.p, nip, NB, o, small_list.p, ctr.p);

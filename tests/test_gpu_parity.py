@@ -72,6 +72,10 @@ CSR_CASES = [
     ("kappa0_stress", 20000, 128, 10, 0.3, 2, 2, 128, 3, 0.01, 0),
     ("K1", 10000, 64, 0, 0.0, 3, 1, 64, 3, 0.3, 5),
     ("d300", 8000, 300, 50, 0.3, 2, 2, 512, 3, 0.05, 20),
+    # NB = 1024, B ~ 175 > 32 with keep = kappa = 20: every bucket on the warp top-k path
+    ("topk_buckets", 60000, 32, 0, 0.0, 2, 2, 16, 3, 0.05, 20),
+    # keep in (32, B): CTA path next to top-k buckets
+    ("keep_gt_32", 60000, 32, 0, 0.0, 2, 2, 16, 3, 0.9, 20),
 ]
 
 
