@@ -81,9 +81,12 @@ template <int P>
 __device__ __forceinline__ void spinner_project(float (&v)[FhtShape<P>::EPT], const uint32_t* sw,
                                                 int g) {
   using S = FhtShape<P>;
+  // the three rounds' sign words are loaded up front (one latency, not three)
+  const uint32_t gi = S::G > 1 ? g : 0;
+  const uint32_t w0 = __ldg(sw + gi), w1 = __ldg(sw + S::W + gi), w2 = __ldg(sw + 2 * S::W + gi);
 #pragma unroll 1
   for (int stage = 0; stage < 3; ++stage) {
-    const uint32_t w = __ldg(sw + stage * S::W + (S::G > 1 ? g : 0));
+    const uint32_t w = stage == 0 ? w0 : (stage == 1 ? w1 : w2);
     apply_signs<S::EPT>(v, w);
     fht_group<P, S::EPT>(v, g);
   }
@@ -170,10 +173,12 @@ template <int P>
 __device__ __forceinline__ void spinner_project_T(float (&v)[32], const uint32_t* sw, int g,
                                                   float* buf) {
   constexpr int G = P / 32;
+  // the three rounds' sign words are loaded up front (one latency, not three)
+  const uint32_t w0 = __ldg(sw + g), w1 = __ldg(sw + G + g), w2 = __ldg(sw + 2 * G + g);
 #pragma unroll 1
   for (int stage = 0; stage < 3; ++stage) {
     if (stage) transpose_B_to_A<P>(v, g, buf);
-    apply_signs<32>(v, __ldg(sw + stage * G + g));
+    apply_signs<32>(v, stage == 0 ? w0 : (stage == 1 ? w1 : w2));
 #pragma unroll
     for (int len = 1; len < 32; len <<= 1) {
 #pragma unroll

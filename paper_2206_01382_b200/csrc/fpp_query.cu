@@ -163,13 +163,15 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
   uint32_t* sk = sk_all[gl];
   float* tbuf = tb_all + gl * PVS;
   float* pv = tbuf;
-  const uint64_t gg = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
-  const uint64_t total = nq * L * K;
+  // launch_query_lists keeps nq * L * K * G < 2^31: 32-bit index math
+  const uint32_t gg = (blockIdx.x * blockDim.x + threadIdx.x) / S::G;
+  const uint32_t total = (uint32_t)nq * L * K;
   const bool active = gg < total;
-  const uint64_t gid = active ? gg : total - 1;
-  const uint32_t f = (uint32_t)(gid % K);
-  const uint32_t t = (uint32_t)((gid / K) % L);
-  const uint64_t q = gid / ((uint64_t)K * L);
+  const uint32_t gid = active ? gg : total - 1;
+  const uint32_t f = gid % K;
+  const uint32_t tl = gid / K;
+  const uint32_t t = tl % L;
+  const uint64_t q = tl / L;
   float v[EPT];
   load_row<P>(Q + q * d, d, g, v);
   if constexpr (TR) spinner_project_T<P>(v, signs + ((uint64_t)t * K + f) * 3 * S::W, g, tbuf);
@@ -1346,6 +1348,14 @@ void launch_query_lists(const Index& ix, const float* Qd, uint64_t nq, uint32_t 
   if (nq == 0) return;
   const uint32_t d = ix.d, D = ix.prm.D, K = ix.prm.K, L = ix.prm.L;
   const uint32_t G = ix.P < 32 ? 1 : ix.P / 32;
+  // sub-batches keep nq * L * K * G < 2^31 (32-bit index math in the kernel)
+  const uint64_t qmax = std::max<uint64_t>(1, ((1ull << 31) - 1) / ((uint64_t)L * K * G));
+  if (nq > qmax) {
+    for (uint64_t q0 = 0; q0 < nq; q0 += qmax)
+      launch_query_lists(ix, Qd + q0 * d, std::min(qmax, nq - q0), s_cap, vals + q0 * lstride,
+                         codes + q0 * lstride, s, lstride);
+    return;
+  }
   const unsigned grid = (unsigned)((nq * L * K * G + 127) / 128);
   // preselection width: the smallest of P/4, P/2 leaving a margin of P/16 above
   // nat = min(s, D) (0 = sort all P keys)
