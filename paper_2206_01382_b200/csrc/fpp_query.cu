@@ -309,6 +309,7 @@ struct ProbeArgs {
   uint32_t* ckey;         // [nq][ccap] candidate pair keys (scratch)
   uint32_t* cpair;        // [nq][ccap] candidate pairs (t<<22 | r1<<11 | r2)
   uint32_t ccap;
+  uint32_t beta_q8;       // first T_lo attempt at arm rank beta * m (beta = beta_q8 / 256)
 };
 
 __device__ const float g_zero_row[1] = {0.0f};
@@ -471,7 +472,7 @@ struct GridRef {
 // The emission order of the selection class is not canonical: the probe set
 // (and so the candidate set and the top-k) is.
 constexpr int PS_RBITS = 12;  // radix digit
-__global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
+__global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
   __shared__ uint64_t red[PS_THREADS / 32];
   __shared__ uint64_t ties[PS_TIE_CAP];
   __shared__ uint32_t hist[1 << PS_RBITS];
@@ -587,7 +588,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
   };
   auto bitlen = [](uint32_t x) { return x ? 32 - __clz(x) : 0; };
   auto pack = [](uint32_t t, uint32_t r1, uint32_t r2) { return (t << 22) | (r1 << 11) | r2; };
-  uint32_t Tstar = 0, Tlo = 0;
+  uint32_t Tstar = 0, Tlo = 0, Tlo_safe = 0, refalls = 0;
   bool flat = false;
   uint32_t C = 0;
   auto enum_stair = [&](auto&& visit) {  // pairs >= Tlo of the selection class
@@ -693,7 +694,17 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       }
       __syncthreads();
       pick_bin(nb, (uint32_t)m_sel);
-      Tlo = amin + (sel_bin << sh);
+      Tlo_safe = amin + (sel_bin << sh);
+      Tlo = Tlo_safe;
+      // optimistic first attempt: with >= 64 selected pairs per grid the arms
+      // hold only about half of the pairs above T*, so a bin edge at arm rank
+      // beta*m usually still leaves >= m pairs above it (checked after the walk;
+      // the safe edge is the fallback).  Thinner staircases are mostly arm.
+      const uint32_t m_try = (uint32_t)(((uint64_t)m_sel * a.beta_q8) >> 8);
+      if (m_try >= 1 && m_try < m_sel && m_sel >= 64ull * NG) {
+        pick_bin(nb, m_try);
+        Tlo = amin + (sel_bin << sh);
+      }
     }
     ck[1] = clock64();
     // ---- 2. materialise every selection-class pair >= Tlo.  Warp per grid.  The
@@ -715,49 +726,62 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
         }
       }
     };
-    for (uint32_t gi = wp; gi < NG; gi += nw) {
-      const GridRef g = grid(sel, gi);
-      uint32_t pb = g.nb, r1 = 0;
-      for (; r1 < g.na && pb > 32; ++r1) {
-        const float x = g.va[r1];
-        uint32_t npb = 0;
-        for (uint32_t c0 = 0; c0 < pb; c0 += 32) {
-          const uint32_t r2 = c0 + lane;
-          const uint32_t key = r2 < pb ? ord_key(x + g.vb[r2]) : 0;
-          const bool ge = r2 < pb && key >= Tlo;
-          const uint32_t bal = __ballot_sync(FULL, ge);
-          npb += __popc(bal);
-          emit(ge && !(g.forced && r1 == 0 && r2 == 0), key, pack(g.t, g.oa + r1, g.ob + r2));
-          if (bal != FULL) break;  // the prefix ended inside this chunk
-        }
-        pb = npb;
-      }
-      for (; r1 < g.na && pb > 0; r1 += 32) {
-        const uint32_t my = r1 + lane;
-        bool alive = my < g.na;
-        const float x = alive ? g.va[my] : 0.0f;
-        uint32_t cnt = 0;
-        for (uint32_t c0 = 0; c0 < pb; c0 += 4) {
-          float y[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) y[u] = c0 + u < pb ? g.vb[c0 + u] : 0.0f;
-          uint32_t any = 0;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t c = c0 + u;
-            const uint32_t key = ord_key(x + y[u]);
-            alive = alive && c < pb && key >= Tlo;
-            cnt += alive;
-            any |= __ballot_sync(FULL, alive);
-            emit(alive && !(g.forced && my == 0 && c == 0), key, pack(g.t, g.oa + my, g.ob + c));
+    auto materialise = [&]() {
+      for (uint32_t gi = wp; gi < NG; gi += nw) {
+        const GridRef g = grid(sel, gi);
+        uint32_t pb = g.nb, r1 = 0;
+        for (; r1 < g.na && pb > 32; ++r1) {
+          const float x = g.va[r1];
+          uint32_t npb = 0;
+          for (uint32_t c0 = 0; c0 < pb; c0 += 32) {
+            const uint32_t r2 = c0 + lane;
+            const uint32_t key = r2 < pb ? ord_key(x + g.vb[r2]) : 0;
+            const bool ge = r2 < pb && key >= Tlo;
+            const uint32_t bal = __ballot_sync(FULL, ge);
+            npb += __popc(bal);
+            emit(ge && !(g.forced && r1 == 0 && r2 == 0), key, pack(g.t, g.oa + r1, g.ob + r2));
+            if (bal != FULL) break;  // the prefix ended inside this chunk
           }
-          if (!any) break;
+          pb = npb;
         }
-        pb = __shfl_sync(FULL, cnt, 31);  // the next block's rows lie below row r1 + 31
+        for (; r1 < g.na && pb > 0; r1 += 32) {
+          const uint32_t my = r1 + lane;
+          bool alive = my < g.na;
+          const float x = alive ? g.va[my] : 0.0f;
+          uint32_t cnt = 0;
+          for (uint32_t c0 = 0; c0 < pb; c0 += 4) {
+            float y[4];
+  #pragma unroll
+            for (int u = 0; u < 4; ++u) y[u] = c0 + u < pb ? g.vb[c0 + u] : 0.0f;
+            uint32_t any = 0;
+  #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t c = c0 + u;
+              const uint32_t key = ord_key(x + y[u]);
+              alive = alive && c < pb && key >= Tlo;
+              cnt += alive;
+              any |= __ballot_sync(FULL, alive);
+              emit(alive && !(g.forced && my == 0 && c == 0), key, pack(g.t, g.oa + my, g.ob + c));
+            }
+            if (!any) break;
+          }
+          pb = __shfl_sync(FULL, cnt, 31);  // the next block's rows lie below row r1 + 31
+        }
       }
-    }
+    };
+    materialise();
     __syncthreads();
     C = n_cand;
+    if (C < m_sel && Tlo != Tlo_safe) {  // the optimistic edge was too high: re-walk
+      __syncthreads();
+      if (threadIdx.x == 0) n_cand = 0;
+      __syncthreads();
+      Tlo = Tlo_safe;
+      refalls = 1;
+      materialise();
+      __syncthreads();
+      C = n_cand;
+    }
     flat = C <= a.ccap;
     ck[2] = clock64();
     // ---- 3. T* (every arm pair is >= every other pair of its row / column, so
@@ -936,6 +960,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_probe_select(ProbeArgs a) {
       d[8] = flat;
       d[9] = C;
       d[10] = ties_total;
+      d[11] = refalls;
     }
   }
 }
@@ -1452,7 +1477,11 @@ static void stage_a(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   const uint32_t ccap = cand_cap(ix, qprobes);
   ProbeArgs pa{sl.vals.p, sl.codes.p, nqc, L, K, scap, ix.prm.D, ix.NB, peff, ix.offsets,
                ix.table_base, sl.ppos.p, sl.plen.p, sl.eq.p, dbg_probes, sl.gbuf.p, lstride,
-               nullptr, sl.ckey.p, sl.cpair.p, ccap};
+               nullptr, sl.ckey.p, sl.cpair.p, ccap, 0};
+  // first T_lo attempt at arm rank 0.7 m (no re-walks on C2; FPP_PS_BETA overrides,
+  // e.g. tests force the exact re-walk fallback with a low beta)
+  const char* beta_env = getenv("FPP_PS_BETA");
+  pa.beta_q8 = beta_env ? (uint32_t)(atof(beta_env) * 256) : 179u;
   static const bool dbg_probe = getenv("FPP_DEBUG_PROBE") != nullptr;
   if (dbg_probe) {
     sl.dbgclk.ensure((size_t)nqc * 16);
@@ -1464,17 +1493,18 @@ static void stage_a(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     std::vector<long long> h((size_t)nqc * 16);
     FPP_CUDA(cudaMemcpyAsync(h.data(), pa.dbg_clk, h.size() * 8, cudaMemcpyDeviceToHost, st));
     FPP_CUDA(cudaStreamSynchronize(st));
-    double acc[6] = {0}, fl = 0, cn = 0, ti = 0;
+    double acc[6] = {0}, fl = 0, cn = 0, ti = 0, rf = 0;
     for (uint32_t i = 0; i < nqc; ++i) {
       for (int j = 0; j < 6; ++j) acc[j] += (double)(h[i * 16 + j + 1] - h[i * 16 + j]);
       fl += (double)h[i * 16 + 8];
       cn += (double)h[i * 16 + 9];
       ti += (double)h[i * 16 + 10];
+      rf += (double)h[i * 16 + 11];
     }
     fprintf(stderr, "[probe dbg] per query cycles: arms %.0f materialise %.0f radix %.0f ties %.0f "
-            "emit %.0f resolve %.0f | flat %.2f candidates %.1f ties %.2f\n", acc[0] / nqc,
-            acc[1] / nqc, acc[2] / nqc, acc[3] / nqc, acc[4] / nqc, acc[5] / nqc, fl / nqc,
-            cn / nqc, ti / nqc);
+            "emit %.0f resolve %.0f | flat %.2f candidates %.1f ties %.2f re-walks %.4f\n",
+            acc[0] / nqc, acc[1] / nqc, acc[2] / nqc, acc[3] / nqc, acc[4] / nqc, acc[5] / nqc,
+            fl / nqc, cn / nqc, ti / nqc, rf / nqc);
   }
   k_scan_eq<<<1, 1024, 0, st>>>(sl.eq.p, nqc, sl.coff.p);
   FPP_LAUNCH();

@@ -174,6 +174,24 @@ def test_query_parity(fpp, orc, case):
             assert np.array_equal(gc, oc), (qp, qi)
 
 
+@pytest.mark.parametrize("beta", ["0.3", "1.0"])
+def test_probe_threshold_fallback(fpp, orc, beta, monkeypatch):
+    # FPP_PS_BETA=0.3: the optimistic first T_lo is too high for most queries, so
+    # k_probe_select re-walks at the safe arm bound; 1.0 disables the first attempt
+    monkeypatch.setenv("FPP_PS_BETA", beta)
+    X = data(fpp, 12000, 300, 100, 0.3)
+    Q = data(fpp, 48, 300, 100, 0.3, stream=1)
+    ix = fpp.Index.build(X, L=8, K=2, D=512, iProbes=3, alpha=0.05)
+    ox = orc.Index(X, L=8, K=2, D=512, iprobes=3, alpha=0.05)
+    for qp in (800, 2000):
+        gi, gs, gst = ix.query(Q, 20, qp, return_stats=True)
+        oi, os_, ost = ox.query(Q, 20, qp)
+        assert np.array_equal(gst, ost) and np.array_equal(gi, oi) and np.array_equal(gs, os_)
+        gp, _ = ix.query_debug(Q[5], qp)
+        op, _ = ox.query_debug(Q[5], qp)
+        assert np.array_equal(gp, op)
+
+
 def test_acceptance4_exhaustive_equals_bruteforce(fpp, orc):
     # alpha=1, iProbes=1, qProbes=L*4D^2 must equal brute force
     X = data(fpp, 2000, 32, seed=3)
