@@ -978,7 +978,8 @@ uint64_t shard_slots(Index& ix, const uint32_t* ghist) {
   st->slot_base_h.assign(L + 1, 0);
   for (uint32_t t = 0; t < L; ++t) st->slot_base_h[t + 1] = st->slot_base_h[t] + th[t];
   st->slot_base.ensure(L + 1);
-  FPP_CUDA(cudaMemcpy(st->slot_base.p, st->slot_base_h.data(), (L + 1) * 8, cudaMemcpyHostToDevice));
+  FPP_CUDA(cudaMemcpyAsync(st->slot_base.p, st->slot_base_h.data(), (L + 1) * 8,
+                           cudaMemcpyHostToDevice, s));
   st->slots = st->slot_base_h[L];
   return st->slots;
 }
@@ -1021,7 +1022,8 @@ void shard_finish(Index& ix, const uint32_t* ghist, const uint64_t* all_prefix, 
   for (uint32_t t = 0; t < L; ++t) ix.table_base_h[t + 1] = ix.table_base_h[t] + th[t];
   ix.kept_total = ix.table_base_h[L];
   ix.table_base = static_cast<uint64_t*>(dmalloc((size_t)(L + 1) * sizeof(uint64_t)));
-  FPP_CUDA(cudaMemcpy(ix.table_base, ix.table_base_h.data(), (L + 1) * 8, cudaMemcpyHostToDevice));
+  FPP_CUDA(cudaMemcpyAsync(ix.table_base, ix.table_base_h.data(), (L + 1) * 8,
+                           cudaMemcpyHostToDevice, s));
   ix.ids = static_cast<uint32_t*>(dmalloc((ix.kept_total + 1) * sizeof(uint32_t)));
   ix.scores = static_cast<float*>(dmalloc((ix.kept_total + 1) * sizeof(float)));
   FPP_CUDA(cudaMemsetAsync(mk.p, 0, 4, s));

@@ -454,8 +454,10 @@ int fpp_shard_hist(const fpp_index* idx, uint32_t* hist_dev) {
     const Index& ix = IX(idx);
     if (!ix.shard) fail(FPP_ERR_INVALID_ARGUMENT, "shard: not a sharded build in progress");
     DeviceGuard dg(ix.device);
-    FPP_CUDA(cudaMemcpy(hist_dev, shard_hist_ptr(ix), (uint64_t)ix.prm.L * ix.NB * 4,
-                        cudaMemcpyDeviceToDevice));
+    // on the index stream, then synchronised: the caller may use hist_dev on any stream
+    FPP_CUDA(cudaMemcpyAsync(hist_dev, shard_hist_ptr(ix), (uint64_t)ix.prm.L * ix.NB * 4,
+                             cudaMemcpyDeviceToDevice, ix.stream));
+    FPP_CUDA(cudaStreamSynchronize(ix.stream));
   });
 }
 
@@ -541,7 +543,7 @@ int fpp_project(const fpp_index* idx, const float* X, uint64_t n, uint32_t t, ui
     DeviceGuard dg(ix.device);
     std::lock_guard<std::mutex> lk(ix.mu);
     DBuf<float> xd(n * ix.d), od(n * ix.prm.D);
-    FPP_CUDA(cudaMemcpy(xd.p, X, n * ix.d * 4, cudaMemcpyHostToDevice));
+    FPP_CUDA(cudaMemcpyAsync(xd.p, X, n * ix.d * 4, cudaMemcpyHostToDevice, ix.stream));
     launch_project(ix, xd.p, n, t, f, od.p, ix.stream);
     FPP_CUDA(cudaStreamSynchronize(ix.stream));
     FPP_CUDA(cudaMemcpy(out, od.p, n * ix.prm.D * 4, cudaMemcpyDeviceToHost));
@@ -559,7 +561,7 @@ int fpp_index_probes(const fpp_index* idx, const float* X, uint64_t n, uint32_t 
     const uint32_t ip = ix.prm.iprobes;
     DBuf<float> xd(n * ix.d);
     DBuf<uint2> od(n * ip);
-    FPP_CUDA(cudaMemcpy(xd.p, X, n * ix.d * 4, cudaMemcpyHostToDevice));
+    FPP_CUDA(cudaMemcpyAsync(xd.p, X, n * ix.d * 4, cudaMemcpyHostToDevice, ix.stream));
     launch_index_probes(ix, xd.p, n, t, od.p, ix.stream);
     FPP_CUDA(cudaStreamSynchronize(ix.stream));
     std::vector<uint2> h(n * ip);
@@ -589,7 +591,7 @@ int fpp_query_lists(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t 
     const uint64_t tot = nq * ix.prm.L * ix.prm.K * s;
     DBuf<float> qd(nq * ix.d), vd(tot);
     DBuf<uint32_t> cd(tot);
-    FPP_CUDA(cudaMemcpy(qd.p, Q, nq * ix.d * 4, cudaMemcpyHostToDevice));
+    FPP_CUDA(cudaMemcpyAsync(qd.p, Q, nq * ix.d * 4, cudaMemcpyHostToDevice, ix.stream));
     launch_query_lists(ix, qd.p, nq, s, vd.p, cd.p, ix.stream);
     FPP_CUDA(cudaStreamSynchronize(ix.stream));
     FPP_CUDA(cudaMemcpy(vals, vd.p, tot * 4, cudaMemcpyDeviceToHost));
@@ -605,7 +607,7 @@ int fpp_query_debug(const fpp_index* idx, const float* q, uint32_t qprobes, uint
     DeviceGuard dg(ix.device);
     std::lock_guard<std::mutex> lk(ix.mu);
     DBuf<float> qd(ix.d);
-    FPP_CUDA(cudaMemcpy(qd.p, q, ix.d * 4, cudaMemcpyHostToDevice));
+    FPP_CUDA(cudaMemcpyAsync(qd.p, q, ix.d * 4, cudaMemcpyHostToDevice, ix.stream));
     std::vector<uint64_t> pv;
     std::vector<uint32_t> cv;
     query_debug(ix, qd.p, qprobes, pv, cv);

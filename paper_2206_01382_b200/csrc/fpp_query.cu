@@ -1024,10 +1024,24 @@ __device__ __forceinline__ void collect_walk(const uint64_t* pp, const uint32_t*
                                              const uint32_t* __restrict__ ids, uint32_t* out,
                                              uint32_t* ucount, NextChunk&& next_chunk, TAS&& tas) {
   const int lane = threadIdx.x & 31;
-  for (uint32_t c = next_chunk(); c * 32 < P; c = next_chunk()) {
-    const uint32_t i = c * 32 + lane;
-    const uint32_t len = i < P ? pl[i] : 0;
-    const uint64_t pos = i < P ? pp[i] : 0;
+  // the next chunk's (pos, len) are loaded while the current chunk's ids are walked
+  uint32_t c = next_chunk();
+  uint32_t nlen = 0;
+  uint64_t npos = 0;
+  if (c * 32 + lane < P) {
+    nlen = pl[c * 32 + lane];
+    npos = pp[c * 32 + lane];
+  }
+  while (c * 32 < P) {
+    const uint32_t len = nlen;
+    const uint64_t pos = npos;
+    c = next_chunk();
+    nlen = 0;
+    npos = 0;
+    if (c * 32 + lane < P) {
+      nlen = pl[c * 32 + lane];
+      npos = pp[c * 32 + lane];
+    }
     uint32_t incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1629,10 +1643,8 @@ void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32
   if (!ix.sA) {
     int lo = 0, hi = 0;
     FPP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    const char* pe = getenv("FPP_PRIO");  // experiment knob: 0 equal, 2 = A high
-    const int pm = pe ? atoi(pe) : 1;
-    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sA, cudaStreamNonBlocking, pm == 2 ? hi : lo));
-    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sB, cudaStreamNonBlocking, pm == 1 ? hi : lo));
+    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sA, cudaStreamNonBlocking, lo));
+    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sB, cudaStreamNonBlocking, hi));
     FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_fork, cudaEventDisableTiming));
     FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_join, cudaEventDisableTiming));
     FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_join2, cudaEventDisableTiming));
