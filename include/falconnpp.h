@@ -39,6 +39,9 @@ extern "C" {
 #define FPP_ERR_CUDA 7             /* no device / CUDA runtime failure */
 #define FPP_ERR_OUT_OF_MEMORY 8
 #define FPP_ERR_UNSUPPORTED 9      /* valid per SPEC but outside the GPU path's envelope */
+#define FPP_ERR_FORMAT 10          /* index file: bad magic, truncated, checksum / dataset mismatch
+                                       */
+#define FPP_ERR_IO 11              /* index file cannot be opened / written */
 
 /* IndexConfig, SPEC.md:233-236 (mode = falconnpp, centering off). */
 typedef struct fpp_params {
@@ -166,6 +169,22 @@ int fpp_shard_finish(fpp_index* idx, const uint32_t* global_hist_dev,
                      const uint64_t* all_prefix_dev, uint32_t world);
 
 /* -------------------------------------------------------------- host helpers */
+/* ---- index persistence: FLPP files (SPEC.md:270-278 save/load, 283-287 format).
+ * Replaces save(index, path) / load(path).  The dataset is stored by reference
+ * (fnv1a64 content hash of the n*d fp32 bytes, common.hpp:50-57): fpp_load takes
+ * the same X again and fails with FPP_ERR_FORMAT if its hash differs.  A save of
+ * the same (dataset, config) is byte-identical; load(save(ix)) answers every
+ * query bit-identically.  Errors: FPP_ERR_IO (open/write), FPP_ERR_FORMAT (bad
+ * magic, truncated file, checksum or dataset mismatch), FPP_ERR_UNSUPPORTED
+ * (other FLPP version), FPP_ERR_DIMENSION (X shape differs from the index). */
+#define FPP_FLPP_VERSION 1
+int fpp_save(const fpp_index* idx, const char* path);
+int fpp_load(const char* path, const float* X, uint64_t n, uint32_t d, int device,
+             fpp_index** out);
+int fpp_load_device(const char* path, const float* X_dev, uint64_t n, uint32_t d, int device,
+                    fpp_index** out);
+uint64_t fpp_content_hash(const float* X, uint64_t n, uint32_t d);
+
 /* normalize(Dataset) in place (dataset.cpp:24-38); FPP_ERR_ZERO_NORM names the row */
 int fpp_normalize(float* X, uint64_t n, uint32_t d);
 /* seeded synthetic data: clusters=0 -> i.i.d. N(0,1);

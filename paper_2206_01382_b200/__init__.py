@@ -22,14 +22,16 @@ from . import _build
 
 __all__ = ["Index", "normalize", "synth", "device_count", "FppError", "FppInvalidArgument",
            "FppEmptyDataset", "FppDimensionError", "FppOutOfRange", "FppNonFinite",
-           "FppZeroNorm", "FppCudaError", "FppOutOfMemory", "FppUnsupported", "lib",
+           "FppZeroNorm", "FppCudaError", "FppOutOfMemory", "FppUnsupported", "FppFormatError",
+           "FppIOError", "content_hash", "lib",
            "LIB_PATH", "Params", "QueryStats", "Timings"]
 
 LIB_PATH = _build.LIB
 
 FPP_OK = 0
 ERRORS = {1: "INVALID_ARGUMENT", 2: "EMPTY_DATASET", 3: "DIMENSION", 4: "OUT_OF_RANGE",
-          5: "NON_FINITE", 6: "ZERO_NORM", 7: "CUDA", 8: "OUT_OF_MEMORY", 9: "UNSUPPORTED"}
+          5: "NON_FINITE", 6: "ZERO_NORM", 7: "CUDA", 8: "OUT_OF_MEMORY", 9: "UNSUPPORTED",
+          10: "FORMAT", 11: "IO"}
 
 
 class FppError(Exception):
@@ -72,9 +74,18 @@ class FppUnsupported(FppError, NotImplementedError):
     code = 9
 
 
+class FppFormatError(FppError, ValueError):
+    """Index file: bad magic, truncated, checksum or dataset-hash mismatch."""
+    code = 10
+
+
+class FppIOError(FppError, OSError):
+    code = 11
+
+
 _EXC = {c.code: c for c in (FppInvalidArgument, FppEmptyDataset, FppDimensionError, FppOutOfRange,
                             FppNonFinite, FppZeroNorm, FppCudaError, FppOutOfMemory,
-                            FppUnsupported)}
+                            FppUnsupported, FppFormatError, FppIOError)}
 
 
 class Params(C.Structure):
@@ -139,6 +150,10 @@ SIGNATURES = [
     ("fpp_shard_slots", C.c_int, [vp, vp, C.POINTER(u64)]),
     ("fpp_shard_prefix", C.c_int, [vp, vp, vp]),
     ("fpp_shard_finish", C.c_int, [vp, vp, vp, u32]),
+    ("fpp_save", C.c_int, [vp, C.c_char_p]),
+    ("fpp_load", C.c_int, [C.c_char_p, vp, u64, u32, i32, C.POINTER(vp)]),
+    ("fpp_load_device", C.c_int, [C.c_char_p, vp, u64, u32, i32, C.POINTER(vp)]),
+    ("fpp_content_hash", u64, [vp, u64, u32]),
     ("fpp_normalize", C.c_int, [vp, u64, u32]),
     ("fpp_synth", C.c_int, [vp, u64, u32, u32, f32, u64, u32, i32]),
 ]
@@ -247,6 +262,32 @@ class Index:
             X = _f32(X)
             n, d = X.shape
             _check(lib().fpp_shard_begin(_ptr(X), n, d, C.byref(p), C.byref(h)))
+        return cls(h, p, n, d)
+
+    # --------------------------------------------------------- persistence
+    def save(self, path) -> None:
+        """save(index, path) -- SPEC.md:270-278; FLPP format (include/falconnpp.h)."""
+        _check(lib().fpp_save(self._h, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path, X, device: int = -1):
+        """load(path) -- the dataset is stored by reference: pass the same X (host
+        numpy or CUDA tensor); its content hash must match the file's."""
+        h = C.c_void_p()
+        if _is_torch_cuda(X):
+            X = X.contiguous()
+            n, d = X.shape
+            dev = (X.device.index or 0) if device < 0 else device
+            _check(lib().fpp_load_device(os.fsencode(path), C.c_void_p(X.data_ptr()), n, d, dev,
+                                         C.byref(h)))
+        else:
+            X = _f32(X)
+            n, d = X.shape
+            _check(lib().fpp_load(os.fsencode(path), _ptr(X), n, d, max(device, 0), C.byref(h)))
+        inf = IndexInfo()
+        _check(lib().fpp_index_info_get(h, C.byref(inf)))
+        p = Params(inf.L, inf.K, inf.D, inf.iprobes, inf.kappa, inf.alpha, inf.seed,
+                   max(device, 0), inf.id_offset, 0)
         return cls(h, p, n, d)
 
     def shard_hist_len(self) -> int:
@@ -369,6 +410,12 @@ class Index:
 
     def reset_timings(self) -> None:
         _check(lib().fpp_timings_reset(self._h))
+
+
+def content_hash(X) -> int:
+    """fnv1a64 of the fp32 bytes (common.hpp:50-57): the FLPP dataset reference."""
+    X = _f32(X)
+    return int(lib().fpp_content_hash(_ptr(X), X.shape[0], X.shape[1]))
 
 
 def _is_torch_cuda(x) -> bool:

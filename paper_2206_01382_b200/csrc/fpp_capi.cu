@@ -226,8 +226,9 @@ static void validate_params(const fpp_params& p, uint64_t n, uint32_t d) {
     fail(FPP_ERR_UNSUPPORTED, "GPU path: n*iProbes must be < 2^32 per shard");
 }
 
-static fpp_index* build_common(const float* X, bool on_device, uint64_t n, uint32_t d,
-                               const fpp_params* pp, bool sharded = false) {
+// Validated index shell: X resident on the device, sign bitmasks uploaded, no
+// tables yet (build_tables, shard_begin or load_tables fill them).
+Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, const fpp_params* pp) {
   if (!pp) fail(FPP_ERR_INVALID_ARGUMENT, "build: params is NULL");
   if (!X && n) fail(FPP_ERR_INVALID_ARGUMENT, "build: X is NULL");
   const fpp_params p = *pp;
@@ -276,10 +277,22 @@ static fpp_index* build_common(const float* X, bool on_device, uint64_t n, uint3
     FPP_CUDA(cudaMemcpyAsync(ix->signs, words.data(), words.size() * 4, cudaMemcpyHostToDevice,
                              ix->stream));
     FPP_CUDA(cudaStreamSynchronize(ix->stream));
+    ix->sign_words = words.size();
+  } catch (...) {
+    delete ix;
+    throw;
+  }
+  return ix;
+}
+
+static fpp_index* build_common(const float* X, bool on_device, uint64_t n, uint32_t d,
+                               const fpp_params* pp, bool sharded = false) {
+  Index* ix = prepare_index(X, on_device, n, d, pp);
+  try {
     if (sharded) shard_begin(*ix);
     else build_tables(*ix);
-    ix->device_bytes = n * d * 4 + words.size() * 4 + (uint64_t)p.L * (ix->NB + 1) * 4 +
-                       (p.L + 1) * 8 + ix->kept_total * 8;
+    ix->device_bytes = n * d * 4 + ix->sign_words * 4 + (uint64_t)ix->prm.L * (ix->NB + 1) * 4 +
+                       (ix->prm.L + 1) * 8 + ix->kept_total * 8;
     double ms[PH_COUNT] = {0};
     ix->timer.collect(ms);
     ix->acc.hash_ms += ms[PH_HASH];
@@ -636,6 +649,35 @@ int fpp_timings_reset(const fpp_index* idx) {
 }
 
 // dataset.cpp:24-38, parallel over rows (per-row arithmetic is the reference's)
+int fpp_save(const fpp_index* idx, const char* path) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    DeviceGuard dg(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    save_index(ix, path, nullptr);
+  });
+}
+
+int fpp_load(const char* path, const float* X, uint64_t n, uint32_t d, int device,
+             fpp_index** out) {
+  return guarded([&] {
+    if (!out) fail(FPP_ERR_INVALID_ARGUMENT, "load: out is NULL");
+    *out = reinterpret_cast<fpp_index*>(load_index(path, X, false, n, d, device));
+  });
+}
+
+int fpp_load_device(const char* path, const float* X_dev, uint64_t n, uint32_t d, int device,
+                    fpp_index** out) {
+  return guarded([&] {
+    if (!out) fail(FPP_ERR_INVALID_ARGUMENT, "load: out is NULL");
+    *out = reinterpret_cast<fpp_index*>(load_index(path, X_dev, true, n, d, device));
+  });
+}
+
+uint64_t fpp_content_hash(const float* X, uint64_t n, uint32_t d) {
+  return X ? content_hash(X, n, d) : 0;
+}
+
 int fpp_normalize(float* X, uint64_t n, uint32_t d) {
   return guarded([&] {
     if (!X || !n || !d) fail(FPP_ERR_EMPTY_DATASET, "dataset: need at least one point");

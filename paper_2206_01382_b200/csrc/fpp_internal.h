@@ -84,6 +84,7 @@ struct Index {
   float* scores = nullptr;   // [kept_total]
   uint64_t kept_total = 0;
   uint32_t max_bucket = 0;
+  uint64_t sign_words = 0;
   uint64_t device_bytes = 0;
   ShardState* shard = nullptr;  // global-filter sharded build in progress
 
@@ -136,6 +137,11 @@ int sm_count();
 
 // build (fpp_build.cu)
 void build_tables(Index& ix);
+Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, const fpp_params* pp);
+uint64_t content_hash(const float* X, uint64_t n, uint32_t d);
+void save_index(const Index& ix, const char* path, const float* X_host);
+Index* load_index(const char* path, const float* X, bool on_device, uint64_t n, uint32_t d,
+                  int device);
 void launch_project(const Index& ix, const float* Xd, uint64_t n, uint32_t t, uint32_t f,
                     float* out, cudaStream_t s);
 void launch_index_probes(const Index& ix, const float* Xd, uint64_t n, uint32_t t,
