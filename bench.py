@@ -502,15 +502,23 @@ def main():
 
     # ---------------------------------------------- qProbes sweep (+ recall)
     sweep = []
+    gt_info = None
     if not args.no_sweep and world == 1:
         gt = None
         if not args.no_recall:
+            # exact ground truth on the GPU (fpp_brute_force: inner_product bit for bit,
+            # ties to the lower id -- SPEC.md:490-503), timed separately from the sweep
             nr = min(nq, 1000)
-            Xall = torch.from_numpy(X).cuda().double()
-            S = Qd[:nr].double() @ Xall.T
-            # ties by lower id: topk on score then stable by id is overkill at fp64; use topk
-            gt = torch.topk(S, K_TOP, dim=1).indices.cpu().numpy()
-            del Xall, S
+            gt_ids = torch.empty((nr, K_TOP), dtype=torch.int32, device="cuda")
+            gt_sc = torch.empty((nr, K_TOP), dtype=torch.float64, device="cuda")
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record()
+            ix.brute_force_device(Qd[:nr].contiguous(), gt_ids, gt_sc, K_TOP, stream=stream)
+            g1.record()
+            torch.cuda.synchronize()
+            gt = gt_ids.cpu().numpy().view(np.uint32)
+            gt_info = {"queries": nr, "ms": g0.elapsed_time(g1),
+                       "method": "exact fp64 brute force on the GPU (fpp_brute_force)"}
         for qp in cfg["sweep"]:
             ix.reset_timings()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -575,6 +583,7 @@ def main():
             "gpu_launches": int(tim["launches"]),
             "cpu_baseline": cpu,
             "sweep": sweep,
+            "ground_truth": gt_info,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -169,6 +169,15 @@ int fpp_shard_finish(fpp_index* idx, const uint32_t* global_hist_dev,
                      const uint64_t* all_prefix_dev, uint32_t world);
 
 /* -------------------------------------------------------------- host helpers */
+/* ---- exact brute force over the index's dataset: the recall ground truth
+ * (SPEC.md:490-503 brute_force_topk).  Scores are inner_product (dataset.cpp:61-69)
+ * bit for bit; top-k by (score desc, id asc), ids global (id_offset added).
+ * Errors as fpp_query (k <= 32, k <= n, dimension, finite Q). */
+int fpp_brute_force(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uint32_t* ids,
+                    double* scores);
+int fpp_brute_force_device(const fpp_index* idx, const float* Q_dev, uint64_t nq, uint32_t k,
+                           uint32_t* ids_dev, double* scores_dev, void* stream);
+
 /* ---- index persistence: FLPP files (SPEC.md:270-278 save/load, 283-287 format).
  * Replaces save(index, path) / load(path).  The dataset is stored by reference
  * (fnv1a64 content hash of the n*d fp32 bytes, common.hpp:50-57): fpp_load takes

@@ -150,6 +150,8 @@ SIGNATURES = [
     ("fpp_shard_slots", C.c_int, [vp, vp, C.POINTER(u64)]),
     ("fpp_shard_prefix", C.c_int, [vp, vp, vp]),
     ("fpp_shard_finish", C.c_int, [vp, vp, vp, u32]),
+    ("fpp_brute_force", C.c_int, [vp, vp, u64, u32, vp, vp]),
+    ("fpp_brute_force_device", C.c_int, [vp, vp, u64, u32, vp, vp, vp]),
     ("fpp_save", C.c_int, [vp, C.c_char_p]),
     ("fpp_load", C.c_int, [C.c_char_p, vp, u64, u32, i32, C.POINTER(vp)]),
     ("fpp_load_device", C.c_int, [C.c_char_p, vp, u64, u32, i32, C.POINTER(vp)]),
@@ -263,6 +265,27 @@ class Index:
             n, d = X.shape
             _check(lib().fpp_shard_begin(_ptr(X), n, d, C.byref(p), C.byref(h)))
         return cls(h, p, n, d)
+
+    def brute_force(self, Q, k: int):
+        """Exact top-k over the index's dataset (recall ground truth):
+        inner_product scores bit for bit, ties to the lower id."""
+        Q = _f32(Q)
+        nq = Q.shape[0]
+        if Q.shape[1] != self.d:
+            raise FppDimensionError("brute_force_topk: dimension mismatch")
+        ids = np.empty((nq, k), np.uint32)
+        sc = np.empty((nq, k), np.float64)
+        _check(lib().fpp_brute_force(self._h, _ptr(Q), nq, k, _ptr(ids), _ptr(sc)))
+        return ids, sc
+
+    def brute_force_device(self, Q, ids, scores, k: int, stream=None):
+        """Device-resident exact top-k on torch CUDA tensors."""
+        if Q.shape[1] != self.d:
+            raise FppDimensionError("brute_force_topk: dimension mismatch")
+        _check(lib().fpp_brute_force_device(self._h, C.c_void_p(Q.data_ptr()), Q.shape[0], k,
+                                            C.c_void_p(ids.data_ptr()),
+                                            C.c_void_p(scores.data_ptr()),
+                                            C.c_void_p(stream) if stream else None))
 
     # --------------------------------------------------------- persistence
     def save(self, path) -> None:

@@ -649,6 +649,47 @@ int fpp_timings_reset(const fpp_index* idx) {
 }
 
 // dataset.cpp:24-38, parallel over rows (per-row arithmetic is the reference's)
+static void validate_brute(const Index& ix, uint64_t nq, uint32_t k, const void* Q,
+                           const void* ids, const void* scores) {
+  if (k == 0) fail(FPP_ERR_INVALID_ARGUMENT, "brute_force_topk: k must be >= 1");
+  if (k > ix.n) fail(FPP_ERR_OUT_OF_RANGE, "brute_force_topk: k > n");
+  if (k > 32) fail(FPP_ERR_UNSUPPORTED, "GPU path: k must be <= 32");
+  if (nq && (!Q || !ids || !scores)) fail(FPP_ERR_INVALID_ARGUMENT, "brute_force_topk: NULL buffer");
+}
+
+int fpp_brute_force(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uint32_t* ids,
+                    double* scores) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    validate_brute(ix, nq, k, Q, ids, scores);
+    if (!nq) return;
+    DeviceGuard dg(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    cudaStream_t s = ix.stream;
+    DBuf<float> qd(nq * ix.d);
+    DBuf<uint32_t> id(nq * k);
+    DBuf<double> sc(nq * k);
+    FPP_CUDA(cudaMemcpyAsync(qd.p, Q, nq * ix.d * 4, cudaMemcpyHostToDevice, s));
+    run_brute_force(ix, qd.p, nq, k, id.p, sc.p, s);
+    FPP_CUDA(cudaMemcpyAsync(ids, id.p, nq * k * 4, cudaMemcpyDeviceToHost, s));
+    FPP_CUDA(cudaMemcpyAsync(scores, sc.p, nq * k * 8, cudaMemcpyDeviceToHost, s));
+    FPP_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int fpp_brute_force_device(const fpp_index* idx, const float* Q_dev, uint64_t nq, uint32_t k,
+                           uint32_t* ids_dev, double* scores_dev, void* stream) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    validate_brute(ix, nq, k, Q_dev, ids_dev, scores_dev);
+    if (!nq) return;
+    DeviceGuard dg(ix.device);
+    std::lock_guard<std::mutex> lk(ix.mu);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ix.stream;
+    run_brute_force(ix, Q_dev, nq, k, ids_dev, scores_dev, s);
+  });
+}
+
 int fpp_save(const fpp_index* idx, const char* path) {
   return guarded([&] {
     const Index& ix = IX(idx);

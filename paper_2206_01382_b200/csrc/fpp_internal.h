@@ -140,6 +140,8 @@ void build_tables(Index& ix);
 Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, const fpp_params* pp);
 uint64_t content_hash(const float* X, uint64_t n, uint32_t d);
 void save_index(const Index& ix, const char* path, const float* X_host);
+void run_brute_force(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t* ids_d,
+                     double* scores_d, cudaStream_t s);
 Index* load_index(const char* path, const float* X, bool on_device, uint64_t n, uint32_t d,
                   int device);
 void launch_project(const Index& ix, const float* Xd, uint64_t n, uint32_t t, uint32_t f,

@@ -310,3 +310,19 @@ def test_sharded_global_filter_equals_single_gpu_index(fpp, orc, world):
                               torch.from_numpy(np.concatenate([o[0].astype(np.int64) for o in outs], 1)), k)
     assert np.array_equal(mi.numpy(), fi.astype(np.int64))
     assert np.array_equal(ms.numpy(), fsc)
+
+
+@pytest.mark.parametrize("n,d,k", [(5000, 300, 20), (3001, 17, 7), (2000, 960, 32), (40, 64, 32)])
+def test_brute_force_exact(fpp, orc, n, d, k):
+    # recall ground truth: inner_product scores bit for bit, ties to lower id
+    X = data(fpp, n, d, 10, 0.3, seed=6)
+    X[n // 2: n // 2 + 5] = X[3]  # exact duplicates: equal scores, lower id first
+    Q = data(fpp, 37, d, 10, 0.3, seed=6, stream=1)
+    Q[0] = X[3]
+    ix = fpp.Index.build(X, L=2, K=2, D=orc.lib().orc_pad_dimension(d) if d >= 16 else 16,
+                         iProbes=1, alpha=1.0)
+    gi, gs = ix.brute_force(Q, k)
+    bi, bs = orc.brute_force(X, Q, k)
+    assert np.array_equal(gi, bi)
+    assert np.array_equal(gs, bs)
+    assert list(gi[0][:6]) == [3] + list(range(n // 2, n // 2 + 5))
