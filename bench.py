@@ -427,7 +427,7 @@ def main():
     Qd = torch.from_numpy(Q).cuda()
     ids_d = torch.empty((nq, K_TOP), dtype=torch.int32, device="cuda")
     sc_d = torch.empty((nq, K_TOP), dtype=torch.float64, device="cuda")
-    st_d = torch.empty((nq, 3), dtype=torch.int64, device="cuda")
+    st_d = torch.empty((nq, 4), dtype=torch.int64, device="cuda")
     stream = torch.cuda.current_stream().cuda_stream
 
     def step(qp, stats=None):
@@ -439,7 +439,7 @@ def main():
     step(qprobes, st_d)
     torch.cuda.synchronize()
     st = st_d.cpu().numpy().astype(np.uint64)
-    P_sum, E_sum, U_sum = (int(x) for x in st.sum(axis=0))
+    P_sum, E_sum, U_sum, _ = (int(x) for x in st.sum(axis=0))
     for _ in range(args.warmup - 1):
         step(qprobes)
     ix.reset_timings()

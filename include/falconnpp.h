@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FPP_ABI_VERSION 1
+#define FPP_ABI_VERSION 2  /* 2: fpp_query_stats.exact, SimHash rerank */
 
 /* error classes ("one exit code per error class") */
 #define FPP_OK 0
@@ -61,7 +61,8 @@ typedef struct fpp_params {
 typedef struct fpp_query_stats {
   uint64_t probes;     /* P_q: buckets probed */
   uint64_t entries;    /* E_q: kept entries walked in the probed buckets */
-  uint64_t candidates; /* U_q: unique ids scored (exact inner products) */
+  uint64_t candidates; /* U_q: unique ids collected */
+  uint64_t exact;      /* exact inner products computed: U_q, or min(B, U_q) with rerank */
 } fpp_query_stats;
 
 /* per-kernel device time accumulated since the last reset (CUDA events) */
@@ -110,6 +111,20 @@ int fpp_query(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uin
 int fpp_query_device(const fpp_index* idx, const float* Q_dev, uint64_t nq, uint32_t k,
                      uint32_t qprobes, uint32_t* ids_dev, double* scores_dev,
                      fpp_query_stats* stats_dev, void* stream);
+
+/* search with a SimHash rerank budget B (SPEC.md:311-314 QueryParams, :330-338
+ * simhash_screen): the collected candidates are screened to the B with the most
+ * agreeing signature bits (64-bit signatures from the (t=0, f=0) projection signs,
+ * ties by lower id) before the exact top-k.  B = 0 is fpp_query; otherwise B >= k
+ * (FPP_ERR_OUT_OF_RANGE).  stats.exact = min(B, U_q). */
+int fpp_query_rerank(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k,
+                     uint32_t qprobes, uint32_t rerank, uint32_t* ids, double* scores,
+                     fpp_query_stats* stats);
+int fpp_query_rerank_device(const fpp_index* idx, const float* Q_dev, uint64_t nq, uint32_t k,
+                            uint32_t qprobes, uint32_t rerank, uint32_t* ids_dev,
+                            double* scores_dev, fpp_query_stats* stats_dev, void* stream);
+/* the 64-bit SimHash signatures of rows X (host), as stored for the index's points */
+int fpp_signatures(const fpp_index* idx, const float* X, uint64_t n, uint64_t* out);
 
 /* ------------------------------------------------------ introspection / parity */
 typedef struct fpp_index_info {

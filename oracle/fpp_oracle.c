@@ -712,12 +712,52 @@ static void clear_visited(qscratch* w, uint64_t nc) {
   for (uint64_t c = 0; c < nc; ++c) w->visited[w->cands[c] >> 6] = 0;
 }
 
+/* SPEC.md "SimHash signatures": signs of the first 64 coordinates of the first
+   table's first-function projection */
+static uint64_t simhash_one(const orc_index* idx, const float* x, float* out, float* buf) {
+  project_signs(stack_signs(idx, 0, 0), idx->d, idx->P, idx->p.D, x, out, buf);
+  const uint32_t m = idx->p.D < 64 ? idx->p.D : 64;
+  uint64_t s = 0;
+  for (uint32_t j = 0; j < m; ++j)
+    if (out[j] >= 0.0f) s |= 1ull << j;
+  return s;
+}
+
+void orc_simhash_rows(const orc_index* idx, const float* X, uint64_t n, uint64_t* out, int threads) {
+  if (threads <= 0) threads = 1;
+  const uint32_t Dw = blocks_of(idx->P, idx->p.D) * idx->P;
+#pragma omp parallel num_threads(threads)
+  {
+    float* o = (float*)malloc((size_t)Dw * sizeof(float));
+    float* buf = (float*)malloc((size_t)idx->P * sizeof(float));
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < (int64_t)n; ++i) out[i] = simhash_one(idx, X + (uint64_t)i * idx->d, o, buf);
+    free(o);
+    free(buf);
+  }
+}
+
+typedef struct { uint32_t dis; uint32_t id; } screened;  /* dis = 64 - agreement */
+static int cmp_screened(const void* x, const void* y) {    /* agreement desc, id asc */
+  const screened* u = (const screened*)x; const screened* v = (const screened*)y;
+  if (u->dis != v->dis) return (u->dis > v->dis) - (u->dis < v->dis);
+  return (u->id > v->id) - (u->id < v->id);
+}
+
 /* SPEC.md:339-347 top_k_exact over the unique candidates */
 int orc_query(const orc_index* idx, const float* Q, uint64_t nq, uint32_t k,
               uint32_t qprobes, uint32_t* ids, double* scores, orc_stats* stats,
               int threads) {
+  return orc_query_rerank(idx, Q, nq, k, qprobes, 0, ids, scores, stats, threads);
+}
+
+/* search, with simhash_screen when B > 0 */
+int orc_query_rerank(const orc_index* idx, const float* Q, uint64_t nq, uint32_t k,
+                     uint32_t qprobes, uint32_t B, uint32_t* ids, double* scores,
+                     orc_stats* stats, int threads) {
   if (idx->t_begin != 0 || idx->t_end != idx->p.L) return -1;
   if (k == 0 || qprobes < idx->p.L) return -1;
+  if (B != 0 && B < k) return -1;  /* QueryParams: B = 0 or B >= k */
   if (threads <= 0) {
 #ifdef _OPENMP
     threads = omp_get_max_threads();
@@ -728,18 +768,37 @@ int orc_query(const orc_index* idx, const float* Q, uint64_t nq, uint32_t k,
   const uint32_t s = orc_query_cap(idx, qprobes);
   const uint64_t peff = orc_query_probes(idx, qprobes);
   const uint32_t d = idx->d;
+  uint64_t* sigs = NULL;
+  if (B) {
+    sigs = (uint64_t*)malloc((size_t)idx->n * sizeof(uint64_t));
+    orc_simhash_rows(idx, idx->X, idx->n, sigs, threads);
+  }
 #pragma omp parallel num_threads(threads)
   {
     qscratch w;
     qscratch_init(&w, idx, s, peff, k);
+    screened* scr = B ? (screened*)malloc((size_t)idx->n * sizeof(screened)) : NULL;
+    float* po = B ? (float*)malloc((size_t)blocks_of(idx->P, idx->p.D) * idx->P * sizeof(float)) : NULL;
+    float* pbuf = B ? (float*)malloc((size_t)idx->P * sizeof(float)) : NULL;
 #pragma omp for schedule(dynamic, 1)
     for (int64_t qi = 0; qi < (int64_t)nq; ++qi) {
       const float* q = Q + (uint64_t)qi * d;
       uint64_t np, ne;
       const uint64_t nc = collect(idx, q, qprobes, &w, &np, &ne);
+      uint64_t nx = nc;  /* exact inner products */
+      if (B && nc > B) {  /* simhash_screen: top B by bit agreement, ties by lower id */
+        const uint64_t sq = simhash_one(idx, q, po, pbuf);
+        for (uint64_t c = 0; c < nc; ++c) {
+          scr[c].dis = (uint32_t)__builtin_popcountll(sigs[w.cands[c]] ^ sq);
+          scr[c].id = w.cands[c];
+        }
+        qsort(scr, nc, sizeof(screened), cmp_screened);
+        nx = B;
+      }
       uint32_t cnt = 0;
-      for (uint64_t c = 0; c < nc; ++c) {
-        scored x = {orc_inner_product(idx->X + (uint64_t)w.cands[c] * d, q, d), w.cands[c]};
+      for (uint64_t c = 0; c < nx; ++c) {
+        const uint32_t cid = nx < nc ? scr[c].id : w.cands[c];
+        scored x = {orc_inner_product(idx->X + (uint64_t)cid * d, q, d), cid};
         if (cnt == k && !better_scored(&x, &w.top[k - 1])) continue;
         uint32_t pos = cnt < k ? cnt++ : k - 1;
         while (pos > 0 && better_scored(&x, &w.top[pos - 1])) { w.top[pos] = w.top[pos - 1]; --pos; }
@@ -753,11 +812,16 @@ int orc_query(const orc_index* idx, const float* Q, uint64_t nq, uint32_t k,
         stats[qi].probes = np;
         stats[qi].entries = ne;
         stats[qi].candidates = nc;
+        stats[qi].exact = nx;
       }
       clear_visited(&w, nc);
     }
     qscratch_free(&w);
+    free(scr);
+    free(po);
+    free(pbuf);
   }
+  free(sigs);
   return 0;
 }
 

@@ -37,7 +37,8 @@ typedef struct {
 typedef struct {
   uint64_t probes;      /* P_q: probes visited */
   uint64_t entries;     /* E_q: kept bucket entries walked */
-  uint64_t candidates;  /* U_q: unique ids scored */
+  uint64_t candidates;  /* U_q: unique ids collected */
+  uint64_t exact;       /* exact inner products computed (U_q, or min(B, U_q) with rerank) */
 } orc_stats;
 
 typedef struct orc_index orc_index;
@@ -104,6 +105,15 @@ int orc_query(const orc_index* idx, const float* Q, uint64_t nq, uint32_t k,
               int threads);
 /* per-query intermediates; probes as t*NB+bucket, sorted asc; cands sorted asc.
    returns 0; sizes written to *np / *nc (buffers must hold P_eff / n). */
+/* search with SimHash rerank budget B (0 = off): candidates are
+   screened to the top B by signature bit agreement (ties by lower id) before the
+   exact top-k.  orc_query == orc_query_rerank(..., B = 0, ...). */
+int orc_query_rerank(const orc_index* idx, const float* Q, uint64_t nq, uint32_t k,
+                     uint32_t qprobes, uint32_t B, uint32_t* ids, double* scores,
+                     orc_stats* stats, int threads);
+/* 64-bit SimHash signature (SPEC.md "SimHash signatures"): bit j < min(64, D) is
+   1 iff p[j] >= 0 for the (t=0, f=0) projection (-0.0 counts as >= 0) */
+void orc_simhash_rows(const orc_index* idx, const float* X, uint64_t n, uint64_t* out, int threads);
 int orc_query_debug(const orc_index* idx, const float* q, uint32_t qprobes,
                     uint64_t* probes, uint64_t* np, uint32_t* cands, uint64_t* nc);
 /* query projections ranked lists [L][K][s] */

@@ -30,7 +30,7 @@ class Params(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("probes", C.c_uint64), ("entries", C.c_uint64),
-                ("candidates", C.c_uint64)]
+                ("candidates", C.c_uint64), ("exact", C.c_uint64)]
 
 
 def build_oracle(with_ref: bool = True) -> None:
@@ -99,6 +99,11 @@ def lib():
         L.orc_query.restype = C.c_int
         L.orc_query.argtypes = [C.c_void_p, f32p, C.c_uint64, C.c_uint32, C.c_uint32, u32p,
                                 f64p, C.c_void_p, C.c_int]
+        L.orc_query_rerank.restype = C.c_int
+        L.orc_query_rerank.argtypes = [C.c_void_p, f32p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                       C.c_uint32, u32p, f64p, C.c_void_p, C.c_int]
+        L.orc_simhash_rows.restype = None
+        L.orc_simhash_rows.argtypes = [C.c_void_p, f32p, C.c_uint64, u64p, C.c_int]
         L.orc_query_debug.restype = C.c_int
         L.orc_query_debug.argtypes = [C.c_void_p, f32p, C.c_uint32, u64p,
                                       C.POINTER(C.c_uint64), u32p, C.POINTER(C.c_uint64)]
@@ -227,18 +232,27 @@ class Index:
     def peff(self, qprobes: int) -> int:
         return lib().orc_query_probes(self.h, qprobes)
 
-    def query(self, Q: np.ndarray, k: int, qprobes: int, threads: int = 0):
+    def query(self, Q: np.ndarray, k: int, qprobes: int, threads: int = 0, rerank: int = 0):
+        """search; rerank = SimHash budget B (0 = off, :330-338).
+        stats columns: probes, entries, candidates, exact inner products."""
         Q = np.ascontiguousarray(Q, dtype=np.float32)
         nq = Q.shape[0]
         ids = np.empty(nq * k, np.uint32)
         sc = np.empty(nq * k, np.float64)
-        st = (Stats * nq)()
-        r = lib().orc_query(self.h, Q.reshape(-1), nq, k, qprobes, ids, sc,
-                            C.cast(st, C.c_void_p), threads)
+        st = (Stats * max(nq, 1))()
+        r = lib().orc_query_rerank(self.h, Q.reshape(-1), nq, k, qprobes, rerank, ids, sc,
+                                   C.cast(st, C.c_void_p), threads)
         if r != 0:
             raise ValueError("oracle query: invalid arguments")
-        stats = np.array([(s.probes, s.entries, s.candidates) for s in st], dtype=np.uint64)
-        return ids.reshape(nq, k), sc.reshape(nq, k), stats.reshape(nq, 3)
+        stats = np.array([(s.probes, s.entries, s.candidates, s.exact) for s in st[:nq]],
+                         dtype=np.uint64)
+        return ids.reshape(nq, k), sc.reshape(nq, k), stats.reshape(nq, 4)
+
+    def simhash(self, X: np.ndarray, threads: int = 0) -> np.ndarray:
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        out = np.empty(X.shape[0], np.uint64)
+        lib().orc_simhash_rows(self.h, X.reshape(-1), X.shape[0], out, threads)
+        return out
 
     def query_debug(self, q: np.ndarray, qprobes: int):
         q = np.ascontiguousarray(q, dtype=np.float32)

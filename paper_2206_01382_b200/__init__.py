@@ -29,6 +29,7 @@ __all__ = ["Index", "normalize", "synth", "device_count", "FppError", "FppInvali
 LIB_PATH = _build.LIB
 
 FPP_OK = 0
+ABI_VERSION = 2  # include/falconnpp.h FPP_ABI_VERSION this binding was written against
 ERRORS = {1: "INVALID_ARGUMENT", 2: "EMPTY_DATASET", 3: "DIMENSION", 4: "OUT_OF_RANGE",
           5: "NON_FINITE", 6: "ZERO_NORM", 7: "CUDA", 8: "OUT_OF_MEMORY", 9: "UNSUPPORTED",
           10: "FORMAT", 11: "IO"}
@@ -96,7 +97,8 @@ class Params(C.Structure):
 
 
 class QueryStats(C.Structure):
-    _fields_ = [("probes", C.c_uint64), ("entries", C.c_uint64), ("candidates", C.c_uint64)]
+    _fields_ = [("probes", C.c_uint64), ("entries", C.c_uint64), ("candidates", C.c_uint64),
+                ("exact", C.c_uint64)]
 
 
 class Timings(C.Structure):
@@ -132,6 +134,9 @@ SIGNATURES = [
     ("fpp_free", None, [vp]),
     ("fpp_query", C.c_int, [vp, vp, u64, u32, u32, vp, vp, vp]),
     ("fpp_query_device", C.c_int, [vp, vp, u64, u32, u32, vp, vp, vp, vp]),
+    ("fpp_query_rerank", C.c_int, [vp, vp, u64, u32, u32, u32, vp, vp, vp]),
+    ("fpp_query_rerank_device", C.c_int, [vp, vp, u64, u32, u32, u32, vp, vp, vp, vp]),
+    ("fpp_signatures", C.c_int, [vp, vp, u64, vp]),
     ("fpp_index_info_get", C.c_int, [vp, C.POINTER(IndexInfo)]),
     ("fpp_table_size", u64, [vp, u32]),
     ("fpp_table_csr", C.c_int, [vp, u32, vp, vp, vp]),
@@ -174,6 +179,9 @@ def lib():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        if L.fpp_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH}: ABI {L.fpp_abi_version()} != binding ABI {ABI_VERSION}"
+                              " (rebuild with paper_2206_01382_b200._build.build(force=True))")
         _lib = L
     return _lib
 
@@ -341,12 +349,13 @@ class Index:
         self.__del__()
 
     # --------------------------------------------------------------- query
-    def query(self, Q, k: int, qProbes: int, return_stats: bool = False):
+    def query(self, Q, k: int, qProbes: int, return_stats: bool = False, rerank: int = 0):
         """Index::query(Q, k, qProbes) -- SPEC.md:321-329, batch over rows of Q.
 
+        rerank = SimHash budget B (0 = off, else B >= k).
         Returns ids [nq,k] uint32 (0xFFFFFFFF past min(k,U)), scores [nq,k] fp64
-        (-inf past min(k,U)) and optionally stats [nq,3] (probes, entries,
-        candidates).
+        (-inf past min(k,U)) and optionally stats [nq,4] (probes, entries,
+        candidates collected, exact inner products).
         """
         Q = _f32(Q)
         if Q.shape[1] != self.d:
@@ -355,22 +364,40 @@ class Index:
         ids = np.empty((nq, k), np.uint32)
         sc = np.empty((nq, k), np.float64)
         st = (QueryStats * max(nq, 1))() if return_stats else None
-        _check(lib().fpp_query(self._h, _ptr(Q), nq, k, qProbes, _ptr(ids), _ptr(sc),
-                               C.cast(st, C.c_void_p) if st is not None else None))
+        stp = C.cast(st, C.c_void_p) if st is not None else None
+        if rerank:
+            _check(lib().fpp_query_rerank(self._h, _ptr(Q), nq, k, qProbes, rerank, _ptr(ids),
+                                          _ptr(sc), stp))
+        else:
+            _check(lib().fpp_query(self._h, _ptr(Q), nq, k, qProbes, _ptr(ids), _ptr(sc), stp))
         if return_stats:
-            stats = np.array([(s.probes, s.entries, s.candidates) for s in st[:nq]],
-                             dtype=np.uint64).reshape(nq, 3)
+            stats = np.array([(s.probes, s.entries, s.candidates, s.exact) for s in st[:nq]],
+                             dtype=np.uint64).reshape(nq, 4)
             return ids, sc, stats
         return ids, sc
 
-    def query_device(self, Q, ids, scores, k: int, qProbes: int, stats=None, stream=None):
-        """Device-resident batch query on torch CUDA tensors (no host copies)."""
+    def query_device(self, Q, ids, scores, k: int, qProbes: int, stats=None, stream=None,
+                     rerank: int = 0):
+        """Device-resident batch query on torch CUDA tensors (no host copies);
+        stats (if given) is an int64 [nq, 4] tensor."""
         if Q.shape[1] != self.d:
             raise FppDimensionError("search: dimension mismatch")
-        _check(lib().fpp_query_device(self._h, C.c_void_p(Q.data_ptr()), Q.shape[0], k, qProbes,
-                                      C.c_void_p(ids.data_ptr()), C.c_void_p(scores.data_ptr()),
-                                      C.c_void_p(stats.data_ptr()) if stats is not None else None,
-                                      C.c_void_p(stream) if stream else None))
+        args = (C.c_void_p(ids.data_ptr()), C.c_void_p(scores.data_ptr()),
+                C.c_void_p(stats.data_ptr()) if stats is not None else None,
+                C.c_void_p(stream) if stream else None)
+        if rerank:
+            _check(lib().fpp_query_rerank_device(self._h, C.c_void_p(Q.data_ptr()), Q.shape[0],
+                                                 k, qProbes, rerank, *args))
+        else:
+            _check(lib().fpp_query_device(self._h, C.c_void_p(Q.data_ptr()), Q.shape[0], k,
+                                          qProbes, *args))
+
+    def signatures(self, X) -> np.ndarray:
+        """64-bit SimHash signatures of rows X (as stored for the index's points)."""
+        X = _f32(X)
+        out = np.empty(X.shape[0], np.uint64)
+        _check(lib().fpp_signatures(self._h, _ptr(X), X.shape[0], _ptr(out)))
+        return out
 
     # ------------------------------------------------------- introspection
     def info(self) -> dict:

@@ -275,6 +275,58 @@ k_project(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D,
   }
 }
 
+// SimHash signatures (SPEC.md "SimHash signatures"; :330-338): bit j < min(64, D)
+// is 1 iff p[j] >= 0 for the (t=0, f=0) projection (-0.0 counts as >= 0, as in
+// cross_polytope_hash).  One lane group per row; partial masks OR-reduced.
+template <int P>
+__global__ void __launch_bounds__(256)
+k_signatures(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D,
+             const uint32_t* __restrict__ sw, uint64_t* __restrict__ out) {
+  using S = FhtShape<P>;
+  constexpr bool TR = P >= 64;
+  constexpr int TS = TR ? TransposeShape<P>::STRIDE : 4;
+  __shared__ __align__(16) float tbuf[(256 / S::G) * TS];
+  const int lane = threadIdx.x & 31;
+  const int g = lane % S::G;
+  float* buf = tbuf + (threadIdx.x / S::G) * TS;
+  const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
+  const bool active = gid < n;
+  const uint64_t i = active ? gid : n - 1;
+  float v[S::EPT];
+  load_row<P>(X + i * d, d, g, v);
+  if constexpr (TR) spinner_project_T<P>(v, sw, g, buf);
+  else spinner_project<P>(v, sw, g);
+  const uint32_t m = D < 64 ? D : 64;
+  uint64_t sig = 0;
+#pragma unroll
+  for (int e = 0; e < S::EPT; ++e) {
+    const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * S::EPT + e;
+    if (j < m && v[e] >= 0.0f) sig |= 1ull << j;
+  }
+#pragma unroll
+  for (int k = 1; k < S::G; k <<= 1) sig |= shfl_xor_u64(sig, k);
+  if (active && g == 0) out[i] = sig;
+}
+
+void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint64_t* out, cudaStream_t s) {
+  if (n == 0) return;
+  const uint32_t P = ix.P;
+  const uint32_t G = P < 32 ? 1 : P / 32;
+  const unsigned blocks = (unsigned)((n * G + 255) / 256);
+  const uint32_t* sw = ix.signs;  // stack (t=0, f=0)
+#define FPP_SIG_CASE(PP)                                                            \
+  case PP:                                                                          \
+    k_signatures<PP><<<blocks, 256, 0, s>>>(Xd, n, ix.d, ix.prm.D, sw, out);        \
+    break;
+  switch (P) {
+    FPP_SIG_CASE(2) FPP_SIG_CASE(4) FPP_SIG_CASE(8) FPP_SIG_CASE(16) FPP_SIG_CASE(32)
+    FPP_SIG_CASE(64) FPP_SIG_CASE(128) FPP_SIG_CASE(256) FPP_SIG_CASE(512) FPP_SIG_CASE(1024)
+    default: fail(FPP_ERR_UNSUPPORTED, "signatures: padded dimension > 1024 not supported on GPU");
+  }
+#undef FPP_SIG_CASE
+  FPP_LAUNCH();
+}
+
 // ------------------------------------------------------------- per-table scan
 constexpr int SCAN_THREADS = 512;
 constexpr int SCAN_PER_THREAD = 8;

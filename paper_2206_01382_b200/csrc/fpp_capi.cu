@@ -86,6 +86,7 @@ Index::~Index() {
   if (stream) cudaStreamSynchronize(stream);
   dfree(X);
   dfree(signs);
+  dfree(sigs);
   dfree(offsets);
   dfree(table_base);
   dfree(ids);
@@ -107,6 +108,7 @@ void Index::QSlot::release() {
   vals.release(); codes.release(); ppos.release(); plen.release(); gbuf.release();
   ckey.release(); cpair.release(); dbgclk.release(); eq.release(); coff.release();
   uq.release(); cands.release(); bitmap.release(); counter.release();
+  qsig.release(); cands2.release(); uq2.release(); coff2.release();
   if (pinned) cudaFreeHost(pinned);
   if (ev_probe) cudaEventDestroy(ev_probe);
   if (ev_bdone) cudaEventDestroy(ev_bdone);
@@ -276,8 +278,11 @@ Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, con
     ix->signs = static_cast<uint32_t*>(dmalloc(words.size() * 4));
     FPP_CUDA(cudaMemcpyAsync(ix->signs, words.data(), words.size() * 4, cudaMemcpyHostToDevice,
                              ix->stream));
-    FPP_CUDA(cudaStreamSynchronize(ix->stream));
     ix->sign_words = words.size();
+    // SimHash signatures of every point (rerank screening; n x 8 B)
+    ix->sigs = static_cast<uint64_t*>(dmalloc(n * sizeof(uint64_t) + 8));
+    launch_signatures(*ix, ix->X, n, ix->sigs, ix->stream);
+    FPP_CUDA(cudaStreamSynchronize(ix->stream));
   } catch (...) {
     delete ix;
     throw;
@@ -404,40 +409,82 @@ int fpp_build_device(const float* X, uint64_t n, uint32_t d, const fpp_params* p
 
 void fpp_free(fpp_index* idx) { delete reinterpret_cast<Index*>(idx); }
 
+static void query_host(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k,
+                       uint32_t qprobes, uint32_t rerank, uint32_t* ids, double* scores,
+                       fpp_query_stats* stats) {
+  const Index& ix = IX(idx);
+  validate_query(ix, nq, k, qprobes, Q, ids, scores);
+  if (rerank && rerank < k) fail(FPP_ERR_OUT_OF_RANGE, "search: rerank budget B must be 0 or >= k");
+  if (!nq) return;
+  DeviceGuard dg(ix.device);
+  std::lock_guard<std::mutex> lk(ix.mu);
+  cudaStream_t s = ix.stream;
+  ix.q_in.ensure(nq * ix.d);
+  ix.q_ids.ensure(nq * k);
+  ix.q_scores.ensure(nq * k);
+  if (stats) ix.q_stats.ensure(nq);
+  FPP_CUDA(cudaMemcpyAsync(ix.q_in.p, Q, nq * ix.d * 4, cudaMemcpyHostToDevice, s));
+  run_query(ix, ix.q_in.p, nq, k, qprobes, ix.q_ids.p, ix.q_scores.p,
+            stats ? ix.q_stats.p : nullptr, s, rerank);
+  FPP_CUDA(cudaMemcpyAsync(ids, ix.q_ids.p, nq * k * 4, cudaMemcpyDeviceToHost, s));
+  FPP_CUDA(cudaMemcpyAsync(scores, ix.q_scores.p, nq * k * 8, cudaMemcpyDeviceToHost, s));
+  if (stats)
+    FPP_CUDA(cudaMemcpyAsync(stats, ix.q_stats.p, nq * sizeof(fpp_query_stats),
+                             cudaMemcpyDeviceToHost, s));
+  FPP_CUDA(cudaStreamSynchronize(s));
+  collect_timings(ix);
+}
+
+static void query_dev(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k,
+                      uint32_t qprobes, uint32_t rerank, uint32_t* ids, double* scores,
+                      fpp_query_stats* stats, void* stream) {
+  const Index& ix = IX(idx);
+  validate_query(ix, nq, k, qprobes, Q, ids, scores);
+  if (rerank && rerank < k) fail(FPP_ERR_OUT_OF_RANGE, "search: rerank budget B must be 0 or >= k");
+  if (!nq) return;
+  DeviceGuard dg(ix.device);
+  std::lock_guard<std::mutex> lk(ix.mu);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ix.stream;
+  run_query(ix, Q, nq, k, qprobes, ids, scores, stats, s, rerank);
+}
+
 int fpp_query(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uint32_t qprobes,
               uint32_t* ids, double* scores, fpp_query_stats* stats) {
-  return guarded([&] {
-    const Index& ix = IX(idx);
-    validate_query(ix, nq, k, qprobes, Q, ids, scores);
-    if (!nq) return;
-    DeviceGuard dg(ix.device);
-    std::lock_guard<std::mutex> lk(ix.mu);
-    cudaStream_t s = ix.stream;
-    ix.q_in.ensure(nq * ix.d);
-    ix.q_ids.ensure(nq * k);
-    ix.q_scores.ensure(nq * k);
-    if (stats) ix.q_stats.ensure(nq);
-    FPP_CUDA(cudaMemcpyAsync(ix.q_in.p, Q, nq * ix.d * 4, cudaMemcpyHostToDevice, s));
-    run_query(ix, ix.q_in.p, nq, k, qprobes, ix.q_ids.p, ix.q_scores.p, stats ? ix.q_stats.p : nullptr, s);
-    FPP_CUDA(cudaMemcpyAsync(ids, ix.q_ids.p, nq * k * 4, cudaMemcpyDeviceToHost, s));
-    FPP_CUDA(cudaMemcpyAsync(scores, ix.q_scores.p, nq * k * 8, cudaMemcpyDeviceToHost, s));
-    if (stats)
-      FPP_CUDA(cudaMemcpyAsync(stats, ix.q_stats.p, nq * sizeof(fpp_query_stats), cudaMemcpyDeviceToHost, s));
-    FPP_CUDA(cudaStreamSynchronize(s));
-    collect_timings(ix);
-  });
+  return guarded([&] { query_host(idx, Q, nq, k, qprobes, 0, ids, scores, stats); });
 }
 
 int fpp_query_device(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uint32_t qprobes,
                      uint32_t* ids, double* scores, fpp_query_stats* stats, void* stream) {
+  return guarded([&] { query_dev(idx, Q, nq, k, qprobes, 0, ids, scores, stats, stream); });
+}
+
+int fpp_query_rerank(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k,
+                     uint32_t qprobes, uint32_t rerank, uint32_t* ids, double* scores,
+                     fpp_query_stats* stats) {
+  return guarded([&] { query_host(idx, Q, nq, k, qprobes, rerank, ids, scores, stats); });
+}
+
+int fpp_query_rerank_device(const fpp_index* idx, const float* Q_dev, uint64_t nq, uint32_t k,
+                            uint32_t qprobes, uint32_t rerank, uint32_t* ids_dev,
+                            double* scores_dev, fpp_query_stats* stats_dev, void* stream) {
+  return guarded([&] {
+    query_dev(idx, Q_dev, nq, k, qprobes, rerank, ids_dev, scores_dev, stats_dev, stream);
+  });
+}
+
+int fpp_signatures(const fpp_index* idx, const float* X, uint64_t n, uint64_t* out) {
   return guarded([&] {
     const Index& ix = IX(idx);
-    validate_query(ix, nq, k, qprobes, Q, ids, scores);
-    if (!nq) return;
+    if (n && (!X || !out)) fail(FPP_ERR_INVALID_ARGUMENT, "signatures: NULL buffer");
+    if (!n) return;
     DeviceGuard dg(ix.device);
     std::lock_guard<std::mutex> lk(ix.mu);
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ix.stream;
-    run_query(ix, Q, nq, k, qprobes, ids, scores, stats, s);
+    DBuf<float> xd(n * ix.d);
+    DBuf<uint64_t> od(n);
+    FPP_CUDA(cudaMemcpyAsync(xd.p, X, n * ix.d * 4, cudaMemcpyHostToDevice, ix.stream));
+    launch_signatures(ix, xd.p, n, od.p, ix.stream);
+    FPP_CUDA(cudaMemcpyAsync(out, od.p, n * 8, cudaMemcpyDeviceToHost, ix.stream));
+    FPP_CUDA(cudaStreamSynchronize(ix.stream));
   });
 }
 

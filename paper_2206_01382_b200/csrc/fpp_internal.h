@@ -85,6 +85,7 @@ struct Index {
   uint64_t kept_total = 0;
   uint32_t max_bucket = 0;
   uint64_t sign_words = 0;
+  uint64_t* sigs = nullptr;  // [n] SimHash signatures (rerank screening)
   uint64_t device_bytes = 0;
   ShardState* shard = nullptr;  // global-filter sharded build in progress
 
@@ -105,6 +106,10 @@ struct Index {
     DBuf<uint32_t> cands;
     DBuf<uint32_t> bitmap;
     DBuf<uint32_t> counter;
+    DBuf<uint64_t> qsig;    // rerank: query signatures
+    DBuf<uint32_t> cands2;  // rerank: screened candidates [nqc][B]
+    DBuf<uint32_t> uq2;
+    DBuf<uint64_t> coff2;
     uint64_t* pinned = nullptr;     // etot readback
     cudaEvent_t ev_probe = nullptr; // stage A (hash + probe select) done
     cudaEvent_t ev_bdone = nullptr; // stage B (collect + score) done
@@ -140,6 +145,7 @@ void build_tables(Index& ix);
 Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, const fpp_params* pp);
 uint64_t content_hash(const float* X, uint64_t n, uint32_t d);
 void save_index(const Index& ix, const char* path, const float* X_host);
+void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint64_t* out, cudaStream_t s);
 void run_brute_force(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t* ids_d,
                      double* scores_d, cudaStream_t s);
 Index* load_index(const char* path, const float* X, bool on_device, uint64_t n, uint32_t d,
@@ -160,7 +166,8 @@ const uint32_t* shard_hist_ptr(const Index& ix);
 
 // query (fpp_query.cu)
 void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t qprobes,
-               uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s);
+               uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s,
+               uint32_t rerank = 0);
 void launch_query_lists(const Index& ix, const float* Qd, uint64_t nq, uint32_t s_cap,
                         float* vals, uint32_t* codes, cudaStream_t s, uint64_t lstride = 0);
 // probes (t*NB+b) and candidates of query 0 of Qd (debug/parity)

@@ -1168,6 +1168,92 @@ k_collect_cluster(CollectArgs a, uint32_t slice_words) {
   }
 }
 
+// ------------------------------------------------------------ SimHash screen
+// CTA per query (SPEC.md:330-338 simhash_screen): keep the B candidates with the
+// most agreeing signature bits, ties by lower id.  dis = popc(sig ^ q_sig) (fewer
+// = better) is histogrammed; the threshold bin's ties are cut by a radix select
+// on the (unique) ids; the survivors are compacted into out[q][0..B).  With
+// U <= B the list is copied unchanged (identity case).
+constexpr int SCR_THREADS = 256;
+__global__ void __launch_bounds__(SCR_THREADS)
+k_screen(const uint32_t* __restrict__ cands, const uint64_t* __restrict__ coff,
+         const uint32_t* __restrict__ uq, const uint64_t* __restrict__ sigs,
+         const uint64_t* __restrict__ qsig, uint32_t B, uint32_t* __restrict__ out,
+         uint32_t* __restrict__ uq2) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t sh_dstar, sh_rem, sh_ties, sh_sel, n_out;
+  const uint32_t q = blockIdx.x;
+  const uint32_t U = uq[q];
+  const uint32_t* c = cands + coff[q];
+  uint32_t* o = out + (uint64_t)q * B;
+  if (U <= B) {
+    for (uint32_t i = threadIdx.x; i < U; i += blockDim.x) o[i] = c[i];
+    if (threadIdx.x == 0) uq2[q] = U;
+    return;
+  }
+  const uint64_t sq = qsig[q];
+  auto dis_of = [&](uint32_t id) { return (uint32_t)__popcll(__ldg(sigs + id) ^ sq); };
+  for (int i = threadIdx.x; i < 65; i += blockDim.x) hist[i] = 0;
+  if (threadIdx.x == 0) n_out = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < U; i += blockDim.x) smem_inc(&hist[dis_of(c[i])]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t cum = 0, dd = 0;
+    for (; dd < 65; ++dd) {
+      if (cum + hist[dd] >= B) break;
+      cum += hist[dd];
+    }
+    sh_dstar = dd;
+    sh_rem = B - cum;  // ties to take at dstar (1-based rank among them)
+    sh_ties = hist[dd];
+  }
+  __syncthreads();
+  const uint32_t dstar = sh_dstar;
+  uint32_t idstar = 0xffffffffu;
+  if (sh_ties > sh_rem) {  // the sh_rem smallest ids among dis == dstar
+    uint32_t prefix = 0, mask = 0, r = sh_rem;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < U; i += blockDim.x) {
+        const uint32_t id = c[i];
+        if ((id & mask) == prefix && dis_of(id) == dstar) smem_inc(&hist[(id >> shift) & 255u]);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t cum = 0, dg = 0;
+        for (; dg < 256; ++dg) {
+          if (cum + hist[dg] >= r) break;
+          cum += hist[dg];
+        }
+        sh_sel = dg;
+        sh_rem = r - cum;
+      }
+      __syncthreads();
+      prefix |= sh_sel << shift;
+      mask |= 255u << shift;
+      r = sh_rem;
+      __syncthreads();
+    }
+    idstar = prefix;
+  }
+  const int lane = threadIdx.x & 31;
+  const uint32_t Ur = (U + 31) & ~31u;
+  for (uint32_t i = threadIdx.x; i < Ur; i += blockDim.x) {
+    const uint32_t id = i < U ? c[i] : 0;
+    uint32_t dd = 0;
+    if (i < U) dd = dis_of(id);
+    const bool take = i < U && (dd < dstar || (dd == dstar && id <= idstar));
+    const uint32_t bal = __ballot_sync(FULL, take);
+    uint32_t base = 0;
+    if (lane == 0 && bal) base = smem_fetch_add(&n_out, __popc(bal));
+    base = __shfl_sync(FULL, base, 0);
+    if (take) o[base + __popc(bal & ((1u << lane) - 1))] = id;
+  }
+  if (threadIdx.x == 0) uq2[q] = B;
+}
+
 // ------------------------------------------------------------------- score
 #ifndef FPP_SC_WARPS
 #define FPP_SC_WARPS 4
@@ -1197,6 +1283,8 @@ struct ScoreArgs {
   uint32_t* out_ids;
   double* out_scores;
   fpp_query_stats* stats;
+  const uint32_t* uq_all;  // collected candidates per query (stats); nullptr: = uq
+  uint32_t cstride;        // != 0: candidates of query q start at q * cstride (screened lists)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1259,7 +1347,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, 2) k_score(ScoreArgs a) {
   for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) qd[j] = (double)a.Q[(uint64_t)q * d + j];
   __syncthreads();
   const uint32_t U = a.uq[q];
-  const uint32_t* cand = a.cands + a.coff[q];
+  const uint32_t* cand = a.cands + (a.cstride ? (uint64_t)q * a.cstride : a.coff[q]);
   const uint32_t k = a.k;
   double bs = -INFINITY;
   uint32_t bi = 0xffffffffu;
@@ -1371,7 +1459,8 @@ __global__ void __launch_bounds__(SC_WARPS * 32, 2) k_score(ScoreArgs a) {
     if (lane == 0 && a.stats) {
       a.stats[q].probes = a.peff;
       a.stats[q].entries = a.eq[q];
-      a.stats[q].candidates = U;
+      a.stats[q].candidates = a.uq_all ? a.uq_all[q] : U;
+      a.stats[q].exact = U;
     }
   }
 }
@@ -1531,7 +1620,7 @@ static void stage_a(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
 // bucket walk + dedup, then row gather + fp64 dot + top-k.
 static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t nqc, uint32_t k,
                     uint32_t qprobes, uint32_t* ids_d, double* scores_d,
-                    fpp_query_stats* stats_d, cudaStream_t st) {
+                    fpp_query_stats* stats_d, cudaStream_t st, uint32_t rerank = 0) {
   const uint64_t peff = query_probes(ix, qprobes);
   const uint64_t etot = sl.pinned[0];
   sl.cands.ensure(etot + 1);
@@ -1587,7 +1676,21 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
 
   ix.timer.begin(PH_SCORE, st, &e0);
   ScoreArgs sa{ix.X, ix.d, Qd, sl.coff.p, sl.cands.p, sl.uq.p, sl.eq.p, peff, k,
-               ix.prm.id_offset, ids_d, scores_d, stats_d};
+               ix.prm.id_offset, ids_d, scores_d, stats_d, nullptr, 0};
+  if (rerank) {  // SimHash screen: at most B candidates per query reach the exact scores
+    sl.qsig.ensure(nqc);
+    sl.cands2.ensure((size_t)nqc * rerank);
+    sl.uq2.ensure(nqc);
+    launch_signatures(ix, Qd, nqc, sl.qsig.p, st);
+    k_screen<<<nqc, SCR_THREADS, 0, st>>>(sl.cands.p, sl.coff.p, sl.uq.p, ix.sigs, sl.qsig.p, rerank,
+                                          sl.cands2.p, sl.uq2.p);
+    FPP_LAUNCH();
+    ix.acc.launches += 2;
+    sa.cands = sl.cands2.p;
+    sa.uq = sl.uq2.p;
+    sa.uq_all = sl.uq.p;
+    sa.cstride = rerank;
+  }
   auto launch_score = [&](auto kern, int sl, int stg) {
     const size_t sm = score_smem(ix.d, sl, stg);
     FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -1625,7 +1728,8 @@ static uint32_t chunk_size(const Index& ix, uint32_t qprobes, uint64_t nq) {
 // SM slots to the bandwidth-bound kernel first and fills the rest with stage A
 // of the next chunk.  Slots alternate; events order slot reuse.
 void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t qprobes,
-               uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s) {
+               uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s,
+               uint32_t rerank) {
   const uint32_t cs = chunk_size(ix, qprobes, nq);
   const uint64_t nch = (nq + cs - 1) / cs;
   static const bool serial = getenv("FPP_SERIAL") != nullptr;
@@ -1636,7 +1740,7 @@ void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32
       stage_a(ix, ix.slot[0], Qd + q0 * ix.d, n, qprobes, s, nullptr);
       FPP_CUDA(cudaEventSynchronize(ix.slot[0].ev_probe));
       stage_b(ix, ix.slot[0], Qd + q0 * ix.d, n, k, qprobes, ids_d + q0 * k, scores_d + q0 * k,
-              stats_d ? stats_d + q0 : nullptr, s);
+              stats_d ? stats_d + q0 : nullptr, s, rerank);
     }
     return;
   }
@@ -1671,7 +1775,7 @@ void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32
     const uint64_t q0 = c * cs;
     const uint32_t n = (uint32_t)std::min<uint64_t>(cs, nq - q0);
     stage_b(ix, sl, Qd + q0 * ix.d, n, k, qprobes, ids_d + q0 * k, scores_d + q0 * k,
-            stats_d ? stats_d + q0 : nullptr, ix.sB);
+            stats_d ? stats_d + q0 : nullptr, ix.sB, rerank);
     FPP_CUDA(cudaEventRecord(sl.ev_bdone, ix.sB));
     if (c + 2 < nch) issue_a(c + 2);
   }

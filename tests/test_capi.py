@@ -39,7 +39,10 @@ def test_header_symbols_exported(fpp):
 
 
 def test_abi_version(fpp):
-    assert fpp.lib().fpp_abi_version() == 1
+    import re
+    hdr = open(os.path.join(ROOT, "include", "falconnpp.h")).read()
+    want = int(re.search(r"#define FPP_ABI_VERSION (\d+)", hdr).group(1))
+    assert fpp.lib().fpp_abi_version() == want == fpp.ABI_VERSION
 
 
 def P(fpp, **kw):

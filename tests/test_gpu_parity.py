@@ -326,3 +326,60 @@ def test_brute_force_exact(fpp, orc, n, d, k):
     assert np.array_equal(gi, bi)
     assert np.array_equal(gs, bs)
     assert list(gi[0][:6]) == [3] + list(range(n // 2, n // 2 + 5))
+
+
+@pytest.mark.parametrize("d,D", [(17, 32), (100, 128), (300, 512), (200, 64), (32, 16)])
+def test_simhash_signatures_bitexact(fpp, orc, d, D):
+    # SPEC.md "SimHash signatures": signs of the first 64 coordinates of the (t=0, f=0)
+    # projection; bits >= D stay 0
+    X = data(fpp, 700, d, 5, 0.3)
+    ix = fpp.Index.build(X, L=2, K=2, D=D, iProbes=1, alpha=0.5)
+    ox = orc.Index(X, L=2, K=2, D=D, iprobes=1, alpha=0.5)
+    assert np.array_equal(ix.signatures(X), ox.simhash(X))
+    if D < 64:
+        assert int(np.bitwise_or.reduce(ix.signatures(X))) >> D == 0
+
+
+@pytest.mark.parametrize("case", [("c2_like", 12000, 300, 100, 0.3, 8, 2, 512, 3, 0.05, 20),
+                                  ("iid_d128", 20000, 128, 0, 0.0, 10, 2, 128, 3, 0.1, 20),
+                                  ("K1", 5000, 64, 0, 0.0, 6, 1, 64, 2, 0.5, 10)],
+                         ids=lambda c: c[0])
+def test_rerank_parity(fpp, orc, case):
+    # top-B by signature agreement (ties by lower id), then exact top-k
+    _, n, d, C_, sg, L, K, D, ip, al, ka = case
+    X = data(fpp, n, d, C_, sg)
+    Q = data(fpp, 48, d, C_, sg, stream=1)
+    ix = fpp.Index.build(X, L=L, K=K, D=D, iProbes=ip, alpha=al, kappa=ka)
+    ox = orc.Index(X, L=L, K=K, D=D, iprobes=ip, alpha=al, kappa=ka)
+    k = 20
+    cap = L * (4 * D * D if K == 2 else 2 * D)
+    for qp, B in ((800, 20), (800, 100), (2000, 500), (2000, 10 ** 6)):
+        qp = min(qp, cap)
+        gi, gs, gst = ix.query(Q, k, qp, return_stats=True, rerank=B)
+        oi, os_, ost = ox.query(Q, k, qp, rerank=B)
+        assert np.array_equal(gst, ost), (qp, B)
+        assert np.array_equal(gi, oi), (qp, B)
+        assert np.array_equal(gs, os_), (qp, B)
+        assert (gst[:, 3] <= np.minimum(gst[:, 2], B)).all() and (gst[:, 3] > 0).all()
+    # B >= U is the identity screen: equals the unscreened search
+    qp = min(800, cap)
+    gi0, gs0 = ix.query(Q, k, qp)
+    gi1, gs1 = ix.query(Q, k, qp, rerank=10 ** 6)
+    assert np.array_equal(gi0, gi1) and np.array_equal(gs0, gs1)
+    with pytest.raises(fpp.FppOutOfRange):
+        ix.query(Q, k, qp, rerank=k - 1)
+
+
+def test_rerank_recall_bound(fpp, orc):
+    # SPEC.md query invariants: recall with B > 0 <= recall with B = 0 at equal qProbes
+    X = data(fpp, 20000, 128, 50, 0.3, seed=8)
+    Q = data(fpp, 200, 128, 50, 0.3, seed=8, stream=1)
+    ix = fpp.Index.build(X, L=10, K=2, D=128, iProbes=3, alpha=0.1)
+    gt, _ = ix.brute_force(Q, 20)
+
+    def recall(ids):
+        return np.mean([len(set(a) & set(b)) / 20 for a, b in zip(ids, gt)])
+
+    full = recall(ix.query(Q, 20, 1000)[0])
+    for B in (20, 100, 400):
+        assert recall(ix.query(Q, 20, 1000, rerank=B)[0]) <= full + 1e-12
