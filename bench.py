@@ -36,7 +36,8 @@ CONFIGS = {
     "c1": dict(n=100_000, d=128, clusters=0, sigma=0.0, L=50, K=2, D=128, iprobes=3, alpha=0.1,
                nq=1000, qprobes=1000, sweep=[50, 200, 1000]),
     "c2": dict(n=1_200_000, d=300, clusters=1000, sigma=0.3, L=100, K=2, D=512, iprobes=3,
-               alpha=0.05, nq=10_000, qprobes=10_000, sweep=[1000, 2000, 5000, 10_000, 20_000]),
+               alpha=0.05, nq=10_000, qprobes=10_000, sweep=[1000, 2000, 5000, 10_000, 20_000],
+               rerank=[200, 1000, 4000]),
     "c3": dict(n=1_000_000, d=960, clusters=500, sigma=0.2, L=100, K=2, D=1024, iprobes=3,
                alpha=0.02, nq=1000, qprobes=10_000, sweep=[10_000]),
     "c4": dict(n=10_000_000, d=128, clusters=10_000, sigma=0.25, L=50, K=2, D=128, iprobes=3,
@@ -533,6 +534,23 @@ def main():
                 got = ids_d[:len(gt)].cpu().numpy().view(np.uint32)
                 rec = np.mean([len(set(got[i]) & set(gt[i])) / K_TOP for i in range(len(gt))])
                 row["recall_at_20"] = float(rec)
+            sweep.append(row)
+        # SimHash rerank at the headline qProbes: exact distances
+        # per query drop from U_q to B
+        for B in cfg.get("rerank", []):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ix.query_device(Qd, ids_d, sc_d, K_TOP, qprobes, stream=stream, rerank=B)
+            torch.cuda.synchronize()
+            e0.record()
+            ix.query_device(Qd, ids_d, sc_d, K_TOP, qprobes, stream=stream, rerank=B)
+            e1.record()
+            torch.cuda.synchronize()
+            row = {"qprobes": qprobes, "rerank_B": B,
+                   "queries_per_s": nq / (e0.elapsed_time(e1) / 1e3)}
+            if gt is not None:
+                got = ids_d[:len(gt)].cpu().numpy().view(np.uint32)
+                row["recall_at_20"] = float(np.mean([len(set(got[i]) & set(gt[i])) / K_TOP
+                                                     for i in range(len(gt))]))
             sweep.append(row)
 
     cpu = None
