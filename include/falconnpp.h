@@ -55,7 +55,13 @@ typedef struct fpp_params {
   int32_t device;    /* CUDA device ordinal (-1 = current) */
   uint32_t id_offset;/* global id of local row 0 (sharded builds) */
   uint64_t scratch_bytes; /* build scratch budget per pass (0 = auto) */
+  uint32_t centering; /* 1: index the centered dataset (dataset.cpp center();
+                         queries are not centered, scores are x'.q -- SPEC.md:358) */
+  uint32_t mode;      /* FPP_MODE_FALCONNPP or FPP_MODE_FALCONN_BASELINE */
 } fpp_params;
+
+#define FPP_MODE_FALCONNPP 0
+#define FPP_MODE_FALCONN_BASELINE 1 /* alpha = 1, iProbes = 1; probes by ascending gap score */
 
 /* SearchResult.stats */
 typedef struct fpp_query_stats {
@@ -138,6 +144,8 @@ typedef struct fpp_index_info {
   uint64_t device_bytes;  /* resident index bytes */
   uint32_t max_bucket;    /* largest kept bucket */
   uint32_t id_offset;
+  uint32_t centering;     /* indexed rows are centered (fpp_index_center) */
+  uint32_t mode;          /* FPP_MODE_* */
 } fpp_index_info;
 
 int fpp_index_info_get(const fpp_index* idx, fpp_index_info* info);
@@ -208,6 +216,13 @@ int fpp_load(const char* path, const float* X, uint64_t n, uint32_t d, int devic
 int fpp_load_device(const char* path, const float* X_dev, uint64_t n, uint32_t d, int device,
                     fpp_index** out);
 uint64_t fpp_content_hash(const float* X, uint64_t n, uint32_t d);
+
+/* center(Dataset) in place (dataset.cpp:40-57): mean by a sequential double sum
+ * over rows per coordinate, center = float(mean / n), rows -= center in fp32 (not
+ * renormalized).  center_out (d floats) may be NULL. */
+int fpp_center(float* X, uint64_t n, uint32_t d, float* center_out);
+/* the index's center vector (d floats; all zero unless built with centering) */
+int fpp_index_center(const fpp_index* idx, float* center_out);
 
 /* normalize(Dataset) in place (dataset.cpp:24-38); FPP_ERR_ZERO_NORM names the row */
 int fpp_normalize(float* X, uint64_t n, uint32_t d);

@@ -136,6 +136,17 @@ void orc_project_rows(uint32_t d, uint32_t D, uint64_t seed, const float* X, uin
 /* --------------------------------------------------------------- dataset */
 
 /* ref: proj/src/dataset.cpp:24-38 */
+/* ref: dataset.cpp:40-57 */
+void orc_center(float* X, uint64_t n, uint32_t d, float* center_out) {
+  double* mean = (double*)calloc(d, sizeof(double));
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint32_t j = 0; j < d; ++j) mean[j] += X[i * d + j];
+  for (uint32_t j = 0; j < d; ++j) center_out[j] = (float)(mean[j] / (double)n);
+  for (uint64_t i = 0; i < n; ++i)
+    for (uint32_t j = 0; j < d; ++j) X[i * d + j] -= center_out[j];
+  free(mean);
+}
+
 int64_t orc_normalize(float* X, uint64_t n, uint32_t d) {
   for (uint64_t i = 0; i < n; ++i) {
     float* row = X + i * d;
@@ -271,7 +282,16 @@ typedef struct {
   const float* va; const float* vb;
   const uint32_t* ca; const uint32_t* cb;
   uint32_t na, nb, oa, ob, t;
+  float ma, mb;  /* natural list maxima max|q.r| of the two functions (baseline gap) */
+  int mode;
 } grid;
+
+/* pair score, larger first: falconnpp fl(v1+v2); falconn_baseline
+   -(fl(m1-v1) + fl(m2-v2)), i.e. ascending gap score */
+static float pscore(const grid* g, uint32_t a, uint32_t b) {
+  if (g->mode == 1) return -((g->ma - g->va[a]) + (g->mb - g->vb[b]));
+  return g->va[a] + g->vb[b];
+}
 
 /*
  * Class-ordered enumeration of (t, r1, r2) pairs of L tables' ranked lists
@@ -285,7 +305,7 @@ typedef struct {
  */
 static uint64_t enum_pairs(const float* vals, const uint32_t* codes, uint32_t L, uint32_t K,
                            uint32_t D, uint32_t s, uint64_t NB, uint64_t limit, int skip_forced,
-                           uint64_t* out_b, float* out_s) {
+                           uint64_t* out_b, float* out_s, int mode) {
   const uint32_t n = s < D ? s : D, o = s > D ? s - D : 0;
   grid* G = (grid*)malloc((size_t)L * 2 * sizeof(grid));
   pairkey* heap = (pairkey*)malloc((size_t)(2 * limit + 4 * L + 4) * sizeof(pairkey));
@@ -317,6 +337,9 @@ static uint64_t enum_pairs(const float* vals, const uint32_t* codes, uint32_t L,
         g.va = v1 + pa[A][0]; g.ca = c1 + pa[A][0]; g.na = pa[A][1]; g.oa = pa[A][2];
         g.vb = v2 + (K == 2 ? pb[B][0] : 0); g.cb = c2 + (K == 2 ? pb[B][0] : 0);
         g.nb = pb[B][1]; g.ob = K == 2 ? pb[B][2] : 0; g.t = t;
+        g.ma = v1[0];
+        g.mb = v2[0];
+        g.mode = mode;
         if (g.na == 0 || g.nb == 0) continue;
         G[ng++] = g;
       }
@@ -326,15 +349,15 @@ static uint64_t enum_pairs(const float* vals, const uint32_t* codes, uint32_t L,
       const grid* g = &G[gi];
       if (cls == 0 && skip_forced) {
         if (g->nb > 1) {
-          pairkey k = {g->va[0] + g->vb[1], g->oa, g->ob + 1, g->t, gi, 0, 1};
+          pairkey k = {pscore(g, 0, 1), g->oa, g->ob + 1, g->t, gi, 0, 1};
           heap_push(heap, &hn, k);
         }
         if (g->na > 1) {
-          pairkey k = {g->va[1] + g->vb[0], g->oa + 1, g->ob, g->t, gi, 1, 0};
+          pairkey k = {pscore(g, 1, 0), g->oa + 1, g->ob, g->t, gi, 1, 0};
           heap_push(heap, &hn, k);
         }
       } else {
-        pairkey k = {g->va[0] + g->vb[0], g->oa, g->ob, g->t, gi, 0, 0};
+        pairkey k = {pscore(g, 0, 0), g->oa, g->ob, g->t, gi, 0, 0};
         heap_push(heap, &hn, k);
       }
     }
@@ -346,11 +369,11 @@ static uint64_t enum_pairs(const float* vals, const uint32_t* codes, uint32_t L,
       if (out_s) out_s[emitted] = k.s;
       ++emitted;
       if (k.b + 1 < g->nb) {
-        pairkey c = {g->va[k.a] + g->vb[k.b + 1], g->oa + k.a, g->ob + k.b + 1, g->t, k.g, k.a, k.b + 1};
+        pairkey c = {pscore(g, k.a, k.b + 1), g->oa + k.a, g->ob + k.b + 1, g->t, k.g, k.a, k.b + 1};
         heap_push(heap, &hn, c);
       }
       if (k.b == 0 && k.a + 1 < g->na) {
-        pairkey c = {g->va[k.a + 1] + g->vb[0], g->oa + k.a + 1, g->ob, g->t, k.g, k.a + 1, 0};
+        pairkey c = {pscore(g, k.a + 1, 0), g->oa + k.a + 1, g->ob, g->t, k.g, k.a + 1, 0};
         heap_push(heap, &hn, c);
       }
     }
@@ -374,7 +397,7 @@ void orc_index_probes(const float* proj, uint32_t K, uint32_t D, uint32_t iprobe
   uint64_t* ob = (uint64_t*)malloc((size_t)iprobes * sizeof(uint64_t));
   for (uint32_t f = 0; f < K; ++f) orc_rank(proj + (uint64_t)f * D, D, r, V + f * r, Cc + f * r);
   const uint64_t NB = K == 2 ? 4ull * D * D : 2ull * D;
-  enum_pairs(V, Cc, 1, K, D, r, NB, iprobes, 0, ob, scores);
+  enum_pairs(V, Cc, 1, K, D, r, NB, iprobes, 0, ob, scores, 0);
   for (uint32_t k = 0; k < iprobes; ++k) buckets[k] = (uint32_t)ob[k];
   free(V);
   free(Cc);
@@ -432,9 +455,14 @@ orc_index* orc_build(const float* X, uint64_t n, uint32_t d, const orc_params* p
   if (!X || n == 0 || d == 0 || !prm) return NULL;
   if (prm->K < 1 || prm->K > 2 || prm->L == 0 || prm->D == 0 || (prm->D & (prm->D - 1)))
     return NULL;
-  if (!(prm->alpha > 0.0f && prm->alpha <= 1.0f) || prm->iprobes == 0) return NULL;
+  if (!(prm->alpha > 0.0f && prm->alpha <= 1.0f) || prm->iprobes == 0 || prm->mode > 1) return NULL;
   orc_index* idx = (orc_index*)calloc(1, sizeof(orc_index));
   idx->p = *prm;
+  if (prm->mode == 1) {  /* SPEC.md:235 falconn_baseline forces alpha = 1, iProbes = 1 */
+    idx->p.alpha = 1.0f;
+    idx->p.iprobes = 1;
+  }
+  prm = &idx->p;
   idx->n = n;
   idx->d = d;
   idx->P = orc_pad_dimension(d);
@@ -639,7 +667,8 @@ static uint64_t probe_set(const orc_index* idx, const float* vals, const uint32_
     const uint32_t* c1 = codes + ((uint64_t)t * K) * s;
     probes[t] = t * NB + (K == 2 ? (uint64_t)c1[0] * 2 * D + c1[s] : c1[0]);
   }
-  return L + enum_pairs(vals, codes, L, K, D, s, NB, peff - L, 1, probes + L, NULL);
+  return L + enum_pairs(vals, codes, L, K, D, s, NB, peff - L, 1, probes + L, NULL,
+                        (int)idx->p.mode);
 }
 
 uint64_t orc_probe_set_lists(const float* vals, const uint32_t* codes, uint32_t L, uint32_t K,

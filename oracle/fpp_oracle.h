@@ -32,6 +32,8 @@ typedef struct {
   uint32_t kappa;    /* limit-scaling floor (default 20) */
   float alpha;       /* scaling factor (0,1] */
   uint64_t seed;     /* master seed */
+  uint32_t mode;     /* 0 falconnpp, 1 falconn_baseline (alpha = 1,
+                        iProbes = 1 forced; probes by ascending gap score) */
 } orc_params;
 
 typedef struct {
@@ -66,6 +68,9 @@ void orc_index_probes_rows(const orc_index* idx, const float* X, uint64_t n, uin
 
 /* dataset.cpp */
 int64_t orc_normalize(float* X, uint64_t n, uint32_t d);   /* -1 ok, else zero row idx */
+/* dataset.cpp:40-57 center(): double mean per coordinate (rows in order), float center,
+   rows -= center in fp32 */
+void orc_center(float* X, uint64_t n, uint32_t d, float* center_out);
 double orc_inner_product(const float* a, const float* b, uint32_t d);
 
 /* hashing */

@@ -25,7 +25,7 @@ f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 class Params(C.Structure):
     _fields_ = [("L", C.c_uint32), ("K", C.c_uint32), ("D", C.c_uint32),
                 ("iprobes", C.c_uint32), ("kappa", C.c_uint32),
-                ("alpha", C.c_float), ("seed", C.c_uint64)]
+                ("alpha", C.c_float), ("seed", C.c_uint64), ("mode", C.c_uint32)]
 
 
 class Stats(C.Structure):
@@ -77,6 +77,8 @@ def lib():
                                           C.c_uint32, C.c_uint64, u64p]
         L.orc_normalize.restype = C.c_int64
         L.orc_normalize.argtypes = [f32p, C.c_uint64, C.c_uint32]
+        L.orc_center.restype = None
+        L.orc_center.argtypes = [f32p, C.c_uint64, C.c_uint32, f32p]
         L.orc_inner_product.restype = C.c_double
         L.orc_inner_product.argtypes = [f32p, f32p, C.c_uint32]
         L.orc_cp_hash.restype = C.c_uint32
@@ -175,6 +177,14 @@ def synth(n: int, d: int, clusters: int = 0, sigma: float = 0.0, seed: int = 1,
     return X
 
 
+def center(X: np.ndarray):
+    """dataset.cpp:40-57 restated: returns (centered copy, center)."""
+    X = np.array(X, dtype=np.float32, order="C", copy=True)
+    c = np.empty(X.shape[1], np.float32)
+    lib().orc_center(X.reshape(-1), X.shape[0], X.shape[1], c)
+    return X, c
+
+
 def normalize(X: np.ndarray) -> np.ndarray:
     X = np.array(X, dtype=np.float32, order="C", copy=True)
     r = lib().orc_normalize(X.reshape(-1), X.shape[0], X.shape[1])
@@ -188,10 +198,10 @@ class Index:
 
     def __init__(self, X: np.ndarray, L: int, K: int, D: int, iprobes: int, alpha: float,
                  kappa: int = 20, seed: int = 1, threads: int = 0,
-                 t_begin: int = 0, t_end: int = 0, csr=None):
+                 t_begin: int = 0, t_end: int = 0, csr=None, mode: int = 0):
         self.X = np.ascontiguousarray(X, dtype=np.float32)
         self.n, self.d = self.X.shape
-        self.prm = Params(L, K, D, iprobes, kappa, alpha, seed)
+        self.prm = Params(L, K, D, iprobes, kappa, alpha, seed, mode)
         self.L, self.K, self.D = L, K, D
         self.t_begin, self.t_end = t_begin, (t_end or L)
         if csr is not None:  # (offsets [L][NB+1], ids, scores, table_base [L+1])

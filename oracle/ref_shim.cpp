@@ -54,6 +54,19 @@ int64_t ref_normalize(float* X, uint64_t n, uint32_t d) {
   }
 }
 
+// center(Dataset) in place, center vector out; returns -1 ok, -2 on error
+int64_t ref_center(float* X, uint64_t n, uint32_t d, float* center_out) {
+  try {
+    lsfann::Dataset ds(std::vector<float>(X, X + n * d), d);
+    lsfann::Dataset out = lsfann::center(ds);
+    std::memcpy(X, out.raw().data(), n * d * sizeof(float));
+    std::memcpy(center_out, out.center().data(), d * sizeof(float));
+    return -1;
+  } catch (const std::invalid_argument&) {
+    return -2;
+  }
+}
+
 double ref_inner_product(const float* a, const float* b, uint32_t d) {
   return lsfann::inner_product(std::span<const float>(a, d), std::span<const float>(b, d));
 }

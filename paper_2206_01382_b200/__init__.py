@@ -23,12 +23,13 @@ from . import _build
 __all__ = ["Index", "normalize", "synth", "device_count", "FppError", "FppInvalidArgument",
            "FppEmptyDataset", "FppDimensionError", "FppOutOfRange", "FppNonFinite",
            "FppZeroNorm", "FppCudaError", "FppOutOfMemory", "FppUnsupported", "FppFormatError",
-           "FppIOError", "content_hash", "lib",
+           "FppIOError", "content_hash", "center", "MODES", "lib",
            "LIB_PATH", "Params", "QueryStats", "Timings"]
 
 LIB_PATH = _build.LIB
 
 FPP_OK = 0
+MODES = {"falconnpp": 0, "falconn_baseline": 1}
 ABI_VERSION = 2  # include/falconnpp.h FPP_ABI_VERSION this binding was written against
 ERRORS = {1: "INVALID_ARGUMENT", 2: "EMPTY_DATASET", 3: "DIMENSION", 4: "OUT_OF_RANGE",
           5: "NON_FINITE", 6: "ZERO_NORM", 7: "CUDA", 8: "OUT_OF_MEMORY", 9: "UNSUPPORTED",
@@ -93,7 +94,7 @@ class Params(C.Structure):
     _fields_ = [("L", C.c_uint32), ("K", C.c_uint32), ("D", C.c_uint32),
                 ("iprobes", C.c_uint32), ("kappa", C.c_uint32), ("alpha", C.c_float),
                 ("seed", C.c_uint64), ("device", C.c_int32), ("id_offset", C.c_uint32),
-                ("scratch_bytes", C.c_uint64)]
+                ("scratch_bytes", C.c_uint64), ("centering", C.c_uint32), ("mode", C.c_uint32)]
 
 
 class QueryStats(C.Structure):
@@ -117,7 +118,8 @@ class IndexInfo(C.Structure):
                 ("kappa", C.c_uint32), ("alpha", C.c_float), ("seed", C.c_uint64),
                 ("num_buckets", C.c_uint64), ("kept_total", C.c_uint64),
                 ("prefilter_total", C.c_uint64), ("device_bytes", C.c_uint64),
-                ("max_bucket", C.c_uint32), ("id_offset", C.c_uint32)]
+                ("max_bucket", C.c_uint32), ("id_offset", C.c_uint32),
+                ("centering", C.c_uint32), ("mode", C.c_uint32)]
 
 
 vp = C.c_void_p
@@ -161,6 +163,8 @@ SIGNATURES = [
     ("fpp_load", C.c_int, [C.c_char_p, vp, u64, u32, i32, C.POINTER(vp)]),
     ("fpp_load_device", C.c_int, [C.c_char_p, vp, u64, u32, i32, C.POINTER(vp)]),
     ("fpp_content_hash", u64, [vp, u64, u32]),
+    ("fpp_center", C.c_int, [vp, u64, u32, vp]),
+    ("fpp_index_center", C.c_int, [vp, vp]),
     ("fpp_normalize", C.c_int, [vp, u64, u32]),
     ("fpp_synth", C.c_int, [vp, u64, u32, u32, f32, u64, u32, i32]),
 ]
@@ -234,12 +238,17 @@ class Index:
     # --------------------------------------------------------------- build
     @classmethod
     def build(cls, X, L: int, K: int, D: int, iProbes: int, alpha: float, kappa: int = 20,
-              seed: int = 1, device: int = -1, id_offset: int = 0, scratch_bytes: int = 0):
+              seed: int = 1, device: int = -1, id_offset: int = 0, scratch_bytes: int = 0,
+              centering: bool = False, mode: str = "falconnpp"):
         """Index::build(X, L, K, D, iProbes, alpha) -- SPEC.md:245-253.
 
         X is host (numpy) n x d fp32, already normalized, or a CUDA torch tensor.
+        centering: index center(X) (queries stay raw, scores x'.q).
+        mode: "falconnpp" or "falconn_baseline" (alpha = 1, iProbes = 1, probes by
+        ascending gap score).
         """
-        p = Params(L, K, D, iProbes, kappa, alpha, seed, device, id_offset, scratch_bytes)
+        p = Params(L, K, D, iProbes, kappa, alpha, seed, device, id_offset, scratch_bytes,
+                   int(bool(centering)), MODES[mode] if isinstance(mode, str) else int(mode))
         h = C.c_void_p()
         if _is_torch_cuda(X):
             X = X.contiguous()
@@ -259,7 +268,7 @@ class Index:
     def shard_begin(cls, X, L: int, K: int, D: int, iProbes: int, alpha: float, kappa: int = 20,
                     seed: int = 1, device: int = -1, id_offset: int = 0):
         """Phase 1 of the global-filter sharded build (see paper_2206_01382_b200.dist)."""
-        p = Params(L, K, D, iProbes, kappa, alpha, seed, device, id_offset, 0)
+        p = Params(L, K, D, iProbes, kappa, alpha, seed, device, id_offset, 0, 0, 0)
         h = C.c_void_p()
         if _is_torch_cuda(X):
             X = X.contiguous()
@@ -318,7 +327,7 @@ class Index:
         inf = IndexInfo()
         _check(lib().fpp_index_info_get(h, C.byref(inf)))
         p = Params(inf.L, inf.K, inf.D, inf.iprobes, inf.kappa, inf.alpha, inf.seed,
-                   max(device, 0), inf.id_offset, 0)
+                   max(device, 0), inf.id_offset, 0, inf.centering, inf.mode)
         return cls(h, p, n, d)
 
     def shard_hist_len(self) -> int:
@@ -392,6 +401,11 @@ class Index:
             _check(lib().fpp_query_device(self._h, C.c_void_p(Q.data_ptr()), Q.shape[0], k,
                                           qProbes, *args))
 
+    def center_vector(self) -> np.ndarray:
+        c = np.empty(self.d, np.float32)
+        _check(lib().fpp_index_center(self._h, _ptr(c)))
+        return c
+
     def signatures(self, X) -> np.ndarray:
         """64-bit SimHash signatures of rows X (as stored for the index's points)."""
         X = _f32(X)
@@ -460,6 +474,15 @@ class Index:
 
     def reset_timings(self) -> None:
         _check(lib().fpp_timings_reset(self._h))
+
+
+def center(X):
+    """center(Dataset) (dataset.cpp:40-57): returns (X - mean, mean) in fp32; the mean is
+    the reference's sequential double sum per coordinate, rows are not renormalized."""
+    X = np.array(X, dtype=np.float32, order="C", copy=True)
+    c = np.empty(X.shape[1], np.float32)
+    _check(lib().fpp_center(_ptr(X), X.shape[0], X.shape[1], _ptr(c)))
+    return X, c
 
 
 def content_hash(X) -> int:

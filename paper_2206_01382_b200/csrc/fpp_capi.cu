@@ -186,6 +186,24 @@ int sm_count() {
   return v;
 }
 
+// center(Dataset) (dataset.cpp:40-57) on the device: thread per coordinate, the
+// rows summed in order in double (so the mean is the reference's bit for bit),
+// center = float(mean / n); then rows -= center in fp32.
+__global__ void k_center_mean(const float* __restrict__ X, uint64_t n, uint32_t d,
+                              float* __restrict__ center) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d) return;
+  double m = 0.0;
+  for (uint64_t i = 0; i < n; ++i) m += (double)X[i * d + j];
+  center[j] = (float)(m / (double)n);
+}
+__global__ void k_center_sub(float* __restrict__ X, uint64_t cnt, uint32_t d,
+                             const float* __restrict__ center) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    X[e] -= center[e % d];
+}
+
 __global__ void k_check_finite(const float* __restrict__ X, uint64_t cnt, unsigned long long* bad) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -204,6 +222,8 @@ static void set_device(int dev) {
 }
 
 static void validate_params(const fpp_params& p, uint64_t n, uint32_t d) {
+  if (p.mode > FPP_MODE_FALCONN_BASELINE) fail(FPP_ERR_INVALID_ARGUMENT, "config: unknown mode");
+  if (p.centering > 1) fail(FPP_ERR_INVALID_ARGUMENT, "config: centering must be 0 or 1");
   if (n == 0) fail(FPP_ERR_EMPTY_DATASET, "dataset: need at least one point");
   if (d == 0) fail(FPP_ERR_INVALID_ARGUMENT, "dataset: dim must be >= 1");
   if (p.L == 0) fail(FPP_ERR_INVALID_ARGUMENT, "build: L must be >= 1");
@@ -233,7 +253,11 @@ static void validate_params(const fpp_params& p, uint64_t n, uint32_t d) {
 Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, const fpp_params* pp) {
   if (!pp) fail(FPP_ERR_INVALID_ARGUMENT, "build: params is NULL");
   if (!X && n) fail(FPP_ERR_INVALID_ARGUMENT, "build: X is NULL");
-  const fpp_params p = *pp;
+  fpp_params p = *pp;
+  if (p.mode == FPP_MODE_FALCONN_BASELINE) {  // baseline forces alpha=1, iProbes=1
+    p.alpha = 1.0f;
+    p.iprobes = 1;
+  }
   validate_params(p, n, d);
   set_device(p.device);
   if (!on_device) {  // dataset.cpp:15-18 finite check
@@ -279,6 +303,16 @@ Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, con
     FPP_CUDA(cudaMemcpyAsync(ix->signs, words.data(), words.size() * 4, cudaMemcpyHostToDevice,
                              ix->stream));
     ix->sign_words = words.size();
+    if (p.centering) {  // index the centered rows
+      DBuf<float> cd(d);
+      k_center_mean<<<(d + 127) / 128, 128, 0, ix->stream>>>(ix->X, n, d, cd.p);
+      FPP_LAUNCH();
+      k_center_sub<<<sm_count() * 4, 256, 0, ix->stream>>>(ix->X, n * d, d, cd.p);
+      FPP_LAUNCH();
+      ix->center.resize(d);
+      FPP_CUDA(cudaMemcpyAsync(ix->center.data(), cd.p, d * 4, cudaMemcpyDeviceToHost, ix->stream));
+      FPP_CUDA(cudaStreamSynchronize(ix->stream));
+    }
     // SimHash signatures of every point (rerank screening; n x 8 B)
     ix->sigs = static_cast<uint64_t*>(dmalloc(n * sizeof(uint64_t) + 8));
     launch_signatures(*ix, ix->X, n, ix->sigs, ix->stream);
@@ -292,6 +326,8 @@ Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, con
 
 static fpp_index* build_common(const float* X, bool on_device, uint64_t n, uint32_t d,
                                const fpp_params* pp, bool sharded = false) {
+  if (sharded && pp && pp->centering)
+    fail(FPP_ERR_UNSUPPORTED, "sharded build: centering needs the global mean (center X first)");
   Index* ix = prepare_index(X, on_device, n, d, pp);
   try {
     if (sharded) shard_begin(*ix);
@@ -571,6 +607,8 @@ int fpp_index_info_get(const fpp_index* idx, fpp_index_info* info) {
     info->device_bytes = ix.device_bytes;
     info->max_bucket = ix.max_bucket;
     info->id_offset = ix.prm.id_offset;
+    info->centering = ix.prm.centering;
+    info->mode = ix.prm.mode;
   });
 }
 
@@ -764,6 +802,31 @@ int fpp_load_device(const char* path, const float* X_dev, uint64_t n, uint32_t d
 
 uint64_t fpp_content_hash(const float* X, uint64_t n, uint32_t d) {
   return X ? content_hash(X, n, d) : 0;
+}
+
+int fpp_center(float* X, uint64_t n, uint32_t d, float* center_out) {
+  return guarded([&] {
+    if (!X || !n || !d) fail(FPP_ERR_EMPTY_DATASET, "dataset: need at least one point");
+    std::vector<float> c(d);
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < (int64_t)d; ++j) {  // dataset.cpp:45-48: rows in order, per coordinate
+      double m = 0.0;
+      for (uint64_t i = 0; i < n; ++i) m += X[i * d + j];
+      c[j] = float(m / double(n));
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < (int64_t)n; ++i)
+      for (uint32_t j = 0; j < d; ++j) X[(uint64_t)i * d + j] -= c[j];
+    if (center_out) std::memcpy(center_out, c.data(), d * 4);
+  });
+}
+
+int fpp_index_center(const fpp_index* idx, float* center_out) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    if (!center_out) fail(FPP_ERR_INVALID_ARGUMENT, "index_center: NULL buffer");
+    for (uint32_t j = 0; j < ix.d; ++j) center_out[j] = ix.center.empty() ? 0.0f : ix.center[j];
+  });
 }
 
 int fpp_normalize(float* X, uint64_t n, uint32_t d) {

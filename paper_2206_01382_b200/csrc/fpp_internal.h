@@ -86,6 +86,7 @@ struct Index {
   uint32_t max_bucket = 0;
   uint64_t sign_words = 0;
   uint64_t* sigs = nullptr;  // [n] SimHash signatures (rerank screening)
+  std::vector<float> center;  // [d] when prm.centering (dataset.cpp center())
   uint64_t device_bytes = 0;
   ShardState* shard = nullptr;  // global-filter sharded build in progress
 

@@ -6,7 +6,8 @@
 //           u32 iProbes, u32 kappa, u32 centering, u32 mode, u32 id_offset |
 //           u64 seed | u64 n | u32 d | f32 center[d] (centering only) |
 //           dataset reference: u32 path_len, path bytes, u64 content hash
-//           (fnv1a64 of the n*d fp32 bytes, common.hpp:50-57)
+//           (fnv1a64 of the indexed n*d fp32 rows -- after centering --
+//           common.hpp:50-57)
 //   body    per table t: u32 non-empty buckets, then per bucket (ascending id):
 //           u32 bucket, u32 count, count x (u32 point_id, f32 score) in the
 //           bucket's (score desc, id asc) order
@@ -80,7 +81,8 @@ void save_index(const Index& ix, const char* path, const float* X_host) {
   if (ix.shard) fail(FPP_ERR_INVALID_ARGUMENT, "save: sharded build not finished");
   const uint32_t L = ix.prm.L;
   const uint64_t NB = ix.NB;
-  // content hash of the dataset: from the caller's host copy, else from the device copy
+  // content hash of the indexed rows (after centering, if any): from the caller's
+  // host copy, else from the device copy
   uint64_t chash;
   if (X_host) {
     chash = content_hash(X_host, ix.n, ix.d);
@@ -101,12 +103,13 @@ void save_index(const Index& ix, const char* path, const float* X_host) {
   w.put<float>(ix.prm.alpha);
   w.put<uint32_t>(ix.prm.iprobes);
   w.put<uint32_t>(ix.prm.kappa);
-  w.put<uint32_t>(0);  // centering: off (SURVEY 8(c) pin)
-  w.put<uint32_t>(0);  // mode: falconnpp
+  w.put<uint32_t>(ix.prm.centering);
+  w.put<uint32_t>(ix.prm.mode);
   w.put<uint32_t>(ix.prm.id_offset);
   w.put<uint64_t>(ix.prm.seed);
   w.put<uint64_t>(ix.n);
   w.put<uint32_t>(ix.d);
+  if (ix.prm.centering) w.put(ix.center.data(), (size_t)ix.d * 4);
   w.put<uint32_t>(0);  // dataset path: not recorded (the caller passes X to load)
   w.put<uint64_t>(chash);
   w.in_body = true;
@@ -172,8 +175,14 @@ Index* load_index(const char* path, const float* X, bool on_device, uint64_t n, 
   p.seed = r.get<uint64_t>("seed");
   const uint64_t fn = r.get<uint64_t>("n");
   const uint32_t fd = r.get<uint32_t>("d");
-  if (centering) fail(FPP_ERR_UNSUPPORTED, "load: centered indexes are not supported");
-  if (mode != 0) fail(FPP_ERR_UNSUPPORTED, "load: only mode falconnpp is supported");
+  if (centering > 1 || mode > FPP_MODE_FALCONN_BASELINE)
+    fail(FPP_ERR_FORMAT, "load: config.centering / config.mode out of range");
+  if (fd == 0 || fd > (1u << 20)) fail(FPP_ERR_FORMAT, "load: d out of range");
+  std::vector<float> center;
+  if (centering) {
+    center.resize(fd);
+    r.get(center.data(), (size_t)fd * 4, "center");
+  }
   const uint32_t plen = r.get<uint32_t>("dataset.path_len");
   if (plen > 4096) fail(FPP_ERR_FORMAT, "load: dataset.path_len out of range");
   std::string dpath(plen, '\0');
@@ -183,20 +192,32 @@ Index* load_index(const char* path, const float* X, bool on_device, uint64_t n, 
     fail(FPP_ERR_DIMENSION, "load: dataset shape " + std::to_string(n) + "x" + std::to_string(d) +
                                 " does not match the index (" + std::to_string(fn) + "x" +
                                 std::to_string(fd) + ")");
-  // dataset reference check before anything is allocated
+  // dataset reference check before anything is allocated.  The hash covers the
+  // indexed rows: for a centered index the caller passes the raw rows and the
+  // stored center is subtracted in fp32 first (dataset.cpp:52-55: bit for bit).
   if (!X && n) fail(FPP_ERR_INVALID_ARGUMENT, "load: X is NULL");
-  uint64_t xhash;
-  if (on_device) {
-    std::vector<float> xh((size_t)n * d);
-    FPP_CUDA(cudaMemcpy(xh.data(), X, xh.size() * 4, cudaMemcpyDeviceToHost));
-    xhash = content_hash(xh.data(), n, d);
-  } else {
-    xhash = content_hash(X, n, d);
+  std::vector<float> xh;
+  const float* xsrc = X;
+  bool src_dev = on_device;
+  if (on_device || centering) {
+    xh.resize((size_t)n * d);
+    if (on_device) FPP_CUDA(cudaMemcpy(xh.data(), X, xh.size() * 4, cudaMemcpyDeviceToHost));
+    else std::memcpy(xh.data(), X, xh.size() * 4);
+    if (centering)
+      for (uint64_t i = 0; i < n; ++i)
+        for (uint32_t j = 0; j < d; ++j) xh[i * d + j] -= center[j];
+    xsrc = xh.data();
+    src_dev = false;
   }
-  if (xhash != chash) fail(FPP_ERR_FORMAT, "load: dataset content hash does not match the index");
+  if (content_hash(xsrc, n, d) != chash)
+    fail(FPP_ERR_FORMAT, "load: dataset content hash does not match the index");
   p.device = device;
   p.scratch_bytes = 0;
-  Index* ix = prepare_index(X, on_device, n, d, &p);
+  p.mode = mode;
+  p.centering = 0;  // xsrc is already centered
+  Index* ix = prepare_index(xsrc, src_dev, n, d, &p);
+  ix->prm.centering = centering;
+  ix->center = center;
   try {
     const uint32_t L = p.L;
     const uint64_t NB = ix->NB;

@@ -314,72 +314,58 @@ struct ProbeArgs {
 
 __device__ const float g_zero_row[1] = {0.0f};
 
-struct TableLists {
-  const float* v1;  // [s]
-  const float* v2;  // [S2] (a zero row when K == 1)
-  uint32_t s1, S2;
-};
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
 }
 
+// Pair key, larger first:
+//   falconnpp          ord(fl(a + b))                       (score sum desc)
+//   falconn_baseline   ord(-(fl(ma - a) + fl(mb - b)))      (gap score asc)
+// with a, b the two functions' |q.r| values and ma, mb their natural-list
+// maxima.  Both are non-increasing in either rank, which is all the staircase
+// machinery below relies on.
+template <int MODE>
+struct PairKey {
+  float ma, mb;
+  __device__ __forceinline__ uint32_t operator()(float a, float b) const {
+    if (MODE == 1) return ord_key(-((ma - a) + (mb - b)));
+    return ord_key(a + b);
+  }
+};
+
 // (lists may live in shared or global memory: generic loads)
-// number of r2 in [0, hi) with key(x + v2[r2]) >= T (a prefix: v2 non-increasing)
-__device__ __forceinline__ uint32_t prefix_bs(float x, const float* v2, uint32_t hi,
+// number of r2 in [0, hi) with key(x, v2[r2]) >= T (a prefix: keys non-increasing)
+template <class PK>
+__device__ __forceinline__ uint32_t prefix_bs(const PK& pk, float x, const float* v2, uint32_t hi,
                                               uint32_t T) {
   uint32_t lo = 0;
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
-    if (ord_key(x + v2[mid]) >= T) lo = mid + 1;
+    if (pk(x, v2[mid]) >= T) lo = mid + 1;
     else hi = mid;
   }
   return lo;
 }
 
-// first row in [lo, hi) with key(v1[row] + y) < T (rows satisfying it form a prefix)
-__device__ __forceinline__ uint32_t first_fail_row(const float* v1, float y, uint32_t lo,
-                                                   uint32_t hi, uint32_t T) {
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (ord_key(v1[mid] + y) >= T) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
-// non-forced pairs with key >= T.  Walks the staircase corner to corner: the
-// rows sharing a boundary p are found by one binary search over r1 and the
-// next boundary by one over r2, so the cost is O(corners * log s) whether the
-// staircase is long in r1, in r2, or both.
-__device__ __forceinline__ uint32_t walk_count(const TableLists& tl, uint32_t T) {
-  uint32_t p = prefix_bs(tl.v1[0], tl.v2, tl.S2, T);
-  if (p == 0) return 0;
-  uint32_t c = 0, r1 = 0;
-  for (;;) {
-    const uint32_t e = first_fail_row(tl.v1, tl.v2[p - 1], r1 + 1, tl.s1, T);
-    c += p * (e - r1);
-    if (e >= tl.s1) break;
-    p = prefix_bs(tl.v1[e], tl.v2, p - 1, T);
-    if (p == 0) break;
-    r1 = e;
-  }
-  return c - 1;  // exclude the forced (0,0)
-}
-
-// visit (r1, pa, pb): prefixes at Ta > Tb (pa <= pb), r1 ascending while pb > 0
-template <class F>
-__device__ __forceinline__ void walk2(const TableLists& tl, uint32_t Ta, uint32_t Tb, F&& visit) {
-  const float x0 = tl.v1[0];
-  uint32_t pb = prefix_bs(x0, tl.v2, tl.S2, Tb);
-  uint32_t pa = prefix_bs(x0, tl.v2, pb, Ta);
-  visit(0u, pa, pb);
-  for (uint32_t r1 = 1; r1 < tl.s1 && pb > 0; ++r1) {
-    const float x = tl.v1[r1];
-    if (ord_key(x + tl.v2[pb - 1]) < Tb) pb = prefix_bs(x, tl.v2, pb - 1, Tb);
+// visit (r1, pa, pb) for rows [rb, re) while pb > 0 (prefixes at Ta > Tb)
+template <class PK, class F>
+__device__ __forceinline__ void walk2_rows(const PK& pk, const float* v1, const float* v2,
+                                           uint32_t S2, uint32_t rb, uint32_t re, uint32_t Ta,
+                                           uint32_t Tb, F&& visit) {
+  if (rb >= re) return;
+  const float x0 = v1[rb];
+  uint32_t pb = prefix_bs(pk, x0, v2, S2, Tb);
+  if (pb == 0) return;
+  uint32_t pa = Ta == 0xffffffffu ? 0 : prefix_bs(pk, x0, v2, pb, Ta);
+  visit(rb, pa, pb);
+  for (uint32_t r1 = rb + 1; r1 < re; ++r1) {
+    const float x = v1[r1];
+    if (pk(x, v2[pb - 1]) < Tb) pb = prefix_bs(pk, x, v2, pb - 1, Tb);
+    if (pb == 0) return;
     if (pa > pb) pa = pb;
-    if (pa > 0 && ord_key(x + tl.v2[pa - 1]) < Ta) pa = prefix_bs(x, tl.v2, pa - 1, Ta);
+    if (pa > 0 && pk(x, v2[pa - 1]) < Ta) pa = prefix_bs(pk, x, v2, pa - 1, Ta);
     visit(r1, pa, pb);
   }
 }
@@ -395,52 +381,6 @@ __device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t* sh) {
   return t;
 }
 
-// CTA per query, thread per table.  The query's value lists are staged in
-// shared memory (when they fit) so the repeated staircase walks never leave the
-// SM; the emitted bucket ids are collected in shared memory and resolved
-// against the CSR directory by a flat, unrolled loop (8 independent loads in
-// flight per thread).
-// pairs >= T among rows [rb, re) of a grid (corner walk on a row block);
-// `forced` grids exclude their (0,0) (the true bucket, emitted separately)
-__device__ __forceinline__ uint32_t walk_count_rows(const float* v1, const float* v2, uint32_t S2,
-                                                    uint32_t rb, uint32_t re, uint32_t T,
-                                                    bool forced = true) {
-  if (rb >= re) return 0;
-  uint32_t p = prefix_bs(v1[rb], v2, S2, T);
-  if (p == 0) return 0;
-  uint32_t c = 0, r1 = rb;
-  for (;;) {
-    const uint32_t e = first_fail_row(v1, v2[p - 1], r1 + 1, re, T);
-    c += p * (e - r1);
-    if (e >= re) break;
-    p = prefix_bs(v1[e], v2, p - 1, T);
-    if (p == 0) break;
-    r1 = e;
-  }
-  return (rb == 0 && forced) ? c - 1 : c;
-}
-
-// visit (r1, pa, pb) for rows [rb, re) while pb > 0 (prefixes at Ta > Tb)
-template <class F>
-__device__ __forceinline__ void walk2_rows(const float* v1, const float* v2, uint32_t S2,
-                                           uint32_t rb, uint32_t re, uint32_t Ta, uint32_t Tb,
-                                           F&& visit) {
-  if (rb >= re) return;
-  const float x0 = v1[rb];
-  uint32_t pb = prefix_bs(x0, v2, S2, Tb);
-  if (pb == 0) return;
-  uint32_t pa = Ta == 0xffffffffu ? 0 : prefix_bs(x0, v2, pb, Ta);
-  visit(rb, pa, pb);
-  for (uint32_t r1 = rb + 1; r1 < re; ++r1) {
-    const float x = v1[r1];
-    if (ord_key(x + v2[pb - 1]) < Tb) pb = prefix_bs(x, v2, pb - 1, Tb);
-    if (pb == 0) return;
-    if (pa > pb) pa = pb;
-    if (pa > 0 && ord_key(x + v2[pa - 1]) < Ta) pa = prefix_bs(x, v2, pa - 1, Ta);
-    visit(r1, pa, pb);
-  }
-}
-
 // A "grid" is one (table, list-part x list-part) block of pairs, sorted in
 // both ranks: class 0 = natural x natural (one per table, its (0,0) is the
 // forced true bucket), class 1 = natural x opposite and opposite x natural,
@@ -453,6 +393,7 @@ struct GridRef {
   uint32_t oa, ob;   // rank offsets (0 natural, D opposite)
   uint32_t t;
   bool forced;
+  float ma, mb;      // natural-list maxima of the table's two functions (baseline gap)
 };
 
 // CTA per query (PS_THREADS threads, ~22 KB shared memory, so several query
@@ -472,6 +413,7 @@ struct GridRef {
 // The emission order of the selection class is not canonical: the probe set
 // (and so the candidate set and the top-k) is.
 constexpr int PS_RBITS = 12;  // radix digit
+template <int MODE>
 __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
   __shared__ uint64_t red[PS_THREADS / 32];
   __shared__ uint64_t ties[PS_TIE_CAP];
@@ -513,6 +455,8 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
     g.vb = v2 + (b_opp ? D : 0);
     g.nb = b_opp ? o : n2;
     g.ob = b_opp ? D : 0;
+    g.ma = v1[0];
+    g.mb = v2[0];
     return g;
   };
   const uint64_t M = a.peff - L;  // non-forced probes
@@ -596,10 +540,11 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
       GridRef g;
       uint32_t rb, re;
       unit(u, g, rb, re);
-      walk2_rows(g.va, g.vb, g.nb, rb, re, 0xffffffffu, Tlo, [&](uint32_t r1, uint32_t, uint32_t pb) {
+      const PairKey<MODE> pk{g.ma, g.mb};
+      walk2_rows(pk, g.va, g.vb, g.nb, rb, re, 0xffffffffu, Tlo, [&](uint32_t r1, uint32_t, uint32_t pb) {
         const float x = g.va[r1];
         for (uint32_t r2 = (r1 == 0 && g.forced) ? 1 : 0; r2 < pb; ++r2)
-          visit(ord_key(x + g.vb[r2]), pack(g.t, g.oa + r1, g.ob + r2));
+          visit(pk(x, g.vb[r2]), pack(g.t, g.oa + r1, g.ob + r2));
       });
     }
   };
@@ -637,14 +582,15 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
     uint32_t amax = 0, amin = 0xffffffffu;
     for (uint32_t gi = threadIdx.x; gi < NG; gi += blockDim.x) {  // runs are sorted: corners
       const GridRef g = grid(sel, gi);
+      const PairKey<MODE> pk{g.ma, g.mb};
       const uint32_t r0 = g.forced ? 1 : 0;
       if (g.nb > r0) {
-        amax = max(amax, ord_key(g.va[0] + g.vb[r0]));
-        amin = min(amin, ord_key(g.va[0] + g.vb[g.nb - 1]));
+        amax = max(amax, pk(g.va[0], g.vb[r0]));
+        amin = min(amin, pk(g.va[0], g.vb[g.nb - 1]));
       }
       if (g.na > 1) {
-        amax = max(amax, ord_key(g.va[1] + g.vb[0]));
-        amin = min(amin, ord_key(g.va[g.na - 1] + g.vb[0]));
+        amax = max(amax, pk(g.va[1], g.vb[0]));
+        amin = min(amin, pk(g.va[g.na - 1], g.vb[0]));
       }
     }
     uint64_t pk = ((uint64_t)amax << 32) | (0xffffffffu - amin);
@@ -673,6 +619,7 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
       constexpr int AU = 8;
       for (uint32_t gi = wp; gi < NG; gi += nw) {
         const GridRef g = grid(sel, gi);
+        const PairKey<MODE> pk{g.ma, g.mb};
         const uint32_t nrow = g.nb - (g.forced ? 1 : 0);
         const float x0 = g.va[0], y0 = g.vb[0];
         for (uint32_t i0 = lane; i0 < A; i0 += 32 * AU) {
@@ -686,8 +633,8 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
           for (int u = 0; u < AU; ++u) {
             const uint32_t i = i0 + 32 * u;
             if (i < A) {
-              const float sc = i < nrow ? x0 + v[u] : v[u] + y0;
-              smem_inc(&hist[(ord_key(sc) - amin) >> sh]);
+              const uint32_t key = i < nrow ? pk(x0, v[u]) : pk(v[u], y0);
+              smem_inc(&hist[(key - amin) >> sh]);
             }
           }
         }
@@ -729,13 +676,14 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
     auto materialise = [&]() {
       for (uint32_t gi = wp; gi < NG; gi += nw) {
         const GridRef g = grid(sel, gi);
+        const PairKey<MODE> pk{g.ma, g.mb};
         uint32_t pb = g.nb, r1 = 0;
         for (; r1 < g.na && pb > 32; ++r1) {
           const float x = g.va[r1];
           uint32_t npb = 0;
           for (uint32_t c0 = 0; c0 < pb; c0 += 32) {
             const uint32_t r2 = c0 + lane;
-            const uint32_t key = r2 < pb ? ord_key(x + g.vb[r2]) : 0;
+            const uint32_t key = r2 < pb ? pk(x, g.vb[r2]) : 0;
             const bool ge = r2 < pb && key >= Tlo;
             const uint32_t bal = __ballot_sync(FULL, ge);
             npb += __popc(bal);
@@ -757,7 +705,7 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
   #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const uint32_t c = c0 + u;
-              const uint32_t key = ord_key(x + y[u]);
+              const uint32_t key = pk(x, y[u]);
               alive = alive && c < pb && key >= Tlo;
               cnt += alive;
               any |= __ballot_sync(FULL, alive);
@@ -1590,7 +1538,8 @@ static void stage_a(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     sl.dbgclk.ensure((size_t)nqc * 16);
     pa.dbg_clk = reinterpret_cast<long long*>(sl.dbgclk.p);
   }
-  k_probe_select<<<nqc, PS_THREADS, 0, st>>>(pa);
+  if (ix.prm.mode == FPP_MODE_FALCONN_BASELINE) k_probe_select<1><<<nqc, PS_THREADS, 0, st>>>(pa);
+  else k_probe_select<0><<<nqc, PS_THREADS, 0, st>>>(pa);
   FPP_LAUNCH();
   if (dbg_probe) {
     std::vector<long long> h((size_t)nqc * 16);

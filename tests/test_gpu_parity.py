@@ -383,3 +383,52 @@ def test_rerank_recall_bound(fpp, orc):
     full = recall(ix.query(Q, 20, 1000)[0])
     for B in (20, 100, 400):
         assert recall(ix.query(Q, 20, 1000, rerank=B)[0]) <= full + 1e-12
+
+
+@pytest.mark.parametrize("K,D,qps", [(2, 64, [8, 300, 3000]), (1, 128, [10, 200])])
+def test_falconn_baseline_parity(fpp, orc, K, D, qps):
+    # alpha = 1, iProbes = 1 forced; probes by ascending gap score
+    X = data(fpp, 8000, 100 if D == 128 else 64, 20, 0.3)
+    Q = data(fpp, 40, X.shape[1], 20, 0.3, stream=1)
+    ix = fpp.Index.build(X, L=6, K=K, D=D, iProbes=3, alpha=0.1, mode="falconn_baseline")
+    ox = orc.Index(X, L=6, K=K, D=D, iprobes=3, alpha=0.1, mode=1)
+    inf = ix.info()
+    assert (inf["alpha"], inf["iprobes"], inf["mode"]) == (1.0, 1, 1)
+    for t in range(6):
+        for u, v in zip(ix.table(t), ox.table(t)):
+            assert np.array_equal(u, v)
+    for qp in qps:
+        gi, gs, gst = ix.query(Q, 10, qp, return_stats=True)
+        oi, os_, ost = ox.query(Q, 10, qp)
+        assert np.array_equal(gst, ost) and np.array_equal(gi, oi) and np.array_equal(gs, os_), qp
+        for qi in (0, 11):
+            gp, gc = ix.query_debug(Q[qi], qp)
+            op, oc = ox.query_debug(Q[qi], qp)
+            assert np.array_equal(gp, op) and np.array_equal(gc, oc), (qp, qi)
+    # the first probe of every table is the true bucket in both modes
+    iy = fpp.Index.build(X, L=6, K=K, D=D, iProbes=1, alpha=1.0)
+    assert np.array_equal(ix.query_debug(Q[0], 6)[0], iy.query_debug(Q[0], 6)[0])
+
+
+def test_centering_parity(fpp, orc, tmp_path):
+    # SPEC.md:53-61 (dataset.cpp center()): index center(X); queries stay raw
+    raw = fpp.synth(6000, 64, 10, 0.3, seed=12)
+    X = fpp.normalize(raw) + np.float32(0.05)  # off-centre data
+    Q = data(fpp, 30, 64, 10, 0.3, seed=12, stream=1)
+    ix = fpp.Index.build(X, L=5, K=2, D=64, iProbes=3, alpha=0.1, centering=True)
+    Xc, c = orc.center(X)
+    ox = orc.Index(Xc, L=5, K=2, D=64, iprobes=3, alpha=0.1)
+    assert np.array_equal(ix.center_vector(), c) and ix.info()["centering"] == 1
+    for t in range(5):
+        for u, v in zip(ix.table(t), ox.table(t)):
+            assert np.array_equal(u, v)
+    gi, gs, gst = ix.query(Q, 10, 400, return_stats=True)
+    oi, os_, ost = ox.query(Q, 10, 400)
+    assert np.array_equal(gi, oi) and np.array_equal(gs, os_) and np.array_equal(gst, ost)
+    # FLPP keeps the center; load takes the raw rows again
+    p = str(tmp_path / "c.flpp")
+    ix.save(p)
+    iy = fpp.Index.load(p, X)
+    li, ls = iy.query(Q, 10, 400)
+    assert np.array_equal(li, gi) and np.array_equal(ls, gs)
+    assert np.array_equal(iy.center_vector(), c)

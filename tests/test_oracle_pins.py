@@ -103,6 +103,21 @@ def test_normalize_and_inner_product_vs_reference(orc):
             R.ref_inner_product(a[i], a[i + 1], 37)
 
 
+def test_center_vs_reference(orc):
+    # dataset.cpp:40-57 center(): double mean, float center, fp32 subtraction
+    R = ref_or_skip(orc)
+    import ctypes as C
+    X = np.random.default_rng(5).standard_normal((3001, 41)).astype(np.float32) + 0.3
+    a, ca = orc.center(X)
+    b = X.copy()
+    cb = np.empty(41, np.float32)
+    R.ref_center.restype = C.c_int64
+    R.ref_center.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p]
+    assert R.ref_center(b.ctypes.data, 3001, 41, cb.ctypes.data) == -1
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert np.array_equal(ca.view(np.uint32), cb.view(np.uint32))
+
+
 def test_normalize_is_not_idempotent(orc):
     # dataset.hpp:50-52 claims idempotence; bit-wise it is not,
     # which is why inputs are normalized exactly once on the host.
