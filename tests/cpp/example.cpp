@@ -3,6 +3,7 @@
 // 2 if no GPU is present (the build step still validates the API).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "lsfann/falconnpp_gpu.hpp"
@@ -24,6 +25,18 @@ int main() {
     for (int j = 0; j + 1 < 10; ++j)
       if (r.ids[i * 10 + j + 1] != 0xFFFFFFFFu && r.scores[i * 10 + j] < r.scores[i * 10 + j + 1])
         return 1;
-  std::printf("cpp ok: kept %llu\n", (unsigned long long)ix.info().kept_total);
+  // rerank, ground truth and FLPP round trip through the C++ surface
+  auto rr = ix.query_rerank(Q, nq, 10, 64, 40, true);
+  for (std::size_t i = 0; i < nq; ++i)
+    if (rr.stats[i].exact > 40) return 1;
+  auto gt = ix.brute_force(Q, nq, 10);
+  const char* path = "/tmp/fpp_cpp_example.flpp";
+  ix.save(path);
+  auto iy = lsfann::gpu::Index::load(path, X, n, d);
+  auto r2 = iy.query(Q, nq, 10, 64, true);
+  if (r2.ids != r.ids || r2.scores != r.scores) return 1;
+  std::remove(path);
+  std::printf("cpp ok: kept %llu, top1 %u (gt %u)\n", (unsigned long long)ix.info().kept_total,
+              r.ids[0], gt.ids[0]);
   return 0;
 }
