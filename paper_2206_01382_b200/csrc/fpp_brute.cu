@@ -66,6 +66,7 @@ struct BruteArgs {
   const float* X;
   uint64_t n;
   uint32_t d;
+  uint32_t ldx;  // row stride of X (floats)
   const float* Q;
   uint32_t nq, k;
   uint64_t rows_per_split;
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(BF_WARPS * 32) k_brute(BruteArgs a) {
           for (int it = 0; it < 8; ++it) {
             const uint64_t row = row0 + rbase + 4 * it;
             if (row < r_end)
-              bf_cp16(buf + (rbase + 4 * it) * BF_ROWPAD + kk * 4, a.X + row * d + col0 + kk * 4);
+              bf_cp16(buf + (rbase + 4 * it) * BF_ROWPAD + kk * 4, a.X + row * a.ldx + col0 + kk * 4);
           }
         }
       } else {
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(BF_WARPS * 32) k_brute(BruteArgs a) {
           const uint64_t row = row0 + r;
           if (row < r_end)
             for (uint32_t c = lane; c < len; c += 32)
-              bf_cp4(buf + r * BF_ROWPAD + c, a.X + row * d + col0 + c);
+              bf_cp4(buf + r * BF_ROWPAD + c, a.X + row * a.ldx + col0 + c);
         }
       }
       if (++ic == nsl) {
@@ -234,7 +235,7 @@ void run_brute_force(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, 
   const uint64_t rows_per_split = (ix.n + splits - 1) / splits;
   DBuf<uint32_t> pids((size_t)splits * nq * k);
   DBuf<double> psc((size_t)splits * nq * k);
-  BruteArgs a{ix.X, ix.n, d, Qd, (uint32_t)nq, k, rows_per_split, pids.p, psc.p};
+  BruteArgs a{ix.X, ix.n, d, ix.ldx, Qd, (uint32_t)nq, k, rows_per_split, pids.p, psc.p};
   static_assert(BF_WARPS * BF_QT * 32 * 12 <= BF_WARPS * BF_STAGES * BF_STAGE_FLOATS * 4,
                 "merge lists must fit in the ring");
   const size_t smem = (size_t)d * BF_QT * 8 + (size_t)BF_WARPS * BF_STAGES * BF_STAGE_FLOATS * 4;

@@ -157,7 +157,8 @@ __device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], in
 
 template <int P, int R>
 __global__ void __launch_bounds__(256, 3)
-k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, uint32_t K,
+k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx, uint32_t D,
+             uint32_t K,
              const uint32_t* __restrict__ signs, uint32_t t0, uint32_t T, uint32_t ip,
              uint2* __restrict__ ent, uint32_t* __restrict__ counts, uint64_t NB) {
   using S = FhtShape<P>;
@@ -179,7 +180,7 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
   const bool active = gid < n;
   const uint64_t i = active ? gid : n - 1;  // inactive groups shadow a real row
   float x[S::EPT];
-  load_row<P>(X + i * d, d, g, x);
+  load_row<P>(X + i * ldx, d, g, x);
   const uint32_t r = ip < D ? ip : D;  // ranks needed per function (host ensures <= R)
   const uint32_t twoD = 2 * D;
   // candidate pairs: (a+1)(b+1) <= ip (every pair with a' <= a, b' <= b strictly
@@ -280,7 +281,7 @@ k_project(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D,
 // cross_polytope_hash).  One lane group per row; partial masks OR-reduced.
 template <int P>
 __global__ void __launch_bounds__(256)
-k_signatures(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D,
+k_signatures(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ld, uint32_t D,
              const uint32_t* __restrict__ sw, uint64_t* __restrict__ out) {
   using S = FhtShape<P>;
   constexpr bool TR = P >= 64;
@@ -293,7 +294,7 @@ k_signatures(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D,
   const bool active = gid < n;
   const uint64_t i = active ? gid : n - 1;
   float v[S::EPT];
-  load_row<P>(X + i * d, d, g, v);
+  load_row<P>(X + i * ld, d, g, v);
   if constexpr (TR) spinner_project_T<P>(v, sw, g, buf);
   else spinner_project<P>(v, sw, g);
   const uint32_t m = D < 64 ? D : 64;
@@ -308,7 +309,8 @@ k_signatures(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D,
   if (active && g == 0) out[i] = sig;
 }
 
-void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint64_t* out, cudaStream_t s) {
+void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint32_t ld, uint64_t* out,
+                       cudaStream_t s) {
   if (n == 0) return;
   const uint32_t P = ix.P;
   const uint32_t G = P < 32 ? 1 : P / 32;
@@ -316,7 +318,7 @@ void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint64_t* o
   const uint32_t* sw = ix.signs;  // stack (t=0, f=0)
 #define FPP_SIG_CASE(PP)                                                            \
   case PP:                                                                          \
-    k_signatures<PP><<<blocks, 256, 0, s>>>(Xd, n, ix.d, ix.prm.D, sw, out);        \
+    k_signatures<PP><<<blocks, 256, 0, s>>>(Xd, n, ix.d, ld, ix.prm.D, sw, out);    \
     break;
   switch (P) {
     FPP_SIG_CASE(2) FPP_SIG_CASE(4) FPP_SIG_CASE(8) FPP_SIG_CASE(16) FPP_SIG_CASE(32)
@@ -686,7 +688,8 @@ k_sort_large(const uint32_t* __restrict__ starts, const uint64_t* __restrict__ k
 
 // ------------------------------------------------------------ host dispatch
 template <int R>
-static void launch_hash_R(const Index& ix, const float* X, uint64_t n, uint32_t t0, uint32_t T,
+static void launch_hash_R(const Index& ix, const float* X, uint32_t ld, uint64_t n, uint32_t t0,
+                          uint32_t T,
                           uint2* ent, uint32_t* counts, cudaStream_t s) {
   const uint32_t P = ix.P;
   uint32_t G = P < 32 ? 1 : P / 32;
@@ -699,7 +702,7 @@ static void launch_hash_R(const Index& ix, const float* X, uint64_t n, uint32_t 
     if (sm > 48 * 1024)                                                                        \
       FPP_CUDA(cudaFuncSetAttribute(k_hash_build<PP, R>,                                       \
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, sm));         \
-    k_hash_build<PP, R><<<blocks, 256, sm, s>>>(X, n, ix.d, D, K, ix.signs, t0, T, ip, ent,    \
+    k_hash_build<PP, R><<<blocks, 256, sm, s>>>(X, n, ix.d, ld, D, K, ix.signs, t0, T, ip, ent, \
                                                 counts, ix.NB);                                \
     break;                                                                                     \
   }
@@ -713,17 +716,18 @@ static void launch_hash_R(const Index& ix, const float* X, uint64_t n, uint32_t 
   FPP_LAUNCH();
 }
 
-static void launch_hash(const Index& ix, const float* X, uint64_t n, uint32_t t0, uint32_t T,
+static void launch_hash(const Index& ix, const float* X, uint32_t ld, uint64_t n, uint32_t t0,
+                        uint32_t T,
                         uint2* ent, uint32_t* counts, cudaStream_t s) {
   const uint32_t r = std::min(ix.prm.iprobes, ix.prm.D);
-  if (r <= 4) launch_hash_R<4>(ix, X, n, t0, T, ent, counts, s);
-  else if (r <= 8) launch_hash_R<8>(ix, X, n, t0, T, ent, counts, s);
-  else launch_hash_R<16>(ix, X, n, t0, T, ent, counts, s);
+  if (r <= 4) launch_hash_R<4>(ix, X, ld, n, t0, T, ent, counts, s);
+  else if (r <= 8) launch_hash_R<8>(ix, X, ld, n, t0, T, ent, counts, s);
+  else launch_hash_R<16>(ix, X, ld, n, t0, T, ent, counts, s);
 }
 
 void launch_index_probes(const Index& ix, const float* Xd, uint64_t n, uint32_t t, uint2* out,
                          cudaStream_t s) {
-  launch_hash(ix, Xd, n, t, 1, out, nullptr, s);
+  launch_hash(ix, Xd, ix.d, n, t, 1, out, nullptr, s);
 }
 
 void launch_project(const Index& ix, const float* Xd, uint64_t n, uint32_t t, uint32_t f,
@@ -788,7 +792,7 @@ void build_tables(Index& ix) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     ix.timer.begin(PH_HASH, s, &e0);
     FPP_CUDA(cudaMemsetAsync(counts.p, 0, (size_t)Tc * NB * sizeof(uint32_t), s));
-    launch_hash(ix, ix.X, n, t0, Tc, ent.p, counts.p, s);
+    launch_hash(ix, ix.X, ix.ldx, n, t0, Tc, ent.p, counts.p, s);
     ix.timer.end(PH_HASH, e0, s);
     ix.timer.begin(PH_SORT, s, &e1);
     uint32_t* offs = ix.offsets + (uint64_t)t0 * (NB + 1);
@@ -895,7 +899,7 @@ void shard_begin(Index& ix) {
   cudaEvent_t e0;
   ix.timer.begin(PH_HASH, s, &e0);
   FPP_CUDA(cudaMemsetAsync(st->hist.p, 0, (size_t)L * NB * 4, s));
-  launch_hash(ix, ix.X, n, 0, L, ent.p, st->hist.p, s);
+  launch_hash(ix, ix.X, ix.ldx, n, 0, L, ent.p, st->hist.p, s);
   ix.timer.end(PH_HASH, e0, s);
   ix.timer.begin(PH_SORT, s, &e0);
   KeepXform ident{0, 0.f, 1, 0};

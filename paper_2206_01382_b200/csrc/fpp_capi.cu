@@ -189,19 +189,23 @@ int sm_count() {
 // center(Dataset) (dataset.cpp:40-57) on the device: thread per coordinate, the
 // rows summed in order in double (so the mean is the reference's bit for bit),
 // center = float(mean / n); then rows -= center in fp32.
-__global__ void k_center_mean(const float* __restrict__ X, uint64_t n, uint32_t d,
+__global__ void k_center_mean(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx,
                               float* __restrict__ center) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d) return;
   double m = 0.0;
-  for (uint64_t i = 0; i < n; ++i) m += (double)X[i * d + j];
+  for (uint64_t i = 0; i < n; ++i) m += (double)X[i * ldx + j];
   center[j] = (float)(m / (double)n);
 }
-__global__ void k_center_sub(float* __restrict__ X, uint64_t cnt, uint32_t d,
+__global__ void k_center_sub(float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx,
                              const float* __restrict__ center) {
+  const uint64_t cnt = n * d;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt;
-       e += (uint64_t)gridDim.x * blockDim.x)
-    X[e] -= center[e % d];
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = e / d;
+    const uint32_t j = (uint32_t)(e - i * d);
+    X[i * ldx + j] -= center[j];
+  }
 }
 
 __global__ void k_check_finite(const float* __restrict__ X, uint64_t cnt, unsigned long long* bad) {
@@ -281,21 +285,25 @@ Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, con
     FPP_CUDA(cudaGetDevice(&ix->device));
     FPP_CUDA(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
     FPP_CUDA(cudaMallocHost(&ix->h_pinned, 64));
-    ix->X = static_cast<float*>(dmalloc(n * d * sizeof(float)));
-    FPP_CUDA(cudaMemcpyAsync(ix->X, X, n * d * sizeof(float),
-                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                             ix->stream));
+    // rows padded to a 128 B multiple (d >= 32): the score gather's row slices then
+    // start on line boundaries (+5% DRAM efficiency on C2's 1200 B rows)
+    ix->ldx = d < 32 ? d : (d + 31) / 32 * 32;
+    ix->X = static_cast<float*>(dmalloc((size_t)n * ix->ldx * sizeof(float)));
+    if (ix->ldx != d) FPP_CUDA(cudaMemsetAsync(ix->X, 0, (size_t)n * ix->ldx * 4, ix->stream));
+    FPP_CUDA(cudaMemcpy2DAsync(ix->X, (size_t)ix->ldx * 4, X, (size_t)d * 4, (size_t)d * 4, n,
+                               on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                               ix->stream));
     if (on_device) {
       DBuf<unsigned long long> bad(1);
       const unsigned long long init = ~0ull;
       FPP_CUDA(cudaMemcpyAsync(bad.p, &init, 8, cudaMemcpyHostToDevice, ix->stream));
-      k_check_finite<<<sm_count() * 4, 256, 0, ix->stream>>>(ix->X, n * d, bad.p);
+      k_check_finite<<<sm_count() * 4, 256, 0, ix->stream>>>(ix->X, n * ix->ldx, bad.p);
       FPP_LAUNCH();
       unsigned long long b = 0;
       FPP_CUDA(cudaMemcpyAsync(&b, bad.p, 8, cudaMemcpyDeviceToHost, ix->stream));
       FPP_CUDA(cudaStreamSynchronize(ix->stream));
       if (b != ~0ull)
-        fail(FPP_ERR_NON_FINITE, "dataset: non-finite coordinate in row " + std::to_string(b / d));
+        fail(FPP_ERR_NON_FINITE, "dataset: non-finite coordinate in row " + std::to_string(b / ix->ldx));
     }
     std::vector<uint32_t> words;
     pack_signs(p, P, words);
@@ -305,9 +313,9 @@ Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, con
     ix->sign_words = words.size();
     if (p.centering) {  // index the centered rows
       DBuf<float> cd(d);
-      k_center_mean<<<(d + 127) / 128, 128, 0, ix->stream>>>(ix->X, n, d, cd.p);
+      k_center_mean<<<(d + 127) / 128, 128, 0, ix->stream>>>(ix->X, n, d, ix->ldx, cd.p);
       FPP_LAUNCH();
-      k_center_sub<<<sm_count() * 4, 256, 0, ix->stream>>>(ix->X, n * d, d, cd.p);
+      k_center_sub<<<sm_count() * 4, 256, 0, ix->stream>>>(ix->X, n, d, ix->ldx, cd.p);
       FPP_LAUNCH();
       ix->center.resize(d);
       FPP_CUDA(cudaMemcpyAsync(ix->center.data(), cd.p, d * 4, cudaMemcpyDeviceToHost, ix->stream));
@@ -315,7 +323,7 @@ Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, con
     }
     // SimHash signatures of every point (rerank screening; n x 8 B)
     ix->sigs = static_cast<uint64_t*>(dmalloc(n * sizeof(uint64_t) + 8));
-    launch_signatures(*ix, ix->X, n, ix->sigs, ix->stream);
+    launch_signatures(*ix, ix->X, n, ix->ldx, ix->sigs, ix->stream);
     FPP_CUDA(cudaStreamSynchronize(ix->stream));
   } catch (...) {
     delete ix;
@@ -332,7 +340,7 @@ static fpp_index* build_common(const float* X, bool on_device, uint64_t n, uint3
   try {
     if (sharded) shard_begin(*ix);
     else build_tables(*ix);
-    ix->device_bytes = n * d * 4 + ix->sign_words * 4 + (uint64_t)ix->prm.L * (ix->NB + 1) * 4 +
+    ix->device_bytes = n * ix->ldx * 4 + ix->sign_words * 4 + (uint64_t)ix->prm.L * (ix->NB + 1) * 4 +
                        (ix->prm.L + 1) * 8 + ix->kept_total * 8;
     double ms[PH_COUNT] = {0};
     ix->timer.collect(ms);
@@ -518,7 +526,7 @@ int fpp_signatures(const fpp_index* idx, const float* X, uint64_t n, uint64_t* o
     DBuf<float> xd(n * ix.d);
     DBuf<uint64_t> od(n);
     FPP_CUDA(cudaMemcpyAsync(xd.p, X, n * ix.d * 4, cudaMemcpyHostToDevice, ix.stream));
-    launch_signatures(ix, xd.p, n, od.p, ix.stream);
+    launch_signatures(ix, xd.p, n, ix.d, od.p, ix.stream);
     FPP_CUDA(cudaMemcpyAsync(out, od.p, n * 8, cudaMemcpyDeviceToHost, ix.stream));
     FPP_CUDA(cudaStreamSynchronize(ix.stream));
   });
@@ -579,7 +587,7 @@ int fpp_shard_finish(fpp_index* idx, const uint32_t* global_hist_dev, const uint
     Index& ix = *reinterpret_cast<Index*>(idx);
     DeviceGuard dg(ix.device);
     shard_finish(ix, global_hist_dev, all_prefix_dev, world);
-    ix.device_bytes = ix.n * ix.d * 4 + (uint64_t)ix.prm.L * (ix.NB + 1) * 4 + ix.kept_total * 8;
+    ix.device_bytes = ix.n * ix.ldx * 4 + (uint64_t)ix.prm.L * (ix.NB + 1) * 4 + ix.kept_total * 8;
     double ms[PH_COUNT] = {0};
     ix.timer.collect(ms);
     ix.acc.hash_ms += ms[PH_HASH];

@@ -70,6 +70,7 @@ struct Index {
   fpp_params prm{};
   uint64_t n = 0;
   uint32_t d = 0, P = 0;  // P = d_pad = FHT length
+  uint32_t ldx = 0;       // row stride of X in floats: d rounded up to 32 (128 B rows)
   uint64_t NB = 0;        // buckets per table
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -146,7 +147,8 @@ void build_tables(Index& ix);
 Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, const fpp_params* pp);
 uint64_t content_hash(const float* X, uint64_t n, uint32_t d);
 void save_index(const Index& ix, const char* path, const float* X_host);
-void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint64_t* out, cudaStream_t s);
+void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint32_t ld, uint64_t* out,
+                       cudaStream_t s);
 void run_brute_force(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t* ids_d,
                      double* scores_d, cudaStream_t s);
 Index* load_index(const char* path, const float* X, bool on_device, uint64_t n, uint32_t d,

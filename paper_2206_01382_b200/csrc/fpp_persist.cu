@@ -88,7 +88,8 @@ void save_index(const Index& ix, const char* path, const float* X_host) {
     chash = content_hash(X_host, ix.n, ix.d);
   } else {
     std::vector<float> xh((size_t)ix.n * ix.d);
-    FPP_CUDA(cudaMemcpyAsync(xh.data(), ix.X, xh.size() * 4, cudaMemcpyDeviceToHost, ix.stream));
+    FPP_CUDA(cudaMemcpy2DAsync(xh.data(), (size_t)ix.d * 4, ix.X, (size_t)ix.ldx * 4,
+                               (size_t)ix.d * 4, ix.n, cudaMemcpyDeviceToHost, ix.stream));
     FPP_CUDA(cudaStreamSynchronize(ix.stream));
     chash = content_hash(xh.data(), ix.n, ix.d);
   }
@@ -279,7 +280,7 @@ Index* load_index(const char* path, const float* X, bool on_device, uint64_t n, 
                                ix->stream));
     }
     FPP_CUDA(cudaStreamSynchronize(ix->stream));
-    ix->device_bytes = n * d * 4 + ix->sign_words * 4 + offs.size() * 4 + (L + 1) * 8 +
+    ix->device_bytes = n * ix->ldx * 4 + ix->sign_words * 4 + offs.size() * 4 + (L + 1) * 8 +
                        ix->kept_total * 8;
   } catch (...) {
     delete ix;

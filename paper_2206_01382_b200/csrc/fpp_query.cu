@@ -1220,6 +1220,7 @@ struct ScRing {
 struct ScoreArgs {
   const float* X;
   uint32_t d;
+  uint32_t ldx;  // row stride of X (floats)
   const float* Q;
   const uint64_t* coff;
   const uint32_t* cands;
@@ -1315,7 +1316,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, 2) k_score(ScoreArgs a) {
 #pragma unroll
       for (int it = 0; it < 8; ++it) {
         const uint32_t idr = __shfl_sync(FULL, my_id, rbase + 4 * it);
-        rp[it] = idr != 0xffffffffu ? X + (uint64_t)idr * d : nullptr;
+        rp[it] = idr != 0xffffffffu ? X + (uint64_t)idr * a.ldx : nullptr;
       }
     }
   };
@@ -1339,7 +1340,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, 2) k_score(ScoreArgs a) {
           const uint32_t idr = __shfl_sync(FULL, my_id, r);
           if (idr != 0xffffffffu)
             for (uint32_t c = lane; c < len; c += 32)
-              cp_async4(buf + r * SC_ROWPAD + c, X + (uint64_t)idr * d + col0 + c);
+              cp_async4(buf + r * SC_ROWPAD + c, X + (uint64_t)idr * a.ldx + col0 + c);
         }
       }
       if (++ic == nsl) {
@@ -1624,13 +1625,13 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   ix.timer.end(PH_COLLECT, e0, st);
 
   ix.timer.begin(PH_SCORE, st, &e0);
-  ScoreArgs sa{ix.X, ix.d, Qd, sl.coff.p, sl.cands.p, sl.uq.p, sl.eq.p, peff, k,
+  ScoreArgs sa{ix.X, ix.d, ix.ldx, Qd, sl.coff.p, sl.cands.p, sl.uq.p, sl.eq.p, peff, k,
                ix.prm.id_offset, ids_d, scores_d, stats_d, nullptr, 0};
   if (rerank) {  // SimHash screen: at most B candidates per query reach the exact scores
     sl.qsig.ensure(nqc);
     sl.cands2.ensure((size_t)nqc * rerank);
     sl.uq2.ensure(nqc);
-    launch_signatures(ix, Qd, nqc, sl.qsig.p, st);
+    launch_signatures(ix, Qd, nqc, ix.d, sl.qsig.p, st);
     k_screen<<<nqc, SCR_THREADS, 0, st>>>(sl.cands.p, sl.coff.p, sl.uq.p, ix.sigs, sl.qsig.p, rerank,
                                           sl.cands2.p, sl.uq2.p);
     FPP_LAUNCH();
