@@ -235,19 +235,6 @@ __device__ __forceinline__ uint32_t rank_code(uint64_t k, uint32_t D) {
   return (k & 1u) ? D + j : j;
 }
 
-template <int R>
-__device__ __forceinline__ void topr_insert(uint64_t (&t)[R], uint64_t key) {
-  if (key >= t[R - 1]) return;
-  t[R - 1] = key;
-#pragma unroll
-  for (int i = R - 1; i > 0; --i) {
-    if (t[i] < t[i - 1]) {
-      const uint64_t a = t[i];
-      t[i] = t[i - 1];
-      t[i - 1] = a;
-    }
-  }
-}
 
 // merge sorted lists across the G lanes of a group (butterfly; every lane ends
 // with the group's R smallest keys, ascending).  Bitonic merge per step.
@@ -319,51 +306,6 @@ __device__ __forceinline__ void group_bitonic_sort(uint64_t (&k)[EPT], int g) {
     }
   }
 }
-
-
-// Rolled bitonic sort (ascending) of 32-bit keys held by a lane group (index
-// i = g*EPT + e): the `size` loop is rolled and the in-register strides are
-// five small unrolled helpers, which keeps the code inside the I-cache.
-template <int S, int EPT>
-__device__ __forceinline__ void ce_reg_u32(uint32_t (&k)[EPT], int g, int size) {
-  if (S >= EPT) return;
-#pragma unroll
-  for (int e = 0; e < EPT; ++e) {
-    if (e & S) continue;
-    const int e2 = e | S;
-    const bool asc = ((g * EPT + e) & size) == 0;
-    const uint32_t a = k[e], b = k[e2];
-    const uint32_t mn = min(a, b), mx = max(a, b);
-    k[e] = asc ? mn : mx;
-    k[e2] = asc ? mx : mn;
-  }
-}
-
-template <int P, int EPT>
-__device__ __forceinline__ void group_bitonic_sort_u32(uint32_t (&k)[EPT], int g) {
-#pragma unroll 1
-  for (int size = 2; size <= P; size <<= 1) {
-#pragma unroll 1
-    for (int stride = size >> 1; stride >= EPT; stride >>= 1) {
-      const int m = stride / EPT;
-      const bool lower = (g & m) == 0;
-      const bool asc = ((g * EPT) & size) == 0;
-      const bool keep_min = lower == asc;
-#pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        const uint32_t o = __shfl_xor_sync(FULL, k[e], m);
-        k[e] = keep_min ? min(k[e], o) : max(k[e], o);
-      }
-    }
-    const int half = size >> 1;
-    if (half >= 16) ce_reg_u32<16, EPT>(k, g, size);
-    if (half >= 8) ce_reg_u32<8, EPT>(k, g, size);
-    if (half >= 4) ce_reg_u32<4, EPT>(k, g, size);
-    if (half >= 2) ce_reg_u32<2, EPT>(k, g, size);
-    ce_reg_u32<1, EPT>(k, g, size);
-  }
-}
-
 
 // Bitonic sort v2 (ascending, 32-bit keys, index i = g*EPT + e).  Sizes below
 // EPT have compile-time directions; for sizes >= EPT every lane's elements share
@@ -467,47 +409,6 @@ __device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* sh
   return wbase + x - v;
 }
 
-// ------------------------------------------------------- TMA bulk copies
-// One elected thread streams a contiguous global block into shared memory with
-// cp.async.bulk (TMA, SASS UBLKCP); completion is tracked by an mbarrier's
-// transaction count.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                             uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n LAB_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra LAB_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// bytes must be a multiple of 16, both addresses 16-byte aligned; call from one thread
-__device__ __forceinline__ void tma_load_block(void* dst, const void* src, uint32_t bytes,
-                                               uint64_t* bar) {
-  mbar_expect_tx(bar, bytes);
-  constexpr uint32_t CH = 32768;
-  for (uint32_t o = 0; o < bytes; o += CH)
-    tma_bulk_g2s(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
-                 bytes - o < CH ? bytes - o : CH, bar);
-}
 
 // ------------------------------------------------------------ misc helpers
 __device__ __forceinline__ uint64_t desc_score_key(float s, uint32_t id) {
