@@ -329,6 +329,71 @@ void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint32_t ld
   FPP_LAUNCH();
 }
 
+// Query-batch ordering keys (fpp_query.cu run_query): the table-0 bucket of each
+// row, i.e. the cross-polytope codes of stacks (0, 0) and (0, 1).  Queries with
+// equal keys are processed next to each other, so concurrently scored queries
+// share more candidate rows in L2.  Scheduling only: results are per query.
+template <int P>
+__global__ void __launch_bounds__(256)
+k_order_keys(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, uint32_t K,
+             const uint32_t* __restrict__ signs, uint64_t* __restrict__ out) {
+  using S = FhtShape<P>;
+  constexpr bool TR = P >= 64;
+  constexpr int TS = TR ? TransposeShape<P>::STRIDE : 4;
+  __shared__ __align__(16) float tbuf[(256 / S::G) * TS];
+  const int lane = threadIdx.x & 31;
+  const int g = lane % S::G;
+  float* buf = tbuf + (threadIdx.x / S::G) * TS;
+  const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / S::G;
+  const bool active = gid < n;
+  const uint64_t i = active ? gid : n - 1;
+  uint64_t key = 0;
+  for (uint32_t f = 0; f < K; ++f) {
+    float v[S::EPT];
+    load_row<P>(X + i * d, d, g, v);
+    const uint32_t* sw = signs + (uint64_t)f * 3 * S::W;  // stack (t = 0, f)
+    if constexpr (TR) spinner_project_T<P>(v, sw, g, buf);
+    else spinner_project<P>(v, sw, g);
+    // argmax |p| (lowest index on ties), sign in bit 0
+    uint64_t best = 0;
+#pragma unroll
+    for (int e = 0; e < S::EPT; ++e) {
+      const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * S::EPT + e;
+      if (j < D) {
+        const uint64_t c = ((uint64_t)ord_key(fabsf(v[e])) << 32) |
+                           ((uint64_t)(0x7fffffffu - j) << 1) | (v[e] < 0.0f ? 1u : 0u);
+        best = c > best ? c : best;
+      }
+    }
+#pragma unroll
+    for (int m = 1; m < S::G; m <<= 1) {
+      const uint64_t o = shfl_xor_u64(best, m);
+      best = o > best ? o : best;
+    }
+    const uint32_t j = 0x7fffffffu - ((uint32_t)best >> 1);
+    key = (key << 32) | ((best & 1u) ? D + j : j);
+  }
+  if (active && g == 0) out[i] = key;
+}
+
+void launch_order_keys(const Index& ix, const float* Qd, uint64_t n, uint64_t* out, cudaStream_t s) {
+  if (n == 0) return;
+  const uint32_t P = ix.P;
+  const uint32_t G = P < 32 ? 1 : P / 32;
+  const unsigned blocks = (unsigned)((n * G + 255) / 256);
+#define FPP_ORD_CASE(PP)                                                                      \
+  case PP:                                                                                    \
+    k_order_keys<PP><<<blocks, 256, 0, s>>>(Qd, n, ix.d, ix.prm.D, ix.prm.K, ix.signs, out);  \
+    break;
+  switch (P) {
+    FPP_ORD_CASE(2) FPP_ORD_CASE(4) FPP_ORD_CASE(8) FPP_ORD_CASE(16) FPP_ORD_CASE(32)
+    FPP_ORD_CASE(64) FPP_ORD_CASE(128) FPP_ORD_CASE(256) FPP_ORD_CASE(512) FPP_ORD_CASE(1024)
+    default: fail(FPP_ERR_UNSUPPORTED, "order keys: padded dimension > 1024 not supported on GPU");
+  }
+#undef FPP_ORD_CASE
+  FPP_LAUNCH();
+}
+
 // ------------------------------------------------------------- per-table scan
 constexpr int SCAN_THREADS = 512;
 constexpr int SCAN_PER_THREAD = 8;

@@ -126,6 +126,13 @@ struct Index {
   mutable DBuf<uint32_t> q_ids;
   mutable DBuf<double> q_scores;
   mutable DBuf<fpp_query_stats> q_stats;
+  // batch reordering scratch (run_query)
+  mutable DBuf<uint64_t> ord_key, ord_key2;
+  mutable DBuf<uint32_t> ord_idx, ord_perm, ord_ids;
+  mutable DBuf<float> ord_q;
+  mutable DBuf<double> ord_sc;
+  mutable DBuf<fpp_query_stats> ord_st;
+  mutable DBuf<unsigned char> ord_tmp;
   uint64_t* h_pinned = nullptr;  // small pinned readback
 
   mutable PhaseTimer timer;
@@ -149,6 +156,7 @@ uint64_t content_hash(const float* X, uint64_t n, uint32_t d);
 void save_index(const Index& ix, const char* path, const float* X_host);
 void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint32_t ld, uint64_t* out,
                        cudaStream_t s);
+void launch_order_keys(const Index& ix, const float* Qd, uint64_t n, uint64_t* out, cudaStream_t s);
 void run_brute_force(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t* ids_d,
                      double* scores_d, cudaStream_t s);
 Index* load_index(const char* path, const float* X, bool on_device, uint64_t n, uint32_t d,

@@ -28,6 +28,7 @@
 #include <cstring>
 
 #include <cooperative_groups.h>
+#include <cub/device/device_radix_sort.cuh>
 
 #include "fpp_device.cuh"
 #include "fpp_internal.h"
@@ -1677,9 +1678,9 @@ static uint32_t chunk_size(const Index& ix, uint32_t qprobes, uint64_t nq) {
 // collect + gather/score) on a high-priority one, so the scheduler hands freed
 // SM slots to the bandwidth-bound kernel first and fills the rest with stage A
 // of the next chunk.  Slots alternate; events order slot reuse.
-void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t qprobes,
-               uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s,
-               uint32_t rerank) {
+static void run_query_core(const Index& ix, const float* Qd, uint64_t nq, uint32_t k,
+                           uint32_t qprobes, uint32_t* ids_d, double* scores_d,
+                           fpp_query_stats* stats_d, cudaStream_t s, uint32_t rerank) {
   const uint32_t cs = chunk_size(ix, qprobes, nq);
   const uint64_t nch = (nq + cs - 1) / cs;
   static const bool serial = getenv("FPP_SERIAL") != nullptr;
@@ -1733,6 +1734,76 @@ void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32
   FPP_CUDA(cudaEventRecord(ix.ev_join2, ix.sB));
   FPP_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
   FPP_CUDA(cudaStreamWaitEvent(s, ix.ev_join2, 0));
+}
+
+__global__ void k_iota(uint32_t* __restrict__ p, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    p[i] = (uint32_t)i;
+}
+__global__ void k_gather_rows(const float* __restrict__ Q, const uint32_t* __restrict__ perm,
+                              uint64_t nq, uint32_t d, float* __restrict__ out) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nq * d;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = e / d;
+    out[e] = Q[(uint64_t)perm[i] * d + (e - i * d)];
+  }
+}
+__global__ void k_scatter_results(const uint32_t* __restrict__ perm, uint64_t nq, uint32_t k,
+                                  const uint32_t* __restrict__ ids_p,
+                                  const double* __restrict__ sc_p,
+                                  const fpp_query_stats* __restrict__ st_p, uint32_t* ids,
+                                  double* sc, fpp_query_stats* st) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nq * k;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = e / k, j = e - i * k;
+    const uint64_t o = (uint64_t)perm[i] * k + j;
+    ids[o] = ids_p[e];
+    sc[o] = sc_p[e];
+    if (st && j == 0) st[perm[i]] = st_p[i];
+  }
+}
+
+// Batched query.  Large batches are processed in table-0-bucket order (similar
+// queries adjacent: concurrently scored queries share candidate rows in L2) and
+// the results scattered back to the caller's order; FPP_NO_REORDER=1 keeps the
+// input order.  Results are identical either way (every query is independent).
+void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t qprobes,
+               uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s,
+               uint32_t rerank) {
+  static const bool no_reorder = getenv("FPP_NO_REORDER") != nullptr;
+  if (no_reorder || nq < 1024 || nq >= (1ull << 31)) {
+    run_query_core(ix, Qd, nq, k, qprobes, ids_d, scores_d, stats_d, s, rerank);
+    return;
+  }
+  const uint32_t d = ix.d;
+  ix.ord_key.ensure(nq);
+  ix.ord_key2.ensure(nq);
+  ix.ord_idx.ensure(nq);
+  ix.ord_perm.ensure(nq);
+  ix.ord_q.ensure(nq * d);
+  ix.ord_ids.ensure(nq * k);
+  ix.ord_sc.ensure(nq * k);
+  if (stats_d) ix.ord_st.ensure(nq);
+  const int sms = sm_count();
+  launch_order_keys(ix, Qd, nq, ix.ord_key.p, s);
+  k_iota<<<sms * 4, 256, 0, s>>>(ix.ord_idx.p, nq);
+  FPP_LAUNCH();
+  size_t tmp = 0;
+  FPP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ix.ord_key.p, ix.ord_key2.p, ix.ord_idx.p,
+                                           ix.ord_perm.p, (int)nq, 0, 64, s));
+  ix.ord_tmp.ensure(tmp);
+  FPP_CUDA(cub::DeviceRadixSort::SortPairs(ix.ord_tmp.p, tmp, ix.ord_key.p, ix.ord_key2.p,
+                                           ix.ord_idx.p, ix.ord_perm.p, (int)nq, 0, 64, s));
+  k_gather_rows<<<sms * 8, 256, 0, s>>>(Qd, ix.ord_perm.p, nq, d, ix.ord_q.p);
+  FPP_LAUNCH();
+  run_query_core(ix, ix.ord_q.p, nq, k, qprobes, ix.ord_ids.p, ix.ord_sc.p,
+                 stats_d ? ix.ord_st.p : nullptr, s, rerank);
+  k_scatter_results<<<sms * 4, 256, 0, s>>>(ix.ord_perm.p, nq, k, ix.ord_ids.p, ix.ord_sc.p,
+                                            stats_d ? ix.ord_st.p : nullptr, ids_d, scores_d,
+                                            stats_d);
+  FPP_LAUNCH();
+  ix.acc.launches += 5;  // order keys, iota, sort (counted once), gather, scatter
 }
 
 void query_debug(const Index& ix, const float* qd, uint32_t qprobes, std::vector<uint64_t>& probes,
