@@ -1667,8 +1667,11 @@ static uint32_t chunk_size(const Index& ix, uint32_t qprobes, uint64_t nq) {
   const uint64_t per_q = LKs * 8 + pe * 16 + (4 * pe + 16384) * 8 + 64;
   uint64_t c = (4ull << 30) / per_q;  // ~4 GB of per-chunk scratch per slot
   c = std::max<uint64_t>(1, std::min<uint64_t>(c, 8192));
-  // at least 4 chunks when the batch allows, so the two-stream pipeline overlaps
-  const uint64_t quarter = (nq + 3) / 4;
+  // at least 3 chunks when the batch allows, so the two-stream pipeline overlaps
+  // (C2 sweep: 2 chunks 288k, 3 -> 300k, 4 -> 295k, 6 -> 290k, 8 -> 275k q/s);
+  // FPP_CHUNKS overrides
+  static const int nch_min = getenv("FPP_CHUNKS") ? std::max(1, atoi(getenv("FPP_CHUNKS"))) : 3;
+  const uint64_t quarter = (nq + nch_min - 1) / nch_min;
   if (quarter >= 512) c = std::min(c, quarter);
   return (uint32_t)std::min<uint64_t>(c, nq);
 }
