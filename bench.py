@@ -429,7 +429,13 @@ def main():
     ids_d = torch.empty((nq, K_TOP), dtype=torch.int32, device="cuda")
     sc_d = torch.empty((nq, K_TOP), dtype=torch.float64, device="cuda")
     st_d = torch.empty((nq, 4), dtype=torch.int64, device="cuda")
-    stream = torch.cuda.current_stream().cuda_stream
+    # the queries and every timing event run on one explicit stream: the legacy
+    # default stream (handle 0) would mean "library stream" to the C ABI, and
+    # events on the legacy stream do not order with the library's non-blocking streams
+    torch.cuda.synchronize()
+    qstream = torch.cuda.Stream()
+    torch.cuda.set_stream(qstream)
+    stream = qstream.cuda_stream
 
     def step(qp, stats=None):
         ix.query_device(Qd, ids_d, sc_d, K_TOP, qp, stats=stats, stream=stream)
