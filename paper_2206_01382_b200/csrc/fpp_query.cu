@@ -1036,6 +1036,7 @@ __device__ __forceinline__ void collect_walk(const uint64_t* pp, const uint32_t*
 __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
   extern __shared__ __align__(16) uint32_t sbm[];
   __shared__ uint32_t ucount, qsh, nextc;
+  __shared__ uint32_t scan_sh[32];
   uint32_t* bm = a.gbitmap ? a.gbitmap + (uint64_t)blockIdx.x * a.nwords : sbm;
   for (;;) {
     if (threadIdx.x == 0) {
@@ -1054,19 +1055,42 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
     if (q >= a.nq) break;
     uint32_t* out = a.cands + a.coff[q];
     const uint32_t P = (uint32_t)a.peff;
-    collect_walk(a.ppos + (uint64_t)q * a.peff, a.plen + (uint64_t)q * a.peff, P, a.ids, out,
-                 &ucount,
-                 [&]() {
-                   uint32_t c = 0;
-                   if ((threadIdx.x & 31) == 0) c = smem_fetch_add(&nextc, 1u);
-                   return __shfl_sync(FULL, c, 0);
-                 },
-                 [&](uint32_t id) {
-                   const uint32_t bit = 1u << (id & 31);
-                   return !(atomicOr(bm + (id >> 5), bit) & bit);
-                 });
-    __syncthreads();
-    const uint32_t U = ucount;
+    auto next_chunk = [&]() {
+      uint32_t c = 0;
+      if ((threadIdx.x & 31) == 0) c = smem_fetch_add(&nextc, 1u);
+      return __shfl_sync(FULL, c, 0);
+    };
+    uint32_t U;
+    if (!a.gbitmap) {
+      // shared-memory bitmap: fire-and-forget ORs during the walk, then the set
+      // bits are emitted in ascending id order (a bitmap scan), so every query's
+      // candidate rows are gathered in address order and similar queries scored
+      // side by side touch shared rows at about the same time
+      collect_walk(a.ppos + (uint64_t)q * a.peff, a.plen + (uint64_t)q * a.peff, P, a.ids, out,
+                   &ucount, next_chunk, [&](uint32_t id) {
+                     asm volatile("red.shared.or.b32 [%0], %1;\n" ::"r"(
+                                      (uint32_t)__cvta_generic_to_shared(bm + (id >> 5))),
+                                  "r"(1u << (id & 31))
+                                  : "memory");
+                     return false;
+                   });
+      __syncthreads();
+      const uint32_t per = (a.nwords + blockDim.x - 1) / blockDim.x;
+      const uint32_t w0 = min(a.nwords, threadIdx.x * per), w1 = min(a.nwords, w0 + per);
+      uint32_t cnt = 0;
+      for (uint32_t w = w0; w < w1; ++w) cnt += __popc(sbm[w]);
+      uint32_t pos = block_excl_scan_u32(cnt, scan_sh, &U);
+      for (uint32_t w = w0; w < w1; ++w)
+        for (uint32_t word = sbm[w]; word; word &= word - 1) out[pos++] = w * 32 + (__ffs(word) - 1);
+    } else {
+      collect_walk(a.ppos + (uint64_t)q * a.peff, a.plen + (uint64_t)q * a.peff, P, a.ids, out,
+                   &ucount, next_chunk, [&](uint32_t id) {
+                     const uint32_t bit = 1u << (id & 31);
+                     return !(atomicOr(bm + (id >> 5), bit) & bit);
+                   });
+      __syncthreads();
+      U = ucount;
+    }
     if (threadIdx.x == 0) a.uq[q] = U;
     if (a.gbitmap)
       for (uint32_t c = threadIdx.x; c < U; c += blockDim.x) bm[out[c] >> 5] = 0;
