@@ -1111,8 +1111,8 @@ k_collect_cluster(CollectArgs a, uint32_t slice_words) {
   const uint32_t rank = cluster.block_rank();
   const uint32_t cid = blockIdx.x / CO_CLUSTER, ncl = gridDim.x / CO_CLUSTER;
   extern __shared__ __align__(16) uint32_t sbm[];
-  __shared__ uint32_t ucount, nextc;
-  uint32_t* ucount0 = cluster.map_shared_rank(&ucount, 0);
+  __shared__ uint32_t ucount, nextc, cta_cnt;
+  __shared__ uint32_t scan_sh[32];
   const uint32_t slice_bits = slice_words * 32;
   for (uint32_t q = cid; q < a.nq; q += ncl) {
     for (uint32_t w = threadIdx.x; w < slice_words; w += blockDim.x) sbm[w] = 0;
@@ -1123,8 +1123,9 @@ k_collect_cluster(CollectArgs a, uint32_t slice_words) {
     cluster.sync();
     uint32_t* out = a.cands + a.coff[q];
     const uint32_t P = (uint32_t)a.peff;
+    // DSMEM ORs on the owning CTA's slice (results unused: no append during the walk)
     collect_walk(a.ppos + (uint64_t)q * a.peff, a.plen + (uint64_t)q * a.peff, P, a.ids, out,
-                 ucount0,
+                 &ucount,
                  [&]() {
                    uint32_t c = 0;
                    if ((threadIdx.x & 31) == 0) c = smem_fetch_add(&nextc, 1u);
@@ -1133,11 +1134,33 @@ k_collect_cluster(CollectArgs a, uint32_t slice_words) {
                  [&](uint32_t id) {
                    const uint32_t owner = id / slice_bits, lb = id - owner * slice_bits;
                    uint32_t* rb = cluster.map_shared_rank(sbm, owner);
-                   const uint32_t bit = 1u << (lb & 31);
-                   return !(atomicOr(rb + (lb >> 5), bit) & bit);
+                   atomicOr(rb + (lb >> 5), 1u << (lb & 31));
+                   return false;
                  });
     cluster.sync();
-    if (rank == 0 && threadIdx.x == 0) a.uq[q] = ucount;
+    // ascending-id emission: CTA `rank` owns ids [rank*slice_bits, ...): scan the
+    // slice, prefix over the cluster's CTAs (DSMEM), write at the global offset
+    const uint32_t per = (slice_words + blockDim.x - 1) / blockDim.x;
+    const uint32_t w0 = min(slice_words, threadIdx.x * per), w1 = min(slice_words, w0 + per);
+    uint32_t cnt = 0;
+    for (uint32_t w = w0; w < w1; ++w) cnt += __popc(sbm[w]);
+    uint32_t tot;
+    uint32_t pos = block_excl_scan_u32(cnt, scan_sh, &tot);
+    if (threadIdx.x == 0) cta_cnt = tot;
+    cluster.sync();
+    uint32_t base = 0, all = 0;
+    for (uint32_t r = 0; r < CO_CLUSTER; ++r) {
+      const uint32_t c = *cluster.map_shared_rank(&cta_cnt, r);
+      if (r < rank) base += c;
+      all += c;
+    }
+    pos += base;
+    const uint32_t id0 = rank * slice_bits;
+    for (uint32_t w = w0; w < w1; ++w)
+      for (uint32_t word = sbm[w]; word; word &= word - 1)
+        out[pos++] = id0 + w * 32 + (__ffs(word) - 1);
+    if (rank == 0 && threadIdx.x == 0) a.uq[q] = all;
+    cluster.sync();  // slices and cta_cnt are reused by the next query
   }
 }
 
