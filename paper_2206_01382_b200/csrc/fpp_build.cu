@@ -329,8 +329,8 @@ void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint32_t ld
   FPP_LAUNCH();
 }
 
-// Query-batch ordering keys (fpp_query.cu run_query): the table-0 bucket of each
-// row, i.e. the cross-polytope codes of stacks (0, 0) and (0, 1).  Queries with
+// Query-batch ordering keys (fpp_query.cu run_query): the cross-polytope code of
+// stack (0, 0) of each row (the first half of its table-0 bucket).  Queries with
 // equal keys are processed next to each other, so concurrently scored queries
 // share more candidate rows in L2.  Scheduling only: results are per query.
 template <int P>
@@ -383,7 +383,7 @@ void launch_order_keys(const Index& ix, const float* Qd, uint64_t n, uint64_t* o
   const unsigned blocks = (unsigned)((n * G + 255) / 256);
 #define FPP_ORD_CASE(PP)                                                                      \
   case PP:                                                                                    \
-    k_order_keys<PP><<<blocks, 256, 0, s>>>(Qd, n, ix.d, ix.prm.D, ix.prm.K, ix.signs, out);  \
+    k_order_keys<PP><<<blocks, 256, 0, s>>>(Qd, n, ix.d, ix.prm.D, 1u, ix.signs, out);        \
     break;
   switch (P) {
     FPP_ORD_CASE(2) FPP_ORD_CASE(4) FPP_ORD_CASE(8) FPP_ORD_CASE(16) FPP_ORD_CASE(32)

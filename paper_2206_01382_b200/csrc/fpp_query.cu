@@ -1814,10 +1814,13 @@ __global__ void k_scatter_results(const uint32_t* __restrict__ perm, uint64_t nq
   }
 }
 
-// Batched query.  Large batches are processed in table-0-bucket order (similar
-// queries adjacent: concurrently scored queries share candidate rows in L2) and
-// the results scattered back to the caller's order; FPP_NO_REORDER=1 keeps the
-// input order.  Results are identical either way (every query is independent).
+// Batched query.  Large batches are processed ordered by the cross-polytope code
+// of stack (0, 0) (similar queries adjacent; the sort is stable): with the
+// ascending-id candidate lists, concurrently scored queries then gather shared
+// rows through L2 (C2: +8% over input order; the full table-0 bucket or the
+// SimHash signature as key group less well).  Results are scattered back to
+// the caller's order; FPP_NO_REORDER=1 keeps the input order.  Results are
+// identical either way (every query is independent).
 void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t qprobes,
                uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s,
                uint32_t rerank) {
@@ -1841,10 +1844,10 @@ void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32
   FPP_LAUNCH();
   size_t tmp = 0;
   FPP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ix.ord_key.p, ix.ord_key2.p, ix.ord_idx.p,
-                                           ix.ord_perm.p, (int)nq, 0, 64, s));
+                                           ix.ord_perm.p, (int)nq, 0, 32, s));
   ix.ord_tmp.ensure(tmp);
   FPP_CUDA(cub::DeviceRadixSort::SortPairs(ix.ord_tmp.p, tmp, ix.ord_key.p, ix.ord_key2.p,
-                                           ix.ord_idx.p, ix.ord_perm.p, (int)nq, 0, 64, s));
+                                           ix.ord_idx.p, ix.ord_perm.p, (int)nq, 0, 32, s));
   k_gather_rows<<<sms * 8, 256, 0, s>>>(Qd, ix.ord_perm.p, nq, d, ix.ord_q.p);
   FPP_LAUNCH();
   run_query_core(ix, ix.ord_q.p, nq, k, qprobes, ix.ord_ids.p, ix.ord_sc.p,
