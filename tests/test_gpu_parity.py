@@ -435,12 +435,12 @@ def test_centering_parity(fpp, orc, tmp_path):
 
 
 def test_large_batch_reordered_equals_oracle(fpp, orc):
-    # batches >= 1024 queries run in table-0-bucket order and are scattered back:
-    # results (ids, scores, stats) must be exactly the per-query oracle answers
-    X = data(fpp, 8000, 64, 30, 0.3, seed=21)
-    Q = data(fpp, 1100, 64, 30, 0.3, seed=21, stream=1)
-    ix = fpp.Index.build(X, L=4, K=2, D=64, iProbes=3, alpha=0.1)
-    ox = orc.Index(X, L=4, K=2, D=64, iprobes=3, alpha=0.1)
+    # batches with nq >= 256 and nq*d >= 512k run in stack-(0,0)-code order and are
+    # scattered back: results (ids, scores, stats) must be the per-query oracle answers
+    X = data(fpp, 6000, 480, 30, 0.3, seed=21)
+    Q = data(fpp, 1100, 480, 30, 0.3, seed=21, stream=1)
+    ix = fpp.Index.build(X, L=4, K=2, D=512, iProbes=3, alpha=0.1)
+    ox = orc.Index(X, L=4, K=2, D=512, iprobes=3, alpha=0.1)
     for rr in (0, 50):
         gi, gs, gst = ix.query(Q, 10, 200, return_stats=True, rerank=rr)
         oi, os_, ost = ox.query(Q, 10, 200, rerank=rr)
