@@ -1256,9 +1256,7 @@ k_screen(const uint32_t* __restrict__ cands, const uint64_t* __restrict__ coff,
 #endif
 constexpr int SC_WARPS = FPP_SC_WARPS;
 // Ring geometry <SL, ST>: SL floats per row slice (a multiple of 32), ST stages
-// per warp.  Wide rows use 96-float slices x 2 stages (longer contiguous runs
-// per row per request, measurably better DRAM efficiency on random row
-// gathers); narrow rows (d < 192) use 32 x 4, whose slice matches the row.
+// per warp (chosen per row width at launch, see stage_b).
 template <int SL>
 struct ScRing {
   static constexpr int ROWPAD = SL + 4;  // odd number of 16 B units: conflict-free LDS.128
@@ -1328,8 +1326,8 @@ __device__ __forceinline__ void topk_insert(double& bs, uint32_t& bi, uint32_t k
 // chunk (l & 7) of rows (l >> 3) + 4*it, it = 0..7, with row addresses resolved
 // once per batch, so a slice costs 8 cp.async per lane.  Lane r then folds row
 // r's slice into its fp64 accumulator in the reference's sequential order.
-template <bool VEC, int SC_SLICE, int SC_STAGES>
-__global__ void __launch_bounds__(SC_WARPS * 32, 2) k_score(ScoreArgs a) {
+template <bool VEC, int SC_SLICE, int SC_STAGES, int MINB = 2>
+__global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
   constexpr int SC_ROWPAD = ScRing<SC_SLICE>::ROWPAD;
   constexpr int SC_STAGE_FLOATS = ScRing<SC_SLICE>::STAGE_FLOATS;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -1694,12 +1692,15 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     kern<<<nqc, SC_WARPS * 32, sm, st>>>(sa);
   };
-  const bool wide = ix.d >= 192;
+  // ring geometry: 64-float slices x 2 stages, 3 CTAs per SM for d >= 64 (with the
+  // ascending-id candidate lists more queries in flight share more rows in L2:
+  // C2 96x2 @ 2/SM 344k -> 64x2 @ 3/SM 352k q/s; C4 +5%); 32 x 4 below
+  const bool wide = ix.d >= 64;
   if ((ix.d & 3u) == 0) {
-    if (wide) launch_score(k_score<true, 96, 2>, 96, 2);
+    if (wide) launch_score(k_score<true, 64, 2, 3>, 64, 2);
     else launch_score(k_score<true, 32, 4>, 32, 4);
   } else {
-    if (wide) launch_score(k_score<false, 96, 2>, 96, 2);
+    if (wide) launch_score(k_score<false, 64, 2, 3>, 64, 2);
     else launch_score(k_score<false, 32, 4>, 32, 4);
   }
   FPP_LAUNCH();
