@@ -87,6 +87,7 @@ Index::~Index() {
   dfree(X);
   dfree(signs);
   dfree(sigs);
+  dfree(xtail);
   dfree(offsets);
   dfree(table_base);
   dfree(ids);
@@ -208,6 +209,43 @@ __global__ void k_center_sub(float* __restrict__ X, uint64_t n, uint32_t d, uint
   }
 }
 
+// Row tail norms (score-gather early termination, fpp_query.cu k_score_pruned):
+// warp per row; fp64 sums of exact squares per segment, suffix-combined; sqrt
+// rounded up to fp32 (with a 1e-12 relative margin for the summation error).
+__global__ void k_tail_norms(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx,
+                             uint32_t nt, float* __restrict__ xt) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+    const float* r = X + i * ldx;
+    double seg[XT_MAX] = {0.0, 0.0, 0.0, 0.0};
+    for (uint32_t c = XT_SLICE + lane; c < d; c += 32) {
+      const uint32_t j = min(c / XT_SLICE - 1, nt - 1);
+      const double v = (double)r[c];
+#pragma unroll
+      for (uint32_t t = 0; t < XT_MAX; ++t)
+        if (t == j) seg[t] = fma(v, v, seg[t]);
+    }
+    double suf = 0.0;
+#pragma unroll
+    for (int t = XT_MAX - 1; t >= 0; --t) {
+      double v = seg[t];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      suf += v;
+      if (lane == 0 && t < (int)nt) xt[(uint64_t)t * n + i] = __double2float_ru(__dsqrt_ru(suf) * (1.0 + 1e-12));
+    }
+  }
+}
+
+void launch_tail_norms(Index& ix) {
+  const uint32_t nsl = (ix.d + XT_SLICE - 1) / XT_SLICE;
+  ix.xt_n = ix.d >= XT_SLICE ? std::min<uint32_t>(nsl - 1, XT_MAX) : 0;
+  if (!ix.xt_n) return;
+  ix.xtail = static_cast<float*>(dmalloc((size_t)ix.xt_n * ix.n * sizeof(float)));
+  k_tail_norms<<<sm_count() * 8, 256, 0, ix.stream>>>(ix.X, ix.n, ix.d, ix.ldx, ix.xt_n, ix.xtail);
+  FPP_LAUNCH();
+}
+
 __global__ void k_check_finite(const float* __restrict__ X, uint64_t cnt, unsigned long long* bad) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -324,6 +362,7 @@ Index* prepare_index(const float* X, bool on_device, uint64_t n, uint32_t d, con
     // SimHash signatures of every point (rerank screening; n x 8 B)
     ix->sigs = static_cast<uint64_t*>(dmalloc(n * sizeof(uint64_t) + 8));
     launch_signatures(*ix, ix->X, n, ix->ldx, ix->sigs, ix->stream);
+    launch_tail_norms(*ix);
     FPP_CUDA(cudaStreamSynchronize(ix->stream));
   } catch (...) {
     delete ix;

@@ -87,6 +87,10 @@ struct Index {
   uint32_t max_bucket = 0;
   uint64_t sign_words = 0;
   uint64_t* sigs = nullptr;  // [n] SimHash signatures (rerank screening)
+  // Row tail norms for exact early termination in the score gather: xtail[j][i] =
+  // ||X[i][(j+1)*XT_SLICE:d)||, rounded up to fp32, checkpoints j < xt_n
+  float* xtail = nullptr;
+  uint32_t xt_n = 0;
   std::vector<float> center;  // [d] when prm.centering (dataset.cpp center())
   uint64_t device_bytes = 0;
   ShardState* shard = nullptr;  // global-filter sharded build in progress
@@ -156,6 +160,9 @@ uint64_t content_hash(const float* X, uint64_t n, uint32_t d);
 void save_index(const Index& ix, const char* path, const float* X_host);
 void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint32_t ld, uint64_t* out,
                        cudaStream_t s);
+constexpr uint32_t XT_SLICE = 64;  // = the score ring's row-slice width for d >= 64
+constexpr uint32_t XT_MAX = 4;     // tail-norm checkpoints per row
+void launch_tail_norms(Index& ix);
 void launch_order_keys(const Index& ix, const float* Qd, uint64_t n, uint64_t* out, cudaStream_t s);
 void run_brute_force(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t* ids_d,
                      double* scores_d, cudaStream_t s);

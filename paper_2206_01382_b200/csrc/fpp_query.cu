@@ -1280,6 +1280,12 @@ struct ScoreArgs {
   fpp_query_stats* stats;
   const uint32_t* uq_all;  // collected candidates per query (stats); nullptr: = uq
   uint32_t cstride;        // != 0: candidates of query q start at q * cstride (screened lists)
+  uint32_t* qctr;          // != nullptr: persistent grid, queries fetched from this counter
+  uint32_t nq;
+  const float* xtail;      // k_score_pruned: row tail norms [xt_n][n] (Index::xtail)
+  uint32_t xt_n;
+  uint64_t n;
+  unsigned long long* dbg;  // FPP_DEBUG_PRUNE: [rows, row slices read]
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1337,8 +1343,16 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
   float* ring = reinterpret_cast<float*>(smraw + qd_bytes);
   __shared__ double mg_s[SC_WARPS][32];
   __shared__ uint32_t mg_i[SC_WARPS][32];
-  const uint32_t q = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ uint32_t q_sh;
+  uint32_t q = blockIdx.x;
+  for (;;) {
+  if (a.qctr) {  // persistent grid: dynamic query fetch
+    if (threadIdx.x == 0) q_sh = atomicAdd(a.qctr, 1u);
+    __syncthreads();
+    q = q_sh;
+    if (q >= a.nq) return;
+  }
   for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) qd[j] = (double)a.Q[(uint64_t)q * d + j];
   __syncthreads();
   const uint32_t U = a.uq[q];
@@ -1457,6 +1471,270 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
       a.stats[q].candidates = a.uq_all ? a.uq_all[q] : U;
       a.stats[q].exact = U;
     }
+  }
+  if (!a.qctr) return;
+  __syncthreads();  // qd, mg_* and q_sh are reused by the next query
+  }
+}
+
+// Exact early termination of the row gather (results identical to k_score).
+// Rows are read as 64-float slices.  Each candidate's first slice (its head) is
+// read and summed; lane r then bounds row r's final score by Cauchy-Schwarz,
+//   S <= s_m + ||x[m:d)|| * ||q[m:d)||   (+1e-10 relative: fp64 summation error),
+// where s_m is the sequential fp64 prefix after m columns (the very value the full
+// sum continues from) and ||x[m:d)|| the index's rounded-up tail norm
+// (Index::xtail).  A row whose bound is below the CTA's running k-th best score
+// (max over the warps' lists; each is the k-th best of distinct candidates, so a
+// lower bound of the final one) ends strictly below the final k-th best: it cannot
+// enter the top-k and its tail is never read.  Survivors (id, s_m) go to a per-warp
+// queue in shared memory and are finished 32 at a time as dense tail batches, with
+// the same check after each of the first xt_n slices.  Jobs (a head slice of 32
+// candidates, a tail slice of 32 survivors, or a bubble) run through a 2-stage
+// cp.async ring; the next job is chosen when it is issued, one job ahead of the
+// compute.  Ring rows are XOR-swizzled in 16 B chunks (conflict-free LDS.128
+// without padding).
+template <bool VEC, int MINB>
+__global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score_pruned(ScoreArgs a) {
+  static_assert(SC_WARPS == 4, "thr_s reduction assumes 4 warps");
+  constexpr int SL = (int)XT_SLICE;
+  constexpr int STAGE = 32 * SL;
+  constexpr uint32_t NONE = 0xffffffffu, QCAP = 128;
+  constexpr uint32_t J_NOP = 0, J_HEAD = 1, J_TAIL = 2, J_END = 3;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const uint32_t d = a.d;
+  double* qd = reinterpret_cast<double*>(smraw);
+  const uint32_t qd_bytes = ((d * 8 + 127) / 128) * 128;
+  float* ring = reinterpret_cast<float*>(smraw + qd_bytes);
+  __shared__ double qt_s[XT_MAX];
+  __shared__ double thr_s[SC_WARPS];
+  __shared__ uint32_t q_sh;
+  __shared__ double sq_acc[SC_WARPS][QCAP];  // survivor queue: prefix sums
+  __shared__ uint32_t sq_id[SC_WARPS][QCAP];  //                 and ids
+  volatile double* thr_v = thr_s;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int kk = lane & 7, rbase = lane >> 3;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const uint32_t nsl = (d + SL - 1) / SL;  // >= 2 (host: d > 64)
+  const uint32_t nt = a.xt_n;              // checks after slices 0 .. nt-1 (nt < nsl)
+  float* wring = ring + (size_t)w * 2 * STAGE;
+  double* qacc = sq_acc[w];
+  uint32_t* qid = sq_id[w];
+  uint32_t q = blockIdx.x;
+  for (;;) {
+    if (a.qctr) {
+      if (threadIdx.x == 0) q_sh = atomicAdd(a.qctr, 1u);
+      __syncthreads();
+      q = q_sh;
+      if (q >= a.nq) return;
+    }
+    for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) qd[j] = (double)a.Q[(uint64_t)q * d + j];
+    if (threadIdx.x < SC_WARPS) thr_s[threadIdx.x] = -INFINITY;
+    __syncthreads();
+    if ((uint32_t)w < nt) {  // query tail norms, rounded up
+      double sq = 0.0;
+      for (uint32_t c = (w + 1) * SL + lane; c < d; c += 32) sq = fma(qd[c], qd[c], sq);
+      for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(FULL, sq, o);
+      if (lane == 0) qt_s[w] = __dsqrt_ru(sq) * (1.0 + 1e-12);
+    }
+    __syncthreads();
+    const uint32_t U = a.uq[q];
+    const uint32_t* cand = a.cands + (a.cstride ? (uint64_t)q * a.cstride : a.coff[q]);
+    const uint32_t k = a.k;
+    double bs = -INFINITY;
+    uint32_t bi = NONE;
+    const uint32_t nb = (U + 31) / 32;
+    const uint32_t nbw = nb > (uint32_t)w ? (nb - w + SC_WARPS - 1) / SC_WARPS : 0;
+    // issue side: next head, tail batch in progress (next slice tis, 0 = none), queue head
+    uint32_t hb = 0, tis = 0, tbase = 0, tcnt = 0, qh = 0, nissued = 0, tgen = 0;
+    // written by the compute side, read by the issue side
+    uint32_t qtl = 0, hdone = 0, tmask = FULL;
+    // job hand-over (issue -> compute), by job parity: descriptor, row id, tail norm
+    uint32_t jd0 = J_END, jd1 = J_END, jid0 = NONE, jid1 = NONE;
+    float jx0 = 0.f, jx1 = 0.f;
+    auto issue = [&]() {
+      uint32_t type, s = 0, m = FULL, jid = NONE;
+      float jx = 0.f;
+      if (tis && tmask == 0) tis = 0;  // every row of the tail batch is out
+      if (tis) {
+        type = J_TAIL;
+        s = tis;
+        m = tmask;
+        tis = s + 1 < nsl ? s + 1 : 0;
+      } else if (qtl - qh >= 32 || (hb == nbw && hdone == nbw && qtl != qh)) {
+        type = J_TAIL;  // a new tail batch (the last one may be partial)
+        s = 1;
+        tbase = qh;
+        tcnt = min(qtl - qh, 32u);
+        qh += tcnt;
+        tmask = FULL;
+        ++tgen;
+        tis = nsl > 2 ? 2 : 0;
+        jid = (uint32_t)lane < tcnt ? qid[(tbase + lane) & (QCAP - 1)] : NONE;
+        if (jid != NONE && nt > 1) jx = __ldg(a.xtail + a.n + jid);
+      } else if (hb < nbw) {
+        type = J_HEAD;
+        const uint32_t ci = (w + hb * SC_WARPS) * 32 + lane;
+        jid = ci < U ? __ldg(cand + ci) : NONE;
+        if (jid != NONE) jx = __ldg(a.xtail + jid);
+        ++hb;
+      } else {
+        type = hdone < nbw ? J_NOP : J_END;
+      }
+      if ((type == J_HEAD || type == J_TAIL) && m) {
+        float* buf = wring + (size_t)(nissued & 1u) * STAGE;
+        const uint32_t col0 = s * SL;
+        const uint32_t len = min((uint32_t)SL, d - col0);
+        if (a.dbg) {
+          const uint32_t rows = type == J_HEAD ? __ballot_sync(FULL, jid != NONE)
+                                               : (tcnt == 32 ? FULL : (1u << tcnt) - 1u);
+          if (lane == 0) {
+            if (type == J_HEAD) atomicAdd(a.dbg, (unsigned long long)__popc(rows));
+            atomicAdd(a.dbg + 1, (unsigned long long)__popc(rows & m));
+          }
+        }
+        if (VEC) {
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int rr = rbase + 4 * it;
+            const uint32_t idr = type == J_HEAD
+                                     ? __shfl_sync(FULL, jid, rr)
+                                     : ((uint32_t)rr < tcnt ? qid[(tbase + rr) & (QCAP - 1)] : NONE);
+            if (idr != NONE && ((m >> rr) & 1u)) {
+              const float* src = a.X + (uint64_t)idr * a.ldx + col0;
+              float* dst = buf + rr * SL;
+#pragma unroll
+              for (int h = 0; h < SL / 32; ++h) {
+                const uint32_t ch = kk + 8 * h;
+                if (ch < (len >> 2)) cp_async16(dst + ((ch ^ (rr & 15)) << 2), src + ch * 4);
+              }
+            }
+          }
+        } else {
+          for (int r = 0; r < 32; ++r) {
+            const uint32_t idr = type == J_HEAD
+                                     ? __shfl_sync(FULL, jid, r)
+                                     : ((uint32_t)r < tcnt ? qid[(tbase + r) & (QCAP - 1)] : NONE);
+            if (idr != NONE && ((m >> r) & 1u))
+              for (uint32_t c = lane; c < len; c += 32)
+                cp_async4(buf + r * SL + ((((c >> 2) ^ (r & 15))) << 2) + (c & 3),
+                          a.X + (uint64_t)idr * a.ldx + col0 + c);
+          }
+        }
+      }
+      const uint32_t desc = type << 30 | (tgen & 1u) << 29 | s << 24 | (tbase & (QCAP - 1)) | tcnt << 8;
+      if (nissued & 1u) { jd1 = desc; jid1 = jid; jx1 = jx; }
+      else { jd0 = desc; jid0 = jid; jx0 = jx; }
+      cp_commit();
+      ++nissued;
+    };
+    // compute side: the tail batch in progress
+    double tacc = 0.0;
+    uint32_t ctid = NONE;
+    bool tlive = false;
+    float txn = 0.f;
+    issue();
+    for (uint32_t ncomp = 0;; ++ncomp) {
+      issue();
+      cp_wait<1>();
+      __syncwarp();
+      const bool p = ncomp & 1u;
+      const uint32_t desc = p ? jd1 : jd0;
+      const uint32_t type = desc >> 30;
+      if (type == J_END) break;
+      if (type == J_NOP) continue;
+      const uint32_t s = (desc >> 24) & 31u;
+      const float* row = wring + (size_t)p * STAGE + lane * SL;
+      const uint32_t col0 = s * SL;
+      const uint32_t len = min((uint32_t)SL, d - col0);
+      const double* qq = qd + col0;
+      const int sw = lane & 15;
+      // dataset.cpp:67 acc += double(a[i]) * double(b[i]), sequential i (exact products)
+      auto fold = [&](double acc) {
+        if (VEC && len == SL) {
+#pragma unroll
+          for (int j = 0; j < SL; j += 4) {
+            const float4 xv = *reinterpret_cast<const float4*>(row + (((j >> 2) ^ sw) << 2));
+            acc = fma((double)xv.x, qq[j], acc);
+            acc = fma((double)xv.y, qq[j + 1], acc);
+            acc = fma((double)xv.z, qq[j + 2], acc);
+            acc = fma((double)xv.w, qq[j + 3], acc);
+          }
+        } else {
+          for (uint32_t j = 0; j < len; ++j)
+            acc = fma((double)row[(((j >> 2) ^ sw) << 2) + (j & 3)], qq[j], acc);
+        }
+        return acc;
+      };
+      const double thr = fmax(fmax(thr_v[0], thr_v[1]), fmax(thr_v[2], thr_v[3]));
+      if (type == J_HEAD) {
+        const uint32_t id = p ? jid1 : jid0;
+        const double acc = fold(0.0);
+        bool live = id != NONE;
+        const double T = (double)(p ? jx1 : jx0) * qt_s[0];
+        if (live && acc + T + 1e-10 * (fabs(acc) + T) < thr) live = false;
+        const uint32_t bal = __ballot_sync(FULL, live);
+        if (live) {
+          const uint32_t pos = (qtl + __popc(bal & lt_mask)) & (QCAP - 1);
+          qid[pos] = id;
+          qacc[pos] = acc;
+        }
+        qtl += __popc(bal);
+        ++hdone;
+        __syncwarp();
+      } else {  // tail slice s of the batch at queue slots tbase' .. tbase' + tcnt' - 1
+        if (s == 1) {
+          const uint32_t b0 = desc & (QCAP - 1), c0 = (desc >> 8) & 63u;
+          ctid = p ? jid1 : jid0;
+          tacc = (uint32_t)lane < c0 ? qacc[(b0 + lane) & (QCAP - 1)] : 0.0;
+          tlive = ctid != NONE;
+          txn = p ? jx1 : jx0;
+        }
+        if (tmask) tacc = fold(tacc);
+        if (s < nt) {
+          if (tlive) {
+            const double T = (double)txn * qt_s[s];
+            if (tacc + T + 1e-10 * (fabs(tacc) + T) < thr) tlive = false;
+            if (tlive && s + 1 < nt) txn = __ldg(a.xtail + (uint64_t)(s + 1) * a.n + ctid);
+          }
+          const uint32_t nm = __ballot_sync(FULL, tlive);
+          // a batch aborted by the issue side may still finish an in-flight slice
+          // after the next batch started: only the current batch owns tmask
+          if (((desc >> 29) & 1u) == (tgen & 1u)) tmask = nm;
+        }
+        if (s + 1 == nsl) {  // batch done: rows still live enter the warp top-k
+          topk_insert(bs, bi, k, tacc, ctid, tlive);
+          const uint32_t wi = __shfl_sync(FULL, bi, k - 1);
+          const double ws = __shfl_sync(FULL, bs, k - 1);
+          if (lane == 0 && wi != NONE) thr_v[w] = ws;
+        }
+      }
+    }
+    cp_wait<0>();
+    __syncthreads();  // the ring is reused for the CTA merge
+    double* mg_s = reinterpret_cast<double*>(ring);
+    uint32_t* mg_i = reinterpret_cast<uint32_t*>(ring + 2 * SC_WARPS * 32);
+    mg_s[w * 32 + lane] = bs;
+    mg_i[w * 32 + lane] = bi;
+    __syncthreads();
+    if (w == 0) {
+      for (int w2 = 1; w2 < SC_WARPS; ++w2) {
+        const bool valid = (uint32_t)lane < k && mg_i[w2 * 32 + lane] != NONE;
+        topk_insert(bs, bi, k, mg_s[w2 * 32 + lane], mg_i[w2 * 32 + lane], valid);
+      }
+      if ((uint32_t)lane < k) {
+        const bool ok = bi != NONE;
+        a.out_ids[(uint64_t)q * k + lane] = ok ? bi + a.id_offset : NONE;
+        a.out_scores[(uint64_t)q * k + lane] = ok ? bs : -INFINITY;
+      }
+      if (lane == 0 && a.stats) {
+        a.stats[q].probes = a.peff;
+        a.stats[q].entries = a.eq[q];
+        a.stats[q].candidates = a.uq_all ? a.uq_all[q] : U;
+        a.stats[q].exact = U;
+      }
+    }
+    __syncthreads();  // mg_* (ring), qd, thr_s are reused by the next query
+    if (!a.qctr) return;
   }
 }
 
@@ -1687,16 +1965,62 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     sa.uq_all = sl.uq.p;
     sa.cstride = rerank;
   }
-  auto launch_score = [&](auto kern, int sl, int stg) {
-    const size_t sm = score_smem(ix.d, sl, stg);
+  // FPP_SC_CTAS=c: persistent grid of c CTAs per SM fetching queries from a counter,
+  // so the remaining SM resources stay free for the next chunk's stage A
+  static const int sc_ctas = getenv("FPP_SC_CTAS") ? atoi(getenv("FPP_SC_CTAS")) : 0;
+  sa.nq = nqc;
+  auto launch_score = [&](auto kern, int slice, int stg) {
+    const size_t sm = score_smem(ix.d, slice, stg);
     FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    kern<<<nqc, SC_WARPS * 32, sm, st>>>(sa);
+    unsigned grid = nqc;
+    if (sc_ctas > 0 && (uint64_t)sm_count() * sc_ctas < nqc) {
+      grid = (unsigned)(sm_count() * sc_ctas);
+      sa.qctr = sl.counter.p + 1;
+      FPP_CUDA(cudaMemsetAsync(sa.qctr, 0, sizeof(uint32_t), st));
+    }
+    kern<<<grid, SC_WARPS * 32, sm, st>>>(sa);
   };
   // ring geometry: 64-float slices x 2 stages, 3 CTAs per SM for d >= 64 (with the
   // ascending-id candidate lists more queries in flight share more rows in L2:
   // C2 96x2 @ 2/SM 344k -> 64x2 @ 3/SM 352k q/s; C4 +5%); 32 x 4 below
   const bool wide = ix.d >= 64;
-  if ((ix.d & 3u) == 0) {
+  // exact early termination (k_score_pruned) whenever the index has tail norms
+  // (d > 64); FPP_NO_PRUNE=1 reads every candidate row in full
+  const bool no_prune = getenv("FPP_NO_PRUNE") != nullptr;
+  if (ix.xt_n && !no_prune) {
+    sa.xtail = ix.xtail;
+    sa.xt_n = ix.xt_n;
+    sa.n = ix.n;
+    const bool dbg = getenv("FPP_DEBUG_PRUNE") != nullptr;
+    DBuf<unsigned long long> dbuf;
+    if (dbg) {
+      dbuf.alloc(2);
+      FPP_CUDA(cudaMemsetAsync(dbuf.p, 0, 16, st));
+      sa.dbg = dbuf.p;
+    }
+    // swizzled ring without row padding: qd + 4 warps x 2 stages x 32 rows x 64 floats
+    auto launch_pruned = [&](auto kern) {
+      const size_t sm = ((ix.d * 8 + 127) / 128) * 128 + (size_t)SC_WARPS * 2 * 32 * XT_SLICE * 4;
+      FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      unsigned grid = nqc;
+      if (sc_ctas > 0 && (uint64_t)sm_count() * sc_ctas < nqc) {
+        grid = (unsigned)(sm_count() * sc_ctas);
+        sa.qctr = sl.counter.p + 1;
+        FPP_CUDA(cudaMemsetAsync(sa.qctr, 0, sizeof(uint32_t), st));
+      }
+      kern<<<grid, SC_WARPS * 32, sm, st>>>(sa);
+    };
+    if ((ix.d & 3u) == 0) launch_pruned(k_score_pruned<true, 3>);
+    else launch_pruned(k_score_pruned<false, 3>);
+    if (dbg) {
+      unsigned long long h[2];
+      FPP_CUDA(cudaMemcpyAsync(h, dbuf.p, 16, cudaMemcpyDeviceToHost, st));
+      FPP_CUDA(cudaStreamSynchronize(st));
+      const double nsl = (double)((ix.d + XT_SLICE - 1) / XT_SLICE);
+      fprintf(stderr, "[prune dbg] rows %llu, slices read per row %.3f of %.0f (%.1f%% of row bytes)\n",
+              h[0], h[0] ? (double)h[1] / h[0] : 0.0, nsl, h[0] ? 100.0 * h[1] / h[0] / nsl : 0.0);
+    }
+  } else if ((ix.d & 3u) == 0) {
     if (wide) launch_score(k_score<true, 64, 2, 3>, 64, 2);
     else launch_score(k_score<true, 32, 4>, 32, 4);
   } else {
