@@ -101,6 +101,9 @@ Index::~Index() {
   if (sB) cudaStreamDestroy(sB);
   q_in.release(); q_ids.release(); q_scores.release(); q_stats.release();
   if (h_pinned) cudaFreeHost(h_pinned);
+  if (prune_h) cudaFreeHost(prune_h);
+  if (prune_ev) cudaEventDestroy(prune_ev);
+  prune_d.release();
   if (stream) cudaStreamDestroy(stream);
   cudaSetDevice(cur);
 }

@@ -138,6 +138,14 @@ struct Index {
   mutable DBuf<fpp_query_stats> ord_st;
   mutable DBuf<unsigned char> ord_tmp;
   uint64_t* h_pinned = nullptr;  // small pinned readback
+  // score-gather early termination (k_score_pruned): measured fraction of row slices
+  // read, probed on the first chunks and every PRUNE_REPROBE-th chunk after
+  mutable double prune_frac = -1.0;
+  mutable uint64_t prune_chunks = 0;
+  mutable bool prune_pending = false;
+  mutable unsigned long long* prune_h = nullptr;  // pinned [2]: rows, row slices read
+  mutable DBuf<unsigned long long> prune_d;
+  mutable cudaEvent_t prune_ev = nullptr;
 
   mutable PhaseTimer timer;
   mutable fpp_timings acc{};

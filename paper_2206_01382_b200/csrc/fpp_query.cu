@@ -1478,7 +1478,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
 }
 
 // Exact early termination of the row gather (results identical to k_score).
-// Rows are read as 64-float slices.  Each candidate's first slice (its head) is
+// Rows are read as 64-float slices.  Every candidate's first slice (its head) is
 // read and summed; lane r then bounds row r's final score by Cauchy-Schwarz,
 //   S <= s_m + ||x[m:d)|| * ||q[m:d)||   (+1e-10 relative: fp64 summation error),
 // where s_m is the sequential fp64 prefix after m columns (the very value the full
@@ -1489,34 +1489,48 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
 // enter the top-k and its tail is never read.  Survivors (id, s_m) go to a per-warp
 // queue in shared memory and are finished 32 at a time as dense tail batches, with
 // the same check after each of the first xt_n slices.  Jobs (a head slice of 32
-// candidates, a tail slice of 32 survivors, or a bubble) run through a 2-stage
-// cp.async ring; the next job is chosen when it is issued, one job ahead of the
-// compute.  Ring rows are XOR-swizzled in 16 B chunks (conflict-free LDS.128
-// without padding).
-template <bool VEC, int MINB>
-__global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score_pruned(ScoreArgs a) {
-  static_assert(SC_WARPS == 4, "thr_s reduction assumes 4 warps");
-  constexpr int SL = (int)XT_SLICE;
-  constexpr int STAGE = 32 * SL;
-  constexpr uint32_t NONE = 0xffffffffu, QCAP = 128;
+// candidates, a tail slice of 32 survivors, or a bubble) run through an ST-stage
+// cp.async ring per warp (ST-1 jobs in flight); the next job is chosen when it is
+// issued and handed to the compute side through shared memory.  Ring rows are
+// XOR-swizzled in 16 B chunks (conflict-free LDS.128 without padding).  Whether the
+// bound pays is data dependent (cluster structure): the host measures the read
+// fraction and falls back to k_score where it does not (stage_b).
+template <int NW, int ST>
+struct PrunedCfg {
+  static constexpr int SL = (int)XT_SLICE;
+  static constexpr int STAGE = 32 * SL;                 // floats per ring stage
+  static constexpr uint32_t QCAP = 32u * (ST + 2);      // >= 31 + 32 (ST - 1) + 64
+  static constexpr size_t ring_bytes = (size_t)NW * ST * STAGE * 4;
+};
+template <bool VEC, int NW, int ST, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
+  using C = PrunedCfg<NW, ST>;
+  constexpr int SL = C::SL;
+  constexpr int STAGE = C::STAGE;
+  constexpr uint32_t QCAP = C::QCAP;
+  constexpr uint32_t NONE = 0xffffffffu, TNONE = 0xffu;
   constexpr uint32_t J_NOP = 0, J_HEAD = 1, J_TAIL = 2, J_END = 3;
   extern __shared__ __align__(16) unsigned char smraw[];
   const uint32_t d = a.d;
-  double* qd = reinterpret_cast<double*>(smraw);
-  const uint32_t qd_bytes = ((d * 8 + 127) / 128) * 128;
-  float* ring = reinterpret_cast<float*>(smraw + qd_bytes);
+  float* ring = reinterpret_cast<float*>(smraw);
+  double* qd = reinterpret_cast<double*>(smraw + C::ring_bytes);
   __shared__ double qt_s[XT_MAX];
-  __shared__ double thr_s[SC_WARPS];
+  __shared__ double thr_s[NW];   // per warp: k-th best (each a lower bound of the final)
+  __shared__ double thr2_s[NW];  // per warp: ceil(k/NW)-th best (the min over warps is one)
   __shared__ uint32_t q_sh;
-  __shared__ double sq_acc[SC_WARPS][QCAP];  // survivor queue: prefix sums
-  __shared__ uint32_t sq_id[SC_WARPS][QCAP];  //                 and ids
+  __shared__ double sq_acc[NW][QCAP];  // survivor queue: prefix sums
+  __shared__ uint32_t sq_id[NW][QCAP];  //                 and ids
+  __shared__ uint32_t jd_s[NW][ST];     // job hand-over: descriptor,
+  __shared__ uint32_t jid_s[NW][ST][32];  // row id per lane,
+  __shared__ float jx_s[NW][ST][32];      // prefetched tail norm per lane
   volatile double* thr_v = thr_s;
+  volatile double* thr2_v = thr2_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int kk = lane & 7, rbase = lane >> 3;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint32_t nsl = (d + SL - 1) / SL;  // >= 2 (host: d > 64)
   const uint32_t nt = a.xt_n;              // checks after slices 0 .. nt-1 (nt < nsl)
-  float* wring = ring + (size_t)w * 2 * STAGE;
+  float* wring = ring + (size_t)w * ST * STAGE;
   double* qacc = sq_acc[w];
   uint32_t* qid = sq_id[w];
   uint32_t q = blockIdx.x;
@@ -1528,13 +1542,15 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score_pruned(ScoreArgs 
       if (q >= a.nq) return;
     }
     for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) qd[j] = (double)a.Q[(uint64_t)q * d + j];
-    if (threadIdx.x < SC_WARPS) thr_s[threadIdx.x] = -INFINITY;
+    if (threadIdx.x < NW) thr_s[threadIdx.x] = thr2_s[threadIdx.x] = -INFINITY;
     __syncthreads();
     if ((uint32_t)w < nt) {  // query tail norms, rounded up
-      double sq = 0.0;
-      for (uint32_t c = (w + 1) * SL + lane; c < d; c += 32) sq = fma(qd[c], qd[c], sq);
-      for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(FULL, sq, o);
-      if (lane == 0) qt_s[w] = __dsqrt_ru(sq) * (1.0 + 1e-12);
+      for (uint32_t t = w; t < nt; t += NW) {
+        double sq = 0.0;
+        for (uint32_t c = (t + 1) * SL + lane; c < d; c += 32) sq = fma(qd[c], qd[c], sq);
+        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(FULL, sq, o);
+        if (lane == 0) qt_s[t] = __dsqrt_ru(sq) * (1.0 + 1e-12);
+      }
     }
     __syncthreads();
     const uint32_t U = a.uq[q];
@@ -1543,24 +1559,23 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score_pruned(ScoreArgs 
     double bs = -INFINITY;
     uint32_t bi = NONE;
     const uint32_t nb = (U + 31) / 32;
-    const uint32_t nbw = nb > (uint32_t)w ? (nb - w + SC_WARPS - 1) / SC_WARPS : 0;
-    // issue side: next head, tail batch in progress (next slice tis, 0 = none), queue head
-    uint32_t hb = 0, tis = 0, tbase = 0, tcnt = 0, qh = 0, nissued = 0, tgen = 0;
+    const uint32_t nbw = nb > (uint32_t)w ? (nb - w + NW - 1) / NW : 0;
+    // issue side: next head batch, heads issued, batch in progress (next slice tis,
+    // row id per lane), queue head
+    uint32_t hb = 0, nh = 0, tis = TNONE, tbase = 0, tcnt = 0, qh = 0, islot = 0, tgen = 0;
+    uint32_t bid = NONE;
     // written by the compute side, read by the issue side
     uint32_t qtl = 0, hdone = 0, tmask = FULL;
-    // job hand-over (issue -> compute), by job parity: descriptor, row id, tail norm
-    uint32_t jd0 = J_END, jd1 = J_END, jid0 = NONE, jid1 = NONE;
-    float jx0 = 0.f, jx1 = 0.f;
     auto issue = [&]() {
       uint32_t type, s = 0, m = FULL, jid = NONE;
       float jx = 0.f;
-      if (tis && tmask == 0) tis = 0;  // every row of the tail batch is out
-      if (tis) {
+      if (tis != TNONE && tmask == 0) tis = TNONE;  // every row of the batch is out
+      if (tis != TNONE) {
         type = J_TAIL;
         s = tis;
         m = tmask;
-        tis = s + 1 < nsl ? s + 1 : 0;
-      } else if (qtl - qh >= 32 || (hb == nbw && hdone == nbw && qtl != qh)) {
+        tis = s + 1 < nsl ? s + 1 : TNONE;
+      } else if (qtl - qh >= 32 || (hb == nbw && hdone == nh && qtl != qh)) {
         type = J_TAIL;  // a new tail batch (the last one may be partial)
         s = 1;
         tbase = qh;
@@ -1568,25 +1583,25 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score_pruned(ScoreArgs 
         qh += tcnt;
         tmask = FULL;
         ++tgen;
-        tis = nsl > 2 ? 2 : 0;
-        jid = (uint32_t)lane < tcnt ? qid[(tbase + lane) & (QCAP - 1)] : NONE;
+        tis = nsl > 2 ? 2 : TNONE;
+        jid = bid = (uint32_t)lane < tcnt ? qid[(tbase + lane) % QCAP] : NONE;
         if (jid != NONE && nt > 1) jx = __ldg(a.xtail + a.n + jid);
       } else if (hb < nbw) {
-        type = J_HEAD;
-        const uint32_t ci = (w + hb * SC_WARPS) * 32 + lane;
+        const uint32_t ci = (w + hb * NW) * 32 + lane;
         jid = ci < U ? __ldg(cand + ci) : NONE;
         if (jid != NONE) jx = __ldg(a.xtail + jid);
         ++hb;
+        type = J_HEAD;
+        ++nh;
       } else {
-        type = hdone < nbw ? J_NOP : J_END;
+        type = hdone < nh ? J_NOP : J_END;
       }
       if ((type == J_HEAD || type == J_TAIL) && m) {
-        float* buf = wring + (size_t)(nissued & 1u) * STAGE;
+        float* buf = wring + (size_t)islot * STAGE;
         const uint32_t col0 = s * SL;
         const uint32_t len = min((uint32_t)SL, d - col0);
         if (a.dbg) {
-          const uint32_t rows = type == J_HEAD ? __ballot_sync(FULL, jid != NONE)
-                                               : (tcnt == 32 ? FULL : (1u << tcnt) - 1u);
+          const uint32_t rows = __ballot_sync(FULL, (type == J_HEAD ? jid : bid) != NONE);
           if (lane == 0) {
             if (type == J_HEAD) atomicAdd(a.dbg, (unsigned long long)__popc(rows));
             atomicAdd(a.dbg + 1, (unsigned long long)__popc(rows & m));
@@ -1596,9 +1611,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score_pruned(ScoreArgs 
 #pragma unroll
           for (int it = 0; it < 8; ++it) {
             const int rr = rbase + 4 * it;
-            const uint32_t idr = type == J_HEAD
-                                     ? __shfl_sync(FULL, jid, rr)
-                                     : ((uint32_t)rr < tcnt ? qid[(tbase + rr) & (QCAP - 1)] : NONE);
+            const uint32_t idr = __shfl_sync(FULL, type == J_HEAD ? jid : bid, rr);
             if (idr != NONE && ((m >> rr) & 1u)) {
               const float* src = a.X + (uint64_t)idr * a.ldx + col0;
               float* dst = buf + rr * SL;
@@ -1611,9 +1624,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score_pruned(ScoreArgs 
           }
         } else {
           for (int r = 0; r < 32; ++r) {
-            const uint32_t idr = type == J_HEAD
-                                     ? __shfl_sync(FULL, jid, r)
-                                     : ((uint32_t)r < tcnt ? qid[(tbase + r) & (QCAP - 1)] : NONE);
+            const uint32_t idr = __shfl_sync(FULL, type == J_HEAD ? jid : bid, r);
             if (idr != NONE && ((m >> r) & 1u))
               for (uint32_t c = lane; c < len; c += 32)
                 cp_async4(buf + r * SL + ((((c >> 2) ^ (r & 15))) << 2) + (c & 3),
@@ -1621,35 +1632,38 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score_pruned(ScoreArgs 
           }
         }
       }
-      const uint32_t desc = type << 30 | (tgen & 1u) << 29 | s << 24 | (tbase & (QCAP - 1)) | tcnt << 8;
-      if (nissued & 1u) { jd1 = desc; jid1 = jid; jx1 = jx; }
-      else { jd0 = desc; jid0 = jid; jx0 = jx; }
+      if (lane == 0)
+        jd_s[w][islot] = type << 30 | (tgen & 3u) << 28 | s << 20 | tcnt << 12 | (tbase % QCAP);
+      jid_s[w][islot][lane] = jid;
+      jx_s[w][islot][lane] = jx;
       cp_commit();
-      ++nissued;
+      islot = islot + 1 == ST ? 0 : islot + 1;
     };
     // compute side: the tail batch in progress
     double tacc = 0.0;
     uint32_t ctid = NONE;
     bool tlive = false;
     float txn = 0.f;
-    issue();
-    for (uint32_t ncomp = 0;; ++ncomp) {
+#pragma unroll
+    for (int i = 0; i < ST - 1; ++i) issue();
+    for (uint32_t cslot = 0;; cslot = cslot + 1 == ST ? 0 : cslot + 1) {
       issue();
-      cp_wait<1>();
+      cp_wait<ST - 1>();
       __syncwarp();
-      const bool p = ncomp & 1u;
-      const uint32_t desc = p ? jd1 : jd0;
+      const uint32_t desc = jd_s[w][cslot];
       const uint32_t type = desc >> 30;
       if (type == J_END) break;
       if (type == J_NOP) continue;
-      const uint32_t s = (desc >> 24) & 31u;
-      const float* row = wring + (size_t)p * STAGE + lane * SL;
-      const uint32_t col0 = s * SL;
-      const uint32_t len = min((uint32_t)SL, d - col0);
-      const double* qq = qd + col0;
+      const uint32_t s = (desc >> 20) & 31u;
+      const uint32_t jid = jid_s[w][cslot][lane];
+      const float jx = jx_s[w][cslot][lane];
+      const float* row = wring + (size_t)cslot * STAGE + lane * SL;
       const int sw = lane & 15;
-      // dataset.cpp:67 acc += double(a[i]) * double(b[i]), sequential i (exact products)
       auto fold = [&](double acc) {
+        const uint32_t col0 = s * SL;
+        const uint32_t len = min((uint32_t)SL, d - col0);
+        const double* qq = qd + col0;
+        // dataset.cpp:67 acc += double(a[i]) * double(b[i]), sequential i (exact products)
         if (VEC && len == SL) {
 #pragma unroll
           for (int j = 0; j < SL; j += 4) {
@@ -1665,31 +1679,40 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score_pruned(ScoreArgs 
         }
         return acc;
       };
-      const double thr = fmax(fmax(thr_v[0], thr_v[1]), fmax(thr_v[2], thr_v[3]));
+      // lower bound of the final k-th best: the best warp's k-th, or the worst warp's
+      // ceil(k/NW)-th (the warps' lists hold disjoint candidates: NW * ceil(k/NW) >= k
+      // scores are at least that)
+      const double thr = [&] {
+        double t = thr_v[0], t2 = thr2_v[0];
+#pragma unroll
+        for (int i = 1; i < NW; ++i) {
+          t = fmax(t, thr_v[i]);
+          t2 = fmin(t2, thr2_v[i]);
+        }
+        return fmax(t, t2);
+      }();
       if (type == J_HEAD) {
-        const uint32_t id = p ? jid1 : jid0;
         const double acc = fold(0.0);
-        bool live = id != NONE;
-        const double T = (double)(p ? jx1 : jx0) * qt_s[0];
+        bool live = jid != NONE;
+        const double T = (double)jx * qt_s[0];
         if (live && acc + T + 1e-10 * (fabs(acc) + T) < thr) live = false;
         const uint32_t bal = __ballot_sync(FULL, live);
         if (live) {
-          const uint32_t pos = (qtl + __popc(bal & lt_mask)) & (QCAP - 1);
-          qid[pos] = id;
+          const uint32_t pos = (qtl + __popc(bal & lt_mask)) % QCAP;
+          qid[pos] = jid;
           qacc[pos] = acc;
         }
         qtl += __popc(bal);
         ++hdone;
-        __syncwarp();
-      } else {  // tail slice s of the batch at queue slots tbase' .. tbase' + tcnt' - 1
+      } else {  // slice s of a tail batch (queue slots b0 .. b0 + c0 - 1)
         if (s == 1) {
-          const uint32_t b0 = desc & (QCAP - 1), c0 = (desc >> 8) & 63u;
-          ctid = p ? jid1 : jid0;
-          tacc = (uint32_t)lane < c0 ? qacc[(b0 + lane) & (QCAP - 1)] : 0.0;
+          const uint32_t b0 = desc & 0xfffu, c0 = (desc >> 12) & 63u;
+          ctid = jid;
+          tacc = (uint32_t)lane >= c0 ? 0.0 : qacc[(b0 + lane) % QCAP];
           tlive = ctid != NONE;
-          txn = p ? jx1 : jx0;
+          txn = jx;
         }
-        if (tmask) tacc = fold(tacc);
+        if (tmask || s == 1) tacc = fold(tacc);
         if (s < nt) {
           if (tlive) {
             const double T = (double)txn * qt_s[s];
@@ -1697,27 +1720,32 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score_pruned(ScoreArgs 
             if (tlive && s + 1 < nt) txn = __ldg(a.xtail + (uint64_t)(s + 1) * a.n + ctid);
           }
           const uint32_t nm = __ballot_sync(FULL, tlive);
-          // a batch aborted by the issue side may still finish an in-flight slice
-          // after the next batch started: only the current batch owns tmask
-          if (((desc >> 29) & 1u) == (tgen & 1u)) tmask = nm;
+          // slices of an aborted batch may finish after the next batch started:
+          // only the current batch owns tmask
+          if (((desc >> 28) & 3u) == (tgen & 3u)) tmask = nm;
         }
         if (s + 1 == nsl) {  // batch done: rows still live enter the warp top-k
           topk_insert(bs, bi, k, tacc, ctid, tlive);
-          const uint32_t wi = __shfl_sync(FULL, bi, k - 1);
-          const double ws = __shfl_sync(FULL, bs, k - 1);
-          if (lane == 0 && wi != NONE) thr_v[w] = ws;
+          const uint32_t ks = (k + NW - 1) / NW;
+          const uint32_t wi = __shfl_sync(FULL, bi, k - 1), wi2 = __shfl_sync(FULL, bi, ks - 1);
+          const double ws = __shfl_sync(FULL, bs, k - 1), ws2 = __shfl_sync(FULL, bs, ks - 1);
+          if (lane == 0) {
+            if (wi != NONE) thr_v[w] = ws;
+            if (wi2 != NONE) thr2_v[w] = ws2;
+          }
         }
       }
+      __syncwarp();
     }
     cp_wait<0>();
     __syncthreads();  // the ring is reused for the CTA merge
     double* mg_s = reinterpret_cast<double*>(ring);
-    uint32_t* mg_i = reinterpret_cast<uint32_t*>(ring + 2 * SC_WARPS * 32);
+    uint32_t* mg_i = reinterpret_cast<uint32_t*>(ring + 2 * NW * 32);
     mg_s[w * 32 + lane] = bs;
     mg_i[w * 32 + lane] = bi;
     __syncthreads();
     if (w == 0) {
-      for (int w2 = 1; w2 < SC_WARPS; ++w2) {
+      for (int w2 = 1; w2 < NW; ++w2) {
         const bool valid = (uint32_t)lane < k && mg_i[w2 * 32 + lane] != NONE;
         topk_insert(bs, bi, k, mg_s[w2 * 32 + lane], mg_i[w2 * 32 + lane], valid);
       }
@@ -1986,21 +2014,43 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   const bool wide = ix.d >= 64;
   // exact early termination (k_score_pruned) whenever the index has tail norms
   // (d > 64); FPP_NO_PRUNE=1 reads every candidate row in full
+  // exact early termination (k_score_pruned) when the index has tail norms (d > 64)
+  // and the bound pays on this data: the read fraction (row slices read / all) is
+  // probed on the first chunk and every 16th after (async readback); above 0.65 the
+  // job overhead outweighs the saved bytes (C1 iid: 1.0, 1.36x slower; C3: 0.77,
+  // 1.2x slower; C2: 0.33, 2.1x faster) and k_score runs.  FPP_NO_PRUNE=1 / FPP_PRUNE=1
+  // force either; FPP_DEBUG_PRUNE=1 prints every chunk's fraction.
   const bool no_prune = getenv("FPP_NO_PRUNE") != nullptr;
+  const bool force_prune = getenv("FPP_PRUNE") != nullptr;
+  const bool dbg = getenv("FPP_DEBUG_PRUNE") != nullptr;
+  bool use_pruned = false, probe = false;
   if (ix.xt_n && !no_prune) {
+    if (ix.prune_pending && cudaEventQuery(ix.prune_ev) == cudaSuccess) {
+      const double nslf = (double)((ix.d + XT_SLICE - 1) / XT_SLICE);
+      if (ix.prune_h[0]) ix.prune_frac = (double)ix.prune_h[1] / ((double)ix.prune_h[0] * nslf);
+      ix.prune_pending = false;
+    }
+    probe = dbg || (!ix.prune_pending && (ix.prune_frac < 0 || ix.prune_chunks % 16 == 0));
+    use_pruned = force_prune || probe || ix.prune_frac < 0 || ix.prune_frac <= 0.65;
+    ++ix.prune_chunks;
+  }
+  if (use_pruned) {
     sa.xtail = ix.xtail;
     sa.xt_n = ix.xt_n;
     sa.n = ix.n;
-    const bool dbg = getenv("FPP_DEBUG_PRUNE") != nullptr;
-    DBuf<unsigned long long> dbuf;
-    if (dbg) {
-      dbuf.alloc(2);
-      FPP_CUDA(cudaMemsetAsync(dbuf.p, 0, 16, st));
-      sa.dbg = dbuf.p;
+    if (probe) {
+      if (!ix.prune_h) {
+        FPP_CUDA(cudaMallocHost(&ix.prune_h, 16));
+        FPP_CUDA(cudaEventCreateWithFlags(&ix.prune_ev, cudaEventDisableTiming));
+        ix.prune_d.alloc(2);
+      }
+      FPP_CUDA(cudaMemsetAsync(ix.prune_d.p, 0, 16, st));
+      sa.dbg = ix.prune_d.p;
     }
-    // swizzled ring without row padding: qd + 4 warps x 2 stages x 32 rows x 64 floats
-    auto launch_pruned = [&](auto kern) {
-      const size_t sm = ((ix.d * 8 + 127) / 128) * 128 + (size_t)SC_WARPS * 2 * 32 * XT_SLICE * 4;
+    // ring geometry (FPP_SC_PR = NW,ST,MINB digits; default 4 warps x 2 stages, 3 CTAs/SM:
+    // C2 score 8.0 ms vs 11.2 (4x3 @ 2/SM), 12.9 (2x4 @ 3/SM), 20.7 (4x4 @ 1/SM))
+    auto launch_pruned = [&](auto kern, int nw, int stg) {
+      const size_t sm = (size_t)nw * stg * 32 * XT_SLICE * 4 + ((ix.d * 8 + 127) / 128) * 128;
       FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       unsigned grid = nqc;
       if (sc_ctas > 0 && (uint64_t)sm_count() * sc_ctas < nqc) {
@@ -2008,17 +2058,35 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
         sa.qctr = sl.counter.p + 1;
         FPP_CUDA(cudaMemsetAsync(sa.qctr, 0, sizeof(uint32_t), st));
       }
-      kern<<<grid, SC_WARPS * 32, sm, st>>>(sa);
+      kern<<<grid, nw * 32, sm, st>>>(sa);
     };
-    if ((ix.d & 3u) == 0) launch_pruned(k_score_pruned<true, 3>);
-    else launch_pruned(k_score_pruned<false, 3>);
-    if (dbg) {
-      unsigned long long h[2];
-      FPP_CUDA(cudaMemcpyAsync(h, dbuf.p, 16, cudaMemcpyDeviceToHost, st));
-      FPP_CUDA(cudaStreamSynchronize(st));
-      const double nsl = (double)((ix.d + XT_SLICE - 1) / XT_SLICE);
-      fprintf(stderr, "[prune dbg] rows %llu, slices read per row %.3f of %.0f (%.1f%% of row bytes)\n",
-              h[0], h[0] ? (double)h[1] / h[0] : 0.0, nsl, h[0] ? 100.0 * h[1] / h[0] / nsl : 0.0);
+    const char* prc = getenv("FPP_SC_PR");
+    const int pr = prc ? atoi(prc) : 423;
+    const bool vec = (ix.d & 3u) == 0;
+#define FPP_PR_CASE(NW_, ST_, MB_)                                                       \
+  case NW_ * 100 + ST_ * 10 + MB_:                                                       \
+    if (vec) launch_pruned(k_score_pruned<true, NW_, ST_, MB_>, NW_, ST_);               \
+    else launch_pruned(k_score_pruned<false, NW_, ST_, MB_>, NW_, ST_);                  \
+    break;
+    switch (pr) {
+      FPP_PR_CASE(4, 3, 2)
+      FPP_PR_CASE(2, 4, 3)
+      FPP_PR_CASE(4, 4, 1)
+      default:
+      FPP_PR_CASE(4, 2, 3)
+    }
+#undef FPP_PR_CASE
+    if (probe) {
+      FPP_CUDA(cudaMemcpyAsync(ix.prune_h, ix.prune_d.p, 16, cudaMemcpyDeviceToHost, st));
+      FPP_CUDA(cudaEventRecord(ix.prune_ev, st));
+      ix.prune_pending = true;
+      if (dbg) {
+        FPP_CUDA(cudaEventSynchronize(ix.prune_ev));
+        const unsigned long long* h = ix.prune_h;
+        const double nsl = (double)((ix.d + XT_SLICE - 1) / XT_SLICE);
+        fprintf(stderr, "[prune dbg] rows %llu, slices read per row %.3f of %.0f (%.1f%% of row bytes)\n",
+                h[0], h[0] ? (double)h[1] / h[0] : 0.0, nsl, h[0] ? 100.0 * h[1] / h[0] / nsl : 0.0);
+      }
     }
   } else if ((ix.d & 3u) == 0) {
     if (wide) launch_score(k_score<true, 64, 2, 3>, 64, 2);

@@ -447,26 +447,42 @@ def test_large_batch_reordered_equals_oracle(fpp, orc):
         assert np.array_equal(gi, oi) and np.array_equal(gs, os_) and np.array_equal(gst, ost)
 
 
+@pytest.mark.parametrize("geom", ["423", "432"])
 @pytest.mark.parametrize("d", [128, 300, 301, 960])
-def test_score_early_termination_exact(fpp, orc, d, monkeypatch, capfd):
+def test_score_early_termination_exact(fpp, orc, d, geom, monkeypatch, capfd):
     # k_score_pruned (Cauchy-Schwarz bound on the tail of each row against the running
     # k-th best) must return exactly the full gather's answers while reading less:
-    # clustered data, many candidates per query; compared with FPP_NO_PRUNE and the oracle
-    X = data(fpp, 20000, d, 40, 0.25, seed=31)
-    Q = data(fpp, 300, d, 40, 0.25, seed=31, stream=1)
-    ix = fpp.Index.build(X, L=8, K=2, D=128 if d <= 128 else 256, iProbes=3, alpha=0.2)
-    ox = orc.Index(X, L=8, K=2, D=128 if d <= 128 else 256, iprobes=3, alpha=0.2)
+    # clustered data (many small clusters: most candidates are far), compared with
+    # FPP_NO_PRUNE and the oracle, for two ring geometries (FPP_SC_PR)
+    monkeypatch.setenv("FPP_SC_PR", geom)
+    X = data(fpp, 20000, d, 200, 0.25, seed=31)
+    Q = data(fpp, 300, d, 200, 0.25, seed=31, stream=1)
+    ix = fpp.Index.build(X, L=16, K=2, D=128 if d <= 128 else 256, iProbes=3, alpha=0.2)
+    ox = orc.Index(X, L=16, K=2, D=128 if d <= 128 else 256, iprobes=3, alpha=0.2)
     monkeypatch.setenv("FPP_DEBUG_PRUNE", "1")
-    gi, gs, gst = ix.query(Q, 20, 2000, return_stats=True)
+    gi, gs, gst = ix.query(Q, 20, 20000, return_stats=True)
     err = capfd.readouterr().err
     monkeypatch.delenv("FPP_DEBUG_PRUNE")
     monkeypatch.setenv("FPP_NO_PRUNE", "1")
-    fi, fs, fst = ix.query(Q, 20, 2000, return_stats=True)
+    fi, fs, fst = ix.query(Q, 20, 20000, return_stats=True)
     monkeypatch.delenv("FPP_NO_PRUNE")
     assert np.array_equal(gi, fi) and np.array_equal(gs, fs) and np.array_equal(gst, fst)
-    oi, os_, ost = ox.query(Q, 20, 2000)
+    oi, os_, ost = ox.query(Q, 20, 20000)
     assert np.array_equal(gi, oi) and np.array_equal(gst, ost)
     ok = np.isfinite(os_)
     assert np.array_equal(gs[ok], os_[ok])
     fr = [float(l.split("(")[1].split("%")[0]) for l in err.splitlines() if "[prune dbg]" in l]
-    assert fr and max(fr) < 90.0, err  # the bound cut row reads
+    assert fr and max(fr) < 80.0, err  # the bound cut row reads
+
+
+def test_score_early_termination_unstructured(fpp, orc, monkeypatch):
+    # i.i.d. data: heads mostly survive, warps switch to full batches; still exact
+    X = data(fpp, 30000, 200, 0, 0.0, seed=5)
+    Q = data(fpp, 200, 200, 0, 0.0, seed=5, stream=1)
+    ix = fpp.Index.build(X, L=8, K=2, D=256, iProbes=3, alpha=0.3)
+    ox = orc.Index(X, L=8, K=2, D=256, iprobes=3, alpha=0.3)
+    gi, gs, gst = ix.query(Q, 20, 3000, return_stats=True)
+    oi, os_, ost = ox.query(Q, 20, 3000)
+    assert np.array_equal(gi, oi) and np.array_equal(gst, ost)
+    ok = np.isfinite(os_)
+    assert np.array_equal(gs[ok], os_[ok])
