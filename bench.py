@@ -468,10 +468,18 @@ def main():
     tim = ix.timings()
     qps = nq * args.steps / (t_ms / 1e3)
 
-    # roofline of the dominant kernel (k_score): algorithmic bytes per launch / launch time
+    # roofline of the dominant kernel (the score gather): bytes it moves per launch /
+    # launch time.  Row bytes are the library's exact count of candidate-row bytes read
+    # (fpp_timings.score_bytes): with exact early termination (k_score_pruned) a
+    # candidate that cannot reach the top-k is read only up to the slice whose bound
+    # rules it out, so this is below SURVEY 8(d)'s full-row formula 4*d*U, which is
+    # reported beside it ("*_full_rows").
     hbm, peak_kind = peaks()
-    score_bytes_step = 4 * d * U_sum + 4 * U_sum + 4 * d * nq + 12 * K_TOP * nq
-    path_bytes_step = 8 * P_sum + 4 * E_sum + 4 * d * U_sum + 4 * d * nq + 12 * K_TOP * nq
+    row_bytes_step = tim["score_bytes"] / args.steps if tim.get("score_bytes") else 4 * d * U_sum
+    score_bytes_step = row_bytes_step + 4 * U_sum + 4 * d * nq + 12 * K_TOP * nq
+    score_bytes_full = 4 * d * U_sum + 4 * U_sum + 4 * d * nq + 12 * K_TOP * nq
+    path_bytes_step = 8 * P_sum + 4 * E_sum + row_bytes_step + 4 * d * nq + 12 * K_TOP * nq
+    path_bytes_full = 8 * P_sum + 4 * E_sum + 4 * d * U_sum + 4 * d * nq + 12 * K_TOP * nq
     score_ms = tim["score_ms"] / args.steps
     achieved = score_bytes_step / (score_ms / 1e3) / 1e9
     traffic = None
@@ -582,15 +590,19 @@ def main():
                        "parallelism": f"shard{world}" if world > 1 else "single",
                        "l2": "inputs larger than L2 (X %.2f GB gathered at random)" % (
                            n * d * 4 / 1e9)},
-            "roofline": {"kernel": "k_score", "bound": "hbm", "achieved": achieved,
+            "roofline": {"kernel": "k_score_pruned" if row_bytes_step < 4 * d * U_sum else "k_score",
+                         "bound": "hbm", "achieved": achieved,
                          "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "algorithmic_bytes_per_launch": score_bytes_step / score_launches_per_step,
                          "algorithmic_bytes_per_step": score_bytes_step,
+                         "row_bytes_read_fraction": row_bytes_step / max(1, 4 * d * U_sum),
+                         "algorithmic_bytes_per_step_full_rows": score_bytes_full,
                          "launches_per_step": launches_per_step,
                          "kernel_ms_per_step": score_ms,
                          "share_of_step": score_ms / (t_ms / args.steps)},
             "path": {"algorithmic_bytes_per_step": path_bytes_step,
+                     "algorithmic_bytes_per_step_full_rows": path_bytes_full,
                      "achieved_gbs": path_bytes_step / (t_ms / args.steps / 1e3) / 1e9,
                      "frac_of_hbm": path_bytes_step / (t_ms / args.steps / 1e3) / 1e9 / hbm,
                      "mean_probes": P_sum / nq, "mean_entries": E_sum / nq,

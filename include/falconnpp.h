@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define FPP_ABI_VERSION 2  /* 2: fpp_query_stats.exact, SimHash rerank */
+#define FPP_ABI_VERSION 3  /* 2: fpp_query_stats.exact, SimHash rerank; 3: fpp_timings.score_bytes */
 
 /* error classes ("one exit code per error class") */
 #define FPP_OK 0
@@ -83,6 +83,8 @@ typedef struct fpp_timings {
   uint64_t score_rows;/* rows gathered by the score kernel */
   uint64_t entries;   /* bucket entries walked */
   uint64_t probes;    /* probes */
+  uint64_t score_bytes; /* candidate-row bytes the score kernel read (early termination
+                           reads only row prefixes of candidates that cannot reach the top-k) */
 } fpp_timings;
 
 typedef struct fpp_index fpp_index;

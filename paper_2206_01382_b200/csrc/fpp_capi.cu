@@ -104,6 +104,7 @@ Index::~Index() {
   if (prune_h) cudaFreeHost(prune_h);
   if (prune_ev) cudaEventDestroy(prune_ev);
   prune_d.release();
+  score_bytes_d.release();
   if (stream) cudaStreamDestroy(stream);
   cudaSetDevice(cur);
 }
@@ -429,6 +430,12 @@ static void collect_timings(const Index& ix) {
   ix.acc.probe_ms += ms[PH_PROBE];
   ix.acc.collect_ms += ms[PH_COLLECT];
   ix.acc.score_ms += ms[PH_SCORE];
+  if (ix.score_bytes_d.p) {  // the phases above have completed: the counter is final
+    unsigned long long b = 0;  // monotone counter: no reset racing later launches
+    FPP_CUDA(cudaMemcpy(&b, ix.score_bytes_d.p, 8, cudaMemcpyDeviceToHost));
+    ix.acc.score_bytes += b - ix.score_bytes_seen;
+    ix.score_bytes_seen = b;
+  }
 }
 
 }  // namespace fpp

@@ -146,6 +146,8 @@ struct Index {
   mutable unsigned long long* prune_h = nullptr;  // pinned [2]: rows, row slices read
   mutable DBuf<unsigned long long> prune_d;
   mutable cudaEvent_t prune_ev = nullptr;
+  mutable DBuf<unsigned long long> score_bytes_d;  // [1] row bytes read by the score kernels
+  mutable unsigned long long score_bytes_seen = 0;
 
   mutable PhaseTimer timer;
   mutable fpp_timings acc{};

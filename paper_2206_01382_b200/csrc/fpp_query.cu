@@ -1286,6 +1286,7 @@ struct ScoreArgs {
   uint32_t xt_n;
   uint64_t n;
   unsigned long long* dbg;  // FPP_DEBUG_PRUNE: [rows, row slices read]
+  unsigned long long* rbytes;  // += candidate-row bytes read (fpp_timings.score_bytes)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1471,6 +1472,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
       a.stats[q].candidates = a.uq_all ? a.uq_all[q] : U;
       a.stats[q].exact = U;
     }
+    if (lane == 0 && a.rbytes) atomicAdd(a.rbytes, (unsigned long long)U * d * 4ull);
   }
   if (!a.qctr) return;
   __syncthreads();  // qd, mg_* and q_sh are reused by the next query
@@ -1564,6 +1566,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
     // row id per lane), queue head
     uint32_t hb = 0, nh = 0, tis = TNONE, tbase = 0, tcnt = 0, qh = 0, islot = 0, tgen = 0;
     uint32_t bid = NONE;
+    unsigned long long wbytes = 0;  // row bytes this warp read (lane 0)
     // written by the compute side, read by the issue side
     uint32_t qtl = 0, hdone = 0, tmask = FULL;
     auto issue = [&]() {
@@ -1600,8 +1603,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
         float* buf = wring + (size_t)islot * STAGE;
         const uint32_t col0 = s * SL;
         const uint32_t len = min((uint32_t)SL, d - col0);
+        const uint32_t rows = __ballot_sync(FULL, (type == J_HEAD ? jid : bid) != NONE);
+        wbytes += (unsigned long long)__popc(rows & m) * len * 4u;
         if (a.dbg) {
-          const uint32_t rows = __ballot_sync(FULL, (type == J_HEAD ? jid : bid) != NONE);
           if (lane == 0) {
             if (type == J_HEAD) atomicAdd(a.dbg, (unsigned long long)__popc(rows));
             atomicAdd(a.dbg + 1, (unsigned long long)__popc(rows & m));
@@ -1738,6 +1742,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
       __syncwarp();
     }
     cp_wait<0>();
+    if (lane == 0 && a.rbytes && wbytes) atomicAdd(a.rbytes, wbytes);
     __syncthreads();  // the ring is reused for the CTA merge
     double* mg_s = reinterpret_cast<double*>(ring);
     uint32_t* mg_i = reinterpret_cast<uint32_t*>(ring + 2 * NW * 32);
@@ -1979,6 +1984,11 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   ix.timer.begin(PH_SCORE, st, &e0);
   ScoreArgs sa{ix.X, ix.d, ix.ldx, Qd, sl.coff.p, sl.cands.p, sl.uq.p, sl.eq.p, peff, k,
                ix.prm.id_offset, ids_d, scores_d, stats_d, nullptr, 0};
+  if (!ix.score_bytes_d.p) {
+    ix.score_bytes_d.alloc(1);
+    FPP_CUDA(cudaMemsetAsync(ix.score_bytes_d.p, 0, 8, st));
+  }
+  sa.rbytes = ix.score_bytes_d.p;
   if (rerank) {  // SimHash screen: at most B candidates per query reach the exact scores
     sl.qsig.ensure(nqc);
     sl.cands2.ensure((size_t)nqc * rerank);

@@ -14,13 +14,14 @@ h = rows[0]
 ki, vi = h.index("Kernel Name"), h.index("Metric Value")
 agg = collections.OrderedDict()
 for r in rows[1:]:
-    name = r[ki].split("(")[0].replace("void ", "").split("<")[0].strip()
+    name = r[ki].split("(")[0].replace("void ", "").split("<")[0].strip().replace("fpp::", "")
     v = float(r[vi].replace(",", ""))
     a = agg.setdefault(name, [0, 0.0])
     a[0] += 1
     a[1] += v
 tot = sum(v for _, v in agg.values())
-QUERY = ("k_query_lists", "k_probe_select", "k_scan_eq", "k_collect", "k_collect_cluster", "k_score")
+QUERY = ("k_query_lists", "k_probe_select", "k_scan_eq", "k_collect", "k_collect_cluster", "k_score",
+         "k_score_pruned", "k_order_keys", "k_gather_rows", "k_scatter_results")
 qtot = sum(v for k, (_, v) in agg.items() if k in QUERY) or 1
 lines = ["| kernel | launches | total ms | share of all | share of query |", "|---|---|---|---|---|"]
 for k, (c, v) in agg.items():
