@@ -191,7 +191,9 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
   for (int e = 0; e < EPT; ++e) {
     const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * EPT + e;  // layout B / A
     pv[j] = v[e];
-    const uint32_t qv = min((uint32_t)(fabsf(v[e]) * qs), 4194303u);
+    // round(|p| * qs) via the 2^23 magic-number trick (FFMA + LOP on the FMA/ALU
+    // pipes instead of F2I); monotone in |p| like the floor it replaces
+    const uint32_t qv = min(__float_as_uint(fmaf(fabsf(v[e]), qs, 8388608.0f)) & 0x7fffffu, 4194303u);
     kk[e] = j < D ? (((4194303u - qv) << 10) | j) : 0xffffffffu;
   }
   __syncwarp();
@@ -227,9 +229,10 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
     for (int it = 0; it < 24; ++it) {
       if (__all_sync(FULL, ok || fail)) break;
       const uint32_t mid = (lo + hi) >> 1;
+      const uint32_t midk = (mid << 10) | 1023u;  // (k >> 10) <= mid  <=>  k <= midk
       uint32_t c = 0;
 #pragma unroll
-      for (int e = 0; e < EPT; ++e) c += (kk[e] >> 10) <= mid;  // sentinels: 4194303 > mid
+      for (int e = 0; e < EPT; ++e) c += kk[e] <= midk;  // sentinels: 0xffffffff > midk
 #pragma unroll
       for (int m = 1; m < S::G; m <<= 1) c += __shfl_xor_sync(FULL, c, m);
       if (!ok && !fail) {
@@ -1677,6 +1680,15 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
             acc = fma((double)xv.z, qq[j + 2], acc);
             acc = fma((double)xv.w, qq[j + 3], acc);
           }
+        } else if (VEC) {  // the last, partial slice (len % 4 == 0)
+#pragma unroll 2
+          for (uint32_t j = 0; j < len; j += 4) {
+            const float4 xv = *reinterpret_cast<const float4*>(row + (((j >> 2) ^ sw) << 2));
+            acc = fma((double)xv.x, qq[j], acc);
+            acc = fma((double)xv.y, qq[j + 1], acc);
+            acc = fma((double)xv.z, qq[j + 2], acc);
+            acc = fma((double)xv.w, qq[j + 3], acc);
+          }
         } else {
           for (uint32_t j = 0; j < len; ++j)
             acc = fma((double)row[(((j >> 2) ^ sw) << 2) + (j & 3)], qq[j], acc);
@@ -1685,8 +1697,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
       };
       // lower bound of the final k-th best: the best warp's k-th, or the worst warp's
       // ceil(k/NW)-th (the warps' lists hold disjoint candidates: NW * ceil(k/NW) >= k
-      // scores are at least that)
-      const double thr = [&] {
+      // scores are at least that); read only where a check needs it
+      auto thr_now = [&] {
         double t = thr_v[0], t2 = thr2_v[0];
 #pragma unroll
         for (int i = 1; i < NW; ++i) {
@@ -1694,12 +1706,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
           t2 = fmin(t2, thr2_v[i]);
         }
         return fmax(t, t2);
-      }();
+      };
       if (type == J_HEAD) {
         const double acc = fold(0.0);
         bool live = jid != NONE;
         const double T = (double)jx * qt_s[0];
-        if (live && acc + T + 1e-10 * (fabs(acc) + T) < thr) live = false;
+        if (live && acc + T + 1e-10 * (fabs(acc) + T) < thr_now()) live = false;
         const uint32_t bal = __ballot_sync(FULL, live);
         if (live) {
           const uint32_t pos = (qtl + __popc(bal & lt_mask)) % QCAP;
@@ -1720,7 +1732,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
         if (s < nt) {
           if (tlive) {
             const double T = (double)txn * qt_s[s];
-            if (tacc + T + 1e-10 * (fabs(tacc) + T) < thr) tlive = false;
+            if (tacc + T + 1e-10 * (fabs(tacc) + T) < thr_now()) tlive = false;
             if (tlive && s + 1 < nt) txn = __ldg(a.xtail + (uint64_t)(s + 1) * a.n + ctid);
           }
           const uint32_t nm = __ballot_sync(FULL, tlive);
