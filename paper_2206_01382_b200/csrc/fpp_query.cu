@@ -1304,6 +1304,36 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// mbarrier + TMA bulk copies (k_score_pruned<..., TMA = true>)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // warp top-k: lane i < k holds the i-th best (score desc, id asc)
 __device__ __forceinline__ bool sbetter(double s1, uint32_t i1, double s2, uint32_t i2) {
   return s1 > s2 || (s1 == s2 && i1 < i2);
@@ -1497,7 +1527,10 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
 // candidates, a tail slice of 32 survivors, or a bubble) run through an ST-stage
 // cp.async ring per warp (ST-1 jobs in flight); the next job is chosen when it is
 // issued and handed to the compute side through shared memory.  Ring rows are
-// XOR-swizzled in 16 B chunks (conflict-free LDS.128 without padding).  Whether the
+// rotated in 16 B chunks (chunk c of row r at (c + r) mod 16: conflict-free LDS.128
+// without padding).  TMA = true moves each row slice with one or two
+// cp.async.bulk copies issued by the row's lane, completing on a per-stage mbarrier
+// (the rotation splits a slice at the wrap point), instead of 16 cp.async per lane.  Whether the
 // bound pays is data dependent (cluster structure): the host measures the read
 // fraction and falls back to k_score where it does not (stage_b).
 template <int NW, int ST>
@@ -1507,8 +1540,9 @@ struct PrunedCfg {
   static constexpr uint32_t QCAP = 32u * (ST + 2);      // >= 31 + 32 (ST - 1) + 64
   static constexpr size_t ring_bytes = (size_t)NW * ST * STAGE * 4;
 };
-template <bool VEC, int NW, int ST, int MINB>
+template <bool VEC, int NW, int ST, int MINB, bool TMA = false>
 __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
+  static_assert(!TMA || VEC, "bulk copies need 16 B-aligned row slices (d % 4 == 0)");
   using C = PrunedCfg<NW, ST>;
   constexpr int SL = C::SL;
   constexpr int STAGE = C::STAGE;
@@ -1528,6 +1562,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
   __shared__ uint32_t jd_s[NW][ST];     // job hand-over: descriptor,
   __shared__ uint32_t jid_s[NW][ST][32];  // row id per lane,
   __shared__ float jx_s[NW][ST][32];      // prefetched tail norm per lane
+  __shared__ __align__(8) uint64_t mbar[NW][ST];  // TMA: ring stage completion
   volatile double* thr_v = thr_s;
   volatile double* thr2_v = thr2_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1538,6 +1573,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
   float* wring = ring + (size_t)w * ST * STAGE;
   double* qacc = sq_acc[w];
   uint32_t* qid = sq_id[w];
+  uint32_t ph = 0;  // TMA: parity of the next wait, bit per stage
+  if (TMA) {
+    if (lane == 0)
+      for (int i = 0; i < ST; ++i) mbar_init(&mbar[w][i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+  }
   uint32_t q = blockIdx.x;
   for (;;) {
     if (a.qctr) {
@@ -1614,7 +1656,18 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
             atomicAdd(a.dbg + 1, (unsigned long long)__popc(rows & m));
           }
         }
-        if (VEC) {
+        if (TMA) {  // lane r copies row r's slice (rotated by r & 15: at most two copies)
+          if (lane == 0) mbar_arrive_tx(&mbar[w][islot], __popc(rows & m) * len * 4u);
+          __syncwarp();
+          const uint32_t idr = type == J_HEAD ? jid : bid;
+          if (idr != NONE && ((m >> lane) & 1u)) {
+            const float* src = a.X + (uint64_t)idr * a.ldx + col0;
+            float* dst = buf + lane * SL;
+            const uint32_t rot = lane & 15, nch = len >> 2, n1 = min(nch, 16u - rot);
+            bulk_g2s(dst + rot * 4, src, n1 * 16, &mbar[w][islot]);
+            if (nch > n1) bulk_g2s(dst, src + n1 * 4, (nch - n1) * 16, &mbar[w][islot]);
+          }
+        } else if (VEC) {
 #pragma unroll
           for (int it = 0; it < 8; ++it) {
             const int rr = rbase + 4 * it;
@@ -1625,7 +1678,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
 #pragma unroll
               for (int h = 0; h < SL / 32; ++h) {
                 const uint32_t ch = kk + 8 * h;
-                if (ch < (len >> 2)) cp_async16(dst + ((ch ^ (rr & 15)) << 2), src + ch * 4);
+                if (ch < (len >> 2)) cp_async16(dst + (((ch + rr) & 15) << 2), src + ch * 4);
               }
             }
           }
@@ -1634,16 +1687,18 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
             const uint32_t idr = __shfl_sync(FULL, type == J_HEAD ? jid : bid, r);
             if (idr != NONE && ((m >> r) & 1u))
               for (uint32_t c = lane; c < len; c += 32)
-                cp_async4(buf + r * SL + ((((c >> 2) ^ (r & 15))) << 2) + (c & 3),
+                cp_async4(buf + r * SL + ((((c >> 2) + r) & 15) << 2) + (c & 3),
                           a.X + (uint64_t)idr * a.ldx + col0 + c);
           }
         }
+      } else if (TMA && lane == 0) {
+        mbar_arrive_tx(&mbar[w][islot], 0);  // every issue completes one stage phase
       }
       if (lane == 0)
         jd_s[w][islot] = type << 30 | (tgen & 3u) << 28 | s << 20 | tcnt << 12 | (tbase % QCAP);
       jid_s[w][islot][lane] = jid;
       jx_s[w][islot][lane] = jx;
-      cp_commit();
+      if (!TMA) cp_commit();
       islot = islot + 1 == ST ? 0 : islot + 1;
     };
     // compute side: the tail batch in progress
@@ -1653,9 +1708,15 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
     float txn = 0.f;
 #pragma unroll
     for (int i = 0; i < ST - 1; ++i) issue();
-    for (uint32_t cslot = 0;; cslot = cslot + 1 == ST ? 0 : cslot + 1) {
+    uint32_t cslot = 0;
+    for (;; cslot = cslot + 1 == ST ? 0 : cslot + 1) {
       issue();
-      cp_wait<ST - 1>();
+      if (TMA) {
+        mbar_wait(&mbar[w][cslot], (ph >> cslot) & 1u);
+        ph ^= 1u << cslot;
+      } else {
+        cp_wait<ST - 1>();
+      }
       __syncwarp();
       const uint32_t desc = jd_s[w][cslot];
       const uint32_t type = desc >> 30;
@@ -1674,7 +1735,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
         if (VEC && len == SL) {
 #pragma unroll
           for (int j = 0; j < SL; j += 4) {
-            const float4 xv = *reinterpret_cast<const float4*>(row + (((j >> 2) ^ sw) << 2));
+            const float4 xv = *reinterpret_cast<const float4*>(row + ((((j >> 2) + sw) & 15) << 2));
             acc = fma((double)xv.x, qq[j], acc);
             acc = fma((double)xv.y, qq[j + 1], acc);
             acc = fma((double)xv.z, qq[j + 2], acc);
@@ -1683,7 +1744,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
         } else if (VEC) {  // the last, partial slice (len % 4 == 0)
 #pragma unroll 2
           for (uint32_t j = 0; j < len; j += 4) {
-            const float4 xv = *reinterpret_cast<const float4*>(row + (((j >> 2) ^ sw) << 2));
+            const float4 xv = *reinterpret_cast<const float4*>(row + ((((j >> 2) + sw) & 15) << 2));
             acc = fma((double)xv.x, qq[j], acc);
             acc = fma((double)xv.y, qq[j + 1], acc);
             acc = fma((double)xv.z, qq[j + 2], acc);
@@ -1691,7 +1752,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
           }
         } else {
           for (uint32_t j = 0; j < len; ++j)
-            acc = fma((double)row[(((j >> 2) ^ sw) << 2) + (j & 3)], qq[j], acc);
+            acc = fma((double)row[((((j >> 2) + sw) & 15) << 2) + (j & 3)], qq[j], acc);
         }
         return acc;
       };
@@ -1753,7 +1814,15 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
       }
       __syncwarp();
     }
-    cp_wait<0>();
+    if (TMA) {  // drain the ST-1 jobs issued past END (no copies): phases stay in step
+      for (int i = 0; i < ST - 1; ++i) {
+        cslot = cslot + 1 == ST ? 0 : cslot + 1;
+        mbar_wait(&mbar[w][cslot], (ph >> cslot) & 1u);
+        ph ^= 1u << cslot;
+      }
+    } else {
+      cp_wait<0>();
+    }
     if (lane == 0 && a.rbytes && wbytes) atomicAdd(a.rbytes, wbytes);
     __syncthreads();  // the ring is reused for the CTA merge
     double* mg_s = reinterpret_cast<double*>(ring);
@@ -1779,6 +1848,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
       }
     }
     __syncthreads();  // mg_* (ring), qd, thr_s are reused by the next query
+    if (TMA) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA
     if (!a.qctr) return;
   }
 }
@@ -2085,9 +2155,13 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     const char* prc = getenv("FPP_SC_PR");
     const int pr = prc ? atoi(prc) : 423;
     const bool vec = (ix.d & 3u) == 0;
+    // FPP_SC_TMA=1: TMA bulk row copies instead of the cp.async ring.  Measured slower
+    // (C2 score 12.4 vs 7.6 ms: 256 B bulk copies are TMA-issue bound), kept as an option
+    const bool tma = getenv("FPP_SC_TMA") && atoi(getenv("FPP_SC_TMA")) != 0;
 #define FPP_PR_CASE(NW_, ST_, MB_)                                                       \
   case NW_ * 100 + ST_ * 10 + MB_:                                                       \
-    if (vec) launch_pruned(k_score_pruned<true, NW_, ST_, MB_>, NW_, ST_);               \
+    if (vec && tma) launch_pruned(k_score_pruned<true, NW_, ST_, MB_, true>, NW_, ST_);  \
+    else if (vec) launch_pruned(k_score_pruned<true, NW_, ST_, MB_>, NW_, ST_);          \
     else launch_pruned(k_score_pruned<false, NW_, ST_, MB_>, NW_, ST_);                  \
     break;
     switch (pr) {

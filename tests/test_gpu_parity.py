@@ -447,14 +447,16 @@ def test_large_batch_reordered_equals_oracle(fpp, orc):
         assert np.array_equal(gi, oi) and np.array_equal(gs, os_) and np.array_equal(gst, ost)
 
 
-@pytest.mark.parametrize("geom", ["423", "432"])
+@pytest.mark.parametrize("geom", ["423", "432", "423-tma"])
 @pytest.mark.parametrize("d", [128, 300, 301, 960])
 def test_score_early_termination_exact(fpp, orc, d, geom, monkeypatch, capfd):
     # k_score_pruned (Cauchy-Schwarz bound on the tail of each row against the running
     # k-th best) must return exactly the full gather's answers while reading less:
     # clustered data (many small clusters: most candidates are far), compared with
     # FPP_NO_PRUNE and the oracle, for two ring geometries (FPP_SC_PR)
-    monkeypatch.setenv("FPP_SC_PR", geom)
+    monkeypatch.setenv("FPP_SC_PR", geom.split("-")[0])
+    if geom.endswith("-tma"):  # TMA bulk row copies + mbarrier ring (d % 4 == 0 only)
+        monkeypatch.setenv("FPP_SC_TMA", "1")
     X = data(fpp, 20000, d, 200, 0.25, seed=31)
     Q = data(fpp, 300, d, 200, 0.25, seed=31, stream=1)
     ix = fpp.Index.build(X, L=16, K=2, D=128 if d <= 128 else 256, iProbes=3, alpha=0.2)
