@@ -47,7 +47,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src):
         obj = os.path.join(LIBDIR, "obj", os.path.basename(src) + ".o")
-        cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
+        # FPP_NVCC_EXTRA: extra flags for experiments (e.g. -DFPP_CO_CL_THREADS=512)
+        cmd = [NVCC] + ARCH + FLAGS + os.environ.get("FPP_NVCC_EXTRA", "").split() + \
+            ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

@@ -146,6 +146,7 @@ struct Index {
   mutable unsigned long long* prune_h = nullptr;  // pinned [2]: rows, row slices read
   mutable DBuf<unsigned long long> prune_d;
   mutable cudaEvent_t prune_ev = nullptr;
+  mutable double dup_ratio = -1.0;  // walked entries / unique candidates (stage_b dedup choice)
   mutable DBuf<unsigned long long> score_bytes_d;  // [1] row bytes read by the score kernels
   mutable unsigned long long score_bytes_seen = 0;
 

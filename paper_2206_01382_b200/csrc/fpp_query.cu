@@ -947,6 +947,10 @@ __global__ void __launch_bounds__(1024) k_scan_eq(const uint32_t* __restrict__ e
 
 // ----------------------------------------------------------------- collect
 constexpr int CO_THREADS = 1024;
+#ifndef FPP_CO_CL_THREADS
+#define FPP_CO_CL_THREADS 1024
+#endif
+constexpr int CO_CL_THREADS = FPP_CO_CL_THREADS;  // k_collect_cluster CTA size
 
 struct CollectArgs {
   const uint64_t* ppos;
@@ -960,6 +964,8 @@ struct CollectArgs {
   uint32_t nwords;       // bitmap words (n bits)
   uint32_t* gbitmap;     // [gridDim.x][nwords] when not in shared memory
   uint32_t* counter;     // dynamic query fetch
+  uint32_t nodedup;      // 1: copy the walked ids without dedup (stage_b: few duplicates)
+  uint32_t bshift;       // nodedup: id >> bshift < 256 (id-range groups)
 };
 
 // Warp-cooperative walk over one query's probes.  A warp takes 32 probes at a
@@ -1039,6 +1045,7 @@ __device__ __forceinline__ void collect_walk(const uint64_t* pp, const uint32_t*
 __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
   extern __shared__ __align__(16) uint32_t sbm[];
   __shared__ uint32_t ucount, qsh, nextc;
+  __shared__ uint32_t bcur[256];  // nodedup: id-range counts, then write cursors
   __shared__ uint32_t scan_sh[32];
   uint32_t* bm = a.gbitmap ? a.gbitmap + (uint64_t)blockIdx.x * a.nwords : sbm;
   for (;;) {
@@ -1047,7 +1054,7 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
       ucount = 0;
       nextc = 0;
     }
-    if (!a.gbitmap) {
+    if (!a.gbitmap && !a.nodedup) {
       const uint32_t n4 = a.nwords >> 2;
       uint4* b4 = reinterpret_cast<uint4*>(sbm);
       for (uint32_t w = threadIdx.x; w < n4; w += blockDim.x) b4[w] = make_uint4(0, 0, 0, 0);
@@ -1064,7 +1071,43 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
       return __shfl_sync(FULL, c, 0);
     };
     uint32_t U;
-    if (!a.gbitmap) {
+    if (a.nodedup) {
+      // every walked entry is a candidate (duplicates kept), grouped by the top 8 bits
+      // of the id (a counting sort over two walks): similar queries scored side by
+      // side then still gather rows of the same id range at about the same time
+      for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) bcur[i] = 0;
+      __syncthreads();
+      const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
+      const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
+      collect_walk(pp, pl, P, a.ids, out, &ucount, next_chunk, [&](uint32_t id) {
+        smem_inc(&bcur[id >> a.bshift]);
+        return false;
+      });
+      __syncthreads();
+      if (threadIdx.x < 32) {  // exclusive scan of the 256 counts (8 per lane)
+        uint32_t v[8], t = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { v[j] = bcur[threadIdx.x * 8 + j]; t += v[j]; }
+        uint32_t x = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, x, o);
+          if ((int)threadIdx.x >= o) x += y;
+        }
+        uint32_t b = x - t;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { bcur[threadIdx.x * 8 + j] = b; b += v[j]; }
+        if (threadIdx.x == 31) ucount = x;
+        if (threadIdx.x == 0) nextc = 0;
+      }
+      __syncthreads();
+      collect_walk(pp, pl, P, a.ids, out, &ucount, next_chunk, [&](uint32_t id) {
+        out[smem_fetch_add(&bcur[id >> a.bshift], 1u)] = id;
+        return false;
+      });
+      __syncthreads();
+      U = ucount;
+    } else if (!a.gbitmap) {
       // shared-memory bitmap: fire-and-forget ORs during the walk, then the set
       // bits are emitted in ascending id order (a bitmap scan), so every query's
       // candidate rows are gathered in address order and similar queries scored
@@ -1095,7 +1138,7 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
       U = ucount;
     }
     if (threadIdx.x == 0) a.uq[q] = U;
-    if (a.gbitmap)
+    if (a.gbitmap && !a.nodedup)
       for (uint32_t c = threadIdx.x; c < U; c += blockDim.x) bm[out[c] >> 5] = 0;
     __syncthreads();
   }
@@ -1108,7 +1151,7 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
 // and the probe chunks are dealt round-robin over the cluster's CTAs.
 constexpr int CO_CLUSTER = 8;
 
-__global__ void __cluster_dims__(CO_CLUSTER, 1, 1) __launch_bounds__(CO_THREADS, 1)
+__global__ void __cluster_dims__(CO_CLUSTER, 1, 1) __launch_bounds__(CO_CL_THREADS, 1)
 k_collect_cluster(CollectArgs a, uint32_t slice_words) {
   cg::cluster_group cluster = cg::this_cluster();
   const uint32_t rank = cluster.block_rank();
@@ -1117,6 +1160,8 @@ k_collect_cluster(CollectArgs a, uint32_t slice_words) {
   __shared__ uint32_t ucount, nextc, cta_cnt;
   __shared__ uint32_t scan_sh[32];
   const uint32_t slice_bits = slice_words * 32;
+  const uint32_t inv_slice = (uint32_t)(0x100000000ull / slice_bits);
+  const uint32_t sbm_base = (uint32_t)__cvta_generic_to_shared(sbm);
   for (uint32_t q = cid; q < a.nq; q += ncl) {
     for (uint32_t w = threadIdx.x; w < slice_words; w += blockDim.x) sbm[w] = 0;
     if (threadIdx.x == 0) {
@@ -1135,9 +1180,17 @@ k_collect_cluster(CollectArgs a, uint32_t slice_words) {
                    return __shfl_sync(FULL, c, 0) * CO_CLUSTER + rank;
                  },
                  [&](uint32_t id) {
-                   const uint32_t owner = id / slice_bits, lb = id - owner * slice_bits;
-                   uint32_t* rb = cluster.map_shared_rank(sbm, owner);
-                   atomicOr(rb + (lb >> 5), 1u << (lb & 31));
+                   // owner = id / slice_bits by a reciprocal multiply (+ one-step fix-up)
+                   uint32_t owner = __umulhi(id, inv_slice);
+                   if ((owner + 1) * slice_bits <= id) ++owner;
+                   if (owner * slice_bits > id) --owner;
+                   const uint32_t lb = id - owner * slice_bits;
+                   uint32_t ra;  // fire-and-forget OR into the owning CTA's slice (DSMEM)
+                   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n"
+                                : "=r"(ra)
+                                : "r"(sbm_base + (lb >> 5) * 4), "r"(owner));
+                   asm volatile("red.shared::cluster.or.b32 [%0], %1;\n" ::"r"(ra), "r"(1u << (lb & 31))
+                                : "memory");
                    return false;
                  });
     cluster.sync();
@@ -1290,6 +1343,7 @@ struct ScoreArgs {
   uint64_t n;
   unsigned long long* dbg;  // FPP_DEBUG_PRUNE: [rows, row slices read]
   unsigned long long* rbytes;  // += candidate-row bytes read (fpp_timings.score_bytes)
+  uint32_t dup;                // 1: candidate lists may repeat ids (CollectArgs::nodedup)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1339,7 +1393,7 @@ __device__ __forceinline__ bool sbetter(double s1, uint32_t i1, double s2, uint3
   return s1 > s2 || (s1 == s2 && i1 < i2);
 }
 __device__ __forceinline__ void topk_insert(double& bs, uint32_t& bi, uint32_t k, double cs_l,
-                                            uint32_t ci_l, bool valid) {
+                                            uint32_t ci_l, bool valid, bool dedup = false) {
   const int lane = threadIdx.x & 31;
   double ws = __shfl_sync(FULL, bs, k - 1);
   uint32_t wi = __shfl_sync(FULL, bi, k - 1);
@@ -1352,6 +1406,8 @@ __device__ __forceinline__ void topk_insert(double& bs, uint32_t& bi, uint32_t k
     ws = __shfl_sync(FULL, bs, k - 1);
     wi = __shfl_sync(FULL, bi, k - 1);
     if (!sbetter(cs, ci, ws, wi)) continue;
+    // candidate lists with duplicates (ScoreArgs::dup): an id enters a list once
+    if (dedup && __any_sync(FULL, (uint32_t)lane < k && bi == ci)) continue;
     const unsigned ahead = __ballot_sync(FULL, (uint32_t)lane < k && sbetter(bs, bi, cs, ci));
     const int pos = __popc(ahead);
     const double us = __shfl_up_sync(FULL, bs, 1);
@@ -1478,7 +1534,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
       const uint32_t ci = cb * 32 + lane;
       const bool valid = ci < U;
       const uint32_t id = valid ? __ldg(cand + ci) : 0xffffffffu;
-      topk_insert(bs, bi, k, acc, id, valid);
+      topk_insert(bs, bi, k, acc, id, valid, a.dup);
       acc = 0.0;
       cc = 0;
       cb += SC_WARPS;
@@ -1492,7 +1548,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
   if (w == 0) {
     for (int w2 = 1; w2 < SC_WARPS; ++w2) {
       const bool valid = (uint32_t)lane < k && mg_i[w2][lane] != 0xffffffffu;
-      topk_insert(bs, bi, k, mg_s[w2][lane], mg_i[w2][lane], valid);
+      topk_insert(bs, bi, k, mg_s[w2][lane], mg_i[w2][lane], valid, a.dup);
     }
     if ((uint32_t)lane < k) {
       const bool ok = bi != 0xffffffffu;
@@ -1802,13 +1858,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
           if (((desc >> 28) & 3u) == (tgen & 3u)) tmask = nm;
         }
         if (s + 1 == nsl) {  // batch done: rows still live enter the warp top-k
-          topk_insert(bs, bi, k, tacc, ctid, tlive);
+          topk_insert(bs, bi, k, tacc, ctid, tlive, a.dup);
           const uint32_t ks = (k + NW - 1) / NW;
           const uint32_t wi = __shfl_sync(FULL, bi, k - 1), wi2 = __shfl_sync(FULL, bi, ks - 1);
           const double ws = __shfl_sync(FULL, bs, k - 1), ws2 = __shfl_sync(FULL, bs, ks - 1);
           if (lane == 0) {
             if (wi != NONE) thr_v[w] = ws;
-            if (wi2 != NONE) thr2_v[w] = ws2;
+            // the warps' lists are disjoint only without duplicates
+            if (wi2 != NONE && !a.dup) thr2_v[w] = ws2;
           }
         }
       }
@@ -1833,7 +1890,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
     if (w == 0) {
       for (int w2 = 1; w2 < NW; ++w2) {
         const bool valid = (uint32_t)lane < k && mg_i[w2 * 32 + lane] != NONE;
-        topk_insert(bs, bi, k, mg_s[w2 * 32 + lane], mg_i[w2 * 32 + lane], valid);
+        topk_insert(bs, bi, k, mg_s[w2 * 32 + lane], mg_i[w2 * 32 + lane], valid, a.dup);
       }
       if ((uint32_t)lane < k) {
         const bool ok = bi != NONE;
@@ -2009,7 +2066,8 @@ static void stage_a(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
 // bucket walk + dedup, then row gather + fp64 dot + top-k.
 static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t nqc, uint32_t k,
                     uint32_t qprobes, uint32_t* ids_d, double* scores_d,
-                    fpp_query_stats* stats_d, cudaStream_t st, uint32_t rerank = 0) {
+                    fpp_query_stats* stats_d, cudaStream_t st, uint32_t rerank = 0,
+                    bool unique = false) {
   const uint64_t peff = query_probes(ix, qprobes);
   const uint64_t etot = sl.pinned[0];
   sl.cands.ensure(etot + 1);
@@ -2017,7 +2075,19 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   ix.timer.begin(PH_COLLECT, st, &e0);
   const uint32_t nwords = (uint32_t)((ix.n + 31) / 32);
   CollectArgs ca{sl.ppos.p, sl.plen.p, peff, ix.ids, sl.coff.p, sl.cands.p, sl.uq.p,
-                 nqc, nwords, nullptr, sl.counter.p};
+                 nqc, nwords, nullptr, sl.counter.p, 0};
+  // Dedup only where it pays: when the visited bitmap does not fit one SM's shared
+  // memory (n > ~1.8 M: the DSMEM cluster or global bitmaps) and ids rarely repeat
+  // (entries/unique < 1.25, e.g. C4's 1.08), the walked ids are scored with their
+  // repeats (grouped by id range) and the top-k lists skip repeated ids: same results,
+  // C4 collect 246 -> 71 ms.  The ratio is measured once per index on a dedup chunk;
+  // per-query stats (unique counts) and rerank screening always dedup.
+  // FPP_DEDUP=1 / FPP_NODEDUP=1 force either.
+  const bool force_dd = getenv("FPP_DEDUP") != nullptr, force_nd = getenv("FPP_NODEDUP") != nullptr;
+  const bool smem_bitmap = (int)((size_t)nwords * 4 + 64) <= co_smem_max();
+  const bool nodedup = !rerank && !stats_d && !unique && !force_dd &&
+                       (force_nd || (!smem_bitmap && ix.dup_ratio > 0.0 && ix.dup_ratio < 1.25));
+  const bool measure_dup = !nodedup && !rerank && ix.dup_ratio < 0.0;
   const size_t static_co = 64;
   size_t co_smem = (size_t)nwords * 4;
   unsigned co_grid;
@@ -2026,7 +2096,13 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   // FPP_FORCE_COLLECT=cluster|global selects a large-shard path at any n (tests)
   const char* force = getenv("FPP_FORCE_COLLECT");
   const bool f_cluster = force && !strcmp(force, "cluster"), f_global = force && !strcmp(force, "global");
-  if (!f_cluster && !f_global && (int)(co_smem + static_co) <= co_smem_max()) {
+  if (nodedup) {
+    ca.nodedup = 1;
+    while ((ix.n - 1) >> ca.bshift >= 256) ++ca.bshift;
+    co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * 2);
+    FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
+    k_collect<<<co_grid, CO_THREADS, 0, st>>>(ca);
+  } else if (!f_cluster && !f_global && (int)(co_smem + static_co) <= co_smem_max()) {
     FPP_CUDA(cudaFuncSetAttribute(k_collect, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)co_smem));
     int occ = 1;
@@ -2041,13 +2117,13 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
                                   (int)sm));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CO_CLUSTER);
-    cfg.blockDim = dim3(CO_THREADS);
+    cfg.blockDim = dim3(CO_CL_THREADS);
     cfg.dynamicSmemBytes = sm;
     cfg.stream = st;
     int ncl = 0;
     FPP_CUDA(cudaOccupancyMaxActiveClusters(&ncl, k_collect_cluster, &cfg));
     ncl = std::max(1, std::min<int>(ncl, (int)nqc));
-    k_collect_cluster<<<ncl * CO_CLUSTER, CO_THREADS, sm, st>>>(ca, slice_words);
+    k_collect_cluster<<<ncl * CO_CLUSTER, CO_CL_THREADS, sm, st>>>(ca, slice_words);
   } else {
     co_smem = 0;
     co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * 2);
@@ -2062,10 +2138,20 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   }
   FPP_LAUNCH();
   ix.timer.end(PH_COLLECT, e0, st);
+  if (measure_dup) {  // once per index: entries / unique candidates of this chunk
+    std::vector<uint32_t> he(nqc), hu(nqc);
+    FPP_CUDA(cudaMemcpyAsync(he.data(), sl.eq.p, nqc * 4, cudaMemcpyDeviceToHost, st));
+    FPP_CUDA(cudaMemcpyAsync(hu.data(), sl.uq.p, nqc * 4, cudaMemcpyDeviceToHost, st));
+    FPP_CUDA(cudaStreamSynchronize(st));
+    double se = 0, su = 0;
+    for (uint32_t i = 0; i < nqc; ++i) { se += he[i]; su += hu[i]; }
+    ix.dup_ratio = su > 0 ? se / su : 1e30;
+  }
 
   ix.timer.begin(PH_SCORE, st, &e0);
   ScoreArgs sa{ix.X, ix.d, ix.ldx, Qd, sl.coff.p, sl.cands.p, sl.uq.p, sl.eq.p, peff, k,
                ix.prm.id_offset, ids_d, scores_d, stats_d, nullptr, 0};
+  sa.dup = nodedup ? 1u : 0u;
   if (!ix.score_bytes_d.p) {
     ix.score_bytes_d.alloc(1);
     FPP_CUDA(cudaMemsetAsync(ix.score_bytes_d.p, 0, 8, st));
@@ -2360,7 +2446,7 @@ void query_debug(const Index& ix, const float* qd, uint32_t qprobes, std::vector
   Index::QSlot& sl = ix.slot[0];
   stage_a(ix, sl, qd, 1, qprobes, s, dbg.p);
   FPP_CUDA(cudaEventSynchronize(sl.ev_probe));
-  stage_b(ix, sl, qd, 1, 1, qprobes, ids.p, sc.p, nullptr, s);
+  stage_b(ix, sl, qd, 1, 1, qprobes, ids.p, sc.p, nullptr, s, 0, true);  // unique candidates
   FPP_CUDA(cudaStreamSynchronize(s));
   probes.resize(peff);
   FPP_CUDA(cudaMemcpy(probes.data(), dbg.p, peff * 8, cudaMemcpyDeviceToHost));

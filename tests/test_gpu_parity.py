@@ -488,3 +488,23 @@ def test_score_early_termination_unstructured(fpp, orc, monkeypatch):
     assert np.array_equal(gi, oi) and np.array_equal(gst, ost)
     ok = np.isfinite(os_)
     assert np.array_equal(gs[ok], os_[ok])
+
+
+@pytest.mark.parametrize("prune", ["0", "1"])
+def test_nodedup_collect_same_answers(fpp, orc, prune, monkeypatch):
+    # FPP_NODEDUP=1: the walked ids are scored with repeats (no visited bitmap) and the
+    # top-k lists skip repeated ids; ids and scores must equal the oracle's.  Stats
+    # requests always dedup (unique candidate counts).
+    monkeypatch.setenv("FPP_NODEDUP", "1")
+    monkeypatch.setenv("FPP_PRUNE" if prune == "1" else "FPP_NO_PRUNE", "1")
+    X = data(fpp, 20000, 128, 200, 0.25, seed=41)
+    Q = data(fpp, 300, 128, 200, 0.25, seed=41, stream=1)
+    ix = fpp.Index.build(X, L=12, K=2, D=128, iProbes=3, alpha=0.2)
+    ox = orc.Index(X, L=12, K=2, D=128, iprobes=3, alpha=0.2)
+    gi, gs = ix.query(Q, 20, 5000)
+    oi, os_, ost = ox.query(Q, 20, 5000)
+    assert np.array_equal(gi, oi)
+    ok = np.isfinite(os_)
+    assert np.array_equal(gs[ok], os_[ok])
+    si, ss, sst = ix.query(Q, 20, 5000, return_stats=True)
+    assert np.array_equal(si, oi) and np.array_equal(sst, ost)
