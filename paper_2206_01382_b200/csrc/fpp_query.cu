@@ -1008,20 +1008,28 @@ __device__ __forceinline__ void collect_walk(const uint64_t* pp, const uint32_t*
     }
     const uint32_t T = __shfl_sync(FULL, incl, 31);
     const uint32_t excl = incl - len;
+    // the chunk's non-empty probes, compacted: lane r holds the r-th one's first
+    // entry (cex) and bucket position
+    const uint32_t ne = __ballot_sync(FULL, len > 0);
+    const bool cval = (uint32_t)lane < (uint32_t)__popc(ne);
+    const uint32_t src = cval ? __fns(ne, 0, lane + 1) : 0u;
+    const uint32_t cex = __shfl_sync(FULL, excl, src);
+    const uint32_t cplo = __shfl_sync(FULL, (uint32_t)pos, src);
+    const uint32_t cphi = __shfl_sync(FULL, (uint32_t)(pos >> 32), src);
     for (uint32_t e0 = 0; e0 < T; e0 += 32 * CO_UNROLL) {
       uint32_t idv[CO_UNROLL];
 #pragma unroll
       for (int u = 0; u < CO_UNROLL; ++u) {
-        const uint32_t e = e0 + 32 * u + lane;
-        uint32_t lo = 0;  // largest lane with excl <= e (it has len > 0 when e < T)
-#pragma unroll
-        for (int st = 16; st > 0; st >>= 1) {
-          const uint32_t cnd = lo + st;
-          if (__shfl_sync(FULL, excl, cnd) <= e) lo = cnd;
-        }
-        const uint32_t plo = __shfl_sync(FULL, (uint32_t)pos, lo);
-        const uint32_t phi = __shfl_sync(FULL, (uint32_t)(pos >> 32), lo);
-        const uint32_t ex = __shfl_sync(FULL, excl, lo);
+        // entries E0 .. E0+31: the probe holding E0 (r0) plus the probes starting inside
+        // the window (a 32-bit mask, one warp reduction) place every lane's entry
+        const uint32_t E0 = e0 + 32 * u, e = E0 + lane;
+        const uint32_t r0 = __popc(__ballot_sync(FULL, cval && cex <= E0)) - 1u;
+        const uint32_t dd = cex - E0;
+        const uint32_t sm = __reduce_or_sync(FULL, (cval && cex > E0 && dd < 32u) ? (1u << dd) : 0u);
+        const uint32_t r = r0 + __popc(sm & ((2u << lane) - 1u));
+        const uint32_t plo = __shfl_sync(FULL, cplo, r);
+        const uint32_t phi = __shfl_sync(FULL, cphi, r);
+        const uint32_t ex = __shfl_sync(FULL, cex, r);
         idv[u] = e < T ? __ldg(ids + ((((uint64_t)phi << 32) | plo) + (e - ex))) : 0xffffffffu;
       }
 #pragma unroll
