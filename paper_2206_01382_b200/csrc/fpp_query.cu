@@ -2234,7 +2234,8 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
       sa.dbg = ix.prune_d.p;
     }
     // ring geometry (FPP_SC_PR = NW,ST,MINB digits; default 4 warps x 2 stages, 3 CTAs/SM:
-    // C2 score 8.0 ms vs 11.2 (4x3 @ 2/SM), 12.9 (2x4 @ 3/SM), 20.7 (4x4 @ 1/SM))
+    // C2 score 8.0 ms vs 11.2 (4x3 @ 2/SM, kept for the tests), 12.9 (2x4 @ 3/SM) and
+    // 20.7 (4x4 @ 1/SM))
     auto launch_pruned = [&](auto kern, int nw, int stg) {
       const size_t sm = (size_t)nw * stg * 32 * XT_SLICE * 4 + ((ix.d * 8 + 127) / 128) * 128;
       FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -2260,8 +2261,6 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     break;
     switch (pr) {
       FPP_PR_CASE(4, 3, 2)
-      FPP_PR_CASE(2, 4, 3)
-      FPP_PR_CASE(4, 4, 1)
       default:
       FPP_PR_CASE(4, 2, 3)
     }
