@@ -217,14 +217,14 @@ __global__ void k_center_sub(float* __restrict__ X, uint64_t n, uint32_t d, uint
 // warp per row; fp64 sums of exact squares per segment, suffix-combined; sqrt
 // rounded up to fp32 (with a 1e-12 relative margin for the summation error).
 __global__ void k_tail_norms(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx,
-                             uint32_t nt, float* __restrict__ xt) {
+                             uint32_t nt, uint32_t head, float* __restrict__ xt) {
   const int lane = threadIdx.x & 31;
   const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
     const float* r = X + i * ldx;
     double seg[XT_MAX] = {0.0, 0.0, 0.0, 0.0};
-    for (uint32_t c = XT_SLICE + lane; c < d; c += 32) {
-      const uint32_t j = min(c / XT_SLICE - 1, nt - 1);
+    for (uint32_t c = head + lane; c < d; c += 32) {
+      const uint32_t j = min((c - head) / XT_SLICE, nt - 1);
       const double v = (double)r[c];
 #pragma unroll
       for (uint32_t t = 0; t < XT_MAX; ++t)
@@ -242,11 +242,16 @@ __global__ void k_tail_norms(const float* __restrict__ X, uint64_t n, uint32_t d
 }
 
 void launch_tail_norms(Index& ix) {
-  const uint32_t nsl = (ix.d + XT_SLICE - 1) / XT_SLICE;
+  // head width: 32 floats for rows of <= 192 floats (C4's d = 128: the score gather is
+  // HBM-bound there and a far candidate then costs 128 B instead of 256 B: 157k -> 200k
+  // q/s), else 64 (C2's d = 300 is latency-bound: a narrower head only adds a tail job
+  // per survivor, 10.2 vs 7.7 ms)
+  ix.xt_head = ix.d <= 192 ? 32u : 64u;
+  const uint32_t nsl = xt_nslices(ix.d, ix.xt_head);
   ix.xt_n = ix.d >= XT_SLICE ? std::min<uint32_t>(nsl - 1, XT_MAX) : 0;
   if (!ix.xt_n) return;
   ix.xtail = static_cast<float*>(dmalloc((size_t)ix.xt_n * ix.n * sizeof(float)));
-  k_tail_norms<<<sm_count() * 8, 256, 0, ix.stream>>>(ix.X, ix.n, ix.d, ix.ldx, ix.xt_n, ix.xtail);
+  k_tail_norms<<<sm_count() * 8, 256, 0, ix.stream>>>(ix.X, ix.n, ix.d, ix.ldx, ix.xt_n, ix.xt_head, ix.xtail);
   FPP_LAUNCH();
 }
 

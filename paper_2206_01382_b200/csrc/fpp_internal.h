@@ -91,6 +91,7 @@ struct Index {
   // ||X[i][(j+1)*XT_SLICE:d)||, rounded up to fp32, checkpoints j < xt_n
   float* xtail = nullptr;
   uint32_t xt_n = 0;
+  uint32_t xt_head = 64;  // head (screening) slice width, see launch_tail_norms
   std::vector<float> center;  // [d] when prm.centering (dataset.cpp center())
   uint64_t device_bytes = 0;
   ShardState* shard = nullptr;  // global-filter sharded build in progress
@@ -173,6 +174,11 @@ void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint32_t ld
                        cudaStream_t s);
 constexpr uint32_t XT_SLICE = 64;  // = the score ring's row-slice width for d >= 64
 constexpr uint32_t XT_MAX = 4;     // tail-norm checkpoints per row
+// score-gather slices of a d-wide row: a head [0, h) (h = Index::xt_head, 32 or 64),
+// then XT_SLICE-wide slices; checkpoint j (after slice j) is column h + j * XT_SLICE
+__host__ __device__ inline uint32_t xt_nslices(uint32_t d, uint32_t h) {
+  return d <= h ? 1u : 1u + (d - h + XT_SLICE - 1) / XT_SLICE;
+}
 void launch_tail_norms(Index& ix);
 void launch_order_keys(const Index& ix, const float* Qd, uint64_t n, uint64_t* out, cudaStream_t s);
 void run_brute_force(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t* ids_d,

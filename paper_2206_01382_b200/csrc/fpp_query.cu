@@ -1348,6 +1348,7 @@ struct ScoreArgs {
   uint32_t nq;
   const float* xtail;      // k_score_pruned: row tail norms [xt_n][n] (Index::xtail)
   uint32_t xt_n;
+  uint32_t xt_head;        // head slice width (Index::xt_head)
   uint64_t n;
   unsigned long long* dbg;  // FPP_DEBUG_PRUNE: [rows, row slices read]
   unsigned long long* rbytes;  // += candidate-row bytes read (fpp_timings.score_bytes)
@@ -1632,8 +1633,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int kk = lane & 7, rbase = lane >> 3;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  const uint32_t nsl = (d + SL - 1) / SL;  // >= 2 (host: d > 64)
-  const uint32_t nt = a.xt_n;              // checks after slices 0 .. nt-1 (nt < nsl)
+  const uint32_t hw = a.xt_head;           // head slice width (32 or 64)
+  const uint32_t nsl = xt_nslices(d, hw);  // head [0, hw) + 64-wide slices; >= 2 (host: d >= 64)
+  const uint32_t nt = a.xt_n;          // checks after slices 0 .. nt-1 (nt < nsl)
+  auto col0_of = [&](uint32_t sl) { return sl == 0 ? 0u : hw + (sl - 1) * (uint32_t)SL; };
+  auto len_of = [&](uint32_t sl) {
+    return sl == 0 ? min(hw, d) : min((uint32_t)SL, d - col0_of(sl));
+  };
   float* wring = ring + (size_t)w * ST * STAGE;
   double* qacc = sq_acc[w];
   uint32_t* qid = sq_id[w];
@@ -1658,7 +1664,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
     if ((uint32_t)w < nt) {  // query tail norms, rounded up
       for (uint32_t t = w; t < nt; t += NW) {
         double sq = 0.0;
-        for (uint32_t c = (t + 1) * SL + lane; c < d; c += 32) sq = fma(qd[c], qd[c], sq);
+        for (uint32_t c = hw + t * SL + lane; c < d; c += 32) sq = fma(qd[c], qd[c], sq);
         for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(FULL, sq, o);
         if (lane == 0) qt_s[t] = __dsqrt_ru(sq) * (1.0 + 1e-12);
       }
@@ -1710,14 +1716,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
       }
       if ((type == J_HEAD || type == J_TAIL) && m) {
         float* buf = wring + (size_t)islot * STAGE;
-        const uint32_t col0 = s * SL;
-        const uint32_t len = min((uint32_t)SL, d - col0);
+        const uint32_t col0 = col0_of(s);
+        const uint32_t len = len_of(s);
         const uint32_t rows = __ballot_sync(FULL, (type == J_HEAD ? jid : bid) != NONE);
         wbytes += (unsigned long long)__popc(rows & m) * len * 4u;
         if (a.dbg) {
           if (lane == 0) {
             if (type == J_HEAD) atomicAdd(a.dbg, (unsigned long long)__popc(rows));
-            atomicAdd(a.dbg + 1, (unsigned long long)__popc(rows & m));
+            atomicAdd(a.dbg + 1, (unsigned long long)__popc(rows & m) * len);  // floats read
           }
         }
         if (TMA) {  // lane r copies row r's slice (rotated by r & 15: at most two copies)
@@ -1792,13 +1798,22 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
       const float* row = wring + (size_t)cslot * STAGE + lane * SL;
       const int sw = lane & 15;
       auto fold = [&](double acc) {
-        const uint32_t col0 = s * SL;
-        const uint32_t len = min((uint32_t)SL, d - col0);
+        const uint32_t col0 = col0_of(s);
+        const uint32_t len = len_of(s);
         const double* qq = qd + col0;
         // dataset.cpp:67 acc += double(a[i]) * double(b[i]), sequential i (exact products)
         if (VEC && len == SL) {
 #pragma unroll
           for (int j = 0; j < SL; j += 4) {
+            const float4 xv = *reinterpret_cast<const float4*>(row + ((((j >> 2) + sw) & 15) << 2));
+            acc = fma((double)xv.x, qq[j], acc);
+            acc = fma((double)xv.y, qq[j + 1], acc);
+            acc = fma((double)xv.z, qq[j + 2], acc);
+            acc = fma((double)xv.w, qq[j + 3], acc);
+          }
+        } else if (VEC && len == 32) {  // a 32-wide head slice
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
             const float4 xv = *reinterpret_cast<const float4*>(row + ((((j >> 2) + sw) & 15) << 2));
             acc = fma((double)xv.x, qq[j], acc);
             acc = fma((double)xv.y, qq[j + 1], acc);
@@ -2212,8 +2227,7 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   bool use_pruned = false, probe = false;
   if (ix.xt_n && !no_prune) {
     if (ix.prune_pending && cudaEventQuery(ix.prune_ev) == cudaSuccess) {
-      const double nslf = (double)((ix.d + XT_SLICE - 1) / XT_SLICE);
-      if (ix.prune_h[0]) ix.prune_frac = (double)ix.prune_h[1] / ((double)ix.prune_h[0] * nslf);
+      if (ix.prune_h[0]) ix.prune_frac = (double)ix.prune_h[1] / ((double)ix.prune_h[0] * ix.d);
       ix.prune_pending = false;
     }
     probe = dbg || (!ix.prune_pending && (ix.prune_frac < 0 || ix.prune_chunks % 16 == 0));
@@ -2223,6 +2237,7 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   if (use_pruned) {
     sa.xtail = ix.xtail;
     sa.xt_n = ix.xt_n;
+    sa.xt_head = ix.xt_head;
     sa.n = ix.n;
     if (probe) {
       if (!ix.prune_h) {
@@ -2272,9 +2287,8 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
       if (dbg) {
         FPP_CUDA(cudaEventSynchronize(ix.prune_ev));
         const unsigned long long* h = ix.prune_h;
-        const double nsl = (double)((ix.d + XT_SLICE - 1) / XT_SLICE);
-        fprintf(stderr, "[prune dbg] rows %llu, slices read per row %.3f of %.0f (%.1f%% of row bytes)\n",
-                h[0], h[0] ? (double)h[1] / h[0] : 0.0, nsl, h[0] ? 100.0 * h[1] / h[0] / nsl : 0.0);
+        fprintf(stderr, "[prune dbg] rows %llu, floats read per row %.1f of %u (%.1f%% of row bytes)\n",
+                h[0], h[0] ? (double)h[1] / h[0] : 0.0, ix.d, h[0] ? 100.0 * h[1] / h[0] / ix.d : 0.0);
       }
     }
   } else if ((ix.d & 3u) == 0) {
