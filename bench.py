@@ -499,11 +499,14 @@ def main():
     import torch as _t
     Qh = _t.empty((nq, d), dtype=_t.float32).pin_memory().numpy()
     Qh[:] = Q
-    ix.query(Qh, K_TOP, qprobes)
+    # page-locked result buffers too: the device writes ids/scores straight into them
+    ids_h = _t.empty((nq, K_TOP), dtype=_t.int32).pin_memory().numpy().view(np.uint32)
+    sc_h = _t.empty((nq, K_TOP), dtype=_t.float64).pin_memory().numpy()
+    ix.query(Qh, K_TOP, qprobes, out=(ids_h, sc_h))
     barrier()
     te0 = time.perf_counter()
     for _ in range(args.steps):
-        ids_h, sc_h = ix.query(Qh, K_TOP, qprobes)
+        ix.query(Qh, K_TOP, qprobes, out=(ids_h, sc_h))
         if world > 1:
             s_t = torch.from_numpy(sc_h).cuda()
             i_t = torch.from_numpy(ids_h.astype(np.int64)).cuda()

@@ -358,20 +358,30 @@ class Index:
         self.__del__()
 
     # --------------------------------------------------------------- query
-    def query(self, Q, k: int, qProbes: int, return_stats: bool = False, rerank: int = 0):
+    def query(self, Q, k: int, qProbes: int, return_stats: bool = False, rerank: int = 0,
+              out=None):
         """Index::query(Q, k, qProbes) -- SPEC.md:321-329, batch over rows of Q.
 
         rerank = SimHash budget B (0 = off, else B >= k).
         Returns ids [nq,k] uint32 (0xFFFFFFFF past min(k,U)), scores [nq,k] fp64
         (-inf past min(k,U)) and optionally stats [nq,4] (probes, entries,
-        candidates collected, exact inner products).
+        candidates collected, exact inner products).  out = (ids, scores): caller-owned
+        C-contiguous result arrays (e.g. page-locked, so the device writes them directly).
         """
         Q = _f32(Q)
         if Q.shape[1] != self.d:
             raise FppDimensionError(f"search: query dim {Q.shape[1]} != index dim {self.d}")
         nq = Q.shape[0]
-        ids = np.empty((nq, k), np.uint32)
-        sc = np.empty((nq, k), np.float64)
+        if out is not None:
+            ids, sc = out
+            if (ids.shape != (nq, k) or ids.dtype != np.uint32 or not ids.flags.c_contiguous
+                    or sc.shape != (nq, k) or sc.dtype != np.float64
+                    or not sc.flags.c_contiguous):
+                raise ValueError("query: out must be (uint32 [nq,k], float64 [nq,k]) "
+                                 "C-contiguous arrays")
+        else:
+            ids = np.empty((nq, k), np.uint32)
+            sc = np.empty((nq, k), np.float64)
         st = (QueryStats * max(nq, 1))() if return_stats else None
         stp = C.cast(st, C.c_void_p) if st is not None else None
         if rerank:

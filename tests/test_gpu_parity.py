@@ -508,3 +508,19 @@ def test_nodedup_collect_same_answers(fpp, orc, prune, monkeypatch):
     assert np.array_equal(gs[ok], os_[ok])
     si, ss, sst = ix.query(Q, 20, 5000, return_stats=True)
     assert np.array_equal(si, oi) and np.array_equal(sst, ost)
+
+
+def test_query_out_buffers(fpp, orc):
+    # query(..., out=(ids, scores)) writes into caller-owned arrays (bench.py's e2e leg
+    # passes page-locked ones): same answers as the allocating call; bad shapes rejected
+    X = data(fpp, 5000, 64, 20, 0.3, seed=7)
+    Q = data(fpp, 50, 64, 20, 0.3, seed=7, stream=1)
+    ix = fpp.Index.build(X, L=6, K=2, D=64, iProbes=3, alpha=0.2)
+    gi, gs = ix.query(Q, 10, 300)
+    oi = np.zeros((50, 10), np.uint32)
+    os_ = np.zeros((50, 10), np.float64)
+    ri, rs = ix.query(Q, 10, 300, out=(oi, os_))
+    assert ri is oi and rs is os_
+    assert np.array_equal(oi, gi) and np.array_equal(os_, gs)
+    with pytest.raises(ValueError):
+        ix.query(Q, 10, 300, out=(np.zeros((50, 9), np.uint32), os_))
