@@ -976,7 +976,10 @@ struct CollectArgs {
 // CO_UNROLL rounds issue their id loads before any is consumed.  `tas(id)`
 // tests-and-sets the visited bit and returns whether the id is new; new ids are
 // appended to `out` with one counter atomic per warp round.
-constexpr int CO_UNROLL = 8;
+#ifndef FPP_CO_UNROLL
+#define FPP_CO_UNROLL 8
+#endif
+constexpr int CO_UNROLL = FPP_CO_UNROLL;
 template <class NextChunk, class TAS>
 __device__ __forceinline__ void collect_walk(const uint64_t* pp, const uint32_t* pl, uint32_t P,
                                              const uint32_t* __restrict__ ids, uint32_t* out,
