@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
       __syncthreads();
       // warp per grid: the row arm vb[r0, nb) and the column arm va[1, na), lanes
       // strided (coalesced), 8 loads per lane in flight
-      constexpr int AU = 8;
+      constexpr int AU = 16;  // one pass per grid for arms of up to 512 entries (C2: 399)
       for (uint32_t gi = wp; gi < NG; gi += nw) {
         const GridRef g = grid(sel, gi);
         const PairKey<MODE> pk{g.ma, g.mb};
