@@ -681,6 +681,14 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
       for (uint32_t gi = wp; gi < NG; gi += nw) {
         const GridRef g = grid(sel, gi);
         const PairKey<MODE> pk{g.ma, g.mb};
+        if (gi + nw < NG) {  // the next grid's list heads into L1 while this one is walked
+          const GridRef gn = grid(sel, gi + nw);
+          const uint32_t la = (min(gn.na, 64u) + 31) / 32, lb = (gn.nb + 31) / 32;
+          if ((uint32_t)lane < la)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(gn.va + lane * 32));
+          else if ((uint32_t)lane < la + lb)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(gn.vb + (lane - la) * 32));
+        }
         uint32_t pb = g.nb, r1 = 0;
         for (; r1 < g.na && pb > 32; ++r1) {
           const float x = g.va[r1];
