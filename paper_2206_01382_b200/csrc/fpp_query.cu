@@ -2118,7 +2118,9 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   // per-query stats (unique counts) and rerank screening always dedup.
   // FPP_DEDUP=1 / FPP_NODEDUP=1 force either.
   const bool force_dd = getenv("FPP_DEDUP") != nullptr, force_nd = getenv("FPP_NODEDUP") != nullptr;
-  const bool smem_bitmap = (int)((size_t)nwords * 4 + 64) <= co_smem_max();
+  // (FPP_FORCE_COLLECT=cluster|global also counts as an off-chip bitmap here: tests)
+  const char* force_co = getenv("FPP_FORCE_COLLECT");
+  const bool smem_bitmap = !force_co && (int)((size_t)nwords * 4 + 64) <= co_smem_max();
   const bool nodedup = !rerank && !stats_d && !unique && !force_dd &&
                        (force_nd || (!smem_bitmap && ix.dup_ratio > 0.0 && ix.dup_ratio < 1.25));
   const bool measure_dup = !nodedup && !rerank && ix.dup_ratio < 0.0;

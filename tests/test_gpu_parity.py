@@ -524,3 +524,21 @@ def test_query_out_buffers(fpp, orc):
     assert np.array_equal(oi, gi) and np.array_equal(os_, gs)
     with pytest.raises(ValueError):
         ix.query(Q, 10, 300, out=(np.zeros((50, 9), np.uint32), os_))
+
+
+def test_dedup_policy_auto_switch(fpp, orc, monkeypatch):
+    # with an off-chip visited bitmap (forced here) and few repeated ids, the first
+    # query call measures entries/unique on a dedup chunk and later calls collect
+    # without dedup; every call must return the oracle's answers
+    monkeypatch.setenv("FPP_FORCE_COLLECT", "cluster")
+    X = data(fpp, 30000, 128, 0, 0.0, seed=9)
+    Q = data(fpp, 200, 128, 0, 0.0, seed=9, stream=1)
+    ix = fpp.Index.build(X, L=4, K=2, D=128, iProbes=2, alpha=0.5)
+    ox = orc.Index(X, L=4, K=2, D=128, iprobes=2, alpha=0.5)
+    oi, os_, ost = ox.query(Q, 10, 400)
+    ok = np.isfinite(os_)
+    assert (ost[:, 1].sum() / max(1, ost[:, 2].sum())) < 1.25  # few repeats
+    for _ in range(3):
+        gi, gs = ix.query(Q, 10, 400)
+        assert np.array_equal(gi, oi)
+        assert np.array_equal(gs[ok], os_[ok])
