@@ -493,7 +493,10 @@ def main():
         except Exception:
             traffic = None
     launches_per_step = tim["launches"] / args.steps
-    score_launches_per_step = max(1.0, launches_per_step / 5.0)  # 5 kernels per query chunk
+    # 5 kernels per query chunk (lists, probe select, scan, collect, score) plus 5 for
+    # the batch reorder (nq >= 256 and nq*d >= 512k, fpp_query.cu run_query)
+    reorder = nq >= 256 and nq * d >= 512 * 1024
+    score_launches_per_step = max(1.0, (launches_per_step - (5 if reorder else 0)) / 5.0)
 
     # --------------------------------------------------------- e2e (host API)
     import torch as _t
