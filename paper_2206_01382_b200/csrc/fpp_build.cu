@@ -109,14 +109,27 @@ __device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], in
       }
       for (uint32_t i = ctot + g; i < (uint32_t)HB_SEL; i += S::G) scratch[i] = ~0ull;
       __syncwarp();
+      // the r smallest of the <= HB_SEL kept keys, in order: r rounds of a group
+      // minimum (keys are unique: they carry the index), the owner retiring its key
+      // (cheaper than sorting all HB_SEL 64-bit keys when r << HB_SEL)
       constexpr int E = HB_SEL / S::G;
       uint64_t k[E];
 #pragma unroll
       for (int e = 0; e < E; ++e) k[e] = scratch[g * E + e];
-      group_bitonic_sort<HB_SEL, E>(k, g);
+      for (uint32_t qq = 0; qq < r; ++qq) {
+        uint64_t m = k[0];
 #pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (g * E + e < R) sel[g * E + e] = k[e];
+        for (int e = 1; e < E; ++e) m = k[e] < m ? k[e] : m;
+#pragma unroll
+        for (int o = 1; o < S::G; o <<= 1) {
+          const uint64_t y = shfl_xor_u64(m, o);
+          m = y < m ? y : m;
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (k[e] == m) k[e] = ~0ull;
+        if (g == 0) sel[qq] = m;
+      }
       __syncwarp();
     }
   }
