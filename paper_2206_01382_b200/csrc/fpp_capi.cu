@@ -247,7 +247,10 @@ void launch_tail_norms(Index& ix) {
   // q/s), else 64 (C2's d = 300 is latency-bound: a narrower head only adds a tail job
   // per survivor, 10.2 vs 7.7 ms)
   ix.xt_head = ix.d <= 192 ? 32u : 64u;
-  if (getenv("FPP_XT_HEAD")) ix.xt_head = (uint32_t)atoi(getenv("FPP_XT_HEAD"));  // experiments
+  if (getenv("FPP_XT_HEAD")) {  // experiments: a multiple of 4 in [32, 64]
+    const int h = atoi(getenv("FPP_XT_HEAD"));
+    if (h >= 32 && h <= 64 && h % 4 == 0) ix.xt_head = (uint32_t)h;
+  }
   const uint32_t nsl = xt_nslices(ix.d, ix.xt_head);
   ix.xt_n = ix.d >= XT_SLICE ? std::min<uint32_t>(nsl - 1, XT_MAX) : 0;
   if (!ix.xt_n) return;
