@@ -1967,7 +1967,9 @@ void launch_query_lists(const Index& ix, const float* Qd, uint64_t nq, uint32_t 
   // preselection width: the smallest of P/4, P/2 leaving a margin of P/16 above
   // nat = min(s, D) (0 = sort all P keys)
   const uint32_t nat = std::min(s_cap, D), P = ix.P;
-  const int ns = P < 256 ? 0 : (nat + P / 16 <= P / 4 ? 4 : (nat + P / 16 <= P / 2 ? 2 : 0));
+  // (margin P/32 for P = 1024: C3's nat = 200 then sorts 256 of 1024 keys, not 512)
+  const uint32_t marg = P >= 1024 ? P / 32 : P / 16;
+  const int ns = P < 256 ? 0 : (nat + marg <= P / 4 ? 4 : (nat + marg <= P / 2 ? 2 : 0));
 #define FPP_QL_LAUNCH(PP, NSV) \
   k_query_lists<PP, NSV><<<grid, 128, 0, s>>>(Qd, nq, d, D, K, ix.signs, L, s_cap, lstride, vals, codes)
 #define FPP_QL_CASE(PP)         \
