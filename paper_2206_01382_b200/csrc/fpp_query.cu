@@ -14,14 +14,20 @@
 //                   threshold search on the fp32 pair score (two-sided prefix
 //                   counts over the sorted lists), tie resolution in
 //                   (r1, r2, t) order, then directory reads -> (pos, len)
-//   k_collect       CTA per query: walk kept entries, test-and-set a visited
-//                   bitmap (shared memory, or global for large shards),
-//                   compact unique ids
+//   k_collect       CTA per query: walk kept entries, OR them into a visited
+//                   bitmap (shared memory; an 8-CTA DSMEM cluster or global
+//                   memory for large shards) and emit unique ids in ascending
+//                   order -- or, where ids rarely repeat and the bitmap is
+//                   off-chip, copy them grouped by id range (no dedup)
 //   k_score         CTA per query: 32-row batches per warp, cp.async column
 //                   slices into shared memory (multi-stage ring), each lane
 //                   accumulates its row's exact products in fp64 in the
 //                   reference's sequential order (bit-identical scores), warp
 //                   register top-k, CTA merge
+//   k_score_pruned  the same scores with exact early termination: row heads,
+//                   a Cauchy-Schwarz bound on the unread tail against the
+//                   running k-th best, survivors finished as dense batches
+//                   (chosen per index by the measured read fraction)
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
