@@ -2284,7 +2284,9 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
       kern<<<grid, nw * 32, sm, st>>>(sa);
     };
     const char* prc = getenv("FPP_SC_PR");
-    const int pr = prc ? atoi(prc) : 423;
+    // narrow rows (32-float heads, d <= 192): 3-warp CTAs, 4 per SM (C4 score 411 -> 395
+    // ms); wider rows: 4-warp CTAs, 3 per SM (C2 7.5 ms vs 8.8 with 3 warps)
+    const int pr = prc ? atoi(prc) : (ix.xt_head == 32 ? 324 : 423);
     const bool vec = (ix.d & 3u) == 0;
     // FPP_SC_TMA=1: TMA bulk row copies instead of the cp.async ring.  Measured slower
     // (C2 score 12.4 vs 7.6 ms: 256 B bulk copies are TMA-issue bound), kept as an option
@@ -2297,6 +2299,7 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     break;
     switch (pr) {
       FPP_PR_CASE(4, 3, 2)
+      FPP_PR_CASE(3, 2, 4)
       default:
       FPP_PR_CASE(4, 2, 3)
     }
