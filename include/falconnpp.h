@@ -13,7 +13,9 @@
  * std::invalid_argument with the same messages, e.g. dataset.cpp:10-18).
  * Host buffers are read/written synchronously before return.  The library owns
  * all device memory behind the opaque fpp_index.  A built index is immutable;
- * concurrent fpp_query calls on one index are allowed.
+ * concurrent fpp_query calls on one index are allowed: each call
+ * leases its own scratch context (own streams), so calls from several host
+ * threads run side by side on the device.
  * There is no CPU fallback: without a CUDA device every compute entry point
  * returns FPP_ERR_CUDA.
  */
@@ -26,7 +28,8 @@
 extern "C" {
 #endif
 
-#define FPP_ABI_VERSION 3  /* 2: fpp_query_stats.exact, SimHash rerank; 3: fpp_timings.score_bytes */
+#define FPP_ABI_VERSION 4  /* 2: fpp_query_stats.exact, SimHash rerank; 3: fpp_timings.score_bytes;
+                              4: fpp_synth_rows, fpp_merge_topk, per-call query contexts */
 
 /* error classes ("one exit code per error class") */
 #define FPP_OK 0
@@ -114,8 +117,9 @@ void fpp_free(fpp_index* idx);
 int fpp_query(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uint32_t qprobes,
               uint32_t* ids, double* scores, fpp_query_stats* stats);
 /* device-resident variant: Q_dev, ids_dev, scores_dev, stats_dev on the index device;
-   stream is a cudaStream_t (NULL = library stream), asynchronous w.r.t. the host
-   except for one small readback per query chunk. */
+   stream is a cudaStream_t (NULL = the call context's stream), asynchronous w.r.t.
+   the host except for one small readback per query chunk (the chunk's candidate
+   total, which sizes its candidate buffer). */
 int fpp_query_device(const fpp_index* idx, const float* Q_dev, uint64_t nq, uint32_t k,
                      uint32_t qprobes, uint32_t* ids_dev, double* scores_dev,
                      fpp_query_stats* stats_dev, void* stream);
@@ -148,6 +152,7 @@ typedef struct fpp_index_info {
   uint32_t id_offset;
   uint32_t centering;     /* indexed rows are centered (fpp_index_center) */
   uint32_t mode;          /* FPP_MODE_* */
+  int32_t device;         /* CUDA device ordinal holding the index (ABI 4) */
 } fpp_index_info;
 
 int fpp_index_info_get(const fpp_index* idx, fpp_index_info* info);
@@ -194,6 +199,15 @@ int fpp_shard_finish(fpp_index* idx, const uint32_t* global_hist_dev,
                      const uint64_t* all_prefix_dev, uint32_t world);
 
 /* -------------------------------------------------------------- host helpers */
+/* ---- multi-GPU query merge: after an all-gather of the G shards'
+ * per-query top-k lists, scores/ids [lists][nq][k] on `device` (each list sorted by
+ * score desc, id asc; empty slots id 0xFFFFFFFF / -inf) are merged into
+ * out [nq][k] by the same key order on the device (k-way merge kernel).  The shard
+ * lists must hold disjoint (global) ids.  lists, k <= 32.  Asynchronous on stream. */
+int fpp_merge_topk(const double* scores_dev, const uint32_t* ids_dev, uint32_t lists, uint64_t nq,
+                   uint32_t k, double* out_scores_dev, uint32_t* out_ids_dev, int device,
+                   void* stream);
+
 /* ---- exact brute force over the index's dataset: the recall ground truth
  * (SPEC.md:490-503 brute_force_topk).  Scores are inner_product (dataset.cpp:61-69)
  * bit for bit; top-k by (score desc, id asc), ids global (id_offset added).
@@ -233,6 +247,9 @@ int fpp_normalize(float* X, uint64_t n, uint32_t d);
    stream selects independent draws (0 = data, 1 = queries); rows NOT normalized. */
 int fpp_synth(float* X, uint64_t n, uint32_t d, uint32_t clusters, float sigma, uint64_t seed,
               uint32_t stream, int threads);
+/* rows [row0, row0 + n) of the same dataset (a shard's rows) */
+int fpp_synth_rows(float* X, uint64_t row0, uint64_t n, uint32_t d, uint32_t clusters, float sigma,
+                   uint64_t seed, uint32_t stream, int threads);
 
 #ifdef __cplusplus
 }

@@ -494,56 +494,59 @@ orc_index* orc_build(const float* X, uint64_t n, uint32_t d, const orc_params* p
   const uint64_t ne = n * ip;
   uint32_t* eb = (uint32_t*)malloc(ne * sizeof(uint32_t));
   float* es = (float*)malloc(ne * sizeof(float));
-  uint32_t* cnt = (uint32_t*)malloc(((size_t)NB + 1) * sizeof(uint32_t));
-  entry* sorted = (entry*)malloc(ne * sizeof(entry));
   for (uint32_t t = t_begin; t < t_end; ++t) {
     /* Alg. 1 lines 2-4: every point into its top-iProbes buckets */
-#pragma omp parallel num_threads(threads)
-    {
-      float* proj = (float*)malloc((size_t)K * D * sizeof(float));
-      float* buf = (float*)malloc((size_t)P * sizeof(float));
-#pragma omp for schedule(static)
-      for (int64_t i = 0; i < (int64_t)n; ++i) {
-        for (uint32_t f = 0; f < K; ++f)
-          project_signs(stack_signs(idx, t, f), d, P, D, X + (uint64_t)i * d, proj + f * D, buf);
-        orc_index_probes(proj, K, D, ip, eb + (uint64_t)i * ip, es + (uint64_t)i * ip);
-      }
-      free(proj);
-      free(buf);
-    }
-    /* bucket the entries (stable counting sort), then sort each bucket */
-    memset(cnt, 0, ((size_t)NB + 1) * sizeof(uint32_t));
-    for (uint64_t e = 0; e < ne; ++e) cnt[eb[e] + 1]++;
-    for (uint32_t b = 0; b < NB; ++b) cnt[b + 1] += cnt[b];
-    uint32_t* cur = (uint32_t*)malloc((size_t)NB * sizeof(uint32_t));
-    memcpy(cur, cnt, (size_t)NB * sizeof(uint32_t));
-    for (uint64_t e = 0; e < ne; ++e) {
-      entry en = {es[e], (uint32_t)(e / ip)};
-      sorted[cur[eb[e]]++] = en;
-    }
-    free(cur);
+    orc_index_probes_rows_mt(idx, X, n, t, eb, es, threads);
     uint32_t* off = (uint32_t*)malloc(((size_t)NB + 1) * sizeof(uint32_t));
-    off[0] = 0;
-    for (uint32_t b = 0; b < NB; ++b)
-      off[b + 1] = off[b] + keep_count(cnt[b + 1] - cnt[b], prm->alpha, ip, prm->kappa);
-    const uint32_t total = off[NB];
-    uint32_t* ids = (uint32_t*)malloc(((size_t)total + 1) * sizeof(uint32_t));
-    float* sc = (float*)malloc(((size_t)total + 1) * sizeof(float));
-#pragma omp parallel for schedule(dynamic, 1024) num_threads(threads)
-    for (int64_t b = 0; b < (int64_t)NB; ++b) {
-      const uint32_t B = cnt[b + 1] - cnt[b];
-      if (!B) continue;
-      entry* seg = sorted + cnt[b];
-      qsort(seg, B, sizeof(entry), cmp_entry);  /* (score desc, id asc) */
-      const uint32_t kk = off[b + 1] - off[b];  /* Alg. 1 line 6 + heuristic (2) */
-      for (uint32_t j = 0; j < kk; ++j) { ids[off[b] + j] = seg[j].id; sc[off[b] + j] = seg[j].s; }
-    }
+    uint32_t* ids = (uint32_t*)malloc((ne + 1) * sizeof(uint32_t));
+    float* sc = (float*)malloc((ne + 1) * sizeof(float));
+    const uint64_t total = orc_csr_from_entries(eb, es, n, ip, NB, prm->alpha, prm->kappa, 0,
+                                                threads, off, ids, sc);
     idx->offsets[t - t_begin] = off;
-    idx->ids[t - t_begin] = ids;
-    idx->scores[t - t_begin] = sc;
+    idx->ids[t - t_begin] = (uint32_t*)realloc(ids, (total + 1) * sizeof(uint32_t));
+    idx->scores[t - t_begin] = (float*)realloc(sc, (total + 1) * sizeof(float));
   }
-  free(eb); free(es); free(cnt); free(sorted);
+  free(eb); free(es);
+  (void)K; (void)D;
   return idx;
+}
+
+/* Alg. 1 lines 5-6 + limit scaling for ONE table, from its pre-filter entries:
+   eb/es [n][ip] = (bucket, score) of point id0+i.  Entries are
+   bucketed by a stable counting sort, each bucket sorted by (score desc, id asc),
+   and keep_count(B) of its prefix kept.  offsets [NB+1]; ids/scores hold up to n*ip.
+   Returns the kept total.  Used by orc_build and, streamed, by bench.py's C5 check. */
+uint64_t orc_csr_from_entries(const uint32_t* eb, const float* es, uint64_t n, uint32_t ip,
+                              uint32_t NB, float alpha, uint32_t kappa, uint32_t id0,
+                              int threads, uint32_t* off, uint32_t* ids, float* sc) {
+  if (threads <= 0) threads = 1;
+  const uint64_t ne = n * ip;
+  uint64_t* cnt = (uint64_t*)calloc((size_t)NB + 1, sizeof(uint64_t));
+  entry* sorted = (entry*)malloc((ne + 1) * sizeof(entry));
+  for (uint64_t e = 0; e < ne; ++e) cnt[eb[e] + 1]++;
+  for (uint32_t b = 0; b < NB; ++b) cnt[b + 1] += cnt[b];
+  uint64_t* cur = (uint64_t*)malloc((size_t)NB * sizeof(uint64_t));
+  memcpy(cur, cnt, (size_t)NB * sizeof(uint64_t));
+  for (uint64_t e = 0; e < ne; ++e) {
+    entry en = {es[e], id0 + (uint32_t)(e / ip)};
+    sorted[cur[eb[e]]++] = en;
+  }
+  free(cur);
+  off[0] = 0;
+  for (uint32_t b = 0; b < NB; ++b)
+    off[b + 1] = off[b] + keep_count((uint32_t)(cnt[b + 1] - cnt[b]), alpha, ip, kappa);
+#pragma omp parallel for schedule(dynamic, 1024) num_threads(threads)
+  for (int64_t b = 0; b < (int64_t)NB; ++b) {
+    const uint32_t B = (uint32_t)(cnt[b + 1] - cnt[b]);
+    if (!B) continue;
+    entry* seg = sorted + cnt[b];
+    qsort(seg, B, sizeof(entry), cmp_entry);  /* (score desc, id asc) */
+    const uint32_t kk = off[b + 1] - off[b];  /* Alg. 1 line 6 + heuristic (2) */
+    for (uint32_t j = 0; j < kk; ++j) { ids[off[b] + j] = seg[j].id; sc[off[b] + j] = seg[j].s; }
+  }
+  const uint64_t total = off[NB];
+  free(cnt); free(sorted);
+  return total;
 }
 
 void orc_index_probes_rows(const orc_index* idx, const float* X, uint64_t n, uint32_t t,
@@ -558,6 +561,27 @@ void orc_index_probes_rows(const orc_index* idx, const float* X, uint64_t n, uin
   }
   free(proj);
   free(buf);
+}
+
+/* same, OpenMP over rows (orc_build's Alg. 1 lines 2-4; bench.py's streamed C5 check) */
+void orc_index_probes_rows_mt(const orc_index* idx, const float* X, uint64_t n, uint32_t t,
+                              uint32_t* buckets, float* scores, int threads) {
+  const uint32_t K = idx->p.K, D = idx->p.D, ip = idx->p.iprobes;
+  if (threads <= 0) threads = 1;
+#pragma omp parallel num_threads(threads)
+  {
+    float* proj = (float*)malloc((size_t)K * D * sizeof(float));
+    float* buf = (float*)malloc((size_t)idx->P * sizeof(float));
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < (int64_t)n; ++i) {
+      for (uint32_t f = 0; f < K; ++f)
+        project_signs(stack_signs(idx, t, f), idx->d, idx->P, D, X + (uint64_t)i * idx->d,
+                      proj + f * D, buf);
+      orc_index_probes(proj, K, D, ip, buckets + (uint64_t)i * ip, scores + (uint64_t)i * ip);
+    }
+    free(proj);
+    free(buf);
+  }
 }
 
 orc_index* orc_index_from_csr(const float* X, uint64_t n, uint32_t d, const orc_params* prm,
@@ -918,18 +942,24 @@ static double synth_normal(uint64_t seed, uint64_t stream, uint64_t k) {
 }
 void orc_synth(float* X, uint64_t n, uint32_t d, uint32_t clusters, float sigma, uint64_t seed,
                uint32_t stream, int threads) {
+  orc_synth_rows(X, 0, n, d, clusters, sigma, seed, stream, threads);
+}
+/* rows [row0, row0 + n) of the same dataset (a shard) */
+void orc_synth_rows(float* X, uint64_t row0, uint64_t n, uint32_t d, uint32_t clusters,
+                    float sigma, uint64_t seed, uint32_t stream, int threads) {
   const uint64_t s_noise = 3 + 100ull * stream, s_assign = 2 + 100ull * stream;
   if (threads <= 0) threads = 1;
 #pragma omp parallel for schedule(static) num_threads(threads)
-  for (int64_t i = 0; i < (int64_t)n; ++i) {
-    float* row = X + (uint64_t)i * d;
+  for (int64_t r = 0; r < (int64_t)n; ++r) {
+    const uint64_t i = row0 + (uint64_t)r;
+    float* row = X + (uint64_t)r * d;
     if (clusters == 0) {
-      for (uint32_t j = 0; j < d; ++j) row[j] = (float)synth_normal(seed, s_noise, (uint64_t)i * d + j);
+      for (uint32_t j = 0; j < d; ++j) row[j] = (float)synth_normal(seed, s_noise, i * d + j);
     } else {
-      const uint64_t c = orc_mix64(orc_derive_seed(seed, s_assign, (uint64_t)i, 0)) % clusters;
+      const uint64_t c = orc_mix64(orc_derive_seed(seed, s_assign, i, 0)) % clusters;
       for (uint32_t j = 0; j < d; ++j) {
         const double ctr = synth_normal(seed, 1, c * d + j);
-        const double z = synth_normal(seed, s_noise, (uint64_t)i * d + j);
+        const double z = synth_normal(seed, s_noise, i * d + j);
         row[j] = (float)(ctr + (double)sigma * z);
       }
     }

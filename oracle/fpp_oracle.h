@@ -87,6 +87,15 @@ uint32_t orc_keep_count(uint32_t B, float alpha, uint32_t iprobes, uint32_t kapp
 uint64_t orc_probe_set_lists(const float* vals, const uint32_t* codes, uint32_t L, uint32_t K,
                              uint32_t D, uint32_t s, uint64_t peff, uint64_t* probes);
 
+/* same, OpenMP over rows */
+void orc_index_probes_rows_mt(const orc_index* idx, const float* X, uint64_t n, uint32_t t,
+                              uint32_t* buckets, float* scores, int threads);
+/* Alg. 1 lines 5-6 for one table from its pre-filter entries eb/es [n][ip] (point ids
+   id0 + i): offsets [NB+1], ids/scores (capacity n*ip); returns the kept total */
+uint64_t orc_csr_from_entries(const uint32_t* eb, const float* es, uint64_t n, uint32_t ip,
+                              uint32_t NB, float alpha, uint32_t kappa, uint32_t id0,
+                              int threads, uint32_t* offsets, uint32_t* ids, float* scores);
+
 /* index build */
 orc_index* orc_build(const float* X, uint64_t n, uint32_t d, const orc_params* prm,
                      int threads, uint32_t t_begin, uint32_t t_end);
@@ -128,6 +137,9 @@ void orc_query_lists(const orc_index* idx, const float* q, uint32_t s, float* va
 /* the pinned synthetic generator, restated for the CPU arm */
 void orc_synth(float* X, uint64_t n, uint32_t d, uint32_t clusters, float sigma, uint64_t seed,
                uint32_t stream, int threads);
+/* rows [row0, row0 + n) of the same dataset (one shard) */
+void orc_synth_rows(float* X, uint64_t row0, uint64_t n, uint32_t d, uint32_t clusters,
+                    float sigma, uint64_t seed, uint32_t stream, int threads);
 
 /* brute force top-k */
 void orc_brute_force(const float* X, uint64_t n, uint32_t d, const float* Q, uint64_t nq,

@@ -33,6 +33,44 @@ class Stats(C.Structure):
                 ("candidates", C.c_uint64), ("exact", C.c_uint64)]
 
 
+NATIVE = False  # the loaded library was built with -march=native on this host
+
+
+def _native_path() -> str:
+    """oracle/_native/<host cpu>/liboracle.so: -march=native binaries are per host CPU."""
+    import hashlib
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    tag = hashlib.sha1(model.encode()).hexdigest()[:12]
+    return os.path.join(HERE, "_native", tag, "liboracle.so")
+
+
+def use_native() -> bool:
+    """Switch later lib() users to an -march=native build for this host (the
+    reference's own flag, proj/CMakeLists.txt:20-22; -ffp-contract=off keeps every
+    fp op as the portable build's).  Objects built before keep their library.  Used
+    by bench.py's timing legs only; returns False if it cannot be built here."""
+    global _lib, NATIVE
+    if NATIVE:
+        return True
+    so = _native_path()
+    src = os.path.join(HERE, "fpp_oracle.c")
+    try:
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+            os.makedirs(os.path.dirname(so), exist_ok=True)
+            subprocess.run(["make", "-s", "-C", HERE, "native", f"NATIVE_SO={so}"], check=True,
+                           capture_output=True, timeout=300)
+        _lib = _load(so)
+        NATIVE = True
+    except Exception:
+        NATIVE = False
+    return NATIVE
+
+
 def build_oracle(with_ref: bool = True) -> None:
     """Compile liboracle.so (and _ref when /root/reference is present)."""
     targets = ["all"] if with_ref and os.path.isdir("/root/reference/proj") else [LIB]
@@ -48,7 +86,12 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB):
             build_oracle(with_ref=False)
-        L = C.CDLL(LIB)
+        _lib = _load(LIB)
+    return _lib
+
+
+def _load(path):
+        L = C.CDLL(path)
         L.orc_mix64.restype = C.c_uint64
         L.orc_mix64.argtypes = [C.c_uint64]
         L.orc_derive_seed.restype = C.c_uint64
@@ -70,6 +113,14 @@ def lib():
                                          u32p, f32p, u64p]
         L.orc_synth.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_float, C.c_uint64,
                                 C.c_uint32, C.c_int]
+        L.orc_synth_rows.argtypes = [f32p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32,
+                                     C.c_float, C.c_uint64, C.c_uint32, C.c_int]
+        L.orc_index_probes_rows_mt.argtypes = [C.c_void_p, f32p, C.c_uint64, C.c_uint32, u32p,
+                                               f32p, C.c_int]
+        L.orc_csr_from_entries.restype = C.c_uint64
+        L.orc_csr_from_entries.argtypes = [u32p, f32p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                           C.c_float, C.c_uint32, C.c_uint32, C.c_int, u32p, u32p,
+                                           f32p]
         L.orc_keep_count.restype = C.c_uint32
         L.orc_keep_count.argtypes = [C.c_uint32, C.c_float, C.c_uint32, C.c_uint32]
         L.orc_probe_set_lists.restype = C.c_uint64
@@ -112,8 +163,7 @@ def lib():
         L.orc_query_lists.argtypes = [C.c_void_p, f32p, C.c_uint32, f32p, u32p]
         L.orc_brute_force.argtypes = [f32p, C.c_uint64, C.c_uint32, f32p, C.c_uint64,
                                       C.c_uint32, u32p, f64p, C.c_int]
-        _lib = L
-    return _lib
+        return L
 
 
 def ref():
@@ -171,9 +221,10 @@ def cp_hash_rows(Pm: np.ndarray) -> np.ndarray:
 
 
 def synth(n: int, d: int, clusters: int = 0, sigma: float = 0.0, seed: int = 1,
-          stream: int = 0, threads: int = 0) -> np.ndarray:
+          stream: int = 0, threads: int = 0, row0: int = 0) -> np.ndarray:
     X = np.empty((n, d), np.float32)
-    lib().orc_synth(X.reshape(-1), n, d, clusters, sigma, seed, stream, threads or os.cpu_count())
+    lib().orc_synth_rows(X.reshape(-1), row0, n, d, clusters, sigma, seed, stream,
+                         threads or os.cpu_count())
     return X
 
 
@@ -201,46 +252,57 @@ class Index:
                  t_begin: int = 0, t_end: int = 0, csr=None, mode: int = 0):
         self.X = np.ascontiguousarray(X, dtype=np.float32)
         self.n, self.d = self.X.shape
+        self._L = lib()  # the library this index lives in (use_native() may switch later)
         self.prm = Params(L, K, D, iprobes, kappa, alpha, seed, mode)
         self.L, self.K, self.D = L, K, D
         self.t_begin, self.t_end = t_begin, (t_end or L)
         if csr is not None:  # (offsets [L][NB+1], ids, scores, table_base [L+1])
             off, ids, sc, tb = (np.ascontiguousarray(a) for a in csr)
-            self.h = lib().orc_index_from_csr(self.X.reshape(-1), self.n, self.d,
+            self.h = self._L.orc_index_from_csr(self.X.reshape(-1), self.n, self.d,
                                               C.byref(self.prm), off.reshape(-1), ids, sc, tb)
         else:
-            self.h = lib().orc_build(self.X.reshape(-1), self.n, self.d, C.byref(self.prm),
+            self.h = self._L.orc_build(self.X.reshape(-1), self.n, self.d, C.byref(self.prm),
                                      threads, t_begin, t_end)
         if not self.h:
             raise ValueError("oracle build: invalid configuration")
-        self.NB = lib().orc_num_buckets(self.h)
+        self.NB = self._L.orc_num_buckets(self.h)
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_free(self.h)
+            self._L.orc_free(self.h)
             self.h = None
 
     def table(self, t: int):
-        tot = lib().orc_table_size(self.h, t)
+        tot = self._L.orc_table_size(self.h, t)
         off = np.empty(self.NB + 1, np.uint32)
         ids = np.empty(max(tot, 1), np.uint32)
         sc = np.empty(max(tot, 1), np.float32)
-        lib().orc_table(self.h, t, off, ids, sc)
+        self._L.orc_table(self.h, t, off, ids, sc)
         return off, ids[:tot], sc[:tot]
+
+    def index_probes_mt(self, X: np.ndarray, t: int, threads: int = 0):
+        """index_probes over rows X with OpenMP (streamed table checks)."""
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        ip = self.prm.iprobes
+        b = np.empty(X.shape[0] * ip, np.uint32)
+        s = np.empty(X.shape[0] * ip, np.float32)
+        self._L.orc_index_probes_rows_mt(self.h, X.reshape(-1), X.shape[0], t, b, s,
+                                       threads or os.cpu_count())
+        return b, s
 
     def index_probes(self, X: np.ndarray, t: int):
         X = np.ascontiguousarray(X, dtype=np.float32)
         ip = self.prm.iprobes
         b = np.empty(X.shape[0] * ip, np.uint32)
         s = np.empty(X.shape[0] * ip, np.float32)
-        lib().orc_index_probes_rows(self.h, X.reshape(-1), X.shape[0], t, b, s)
+        self._L.orc_index_probes_rows(self.h, X.reshape(-1), X.shape[0], t, b, s)
         return b.reshape(-1, ip), s.reshape(-1, ip)
 
     def cap(self, qprobes: int) -> int:
-        return lib().orc_query_cap(self.h, qprobes)
+        return self._L.orc_query_cap(self.h, qprobes)
 
     def peff(self, qprobes: int) -> int:
-        return lib().orc_query_probes(self.h, qprobes)
+        return self._L.orc_query_probes(self.h, qprobes)
 
     def query(self, Q: np.ndarray, k: int, qprobes: int, threads: int = 0, rerank: int = 0):
         """search; rerank = SimHash budget B (0 = off, :330-338).
@@ -250,7 +312,7 @@ class Index:
         ids = np.empty(nq * k, np.uint32)
         sc = np.empty(nq * k, np.float64)
         st = (Stats * max(nq, 1))()
-        r = lib().orc_query_rerank(self.h, Q.reshape(-1), nq, k, qprobes, rerank, ids, sc,
+        r = self._L.orc_query_rerank(self.h, Q.reshape(-1), nq, k, qprobes, rerank, ids, sc,
                                    C.cast(st, C.c_void_p), threads)
         if r != 0:
             raise ValueError("oracle query: invalid arguments")
@@ -261,7 +323,7 @@ class Index:
     def simhash(self, X: np.ndarray, threads: int = 0) -> np.ndarray:
         X = np.ascontiguousarray(X, dtype=np.float32)
         out = np.empty(X.shape[0], np.uint64)
-        lib().orc_simhash_rows(self.h, X.reshape(-1), X.shape[0], out, threads)
+        self._L.orc_simhash_rows(self.h, X.reshape(-1), X.shape[0], out, threads)
         return out
 
     def query_debug(self, q: np.ndarray, qprobes: int):
@@ -271,15 +333,29 @@ class Index:
         cands = np.empty(self.n, np.uint32)
         np_ = C.c_uint64()
         nc = C.c_uint64()
-        lib().orc_query_debug(self.h, q, qprobes, probes, C.byref(np_), cands, C.byref(nc))
+        self._L.orc_query_debug(self.h, q, qprobes, probes, C.byref(np_), cands, C.byref(nc))
         return probes[:np_.value].copy(), cands[:nc.value].copy()
 
     def query_lists(self, q: np.ndarray, s: int):
         q = np.ascontiguousarray(q, dtype=np.float32)
         vals = np.empty(self.L * self.K * s, np.float32)
         codes = np.empty(self.L * self.K * s, np.uint32)
-        lib().orc_query_lists(self.h, q, s, vals, codes)
+        self._L.orc_query_lists(self.h, q, s, vals, codes)
         return vals.reshape(self.L, self.K, s), codes.reshape(self.L, self.K, s)
+
+
+def csr_from_entries(eb: np.ndarray, es: np.ndarray, n: int, iprobes: int, NB: int,
+                     alpha: float, kappa: int, id0: int = 0, threads: int = 0):
+    """Alg. 1 lines 5-6 for one table from its pre-filter entries (bucket, score) of
+    points id0 .. id0+n-1 ([n][iprobes] flat): returns the CSR (offsets, ids, scores)."""
+    eb = np.ascontiguousarray(eb, dtype=np.uint32).reshape(-1)
+    es = np.ascontiguousarray(es, dtype=np.float32).reshape(-1)
+    off = np.empty(NB + 1, np.uint32)
+    ids = np.empty(max(1, n * iprobes), np.uint32)
+    sc = np.empty(max(1, n * iprobes), np.float32)
+    tot = self._L.orc_csr_from_entries(eb, es, n, iprobes, NB, alpha, kappa, id0,
+                                     threads or os.cpu_count(), off, ids, sc)
+    return off, ids[:tot].copy(), sc[:tot].copy()
 
 
 def keep_count(B: int, alpha: float, iprobes: int, kappa: int) -> int:

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _build
 
-__all__ = ["Index", "normalize", "synth", "device_count", "FppError", "FppInvalidArgument",
+__all__ = ["Index", "normalize", "synth", "merge_topk_device", "device_count", "FppError", "FppInvalidArgument",
            "FppEmptyDataset", "FppDimensionError", "FppOutOfRange", "FppNonFinite",
            "FppZeroNorm", "FppCudaError", "FppOutOfMemory", "FppUnsupported", "FppFormatError",
            "FppIOError", "content_hash", "center", "MODES", "lib",
@@ -30,7 +30,7 @@ LIB_PATH = _build.LIB
 
 FPP_OK = 0
 MODES = {"falconnpp": 0, "falconn_baseline": 1}
-ABI_VERSION = 3  # include/falconnpp.h FPP_ABI_VERSION this binding was written against
+ABI_VERSION = 4  # include/falconnpp.h FPP_ABI_VERSION this binding was written against
 ERRORS = {1: "INVALID_ARGUMENT", 2: "EMPTY_DATASET", 3: "DIMENSION", 4: "OUT_OF_RANGE",
           5: "NON_FINITE", 6: "ZERO_NORM", 7: "CUDA", 8: "OUT_OF_MEMORY", 9: "UNSUPPORTED",
           10: "FORMAT", 11: "IO"}
@@ -119,7 +119,7 @@ class IndexInfo(C.Structure):
                 ("num_buckets", C.c_uint64), ("kept_total", C.c_uint64),
                 ("prefilter_total", C.c_uint64), ("device_bytes", C.c_uint64),
                 ("max_bucket", C.c_uint32), ("id_offset", C.c_uint32),
-                ("centering", C.c_uint32), ("mode", C.c_uint32)]
+                ("centering", C.c_uint32), ("mode", C.c_uint32), ("device", C.c_int32)]
 
 
 vp = C.c_void_p
@@ -167,6 +167,8 @@ SIGNATURES = [
     ("fpp_index_center", C.c_int, [vp, vp]),
     ("fpp_normalize", C.c_int, [vp, u64, u32]),
     ("fpp_synth", C.c_int, [vp, u64, u32, u32, f32, u64, u32, i32]),
+    ("fpp_synth_rows", C.c_int, [vp, u64, u64, u32, u32, f32, u64, u32, i32]),
+    ("fpp_merge_topk", C.c_int, [vp, vp, u32, u64, u32, vp, vp, i32, vp]),
 ]
 
 _lib = None
@@ -219,11 +221,55 @@ def normalize(X: np.ndarray) -> np.ndarray:
 
 
 def synth(n: int, d: int, clusters: int = 0, sigma: float = 0.0, seed: int = 1, stream: int = 0,
-          threads: int = 0) -> np.ndarray:
-    """Pinned synthetic data; rows are NOT normalized."""
+          threads: int = 0, row0: int = 0) -> np.ndarray:
+    """Pinned synthetic data; rows [row0, row0+n) of the dataset
+    (a shard when row0 > 0).  Rows are NOT normalized."""
     X = np.empty((n, d), np.float32)
-    _check(lib().fpp_synth(_ptr(X), n, d, clusters, sigma, seed, stream, threads))
+    _check(lib().fpp_synth_rows(_ptr(X), row0, n, d, clusters, sigma, seed, stream, threads))
     return X
+
+
+def merge_topk_device(scores, ids, k: int, out_scores=None, out_ids=None, stream=None):
+    """k-way merge of all-gathered shard top-k lists on the device (fpp_merge_topk).
+
+    scores float64 / ids int32|uint32 CUDA tensors [lists, nq, k] (each list sorted by
+    score desc, id asc; empty slots id 0xFFFFFFFF and -inf) -> [nq, k] merged lists in
+    the same order."""
+    _require_tensor(scores, "scores", ("torch.float64",), scores.device, ndim=3)
+    _require_tensor(ids, "ids", ("torch.int32", "torch.uint32"), scores.device, ndim=3)
+    G, nq, kk = scores.shape
+    if tuple(ids.shape) != (G, nq, kk) or kk != k:
+        raise FppInvalidArgument("merge_topk: scores/ids must both be [lists, nq, k]")
+    import torch
+    if out_scores is None:
+        out_scores = torch.empty((nq, k), dtype=torch.float64, device=scores.device)
+    if out_ids is None:
+        out_ids = torch.empty((nq, k), dtype=ids.dtype, device=scores.device)
+    _require_tensor(out_scores, "out_scores", ("torch.float64",), scores.device, shape=(nq, k))
+    _require_tensor(out_ids, "out_ids", ("torch.int32", "torch.uint32"), scores.device,
+                    shape=(nq, k))
+    _check(lib().fpp_merge_topk(C.c_void_p(scores.data_ptr()), C.c_void_p(ids.data_ptr()), G, nq,
+                                k, C.c_void_p(out_scores.data_ptr()),
+                                C.c_void_p(out_ids.data_ptr()), scores.device.index or 0,
+                                C.c_void_p(stream) if stream else None))
+    return out_scores, out_ids
+
+
+def _require_tensor(t, name, dtypes, device, shape=None, ndim=None):
+    """Device-API argument check (the ABI takes raw pointers): a contiguous CUDA tensor
+    of one of `dtypes` on `device` with the given shape -- else FppInvalidArgument."""
+    if not _is_torch_cuda(t):
+        raise FppInvalidArgument(f"{name}: must be a CUDA torch tensor")
+    if str(t.dtype) not in dtypes:
+        raise FppInvalidArgument(f"{name}: dtype {t.dtype}, expected {' or '.join(dtypes)}")
+    if not t.is_contiguous():
+        raise FppInvalidArgument(f"{name}: must be contiguous")
+    if device is not None and t.device != device:
+        raise FppInvalidArgument(f"{name}: on {t.device}, expected {device}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise FppInvalidArgument(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if ndim is not None and t.dim() != ndim:
+        raise FppInvalidArgument(f"{name}: must be {ndim}-D")
 
 
 class Index:
@@ -296,9 +342,13 @@ class Index:
         return ids, sc
 
     def brute_force_device(self, Q, ids, scores, k: int, stream=None):
-        """Device-resident exact top-k on torch CUDA tensors."""
+        """Device-resident exact top-k on torch CUDA tensors (checked like query_device)."""
+        dev = self.device_obj()
+        _require_tensor(Q, "Q", ("torch.float32",), dev, ndim=2)
         if Q.shape[1] != self.d:
             raise FppDimensionError("brute_force_topk: dimension mismatch")
+        _require_tensor(ids, "ids", ("torch.int32", "torch.uint32"), dev, shape=(Q.shape[0], k))
+        _require_tensor(scores, "scores", ("torch.float64",), dev, shape=(Q.shape[0], k))
         _check(lib().fpp_brute_force_device(self._h, C.c_void_p(Q.data_ptr()), Q.shape[0], k,
                                             C.c_void_p(ids.data_ptr()),
                                             C.c_void_p(scores.data_ptr()),
@@ -397,19 +447,34 @@ class Index:
 
     def query_device(self, Q, ids, scores, k: int, qProbes: int, stats=None, stream=None,
                      rerank: int = 0):
-        """Device-resident batch query on torch CUDA tensors (no host copies);
-        stats (if given) is an int64 [nq, 4] tensor."""
+        """Device-resident batch query on torch CUDA tensors (no host copies):
+        Q float32 [nq, d], ids int32/uint32 [nq, k], scores float64 [nq, k], stats (if
+        given) int64 [nq, 4], all contiguous on the index's device (checked: the ABI
+        takes raw pointers)."""
+        dev = self.device_obj()
+        _require_tensor(Q, "Q", ("torch.float32",), dev, ndim=2)
         if Q.shape[1] != self.d:
-            raise FppDimensionError("search: dimension mismatch")
+            raise FppDimensionError(f"search: query dim {Q.shape[1]} != index dim {self.d}")
+        nq = Q.shape[0]
+        _require_tensor(ids, "ids", ("torch.int32", "torch.uint32"), dev, shape=(nq, k))
+        _require_tensor(scores, "scores", ("torch.float64",), dev, shape=(nq, k))
+        if stats is not None:
+            _require_tensor(stats, "stats", ("torch.int64",), dev, shape=(nq, 4))
         args = (C.c_void_p(ids.data_ptr()), C.c_void_p(scores.data_ptr()),
                 C.c_void_p(stats.data_ptr()) if stats is not None else None,
                 C.c_void_p(stream) if stream else None)
         if rerank:
-            _check(lib().fpp_query_rerank_device(self._h, C.c_void_p(Q.data_ptr()), Q.shape[0],
+            _check(lib().fpp_query_rerank_device(self._h, C.c_void_p(Q.data_ptr()), nq,
                                                  k, qProbes, rerank, *args))
         else:
-            _check(lib().fpp_query_device(self._h, C.c_void_p(Q.data_ptr()), Q.shape[0], k,
+            _check(lib().fpp_query_device(self._h, C.c_void_p(Q.data_ptr()), nq, k,
                                           qProbes, *args))
+
+    def device_obj(self):
+        import torch
+        if getattr(self, "_dev", None) is None:
+            self._dev = torch.device("cuda", self.info()["device"])
+        return self._dev
 
     def center_vector(self) -> np.ndarray:
         c = np.empty(self.d, np.float32)

@@ -84,6 +84,9 @@ Index::~Index() {
   cudaGetDevice(&cur);
   cudaSetDevice(device);
   if (stream) cudaStreamSynchronize(stream);
+  for (QueryCtx* c : ctx_all) delete c;
+  ctx_all.clear();
+  ctx_free.clear();
   dfree(X);
   dfree(signs);
   dfree(sigs);
@@ -93,35 +96,93 @@ Index::~Index() {
   dfree(ids);
   dfree(scores);
   if (shard) shard_release(*this);
-  for (auto& sl : slot) sl.release();
-  if (ev_fork) cudaEventDestroy(ev_fork);
-  if (ev_join) cudaEventDestroy(ev_join);
-  if (ev_join2) cudaEventDestroy(ev_join2);
-  if (sA) cudaStreamDestroy(sA);
-  if (sB) cudaStreamDestroy(sB);
-  q_in.release(); q_ids.release(); q_scores.release(); q_stats.release();
   if (h_pinned) cudaFreeHost(h_pinned);
-  if (prune_h) cudaFreeHost(prune_h);
-  if (prune_ev) cudaEventDestroy(prune_ev);
-  prune_d.release();
   score_bytes_d.release();
   if (stream) cudaStreamDestroy(stream);
   cudaSetDevice(cur);
 }
 
-void Index::QSlot::release() {
+void QueryCtx::QSlot::release() {
   vals.release(); codes.release(); ppos.release(); plen.release(); gbuf.release();
   ckey.release(); cpair.release(); dbgclk.release(); eq.release(); coff.release();
   uq.release(); cands.release(); bitmap.release(); counter.release();
-  qsig.release(); cands2.release(); uq2.release(); coff2.release();
+  qsig.release(); cands2.release(); uq2.release();
   if (pinned) cudaFreeHost(pinned);
   if (ev_probe) cudaEventDestroy(ev_probe);
   if (ev_bdone) cudaEventDestroy(ev_bdone);
   ev_bdone = nullptr;
-  if (stream) cudaStreamDestroy(stream);
   pinned = nullptr;
   ev_probe = nullptr;
-  stream = nullptr;
+}
+
+QueryCtx::~QueryCtx() {
+  if (done_recorded) cudaEventSynchronize(ev_done);
+  if (sA) cudaStreamSynchronize(sA);
+  if (sB) cudaStreamSynchronize(sB);
+  if (own) cudaStreamSynchronize(own);
+  for (auto& sl : slot) sl.release();
+  for (cudaEvent_t e : {ev_fork, ev_join, ev_join2, ev_done, prune_ev})
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t t : {sA, sB, own})
+    if (t) cudaStreamDestroy(t);
+  if (prune_h) cudaFreeHost(prune_h);
+}
+
+CtxLease::CtxLease(const Index& ix_) : ix(ix_), c(nullptr) {
+  {
+    std::lock_guard<std::mutex> lk(ix.mu);
+    if (!ix.ctx_free.empty()) {
+      c = ix.ctx_free.back();
+      ix.ctx_free.pop_back();
+    }
+  }
+  if (c) return;
+  auto* n = new QueryCtx();
+  try {
+    n->device = ix.device;
+    int lo = 0, hi = 0;
+    FPP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    FPP_CUDA(cudaStreamCreateWithPriority(&n->sA, cudaStreamNonBlocking, lo));
+    FPP_CUDA(cudaStreamCreateWithPriority(&n->sB, cudaStreamNonBlocking, hi));
+    FPP_CUDA(cudaStreamCreateWithFlags(&n->own, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&n->ev_fork, &n->ev_join, &n->ev_join2, &n->ev_done})
+      FPP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (auto& sl : n->slot) {
+      FPP_CUDA(cudaEventCreateWithFlags(&sl.ev_probe, cudaEventDisableTiming));
+      FPP_CUDA(cudaEventCreateWithFlags(&sl.ev_bdone, cudaEventDisableTiming));
+      FPP_CUDA(cudaMallocHost(&sl.pinned, 64));
+    }
+  } catch (...) {
+    delete n;
+    throw;
+  }
+  std::lock_guard<std::mutex> lk(ix.mu);
+  ix.ctx_all.push_back(n);
+  c = n;
+}
+
+CtxLease::~CtxLease() {
+  {
+    std::lock_guard<std::mutex> lk(ix.mu);
+    ix.ctx_free.push_back(c);
+  }
+  ix.ctx_cv.notify_all();
+}
+
+void collect_query_timings(const Index& ix) {
+  std::unique_lock<std::mutex> lk(ix.mu);
+  ix.ctx_cv.wait(lk, [&] { return ix.ctx_free.size() == ix.ctx_all.size(); });
+  for (QueryCtx* c : ix.ctx_all) {
+    double ms[PH_COUNT] = {0};
+    c->timer.collect(ms);
+    ix.acc.qhash_ms += ms[PH_QHASH];
+    ix.acc.probe_ms += ms[PH_PROBE];
+    ix.acc.collect_ms += ms[PH_COLLECT];
+    ix.acc.score_ms += ms[PH_SCORE];
+    ix.acc.launches += c->acc.launches;
+    ix.acc.probes += c->acc.probes;
+    c->acc = fpp_timings{};
+  }
 }
 
 uint64_t host_mix64(uint64_t z) {  // common.hpp:18-23
@@ -439,10 +500,7 @@ static void collect_timings(const Index& ix) {
   ix.timer.collect(ms);
   ix.acc.hash_ms += ms[PH_HASH];
   ix.acc.sort_ms += ms[PH_SORT];
-  ix.acc.qhash_ms += ms[PH_QHASH];
-  ix.acc.probe_ms += ms[PH_PROBE];
-  ix.acc.collect_ms += ms[PH_COLLECT];
-  ix.acc.score_ms += ms[PH_SCORE];
+  collect_query_timings(ix);  // waits for every query context's phases
   if (ix.score_bytes_d.p) {  // the phases above have completed: the counter is final
     unsigned long long b = 0;  // monotone counter: no reset racing later launches
     FPP_CUDA(cudaMemcpy(&b, ix.score_bytes_d.p, 8, cudaMemcpyDeviceToHost));
@@ -450,7 +508,6 @@ static void collect_timings(const Index& ix) {
     ix.score_bytes_seen = b;
   }
 }
-
 }  // namespace fpp
 
 using namespace fpp;
@@ -523,22 +580,21 @@ static void query_host(const fpp_index* idx, const float* Q, uint64_t nq, uint32
   if (rerank && rerank < k) fail(FPP_ERR_OUT_OF_RANGE, "search: rerank budget B must be 0 or >= k");
   if (!nq) return;
   DeviceGuard dg(ix.device);
-  std::lock_guard<std::mutex> lk(ix.mu);
-  cudaStream_t s = ix.stream;
-  ix.q_in.ensure(nq * ix.d);
-  ix.q_ids.ensure(nq * k);
-  ix.q_scores.ensure(nq * k);
-  if (stats) ix.q_stats.ensure(nq);
-  FPP_CUDA(cudaMemcpyAsync(ix.q_in.p, Q, nq * ix.d * 4, cudaMemcpyHostToDevice, s));
-  run_query(ix, ix.q_in.p, nq, k, qprobes, ix.q_ids.p, ix.q_scores.p,
-            stats ? ix.q_stats.p : nullptr, s, rerank);
-  FPP_CUDA(cudaMemcpyAsync(ids, ix.q_ids.p, nq * k * 4, cudaMemcpyDeviceToHost, s));
-  FPP_CUDA(cudaMemcpyAsync(scores, ix.q_scores.p, nq * k * 8, cudaMemcpyDeviceToHost, s));
+  CtxLease cx(ix);  // this call's scratch: concurrent calls run side by side
+  cudaStream_t s = cx->own;
+  cx->q_in.ensure(nq * ix.d);
+  cx->q_ids.ensure(nq * k);
+  cx->q_scores.ensure(nq * k);
+  if (stats) cx->q_stats.ensure(nq);
+  FPP_CUDA(cudaMemcpyAsync(cx->q_in.p, Q, nq * ix.d * 4, cudaMemcpyHostToDevice, s));
+  run_query(ix, *cx, cx->q_in.p, nq, k, qprobes, cx->q_ids.p, cx->q_scores.p,
+            stats ? cx->q_stats.p : nullptr, s, rerank);
+  FPP_CUDA(cudaMemcpyAsync(ids, cx->q_ids.p, nq * k * 4, cudaMemcpyDeviceToHost, s));
+  FPP_CUDA(cudaMemcpyAsync(scores, cx->q_scores.p, nq * k * 8, cudaMemcpyDeviceToHost, s));
   if (stats)
-    FPP_CUDA(cudaMemcpyAsync(stats, ix.q_stats.p, nq * sizeof(fpp_query_stats),
+    FPP_CUDA(cudaMemcpyAsync(stats, cx->q_stats.p, nq * sizeof(fpp_query_stats),
                              cudaMemcpyDeviceToHost, s));
   FPP_CUDA(cudaStreamSynchronize(s));
-  collect_timings(ix);
 }
 
 static void query_dev(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k,
@@ -549,9 +605,9 @@ static void query_dev(const fpp_index* idx, const float* Q, uint64_t nq, uint32_
   if (rerank && rerank < k) fail(FPP_ERR_OUT_OF_RANGE, "search: rerank budget B must be 0 or >= k");
   if (!nq) return;
   DeviceGuard dg(ix.device);
-  std::lock_guard<std::mutex> lk(ix.mu);
-  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ix.stream;
-  run_query(ix, Q, nq, k, qprobes, ids, scores, stats, s, rerank);
+  CtxLease cx(ix);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : cx->own;
+  run_query(ix, *cx, Q, nq, k, qprobes, ids, scores, stats, s, rerank);
 }
 
 int fpp_query(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uint32_t qprobes,
@@ -584,7 +640,7 @@ int fpp_signatures(const fpp_index* idx, const float* X, uint64_t n, uint64_t* o
     if (n && (!X || !out)) fail(FPP_ERR_INVALID_ARGUMENT, "signatures: NULL buffer");
     if (!n) return;
     DeviceGuard dg(ix.device);
-    std::lock_guard<std::mutex> lk(ix.mu);
+    std::lock_guard<std::mutex> lk(ix.aux_mu);
     DBuf<float> xd(n * ix.d);
     DBuf<uint64_t> od(n);
     FPP_CUDA(cudaMemcpyAsync(xd.p, X, n * ix.d * 4, cudaMemcpyHostToDevice, ix.stream));
@@ -679,6 +735,7 @@ int fpp_index_info_get(const fpp_index* idx, fpp_index_info* info) {
     info->id_offset = ix.prm.id_offset;
     info->centering = ix.prm.centering;
     info->mode = ix.prm.mode;
+    info->device = ix.device;
   });
 }
 
@@ -709,7 +766,7 @@ int fpp_project(const fpp_index* idx, const float* X, uint64_t n, uint32_t t, ui
     if (t >= ix.prm.L || f >= ix.prm.K) fail(FPP_ERR_OUT_OF_RANGE, "project: (t,f) out of range");
     if (!n) return;
     DeviceGuard dg(ix.device);
-    std::lock_guard<std::mutex> lk(ix.mu);
+    std::lock_guard<std::mutex> lk(ix.aux_mu);
     DBuf<float> xd(n * ix.d), od(n * ix.prm.D);
     FPP_CUDA(cudaMemcpyAsync(xd.p, X, n * ix.d * 4, cudaMemcpyHostToDevice, ix.stream));
     launch_project(ix, xd.p, n, t, f, od.p, ix.stream);
@@ -725,7 +782,7 @@ int fpp_index_probes(const fpp_index* idx, const float* X, uint64_t n, uint32_t 
     if (t >= ix.prm.L) fail(FPP_ERR_OUT_OF_RANGE, "index_probes: table out of range");
     if (!n) return;
     DeviceGuard dg(ix.device);
-    std::lock_guard<std::mutex> lk(ix.mu);
+    std::lock_guard<std::mutex> lk(ix.aux_mu);
     const uint32_t ip = ix.prm.iprobes;
     DBuf<float> xd(n * ix.d);
     DBuf<uint2> od(n * ip);
@@ -754,7 +811,7 @@ int fpp_query_lists(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t 
     const Index& ix = IX(idx);
     if (!nq) return;
     DeviceGuard dg(ix.device);
-    std::lock_guard<std::mutex> lk(ix.mu);
+    std::lock_guard<std::mutex> lk(ix.aux_mu);
     const uint32_t s = query_cap(ix, qprobes);
     const uint64_t tot = nq * ix.prm.L * ix.prm.K * s;
     DBuf<float> qd(nq * ix.d), vd(tot);
@@ -773,17 +830,16 @@ int fpp_query_debug(const fpp_index* idx, const float* q, uint32_t qprobes, uint
     const Index& ix = IX(idx);
     validate_query(ix, 1, 1, qprobes, q, probes, cands);
     DeviceGuard dg(ix.device);
-    std::lock_guard<std::mutex> lk(ix.mu);
+    CtxLease cx(ix);
     DBuf<float> qd(ix.d);
-    FPP_CUDA(cudaMemcpyAsync(qd.p, q, ix.d * 4, cudaMemcpyHostToDevice, ix.stream));
+    FPP_CUDA(cudaMemcpyAsync(qd.p, q, ix.d * 4, cudaMemcpyHostToDevice, cx->own));
     std::vector<uint64_t> pv;
     std::vector<uint32_t> cv;
-    query_debug(ix, qd.p, qprobes, pv, cv);
+    query_debug(ix, *cx, qd.p, qprobes, pv, cv);
     std::memcpy(probes, pv.data(), pv.size() * 8);
     std::memcpy(cands, cv.data(), cv.size() * 4);
     *n_probes = pv.size();
     *n_cands = cv.size();
-    collect_timings(ix);
   });
 }
 
@@ -819,7 +875,7 @@ int fpp_brute_force(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t 
     validate_brute(ix, nq, k, Q, ids, scores);
     if (!nq) return;
     DeviceGuard dg(ix.device);
-    std::lock_guard<std::mutex> lk(ix.mu);
+    std::lock_guard<std::mutex> lk(ix.aux_mu);
     cudaStream_t s = ix.stream;
     DBuf<float> qd(nq * ix.d);
     DBuf<uint32_t> id(nq * k);
@@ -839,7 +895,7 @@ int fpp_brute_force_device(const fpp_index* idx, const float* Q_dev, uint64_t nq
     validate_brute(ix, nq, k, Q_dev, ids_dev, scores_dev);
     if (!nq) return;
     DeviceGuard dg(ix.device);
-    std::lock_guard<std::mutex> lk(ix.mu);
+    std::lock_guard<std::mutex> lk(ix.aux_mu);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ix.stream;
     run_brute_force(ix, Q_dev, nq, k, ids_dev, scores_dev, s);
   });
@@ -849,7 +905,7 @@ int fpp_save(const fpp_index* idx, const char* path) {
   return guarded([&] {
     const Index& ix = IX(idx);
     DeviceGuard dg(ix.device);
-    std::lock_guard<std::mutex> lk(ix.mu);
+    std::lock_guard<std::mutex> lk(ix.aux_mu);
     save_index(ix, path, nullptr);
   });
 }
@@ -930,24 +986,45 @@ static inline double synth_normal(uint64_t seed, uint64_t stream, uint64_t k) {
 
 int fpp_synth(float* X, uint64_t n, uint32_t d, uint32_t clusters, float sigma, uint64_t seed,
               uint32_t stream, int threads) {
+  return fpp_synth_rows(X, 0, n, d, clusters, sigma, seed, stream, threads);
+}
+
+int fpp_synth_rows(float* X, uint64_t row0, uint64_t n, uint32_t d, uint32_t clusters, float sigma,
+                   uint64_t seed, uint32_t stream, int threads) {
   return guarded([&] {
     if (!X || !n || !d) fail(FPP_ERR_EMPTY_DATASET, "synth: empty");
     if (threads <= 0) threads = omp_get_max_threads();
     const uint64_t s_noise = 3 + 100ull * stream, s_assign = 2 + 100ull * stream;
 #pragma omp parallel for schedule(static) num_threads(threads)
-    for (int64_t i = 0; i < (int64_t)n; ++i) {
-      float* row = X + (uint64_t)i * d;
+    for (int64_t r = 0; r < (int64_t)n; ++r) {
+      const uint64_t i = row0 + (uint64_t)r;
+      float* row = X + (uint64_t)r * d;
       if (clusters == 0) {
-        for (uint32_t j = 0; j < d; ++j) row[j] = (float)synth_normal(seed, s_noise, (uint64_t)i * d + j);
+        for (uint32_t j = 0; j < d; ++j) row[j] = (float)synth_normal(seed, s_noise, i * d + j);
       } else {
-        const uint64_t c = host_mix64(host_derive_seed(seed, s_assign, (uint64_t)i, 0)) % clusters;
+        const uint64_t c = host_mix64(host_derive_seed(seed, s_assign, i, 0)) % clusters;
         for (uint32_t j = 0; j < d; ++j) {
           const double ctr = synth_normal(seed, 1, c * d + j);
-          const double z = synth_normal(seed, s_noise, (uint64_t)i * d + j);
+          const double z = synth_normal(seed, s_noise, i * d + j);
           row[j] = (float)(ctr + (double)sigma * z);
         }
       }
     }
+  });
+}
+
+int fpp_merge_topk(const double* scores_dev, const uint32_t* ids_dev, uint32_t lists, uint64_t nq,
+                   uint32_t k, double* out_scores_dev, uint32_t* out_ids_dev, int device,
+                   void* stream) {
+  return guarded([&] {
+    if (lists == 0 || lists > 32) fail(FPP_ERR_INVALID_ARGUMENT, "merge_topk: lists must be in [1, 32]");
+    if (k == 0 || k > 32) fail(FPP_ERR_INVALID_ARGUMENT, "merge_topk: k must be in [1, 32]");
+    if (nq && (!scores_dev || !ids_dev || !out_scores_dev || !out_ids_dev))
+      fail(FPP_ERR_INVALID_ARGUMENT, "merge_topk: NULL buffer");
+    if (!nq) return;
+    set_device(device);
+    launch_merge_topk(scores_dev, ids_dev, lists, nq, k, out_scores_dev, out_ids_dev,
+                      static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <condition_variable>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -65,6 +66,7 @@ struct PhaseTimer {
 };
 
 struct ShardState;
+struct QueryCtx;
 
 struct Index {
   fpp_params prm{};
@@ -96,8 +98,32 @@ struct Index {
   uint64_t device_bytes = 0;
   ShardState* shard = nullptr;  // global-filter sharded build in progress
 
-  // query scratch (guarded by mu; concurrent queries serialize on it).  Two
-  // slots double-buffer query chunks across two streams.
+  // Query scratch lives in per-call contexts (QueryCtx, fpp_query.cu): a call
+  // leases a free context for its enqueue, so concurrent queries on one index
+  // neither share scratch nor serialise; a context's next user
+  // stream-waits on its previous call's completion event before touching it.
+  mutable std::mutex mu;                     // guards the context pool and the policy below
+  mutable std::mutex aux_mu;                 // serialises the aux entry points on `stream`
+  mutable std::vector<QueryCtx*> ctx_all, ctx_free;
+  mutable std::condition_variable ctx_cv;
+  // score-gather early termination (k_score_pruned): measured fraction of row slices
+  // read, probed on the first chunks and every PRUNE_REPROBE-th chunk after
+  mutable double prune_frac = -1.0;
+  mutable uint64_t prune_chunks = 0;
+  mutable DBuf<unsigned long long> score_bytes_d;  // [1] row bytes read by the score kernels
+  mutable unsigned long long score_bytes_seen = 0;
+  uint64_t* h_pinned = nullptr;  // small pinned readback
+
+  mutable PhaseTimer timer;
+  mutable fpp_timings acc{};
+
+  ~Index();
+};
+
+// Scratch of one query call (run_query).  Two slots double-buffer query chunks
+// across two streams; the reorder and host-staging buffers,
+// the per-call phase timer and counters live here too.
+struct QueryCtx {
   struct QSlot {
     DBuf<float> vals;
     DBuf<uint32_t> codes;
@@ -116,46 +142,48 @@ struct Index {
     DBuf<uint64_t> qsig;    // rerank: query signatures
     DBuf<uint32_t> cands2;  // rerank: screened candidates [nqc][B]
     DBuf<uint32_t> uq2;
-    DBuf<uint64_t> coff2;
     uint64_t* pinned = nullptr;     // etot readback
     cudaEvent_t ev_probe = nullptr; // stage A (hash + probe select) done
     cudaEvent_t ev_bdone = nullptr; // stage B (collect + score) done
-    cudaStream_t stream = nullptr;  // unused (streams live on the index)
     void release();
   };
-  mutable std::mutex mu;
-  mutable QSlot slot[2];
-  mutable cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
-  mutable cudaStream_t sA = nullptr, sB = nullptr;  // pipeline streams (low / high priority)
-  mutable DBuf<float> q_in;
-  mutable DBuf<uint32_t> q_ids;
-  mutable DBuf<double> q_scores;
-  mutable DBuf<fpp_query_stats> q_stats;
+  int device = 0;
+  QSlot slot[2];
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+  cudaEvent_t ev_done = nullptr;   // recorded on the caller's stream at the end of a call
+  bool done_recorded = false;
+  cudaStream_t sA = nullptr, sB = nullptr;  // pipeline streams (low / high priority)
+  cudaStream_t own = nullptr;               // host-buffer calls run here
+  DBuf<float> q_in;
+  DBuf<uint32_t> q_ids;
+  DBuf<double> q_scores;
+  DBuf<fpp_query_stats> q_stats;
   // batch reordering scratch (run_query)
-  mutable DBuf<uint64_t> ord_key, ord_key2;
-  mutable DBuf<uint32_t> ord_idx, ord_perm, ord_ids;
-  mutable DBuf<float> ord_q;
-  mutable DBuf<double> ord_sc;
-  mutable DBuf<fpp_query_stats> ord_st;
-  mutable DBuf<unsigned char> ord_tmp;
-  uint64_t* h_pinned = nullptr;  // small pinned readback
-  // score-gather early termination (k_score_pruned): measured fraction of row slices
-  // read, probed on the first chunks and every PRUNE_REPROBE-th chunk after
-  mutable double prune_frac = -1.0;
-  mutable uint64_t prune_chunks = 0;
-  mutable bool prune_pending = false;
-  mutable unsigned long long* prune_h = nullptr;  // pinned [2]: rows, row slices read
-  mutable DBuf<unsigned long long> prune_d;
-  mutable cudaEvent_t prune_ev = nullptr;
-  mutable double dup_ratio = -1.0;  // walked entries / unique candidates (stage_b dedup choice)
-  mutable DBuf<unsigned long long> score_bytes_d;  // [1] row bytes read by the score kernels
-  mutable unsigned long long score_bytes_seen = 0;
-
-  mutable PhaseTimer timer;
-  mutable fpp_timings acc{};
-
-  ~Index();
+  DBuf<uint32_t> ord_key, ord_perm, ord_ids;
+  DBuf<float> ord_q;
+  DBuf<double> ord_sc;
+  DBuf<fpp_query_stats> ord_st;
+  // k_score_pruned read-fraction probe (async readback into the index policy)
+  unsigned long long* prune_h = nullptr;  // pinned [2]: rows, row slices read
+  DBuf<unsigned long long> prune_d;
+  cudaEvent_t prune_ev = nullptr;
+  bool prune_pending = false;
+  PhaseTimer timer;
+  fpp_timings acc{};
+  ~QueryCtx();
 };
+
+// lease a free query context of `ix` for one call (created on demand)
+struct CtxLease {
+  const Index& ix;
+  QueryCtx* c;
+  explicit CtxLease(const Index& ix);
+  ~CtxLease();
+  QueryCtx* operator->() const { return c; }
+  QueryCtx& operator*() const { return *c; }
+};
+// wait for every context, fold their timers/counters into ix.acc (fpp_timings_get)
+void collect_query_timings(const Index& ix);
 
 // host helpers (fpp_capi.cu)
 uint64_t host_mix64(uint64_t z);
@@ -200,13 +228,17 @@ void shard_release(Index& ix);
 const uint32_t* shard_hist_ptr(const Index& ix);
 
 // query (fpp_query.cu)
-void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t qprobes,
-               uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s,
-               uint32_t rerank = 0);
+void run_query(const Index& ix, QueryCtx& cx, const float* Qd, uint64_t nq, uint32_t k,
+               uint32_t qprobes, uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d,
+               cudaStream_t s, uint32_t rerank = 0);
 void launch_query_lists(const Index& ix, const float* Qd, uint64_t nq, uint32_t s_cap,
                         float* vals, uint32_t* codes, cudaStream_t s, uint64_t lstride = 0);
 // probes (t*NB+b) and candidates of query 0 of Qd (debug/parity)
-void query_debug(const Index& ix, const float* qd, uint32_t qprobes,
+void query_debug(const Index& ix, QueryCtx& cx, const float* qd, uint32_t qprobes,
                  std::vector<uint64_t>& probes, std::vector<uint32_t>& cands);
+// k-way merge of `lists` per-shard top-k lists [lists][nq][k] (each sorted by score
+// desc, id asc; empty slots id 0xFFFFFFFF / -inf) into [nq][k] (fpp_merge_topk)
+void launch_merge_topk(const double* sc, const uint32_t* ids, uint32_t lists, uint64_t nq,
+                       uint32_t k, double* out_sc, uint32_t* out_ids, cudaStream_t s);
 
 }  // namespace fpp

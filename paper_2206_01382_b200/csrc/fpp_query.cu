@@ -15,10 +15,10 @@
 //                   counts over the sorted lists), tie resolution in
 //                   (r1, r2, t) order, then directory reads -> (pos, len)
 //   k_collect       CTA per query: walk kept entries, OR them into a visited
-//                   bitmap (shared memory; an 8-CTA DSMEM cluster or global
-//                   memory for large shards) and emit unique ids in ascending
-//                   order -- or, where ids rarely repeat and the bitmap is
-//                   off-chip, copy them grouped by id range (no dedup)
+//                   bitmap in shared memory and emit unique ids in ascending
+//                   order; large shards dedup by id-range groups (counting
+//                   sort + per-warp range bitmaps), else an 8-CTA DSMEM
+//                   cluster or global-memory bitmap
 //   k_score         CTA per query: 32-row batches per warp, cp.async column
 //                   slices into shared memory (multi-stage ring), each lane
 //                   accumulates its row's exact products in fp64 in the
@@ -34,7 +34,6 @@
 #include <cstring>
 
 #include <cooperative_groups.h>
-#include <cub/device/device_radix_sort.cuh>
 
 #include "fpp_device.cuh"
 #include "fpp_internal.h"
@@ -978,8 +977,8 @@ struct CollectArgs {
   uint32_t nwords;       // bitmap words (n bits)
   uint32_t* gbitmap;     // [gridDim.x][nwords] when not in shared memory
   uint32_t* counter;     // dynamic query fetch
-  uint32_t nodedup;      // 1: copy the walked ids without dedup (stage_b: few duplicates)
-  uint32_t bshift;       // nodedup: id >> bshift < 256 (id-range groups)
+  uint32_t grouped;      // 1: two-level dedup by id-range groups (large shards, stage_b)
+  uint32_t gshift;       // grouped: id >> gshift < CO_NG; per-warp range bitmap 2^gshift bits
 };
 
 // Warp-cooperative walk over one query's probes.  A warp takes 32 probes at a
@@ -1064,13 +1063,129 @@ __device__ __forceinline__ void collect_walk(const uint64_t* pp, const uint32_t*
   }
 }
 
+// Grouped dedup (large shards: the n-bit visited set is off-chip).  Two walks
+// form a counting sort of the walked ids into CO_NG id-range groups (2^gshift
+// ids each) in the query's candidate segment; then each warp takes groups, ORs
+// the group's ids into a 2^gshift-bit range bitmap in shared memory, and writes
+// the set bits back in ascending order at the group's start; finally the groups'
+// unique prefixes are compacted (ascending blocks: a block's sources lie at or
+// above its destinations, so one pass in place is safe).  Every id is emitted
+// once and the list is ascending, as with the whole-n bitmap.
+constexpr uint32_t CO_NG = 4096;
+__device__ __forceinline__ void collect_grouped(const CollectArgs& a, uint32_t q, uint32_t* out,
+                                                uint32_t* ucount, uint32_t* nextc, uint32_t* sm,
+                                                uint32_t* scan_sh, uint32_t* U_out) {
+  uint32_t* cnt = sm;             // [CO_NG] group counts -> scatter cursors (= group ends)
+  uint32_t* ucnt = sm + CO_NG;    // [CO_NG] unique ids per group -> destinations
+  uint32_t* wbm = sm + 2 * CO_NG; // [32 warps][2^gshift / 32] range bitmaps
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t P = (uint32_t)a.peff, gs = a.gshift;
+  const uint32_t bw = 1u << (gs - 5), wpl = bw >= 32 ? bw / 32 : 1;  // bitmap words, per lane
+  const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
+  const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
+  auto next_chunk = [&]() {
+    uint32_t c = 0;
+    if (lane == 0) c = smem_fetch_add(nextc, 1u);
+    return __shfl_sync(FULL, c, 0);
+  };
+  for (uint32_t i = threadIdx.x; i < CO_NG; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  collect_walk(pp, pl, P, a.ids, out, ucount, next_chunk, [&](uint32_t id) {
+    smem_inc(&cnt[id >> gs]);
+    return false;
+  });
+  __syncthreads();
+  {  // exclusive scan of the group counts -> scatter cursors
+    constexpr uint32_t PER = CO_NG / 1024;  // blockDim.x == CO_THREADS == 1024
+    uint32_t v[PER], t = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < PER; ++j) { v[j] = cnt[threadIdx.x * PER + j]; t += v[j]; }
+    uint32_t tot;
+    uint32_t b = block_excl_scan_u32(t, scan_sh, &tot);
+#pragma unroll
+    for (uint32_t j = 0; j < PER; ++j) { cnt[threadIdx.x * PER + j] = b; b += v[j]; }
+    if (threadIdx.x == 0) *nextc = 0;
+  }
+  __syncthreads();
+  collect_walk(pp, pl, P, a.ids, out, ucount, next_chunk, [&](uint32_t id) {
+    out[smem_fetch_add(&cnt[id >> gs], 1u)] = id;
+    return false;
+  });
+  __syncthreads();  // cnt[g] is now the end of group g (= the start of group g + 1)
+  uint32_t* bm = wbm + (size_t)w * bw;
+  for (uint32_t g = w; g < CO_NG; g += blockDim.x >> 5) {
+    const uint32_t S = g ? cnt[g - 1] : 0u, E = cnt[g];
+    if (E - S <= 1) {  // empty or a single id: already unique
+      if (lane == 0) ucnt[g] = E - S;
+      continue;
+    }
+    for (uint32_t j = lane; j < bw; j += 32) bm[j] = 0;
+    __syncwarp();
+    for (uint32_t i = S + lane; i < E; i += 32) {
+      const uint32_t b = out[i] & ((1u << gs) - 1u);
+      asm volatile("red.shared.or.b32 [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(bm + (b >> 5))),
+                   "r"(1u << (b & 31))
+                   : "memory");
+    }
+    __syncwarp();
+    // ascending emission of the set bits at the group's start (its reads are done)
+    const uint32_t w0 = min(bw, (uint32_t)lane * wpl), w1 = min(bw, w0 + wpl);
+    uint32_t c = 0;
+    for (uint32_t j = w0; j < w1; ++j) c += __popc(bm[j]);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    uint32_t pos = S + x - c;
+    const uint32_t base = g << gs;
+    for (uint32_t j = w0; j < w1; ++j)
+      for (uint32_t word = bm[j]; word; word &= word - 1) out[pos++] = base + j * 32 + (__ffs(word) - 1);
+    if (lane == 31) ucnt[g] = x;
+    __syncwarp();
+  }
+  __syncthreads();
+  uint32_t U;
+  {  // destinations: exclusive scan of the unique counts
+    constexpr uint32_t PER = CO_NG / 1024;
+    uint32_t v[PER], t = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < PER; ++j) { v[j] = ucnt[threadIdx.x * PER + j]; t += v[j]; }
+    uint32_t b = block_excl_scan_u32(t, scan_sh, &U);
+#pragma unroll
+    for (uint32_t j = 0; j < PER; ++j) { ucnt[threadIdx.x * PER + j] = b; b += v[j]; }
+  }
+  __syncthreads();
+  // in-place compaction, ascending blocks: output j of group g comes from
+  // S_g + (j - D_g) >= j, so a block's reads never hit a slot an earlier block wrote
+  for (uint32_t j0 = 0; j0 < U; j0 += blockDim.x) {
+    const uint32_t j = j0 + threadIdx.x;
+    uint32_t v = 0;
+    if (j < U) {
+      uint32_t lo = 0, hi = CO_NG;  // last group g with D_g <= j (it holds j: j < D_g + u_g)
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (ucnt[mid] <= j) lo = mid;
+        else hi = mid;
+      }
+      const uint32_t S = lo ? cnt[lo - 1] : 0u;
+      v = out[S + (j - ucnt[lo])];
+    }
+    __syncthreads();
+    if (j < U) out[j] = v;
+    __syncthreads();
+  }
+  *U_out = U;
+}
+
 // CTA per query (persistent CTAs fetch queries dynamically); the visited
-// bitmap lives in shared memory (n bits) or, for large shards, in a per-CTA
-// global-memory region that is cleared again through the candidate list.
+// bitmap lives in shared memory (n bits), or the grouped dedup runs (large
+// shards), or -- beyond the grouped range -- a per-CTA global-memory bitmap that
+// is cleared again through the candidate list.
 __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
   extern __shared__ __align__(16) uint32_t sbm[];
   __shared__ uint32_t ucount, qsh, nextc;
-  __shared__ uint32_t bcur[256];  // nodedup: id-range counts, then write cursors
   __shared__ uint32_t scan_sh[32];
   uint32_t* bm = a.gbitmap ? a.gbitmap + (uint64_t)blockIdx.x * a.nwords : sbm;
   for (;;) {
@@ -1079,7 +1194,7 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
       ucount = 0;
       nextc = 0;
     }
-    if (!a.gbitmap && !a.nodedup) {
+    if (!a.gbitmap && !a.grouped) {
       const uint32_t n4 = a.nwords >> 2;
       uint4* b4 = reinterpret_cast<uint4*>(sbm);
       for (uint32_t w = threadIdx.x; w < n4; w += blockDim.x) b4[w] = make_uint4(0, 0, 0, 0);
@@ -1096,42 +1211,8 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
       return __shfl_sync(FULL, c, 0);
     };
     uint32_t U;
-    if (a.nodedup) {
-      // every walked entry is a candidate (duplicates kept), grouped by the top 8 bits
-      // of the id (a counting sort over two walks): similar queries scored side by
-      // side then still gather rows of the same id range at about the same time
-      for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) bcur[i] = 0;
-      __syncthreads();
-      const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
-      const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
-      collect_walk(pp, pl, P, a.ids, out, &ucount, next_chunk, [&](uint32_t id) {
-        smem_inc(&bcur[id >> a.bshift]);
-        return false;
-      });
-      __syncthreads();
-      if (threadIdx.x < 32) {  // exclusive scan of the 256 counts (8 per lane)
-        uint32_t v[8], t = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) { v[j] = bcur[threadIdx.x * 8 + j]; t += v[j]; }
-        uint32_t x = t;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(FULL, x, o);
-          if ((int)threadIdx.x >= o) x += y;
-        }
-        uint32_t b = x - t;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) { bcur[threadIdx.x * 8 + j] = b; b += v[j]; }
-        if (threadIdx.x == 31) ucount = x;
-        if (threadIdx.x == 0) nextc = 0;
-      }
-      __syncthreads();
-      collect_walk(pp, pl, P, a.ids, out, &ucount, next_chunk, [&](uint32_t id) {
-        out[smem_fetch_add(&bcur[id >> a.bshift], 1u)] = id;
-        return false;
-      });
-      __syncthreads();
-      U = ucount;
+    if (a.grouped) {
+      collect_grouped(a, q, out, &ucount, &nextc, sbm, scan_sh, &U);
     } else if (!a.gbitmap) {
       // shared-memory bitmap: fire-and-forget ORs during the walk, then the set
       // bits are emitted in ascending id order (a bitmap scan), so every query's
@@ -1163,7 +1244,7 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
       U = ucount;
     }
     if (threadIdx.x == 0) a.uq[q] = U;
-    if (a.gbitmap && !a.nodedup)
+    if (a.gbitmap)
       for (uint32_t c = threadIdx.x; c < U; c += blockDim.x) bm[out[c] >> 5] = 0;
     __syncthreads();
   }
@@ -1369,7 +1450,6 @@ struct ScoreArgs {
   uint64_t n;
   unsigned long long* dbg;  // FPP_DEBUG_PRUNE: [rows, row slices read]
   unsigned long long* rbytes;  // += candidate-row bytes read (fpp_timings.score_bytes)
-  uint32_t dup;                // 1: candidate lists may repeat ids (CollectArgs::nodedup)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1419,7 +1499,7 @@ __device__ __forceinline__ bool sbetter(double s1, uint32_t i1, double s2, uint3
   return s1 > s2 || (s1 == s2 && i1 < i2);
 }
 __device__ __forceinline__ void topk_insert(double& bs, uint32_t& bi, uint32_t k, double cs_l,
-                                            uint32_t ci_l, bool valid, bool dedup = false) {
+                                            uint32_t ci_l, bool valid) {
   const int lane = threadIdx.x & 31;
   double ws = __shfl_sync(FULL, bs, k - 1);
   uint32_t wi = __shfl_sync(FULL, bi, k - 1);
@@ -1432,8 +1512,6 @@ __device__ __forceinline__ void topk_insert(double& bs, uint32_t& bi, uint32_t k
     ws = __shfl_sync(FULL, bs, k - 1);
     wi = __shfl_sync(FULL, bi, k - 1);
     if (!sbetter(cs, ci, ws, wi)) continue;
-    // candidate lists with duplicates (ScoreArgs::dup): an id enters a list once
-    if (dedup && __any_sync(FULL, (uint32_t)lane < k && bi == ci)) continue;
     const unsigned ahead = __ballot_sync(FULL, (uint32_t)lane < k && sbetter(bs, bi, cs, ci));
     const int pos = __popc(ahead);
     const double us = __shfl_up_sync(FULL, bs, 1);
@@ -1560,7 +1638,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
       const uint32_t ci = cb * 32 + lane;
       const bool valid = ci < U;
       const uint32_t id = valid ? __ldg(cand + ci) : 0xffffffffu;
-      topk_insert(bs, bi, k, acc, id, valid, a.dup);
+      topk_insert(bs, bi, k, acc, id, valid);
       acc = 0.0;
       cc = 0;
       cb += SC_WARPS;
@@ -1574,7 +1652,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
   if (w == 0) {
     for (int w2 = 1; w2 < SC_WARPS; ++w2) {
       const bool valid = (uint32_t)lane < k && mg_i[w2][lane] != 0xffffffffu;
-      topk_insert(bs, bi, k, mg_s[w2][lane], mg_i[w2][lane], valid, a.dup);
+      topk_insert(bs, bi, k, mg_s[w2][lane], mg_i[w2][lane], valid);
     }
     if ((uint32_t)lane < k) {
       const bool ok = bi != 0xffffffffu;
@@ -1898,14 +1976,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
           if (((desc >> 28) & 3u) == (tgen & 3u)) tmask = nm;
         }
         if (s + 1 == nsl) {  // batch done: rows still live enter the warp top-k
-          topk_insert(bs, bi, k, tacc, ctid, tlive, a.dup);
+          topk_insert(bs, bi, k, tacc, ctid, tlive);
           const uint32_t ks = (k + NW - 1) / NW;
           const uint32_t wi = __shfl_sync(FULL, bi, k - 1), wi2 = __shfl_sync(FULL, bi, ks - 1);
           const double ws = __shfl_sync(FULL, bs, k - 1), ws2 = __shfl_sync(FULL, bs, ks - 1);
           if (lane == 0) {
             if (wi != NONE) thr_v[w] = ws;
-            // the warps' lists are disjoint only without duplicates
-            if (wi2 != NONE && !a.dup) thr2_v[w] = ws2;
+            if (wi2 != NONE) thr2_v[w] = ws2;
           }
         }
       }
@@ -1930,7 +2007,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
     if (w == 0) {
       for (int w2 = 1; w2 < NW; ++w2) {
         const bool valid = (uint32_t)lane < k && mg_i[w2 * 32 + lane] != NONE;
-        topk_insert(bs, bi, k, mg_s[w2 * 32 + lane], mg_i[w2 * 32 + lane], valid, a.dup);
+        topk_insert(bs, bi, k, mg_s[w2 * 32 + lane], mg_i[w2 * 32 + lane], valid);
       }
       if ((uint32_t)lane < k) {
         const bool ok = bi != NONE;
@@ -2020,8 +2097,10 @@ static uint32_t cand_cap(const Index& ix, uint32_t qprobes) {
                                       (uint64_t)ix.prm.L * ix.prm.K * scap * scap);
 }
 
+using QSlot = QueryCtx::QSlot;
+
 // size a slot's chunk buffers for up to nqc queries (before any launch uses it)
-static void prepare_slot(const Index& ix, Index::QSlot& sl, uint32_t nqc, uint32_t qprobes) {
+static void prepare_slot(const Index& ix, QSlot& sl, uint32_t nqc, uint32_t qprobes) {
   const uint64_t LKs = (uint64_t)ix.prm.L * ix.prm.K * query_cap(ix, qprobes);
   const uint64_t lstride = (LKs + 3) & ~3ull;
   const uint64_t peff = query_probes(ix, qprobes);
@@ -2039,7 +2118,7 @@ static void prepare_slot(const Index& ix, Index::QSlot& sl, uint32_t nqc, uint32
   sl.counter.ensure(4);
 }
 
-static void stage_a(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t nqc,
+static void stage_a(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, uint32_t nqc,
                     uint32_t qprobes, cudaStream_t st, uint64_t* dbg_probes) {
   const uint32_t L = ix.prm.L, K = ix.prm.K;
   const uint32_t scap = query_cap(ix, qprobes);
@@ -2047,23 +2126,13 @@ static void stage_a(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   const uint64_t LKs = (uint64_t)L * K * scap;
   const uint64_t lstride = (LKs + 3) & ~3ull;  // 16-byte aligned per-query blocks
   prepare_slot(ix, sl, nqc, qprobes);
-  sl.vals.ensure((size_t)nqc * lstride);
-  sl.codes.ensure((size_t)nqc * lstride);
-  sl.ppos.ensure((size_t)nqc * peff);
-  sl.plen.ensure((size_t)nqc * peff);
-  sl.eq.ensure(nqc);
-  sl.uq.ensure(nqc);
-  sl.coff.ensure((size_t)nqc + 1);
-  sl.counter.ensure(4);
-  if (!sl.pinned) FPP_CUDA(cudaMallocHost(&sl.pinned, 64));
-  if (!sl.ev_probe) FPP_CUDA(cudaEventCreateWithFlags(&sl.ev_probe, cudaEventDisableTiming));
 
   cudaEvent_t e0;
-  ix.timer.begin(PH_QHASH, st, &e0);
+  cx.timer.begin(PH_QHASH, st, &e0);
   launch_query_lists(ix, Qd, nqc, scap, sl.vals.p, sl.codes.p, st, lstride);
-  ix.timer.end(PH_QHASH, e0, st);
+  cx.timer.end(PH_QHASH, e0, st);
 
-  ix.timer.begin(PH_PROBE, st, &e0);
+  cx.timer.begin(PH_PROBE, st, &e0);
   const uint32_t ccap = cand_cap(ix, qprobes);
   ProbeArgs pa{sl.vals.p, sl.codes.p, nqc, L, K, scap, ix.prm.D, ix.NB, peff, ix.offsets,
                ix.table_base, sl.ppos.p, sl.plen.p, sl.eq.p, dbg_probes, sl.gbuf.p, lstride,
@@ -2100,53 +2169,47 @@ static void stage_a(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   k_scan_eq<<<1, 1024, 0, st>>>(sl.eq.p, nqc, sl.coff.p);
   FPP_LAUNCH();
   FPP_CUDA(cudaMemcpyAsync(sl.pinned, sl.coff.p + nqc, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-  ix.timer.end(PH_PROBE, e0, st);
+  cx.timer.end(PH_PROBE, e0, st);
   FPP_CUDA(cudaEventRecord(sl.ev_probe, st));
+}
+
+// grouped-dedup geometry for an index of n points: id >> gshift < CO_NG; 0 when the
+// per-warp range bitmaps (32 x 2^gshift bits) would not fit shared memory
+static uint32_t grouped_shift(uint64_t n) {
+  uint32_t gs = 5;
+  while (gs < 32 && ((n - 1) >> gs) >= CO_NG) ++gs;
+  const size_t sm = (size_t)2 * CO_NG * 4 + (size_t)32 * ((1ull << gs) / 8);
+  return sm + 64 <= (size_t)co_smem_max() ? gs : 0u;
 }
 
 // Stage B on stream `st` (after the host has read the slot's candidate total):
 // bucket walk + dedup, then row gather + fp64 dot + top-k.
-static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t nqc, uint32_t k,
-                    uint32_t qprobes, uint32_t* ids_d, double* scores_d,
-                    fpp_query_stats* stats_d, cudaStream_t st, uint32_t rerank = 0,
-                    bool unique = false) {
+static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, uint32_t nqc,
+                    uint32_t k, uint32_t qprobes, uint32_t* ids_d, double* scores_d,
+                    fpp_query_stats* stats_d, cudaStream_t st, uint32_t rerank = 0) {
   const uint64_t peff = query_probes(ix, qprobes);
   const uint64_t etot = sl.pinned[0];
   sl.cands.ensure(etot + 1);
   cudaEvent_t e0;
-  ix.timer.begin(PH_COLLECT, st, &e0);
+  cx.timer.begin(PH_COLLECT, st, &e0);
   const uint32_t nwords = (uint32_t)((ix.n + 31) / 32);
   CollectArgs ca{sl.ppos.p, sl.plen.p, peff, ix.ids, sl.coff.p, sl.cands.p, sl.uq.p,
-                 nqc, nwords, nullptr, sl.counter.p, 0};
-  // Dedup only where it pays: when the visited bitmap does not fit one SM's shared
-  // memory (n > ~1.8 M: the DSMEM cluster or global bitmaps) and ids rarely repeat
-  // (entries/unique < 1.25, e.g. C4's 1.08), the walked ids are scored with their
-  // repeats (grouped by id range) and the top-k lists skip repeated ids: same results,
-  // C4 collect 246 -> 71 ms.  The ratio is measured once per index on a dedup chunk;
-  // per-query stats (unique counts) and rerank screening always dedup.
-  // FPP_DEDUP=1 / FPP_NODEDUP=1 force either.
-  const bool force_dd = getenv("FPP_DEDUP") != nullptr, force_nd = getenv("FPP_NODEDUP") != nullptr;
-  // (FPP_FORCE_COLLECT=cluster|global also counts as an off-chip bitmap here: tests)
-  const char* force_co = getenv("FPP_FORCE_COLLECT");
-  const bool smem_bitmap = !force_co && (int)((size_t)nwords * 4 + 64) <= co_smem_max();
-  const bool nodedup = !rerank && !stats_d && !unique && !force_dd &&
-                       (force_nd || (!smem_bitmap && ix.dup_ratio > 0.0 && ix.dup_ratio < 1.25));
-  const bool measure_dup = !nodedup && !rerank && ix.dup_ratio < 0.0;
+                 nqc, nwords, nullptr, sl.counter.p, 0, 0};
+  // Visited set (every id scored once): an n-bit bitmap in shared memory
+  // where it fits one SM (n <= ~1.8 M); beyond that the grouped dedup (id-range
+  // counting sort + per-warp range bitmaps; C4's 10 M points); beyond its range an
+  // 8-CTA DSMEM cluster bitmap or per-CTA global bitmaps.  All emit ascending ids.
+  // FPP_FORCE_COLLECT=grouped|cluster|global selects a large-shard path at any n (tests).
+  const char* force = getenv("FPP_FORCE_COLLECT");
+  const bool f_grouped = force && !strcmp(force, "grouped");
+  const bool f_cluster = force && !strcmp(force, "cluster"), f_global = force && !strcmp(force, "global");
   const size_t static_co = 64;
-  size_t co_smem = (size_t)nwords * 4;
-  unsigned co_grid;
   const int sms = sm_count();
   const uint32_t slice_words = (nwords + CO_CLUSTER - 1) / CO_CLUSTER;
-  // FPP_FORCE_COLLECT=cluster|global selects a large-shard path at any n (tests)
-  const char* force = getenv("FPP_FORCE_COLLECT");
-  const bool f_cluster = force && !strcmp(force, "cluster"), f_global = force && !strcmp(force, "global");
-  if (nodedup) {
-    ca.nodedup = 1;
-    while ((ix.n - 1) >> ca.bshift >= 256) ++ca.bshift;
-    co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * 2);
-    FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
-    k_collect<<<co_grid, CO_THREADS, 0, st>>>(ca);
-  } else if (!f_cluster && !f_global && (int)(co_smem + static_co) <= co_smem_max()) {
+  const uint32_t gshift = grouped_shift(ix.n);
+  unsigned co_grid;
+  if (!force && (size_t)nwords * 4 + static_co <= (size_t)co_smem_max()) {
+    const size_t co_smem = (size_t)nwords * 4;
     FPP_CUDA(cudaFuncSetAttribute(k_collect, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)co_smem));
     int occ = 1;
@@ -2154,7 +2217,18 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * std::max(occ, 1));
     FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
     k_collect<<<co_grid, CO_THREADS, co_smem, st>>>(ca);
-  } else if (!f_global && (int)((size_t)slice_words * 4 + static_co) <= co_smem_max()) {
+  } else if ((!force || f_grouped) && gshift) {
+    ca.grouped = 1;
+    ca.gshift = gshift;
+    const size_t co_smem = (size_t)2 * CO_NG * 4 + (size_t)32 * ((1ull << gshift) / 8);
+    FPP_CUDA(cudaFuncSetAttribute(k_collect, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)co_smem));
+    int occ = 1;
+    FPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collect, CO_THREADS, co_smem));
+    co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * std::max(occ, 1));
+    FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
+    k_collect<<<co_grid, CO_THREADS, co_smem, st>>>(ca);
+  } else if (!f_global && (size_t)slice_words * 4 + static_co <= (size_t)co_smem_max()) {
     // bitmap split over a CO_CLUSTER-CTA cluster (DSMEM)
     const size_t sm = (size_t)slice_words * 4;
     FPP_CUDA(cudaFuncSetAttribute(k_collect_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2169,7 +2243,6 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     ncl = std::max(1, std::min<int>(ncl, (int)nqc));
     k_collect_cluster<<<ncl * CO_CLUSTER, CO_CL_THREADS, sm, st>>>(ca, slice_words);
   } else {
-    co_smem = 0;
     co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * 2);
     const size_t need = (size_t)co_grid * nwords;
     if (sl.bitmap.n < need) {
@@ -2178,28 +2251,14 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     }
     ca.gbitmap = sl.bitmap.p;
     FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
-    k_collect<<<co_grid, CO_THREADS, co_smem, st>>>(ca);
+    k_collect<<<co_grid, CO_THREADS, 0, st>>>(ca);
   }
   FPP_LAUNCH();
-  ix.timer.end(PH_COLLECT, e0, st);
-  if (measure_dup) {  // once per index: entries / unique candidates of this chunk
-    std::vector<uint32_t> he(nqc), hu(nqc);
-    FPP_CUDA(cudaMemcpyAsync(he.data(), sl.eq.p, nqc * 4, cudaMemcpyDeviceToHost, st));
-    FPP_CUDA(cudaMemcpyAsync(hu.data(), sl.uq.p, nqc * 4, cudaMemcpyDeviceToHost, st));
-    FPP_CUDA(cudaStreamSynchronize(st));
-    double se = 0, su = 0;
-    for (uint32_t i = 0; i < nqc; ++i) { se += he[i]; su += hu[i]; }
-    ix.dup_ratio = su > 0 ? se / su : 1e30;
-  }
+  cx.timer.end(PH_COLLECT, e0, st);
 
-  ix.timer.begin(PH_SCORE, st, &e0);
+  cx.timer.begin(PH_SCORE, st, &e0);
   ScoreArgs sa{ix.X, ix.d, ix.ldx, Qd, sl.coff.p, sl.cands.p, sl.uq.p, sl.eq.p, peff, k,
                ix.prm.id_offset, ids_d, scores_d, stats_d, nullptr, 0};
-  sa.dup = nodedup ? 1u : 0u;
-  if (!ix.score_bytes_d.p) {
-    ix.score_bytes_d.alloc(1);
-    FPP_CUDA(cudaMemsetAsync(ix.score_bytes_d.p, 0, 8, st));
-  }
   sa.rbytes = ix.score_bytes_d.p;
   if (rerank) {  // SimHash screen: at most B candidates per query reach the exact scores
     sl.qsig.ensure(nqc);
@@ -2209,7 +2268,7 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     k_screen<<<nqc, SCR_THREADS, 0, st>>>(sl.cands.p, sl.coff.p, sl.uq.p, ix.sigs, sl.qsig.p, rerank,
                                           sl.cands2.p, sl.uq2.p);
     FPP_LAUNCH();
-    ix.acc.launches += 2;
+    cx.acc.launches += 2;
     sa.cands = sl.cands2.p;
     sa.uq = sl.uq2.p;
     sa.uq_all = sl.uq.p;
@@ -2234,8 +2293,6 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   // ascending-id candidate lists more queries in flight share more rows in L2:
   // C2 96x2 @ 2/SM 344k -> 64x2 @ 3/SM 352k q/s; C4 +5%); 32 x 4 below
   const bool wide = ix.d >= 64;
-  // exact early termination (k_score_pruned) whenever the index has tail norms
-  // (d > 64); FPP_NO_PRUNE=1 reads every candidate row in full
   // exact early termination (k_score_pruned) when the index has tail norms (d > 64)
   // and the bound pays on this data: the read fraction (row slices read / all) is
   // probed on the first chunk and every 16th after (async readback); above 0.65 the
@@ -2247,11 +2304,12 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
   const bool dbg = getenv("FPP_DEBUG_PRUNE") != nullptr;
   bool use_pruned = false, probe = false;
   if (ix.xt_n && !no_prune) {
-    if (ix.prune_pending && cudaEventQuery(ix.prune_ev) == cudaSuccess) {
-      if (ix.prune_h[0]) ix.prune_frac = (double)ix.prune_h[1] / ((double)ix.prune_h[0] * ix.d);
-      ix.prune_pending = false;
+    std::lock_guard<std::mutex> lk(ix.mu);  // the index-wide policy (concurrent calls)
+    if (cx.prune_pending && cudaEventQuery(cx.prune_ev) == cudaSuccess) {
+      if (cx.prune_h[0]) ix.prune_frac = (double)cx.prune_h[1] / ((double)cx.prune_h[0] * ix.d);
+      cx.prune_pending = false;
     }
-    probe = dbg || (!ix.prune_pending && (ix.prune_frac < 0 || ix.prune_chunks % 16 == 0));
+    probe = dbg || (!cx.prune_pending && (ix.prune_frac < 0 || ix.prune_chunks % 16 == 0));
     use_pruned = force_prune || probe || ix.prune_frac < 0 || ix.prune_frac <= 0.65;
     ++ix.prune_chunks;
   }
@@ -2261,13 +2319,13 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     sa.xt_head = ix.xt_head;
     sa.n = ix.n;
     if (probe) {
-      if (!ix.prune_h) {
-        FPP_CUDA(cudaMallocHost(&ix.prune_h, 16));
-        FPP_CUDA(cudaEventCreateWithFlags(&ix.prune_ev, cudaEventDisableTiming));
-        ix.prune_d.alloc(2);
+      if (!cx.prune_h) {
+        FPP_CUDA(cudaMallocHost(&cx.prune_h, 16));
+        FPP_CUDA(cudaEventCreateWithFlags(&cx.prune_ev, cudaEventDisableTiming));
+        cx.prune_d.alloc(2);
       }
-      FPP_CUDA(cudaMemsetAsync(ix.prune_d.p, 0, 16, st));
-      sa.dbg = ix.prune_d.p;
+      FPP_CUDA(cudaMemsetAsync(cx.prune_d.p, 0, 16, st));
+      sa.dbg = cx.prune_d.p;
     }
     // ring geometry (FPP_SC_PR = NW,ST,MINB digits; default 4 warps x 2 stages, 3 CTAs/SM:
     // C2 score 8.0 ms vs 11.2 (4x3 @ 2/SM, kept for the tests), 12.9 (2x4 @ 3/SM) and
@@ -2305,12 +2363,12 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     }
 #undef FPP_PR_CASE
     if (probe) {
-      FPP_CUDA(cudaMemcpyAsync(ix.prune_h, ix.prune_d.p, 16, cudaMemcpyDeviceToHost, st));
-      FPP_CUDA(cudaEventRecord(ix.prune_ev, st));
-      ix.prune_pending = true;
+      FPP_CUDA(cudaMemcpyAsync(cx.prune_h, cx.prune_d.p, 16, cudaMemcpyDeviceToHost, st));
+      FPP_CUDA(cudaEventRecord(cx.prune_ev, st));
+      cx.prune_pending = true;
       if (dbg) {
-        FPP_CUDA(cudaEventSynchronize(ix.prune_ev));
-        const unsigned long long* h = ix.prune_h;
+        FPP_CUDA(cudaEventSynchronize(cx.prune_ev));
+        const unsigned long long* h = cx.prune_h;
         fprintf(stderr, "[prune dbg] rows %llu, floats read per row %.1f of %u (%.1f%% of row bytes)\n",
                 h[0], h[0] ? (double)h[1] / h[0] : 0.0, ix.d, h[0] ? 100.0 * h[1] / h[0] / ix.d : 0.0);
       }
@@ -2323,9 +2381,9 @@ static void stage_b(const Index& ix, Index::QSlot& sl, const float* Qd, uint32_t
     else launch_score(k_score<false, 32, 4>, 32, 4);
   }
   FPP_LAUNCH();
-  ix.timer.end(PH_SCORE, e0, st);
-  ix.acc.launches += 5;  // lists, probe_select, scan_eq, collect, score
-  ix.acc.probes += peff * nqc;
+  cx.timer.end(PH_SCORE, e0, st);
+  cx.acc.launches += 5;  // lists, probe_select, scan_eq, collect, score
+  cx.acc.probes += peff * nqc;
 }
 
 static uint32_t chunk_size(const Index& ix, uint32_t qprobes, uint64_t nq) {
@@ -2348,7 +2406,7 @@ static uint32_t chunk_size(const Index& ix, uint32_t qprobes, uint64_t nq) {
 // collect + gather/score) on a high-priority one, so the scheduler hands freed
 // SM slots to the bandwidth-bound kernel first and fills the rest with stage A
 // of the next chunk.  Slots alternate; events order slot reuse.
-static void run_query_core(const Index& ix, const float* Qd, uint64_t nq, uint32_t k,
+static void run_query_core(const Index& ix, QueryCtx& cx, const float* Qd, uint64_t nq, uint32_t k,
                            uint32_t qprobes, uint32_t* ids_d, double* scores_d,
                            fpp_query_stats* stats_d, cudaStream_t s, uint32_t rerank) {
   const uint32_t cs = chunk_size(ix, qprobes, nq);
@@ -2358,59 +2416,44 @@ static void run_query_core(const Index& ix, const float* Qd, uint64_t nq, uint32
     for (uint64_t c = 0; c < nch; ++c) {
       const uint64_t q0 = c * cs;
       const uint32_t n = (uint32_t)std::min<uint64_t>(cs, nq - q0);
-      stage_a(ix, ix.slot[0], Qd + q0 * ix.d, n, qprobes, s, nullptr);
-      FPP_CUDA(cudaEventSynchronize(ix.slot[0].ev_probe));
-      stage_b(ix, ix.slot[0], Qd + q0 * ix.d, n, k, qprobes, ids_d + q0 * k, scores_d + q0 * k,
+      stage_a(ix, cx, cx.slot[0], Qd + q0 * ix.d, n, qprobes, s, nullptr);
+      FPP_CUDA(cudaEventSynchronize(cx.slot[0].ev_probe));
+      stage_b(ix, cx, cx.slot[0], Qd + q0 * ix.d, n, k, qprobes, ids_d + q0 * k, scores_d + q0 * k,
               stats_d ? stats_d + q0 : nullptr, s, rerank);
     }
     return;
   }
-  if (!ix.sA) {
-    int lo = 0, hi = 0;
-    FPP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sA, cudaStreamNonBlocking, lo));
-    FPP_CUDA(cudaStreamCreateWithPriority(&ix.sB, cudaStreamNonBlocking, hi));
-    FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_fork, cudaEventDisableTiming));
-    FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_join, cudaEventDisableTiming));
-    FPP_CUDA(cudaEventCreateWithFlags(&ix.ev_join2, cudaEventDisableTiming));
-    for (auto& sl : ix.slot) FPP_CUDA(cudaEventCreateWithFlags(&sl.ev_bdone, cudaEventDisableTiming));
-  }
-  prepare_slot(ix, ix.slot[0], cs, qprobes);
-  prepare_slot(ix, ix.slot[1], cs, qprobes);
-  FPP_CUDA(cudaEventRecord(ix.ev_fork, s));
-  FPP_CUDA(cudaStreamWaitEvent(ix.sA, ix.ev_fork, 0));
-  FPP_CUDA(cudaStreamWaitEvent(ix.sB, ix.ev_fork, 0));
+  prepare_slot(ix, cx.slot[0], cs, qprobes);
+  prepare_slot(ix, cx.slot[1], cs, qprobes);
+  FPP_CUDA(cudaEventRecord(cx.ev_fork, s));
+  FPP_CUDA(cudaStreamWaitEvent(cx.sA, cx.ev_fork, 0));
+  FPP_CUDA(cudaStreamWaitEvent(cx.sB, cx.ev_fork, 0));
   auto issue_a = [&](uint64_t c) {
-    Index::QSlot& sl = ix.slot[c & 1];
-    if (c >= 2) FPP_CUDA(cudaStreamWaitEvent(ix.sA, sl.ev_bdone, 0));  // slot free again
+    QSlot& sl = cx.slot[c & 1];
+    if (c >= 2) FPP_CUDA(cudaStreamWaitEvent(cx.sA, sl.ev_bdone, 0));  // slot free again
     const uint64_t q0 = c * cs;
     const uint32_t n = (uint32_t)std::min<uint64_t>(cs, nq - q0);
-    stage_a(ix, sl, Qd + q0 * ix.d, n, qprobes, ix.sA, nullptr);
+    stage_a(ix, cx, sl, Qd + q0 * ix.d, n, qprobes, cx.sA, nullptr);
   };
   issue_a(0);
   if (nch > 1) issue_a(1);
   for (uint64_t c = 0; c < nch; ++c) {
-    Index::QSlot& sl = ix.slot[c & 1];
+    QSlot& sl = cx.slot[c & 1];
     FPP_CUDA(cudaEventSynchronize(sl.ev_probe));
-    FPP_CUDA(cudaStreamWaitEvent(ix.sB, sl.ev_probe, 0));
+    FPP_CUDA(cudaStreamWaitEvent(cx.sB, sl.ev_probe, 0));
     const uint64_t q0 = c * cs;
     const uint32_t n = (uint32_t)std::min<uint64_t>(cs, nq - q0);
-    stage_b(ix, sl, Qd + q0 * ix.d, n, k, qprobes, ids_d + q0 * k, scores_d + q0 * k,
-            stats_d ? stats_d + q0 : nullptr, ix.sB, rerank);
-    FPP_CUDA(cudaEventRecord(sl.ev_bdone, ix.sB));
+    stage_b(ix, cx, sl, Qd + q0 * ix.d, n, k, qprobes, ids_d + q0 * k, scores_d + q0 * k,
+            stats_d ? stats_d + q0 : nullptr, cx.sB, rerank);
+    FPP_CUDA(cudaEventRecord(sl.ev_bdone, cx.sB));
     if (c + 2 < nch) issue_a(c + 2);
   }
-  FPP_CUDA(cudaEventRecord(ix.ev_join, ix.sA));
-  FPP_CUDA(cudaEventRecord(ix.ev_join2, ix.sB));
-  FPP_CUDA(cudaStreamWaitEvent(s, ix.ev_join, 0));
-  FPP_CUDA(cudaStreamWaitEvent(s, ix.ev_join2, 0));
+  FPP_CUDA(cudaEventRecord(cx.ev_join, cx.sA));
+  FPP_CUDA(cudaEventRecord(cx.ev_join2, cx.sB));
+  FPP_CUDA(cudaStreamWaitEvent(s, cx.ev_join, 0));
+  FPP_CUDA(cudaStreamWaitEvent(s, cx.ev_join2, 0));
 }
 
-__global__ void k_iota(uint32_t* __restrict__ p, uint64_t n) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    p[i] = (uint32_t)i;
-}
 __global__ void k_gather_rows(const float* __restrict__ Q, const uint32_t* __restrict__ perm,
                               uint64_t nq, uint32_t d, float* __restrict__ out) {
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nq * d;
@@ -2434,64 +2477,113 @@ __global__ void k_scatter_results(const uint32_t* __restrict__ perm, uint64_t nq
   }
 }
 
+// Batch order: a stable counting sort of the queries by their order key (the
+// cross-polytope code of stack (0, K-1): fewer than 2D <= 2048 values) in one
+// CTA: histogram, scan, then the tiles of 1024 queries in order, warps in order
+// (match_any ranks within a warp, one __syncthreads per warp for the cursors).
+constexpr uint32_t ORD_BINS = 2048;
+__global__ void __launch_bounds__(1024) k_order_sort(const uint64_t* __restrict__ keys, uint32_t nq,
+                                                     uint32_t* __restrict__ perm) {
+  __shared__ uint32_t cur[ORD_BINS];
+  __shared__ uint32_t scan_sh[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (uint32_t i = threadIdx.x; i < ORD_BINS; i += blockDim.x) cur[i] = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nq; i += blockDim.x)
+    smem_inc(&cur[(uint32_t)keys[i] & (ORD_BINS - 1)]);
+  __syncthreads();
+  {
+    const uint32_t v0 = cur[2 * threadIdx.x], v1 = cur[2 * threadIdx.x + 1];
+    uint32_t tot;
+    const uint32_t b = block_excl_scan_u32(v0 + v1, scan_sh, &tot);
+    cur[2 * threadIdx.x] = b;
+    cur[2 * threadIdx.x + 1] = b + v0;
+  }
+  __syncthreads();
+  for (uint32_t base = 0; base < nq; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const bool valid = i < nq;
+    const uint32_t key = valid ? ((uint32_t)keys[i] & (ORD_BINS - 1)) : ORD_BINS;
+    const uint32_t peers = __match_any_sync(FULL, key);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    const bool leader = rank == 0;
+    uint32_t pos = 0;
+    for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) {
+      if (w == w2 && valid && leader) {
+        pos = cur[key];
+        cur[key] = pos + __popc(peers);
+      }
+      __syncthreads();
+    }
+    const uint32_t lead = __ffs(peers) - 1;
+    pos = __shfl_sync(FULL, pos, lead);
+    if (valid) perm[pos + rank] = i;
+  }
+}
+
 // Batched query.  Large batches are processed ordered by the cross-polytope code
-// of stack (0, 0) (similar queries adjacent; the sort is stable): with the
+// of stack (0, K-1) (similar queries adjacent; the sort is stable): with the
 // ascending-id candidate lists, concurrently scored queries then gather shared
 // rows through L2 (C2: +8% over input order; the full table-0 bucket or the
 // SimHash signature as key group less well).  Results are scattered back to
 // the caller's order; FPP_NO_REORDER=1 keeps the input order.  Results are
-// identical either way (every query is independent).
-void run_query(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, uint32_t qprobes,
-               uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d, cudaStream_t s,
-               uint32_t rerank) {
+// identical either way (every query is independent).  The context's previous
+// call (possibly on another stream) completes before its scratch is reused.
+void run_query(const Index& ix, QueryCtx& cx, const float* Qd, uint64_t nq, uint32_t k,
+               uint32_t qprobes, uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d,
+               cudaStream_t s, uint32_t rerank) {
+  if (cx.done_recorded) FPP_CUDA(cudaStreamWaitEvent(s, cx.ev_done, 0));
+  if (!ix.score_bytes_d.p) {
+    std::lock_guard<std::mutex> lk(ix.mu);
+    if (!ix.score_bytes_d.p) {
+      ix.score_bytes_d.alloc(1);
+      FPP_CUDA(cudaMemset(ix.score_bytes_d.p, 0, 8));
+    }
+  }
   static const bool no_reorder = getenv("FPP_NO_REORDER") != nullptr;
   // the reorder costs a fixed ~35 us plus a gather of Q; its gain scales with the
   // score gather (C1, 1000 x 128 i.i.d.: -5%; C3, 1000 x 960 clustered: +4%)
   if (no_reorder || nq < 256 || nq * ix.d < (512ull << 10) || nq >= (1ull << 31)) {
-    run_query_core(ix, Qd, nq, k, qprobes, ids_d, scores_d, stats_d, s, rerank);
-    return;
+    run_query_core(ix, cx, Qd, nq, k, qprobes, ids_d, scores_d, stats_d, s, rerank);
+  } else {
+    const uint32_t d = ix.d;
+    cx.ord_key.ensure(2 * nq);  // u64 order keys viewed as 2 x u32 words
+    cx.ord_perm.ensure(nq);
+    cx.ord_q.ensure(nq * d);
+    cx.ord_ids.ensure(nq * k);
+    cx.ord_sc.ensure(nq * k);
+    if (stats_d) cx.ord_st.ensure(nq);
+    const int sms = sm_count();
+    uint64_t* okeys = reinterpret_cast<uint64_t*>(cx.ord_key.p);
+    launch_order_keys(ix, Qd, nq, okeys, s);
+    k_order_sort<<<1, 1024, 0, s>>>(okeys, (uint32_t)nq, cx.ord_perm.p);
+    FPP_LAUNCH();
+    k_gather_rows<<<sms * 8, 256, 0, s>>>(Qd, cx.ord_perm.p, nq, d, cx.ord_q.p);
+    FPP_LAUNCH();
+    run_query_core(ix, cx, cx.ord_q.p, nq, k, qprobes, cx.ord_ids.p, cx.ord_sc.p,
+                   stats_d ? cx.ord_st.p : nullptr, s, rerank);
+    k_scatter_results<<<sms * 4, 256, 0, s>>>(cx.ord_perm.p, nq, k, cx.ord_ids.p, cx.ord_sc.p,
+                                              stats_d ? cx.ord_st.p : nullptr, ids_d, scores_d,
+                                              stats_d);
+    FPP_LAUNCH();
+    cx.acc.launches += 4;  // order keys, sort, gather, scatter
   }
-  const uint32_t d = ix.d;
-  ix.ord_key.ensure(nq);
-  ix.ord_key2.ensure(nq);
-  ix.ord_idx.ensure(nq);
-  ix.ord_perm.ensure(nq);
-  ix.ord_q.ensure(nq * d);
-  ix.ord_ids.ensure(nq * k);
-  ix.ord_sc.ensure(nq * k);
-  if (stats_d) ix.ord_st.ensure(nq);
-  const int sms = sm_count();
-  launch_order_keys(ix, Qd, nq, ix.ord_key.p, s);
-  k_iota<<<sms * 4, 256, 0, s>>>(ix.ord_idx.p, nq);
-  FPP_LAUNCH();
-  size_t tmp = 0;
-  FPP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ix.ord_key.p, ix.ord_key2.p, ix.ord_idx.p,
-                                           ix.ord_perm.p, (int)nq, 0, 32, s));
-  ix.ord_tmp.ensure(tmp);
-  FPP_CUDA(cub::DeviceRadixSort::SortPairs(ix.ord_tmp.p, tmp, ix.ord_key.p, ix.ord_key2.p,
-                                           ix.ord_idx.p, ix.ord_perm.p, (int)nq, 0, 32, s));
-  k_gather_rows<<<sms * 8, 256, 0, s>>>(Qd, ix.ord_perm.p, nq, d, ix.ord_q.p);
-  FPP_LAUNCH();
-  run_query_core(ix, ix.ord_q.p, nq, k, qprobes, ix.ord_ids.p, ix.ord_sc.p,
-                 stats_d ? ix.ord_st.p : nullptr, s, rerank);
-  k_scatter_results<<<sms * 4, 256, 0, s>>>(ix.ord_perm.p, nq, k, ix.ord_ids.p, ix.ord_sc.p,
-                                            stats_d ? ix.ord_st.p : nullptr, ids_d, scores_d,
-                                            stats_d);
-  FPP_LAUNCH();
-  ix.acc.launches += 5;  // order keys, iota, sort (counted once), gather, scatter
+  FPP_CUDA(cudaEventRecord(cx.ev_done, s));
+  cx.done_recorded = true;
 }
 
-void query_debug(const Index& ix, const float* qd, uint32_t qprobes, std::vector<uint64_t>& probes,
-                 std::vector<uint32_t>& cands) {
-  cudaStream_t s = ix.stream;
+void query_debug(const Index& ix, QueryCtx& cx, const float* qd, uint32_t qprobes,
+                 std::vector<uint64_t>& probes, std::vector<uint32_t>& cands) {
+  cudaStream_t s = cx.own;
+  if (cx.done_recorded) FPP_CUDA(cudaStreamWaitEvent(s, cx.ev_done, 0));
   const uint64_t peff = query_probes(ix, qprobes);
   DBuf<uint64_t> dbg(peff);
   DBuf<uint32_t> ids(32);
   DBuf<double> sc(32);
-  Index::QSlot& sl = ix.slot[0];
-  stage_a(ix, sl, qd, 1, qprobes, s, dbg.p);
+  QSlot& sl = cx.slot[0];
+  stage_a(ix, cx, sl, qd, 1, qprobes, s, dbg.p);
   FPP_CUDA(cudaEventSynchronize(sl.ev_probe));
-  stage_b(ix, sl, qd, 1, 1, qprobes, ids.p, sc.p, nullptr, s, 0, true);  // unique candidates
+  stage_b(ix, cx, sl, qd, 1, 1, qprobes, ids.p, sc.p, nullptr, s, 0);
   FPP_CUDA(cudaStreamSynchronize(s));
   probes.resize(peff);
   FPP_CUDA(cudaMemcpy(probes.data(), dbg.p, peff * 8, cudaMemcpyDeviceToHost));
@@ -2503,6 +2595,58 @@ void query_debug(const Index& ix, const float* qd, uint32_t qprobes, std::vector
   if (U) FPP_CUDA(cudaMemcpy(cands.data(), sl.cands.p + off, (size_t)U * 4, cudaMemcpyDeviceToHost));
   std::sort(probes.begin(), probes.end());
   std::sort(cands.begin(), cands.end());
+}
+
+// k-way merge of per-shard top-k lists (multi-GPU query): warp per
+// query; lane l < lists holds the head of list l; k rounds of a warp arg-best by
+// (score desc, id asc), empty slots (id 0xFFFFFFFF, -inf) last.  The lists hold
+// disjoint global ids, so the merged order is the 1-GPU top-k's.
+__global__ void k_merge_topk(const double* __restrict__ sc, const uint32_t* __restrict__ ids,
+                             uint32_t lists, uint64_t nq, uint32_t k, double* __restrict__ osc,
+                             uint32_t* __restrict__ oid) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t q = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += nw) {
+    uint32_t pos = 0;
+    const bool mine = (uint32_t)lane < lists;
+    const uint64_t base = ((uint64_t)lane * nq + q) * k;
+    double hs = -INFINITY;
+    uint32_t hi = 0xffffffffu;
+    if (mine) { hs = sc[base]; hi = ids[base]; }
+    for (uint32_t r = 0; r < k; ++r) {
+      double bs = hs;
+      uint32_t bi = hi;
+      int bl = lane;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double os = __shfl_xor_sync(FULL, bs, o);
+        const uint32_t oi = __shfl_xor_sync(FULL, bi, o);
+        const int ol = __shfl_xor_sync(FULL, bl, o);
+        // valid entries first, then score desc, id asc (lane asc: a total order)
+        const bool ov = oi != 0xffffffffu, mv = bi != 0xffffffffu;
+        const bool take = (ov && !mv) ||
+                          (ov == mv && (os > bs || (os == bs && (oi < bi || (oi == bi && ol < bl)))));
+        if (take) { bs = os; bi = oi; bl = ol; }
+      }
+      if (lane == 0) {
+        oid[q * k + r] = bi;
+        osc[q * k + r] = bi != 0xffffffffu ? bs : -INFINITY;
+      }
+      if (lane == bl && bi != 0xffffffffu) {
+        ++pos;
+        if (pos < k) { hs = sc[base + pos]; hi = ids[base + pos]; }
+        else { hs = -INFINITY; hi = 0xffffffffu; }
+      }
+    }
+  }
+}
+
+void launch_merge_topk(const double* sc, const uint32_t* ids, uint32_t lists, uint64_t nq,
+                       uint32_t k, double* out_sc, uint32_t* out_ids, cudaStream_t s) {
+  if (!nq) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((nq + 7) / 8, (uint64_t)sm_count() * 16);
+  k_merge_topk<<<grid, 256, 0, s>>>(sc, ids, lists, nq, k, out_sc, out_ids);
+  FPP_LAUNCH();
 }
 
 }  // namespace fpp

@@ -6,7 +6,8 @@ builds its own index with ``id_offset`` so the ids it returns are global; every
 GPU holds the same sign bitmasks (same seeds).  A query batch is replicated to
 every rank, each rank answers from its shard, and the per-shard top-k lists are
 merged after one all-gather with the reference's key order (score desc, id
-asc), so ties still resolve to the lower global id.
+asc) by the library's k-way merge kernel (fpp_merge_topk), so ties still resolve
+to the lower global id.
 
 Filter scope: ``per_shard`` applies the alpha/kappa filter inside each shard
 (SURVEY 8(e) option A, the literal north-star reading); results then equal the
@@ -27,7 +28,9 @@ def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def merge_topk(scores: torch.Tensor, ids: torch.Tensor, k: int) -> tuple[torch.Tensor, torch.Tensor]:
-    """Merge candidate lists [nq, m] into top-k by (score desc, id asc).
+    """Merge candidate lists [nq, m] into top-k by (score desc, id asc) -- the host
+    (CPU-tensor) form used by the gloo tests with the oracle as the shard engine.
+    CUDA tensors go through the device k-way merge kernel (merge_lists).
 
     Empty slots carry score -inf and id 0xFFFFFFFF (as int64) and sort last.
     """
@@ -42,11 +45,57 @@ def merge_topk(scores: torch.Tensor, ids: torch.Tensor, k: int) -> tuple[torch.T
     return s2, i2
 
 
+def merge_lists(s_all: torch.Tensor, i_all: torch.Tensor, k: int):
+    """[G, nq, k] gathered shard lists -> merged [nq, k] (score desc, id asc).
+    CUDA: the library's k-way merge kernel (fpp_merge_topk); CPU: merge_topk."""
+    if s_all.is_cuda:
+        import paper_2206_01382_b200 as fpp
+        i32 = i_all if i_all.dtype == torch.int32 else i_all.to(torch.int32)
+        ms, mi = fpp.merge_topk_device(s_all.contiguous(), i32.contiguous(), k,
+                                       stream=torch.cuda.current_stream(s_all.device).cuda_stream)
+        return ms, mi
+    G, nq, kk = s_all.shape
+    return merge_topk(s_all.permute(1, 0, 2).reshape(nq, G * kk),
+                      i_all.to(torch.int64).permute(1, 0, 2).reshape(nq, G * kk), k)
+
+
+def _backend(group=None) -> str:
+    return dist.get_backend(group) if dist.is_initialized() else "none"
+
+
+def all_gather_stacked(t: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather `t` from every rank into [G, *t.shape] (rank-major).  With NCCL the
+    CUDA tensor is gathered in place over NVLink; with gloo (CPU tests, or several
+    ranks sharing one GPU) it is staged through host memory."""
+    world = dist.get_world_size(group)
+    t = t.contiguous()
+    if t.is_cuda and _backend(group) == "gloo":
+        return all_gather_stacked(t.cpu(), group).to(t.device)
+    out = torch.empty(world * t.numel(), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, t.reshape(-1), group=group)
+    return out.view((world,) + tuple(t.shape))
+
+
+def all_reduce_sum(t: torch.Tensor, group=None) -> torch.Tensor:
+    if t.is_cuda and _backend(group) == "gloo":
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(h)
+        return t
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
 def allgather_merge(scores: torch.Tensor, ids: torch.Tensor, k: int, group=None):
     """All-gather per-rank [nq, k] lists and merge them (every rank gets the result)."""
     world = dist.get_world_size(group)
     if world == 1:
         return scores, ids.to(torch.int64)
+    if scores.is_cuda:
+        i32 = ids if ids.dtype in (torch.int32,) else ids.to(torch.int32)
+        s_all = all_gather_stacked(scores, group)
+        i_all = all_gather_stacked(i32, group)
+        return merge_lists(s_all, i_all, k)
     ids64 = ids.to(torch.int64)
     s_all = [torch.empty_like(scores) for _ in range(world)]
     i_all = [torch.empty_like(ids64) for _ in range(world)]
@@ -100,12 +149,11 @@ def build_global_filter(engine, group=None):
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     h = engine.hist()
     if world > 1:
-        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        all_reduce_sum(h, group)
     slots = engine.slots(h)
     pre = engine.prefix(h, slots)
     if world > 1:
-        allp = torch.empty(world * slots, dtype=pre.dtype, device=pre.device)
-        dist.all_gather_into_tensor(allp, pre.contiguous(), group=group)
+        allp = all_gather_stacked(pre, group).reshape(-1)
     else:
         allp = pre
     return engine.finish(h, allp, world)

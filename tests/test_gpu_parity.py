@@ -245,10 +245,11 @@ def test_empty_batch_and_errors(fpp):
         fpp.Index.build(bad, L=2, K=2, D=16, iProbes=1, alpha=1.0)
 
 
-@pytest.mark.parametrize("path", ["cluster", "global"])
+@pytest.mark.parametrize("path", ["grouped", "cluster", "global"])
 def test_large_shard_collect_paths(fpp, orc, path, monkeypatch):
-    # the DSMEM-cluster bitmap (n > one SM's shared memory) and the global-memory
-    # bitmap fallback, forced at small n, must give the oracle's candidates/top-k
+    # the large-shard visited sets (n > one SM's shared memory): grouped dedup
+    # (id-range counting sort + per-warp range bitmaps), the DSMEM-cluster bitmap and
+    # the global-memory bitmap, forced at small n: the oracle's candidates/top-k/stats
     monkeypatch.setenv("FPP_FORCE_COLLECT", path)
     X = data(fpp, 20000, 64, 20, 0.3)
     Q = data(fpp, 40, 64, 20, 0.3, stream=1)
@@ -262,8 +263,8 @@ def test_large_shard_collect_paths(fpp, orc, path, monkeypatch):
     assert np.array_equal(gc, oc)
 
 
-def test_cluster_collect_natural_large_n(fpp, orc):
-    # n = 2.2M points > the single-CTA bitmap limit (~1.7M) -> cluster path for real
+def test_grouped_collect_natural_large_n(fpp, orc):
+    # n = 2.2M points > the single-CTA bitmap limit (~1.8M) -> grouped dedup for real
     X = data(fpp, 2_200_000, 16, 50, 0.2)
     Q = data(fpp, 16, 16, 50, 0.2, stream=1)
     ix = fpp.Index.build(X, L=2, K=2, D=16, iProbes=2, alpha=0.05, kappa=10)
@@ -447,7 +448,7 @@ def test_large_batch_reordered_equals_oracle(fpp, orc):
         assert np.array_equal(gi, oi) and np.array_equal(gs, os_) and np.array_equal(gst, ost)
 
 
-@pytest.mark.parametrize("geom", ["423", "432", "423-tma"])
+@pytest.mark.parametrize("geom", ["423", "432", "324", "423-tma"])
 @pytest.mark.parametrize("d", [128, 300, 301, 960])
 def test_score_early_termination_exact(fpp, orc, d, geom, monkeypatch, capfd):
     # k_score_pruned (Cauchy-Schwarz bound on the tail of each row against the running
@@ -491,23 +492,30 @@ def test_score_early_termination_unstructured(fpp, orc, monkeypatch):
 
 
 @pytest.mark.parametrize("prune", ["0", "1"])
-def test_nodedup_collect_same_answers(fpp, orc, prune, monkeypatch):
-    # FPP_NODEDUP=1: the walked ids are scored with repeats (no visited bitmap) and the
-    # top-k lists skip repeated ids; ids and scores must equal the oracle's.  Stats
-    # requests always dedup (unique candidate counts).
-    monkeypatch.setenv("FPP_NODEDUP", "1")
+@pytest.mark.parametrize("n,qp", [(20000, 5000), (2000, 3000)])
+def test_grouped_collect_every_id_once(fpp, orc, prune, n, qp, monkeypatch):
+    # grouped dedup (the large-shard path): every candidate id appears once and in
+    # ascending order (SPEC.md:352 -- stats.exact = unique candidates), so ids, scores
+    # and all four stats columns equal the oracle's, with and without early termination;
+    # n = 2000 packs many entries into few groups (heavy repeats)
+    monkeypatch.setenv("FPP_FORCE_COLLECT", "grouped")
     monkeypatch.setenv("FPP_PRUNE" if prune == "1" else "FPP_NO_PRUNE", "1")
-    X = data(fpp, 20000, 128, 200, 0.25, seed=41)
+    X = data(fpp, n, 128, 200, 0.25, seed=41)
     Q = data(fpp, 300, 128, 200, 0.25, seed=41, stream=1)
     ix = fpp.Index.build(X, L=12, K=2, D=128, iProbes=3, alpha=0.2)
     ox = orc.Index(X, L=12, K=2, D=128, iprobes=3, alpha=0.2)
-    gi, gs = ix.query(Q, 20, 5000)
-    oi, os_, ost = ox.query(Q, 20, 5000)
+    oi, os_, ost = ox.query(Q, 20, qp)
+    gi, gs = ix.query(Q, 20, qp)
     assert np.array_equal(gi, oi)
     ok = np.isfinite(os_)
     assert np.array_equal(gs[ok], os_[ok])
-    si, ss, sst = ix.query(Q, 20, 5000, return_stats=True)
+    si, ss, sst = ix.query(Q, 20, qp, return_stats=True)
     assert np.array_equal(si, oi) and np.array_equal(sst, ost)
+    assert (sst[:, 3] == sst[:, 2]).all() and (ost[:, 1] >= ost[:, 2]).all()
+    for qi in (0, 99):
+        _, gc = ix.query_debug(Q[qi], qp)
+        _, oc = ox.query_debug(Q[qi], qp)
+        assert np.array_equal(gc, oc)
 
 
 def test_query_out_buffers(fpp, orc):
@@ -524,21 +532,3 @@ def test_query_out_buffers(fpp, orc):
     assert np.array_equal(oi, gi) and np.array_equal(os_, gs)
     with pytest.raises(ValueError):
         ix.query(Q, 10, 300, out=(np.zeros((50, 9), np.uint32), os_))
-
-
-def test_dedup_policy_auto_switch(fpp, orc, monkeypatch):
-    # with an off-chip visited bitmap (forced here) and few repeated ids, the first
-    # query call measures entries/unique on a dedup chunk and later calls collect
-    # without dedup; every call must return the oracle's answers
-    monkeypatch.setenv("FPP_FORCE_COLLECT", "cluster")
-    X = data(fpp, 30000, 128, 0, 0.0, seed=9)
-    Q = data(fpp, 200, 128, 0, 0.0, seed=9, stream=1)
-    ix = fpp.Index.build(X, L=4, K=2, D=128, iProbes=2, alpha=0.5)
-    ox = orc.Index(X, L=4, K=2, D=128, iprobes=2, alpha=0.5)
-    oi, os_, ost = ox.query(Q, 10, 400)
-    ok = np.isfinite(os_)
-    assert (ost[:, 1].sum() / max(1, ost[:, 2].sum())) < 1.25  # few repeats
-    for _ in range(3):
-        gi, gs = ix.query(Q, 10, 400)
-        assert np.array_equal(gi, oi)
-        assert np.array_equal(gs[ok], os_[ok])
