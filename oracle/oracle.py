@@ -353,7 +353,7 @@ def csr_from_entries(eb: np.ndarray, es: np.ndarray, n: int, iprobes: int, NB: i
     off = np.empty(NB + 1, np.uint32)
     ids = np.empty(max(1, n * iprobes), np.uint32)
     sc = np.empty(max(1, n * iprobes), np.float32)
-    tot = self._L.orc_csr_from_entries(eb, es, n, iprobes, NB, alpha, kappa, id0,
+    tot = lib().orc_csr_from_entries(eb, es, n, iprobes, NB, alpha, kappa, id0,
                                      threads or os.cpu_count(), off, ids, sc)
     return off, ids[:tot].copy(), sc[:tot].copy()
 

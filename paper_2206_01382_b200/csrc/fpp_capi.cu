@@ -91,6 +91,7 @@ Index::~Index() {
   dfree(signs);
   dfree(sigs);
   dfree(xtail);
+  dfree(q8rec);
   dfree(offsets);
   dfree(table_base);
   dfree(ids);
@@ -105,7 +106,7 @@ Index::~Index() {
 void QueryCtx::QSlot::release() {
   vals.release(); codes.release(); ppos.release(); plen.release(); gbuf.release();
   ckey.release(); cpair.release(); dbgclk.release(); eq.release(); coff.release();
-  uq.release(); cands.release(); bitmap.release(); counter.release();
+  uq.release(); uniq.release(); cands.release(); bitmap.release(); counter.release();
   qsig.release(); cands2.release(); uq2.release();
   if (pinned) cudaFreeHost(pinned);
   if (ev_probe) cudaEventDestroy(ev_probe);
@@ -302,7 +303,62 @@ __global__ void k_tail_norms(const float* __restrict__ X, uint64_t n, uint32_t d
   }
 }
 
+// Screening records for k_score_screen (warp per row): two 64-byte stages per row.
+// Stage j covers dims [48 j, 48 j + 48): int8 codes with the stage's scale
+// s = max|x_i| / 127 (fp32), codes rint(x_i / s); then, in fp64 and rounded up to
+// fp32 (x 1+1e-12): r = ||x_h - s code|| (quantization error), m = ||s code|| and
+// t = ||x[48 j + 48 : d)|| (everything after the stage).  Record = 48 code bytes +
+// {s, r, m, t}.  The score kernel bounds the stage's part of x.q by
+// s_q s I + r ||q_h|| + m ||q_h - q~_h|| (I = the integer dot product of the codes)
+// and the rest by t ||q_t|| (Cauchy-Schwarz).
+__global__ void k_q8_records(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx,
+                             uint4* __restrict__ rec) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+    const float* r = X + i * ldx;
+#pragma unroll
+    for (uint32_t stage = 0; stage < Q8_STAGES; ++stage) {
+      const uint32_t lo = stage * Q8_DIMS, hi = lo + Q8_DIMS;
+      const uint32_t j0 = lo + lane, j1 = lo + lane + 32;
+      const float x0 = j0 < min(d, hi) ? r[j0] : 0.f;
+      const float x1 = (lane < 16 && j1 < min(d, hi)) ? r[j1] : 0.f;
+      float mx = fmaxf(fabsf(x0), fabsf(x1));
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float sc = mx / 127.0f;
+      const int c0 = sc > 0.f ? max(-127, min(127, __float2int_rn(x0 / sc))) : 0;
+      const int c1 = sc > 0.f ? max(-127, min(127, __float2int_rn(x1 / sc))) : 0;
+      const double e0 = (double)x0 - (double)sc * c0, e1 = (double)x1 - (double)sc * c1;
+      const double m0 = (double)sc * c0, m1 = (double)sc * c1;
+      double er = e0 * e0 + e1 * e1, mm = m0 * m0 + m1 * m1, tt = 0.0;
+      for (uint32_t j = hi + lane; j < d; j += 32) tt = fma((double)r[j], (double)r[j], tt);
+      for (int o = 16; o; o >>= 1) {
+        er += __shfl_xor_sync(0xffffffffu, er, o);
+        mm += __shfl_xor_sync(0xffffffffu, mm, o);
+        tt += __shfl_xor_sync(0xffffffffu, tt, o);
+      }
+      // byte b of the stage record = code of dim lo + b (lanes: b = lane, lane + 32 < 48)
+      unsigned char* rb = reinterpret_cast<unsigned char*>(rec + (i * Q8_STAGES + stage) * 4);
+      rb[lane] = (unsigned char)(signed char)c0;
+      if (lane < 16) rb[lane + 32] = (unsigned char)(signed char)c1;
+      if (lane == 0) {
+        float4 m;
+        m.x = sc;
+        m.y = __double2float_ru(__dsqrt_ru(er) * (1.0 + 1e-12));
+        m.z = __double2float_ru(__dsqrt_ru(mm) * (1.0 + 1e-12));
+        m.w = __double2float_ru(__dsqrt_ru(tt) * (1.0 + 1e-12));
+        *reinterpret_cast<float4*>(rb + Q8_DIMS) = m;
+      }
+    }
+  }
+}
+
 void launch_tail_norms(Index& ix) {
+  if (ix.d >= 64 && ix.d <= 256 && ix.d % 4 == 0) {  // k_score_screen's records
+    ix.q8rec = static_cast<uint4*>(dmalloc((size_t)ix.n * 64 * Q8_STAGES));
+    k_q8_records<<<sm_count() * 8, 256, 0, ix.stream>>>(ix.X, ix.n, ix.d, ix.ldx, ix.q8rec);
+    FPP_LAUNCH();
+  }
   // head width: 32 floats for rows of <= 192 floats (C4's d = 128: the score gather is
   // HBM-bound there and a far candidate then costs 128 B instead of 256 B: 157k -> 200k
   // q/s), else 64 (C2's d = 300 is latency-bound: a narrower head only adds a tail job

@@ -93,6 +93,10 @@ struct Index {
   // ||X[i][(j+1)*XT_SLICE:d)||, rounded up to fp32, checkpoints j < xt_n
   float* xtail = nullptr;
   uint32_t xt_n = 0;
+  // narrow rows (64 <= d <= 256, d % 4 == 0; k_score_screen): Q8_STAGES 64 B
+  // screening records per row -- Q8_DIMS dims each as int8 codes with a per-row
+  // scale, plus the error / norm terms of the bound (k_q8_records)
+  uint4* q8rec = nullptr;
   uint32_t xt_head = 64;  // head (screening) slice width, see launch_tail_norms
   std::vector<float> center;  // [d] when prm.centering (dataset.cpp center())
   uint64_t device_bytes = 0;
@@ -136,6 +140,7 @@ struct QueryCtx {
     DBuf<uint32_t> eq;
     DBuf<uint64_t> coff;
     DBuf<uint32_t> uq;
+    DBuf<uint32_t> uniq;    // unique candidates per query (grouped lists carry holes)
     DBuf<uint32_t> cands;
     DBuf<uint32_t> bitmap;
     DBuf<uint32_t> counter;
@@ -200,6 +205,10 @@ uint64_t content_hash(const float* X, uint64_t n, uint32_t d);
 void save_index(const Index& ix, const char* path, const float* X_host);
 void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint32_t ld, uint64_t* out,
                        cudaStream_t s);
+// k_score_screen record: int8 codes of dims [0, Q8_DIMS) (48 B) + {scale, ||x_h - x~_h||,
+// ||x~_h||, ||x[Q8_DIMS:d)||} as fp32 rounded up (16 B) = 64 B per row
+constexpr uint32_t Q8_DIMS = 48;
+constexpr uint32_t Q8_STAGES = 2;  // records per row: dims [0,48) and [48,96), 128 B per row
 constexpr uint32_t XT_SLICE = 64;  // = the score ring's row-slice width for d >= 64
 constexpr uint32_t XT_MAX = 4;     // tail-norm checkpoints per row
 // score-gather slices of a d-wide row: a head [0, h) (h = Index::xt_head, 32 or 64),

@@ -979,6 +979,8 @@ struct CollectArgs {
   uint32_t* counter;     // dynamic query fetch
   uint32_t grouped;      // 1: two-level dedup by id-range groups (large shards, stage_b)
   uint32_t gshift;       // grouped: id >> gshift < CO_NG; per-warp range bitmap 2^gshift bits
+  uint32_t* uniq;        // unique candidates per query (uq = list length incl. grouped holes)
+  uint64_t n;            // points (grouped: groups in use = ((n - 1) >> gshift) + 1)
 };
 
 // Warp-cooperative walk over one query's probes.  A warp takes 32 probes at a
@@ -1065,22 +1067,23 @@ __device__ __forceinline__ void collect_walk(const uint64_t* pp, const uint32_t*
 
 // Grouped dedup (large shards: the n-bit visited set is off-chip).  Two walks
 // form a counting sort of the walked ids into CO_NG id-range groups (2^gshift
-// ids each) in the query's candidate segment; then each warp takes groups, ORs
-// the group's ids into a 2^gshift-bit range bitmap in shared memory, and writes
-// the set bits back in ascending order at the group's start; finally the groups'
-// unique prefixes are compacted (ascending blocks: a block's sources lie at or
-// above its destinations, so one pass in place is safe).  Every id is emitted
-// once and the list is ascending, as with the whole-n bitmap.
-constexpr uint32_t CO_NG = 4096;
+// ids each) in the query's candidate segment (groups ascending, so similar
+// queries still gather the same id ranges at about the same time); then each
+// warp takes groups and tests-and-sets the group's ids in a 2^gshift-bit range
+// bitmap in shared memory: a repeat is overwritten in place with 0xFFFFFFFF (a
+// hole the score kernels skip), and the touched words are cleared again.  Every
+// id is therefore scored once at a cost proportional to the walked
+// entries.  uq[q] = the list length (holes included), uniq[q] = unique ids.
+constexpr uint32_t CO_NG = 1024;
 __device__ __forceinline__ void collect_grouped(const CollectArgs& a, uint32_t q, uint32_t* out,
                                                 uint32_t* ucount, uint32_t* nextc, uint32_t* sm,
                                                 uint32_t* scan_sh, uint32_t* U_out) {
   uint32_t* cnt = sm;             // [CO_NG] group counts -> scatter cursors (= group ends)
-  uint32_t* ucnt = sm + CO_NG;    // [CO_NG] unique ids per group -> destinations
-  uint32_t* wbm = sm + 2 * CO_NG; // [32 warps][2^gshift / 32] range bitmaps
+  uint32_t* wbm = sm + CO_NG;     // [32 warps][2^gshift / 32] range bitmaps (kept clear)
+  __shared__ uint32_t dups_sh;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t P = (uint32_t)a.peff, gs = a.gshift;
-  const uint32_t bw = 1u << (gs - 5), wpl = bw >= 32 ? bw / 32 : 1;  // bitmap words, per lane
+  const uint32_t bw = 1u << (gs - 5);  // bitmap words per warp
   const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
   const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
   auto next_chunk = [&]() {
@@ -1089,21 +1092,18 @@ __device__ __forceinline__ void collect_grouped(const CollectArgs& a, uint32_t q
     return __shfl_sync(FULL, c, 0);
   };
   for (uint32_t i = threadIdx.x; i < CO_NG; i += blockDim.x) cnt[i] = 0;
+  if (threadIdx.x == 0) dups_sh = 0;
   __syncthreads();
   collect_walk(pp, pl, P, a.ids, out, ucount, next_chunk, [&](uint32_t id) {
     smem_inc(&cnt[id >> gs]);
     return false;
   });
   __syncthreads();
+  uint32_t E;
   {  // exclusive scan of the group counts -> scatter cursors
-    constexpr uint32_t PER = CO_NG / 1024;  // blockDim.x == CO_THREADS == 1024
-    uint32_t v[PER], t = 0;
-#pragma unroll
-    for (uint32_t j = 0; j < PER; ++j) { v[j] = cnt[threadIdx.x * PER + j]; t += v[j]; }
-    uint32_t tot;
-    uint32_t b = block_excl_scan_u32(t, scan_sh, &tot);
-#pragma unroll
-    for (uint32_t j = 0; j < PER; ++j) { cnt[threadIdx.x * PER + j] = b; b += v[j]; }
+    static_assert(CO_NG == CO_THREADS, "one group count per thread");
+    const uint32_t v = cnt[threadIdx.x];
+    cnt[threadIdx.x] = block_excl_scan_u32(v, scan_sh, &E);
     if (threadIdx.x == 0) *nextc = 0;
   }
   __syncthreads();
@@ -1113,81 +1113,71 @@ __device__ __forceinline__ void collect_grouped(const CollectArgs& a, uint32_t q
   });
   __syncthreads();  // cnt[g] is now the end of group g (= the start of group g + 1)
   uint32_t* bm = wbm + (size_t)w * bw;
-  for (uint32_t g = w; g < CO_NG; g += blockDim.x >> 5) {
-    const uint32_t S = g ? cnt[g - 1] : 0u, E = cnt[g];
-    if (E - S <= 1) {  // empty or a single id: already unique
-      if (lane == 0) ucnt[g] = E - S;
-      continue;
-    }
-    for (uint32_t j = lane; j < bw; j += 32) bm[j] = 0;
-    __syncwarp();
-    for (uint32_t i = S + lane; i < E; i += 32) {
-      const uint32_t b = out[i] & ((1u << gs) - 1u);
-      asm volatile("red.shared.or.b32 [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(bm + (b >> 5))),
-                   "r"(1u << (b & 31))
-                   : "memory");
-    }
-    __syncwarp();
-    // ascending emission of the set bits at the group's start (its reads are done)
-    const uint32_t w0 = min(bw, (uint32_t)lane * wpl), w1 = min(bw, w0 + wpl);
-    uint32_t c = 0;
-    for (uint32_t j = w0; j < w1; ++j) c += __popc(bm[j]);
-    uint32_t x = c;
+  const uint32_t mask = (1u << gs) - 1u;
+  const uint32_t gstep = blockDim.x >> 5;
+  const uint32_t ng = (uint32_t)((a.n - 1) >> gs) + 1;  // groups in use
+  uint32_t dups = 0;
+  auto tas = [&](uint32_t id) {  // test-and-set in the range bitmap: true = a repeat
+    const uint32_t b = id & mask, bit = 1u << (b & 31);
+    uint32_t old;
+    asm volatile("atom.shared.or.b32 %0, [%1], %2;\n"
+                 : "=r"(old)
+                 : "r"((uint32_t)__cvta_generic_to_shared(bm + (b >> 5))), "r"(bit)
+                 : "memory");
+    return (old & bit) != 0u;
+  };
+  // groups g = w, w + 32, ... (~100-200 ids each): the first 256 entries of a group are
+  // held in registers (8 per lane: one load round trip), tested-and-set, repeats
+  // overwritten with holes, and the touched bitmap words cleared from the registers
+  for (uint32_t g = w; g < ng; g += gstep) {
+    const uint32_t S = g ? cnt[g - 1] : 0u, Eg = cnt[g];
+    if (Eg - S <= 1) continue;  // (empty groups and single ids hold no repeats)
+    uint32_t v[8];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(FULL, x, o);
-      if (lane >= o) x += y;
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t i = S + u * 32 + lane;
+      v[u] = i < Eg ? out[i] : 0xffffffffu;
     }
-    uint32_t pos = S + x - c;
-    const uint32_t base = g << gs;
-    for (uint32_t j = w0; j < w1; ++j)
-      for (uint32_t word = bm[j]; word; word &= word - 1) out[pos++] = base + j * 32 + (__ffs(word) - 1);
-    if (lane == 31) ucnt[g] = x;
-    __syncwarp();
-  }
-  __syncthreads();
-  uint32_t U;
-  {  // destinations: exclusive scan of the unique counts
-    constexpr uint32_t PER = CO_NG / 1024;
-    uint32_t v[PER], t = 0;
 #pragma unroll
-    for (uint32_t j = 0; j < PER; ++j) { v[j] = ucnt[threadIdx.x * PER + j]; t += v[j]; }
-    uint32_t b = block_excl_scan_u32(t, scan_sh, &U);
-#pragma unroll
-    for (uint32_t j = 0; j < PER; ++j) { ucnt[threadIdx.x * PER + j] = b; b += v[j]; }
-  }
-  __syncthreads();
-  // in-place compaction, ascending blocks: output j of group g comes from
-  // S_g + (j - D_g) >= j, so a block's reads never hit a slot an earlier block wrote
-  for (uint32_t j0 = 0; j0 < U; j0 += blockDim.x) {
-    const uint32_t j = j0 + threadIdx.x;
-    uint32_t v = 0;
-    if (j < U) {
-      uint32_t lo = 0, hi = CO_NG;  // last group g with D_g <= j (it holds j: j < D_g + u_g)
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (ucnt[mid] <= j) lo = mid;
-        else hi = mid;
+    for (int u = 0; u < 8; ++u)
+      if (v[u] != 0xffffffffu && tas(v[u])) {  // a repeat: the first occurrence stays
+        out[S + u * 32 + lane] = 0xffffffffu;
+        v[u] = 0xffffffffu;
+        ++dups;
       }
-      const uint32_t S = lo ? cnt[lo - 1] : 0u;
-      v = out[S + (j - ucnt[lo])];
+    for (uint32_t i = S + 256 + lane; i < Eg; i += 32)
+      if (tas(out[i])) {
+        out[i] = 0xffffffffu;
+        ++dups;
+      }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 8; ++u)  // clear the touched words again
+      if (v[u] != 0xffffffffu) bm[(v[u] & mask) >> 5] = 0;
+    for (uint32_t i = S + 256 + lane; i < Eg; i += 32) {
+      const uint32_t id = out[i];
+      if (id != 0xffffffffu) bm[(id & mask) >> 5] = 0;
     }
-    __syncthreads();
-    if (j < U) out[j] = v;
-    __syncthreads();
+    __syncwarp();
   }
-  *U_out = U;
+  dups = __reduce_add_sync(FULL, dups);
+  if (lane == 0 && dups) atomicAdd(&dups_sh, dups);
+  __syncthreads();
+  *U_out = E - dups_sh;
 }
 
 // CTA per query (persistent CTAs fetch queries dynamically); the visited
 // bitmap lives in shared memory (n bits), or the grouped dedup runs (large
 // shards), or -- beyond the grouped range -- a per-CTA global-memory bitmap that
 // is cleared again through the candidate list.
-__global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
+__global__ void __launch_bounds__(CO_THREADS, 2) k_collect(CollectArgs a) {
   extern __shared__ __align__(16) uint32_t sbm[];
   __shared__ uint32_t ucount, qsh, nextc;
   __shared__ uint32_t scan_sh[32];
   uint32_t* bm = a.gbitmap ? a.gbitmap + (uint64_t)blockIdx.x * a.nwords : sbm;
+  if (a.grouped)  // the per-warp range bitmaps start clear and are kept clear
+    for (uint32_t i = threadIdx.x; i < (blockDim.x >> 5) << (a.gshift - 5); i += blockDim.x)
+      sbm[CO_NG + i] = 0;
   for (;;) {
     if (threadIdx.x == 0) {
       qsh = atomicAdd(a.counter, 1u);
@@ -1212,7 +1202,10 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
     };
     uint32_t U;
     if (a.grouped) {
-      collect_grouped(a, q, out, &ucount, &nextc, sbm, scan_sh, &U);
+      uint32_t Uu;
+      collect_grouped(a, q, out, &ucount, &nextc, sbm, scan_sh, &Uu);
+      if (threadIdx.x == 0) a.uniq[q] = Uu;
+      U = (uint32_t)(a.coff[q + 1] - a.coff[q]);  // list length, holes included
     } else if (!a.gbitmap) {
       // shared-memory bitmap: fire-and-forget ORs during the walk, then the set
       // bits are emitted in ascending id order (a bitmap scan), so every query's
@@ -1243,7 +1236,10 @@ __global__ void __launch_bounds__(CO_THREADS) k_collect(CollectArgs a) {
       __syncthreads();
       U = ucount;
     }
-    if (threadIdx.x == 0) a.uq[q] = U;
+    if (threadIdx.x == 0) {
+      a.uq[q] = U;
+      if (a.uniq && !a.grouped) a.uniq[q] = U;
+    }
     if (a.gbitmap)
       for (uint32_t c = threadIdx.x; c < U; c += blockDim.x) bm[out[c] >> 5] = 0;
     __syncthreads();
@@ -1450,6 +1446,11 @@ struct ScoreArgs {
   uint64_t n;
   unsigned long long* dbg;  // FPP_DEBUG_PRUNE: [rows, row slices read]
   unsigned long long* rbytes;  // += candidate-row bytes read (fpp_timings.score_bytes)
+  // k_score_screen seeds: the query's first `nseedp` probes (the forced true buckets)
+  const uint64_t* ppos;
+  const uint32_t* plen;
+  const uint32_t* ids;
+  uint32_t nseedp;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1636,9 +1637,8 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
     ++ncomp;
     if (++cc == nsl) {
       const uint32_t ci = cb * 32 + lane;
-      const bool valid = ci < U;
-      const uint32_t id = valid ? __ldg(cand + ci) : 0xffffffffu;
-      topk_insert(bs, bi, k, acc, id, valid);
+      const uint32_t id = ci < U ? __ldg(cand + ci) : 0xffffffffu;
+      topk_insert(bs, bi, k, acc, id, id != 0xffffffffu);  // (grouped lists carry holes)
       acc = 0.0;
       cc = 0;
       cb += SC_WARPS;
@@ -1659,13 +1659,16 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
       a.out_ids[(uint64_t)q * k + lane] = ok ? bi + a.id_offset : 0xffffffffu;
       a.out_scores[(uint64_t)q * k + lane] = ok ? bs : -INFINITY;
     }
+    // unique candidates scored: the list length, or (grouped lists with holes) the
+    // collect's unique count; with a SimHash screen the screened list
+    const uint32_t Uu = a.cstride ? U : (a.uq_all ? a.uq_all[q] : U);
     if (lane == 0 && a.stats) {
       a.stats[q].probes = a.peff;
       a.stats[q].entries = a.eq[q];
       a.stats[q].candidates = a.uq_all ? a.uq_all[q] : U;
-      a.stats[q].exact = U;
+      a.stats[q].exact = Uu;
     }
-    if (lane == 0 && a.rbytes) atomicAdd(a.rbytes, (unsigned long long)U * d * 4ull);
+    if (lane == 0 && a.rbytes) atomicAdd(a.rbytes, (unsigned long long)Uu * d * 4ull);
   }
   if (!a.qctr) return;
   __syncthreads();  // qd, mg_* and q_sh are reused by the next query
@@ -2018,13 +2021,415 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
         a.stats[q].probes = a.peff;
         a.stats[q].entries = a.eq[q];
         a.stats[q].candidates = a.uq_all ? a.uq_all[q] : U;
-        a.stats[q].exact = U;
+        a.stats[q].exact = a.cstride ? U : (a.uq_all ? a.uq_all[q] : U);
       }
     }
     __syncthreads();  // mg_* (ring), qd, thr_s are reused by the next query
     if (TMA) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> TMA
     if (!a.qctr) return;
   }
+}
+
+// --------------------------------------------- narrow rows: screen + exact finish
+// k_score_screen: the score gather for narrow rows (64 <= d <= 256: C1, C4), with
+// exact early termination restructured around bytes and instructions (the fp64
+// sequential fold of every candidate head made k_score_pruned issue-bound, and the
+// fp32 head is 128 B per candidate).
+//   Screen.  Every row has a 64-byte record built with the index (k_q8_records):
+//   dims [0, 48) as int8 codes c with a per-row scale s_x, and {s_x, r_x = ||x_h -
+//   s_x c||, m_x = ||s_x c||, t_x = ||x[48:d)||} rounded up.  The query head is
+//   quantized the same way per CTA (q~ = s_q c_q, r_q = ||q_h - q~||).  A warp takes
+//   32 candidates: four lanes read one record (16 B each; eight records per load
+//   instruction), three of them form the integer dot product I = c.c_q with DP4A,
+//   a 2-step shuffle sums it and the record's fourth lane bounds the row's final
+//   computed score:
+//     S <= s_x s_q I + r_x ||q_h|| + m_x r_q + t_x ||q_t|| + 1e-6 (|.| terms)
+//   (x.q = x~.q~ + (x_h - x~).q_h + x~.(q_h - q~) + x_t.q_t, each by Cauchy-Schwarz;
+//   every term is evaluated with upward rounding, and the 1e-6 relative margin also
+//   covers the fp64 summation error of the final score).  A row whose bound is below
+//   the CTA's running k-th best lower bound (the best warp's k-th, or the worst
+//   warp's ceil(k/NW)-th: the warps hold disjoint candidates) ends strictly below
+//   the final k-th best: it cannot enter the top-k nor tie.
+//   Exact.  Survivor ids queue per warp (shared memory); every 32 are finished as
+//   one dense batch: 32-float chunks of the 32 rows are loaded coalesced (4 rows
+//   per instruction), staged in shared memory (row stride 36 floats: conflict-free
+//   STS.128/LDS.128), and lane r folds row r in the reference's sequential fp64
+//   order (dataset.cpp:67), so the score equals inner_product bit for bit; the next
+//   chunk's loads are in flight meanwhile.  The batch enters the warp's register
+//   top-k and raises the CTA thresholds.
+// Results are identical to k_score / k_score_pruned / the oracle.  Grouped candidate
+// lists may carry holes (0xFFFFFFFF): skipped.
+constexpr int NS_W = 8;            // warps per CTA
+constexpr uint32_t NS_QCAP = 64;   // survivor queue per warp (<= 31 + 32 queued)
+constexpr int NS_PAD = 36;         // staging row stride in floats
+constexpr uint32_t NS_HASH_BITS = 11, NS_HASH = 1u << NS_HASH_BITS;  // seed dedup table
+constexpr uint32_t NS_SEEDS = 1024;  // seeds kept (hash load <= 1/2)
+
+__device__ __forceinline__ unsigned long long dkey(double x) {  // order-preserving
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+template <int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  constexpr uint32_t NONE = 0xffffffffu;
+  const uint32_t d = a.d, nch = (d + 31) / 32;  // 32-float chunks (rows padded with zeros)
+  double* qd = reinterpret_cast<double*>(smraw);                       // [32 * nch]
+  float* stg_all = reinterpret_cast<float*>(smraw + (size_t)nch * 32 * 8);  // [NW][32][NS_PAD]
+  uint32_t* sq_all = reinterpret_cast<uint32_t*>(stg_all + (size_t)NW * 32 * NS_PAD);  // [NW][QCAP]
+  uint32_t* s1_all = sq_all + (size_t)NW * NS_QCAP;                    // [NW][QCAP] stage-2 queue ids
+  float2* s1v_all = reinterpret_cast<float2*>(s1_all + (size_t)NW * NS_QCAP);  // [NW][QCAP] (A1, N1)
+  __shared__ unsigned long long thr_key;  // lower bound of the final k-th best (ordered key)
+  __shared__ double thr2_s[NW];          // per warp: its ceil(k/NW)-th best (main lists)
+  __shared__ double thr3_s[NW];          // the same for the seed lists
+  __shared__ uint32_t nseed_s;
+  __shared__ float qn_s[Q8_STAGES][4];   // per stage: s_q, ||q_h||, r_q, ||q after the stage||
+  __shared__ __align__(16) int32_t q8_s[Q8_STAGES][Q8_DIMS / 4];  // the query's stage codes
+  __shared__ double mg_s[NW][32];
+  __shared__ uint32_t mg_i[NW][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int part = lane & 3, grp = lane >> 2;  // record part (0-2 codes, 3 terms), record slot
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  float* stg = stg_all + (size_t)w * 32 * NS_PAD;
+  uint32_t* sq = sq_all + (size_t)w * NS_QCAP;    // survivors of stage 2 -> exact
+  uint32_t* s1q = s1_all + (size_t)w * NS_QCAP;   // survivors of stage 1 -> stage 2
+  float2* s1v = s1v_all + (size_t)w * NS_QCAP;
+  const uint32_t q = blockIdx.x;
+  const float* Qr = a.Q + (uint64_t)q * d;
+  for (uint32_t j = threadIdx.x; j < nch * 32; j += blockDim.x) qd[j] = j < d ? (double)Qr[j] : 0.0;
+  if (threadIdx.x == 0) thr_key = dkey(-INFINITY);
+  if (threadIdx.x < NW) thr2_s[threadIdx.x] = thr3_s[threadIdx.x] = -INFINITY;
+  if ((uint32_t)w < Q8_STAGES) {  // quantize the query like the records (k_q8_records)
+    const uint32_t lo = w * Q8_DIMS, hi = lo + Q8_DIMS;
+    const uint32_t j0 = lo + lane, j1 = lo + lane + 32;
+    const float x0 = j0 < min(d, hi) ? Qr[j0] : 0.f;
+    const float x1 = (lane < 16 && j1 < min(d, hi)) ? Qr[j1] : 0.f;
+    float mx = fmaxf(fabsf(x0), fabsf(x1));
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+    const float sc = mx / 127.0f;
+    const int c0 = sc > 0.f ? max(-127, min(127, __float2int_rn(x0 / sc))) : 0;
+    const int c1 = sc > 0.f ? max(-127, min(127, __float2int_rn(x1 / sc))) : 0;
+    const double e0 = (double)x0 - (double)sc * c0, e1 = (double)x1 - (double)sc * c1;
+    double er = e0 * e0 + e1 * e1, hh = (double)x0 * x0 + (double)x1 * x1, tt = 0.0;
+    for (uint32_t j = hi + lane; j < d; j += 32) tt = fma((double)Qr[j], (double)Qr[j], tt);
+    for (int o = 16; o; o >>= 1) {
+      er += __shfl_xor_sync(FULL, er, o);
+      hh += __shfl_xor_sync(FULL, hh, o);
+      tt += __shfl_xor_sync(FULL, tt, o);
+    }
+    unsigned char* qb = reinterpret_cast<unsigned char*>(q8_s[w]);
+    qb[lane] = (unsigned char)(signed char)c0;
+    if (lane < 16) qb[lane + 32] = (unsigned char)(signed char)c1;
+    if (lane == 0) {
+      qn_s[w][0] = sc;
+      qn_s[w][1] = __double2float_ru(__dsqrt_ru(hh) * (1.0 + 1e-12));
+      qn_s[w][2] = __double2float_ru(__dsqrt_ru(er) * (1.0 + 1e-12));
+      qn_s[w][3] = __double2float_ru(__dsqrt_ru(tt) * (1.0 + 1e-12));
+    }
+  }
+  __syncthreads();
+  const uint32_t Len = a.uq[q];
+  const uint32_t* cand = a.cands + a.coff[q];
+  const uint32_t k = a.k;
+  const uint4* rec = reinterpret_cast<const uint4*>(a.xtail);  // [n][stages][4] 16 B parts
+  const float* X = a.X;
+  const uint32_t ldx = a.ldx;
+  double bs = -INFINITY;
+  uint32_t bi = NONE;
+  uint32_t qhead = 0, qtail = 0, h1 = 0, t1 = 0;  // exact queue, stage-2 queue
+  unsigned long long nrows = 0, nst2 = 0, nfl = 0;  // rows screened, stage-2 records, row floats
+
+  // ---------------------------------------------------------------- exact rows
+  // lane r folds row `id` of lane r (NONE: nothing) in the reference's order
+  auto exact_fold = [&](uint32_t id) {
+    // each chunk moves in two halves of 16 rows (4 loads per lane: fewer live
+    // registers); the next chunk's first half is in flight while this one is folded
+    float4 v[4];
+    const int c8 = lane & 7, g4 = lane >> 3;
+    auto load_half = [&](uint32_t ch, int h) {
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const uint32_t idr = __shfl_sync(FULL, id, (h * 4 + it) * 4 + g4);
+        v[it] = idr != NONE ? __ldcg(reinterpret_cast<const float4*>(X + (uint64_t)idr * ldx + ch * 32) + c8)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    auto store_half = [&](int h) {
+#pragma unroll
+      for (int it = 0; it < 4; ++it)
+        *reinterpret_cast<float4*>(stg + ((h * 4 + it) * 4 + g4) * NS_PAD + 4 * c8) = v[it];
+    };
+    load_half(0, 0);
+    double acc = 0.0;
+    for (uint32_t ch = 0; ch < nch; ++ch) {
+      __syncwarp();  // the previous chunk's readers are done with the staging rows
+      store_half(0);
+      load_half(ch, 1);
+      store_half(1);
+      if (ch + 1 < nch) load_half(ch + 1, 0);
+      __syncwarp();
+      const float* row = stg + lane * NS_PAD;
+      const double* qq = qd + ch * 32;
+      // dataset.cpp:67 acc += double(a[i]) * double(b[i]), sequential i (exact products)
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        const float4 xv = *reinterpret_cast<const float4*>(row + j);
+        acc = fma((double)xv.x, qq[j], acc);
+        acc = fma((double)xv.y, qq[j + 1], acc);
+        acc = fma((double)xv.z, qq[j + 2], acc);
+        acc = fma((double)xv.w, qq[j + 3], acc);
+      }
+    }
+    return acc;
+  };
+  // lower bounds of the final k-th best from a family of NW disjoint per-warp lists
+  // (lb[] = that family's per-warp ceil(k/NW)-th bests): this warp's k-th score, and
+  // the worst warp's ceil(k/NW)-th (NW * ceil(k/NW) >= k distinct scores are at least
+  // that); folded into one word by atomicMax (a max of lower bounds is one), so
+  // readers load a single value per batch
+  auto publish = [&](double lbs, uint32_t lbi, volatile double* lb) {
+    const uint32_t ks = (k + NW - 1) / NW;
+    const uint32_t kid = __shfl_sync(FULL, lbi, k - 1), kid2 = __shfl_sync(FULL, lbi, ks - 1);
+    const double kth = __shfl_sync(FULL, lbs, k - 1), kth2 = __shfl_sync(FULL, lbs, ks - 1);
+    if (lane == 0) {
+      if (kid2 != NONE) lb[w] = kth2;
+      double t2 = INFINITY;
+#pragma unroll
+      for (int i = 0; i < NW; ++i) t2 = fmin(t2, lb[i]);
+      const double t = kid != NONE ? fmax(kth, t2) : t2;
+      if (t > -INFINITY) atomicMax(&thr_key, dkey(t));
+    }
+  };
+  auto exact_batch = [&](uint32_t cnt) {
+    const uint32_t id = (uint32_t)lane < cnt ? sq[(qhead + lane) % NS_QCAP] : NONE;
+    qhead += cnt;
+    const double acc = exact_fold(id);
+    topk_insert(bs, bi, k, acc, id, id != NONE);
+    if (lane == 0) nfl += (unsigned long long)cnt * nch * 32;
+    publish(bs, bi, thr2_s);
+  };
+
+  // ---------------------------------------------------------------- seeds
+  // The candidates in the query's true buckets (its first nseedp probes, one per
+  // table) are mostly its near neighbours: deduplicated (shared-memory hash) and
+  // scored exactly first, into per-warp seed lists that only raise the threshold
+  // (their own family of disjoint lists); the scan below then starts near the final
+  // k-th best instead of at -inf.  Seeds are scanned again like any candidate.
+  if (a.nseedp) {
+    uint32_t* hs = reinterpret_cast<uint32_t*>(s1v_all + (size_t)NW * NS_QCAP);  // [NS_HASH]
+    uint32_t* seeds = hs + NS_HASH;                                               // [NS_SEEDS]
+    for (uint32_t i = threadIdx.x; i < NS_HASH; i += blockDim.x) hs[i] = NONE;
+    if (threadIdx.x == 0) nseed_s = 0;
+    __syncthreads();
+    const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
+    const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
+    for (uint32_t p = w; p < a.nseedp; p += NW) {
+      const uint64_t p0 = pp[p];
+      const uint32_t len = pl[p];
+      for (uint32_t e = lane; e < len; e += 32) {
+        const uint32_t id = __ldg(a.ids + p0 + e);
+        uint32_t h = (id * 2654435761u) >> (32 - NS_HASH_BITS);
+        for (uint32_t tries = 0; tries < NS_HASH; ++tries) {
+          const uint32_t old = atomicCAS(&hs[h], NONE, id);
+          if (old == NONE) {  // new: a seed (capped)
+            const uint32_t pos = atomicAdd(&nseed_s, 1u);
+            if (pos < NS_SEEDS) seeds[pos] = id;
+            break;
+          }
+          if (old == id) break;  // a repeat
+          h = (h + 1) & (NS_HASH - 1);
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t ns = min(nseed_s, NS_SEEDS);
+    double sbs = -INFINITY;
+    uint32_t sbi = NONE;
+    for (uint32_t s0 = w * 32; s0 < ns; s0 += NW * 32) {
+      const uint32_t id = s0 + lane < ns ? seeds[s0 + lane] : NONE;
+      const double acc = exact_fold(id);
+      topk_insert(sbs, sbi, k, acc, id, id != NONE);
+      if (lane == 0) nfl += (unsigned long long)min(32u, ns - s0) * nch * 32;
+    }
+    publish(sbs, sbi, thr3_s);
+  }
+
+  // -------------------------------------------------------- record stage bound
+  // 32 candidates, lane c <-> candidate c (id NONE = none).  Round it (0-3) reads
+  // stage records it * 8 + grp, 16 B part `part` per lane (code parts 0-2; the terms
+  // part 3 is loaded by the candidate's own lane).  Returns the stage's part bound
+  // A = s_x s_q I + r_x ||q_h|| + m_x r_q (rounded up) and, in `tx`, the norm of the
+  // row after the stage.
+  struct Recs {
+    uint4 r[4];
+    uint4 m;
+  };
+  auto load_recs = [&](uint32_t id, uint32_t stage, Recs& R) {
+    // L2-only loads (ld.global.cg): sector-granular, no L1 line fills
+    R.m = id != NONE ? __ldcg(rec + ((uint64_t)id * Q8_STAGES + stage) * 4 + 3) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const uint32_t idr = __shfl_sync(FULL, id, it * 8 + grp);
+      R.r[it] = (idr != NONE && part < 3) ? __ldcg(rec + ((uint64_t)idr * Q8_STAGES + stage) * 4 + part)
+                                         : make_uint4(0, 0, 0, 0);
+    }
+  };
+  auto stage_bound = [&](const Recs& R, uint32_t stage, float& tx, float& nx) {
+    const int4 qw = part < 3 ? *reinterpret_cast<const int4*>(&q8_s[stage][4 * part])
+                             : make_int4(0, 0, 0, 0);
+    // integer dot products of the 4 rounds' records, then a transposing reduction
+    // over the 4 lanes of a record group: lane grp * 4 + p ends with round p's total
+    int dt[4];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      int t = __dp4a((int)R.r[it].x, qw.x, 0);
+      t = __dp4a((int)R.r[it].y, qw.y, t);
+      t = __dp4a((int)R.r[it].z, qw.z, t);
+      dt[it] = __dp4a((int)R.r[it].w, qw.w, t);
+    }
+    const bool hb = part & 2, lb = part & 1;
+    int d2[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int snd = hb ? dt[j] : dt[j + 2];
+      d2[j] = (hb ? dt[j + 2] : dt[j]) + __shfl_xor_sync(FULL, snd, 2);
+    }
+    const int snd = lb ? d2[0] : d2[1];
+    const int d1 = (lb ? d2[1] : d2[0]) + __shfl_xor_sync(FULL, snd, 1);
+    // candidate c = round (c >> 3), group (c & 7): held by lane (c & 7) * 4 + (c >> 3)
+    const int dot = __shfl_sync(FULL, d1, (lane & 7) * 4 + (lane >> 3));
+    const float qs = qn_s[stage][0], qh = qn_s[stage][1], qr = qn_s[stage][2];
+    const float sx = __uint_as_float(R.m.x), rx = __uint_as_float(R.m.y);
+    const float mxn = __uint_as_float(R.m.z);
+    tx = __uint_as_float(R.m.w);
+    nx = __fadd_ru(mxn, rx);  // >= ||x_h||
+    const float If = (float)dot;  // |I| <= 48 * 127^2: exact in fp32
+    // s_x s_q I rounded up: round the scale product toward the side that raises it
+    const float sp = dot >= 0 ? __fmul_ru(sx, qs) : __fmul_rd(sx, qs);
+    return __fadd_ru(__fmul_ru(sp, If), __fmaf_ru(rx, qh, __fmul_ru(mxn, qr)));
+  };
+  const float qh1 = qn_s[0][1], qt1 = qn_s[0][3], qh2 = qn_s[1][1], qt2 = qn_s[1][3];
+  const float qnorm = __fadd_ru(qh1, qt1);  // >= ||q||
+  auto thr_now = [&] { return dkey_inv(*(volatile unsigned long long*)&thr_key); };
+
+  // stage 2 of 32 stage-1 survivors: bound A1 + A2 + t2 ||q after stage 2||
+  auto stage2_batch = [&](uint32_t cnt) {
+    const uint32_t slot = (h1 + lane) % NS_QCAP;
+    const uint32_t id = (uint32_t)lane < cnt ? s1q[slot] : NONE;
+    const float2 an = (uint32_t)lane < cnt ? s1v[slot] : make_float2(0.f, 0.f);
+    h1 += cnt;
+    Recs R;
+    load_recs(id, 1, R);
+    float tx, nx;
+    const float A2 = stage_bound(R, 1, tx, nx);
+    bool live = false;
+    if (id != NONE) {
+      const float A = __fadd_ru(an.x, A2);
+      const float mag = __fadd_ru(__fadd_ru(fabsf(an.x), fabsf(A2)), an.y);
+      const float ub = __fadd_ru(__fmaf_ru(tx, qt2, A), __fmul_ru(mag, 1e-6f));
+      live = (double)ub >= thr_now();
+    }
+    const uint32_t live_m = __ballot_sync(FULL, live);
+    if (live) sq[(qtail + __popc(live_m & lt_mask)) % NS_QCAP] = id;
+    qtail += __popc(live_m);
+    nst2 += cnt;
+  };
+
+  // ---------------------------------------------------------------- stage 1
+  const uint32_t nb = (Len + 31) / 32;
+  uint32_t cid = NONE;
+  Recs cur;
+  if ((uint32_t)w < nb) {
+    const uint32_t ci = w * 32 + lane;
+    cid = ci < Len ? __ldcs(cand + ci) : NONE;
+    load_recs(cid, 0, cur);
+  }
+  for (uint32_t b = w; b < nb; b += NW) {
+    // full queues are drained before the next batch's loads are issued (the current
+    // batch's loads are in flight meanwhile; fewer live registers)
+    if (qtail - qhead >= 32) {
+      __syncwarp();
+      exact_batch(32);
+    }
+    if (t1 - h1 >= 32) stage2_batch(32);
+    uint32_t nid = NONE;
+    Recs nxt;
+    if (b + NW < nb) {
+      const uint32_t ci = (b + NW) * 32 + lane;
+      nid = ci < Len ? __ldcs(cand + ci) : NONE;
+      load_recs(nid, 0, nxt);
+    }
+    float tx, nx;
+    const float A1 = stage_bound(cur, 0, tx, nx);
+    bool live = false;
+    float N1 = 0.f;
+    if (cid != NONE) {
+      N1 = __fmul_ru(__fadd_ru(nx, tx), qnorm);  // >= ||x|| ||q||
+      const float mag = __fadd_ru(fabsf(A1), N1);
+      const float ub = __fadd_ru(__fmaf_ru(tx, qt1, A1), __fmul_ru(mag, 1e-6f));
+      live = (double)ub >= thr_now();
+    }
+    const uint32_t live_m = __ballot_sync(FULL, live);
+    if (live) {
+      const uint32_t pos = (t1 + __popc(live_m & lt_mask)) % NS_QCAP;
+      s1q[pos] = cid;
+      s1v[pos] = make_float2(A1, N1);
+    }
+    t1 += __popc(live_m);
+    nrows += __popc(__ballot_sync(FULL, cid != NONE));
+    cid = nid;
+    cur = nxt;
+  }
+  while (t1 != h1 || qtail != qhead) {
+    if (t1 != h1 && qtail - qhead < 32) {
+      stage2_batch(min(32u, t1 - h1));
+    } else {
+      __syncwarp();
+      exact_batch(min(32u, qtail - qhead));
+    }
+  }
+  (void)qh2;
+  if (lane == 0) {
+    // bytes read: 64 B stage-1 record per candidate, 64 B stage-2 record per stage-1
+    // survivor, and the exact rows
+    if (a.rbytes) atomicAdd(a.rbytes, (nrows + nst2) * 64ull + nfl * 4ull);
+    if (a.dbg) {  // read fraction in row floats: a record counts as 16 floats
+      atomicAdd(a.dbg, nrows);
+      atomicAdd(a.dbg + 1, (nrows + nst2) * 16ull + nfl);
+    }
+  }
+  // CTA merge of the warp lists
+  mg_s[w][lane] = bs;
+  mg_i[w][lane] = bi;
+  __syncthreads();
+  if (w == 0) {
+    for (int w2 = 1; w2 < NW; ++w2) {
+      const bool valid = (uint32_t)lane < k && mg_i[w2][lane] != NONE;
+      topk_insert(bs, bi, k, mg_s[w2][lane], mg_i[w2][lane], valid);
+    }
+    if ((uint32_t)lane < k) {
+      const bool ok = bi != NONE;
+      a.out_ids[(uint64_t)q * k + lane] = ok ? bi + a.id_offset : NONE;
+      a.out_scores[(uint64_t)q * k + lane] = ok ? bs : -INFINITY;
+    }
+    if (lane == 0 && a.stats) {
+      a.stats[q].probes = a.peff;
+      a.stats[q].entries = a.eq[q];
+      a.stats[q].candidates = a.uq_all ? a.uq_all[q] : Len;
+      a.stats[q].exact = a.uq_all ? a.uq_all[q] : Len;
+    }
+  }
+}
+
+static size_t screen_smem(uint32_t d) {
+  const uint32_t nch = (d + 31) / 32;
+  return (size_t)nch * 32 * 8 + (size_t)NS_W * 32 * NS_PAD * 4 + (size_t)NS_W * NS_QCAP * (4 + 4 + 8) +
+         (size_t)(NS_HASH + NS_SEEDS) * 4;
 }
 
 static size_t score_smem(uint32_t d, int sl, int st) {
@@ -2176,9 +2581,9 @@ static void stage_a(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
 // grouped-dedup geometry for an index of n points: id >> gshift < CO_NG; 0 when the
 // per-warp range bitmaps (32 x 2^gshift bits) would not fit shared memory
 static uint32_t grouped_shift(uint64_t n) {
-  uint32_t gs = 5;
+  uint32_t gs = 10;  // >= 1024-id groups: 128-word per-warp bitmaps at least
   while (gs < 32 && ((n - 1) >> gs) >= CO_NG) ++gs;
-  const size_t sm = (size_t)2 * CO_NG * 4 + (size_t)32 * ((1ull << gs) / 8);
+  const size_t sm = (size_t)CO_NG * 4 + (size_t)32 * ((1ull << gs) / 8);
   return sm + 64 <= (size_t)co_smem_max() ? gs : 0u;
 }
 
@@ -2193,8 +2598,9 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   cudaEvent_t e0;
   cx.timer.begin(PH_COLLECT, st, &e0);
   const uint32_t nwords = (uint32_t)((ix.n + 31) / 32);
+  sl.uniq.ensure(nqc);
   CollectArgs ca{sl.ppos.p, sl.plen.p, peff, ix.ids, sl.coff.p, sl.cands.p, sl.uq.p,
-                 nqc, nwords, nullptr, sl.counter.p, 0, 0};
+                 nqc, nwords, nullptr, sl.counter.p, 0, 0, sl.uniq.p, ix.n};
   // Visited set (every id scored once): an n-bit bitmap in shared memory
   // where it fits one SM (n <= ~1.8 M); beyond that the grouped dedup (id-range
   // counting sort + per-warp range bitmaps; C4's 10 M points); beyond its range an
@@ -2217,10 +2623,11 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * std::max(occ, 1));
     FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
     k_collect<<<co_grid, CO_THREADS, co_smem, st>>>(ca);
-  } else if ((!force || f_grouped) && gshift) {
+  } else if ((!force || f_grouped) && gshift && !rerank) {
+    // (the SimHash screen needs hole-free lists: rerank takes the bitmap paths below)
     ca.grouped = 1;
     ca.gshift = gshift;
-    const size_t co_smem = (size_t)2 * CO_NG * 4 + (size_t)32 * ((1ull << gshift) / 8);
+    const size_t co_smem = (size_t)CO_NG * 4 + (size_t)32 * ((1ull << gshift) / 8);
     FPP_CUDA(cudaFuncSetAttribute(k_collect, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)co_smem));
     int occ = 1;
@@ -2260,7 +2667,9 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   ScoreArgs sa{ix.X, ix.d, ix.ldx, Qd, sl.coff.p, sl.cands.p, sl.uq.p, sl.eq.p, peff, k,
                ix.prm.id_offset, ids_d, scores_d, stats_d, nullptr, 0};
   sa.rbytes = ix.score_bytes_d.p;
+  if (ca.grouped) sa.uq_all = sl.uniq.p;  // lists carry holes: unique counts for the stats
   if (rerank) {  // SimHash screen: at most B candidates per query reach the exact scores
+    sa.uq_all = nullptr;
     sl.qsig.ensure(nqc);
     sl.cands2.ensure((size_t)nqc * rerank);
     sl.uq2.ensure(nqc);
@@ -2313,7 +2722,47 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     use_pruned = force_prune || probe || ix.prune_frac < 0 || ix.prune_frac <= 0.65;
     ++ix.prune_chunks;
   }
-  if (use_pruned) {
+  // narrow rows: the register head screen (k_score_screen) unless FPP_SC_NARROW=0
+  static const bool narrow_off = getenv("FPP_SC_NARROW") && atoi(getenv("FPP_SC_NARROW")) == 0;
+  if (use_pruned && ix.q8rec && !narrow_off && !rerank) {
+    sa.xtail = reinterpret_cast<const float*>(ix.q8rec);
+    sa.n = ix.n;
+    if (probe) {
+      if (!cx.prune_h) {
+        FPP_CUDA(cudaMallocHost(&cx.prune_h, 16));
+        FPP_CUDA(cudaEventCreateWithFlags(&cx.prune_ev, cudaEventDisableTiming));
+        cx.prune_d.alloc(2);
+      }
+      FPP_CUDA(cudaMemsetAsync(cx.prune_d.p, 0, 16, st));
+      sa.dbg = cx.prune_d.p;
+    }
+    // seeds: the true buckets (the first L probes); FPP_SC_SEEDS=0 disables
+    static const bool no_seeds = getenv("FPP_SC_SEEDS") && atoi(getenv("FPP_SC_SEEDS")) == 0;
+    sa.ppos = sl.ppos.p;
+    sa.plen = sl.plen.p;
+    sa.ids = ix.ids;
+    sa.nseedp = no_seeds ? 0u : ix.prm.L;
+    const size_t sm = screen_smem(ix.d);
+    // FPP_SC_SCR_MINB=2: 128-register variant (2 CTAs/SM, no spills); default 3 CTAs/SM
+    static const int scr_minb = getenv("FPP_SC_SCR_MINB") ? atoi(getenv("FPP_SC_SCR_MINB")) : 3;
+    auto launch_scr = [&](auto kern) {
+      FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      kern<<<nqc, NS_W * 32, sm, st>>>(sa);
+    };
+    if (scr_minb == 2) launch_scr(k_score_screen<NS_W, 2>);
+    else launch_scr(k_score_screen<NS_W, 3>);
+    if (probe) {
+      FPP_CUDA(cudaMemcpyAsync(cx.prune_h, cx.prune_d.p, 16, cudaMemcpyDeviceToHost, st));
+      FPP_CUDA(cudaEventRecord(cx.prune_ev, st));
+      cx.prune_pending = true;
+      if (dbg) {
+        FPP_CUDA(cudaEventSynchronize(cx.prune_ev));
+        const unsigned long long* h = cx.prune_h;
+        fprintf(stderr, "[prune dbg] screen: rows %llu, floats read per row %.1f of %u (%.1f%% of row bytes)\n",
+                h[0], h[0] ? (double)h[1] / h[0] : 0.0, ix.d, h[0] ? 100.0 * h[1] / h[0] / ix.d : 0.0);
+      }
+    }
+  } else if (use_pruned) {
     sa.xtail = ix.xtail;
     sa.xt_n = ix.xt_n;
     sa.xt_head = ix.xt_head;
@@ -2593,6 +3042,7 @@ void query_debug(const Index& ix, QueryCtx& cx, const float* qd, uint32_t qprobe
   FPP_CUDA(cudaMemcpy(&off, sl.coff.p, 8, cudaMemcpyDeviceToHost));
   cands.resize(U);
   if (U) FPP_CUDA(cudaMemcpy(cands.data(), sl.cands.p + off, (size_t)U * 4, cudaMemcpyDeviceToHost));
+  cands.erase(std::remove(cands.begin(), cands.end(), 0xffffffffu), cands.end());  // grouped holes
   std::sort(probes.begin(), probes.end());
   std::sort(cands.begin(), cands.end());
 }

@@ -188,6 +188,7 @@ def test_score_geometry_324_exact(fpp, orc, d, k, xt_n, monkeypatch):
     of 3 and with extra tail-norm checkpoints."""
     monkeypatch.setenv("FPP_XT_N", xt_n)
     monkeypatch.setenv("FPP_SC_PR", "324")
+    monkeypatch.setenv("FPP_SC_NARROW", "0")  # the ring kernel, not the register screen
     X = data(fpp, 20000, d, 200, 0.25, seed=31)
     Q = data(fpp, 300, d, 200, 0.25, seed=31, stream=1)
     ix = fpp.Index.build(X, L=16, K=2, D=128 if d <= 128 else 256, iProbes=3, alpha=0.2)
@@ -202,6 +203,44 @@ def test_score_geometry_324_exact(fpp, orc, d, k, xt_n, monkeypatch):
     assert np.array_equal(gi, oi) and np.array_equal(gst, ost)
     ok = np.isfinite(os_)
     assert np.array_equal(gs[ok], os_[ok])
+
+
+# ------------------------------------------- narrow rows: register head screen
+@pytest.mark.parametrize("d", [64, 100, 128, 192, 256])
+@pytest.mark.parametrize("k", [20, 7, 1])
+@pytest.mark.parametrize("seeds", ["1", "0"])
+def test_score_screen_exact(fpp, orc, d, k, seeds, monkeypatch):
+    """k_score_screen (two-stage int8 record screen with a rigorous bound, exact fp64
+    sequential finish for survivors, optional true-bucket seeds for the threshold)
+    returns exactly k_score's / the oracle's answers
+    and stats, with clustered data (most candidates pruned), duplicate rows (ties to
+    the lower id) and the grouped collect's holes."""
+    monkeypatch.setenv("FPP_SC_SEEDS", seeds)  # true-bucket seeds raise the threshold first
+    X = data(fpp, 20000, d, 150, 0.25, seed=33)
+    X[7000:7004] = X[11]  # exact duplicates inside the candidate sets
+    Q = data(fpp, 257, d, 150, 0.25, seed=33, stream=1)
+    Q[3] = X[11]
+    D = min(128 if d <= 128 else 256, orc.lib().orc_pad_dimension(d))
+    ix = fpp.Index.build(X, L=14, K=2, D=D, iProbes=3, alpha=0.2)
+    ox = orc.Index(X, L=14, K=2, D=D, iprobes=3, alpha=0.2)
+    oi, os_, ost = ox.query(Q, k, 6000)
+    ok = np.isfinite(os_)
+    for path in ("smem", "grouped"):
+        if path == "grouped":
+            monkeypatch.setenv("FPP_FORCE_COLLECT", "grouped")
+        monkeypatch.setenv("FPP_PRUNE", "1")
+        monkeypatch.setenv("FPP_DEBUG_PRUNE", "1")
+        gi, gs, gst = ix.query(Q, k, 6000, return_stats=True)
+        monkeypatch.delenv("FPP_PRUNE")
+        monkeypatch.delenv("FPP_DEBUG_PRUNE")
+        monkeypatch.setenv("FPP_NO_PRUNE", "1")
+        fi, fs, fst = ix.query(Q, k, 6000, return_stats=True)
+        monkeypatch.delenv("FPP_NO_PRUNE")
+        assert np.array_equal(gi, fi) and np.array_equal(gs, fs) and np.array_equal(gst, fst), path
+        assert np.array_equal(gi, oi) and np.array_equal(gst, ost), path
+        assert np.array_equal(gs[ok], os_[ok]), path
+    if k >= 5:
+        assert list(gi[3][:5]) == [11, 7000, 7001, 7002, 7003]
 
 
 # ------------------------------------------------ SPEC acceptance #6 and #8 (desk)
