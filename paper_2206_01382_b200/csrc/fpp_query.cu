@@ -2061,7 +2061,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
 // lists may carry holes (0xFFFFFFFF): skipped.
 constexpr int NS_W = 8;            // warps per CTA
 constexpr uint32_t NS_QCAP = 64;   // survivor queue per warp (<= 31 + 32 queued)
-constexpr int NS_PAD = 36;         // staging row stride in floats
+constexpr int NS_PAD = 20;         // exact staging: 16-float half chunks, row stride 20 floats
+constexpr int NS_RING = 4;         // stage-1 record ring depth per warp (cp.async)
 constexpr uint32_t NS_HASH_BITS = 11, NS_HASH = 1u << NS_HASH_BITS;  // seed dedup table
 constexpr uint32_t NS_SEEDS = 1024;  // seeds kept (hash load <= 1/2)
 
@@ -2080,7 +2081,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   constexpr uint32_t NONE = 0xffffffffu;
   const uint32_t d = a.d, nch = (d + 31) / 32;  // 32-float chunks (rows padded with zeros)
   double* qd = reinterpret_cast<double*>(smraw);                       // [32 * nch]
-  float* stg_all = reinterpret_cast<float*>(smraw + (size_t)nch * 32 * 8);  // [NW][32][NS_PAD]
+  uint4* ring_all = reinterpret_cast<uint4*>(smraw + (size_t)nch * 32 * 8);  // [NW][RING][32][4]
+  uint32_t* rid_all = reinterpret_cast<uint32_t*>(ring_all + (size_t)NW * NS_RING * 128);  // [NW][RING][32]
+  float* stg_all = reinterpret_cast<float*>(rid_all + (size_t)NW * NS_RING * 32);  // [NW][32][NS_PAD]
   uint32_t* sq_all = reinterpret_cast<uint32_t*>(stg_all + (size_t)NW * 32 * NS_PAD);  // [NW][QCAP]
   uint32_t* s1_all = sq_all + (size_t)NW * NS_QCAP;                    // [NW][QCAP] stage-2 queue ids
   float2* s1v_all = reinterpret_cast<float2*>(s1_all + (size_t)NW * NS_QCAP);  // [NW][QCAP] (A1, N1)
@@ -2096,6 +2099,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   const int part = lane & 3, grp = lane >> 2;  // record part (0-2 codes, 3 terms), record slot
   const uint32_t lt_mask = (1u << lane) - 1u;
   float* stg = stg_all + (size_t)w * 32 * NS_PAD;
+  uint4* ring = ring_all + (size_t)w * NS_RING * 128;
+  uint32_t* rid = rid_all + (size_t)w * NS_RING * 32;
   uint32_t* sq = sq_all + (size_t)w * NS_QCAP;    // survivors of stage 2 -> exact
   uint32_t* s1q = s1_all + (size_t)w * NS_QCAP;   // survivors of stage 1 -> stage 2
   float2* s1v = s1v_all + (size_t)w * NS_QCAP;
@@ -2147,37 +2152,34 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   // ---------------------------------------------------------------- exact rows
   // lane r folds row `id` of lane r (NONE: nothing) in the reference's order
   auto exact_fold = [&](uint32_t id) {
-    // each chunk moves in two halves of 16 rows (4 loads per lane: fewer live
-    // registers); the next chunk's first half is in flight while this one is folded
+    // 16-float half chunks of the 32 rows: 4 lanes per row (16 B each), 8 rows per
+    // load instruction, staged in shared memory (row stride 20 floats); the next half
+    // chunk is in flight while lane r folds row r's 16 floats
     float4 v[4];
-    const int c8 = lane & 7, g4 = lane >> 3;
-    auto load_half = [&](uint32_t ch, int h) {
+    const int p4 = lane & 3, r8 = lane >> 2;
+    const uint32_t nh = nch * 2;
+    auto load_h = [&](uint32_t hc) {
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
-        const uint32_t idr = __shfl_sync(FULL, id, (h * 4 + it) * 4 + g4);
-        v[it] = idr != NONE ? __ldcg(reinterpret_cast<const float4*>(X + (uint64_t)idr * ldx + ch * 32) + c8)
+        const uint32_t idr = __shfl_sync(FULL, id, it * 8 + r8);
+        v[it] = idr != NONE ? __ldcg(reinterpret_cast<const float4*>(X + (uint64_t)idr * ldx + hc * 16) + p4)
                             : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     };
-    auto store_half = [&](int h) {
+    load_h(0);
+    double acc = 0.0;
+    for (uint32_t hc = 0; hc < nh; ++hc) {
+      __syncwarp();  // the previous half chunk's readers are done with the staging rows
 #pragma unroll
       for (int it = 0; it < 4; ++it)
-        *reinterpret_cast<float4*>(stg + ((h * 4 + it) * 4 + g4) * NS_PAD + 4 * c8) = v[it];
-    };
-    load_half(0, 0);
-    double acc = 0.0;
-    for (uint32_t ch = 0; ch < nch; ++ch) {
-      __syncwarp();  // the previous chunk's readers are done with the staging rows
-      store_half(0);
-      load_half(ch, 1);
-      store_half(1);
-      if (ch + 1 < nch) load_half(ch + 1, 0);
+        *reinterpret_cast<float4*>(stg + (it * 8 + r8) * NS_PAD + 4 * p4) = v[it];
+      if (hc + 1 < nh) load_h(hc + 1);
       __syncwarp();
       const float* row = stg + lane * NS_PAD;
-      const double* qq = qd + ch * 32;
+      const double* qq = qd + hc * 16;
       // dataset.cpp:67 acc += double(a[i]) * double(b[i]), sequential i (exact products)
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
+      for (int j = 0; j < 16; j += 4) {
         const float4 xv = *reinterpret_cast<const float4*>(row + j);
         acc = fma((double)xv.x, qq[j], acc);
         acc = fma((double)xv.y, qq[j + 1], acc);
@@ -2221,8 +2223,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   // (their own family of disjoint lists); the scan below then starts near the final
   // k-th best instead of at -inf.  Seeds are scanned again like any candidate.
   if (a.nseedp) {
-    uint32_t* hs = reinterpret_cast<uint32_t*>(s1v_all + (size_t)NW * NS_QCAP);  // [NS_HASH]
-    uint32_t* seeds = hs + NS_HASH;                                               // [NS_SEEDS]
+    uint32_t* hs = reinterpret_cast<uint32_t*>(ring_all);  // [NS_HASH] (the ring: free until the scan)
+    uint32_t* seeds = hs + NS_HASH;                       // [NS_SEEDS]
     for (uint32_t i = threadIdx.x; i < NS_HASH; i += blockDim.x) hs[i] = NONE;
     if (threadIdx.x == 0) nseed_s = 0;
     __syncthreads();
@@ -2257,6 +2259,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       if (lane == 0) nfl += (unsigned long long)min(32u, ns - s0) * nch * 32;
     }
     publish(sbs, sbi, thr3_s);
+    __syncthreads();  // the ring is the records' from here on
   }
 
   // -------------------------------------------------------- record stage bound
@@ -2341,29 +2344,49 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   };
 
   // ---------------------------------------------------------------- stage 1
+  // A per-warp ring of NS_RING batches: the 32 stage-1 records of batch i + RING - 1
+  // move by cp.async (16 B per lane, four per lane) while batch i is bounded, so
+  // RING - 1 batches (6 KB) per warp are in flight without holding registers; the
+  // ids of the batch after that are loaded one iteration early.
   const uint32_t nb = (Len + 31) / 32;
-  uint32_t cid = NONE;
-  Recs cur;
-  if ((uint32_t)w < nb) {
-    const uint32_t ci = w * 32 + lane;
-    cid = ci < Len ? __ldcs(cand + ci) : NONE;
-    load_recs(cid, 0, cur);
-  }
-  for (uint32_t b = w; b < nb; b += NW) {
-    // full queues are drained before the next batch's loads are issued (the current
-    // batch's loads are in flight meanwhile; fewer live registers)
+  const uint32_t nbw = nb > (uint32_t)w ? (nb - w + NW - 1) / NW : 0;  // this warp's batches
+  auto batch_ids = [&](uint32_t i) {  // lane c: candidate c of the warp's i-th batch
+    const uint32_t ci = (w + i * NW) * 32 + lane;
+    return (i < nbw && ci < Len) ? __ldcs(cand + ci) : NONE;
+  };
+  auto issue = [&](uint32_t i, uint32_t id) {  // records of the warp's i-th batch -> slot
+    const uint32_t slot = i % NS_RING;
+    rid[slot * 32 + lane] = id;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const uint32_t r = it * 8 + grp;
+      const uint32_t idr = __shfl_sync(FULL, id, r);
+      if (idr != NONE)
+        cp_async16(ring + (slot * 32 + r) * 4 + part, rec + ((uint64_t)idr * Q8_STAGES) * 4 + part);
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (uint32_t i = 0; i < NS_RING - 1; ++i) issue(i, batch_ids(i));
+  uint32_t nid = batch_ids(NS_RING - 1);
+  for (uint32_t i = 0; i < nbw; ++i) {
+    // full queues are drained first (their own loads; the ring stays in flight)
     if (qtail - qhead >= 32) {
       __syncwarp();
       exact_batch(32);
     }
     if (t1 - h1 >= 32) stage2_batch(32);
-    uint32_t nid = NONE;
-    Recs nxt;
-    if (b + NW < nb) {
-      const uint32_t ci = (b + NW) * 32 + lane;
-      nid = ci < Len ? __ldcs(cand + ci) : NONE;
-      load_recs(nid, 0, nxt);
-    }
+    issue(i + NS_RING - 1, nid);   // (an empty commit past the end keeps the count)
+    nid = batch_ids(i + NS_RING);
+    cp_wait<NS_RING - 1>();
+    __syncwarp();
+    const uint32_t slot = i % NS_RING;
+    const uint32_t cid = rid[slot * 32 + lane];
+    Recs cur;
+#pragma unroll
+    for (int it = 0; it < 4; ++it)
+      cur.r[it] = part < 3 ? ring[(slot * 32 + it * 8 + grp) * 4 + part] : make_uint4(0, 0, 0, 0);
+    cur.m = ring[(slot * 32 + lane) * 4 + 3];
     float tx, nx;
     const float A1 = stage_bound(cur, 0, tx, nx);
     bool live = false;
@@ -2382,9 +2405,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     }
     t1 += __popc(live_m);
     nrows += __popc(__ballot_sync(FULL, cid != NONE));
-    cid = nid;
-    cur = nxt;
+    __syncwarp();  // slot i % RING is refilled by the next iteration's issue
   }
+  cp_wait<0>();
   while (t1 != h1 || qtail != qhead) {
     if (t1 != h1 && qtail - qhead < 32) {
       stage2_batch(min(32u, t1 - h1));
@@ -2428,8 +2451,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
 
 static size_t screen_smem(uint32_t d) {
   const uint32_t nch = (d + 31) / 32;
-  return (size_t)nch * 32 * 8 + (size_t)NS_W * 32 * NS_PAD * 4 + (size_t)NS_W * NS_QCAP * (4 + 4 + 8) +
-         (size_t)(NS_HASH + NS_SEEDS) * 4;
+  static_assert((size_t)NS_W * NS_RING * 128 * 16 >= (size_t)(NS_HASH + NS_SEEDS) * 4,
+                "the seed table lives in the record ring");
+  return (size_t)nch * 32 * 8 + (size_t)NS_W * NS_RING * (128 * 16 + 32 * 4) +
+         (size_t)NS_W * 32 * NS_PAD * 4 + (size_t)NS_W * NS_QCAP * (4 + 4 + 8);
 }
 
 static size_t score_smem(uint32_t d, int sl, int st) {
@@ -2743,8 +2768,8 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     sa.ids = ix.ids;
     sa.nseedp = no_seeds ? 0u : ix.prm.L;
     const size_t sm = screen_smem(ix.d);
-    // FPP_SC_SCR_MINB=2: 128-register variant (2 CTAs/SM, no spills); default 3 CTAs/SM
-    static const int scr_minb = getenv("FPP_SC_SCR_MINB") ? atoi(getenv("FPP_SC_SCR_MINB")) : 3;
+    // 2 CTAs/SM (shared memory: the record rings); FPP_SC_SCR_MINB=3 caps registers at 80
+    static const int scr_minb = getenv("FPP_SC_SCR_MINB") ? atoi(getenv("FPP_SC_SCR_MINB")) : 2;
     auto launch_scr = [&](auto kern) {
       FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       kern<<<nqc, NS_W * 32, sm, st>>>(sa);
