@@ -338,7 +338,9 @@ __global__ void k_q8_records(const float* __restrict__ X, uint64_t n, uint32_t d
         tt += __shfl_xor_sync(0xffffffffu, tt, o);
       }
       // byte b of the stage record = code of dim lo + b (lanes: b = lane, lane + 32 < 48)
-      unsigned char* rb = reinterpret_cast<unsigned char*>(rec + (i * Q8_STAGES + stage) * 4);
+      // stage tables are separate ([stage][n] records): a stage-1 read never drags the
+      // stage-2 record of the row into L2
+      unsigned char* rb = reinterpret_cast<unsigned char*>(rec + ((uint64_t)stage * n + i) * 4);
       rb[lane] = (unsigned char)(signed char)c0;
       if (lane < 16) rb[lane + 32] = (unsigned char)(signed char)c1;
       if (lane == 0) {
@@ -354,6 +356,8 @@ __global__ void k_q8_records(const float* __restrict__ X, uint64_t n, uint32_t d
 }
 
 void launch_tail_norms(Index& ix) {
+  // FPP_L2_FETCH=32|64|128: cudaLimitMaxL2FetchGranularity hint (experiments)
+  if (getenv("FPP_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(getenv("FPP_L2_FETCH")));
   if (ix.d >= 64 && ix.d <= 256 && ix.d % 4 == 0) {  // k_score_screen's records
     ix.q8rec = static_cast<uint4*>(dmalloc((size_t)ix.n * 64 * Q8_STAGES));
     k_q8_records<<<sm_count() * 8, 256, 0, ix.stream>>>(ix.X, ix.n, ix.d, ix.ldx, ix.q8rec);

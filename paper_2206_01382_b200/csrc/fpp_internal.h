@@ -208,7 +208,7 @@ void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint32_t ld
 // k_score_screen record: int8 codes of dims [0, Q8_DIMS) (48 B) + {scale, ||x_h - x~_h||,
 // ||x~_h||, ||x[Q8_DIMS:d)||} as fp32 rounded up (16 B) = 64 B per row
 constexpr uint32_t Q8_DIMS = 48;
-constexpr uint32_t Q8_STAGES = 2;  // records per row: dims [0,48) and [48,96), 128 B per row
+constexpr uint32_t Q8_STAGES = 2;  // record tables [stage][n]: dims [0,48) and [48,96)
 constexpr uint32_t XT_SLICE = 64;  // = the score ring's row-slice width for d >= 64
 constexpr uint32_t XT_MAX = 4;     // tail-norm checkpoints per row
 // score-gather slices of a d-wide row: a head [0, h) (h = Index::xt_head, 32 or 64),

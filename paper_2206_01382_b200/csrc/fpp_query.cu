@@ -1094,8 +1094,9 @@ __device__ __forceinline__ void collect_grouped(const CollectArgs& a, uint32_t q
   for (uint32_t i = threadIdx.x; i < CO_NG; i += blockDim.x) cnt[i] = 0;
   if (threadIdx.x == 0) dups_sh = 0;
   __syncthreads();
+  const uint32_t cnt_base = (uint32_t)__cvta_generic_to_shared(cnt);
   collect_walk(pp, pl, P, a.ids, out, ucount, next_chunk, [&](uint32_t id) {
-    smem_inc(&cnt[id >> gs]);
+    asm volatile("red.shared.add.u32 [%0], 1;\n" ::"r"(cnt_base + ((id >> gs) << 2)) : "memory");
     return false;
   });
   __syncthreads();
@@ -1107,8 +1108,12 @@ __device__ __forceinline__ void collect_grouped(const CollectArgs& a, uint32_t q
     if (threadIdx.x == 0) *nextc = 0;
   }
   __syncthreads();
+  // walk 2 (a second probe decode measured faster than re-streaming a walk-order
+  // copy: 93 vs 102 ms per C4 step): scatter into the groups
   collect_walk(pp, pl, P, a.ids, out, ucount, next_chunk, [&](uint32_t id) {
-    out[smem_fetch_add(&cnt[id >> gs], 1u)] = id;
+    uint32_t pos;
+    asm volatile("atom.shared.add.u32 %0, [%1], 1;\n" : "=r"(pos) : "r"(cnt_base + ((id >> gs) << 2)) : "memory");
+    out[pos] = id;
     return false;
   });
   __syncthreads();  // cnt[g] is now the end of group g (= the start of group g + 1)
@@ -1117,12 +1122,13 @@ __device__ __forceinline__ void collect_grouped(const CollectArgs& a, uint32_t q
   const uint32_t gstep = blockDim.x >> 5;
   const uint32_t ng = (uint32_t)((a.n - 1) >> gs) + 1;  // groups in use
   uint32_t dups = 0;
+  const uint32_t bm_base = (uint32_t)__cvta_generic_to_shared(bm);
   auto tas = [&](uint32_t id) {  // test-and-set in the range bitmap: true = a repeat
     const uint32_t b = id & mask, bit = 1u << (b & 31);
     uint32_t old;
     asm volatile("atom.shared.or.b32 %0, [%1], %2;\n"
                  : "=r"(old)
-                 : "r"((uint32_t)__cvta_generic_to_shared(bm + (b >> 5))), "r"(bit)
+                 : "r"(bm_base + ((b >> 5) << 2)), "r"(bit)
                  : "memory");
     return (old & bit) != 0u;
   };
@@ -2274,11 +2280,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   };
   auto load_recs = [&](uint32_t id, uint32_t stage, Recs& R) {
     // L2-only loads (ld.global.cg): sector-granular, no L1 line fills
-    R.m = id != NONE ? __ldcg(rec + ((uint64_t)id * Q8_STAGES + stage) * 4 + 3) : make_uint4(0, 0, 0, 0);
+    const uint4* rs = rec + (uint64_t)stage * a.n * 4;  // this stage's table
+    R.m = id != NONE ? __ldcg(rs + (uint64_t)id * 4 + 3) : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const uint32_t idr = __shfl_sync(FULL, id, it * 8 + grp);
-      R.r[it] = (idr != NONE && part < 3) ? __ldcg(rec + ((uint64_t)idr * Q8_STAGES + stage) * 4 + part)
+      R.r[it] = (idr != NONE && part < 3) ? __ldcg(rs + (uint64_t)idr * 4 + part)
                                          : make_uint4(0, 0, 0, 0);
     }
   };
@@ -2362,7 +2369,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       const uint32_t r = it * 8 + grp;
       const uint32_t idr = __shfl_sync(FULL, id, r);
       if (idr != NONE)
-        cp_async16(ring + (slot * 32 + r) * 4 + part, rec + ((uint64_t)idr * Q8_STAGES) * 4 + part);
+        cp_async16(ring + (slot * 32 + r) * 4 + part, rec + (uint64_t)idr * 4 + part);
     }
     cp_commit();
   };
@@ -2885,7 +2892,14 @@ static void run_query_core(const Index& ix, QueryCtx& cx, const float* Qd, uint6
                            fpp_query_stats* stats_d, cudaStream_t s, uint32_t rerank) {
   const uint32_t cs = chunk_size(ix, qprobes, nq);
   const uint64_t nch = (nq + cs - 1) / cs;
-  static const bool serial = getenv("FPP_SERIAL") != nullptr;
+  // Stage order: the two-stream pipeline pays where stage A is a large share (C2:
+  // 19.6 vs 20.2 ms per step); the narrow-row screen kernel (rows with screening
+  // records, C4) is L2-latency bound and loses to the overlapped stage A (327 vs 323
+  // ms), so those indexes run the stages in stream order.  FPP_PIPELINE=0/1 forces
+  // either (FPP_SERIAL=1 = serial).
+  static const char* pe = getenv("FPP_PIPELINE");
+  const bool serial = getenv("FPP_SERIAL") != nullptr ||
+                      (pe ? atoi(pe) == 0 : ix.q8rec != nullptr);
   if (serial) {  // single-stream order (per-kernel timing without overlap)
     for (uint64_t c = 0; c < nch; ++c) {
       const uint64_t q0 = c * cs;
