@@ -28,8 +28,9 @@
 extern "C" {
 #endif
 
-#define FPP_ABI_VERSION 4  /* 2: fpp_query_stats.exact, SimHash rerank; 3: fpp_timings.score_bytes;
-                              4: fpp_synth_rows, fpp_merge_topk, per-call query contexts */
+#define FPP_ABI_VERSION 5  /* 2: fpp_query_stats.exact, SimHash rerank; 3: fpp_timings.score_bytes;
+                              4: fpp_synth_rows, fpp_merge_topk, per-call query contexts;
+                              5: fpp_timings.score_launches */
 
 /* error classes ("one exit code per error class") */
 #define FPP_OK 0
@@ -88,6 +89,7 @@ typedef struct fpp_timings {
   uint64_t probes;    /* probes */
   uint64_t score_bytes; /* candidate-row bytes the score kernel read (early termination
                            reads only row prefixes of candidates that cannot reach the top-k) */
+  uint64_t score_launches; /* launches of the score kernel (one per query chunk) */
 } fpp_timings;
 
 typedef struct fpp_index fpp_index;

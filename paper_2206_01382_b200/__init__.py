@@ -30,7 +30,7 @@ LIB_PATH = _build.LIB
 
 FPP_OK = 0
 MODES = {"falconnpp": 0, "falconn_baseline": 1}
-ABI_VERSION = 4  # include/falconnpp.h FPP_ABI_VERSION this binding was written against
+ABI_VERSION = 5  # include/falconnpp.h FPP_ABI_VERSION this binding was written against
 ERRORS = {1: "INVALID_ARGUMENT", 2: "EMPTY_DATASET", 3: "DIMENSION", 4: "OUT_OF_RANGE",
           5: "NON_FINITE", 6: "ZERO_NORM", 7: "CUDA", 8: "OUT_OF_MEMORY", 9: "UNSUPPORTED",
           10: "FORMAT", 11: "IO"}
@@ -106,7 +106,8 @@ class Timings(C.Structure):
     _fields_ = [("hash_ms", C.c_double), ("sort_ms", C.c_double), ("qhash_ms", C.c_double),
                 ("probe_ms", C.c_double), ("collect_ms", C.c_double), ("score_ms", C.c_double),
                 ("launches", C.c_uint64), ("score_rows", C.c_uint64), ("entries", C.c_uint64),
-                ("probes", C.c_uint64), ("score_bytes", C.c_uint64)]
+                ("probes", C.c_uint64), ("score_bytes", C.c_uint64),
+                ("score_launches", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -107,7 +107,7 @@ void QueryCtx::QSlot::release() {
   vals.release(); codes.release(); ppos.release(); plen.release(); gbuf.release();
   ckey.release(); cpair.release(); dbgclk.release(); eq.release(); coff.release();
   uq.release(); uniq.release(); cands.release(); bitmap.release(); counter.release();
-  qsig.release(); cands2.release(); uq2.release();
+  qsig.release(); cands2.release(); uq2.release(); wlog.release();
   if (pinned) cudaFreeHost(pinned);
   if (ev_probe) cudaEventDestroy(ev_probe);
   if (ev_bdone) cudaEventDestroy(ev_bdone);
@@ -182,6 +182,7 @@ void collect_query_timings(const Index& ix) {
     ix.acc.score_ms += ms[PH_SCORE];
     ix.acc.launches += c->acc.launches;
     ix.acc.probes += c->acc.probes;
+    ix.acc.score_launches += c->acc.score_launches;
     c->acc = fpp_timings{};
   }
 }

@@ -1457,6 +1457,13 @@ struct ScoreArgs {
   const uint32_t* plen;
   const uint32_t* ids;
   uint32_t nseedp;
+  // k_score_screen<WALK>: the kernel walks the probes itself (no candidate lists);
+  // exact-score dedup through a per-CTA visited bitmap [gridDim.x][nwords] that is
+  // left clear (cleared through the per-CTA log of set ids, [gridDim.x][logcap])
+  uint32_t* gbm;
+  uint32_t nwords;
+  uint32_t* wlog;
+  uint32_t logcap;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -2081,7 +2088,22 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
   return __longlong_as_double((long long)b);
 }
 
-template <int NW, int MINB>
+// WALK = true (large shards without stats): the kernel walks the query's probes
+// itself -- no collect pass and no candidate lists.  Warps take 32-probe chunks in
+// rank order from a CTA counter and cover each chunk's entries 32 at a time (the
+// warp-cooperative walk of k_collect: coalesced id loads, one window ahead of the
+// record ring).  Entries repeat across tables (C4: 1.08 walked per unique id); a
+// repeat is screened again, but every id is scored exactly at most once
+// (SPEC.md:352): the exact stage admits an id only after a test-and-set in the
+// CTA's visited bitmap (global memory, n bits, L2 atomics on the few stage-2
+// survivors), whose set bits are logged and cleared at the end of the query.  The
+// seeds (all entries of the leading true buckets, up to WK_SEEDCAP) are scored
+// exactly straight into the warps' lists through the same bitmap, and the walk
+// starts after them.  Persistent CTAs fetch queries from a counter (one bitmap
+// each).
+constexpr uint32_t WK_SEEDCAP = 2048;  // seed entries per query (whole leading true buckets)
+
+template <int NW, int MINB, bool WALK>
 __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr uint32_t NONE = 0xffffffffu;
@@ -2101,6 +2123,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   __shared__ __align__(16) int32_t q8_s[Q8_STAGES][Q8_DIMS / 4];  // the query's stage codes
   __shared__ double mg_s[NW][32];
   __shared__ uint32_t mg_i[NW][32];
+  __shared__ uint32_t q_s, wctr_s[2], logn_s;  // WALK: query, chunk counters, log length
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int part = lane & 3, grp = lane >> 2;  // record part (0-2 codes, 3 terms), record slot
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -2110,7 +2133,27 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   uint32_t* sq = sq_all + (size_t)w * NS_QCAP;    // survivors of stage 2 -> exact
   uint32_t* s1q = s1_all + (size_t)w * NS_QCAP;   // survivors of stage 1 -> stage 2
   float2* s1v = s1v_all + (size_t)w * NS_QCAP;
-  const uint32_t q = blockIdx.x;
+  uint32_t* const bm = WALK ? a.gbm + (size_t)blockIdx.x * a.nwords : nullptr;
+  uint32_t* const wlog = WALK ? a.wlog + (size_t)blockIdx.x * a.logcap : nullptr;
+  const uint4* rec = reinterpret_cast<const uint4*>(a.xtail);  // [stages][n][4] 16 B parts
+  const float* X = a.X;
+  const uint32_t ldx = a.ldx;
+  const uint32_t k = a.k;
+  for (uint32_t qi = 0;; ++qi) {
+  uint32_t q;
+  if constexpr (WALK) {
+    if (threadIdx.x == 0) {
+      q_s = atomicAdd(a.qctr, 1u);
+      wctr_s[0] = wctr_s[1] = 0;
+      logn_s = 0;
+    }
+    __syncthreads();
+    q = q_s;
+    if (q >= a.nq) break;
+  } else {
+    if (qi) break;
+    q = blockIdx.x;
+  }
   const float* Qr = a.Q + (uint64_t)q * d;
   for (uint32_t j = threadIdx.x; j < nch * 32; j += blockDim.x) qd[j] = j < d ? (double)Qr[j] : 0.0;
   if (threadIdx.x == 0) thr_key = dkey(-INFINITY);
@@ -2144,12 +2187,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     }
   }
   __syncthreads();
-  const uint32_t Len = a.uq[q];
-  const uint32_t* cand = a.cands + a.coff[q];
-  const uint32_t k = a.k;
-  const uint4* rec = reinterpret_cast<const uint4*>(a.xtail);  // [n][stages][4] 16 B parts
-  const float* X = a.X;
-  const uint32_t ldx = a.ldx;
+  const uint32_t Len = WALK ? 0u : a.uq[q];
+  const uint32_t* cand = WALK ? nullptr : a.cands + a.coff[q];
   double bs = -INFINITY;
   uint32_t bi = NONE;
   uint32_t qhead = 0, qtail = 0, h1 = 0, t1 = 0;  // exact queue, stage-2 queue
@@ -2221,21 +2260,158 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     if (lane == 0) nfl += (unsigned long long)cnt * nch * 32;
     publish(bs, bi, thr2_s);
   };
+  // WALK: test-and-set `id` (lanes with `want`) in the CTA's visited bitmap; true for
+  // an id not scored exactly before in this query (logged for the clear)
+  auto admit = [&](uint32_t id, bool want) {
+    bool fresh = false;
+    if (WALK && want) {
+      const uint32_t bit = 1u << (id & 31);
+      fresh = !(atomicOr(bm + (id >> 5), bit) & bit);
+    }
+    if (WALK) {
+      const uint32_t bal = __ballot_sync(FULL, fresh);
+      if (bal) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&logn_s, (uint32_t)__popc(bal));
+        base = __shfl_sync(FULL, base, 0) + __popc(bal & lt_mask);
+        if (fresh && base < a.logcap) wlog[base] = id;
+      }
+    }
+    return fresh;
+  };
+  // sq push of the lanes with `live` (ids), ballot-compacted
+  auto push_exact = [&](uint32_t id, bool live) {
+    const uint32_t live_m = __ballot_sync(FULL, live);
+    if (live) sq[(qtail + __popc(live_m & lt_mask)) % NS_QCAP] = id;
+    qtail += __popc(live_m);
+  };
+
+  // ----------------------------------------------------------- probe walker (WALK)
+  // Warp-cooperative walk over probes [wk_p0, wk_p1): 32-probe chunks from a CTA
+  // counter (the next chunk's (pos, len) loads in flight while the current one is
+  // walked); wk_next() returns lane l's id of the next 32-entry window (NONE past a
+  // chunk's end) and sets wk_done, with NONE, once the range is exhausted.
+  const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
+  const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
+  uint32_t wk_p0 = 0, wk_p1 = 0, wk_T = 0, wk_e0 = 0, wk_nc = 0, wk_cex = 0, wk_plo = 0, wk_phi = 0;
+  uint32_t wk_nlen = 0, nprod = 0;
+  uint64_t wk_npos = 0;
+  bool wk_nhas = false, wk_done = true;
+  uint32_t* wk_ctr = nullptr;
+  auto wk_fetch = [&] {
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(wk_ctr, 1u);
+    c = __shfl_sync(FULL, c, 0);
+    const uint32_t p = wk_p0 + c * 32 + lane;
+    wk_nhas = wk_p0 + c * 32 < wk_p1;
+    wk_nlen = 0;
+    wk_npos = 0;
+    if (p < wk_p1) {
+      wk_nlen = pl[p];
+      wk_npos = pp[p];
+    }
+  };
+  auto wk_begin = [&](uint32_t p0, uint32_t p1, uint32_t* ctr) {
+    wk_p0 = p0;
+    wk_p1 = p1;
+    wk_ctr = ctr;
+    wk_T = wk_e0 = 0;
+    wk_done = false;
+    nprod = 0;
+    wk_fetch();
+  };
+  auto wk_next = [&]() -> uint32_t {
+    while (wk_e0 >= wk_T) {
+      if (!wk_nhas) {
+        wk_done = true;
+        return NONE;
+      }
+      const uint32_t len = wk_nlen;
+      const uint64_t pos = wk_npos;
+      wk_fetch();
+      uint32_t incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      wk_T = __shfl_sync(FULL, incl, 31);
+      const uint32_t ne = __ballot_sync(FULL, len > 0);
+      wk_nc = __popc(ne);
+      const uint32_t src = (uint32_t)lane < wk_nc ? __fns(ne, 0, lane + 1) : 0u;
+      wk_cex = __shfl_sync(FULL, incl - len, src);
+      wk_plo = __shfl_sync(FULL, (uint32_t)pos, src);
+      wk_phi = __shfl_sync(FULL, (uint32_t)(pos >> 32), src);
+      wk_e0 = 0;
+    }
+    const uint32_t E0 = wk_e0, e = E0 + lane;
+    const bool cval = (uint32_t)lane < wk_nc;
+    const uint32_t r0 = __popc(__ballot_sync(FULL, cval && wk_cex <= E0)) - 1u;
+    const uint32_t dd = wk_cex - E0;
+    const uint32_t sm = __reduce_or_sync(FULL, (cval && wk_cex > E0 && dd < 32u) ? (1u << dd) : 0u);
+    const uint32_t r = r0 + __popc(sm & ((2u << lane) - 1u));
+    const uint32_t plo = __shfl_sync(FULL, wk_plo, r);
+    const uint32_t phi = __shfl_sync(FULL, wk_phi, r);
+    const uint32_t ex = __shfl_sync(FULL, wk_cex, r);
+    wk_e0 += 32;
+    ++nprod;
+    return e < wk_T ? __ldg(a.ids + ((((uint64_t)phi << 32) | plo) + (e - ex))) : NONE;
+  };
 
   // ---------------------------------------------------------------- seeds
   // The candidates in the query's true buckets (its first nseedp probes, one per
-  // table) are mostly its near neighbours: deduplicated (shared-memory hash) and
-  // scored exactly first, into per-warp seed lists that only raise the threshold
-  // (their own family of disjoint lists); the scan below then starts near the final
-  // k-th best instead of at -inf.  Seeds are scanned again like any candidate.
-  if (a.nseedp) {
+  // table) are mostly its near neighbours: scored exactly first, so the scan below
+  // starts near the final k-th best instead of at -inf.
+  //   WALK: every entry of the leading true buckets (whole buckets, up to WK_SEEDCAP
+  //   entries) is admitted through the visited bitmap and scored into the warps'
+  //   main lists; the walk then starts after those probes.
+  //   Lists: deduplicated in a shared-memory hash (capped), scored into per-warp seed
+  //   lists that only raise the threshold (their own family of disjoint lists); the
+  //   seeds are scanned again like any candidate.
+  uint32_t pstart = 0;
+  if constexpr (WALK) {
+    if (a.nseedp) {
+      if (w == 0) {  // leading true buckets whose cumulative length stays <= WK_SEEDCAP
+        uint32_t acc = 0, cnt = 0;
+        for (uint32_t p0 = 0; p0 < a.nseedp; p0 += 32) {
+          const uint32_t p = p0 + lane;
+          const uint32_t len = p < a.nseedp ? pl[p] : 0u;
+          uint32_t incl = len;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const uint32_t ok = __ballot_sync(FULL, p < a.nseedp && acc + incl <= WK_SEEDCAP);
+          cnt += __popc(ok);
+          if (ok != FULL) break;
+          acc += __shfl_sync(FULL, incl, 31);
+        }
+        if (lane == 0) nseed_s = cnt;
+      }
+      __syncthreads();
+      pstart = nseed_s;
+      wk_begin(0, pstart, &wctr_s[0]);
+      for (;;) {
+        const uint32_t id = wk_next();
+        if (wk_done) break;
+        push_exact(id, admit(id, id != NONE));
+        if (qtail - qhead >= 32) {
+          __syncwarp();
+          exact_batch(32);
+        }
+      }
+      if (qtail != qhead) {
+        __syncwarp();
+        exact_batch(qtail - qhead);
+      }
+    }
+  } else if (a.nseedp) {
     uint32_t* hs = reinterpret_cast<uint32_t*>(ring_all);  // [NS_HASH] (the ring: free until the scan)
     uint32_t* seeds = hs + NS_HASH;                       // [NS_SEEDS]
     for (uint32_t i = threadIdx.x; i < NS_HASH; i += blockDim.x) hs[i] = NONE;
     if (threadIdx.x == 0) nseed_s = 0;
     __syncthreads();
-    const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
-    const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
     for (uint32_t p = w; p < a.nseedp; p += NW) {
       const uint64_t p0 = pp[p];
       const uint32_t len = pl[p];
@@ -2323,8 +2499,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     const float sp = dot >= 0 ? __fmul_ru(sx, qs) : __fmul_rd(sx, qs);
     return __fadd_ru(__fmul_ru(sp, If), __fmaf_ru(rx, qh, __fmul_ru(mxn, qr)));
   };
-  const float qh1 = qn_s[0][1], qt1 = qn_s[0][3], qh2 = qn_s[1][1], qt2 = qn_s[1][3];
-  const float qnorm = __fadd_ru(qh1, qt1);  // >= ||q||
+  const float qt1 = qn_s[0][3], qt2 = qn_s[1][3];
+  const float qnorm = __fadd_ru(qn_s[0][1], qt1);  // >= ||q||
   auto thr_now = [&] { return dkey_inv(*(volatile unsigned long long*)&thr_key); };
 
   // stage 2 of 32 stage-1 survivors: bound A1 + A2 + t2 ||q after stage 2||
@@ -2344,9 +2520,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       const float ub = __fadd_ru(__fmaf_ru(tx, qt2, A), __fmul_ru(mag, 1e-6f));
       live = (double)ub >= thr_now();
     }
-    const uint32_t live_m = __ballot_sync(FULL, live);
-    if (live) sq[(qtail + __popc(live_m & lt_mask)) % NS_QCAP] = id;
-    qtail += __popc(live_m);
+    if (WALK) live = admit(id, live);  // every id scored exactly at most once
+    push_exact(id, live);
     nst2 += cnt;
   };
 
@@ -2358,9 +2533,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   const uint32_t nb = (Len + 31) / 32;
   const uint32_t nbw = nb > (uint32_t)w ? (nb - w + NW - 1) / NW : 0;  // this warp's batches
   auto batch_ids = [&](uint32_t i) {  // lane c: candidate c of the warp's i-th batch
-    const uint32_t ci = (w + i * NW) * 32 + lane;
-    return (i < nbw && ci < Len) ? __ldcs(cand + ci) : NONE;
+    if constexpr (WALK) {
+      return wk_next();
+    } else {
+      const uint32_t ci = (w + i * NW) * 32 + lane;
+      return (i < nbw && ci < Len) ? __ldcs(cand + ci) : NONE;
+    }
   };
+  auto more = [&](uint32_t i) { return WALK ? !(wk_done && i >= nprod) : i < nbw; };
   auto issue = [&](uint32_t i, uint32_t id) {  // records of the warp's i-th batch -> slot
     const uint32_t slot = i % NS_RING;
     rid[slot * 32 + lane] = id;
@@ -2373,10 +2553,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     }
     cp_commit();
   };
+  if constexpr (WALK) wk_begin(pstart, (uint32_t)a.peff, &wctr_s[1]);
 #pragma unroll
   for (uint32_t i = 0; i < NS_RING - 1; ++i) issue(i, batch_ids(i));
   uint32_t nid = batch_ids(NS_RING - 1);
-  for (uint32_t i = 0; i < nbw; ++i) {
+  for (uint32_t i = 0; more(i); ++i) {
     // full queues are drained first (their own loads; the ring stays in flight)
     if (qtail - qhead >= 32) {
       __syncwarp();
@@ -2423,7 +2604,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       exact_batch(min(32u, qtail - qhead));
     }
   }
-  (void)qh2;
   if (lane == 0) {
     // bytes read: 64 B stage-1 record per candidate, 64 B stage-2 record per stage-1
     // survivor, and the exact rows
@@ -2454,6 +2634,17 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       a.stats[q].exact = a.uq_all ? a.uq_all[q] : Len;
     }
   }
+  if constexpr (WALK) {  // leave the visited bitmap clear for the next query
+    __syncthreads();
+    const uint32_t nl = logn_s;
+    if (nl > a.logcap) {  // log overflow (pathological survivor counts): clear it all
+      for (uint32_t i = threadIdx.x; i < a.nwords; i += blockDim.x) bm[i] = 0;
+    } else {
+      for (uint32_t i = threadIdx.x; i < nl; i += blockDim.x) bm[wlog[i] >> 5] = 0;
+    }
+    __syncthreads();
+  }
+  }  // queries
 }
 
 static size_t screen_smem(uint32_t d) {
@@ -2607,6 +2798,7 @@ static void stage_a(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   FPP_LAUNCH();
   FPP_CUDA(cudaMemcpyAsync(sl.pinned, sl.coff.p + nqc, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   cx.timer.end(PH_PROBE, e0, st);
+  cx.acc.launches += 3;  // lists, probe_select, scan_eq
   FPP_CUDA(cudaEventRecord(sl.ev_probe, st));
 }
 
@@ -2619,20 +2811,67 @@ static uint32_t grouped_shift(uint64_t n) {
   return sm + 64 <= (size_t)co_smem_max() ? gs : 0u;
 }
 
-// Stage B on stream `st` (after the host has read the slot's candidate total):
-// bucket walk + dedup, then row gather + fp64 dot + top-k.
+// zero-initialised on (re)allocation; every kernel using it leaves it clear
+static uint32_t* slot_bitmap(QSlot& sl, size_t words, cudaStream_t st) {
+  if (sl.bitmap.n < words) {
+    sl.bitmap.alloc(words);
+    FPP_CUDA(cudaMemsetAsync(sl.bitmap.p, 0, words * 4, st));
+  }
+  return sl.bitmap.p;
+}
+
+constexpr uint32_t WK_LOGCAP = 16384;  // per-CTA log of ids admitted to the exact stage
+
+// Stage B on stream `st`: bucket walk + dedup, then row gather + fp64 dot + top-k.
+// The collect pass needs the slot's candidate total on the host (it sizes the
+// lists): it waits for stage A's readback.  The walking screen kernel (narrow rows
+// with screening records) needs no lists and no host sync; it still runs the
+// collect when per-query stats (unique candidate counts) or the lists themselves
+// (`lists`: fpp_query_debug) are requested.
 static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, uint32_t nqc,
                     uint32_t k, uint32_t qprobes, uint32_t* ids_d, double* scores_d,
-                    fpp_query_stats* stats_d, cudaStream_t st, uint32_t rerank = 0) {
+                    fpp_query_stats* stats_d, cudaStream_t st, uint32_t rerank = 0,
+                    bool lists = false) {
   const uint64_t peff = query_probes(ix, qprobes);
-  const uint64_t etot = sl.pinned[0];
-  sl.cands.ensure(etot + 1);
-  cudaEvent_t e0;
-  cx.timer.begin(PH_COLLECT, st, &e0);
   const uint32_t nwords = (uint32_t)((ix.n + 31) / 32);
+  // score policy first: exact early termination (k_score_pruned / k_score_screen)
+  // when the index has tail norms (d > 64) and the bound pays on this data: the read
+  // fraction (row slices read / all) is probed on the first chunk and every 16th after
+  // (async readback); above 0.65 the job overhead outweighs the saved bytes (C1 iid:
+  // 1.0, 1.36x slower; C3: 0.77, 1.2x slower; C2: 0.33, 2.1x faster) and k_score runs.
+  // FPP_NO_PRUNE=1 / FPP_PRUNE=1 force either; FPP_DEBUG_PRUNE=1 prints every chunk's
+  // fraction.
+  const bool no_prune = getenv("FPP_NO_PRUNE") != nullptr;
+  const bool force_prune = getenv("FPP_PRUNE") != nullptr;
+  const bool dbg = getenv("FPP_DEBUG_PRUNE") != nullptr;
+  bool use_pruned = false, probe = false;
+  if (ix.xt_n && !no_prune) {
+    std::lock_guard<std::mutex> lk(ix.mu);  // the index-wide policy (concurrent calls)
+    if (cx.prune_pending && cudaEventQuery(cx.prune_ev) == cudaSuccess) {
+      if (cx.prune_h[0]) ix.prune_frac = (double)cx.prune_h[1] / ((double)cx.prune_h[0] * ix.d);
+      cx.prune_pending = false;
+    }
+    probe = dbg || (!cx.prune_pending && (ix.prune_frac < 0 || ix.prune_chunks % 16 == 0));
+    use_pruned = force_prune || probe || ix.prune_frac < 0 || ix.prune_frac <= 0.65;
+    ++ix.prune_chunks;
+  }
+  // narrow rows: the record screen (k_score_screen) unless FPP_SC_NARROW=0; it walks
+  // the probes itself unless FPP_SC_WALK=0
+  static const bool narrow_off = getenv("FPP_SC_NARROW") && atoi(getenv("FPP_SC_NARROW")) == 0;
+  static const bool walk_off = getenv("FPP_SC_WALK") && atoi(getenv("FPP_SC_WALK")) == 0;
+  const bool screen = use_pruned && ix.q8rec && !narrow_off && !rerank;
+  const bool walk = screen && !walk_off && !lists;
+  const bool collect = !walk || stats_d != nullptr;
+  cudaEvent_t e0;
   sl.uniq.ensure(nqc);
   CollectArgs ca{sl.ppos.p, sl.plen.p, peff, ix.ids, sl.coff.p, sl.cands.p, sl.uq.p,
                  nqc, nwords, nullptr, sl.counter.p, 0, 0, sl.uniq.p, ix.n};
+  if (collect) {
+  FPP_CUDA(cudaEventSynchronize(sl.ev_probe));  // the candidate total (stage A readback)
+  const uint64_t etot = sl.pinned[0];
+  sl.cands.ensure(etot + 1);
+  ca.cands = sl.cands.p;
+  cx.timer.begin(PH_COLLECT, st, &e0);
   // Visited set (every id scored once): an n-bit bitmap in shared memory
   // where it fits one SM (n <= ~1.8 M); beyond that the grouped dedup (id-range
   // counting sort + per-warp range bitmaps; C4's 10 M points); beyond its range an
@@ -2683,23 +2922,21 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     k_collect_cluster<<<ncl * CO_CLUSTER, CO_CL_THREADS, sm, st>>>(ca, slice_words);
   } else {
     co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * 2);
-    const size_t need = (size_t)co_grid * nwords;
-    if (sl.bitmap.n < need) {
-      sl.bitmap.alloc(need);
-      FPP_CUDA(cudaMemsetAsync(sl.bitmap.p, 0, need * 4, st));
-    }
-    ca.gbitmap = sl.bitmap.p;
+    ca.gbitmap = slot_bitmap(sl, (size_t)co_grid * nwords, st);
     FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
     k_collect<<<co_grid, CO_THREADS, 0, st>>>(ca);
   }
   FPP_LAUNCH();
   cx.timer.end(PH_COLLECT, e0, st);
+  cx.acc.launches += 1;
+  }  // collect
 
   cx.timer.begin(PH_SCORE, st, &e0);
   ScoreArgs sa{ix.X, ix.d, ix.ldx, Qd, sl.coff.p, sl.cands.p, sl.uq.p, sl.eq.p, peff, k,
                ix.prm.id_offset, ids_d, scores_d, stats_d, nullptr, 0};
   sa.rbytes = ix.score_bytes_d.p;
   if (ca.grouped) sa.uq_all = sl.uniq.p;  // lists carry holes: unique counts for the stats
+  else if (walk && collect) sa.uq_all = sl.uq.p;  // (the walking kernel reads no lists)
   if (rerank) {  // SimHash screen: at most B candidates per query reach the exact scores
     sa.uq_all = nullptr;
     sl.qsig.ensure(nqc);
@@ -2734,29 +2971,7 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   // ascending-id candidate lists more queries in flight share more rows in L2:
   // C2 96x2 @ 2/SM 344k -> 64x2 @ 3/SM 352k q/s; C4 +5%); 32 x 4 below
   const bool wide = ix.d >= 64;
-  // exact early termination (k_score_pruned) when the index has tail norms (d > 64)
-  // and the bound pays on this data: the read fraction (row slices read / all) is
-  // probed on the first chunk and every 16th after (async readback); above 0.65 the
-  // job overhead outweighs the saved bytes (C1 iid: 1.0, 1.36x slower; C3: 0.77,
-  // 1.2x slower; C2: 0.33, 2.1x faster) and k_score runs.  FPP_NO_PRUNE=1 / FPP_PRUNE=1
-  // force either; FPP_DEBUG_PRUNE=1 prints every chunk's fraction.
-  const bool no_prune = getenv("FPP_NO_PRUNE") != nullptr;
-  const bool force_prune = getenv("FPP_PRUNE") != nullptr;
-  const bool dbg = getenv("FPP_DEBUG_PRUNE") != nullptr;
-  bool use_pruned = false, probe = false;
-  if (ix.xt_n && !no_prune) {
-    std::lock_guard<std::mutex> lk(ix.mu);  // the index-wide policy (concurrent calls)
-    if (cx.prune_pending && cudaEventQuery(cx.prune_ev) == cudaSuccess) {
-      if (cx.prune_h[0]) ix.prune_frac = (double)cx.prune_h[1] / ((double)cx.prune_h[0] * ix.d);
-      cx.prune_pending = false;
-    }
-    probe = dbg || (!cx.prune_pending && (ix.prune_frac < 0 || ix.prune_chunks % 16 == 0));
-    use_pruned = force_prune || probe || ix.prune_frac < 0 || ix.prune_frac <= 0.65;
-    ++ix.prune_chunks;
-  }
-  // narrow rows: the register head screen (k_score_screen) unless FPP_SC_NARROW=0
-  static const bool narrow_off = getenv("FPP_SC_NARROW") && atoi(getenv("FPP_SC_NARROW")) == 0;
-  if (use_pruned && ix.q8rec && !narrow_off && !rerank) {
+  if (screen) {
     sa.xtail = reinterpret_cast<const float*>(ix.q8rec);
     sa.n = ix.n;
     if (probe) {
@@ -2779,10 +2994,28 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     static const int scr_minb = getenv("FPP_SC_SCR_MINB") ? atoi(getenv("FPP_SC_SCR_MINB")) : 2;
     auto launch_scr = [&](auto kern) {
       FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      kern<<<nqc, NS_W * 32, sm, st>>>(sa);
+      unsigned grid = nqc;
+      if (walk) {  // persistent CTAs, one visited bitmap + admission log each
+        int occ = 1;
+        FPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NS_W * 32, sm));
+        grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sm_count() * std::max(occ, 1));
+        sa.gbm = slot_bitmap(sl, (size_t)grid * nwords, st);
+        sa.nwords = nwords;
+        sl.wlog.ensure((size_t)grid * WK_LOGCAP);
+        sa.wlog = sl.wlog.p;
+        sa.logcap = WK_LOGCAP;
+        sa.qctr = sl.counter.p + 1;
+        FPP_CUDA(cudaMemsetAsync(sa.qctr, 0, sizeof(uint32_t), st));
+      }
+      kern<<<grid, NS_W * 32, sm, st>>>(sa);
     };
-    if (scr_minb == 2) launch_scr(k_score_screen<NS_W, 2>);
-    else launch_scr(k_score_screen<NS_W, 3>);
+    if (walk) {
+      if (scr_minb == 2) launch_scr(k_score_screen<NS_W, 2, true>);
+      else launch_scr(k_score_screen<NS_W, 3, true>);
+    } else {
+      if (scr_minb == 2) launch_scr(k_score_screen<NS_W, 2, false>);
+      else launch_scr(k_score_screen<NS_W, 3, false>);
+    }
     if (probe) {
       FPP_CUDA(cudaMemcpyAsync(cx.prune_h, cx.prune_d.p, 16, cudaMemcpyDeviceToHost, st));
       FPP_CUDA(cudaEventRecord(cx.prune_ev, st));
@@ -2863,7 +3096,8 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   }
   FPP_LAUNCH();
   cx.timer.end(PH_SCORE, e0, st);
-  cx.acc.launches += 5;  // lists, probe_select, scan_eq, collect, score
+  cx.acc.launches += 1;  // score (stage A: lists, probe_select, scan_eq)
+  cx.acc.score_launches += 1;
   cx.acc.probes += peff * nqc;
 }
 
@@ -2905,7 +3139,6 @@ static void run_query_core(const Index& ix, QueryCtx& cx, const float* Qd, uint6
       const uint64_t q0 = c * cs;
       const uint32_t n = (uint32_t)std::min<uint64_t>(cs, nq - q0);
       stage_a(ix, cx, cx.slot[0], Qd + q0 * ix.d, n, qprobes, s, nullptr);
-      FPP_CUDA(cudaEventSynchronize(cx.slot[0].ev_probe));
       stage_b(ix, cx, cx.slot[0], Qd + q0 * ix.d, n, k, qprobes, ids_d + q0 * k, scores_d + q0 * k,
               stats_d ? stats_d + q0 : nullptr, s, rerank);
     }
@@ -2927,7 +3160,6 @@ static void run_query_core(const Index& ix, QueryCtx& cx, const float* Qd, uint6
   if (nch > 1) issue_a(1);
   for (uint64_t c = 0; c < nch; ++c) {
     QSlot& sl = cx.slot[c & 1];
-    FPP_CUDA(cudaEventSynchronize(sl.ev_probe));
     FPP_CUDA(cudaStreamWaitEvent(cx.sB, sl.ev_probe, 0));
     const uint64_t q0 = c * cs;
     const uint32_t n = (uint32_t)std::min<uint64_t>(cs, nq - q0);
@@ -3071,7 +3303,7 @@ void query_debug(const Index& ix, QueryCtx& cx, const float* qd, uint32_t qprobe
   QSlot& sl = cx.slot[0];
   stage_a(ix, cx, sl, qd, 1, qprobes, s, dbg.p);
   FPP_CUDA(cudaEventSynchronize(sl.ev_probe));
-  stage_b(ix, cx, sl, qd, 1, 1, qprobes, ids.p, sc.p, nullptr, s, 0);
+  stage_b(ix, cx, sl, qd, 1, 1, qprobes, ids.p, sc.p, nullptr, s, 0, true);
   FPP_CUDA(cudaStreamSynchronize(s));
   probes.resize(peff);
   FPP_CUDA(cudaMemcpy(probes.data(), dbg.p, peff * 8, cudaMemcpyDeviceToHost));

@@ -21,7 +21,8 @@ for r in rows[1:]:
     a[1] += v
 tot = sum(v for _, v in agg.values())
 QUERY = ("k_query_lists", "k_probe_select", "k_scan_eq", "k_collect", "k_collect_cluster", "k_score",
-         "k_score_pruned", "k_order_keys", "k_gather_rows", "k_scatter_results")
+         "k_score_pruned", "k_score_screen", "k_order_keys", "k_order_sort", "k_gather_rows",
+         "k_scatter_results", "k_merge_topk")
 qtot = sum(v for k, (_, v) in agg.items() if k in QUERY) or 1
 lines = ["| kernel | launches | total ms | share of all | share of query |", "|---|---|---|---|---|"]
 for k, (c, v) in agg.items():

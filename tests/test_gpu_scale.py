@@ -225,22 +225,62 @@ def test_score_screen_exact(fpp, orc, d, k, seeds, monkeypatch):
     ox = orc.Index(X, L=14, K=2, D=D, iprobes=3, alpha=0.2)
     oi, os_, ost = ox.query(Q, k, 6000)
     ok = np.isfinite(os_)
-    for path in ("smem", "grouped"):
-        if path == "grouped":
+    monkeypatch.setenv("FPP_NO_PRUNE", "1")
+    fi, fs, fst = ix.query(Q, k, 6000, return_stats=True)
+    monkeypatch.delenv("FPP_NO_PRUNE")
+    # walk: the screen walks the probes itself (the default; without stats no collect
+    # runs at all); lists: it reads the collect's candidate lists (FPP_SC_WALK=0)
+    for path in ("smem", "grouped", "walk-nostats", "lists-smem", "lists-grouped"):
+        monkeypatch.setenv("FPP_SC_WALK", "0" if path.startswith("lists") else "1")
+        if path.endswith("grouped"):
             monkeypatch.setenv("FPP_FORCE_COLLECT", "grouped")
+        else:
+            monkeypatch.delenv("FPP_FORCE_COLLECT", raising=False)
         monkeypatch.setenv("FPP_PRUNE", "1")
         monkeypatch.setenv("FPP_DEBUG_PRUNE", "1")
-        gi, gs, gst = ix.query(Q, k, 6000, return_stats=True)
+        if path == "walk-nostats":
+            gi, gs = ix.query(Q, k, 6000)
+            gst = fst
+        else:
+            gi, gs, gst = ix.query(Q, k, 6000, return_stats=True)
         monkeypatch.delenv("FPP_PRUNE")
         monkeypatch.delenv("FPP_DEBUG_PRUNE")
-        monkeypatch.setenv("FPP_NO_PRUNE", "1")
-        fi, fs, fst = ix.query(Q, k, 6000, return_stats=True)
-        monkeypatch.delenv("FPP_NO_PRUNE")
         assert np.array_equal(gi, fi) and np.array_equal(gs, fs) and np.array_equal(gst, fst), path
         assert np.array_equal(gi, oi) and np.array_equal(gst, ost), path
         assert np.array_equal(gs[ok], os_[ok]), path
-    if k >= 5:
-        assert list(gi[3][:5]) == [11, 7000, 7001, 7002, 7003]
+        if k >= 5:
+            assert list(gi[3][:5]) == [11, 7000, 7001, 7002, 7003], path
+
+
+@pytest.mark.parametrize("case", ["seedcap", "log-overflow"])
+def test_score_walk_limits(fpp, orc, case, monkeypatch):
+    """The walking screen's bounded structures: true buckets longer than WK_SEEDCAP
+    (2048 entries: one-cluster data, huge buckets, so the seeds stop after a prefix of
+    the true buckets and the walk covers the rest), and more than WK_LOGCAP (16384)
+    ids admitted to the exact stage in one query (one tight cluster, where the bound
+    prunes nothing: the CTA clears its whole visited bitmap).  Answers equal the oracle's, and
+    repeated runs on the same contexts stay exact (the bitmaps are left clear)."""
+    if case == "seedcap":
+        X = data(fpp, 30000, 128, 1, 0.05, seed=41)
+        Q = data(fpp, 64, 128, 1, 0.05, seed=41, stream=1)
+        prm = dict(L=6, K=2, D=128, iProbes=2, alpha=0.5)
+        qp, k = 200, 10
+    else:
+        X = data(fpp, 40000, 128, 1, 0.002, seed=43)  # one tight cluster: nothing prunes
+        Q = data(fpp, 40, 128, 1, 0.002, seed=43, stream=1)
+        prm = dict(L=4, K=2, D=128, iProbes=1, alpha=1.0)
+        qp, k = 16, 20
+    ix = fpp.Index.build(X, **prm)
+    ox = orc.Index(X, **{("iprobes" if a == "iProbes" else a): v for a, v in prm.items()})
+    oi, os_, ost = ox.query(Q, k, qp)
+    if case == "log-overflow":
+        assert ost[:, 2].max() > 16384  # candidates per query beyond the log
+    ok = np.isfinite(os_)
+    monkeypatch.setenv("FPP_PRUNE", "1")
+    for _ in range(3):
+        gi, gs = ix.query(Q, k, qp)
+        assert np.array_equal(gi, oi)
+        assert np.array_equal(gs[ok], os_[ok])
 
 
 # ------------------------------------------------ SPEC acceptance #6 and #8 (desk)
