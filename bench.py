@@ -672,13 +672,14 @@ def run_query_bench(args, cfg, qprobes):
     score_bytes_full = 4 * d * U_sum + 4 * U_sum + 4 * d * nq + 12 * K_TOP * nq
     path_bytes_full = 8 * P_sum + 4 * E_sum + 4 * d * U_sum + 4 * d * nq + 12 * K_TOP * nq
     score_ms = tim["score_ms"] / args.steps
-    launches_per_step = tim["launches"] / args.steps
-    reorder = nq >= 256 and nq * d >= 512 * 1024
-    score_launches = max(1.0, (launches_per_step - (4 if reorder else 0)) / 5.0)
+    score_launches = max(1.0, tim["score_launches"] / args.steps)
     launch_s = score_ms / score_launches / 1e3
     tr = dram_traffic(args.config, qprobes) if world == 1 else None
     pruned = row_bytes_step < 4 * d * U_sum
-    roof = {"kernel": "k_score_pruned" if pruned else "k_score", "bound": "hbm", "unit": "GB/s",
+    kname = ("k_score_screen" if 64 <= d <= 256 and d % 4 == 0 else "k_score_pruned") \
+        if pruned else "k_score"
+    roof = {"kernel": tr["kernel"].split("(")[0].replace("void ", "") if tr else kname,
+            "bound": "hbm", "unit": "GB/s",
             "peak": hbm, "peak_kind": peak_kind,
             "kernel_ms_per_launch": launch_s * 1e3, "launches_per_step": score_launches,
             "kernel_ms_per_step": score_ms, "share_of_step": score_ms / (t_ms / args.steps),

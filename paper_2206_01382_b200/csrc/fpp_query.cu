@@ -319,6 +319,7 @@ struct ProbeArgs {
   uint32_t* cpair;        // [nq][ccap] candidate pairs (t<<22 | r1<<11 | r2)
   uint32_t ccap;
   uint32_t beta_q8;       // first T_lo attempt at arm rank beta * m (beta = beta_q8 / 256)
+  uint32_t rank_order;    // 1: keep the selection's emission order (no table-major sort)
 };
 
 __device__ const float g_zero_row[1] = {0.0f};
@@ -880,6 +881,33 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
   const uint32_t P = (uint32_t)a.peff;
   const uint32_t twoD = 2 * D;
   const uint32_t NB = (uint32_t)a.NB;
+  // Table-major probe order: the non-forced probes [L, P) are counting-sorted by
+  // table (order within a table: arbitrary), so the walking score kernel
+  // (k_score_screen<WALK>) sweeps the tables in order and similar queries scored side
+  // by side read the same buckets' rows at about the same time (L2 reuse).  The L
+  // forced true buckets stay in front (the kernel's seeds).  The probe set, hence
+  // every result, is unchanged.
+  uint32_t* tcur = hist;  // [L] table cursors (the selection histogram is free now)
+  const bool tmajor = !a.rank_order && P > L;
+  if (tmajor) {
+    for (uint32_t i = threadIdx.x; i < L; i += blockDim.x) tcur[i] = 0;
+    __syncthreads();
+    for (uint32_t pp = L + threadIdx.x; pp < P; pp += blockDim.x)
+      atomicAdd(&tcur[__ldcg(gb_out + pp) >> 22], 1u);
+    __syncthreads();
+    const uint32_t per = (L + blockDim.x - 1) / blockDim.x;
+    const uint32_t i0 = min(L, threadIdx.x * per), i1 = min(L, i0 + per);
+    uint32_t loc = 0;
+    for (uint32_t i = i0; i < i1; ++i) loc += tcur[i];
+    uint32_t tot;
+    uint32_t base = L + block_excl_scan_u32(loc, (uint32_t*)red, &tot);
+    for (uint32_t i = i0; i < i1; ++i) {
+      const uint32_t c = tcur[i];
+      tcur[i] = base;
+      base += c;
+    }
+    __syncthreads();
+  }
   constexpr int UR = 8;
   for (uint32_t p0 = threadIdx.x; p0 < P; p0 += UR * blockDim.x) {
     uint32_t pr[UR], c1[UR], c2[UR], o0[UR], o1[UR];
@@ -908,10 +936,11 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
       const uint32_t pp = p0 + u * blockDim.x;
       if (pp < P) {
         const uint32_t t = pr[u] >> 22;
-        ppos[pp] = __ldg(a.tbase + t) + o0[u];
-        plen[pp] = o1[u] - o0[u];
+        const uint32_t dst = (tmajor && pp >= L) ? atomicAdd(&tcur[t], 1u) : pp;
+        ppos[dst] = __ldg(a.tbase + t) + o0[u];
+        plen[dst] = o1[u] - o0[u];
         esum += o1[u] - o0[u];
-        if (dbg) dbg[pp] = (uint64_t)t * a.NB + c1[u];
+        if (dbg) dbg[dst] = (uint64_t)t * a.NB + c1[u];
       }
     }
   }
@@ -2076,8 +2105,11 @@ constexpr int NS_W = 8;            // warps per CTA
 constexpr uint32_t NS_QCAP = 64;   // survivor queue per warp (<= 31 + 32 queued)
 constexpr int NS_PAD = 20;         // exact staging: 16-float half chunks, row stride 20 floats
 constexpr int NS_RING = 4;         // stage-1 record ring depth per warp (cp.async)
-constexpr uint32_t NS_HASH_BITS = 11, NS_HASH = 1u << NS_HASH_BITS;  // seed dedup table
-constexpr uint32_t NS_SEEDS = 1024;  // seeds kept (hash load <= 1/2)
+constexpr uint32_t NS_SH_BITS = 11, NS_SH = 1u << NS_SH_BITS;  // seed id hash (lists)
+#ifndef FPP_NS_IDPF
+#define FPP_NS_IDPF 1
+#endif
+constexpr int NS_IDPF = FPP_NS_IDPF;  // candidate-id register queue depth (iterations ahead)
 
 __device__ __forceinline__ unsigned long long dkey(double x) {  // order-preserving
   const unsigned long long b = (unsigned long long)__double_as_longlong(x);
@@ -2088,19 +2120,20 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
   return __longlong_as_double((long long)b);
 }
 
-// WALK = true (large shards without stats): the kernel walks the query's probes
-// itself -- no collect pass and no candidate lists.  Warps take 32-probe chunks in
-// rank order from a CTA counter and cover each chunk's entries 32 at a time (the
-// warp-cooperative walk of k_collect: coalesced id loads, one window ahead of the
-// record ring).  Entries repeat across tables (C4: 1.08 walked per unique id); a
-// repeat is screened again, but every id is scored exactly at most once
-// (SPEC.md:352): the exact stage admits an id only after a test-and-set in the
-// CTA's visited bitmap (global memory, n bits, L2 atomics on the few stage-2
-// survivors), whose set bits are logged and cleared at the end of the query.  The
-// seeds (all entries of the leading true buckets, up to WK_SEEDCAP) are scored
-// exactly straight into the warps' lists through the same bitmap, and the walk
-// starts after them.  Persistent CTAs fetch queries from a counter (one bitmap
-// each).
+// Seeds: all entries of the leading true buckets (whole buckets, up to a cap) are
+// scored exactly first, straight into the warps' lists, so the scan starts near the
+// final k-th best.  Every id is scored exactly at most once: the
+// collect's lists hold each id once, and their seeds are recognised by a
+// shared-memory hash of the seed ids at the exact stage's admission.
+// WALK = true (FPP_SC_WALK=1): the kernel walks the query's probes itself -- no
+// collect pass and no candidate lists.  Warps take 32-probe chunks from a CTA
+// counter and cover each chunk's entries 32 at a time (the warp-cooperative walk of
+// k_collect: coalesced id loads ahead of the record ring).  Entries repeat across
+// tables, so admission is a test-and-set in a per-CTA visited bitmap (global memory,
+// n bits, L2 atomics on the few stage-2 survivors; its set bits are logged and
+// cleared at the end of the query); persistent CTAs (one bitmap each) fetch queries
+// from a counter.  Measured slower on C4 (rows gathered in probe order miss L2 far
+// more often than in id order).
 constexpr uint32_t WK_SEEDCAP = 2048;  // seed entries per query (whole leading true buckets)
 
 template <int NW, int MINB, bool WALK>
@@ -2116,14 +2149,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   uint32_t* s1_all = sq_all + (size_t)NW * NS_QCAP;                    // [NW][QCAP] stage-2 queue ids
   float2* s1v_all = reinterpret_cast<float2*>(s1_all + (size_t)NW * NS_QCAP);  // [NW][QCAP] (A1, N1)
   __shared__ unsigned long long thr_key;  // lower bound of the final k-th best (ordered key)
-  __shared__ double thr2_s[NW];          // per warp: its ceil(k/NW)-th best (main lists)
-  __shared__ double thr3_s[NW];          // the same for the seed lists
+  __shared__ double thr2_s[NW];          // per warp: its ceil(k/NW)-th best
   __shared__ uint32_t nseed_s;
   __shared__ float qn_s[Q8_STAGES][4];   // per stage: s_q, ||q_h||, r_q, ||q after the stage||
   __shared__ __align__(16) int32_t q8_s[Q8_STAGES][Q8_DIMS / 4];  // the query's stage codes
   __shared__ double mg_s[NW][32];
   __shared__ uint32_t mg_i[NW][32];
-  __shared__ uint32_t q_s, wctr_s[2], logn_s;  // WALK: query, chunk counters, log length
+  __shared__ uint32_t q_s, wctr_s[2], logn_s;  // query, walker chunk counters, log length
+  __shared__ uint32_t seedh[NS_SH];     // lists: the seeds' ids (open addressing)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int part = lane & 3, grp = lane >> 2;  // record part (0-2 codes, 3 terms), record slot
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -2133,31 +2166,28 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   uint32_t* sq = sq_all + (size_t)w * NS_QCAP;    // survivors of stage 2 -> exact
   uint32_t* s1q = s1_all + (size_t)w * NS_QCAP;   // survivors of stage 1 -> stage 2
   float2* s1v = s1v_all + (size_t)w * NS_QCAP;
-  uint32_t* const bm = WALK ? a.gbm + (size_t)blockIdx.x * a.nwords : nullptr;
-  uint32_t* const wlog = WALK ? a.wlog + (size_t)blockIdx.x * a.logcap : nullptr;
+  // WALK: the CTA's visited bitmap (exact-stage admission, every id scored once)
+  uint32_t* const bm = a.gbm ? a.gbm + (size_t)blockIdx.x * a.nwords : nullptr;
+  uint32_t* const wlog = a.gbm ? a.wlog + (size_t)blockIdx.x * a.logcap : nullptr;
   const uint4* rec = reinterpret_cast<const uint4*>(a.xtail);  // [stages][n][4] 16 B parts
   const float* X = a.X;
   const uint32_t ldx = a.ldx;
   const uint32_t k = a.k;
   for (uint32_t qi = 0;; ++qi) {
-  uint32_t q;
-  if constexpr (WALK) {
-    if (threadIdx.x == 0) {
-      q_s = atomicAdd(a.qctr, 1u);
-      wctr_s[0] = wctr_s[1] = 0;
-      logn_s = 0;
-    }
-    __syncthreads();
-    q = q_s;
-    if (q >= a.nq) break;
-  } else {
-    if (qi) break;
-    q = blockIdx.x;
+  if (!a.qctr && qi) break;  // (one query per CTA unless persistent)
+  if (threadIdx.x == 0) {  // persistent CTAs fetch queries from a counter
+    q_s = a.qctr ? atomicAdd(a.qctr, 1u) : blockIdx.x;
+    wctr_s[0] = wctr_s[1] = 0;
+    logn_s = 0;
   }
+  for (uint32_t i = threadIdx.x; i < NS_SH; i += blockDim.x) seedh[i] = NONE;
+  __syncthreads();
+  const uint32_t q = q_s;
+  if (q >= a.nq) break;
   const float* Qr = a.Q + (uint64_t)q * d;
   for (uint32_t j = threadIdx.x; j < nch * 32; j += blockDim.x) qd[j] = j < d ? (double)Qr[j] : 0.0;
   if (threadIdx.x == 0) thr_key = dkey(-INFINITY);
-  if (threadIdx.x < NW) thr2_s[threadIdx.x] = thr3_s[threadIdx.x] = -INFINITY;
+  if (threadIdx.x < NW) thr2_s[threadIdx.x] = -INFINITY;
   if ((uint32_t)w < Q8_STAGES) {  // quantize the query like the records (k_q8_records)
     const uint32_t lo = w * Q8_DIMS, hi = lo + Q8_DIMS;
     const uint32_t j0 = lo + lane, j1 = lo + lane + 32;
@@ -2260,15 +2290,33 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     if (lane == 0) nfl += (unsigned long long)cnt * nch * 32;
     publish(bs, bi, thr2_s);
   };
-  // WALK: test-and-set `id` (lanes with `want`) in the CTA's visited bitmap; true for
-  // an id not scored exactly before in this query (logged for the clear)
+  // admission to the exact stage (lanes with `want`): true for an id not scored exactly
+  // before in this query.  WALK: a test-and-set in the CTA's visited bitmap (logged
+  // for the clear).
+  // Lists (deduplicated by the collect) meet only the seeds again: an id found in the
+  // seed hash is not admitted (the seeds are scored from the hash itself).
+  auto hslot = [](uint32_t id) { return (id * 2654435761u) >> (32 - NS_SH_BITS); };
+  auto seed_insert = [&](uint32_t id) {
+    for (uint32_t h = hslot(id);; h = (h + 1) & (NS_SH - 1)) {
+      const uint32_t old = atomicCAS(&seedh[h], NONE, id);
+      if (old == NONE) return true;
+      if (old == id) return false;
+    }
+  };
+  auto seed_has = [&](uint32_t id) {
+    for (uint32_t h = hslot(id);; h = (h + 1) & (NS_SH - 1)) {
+      const uint32_t v = seedh[h];
+      if (v == id) return true;
+      if (v == NONE) return false;
+    }
+  };
   auto admit = [&](uint32_t id, bool want) {
     bool fresh = false;
-    if (WALK && want) {
-      const uint32_t bit = 1u << (id & 31);
-      fresh = !(atomicOr(bm + (id >> 5), bit) & bit);
-    }
-    if (WALK) {
+    if (bm) {  // WALK: lists repeat ids
+      if (want) {
+        const uint32_t bit = 1u << (id & 31);
+        fresh = !(atomicOr(bm + (id >> 5), bit) & bit);
+      }
       const uint32_t bal = __ballot_sync(FULL, fresh);
       if (bal) {
         uint32_t base = 0;
@@ -2276,6 +2324,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
         base = __shfl_sync(FULL, base, 0) + __popc(bal & lt_mask);
         if (fresh && base < a.logcap) wlog[base] = id;
       }
+    } else {
+      fresh = want && !seed_has(id);
     }
     return fresh;
   };
@@ -2361,37 +2411,38 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   // ---------------------------------------------------------------- seeds
   // The candidates in the query's true buckets (its first nseedp probes, one per
   // table) are mostly its near neighbours: scored exactly first, so the scan below
-  // starts near the final k-th best instead of at -inf.
-  //   WALK: every entry of the leading true buckets (whole buckets, up to WK_SEEDCAP
-  //   entries) is admitted through the visited bitmap and scored into the warps'
-  //   main lists; the walk then starts after those probes.
-  //   Lists: deduplicated in a shared-memory hash (capped), scored into per-warp seed
-  //   lists that only raise the threshold (their own family of disjoint lists); the
-  //   seeds are scanned again like any candidate.
+  // starts near the final k-th best instead of at -inf.  Every entry of the leading
+  // true buckets (whole buckets, up to WK_SEEDCAP entries) is admitted through the
+  // visited bitmap and scored into the warps' main lists; WALK then starts the walk
+  // after those probes, and lists meet the seeds again in the scan, where the
+  // bitmap drops them before the exact stage.
   uint32_t pstart = 0;
-  if constexpr (WALK) {
-    if (a.nseedp) {
-      if (w == 0) {  // leading true buckets whose cumulative length stays <= WK_SEEDCAP
-        uint32_t acc = 0, cnt = 0;
-        for (uint32_t p0 = 0; p0 < a.nseedp; p0 += 32) {
-          const uint32_t p = p0 + lane;
-          const uint32_t len = p < a.nseedp ? pl[p] : 0u;
-          uint32_t incl = len;
+  if (a.nseedp) {
+    // leading true buckets whose cumulative length stays <= the seed cap (lists: half
+    // the seed hash, so its load stays <= 1/2)
+    const uint32_t seedcap = bm ? WK_SEEDCAP : NS_SH / 2;
+    if (w == 0) {
+      uint32_t acc = 0, cnt = 0;
+      for (uint32_t p0 = 0; p0 < a.nseedp; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        const uint32_t len = p < a.nseedp ? pl[p] : 0u;
+        uint32_t incl = len;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-          }
-          const uint32_t ok = __ballot_sync(FULL, p < a.nseedp && acc + incl <= WK_SEEDCAP);
-          cnt += __popc(ok);
-          if (ok != FULL) break;
-          acc += __shfl_sync(FULL, incl, 31);
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += y;
         }
-        if (lane == 0) nseed_s = cnt;
+        const uint32_t ok = __ballot_sync(FULL, p < a.nseedp && acc + incl <= seedcap);
+        cnt += __popc(ok);
+        if (ok != FULL) break;
+        acc += __shfl_sync(FULL, incl, 31);
       }
-      __syncthreads();
-      pstart = nseed_s;
-      wk_begin(0, pstart, &wctr_s[0]);
+      if (lane == 0) nseed_s = cnt;
+    }
+    __syncthreads();
+    pstart = nseed_s;
+    wk_begin(0, pstart, &wctr_s[0]);
+    if (bm) {  // WALK: admitted through the bitmap and scored as they come
       for (;;) {
         const uint32_t id = wk_next();
         if (wk_done) break;
@@ -2401,47 +2452,29 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
           exact_batch(32);
         }
       }
-      if (qtail != qhead) {
-        __syncwarp();
-        exact_batch(qtail - qhead);
+    } else {
+      // lists: insert every seed id into the hash (a short, balanced walk), then each
+      // warp scores the ids of its slice of the hash.  The barrier between the two
+      // makes the hash complete before any admission of the scan reads it.
+      for (;;) {
+        const uint32_t id = wk_next();
+        if (wk_done) break;
+        if (id != NONE) seed_insert(id);
       }
-    }
-  } else if (a.nseedp) {
-    uint32_t* hs = reinterpret_cast<uint32_t*>(ring_all);  // [NS_HASH] (the ring: free until the scan)
-    uint32_t* seeds = hs + NS_HASH;                       // [NS_SEEDS]
-    for (uint32_t i = threadIdx.x; i < NS_HASH; i += blockDim.x) hs[i] = NONE;
-    if (threadIdx.x == 0) nseed_s = 0;
-    __syncthreads();
-    for (uint32_t p = w; p < a.nseedp; p += NW) {
-      const uint64_t p0 = pp[p];
-      const uint32_t len = pl[p];
-      for (uint32_t e = lane; e < len; e += 32) {
-        const uint32_t id = __ldg(a.ids + p0 + e);
-        uint32_t h = (id * 2654435761u) >> (32 - NS_HASH_BITS);
-        for (uint32_t tries = 0; tries < NS_HASH; ++tries) {
-          const uint32_t old = atomicCAS(&hs[h], NONE, id);
-          if (old == NONE) {  // new: a seed (capped)
-            const uint32_t pos = atomicAdd(&nseed_s, 1u);
-            if (pos < NS_SEEDS) seeds[pos] = id;
-            break;
-          }
-          if (old == id) break;  // a repeat
-          h = (h + 1) & (NS_HASH - 1);
+      __syncthreads();
+      for (uint32_t h0 = w * (NS_SH / NW); h0 < (w + 1) * (NS_SH / NW); h0 += 32) {
+        const uint32_t id = seedh[h0 + lane];
+        push_exact(id, id != NONE);
+        if (qtail - qhead >= 32) {
+          __syncwarp();
+          exact_batch(32);
         }
       }
     }
-    __syncthreads();
-    const uint32_t ns = min(nseed_s, NS_SEEDS);
-    double sbs = -INFINITY;
-    uint32_t sbi = NONE;
-    for (uint32_t s0 = w * 32; s0 < ns; s0 += NW * 32) {
-      const uint32_t id = s0 + lane < ns ? seeds[s0 + lane] : NONE;
-      const double acc = exact_fold(id);
-      topk_insert(sbs, sbi, k, acc, id, id != NONE);
-      if (lane == 0) nfl += (unsigned long long)min(32u, ns - s0) * nch * 32;
+    if (qtail != qhead) {
+      __syncwarp();
+      exact_batch(qtail - qhead);
     }
-    publish(sbs, sbi, thr3_s);
-    __syncthreads();  // the ring is the records' from here on
   }
 
   // -------------------------------------------------------- record stage bound
@@ -2520,7 +2553,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       const float ub = __fadd_ru(__fmaf_ru(tx, qt2, A), __fmul_ru(mag, 1e-6f));
       live = (double)ub >= thr_now();
     }
-    if (WALK) live = admit(id, live);  // every id scored exactly at most once
+    live = admit(id, live);  // every id scored exactly at most once
     push_exact(id, live);
     nst2 += cnt;
   };
@@ -2556,7 +2589,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   if constexpr (WALK) wk_begin(pstart, (uint32_t)a.peff, &wctr_s[1]);
 #pragma unroll
   for (uint32_t i = 0; i < NS_RING - 1; ++i) issue(i, batch_ids(i));
-  uint32_t nid = batch_ids(NS_RING - 1);
+  // candidate ids are loaded NS_IDPF iterations before their records are issued (a
+  // register queue): one iteration did not cover the id load's DRAM latency (the
+  // top stall)
+  uint32_t nid[NS_IDPF];
+#pragma unroll
+  for (int j = 0; j < NS_IDPF; ++j) nid[j] = batch_ids(NS_RING - 1 + j);
   for (uint32_t i = 0; more(i); ++i) {
     // full queues are drained first (their own loads; the ring stays in flight)
     if (qtail - qhead >= 32) {
@@ -2564,8 +2602,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       exact_batch(32);
     }
     if (t1 - h1 >= 32) stage2_batch(32);
-    issue(i + NS_RING - 1, nid);   // (an empty commit past the end keeps the count)
-    nid = batch_ids(i + NS_RING);
+    issue(i + NS_RING - 1, nid[0]);   // (an empty commit past the end keeps the count)
+#pragma unroll
+    for (int j = 0; j + 1 < NS_IDPF; ++j) nid[j] = nid[j + 1];
+    nid[NS_IDPF - 1] = batch_ids(i + NS_RING - 1 + NS_IDPF);
     cp_wait<NS_RING - 1>();
     __syncwarp();
     const uint32_t slot = i % NS_RING;
@@ -2634,7 +2674,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       a.stats[q].exact = a.uq_all ? a.uq_all[q] : Len;
     }
   }
-  if constexpr (WALK) {  // leave the visited bitmap clear for the next query
+  if (bm) {  // leave the visited bitmap clear for the next query
     __syncthreads();
     const uint32_t nl = logn_s;
     if (nl > a.logcap) {  // log overflow (pathological survivor counts): clear it all
@@ -2649,8 +2689,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
 
 static size_t screen_smem(uint32_t d) {
   const uint32_t nch = (d + 31) / 32;
-  static_assert((size_t)NS_W * NS_RING * 128 * 16 >= (size_t)(NS_HASH + NS_SEEDS) * 4,
-                "the seed table lives in the record ring");
   return (size_t)nch * 32 * 8 + (size_t)NS_W * NS_RING * (128 * 16 + 32 * 4) +
          (size_t)NS_W * 32 * NS_PAD * 4 + (size_t)NS_W * NS_QCAP * (4 + 4 + 8);
 }
@@ -2769,6 +2807,8 @@ static void stage_a(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   // e.g. tests force the exact re-walk fallback with a low beta)
   const char* beta_env = getenv("FPP_PS_BETA");
   pa.beta_q8 = beta_env ? (uint32_t)(atof(beta_env) * 256) : 179u;
+  static const bool rank_order = getenv("FPP_PROBE_RANKORDER") != nullptr;
+  pa.rank_order = rank_order ? 1u : 0u;
   static const bool dbg_probe = getenv("FPP_DEBUG_PROBE") != nullptr;
   if (dbg_probe) {
     sl.dbgclk.ensure((size_t)nqc * 16);
@@ -2855,12 +2895,14 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     use_pruned = force_prune || probe || ix.prune_frac < 0 || ix.prune_frac <= 0.65;
     ++ix.prune_chunks;
   }
-  // narrow rows: the record screen (k_score_screen) unless FPP_SC_NARROW=0; it walks
-  // the probes itself unless FPP_SC_WALK=0
+  // narrow rows: the record screen (k_score_screen) unless FPP_SC_NARROW=0.  It reads
+  // the collect's id-ordered candidate lists; FPP_SC_WALK=1 makes it walk the probes
+  // itself instead (no collect pass; measured slower on C4: 256 vs 94 + 175 ms per
+  // step -- rows gathered in probe order miss L2 far more often than in id order).
   static const bool narrow_off = getenv("FPP_SC_NARROW") && atoi(getenv("FPP_SC_NARROW")) == 0;
-  static const bool walk_off = getenv("FPP_SC_WALK") && atoi(getenv("FPP_SC_WALK")) == 0;
+  static const bool walk_on = getenv("FPP_SC_WALK") && atoi(getenv("FPP_SC_WALK")) != 0;
   const bool screen = use_pruned && ix.q8rec && !narrow_off && !rerank;
-  const bool walk = screen && !walk_off && !lists;
+  const bool walk = screen && walk_on && !lists;
   const bool collect = !walk || stats_d != nullptr;
   cudaEvent_t e0;
   sl.uniq.ensure(nqc);

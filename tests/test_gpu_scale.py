@@ -228,17 +228,18 @@ def test_score_screen_exact(fpp, orc, d, k, seeds, monkeypatch):
     monkeypatch.setenv("FPP_NO_PRUNE", "1")
     fi, fs, fst = ix.query(Q, k, 6000, return_stats=True)
     monkeypatch.delenv("FPP_NO_PRUNE")
-    # walk: the screen walks the probes itself (the default; without stats no collect
-    # runs at all); lists: it reads the collect's candidate lists (FPP_SC_WALK=0)
-    for path in ("smem", "grouped", "walk-nostats", "lists-smem", "lists-grouped"):
-        monkeypatch.setenv("FPP_SC_WALK", "0" if path.startswith("lists") else "1")
-        if path.endswith("grouped"):
+    # lists: the screen reads the collect's id-ordered lists (default; without stats
+    # the grouped collect leaves repeats, which the exact stage's bitmap drops);
+    # walk: it walks the probes itself (FPP_SC_WALK=1; without stats no collect runs)
+    for path in ("smem", "grouped", "grouped-nostats", "walk", "walk-nostats"):
+        monkeypatch.setenv("FPP_SC_WALK", "1" if path.startswith("walk") else "0")
+        if path.startswith("grouped"):
             monkeypatch.setenv("FPP_FORCE_COLLECT", "grouped")
         else:
             monkeypatch.delenv("FPP_FORCE_COLLECT", raising=False)
         monkeypatch.setenv("FPP_PRUNE", "1")
         monkeypatch.setenv("FPP_DEBUG_PRUNE", "1")
-        if path == "walk-nostats":
+        if path.endswith("nostats"):
             gi, gs = ix.query(Q, k, 6000)
             gst = fst
         else:
@@ -277,10 +278,12 @@ def test_score_walk_limits(fpp, orc, case, monkeypatch):
         assert ost[:, 2].max() > 16384  # candidates per query beyond the log
     ok = np.isfinite(os_)
     monkeypatch.setenv("FPP_PRUNE", "1")
-    for _ in range(3):
-        gi, gs = ix.query(Q, k, qp)
-        assert np.array_equal(gi, oi)
-        assert np.array_equal(gs[ok], os_[ok])
+    for walk in ("0", "1"):
+        monkeypatch.setenv("FPP_SC_WALK", walk)
+        for _ in range(3):
+            gi, gs = ix.query(Q, k, qp)
+            assert np.array_equal(gi, oi), walk
+            assert np.array_equal(gs[ok], os_[ok]), walk
 
 
 # ------------------------------------------------ SPEC acceptance #6 and #8 (desk)
