@@ -26,7 +26,9 @@ __all__ = ["Index", "normalize", "synth", "merge_topk_device", "device_count", "
            "FppIOError", "content_hash", "center", "MODES", "lib",
            "LIB_PATH", "Params", "QueryStats", "Timings"]
 
-LIB_PATH = _build.LIB
+# FPP_LIB_PATH: a variant build (python -m paper_2206_01382_b200._build <name> -D...) for
+# tuning experiments; the default is the in-tree library
+LIB_PATH = os.environ.get("FPP_LIB_PATH") or _build.LIB
 
 FPP_OK = 0
 MODES = {"falconnpp": 0, "falconn_baseline": 1}

@@ -39,21 +39,26 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, variant: str = "",
+          extra: tuple = ()) -> str:
+    """variant: build lib/var_<variant>.so with the extra nvcc flags instead (tuning
+    experiments; loaded with FPP_LIB_PATH)."""
+    lib = os.path.join(LIBDIR, f"var_{variant}.so") if variant else LIB
+    if not variant and not force and not needs_build():
         return LIB
-    os.makedirs(os.path.join(LIBDIR, "obj"), exist_ok=True)
+    objdir = os.path.join(LIBDIR, "obj" + (f"_{variant}" if variant else ""))
+    os.makedirs(objdir, exist_ok=True)
     objs = []
 
     def compile_one(src):
-        obj = os.path.join(LIBDIR, "obj", os.path.basename(src) + ".o")
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
         # FPP_NVCC_EXTRA: extra flags for experiments (e.g. -DFPP_CO_CL_THREADS=512)
         cmd = [NVCC] + ARCH + FLAGS + os.environ.get("FPP_NVCC_EXTRA", "").split() + \
-            ["-c", src, "-o", obj]
+            list(extra) + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
-        log = os.path.join(LIBDIR, "obj", os.path.basename(src) + ".ptxas.txt")
+        log = os.path.join(objdir, os.path.basename(src) + ".ptxas.txt")
         with open(log, "w") as f:
             f.write(r.stderr)
         if verbose:
@@ -62,15 +67,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, _sources()))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC] + ARCH + ["-shared", "-ccbin", "/usr/bin/g++", "-o", tmp] + objs + \
         ["-Xcompiler", "-fopenmp", "-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=False))
+    import sys
+    if len(sys.argv) > 1:  # python -m paper_2206_01382_b200._build <variant> -DFLAG=..
+        print(build(variant=sys.argv[1], extra=tuple(sys.argv[2:])))
+    else:
+        print(build(force=True, verbose=False))

@@ -92,6 +92,7 @@ Index::~Index() {
   dfree(sigs);
   dfree(xtail);
   dfree(q8rec);
+  dfree(q8csr);
   dfree(offsets);
   dfree(table_base);
   dfree(ids);

@@ -97,6 +97,11 @@ struct Index {
   // screening records per row -- Q8_DIMS dims each as int8 codes with a per-row
   // scale, plus the error / norm terms of the bound (k_q8_records)
   uint4* q8rec = nullptr;
+  // the stage-1 records again, in CSR entry order ([kept_total][4] uint4: entry e's
+  // record is q8rec[ids[e]]), so the walking screen streams them with its bucket walk
+  // instead of one random 128 B DRAM line per 64 B record; built by the first query
+  // that walks (ensure_q8csr)
+  mutable uint4* q8csr = nullptr;
   uint32_t xt_head = 64;  // head (screening) slice width, see launch_tail_norms
   std::vector<float> center;  // [d] when prm.centering (dataset.cpp center())
   uint64_t device_bytes = 0;

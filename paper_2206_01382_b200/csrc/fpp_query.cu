@@ -1010,6 +1010,7 @@ struct CollectArgs {
   uint32_t gshift;       // grouped: id >> gshift < CO_NG; per-warp range bitmap 2^gshift bits
   uint32_t* uniq;        // unique candidates per query (uq = list length incl. grouped holes)
   uint64_t n;            // points (grouped: groups in use = ((n - 1) >> gshift) + 1)
+  uint32_t sliced;       // 1: sliced bitmap dedup (gshift = slice bits), see collect_sliced
 };
 
 // Warp-cooperative walk over one query's probes.  A warp takes 32 probes at a
@@ -1201,6 +1202,93 @@ __device__ __forceinline__ void collect_grouped(const CollectArgs& a, uint32_t q
   *U_out = E - dups_sh;
 }
 
+// Sliced dedup (large shards: the n-bit visited set is off-chip).  A counting sort
+// of the walked ids into id slices of 2^gshift ids (two walks: counts, then the
+// scatter into the query's candidate segment -- few slices, so the scatter streams
+// are nearly sequential), then slice by slice: the slice's ids are ORed into a
+// 2^gshift-bit bitmap in shared memory, and the bitmap is scanned (each thread a
+// contiguous word range, a block scan for the positions) to emit the slice's unique
+// ids in ascending order, clearing the words as it goes.  The output trails the
+// input (slices 0..s hold at most as many unique ids as entries, so slice s's output
+// ends at or before slice s + 1's input starts): it is written in place.  Result: the query's unique candidates in ascending
+// id order, like the one-slice shared-memory path.
+constexpr uint32_t CO_SLICE_BITS = 19;  // 64 KB slice bitmaps (two CTAs per SM)
+__device__ __forceinline__ void collect_sliced(const CollectArgs& a, uint32_t q, uint32_t* out,
+                                               uint32_t* ucount, uint32_t* nextc, uint32_t* sm,
+                                               uint32_t* scan_sh, uint32_t* U_out) {
+  uint32_t* cnt = sm;          // [CO_NG] slice counts -> scatter cursors (= slice ends)
+  uint32_t* bmp = sm + CO_NG;  // [2^gshift / 32] slice bitmap (kept clear)
+  const int lane = threadIdx.x & 31;
+  const uint32_t P = (uint32_t)a.peff, sb = a.gshift;
+  const uint32_t ns = (uint32_t)((a.n - 1) >> sb) + 1;
+  const uint32_t bw = 1u << (sb - 5);
+  const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
+  const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
+  auto next_chunk = [&]() {
+    uint32_t c = 0;
+    if (lane == 0) c = smem_fetch_add(nextc, 1u);
+    return __shfl_sync(FULL, c, 0);
+  };
+  for (uint32_t i = threadIdx.x; i < CO_NG; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  const uint32_t cnt_base = (uint32_t)__cvta_generic_to_shared(cnt);
+  const uint32_t bmp_base = (uint32_t)__cvta_generic_to_shared(bmp);
+  collect_walk(pp, pl, P, a.ids, out, ucount, next_chunk, [&](uint32_t id) {
+    asm volatile("red.shared.add.u32 [%0], 1;\n" ::"r"(cnt_base + ((id >> sb) << 2)) : "memory");
+    return false;
+  });
+  __syncthreads();
+  {
+    static_assert(CO_NG == CO_THREADS, "one slice count per thread");
+    uint32_t E;
+    const uint32_t v = cnt[threadIdx.x];
+    cnt[threadIdx.x] = block_excl_scan_u32(v, scan_sh, &E);
+    if (threadIdx.x == 0) *nextc = 0;
+  }
+  __syncthreads();
+  collect_walk(pp, pl, P, a.ids, out, ucount, next_chunk, [&](uint32_t id) {
+    uint32_t pos;
+    asm volatile("atom.shared.add.u32 %0, [%1], 1;\n" : "=r"(pos) : "r"(cnt_base + ((id >> sb) << 2)) : "memory");
+    out[pos] = id;
+    return false;
+  });
+  __syncthreads();  // cnt[s] is now the end of slice s
+  const uint32_t mask = (1u << sb) - 1u;
+  const uint32_t per = bw / blockDim.x;  // bitmap words per thread (>= 4, multiple of 4)
+  uint32_t wpos = 0;
+  for (uint32_t s = 0; s < ns; ++s) {
+    const uint32_t S = s ? cnt[s - 1] : 0u, Es = cnt[s];
+    if (Es == S) continue;
+    for (uint32_t i = S + threadIdx.x; i < Es; i += blockDim.x) {
+      const uint32_t b = out[i] & mask;
+      asm volatile("red.shared.or.b32 [%0], %1;\n" ::"r"(bmp_base + ((b >> 5) << 2)), "r"(1u << (b & 31))
+                   : "memory");
+    }
+    __syncthreads();
+    uint4* w4 = reinterpret_cast<uint4*>(bmp + threadIdx.x * per);
+    uint32_t c = 0;
+    for (uint32_t j = 0; j < per / 4; ++j) {
+      const uint4 x = w4[j];
+      c += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+    }
+    uint32_t tot;
+    uint32_t pos = wpos + block_excl_scan_u32(c, scan_sh, &tot);
+    const uint32_t id0 = (s << sb) + threadIdx.x * per * 32;
+    for (uint32_t j = 0; j < per / 4; ++j) {
+      const uint4 x = w4[j];
+      const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        for (uint32_t word = wv[e]; word; word &= word - 1)
+          out[pos++] = id0 + (j * 4 + e) * 32 + (__ffs(word) - 1);
+      if (x.x | x.y | x.z | x.w) w4[j] = make_uint4(0, 0, 0, 0);
+    }
+    wpos += tot;
+    __syncthreads();  // the bitmap is clear and scan_sh free for the next slice
+  }
+  *U_out = wpos;
+}
+
 // CTA per query (persistent CTAs fetch queries dynamically); the visited
 // bitmap lives in shared memory (n bits), or the grouped dedup runs (large
 // shards), or -- beyond the grouped range -- a per-CTA global-memory bitmap that
@@ -1213,13 +1301,15 @@ __global__ void __launch_bounds__(CO_THREADS, 2) k_collect(CollectArgs a) {
   if (a.grouped)  // the per-warp range bitmaps start clear and are kept clear
     for (uint32_t i = threadIdx.x; i < (blockDim.x >> 5) << (a.gshift - 5); i += blockDim.x)
       sbm[CO_NG + i] = 0;
+  if (a.sliced)  // the slice bitmap starts clear and is kept clear
+    for (uint32_t i = threadIdx.x; i < (1u << (a.gshift - 5)); i += blockDim.x) sbm[CO_NG + i] = 0;
   for (;;) {
     if (threadIdx.x == 0) {
       qsh = atomicAdd(a.counter, 1u);
       ucount = 0;
       nextc = 0;
     }
-    if (!a.gbitmap && !a.grouped) {
+    if (!a.gbitmap && !a.grouped && !a.sliced) {
       const uint32_t n4 = a.nwords >> 2;
       uint4* b4 = reinterpret_cast<uint4*>(sbm);
       for (uint32_t w = threadIdx.x; w < n4; w += blockDim.x) b4[w] = make_uint4(0, 0, 0, 0);
@@ -1236,7 +1326,9 @@ __global__ void __launch_bounds__(CO_THREADS, 2) k_collect(CollectArgs a) {
       return __shfl_sync(FULL, c, 0);
     };
     uint32_t U;
-    if (a.grouped) {
+    if (a.sliced) {
+      collect_sliced(a, q, out, &ucount, &nextc, sbm, scan_sh, &U);
+    } else if (a.grouped) {
       uint32_t Uu;
       collect_grouped(a, q, out, &ucount, &nextc, sbm, scan_sh, &Uu);
       if (threadIdx.x == 0) a.uniq[q] = Uu;
@@ -1275,6 +1367,7 @@ __global__ void __launch_bounds__(CO_THREADS, 2) k_collect(CollectArgs a) {
       a.uq[q] = U;
       if (a.uniq && !a.grouped) a.uniq[q] = U;
     }
+    if (a.sliced) __syncthreads();  // (the slice counters are reused by the next query)
     if (a.gbitmap)
       for (uint32_t c = threadIdx.x; c < U; c += blockDim.x) bm[out[c] >> 5] = 0;
     __syncthreads();
@@ -1493,6 +1586,8 @@ struct ScoreArgs {
   uint32_t nwords;
   uint32_t* wlog;
   uint32_t logcap;
+  uint32_t seedcap;  // k_score_screen: seed entries per query (whole leading true buckets)
+  const uint4* csrrec;  // WALK: stage-1 records in CSR entry order [kept_total][4] (Index::q8csr)
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -2103,13 +2198,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
 // lists may carry holes (0xFFFFFFFF): skipped.
 constexpr int NS_W = 8;            // warps per CTA
 constexpr uint32_t NS_QCAP = 64;   // survivor queue per warp (<= 31 + 32 queued)
-constexpr int NS_PAD = 20;         // exact staging: 16-float half chunks, row stride 20 floats
-constexpr int NS_RING = 4;         // stage-1 record ring depth per warp (cp.async)
-constexpr uint32_t NS_SH_BITS = 11, NS_SH = 1u << NS_SH_BITS;  // seed id hash (lists)
-#ifndef FPP_NS_IDPF
-#define FPP_NS_IDPF 1
+#ifndef FPP_NS_RING
+#define FPP_NS_RING 4
 #endif
-constexpr int NS_IDPF = FPP_NS_IDPF;  // candidate-id register queue depth (iterations ahead)
+constexpr int NS_RING = FPP_NS_RING;  // stage-1 record ring depth per warp (cp.async)
+constexpr int NS_IDR = 2 * NS_RING;   // candidate-id ring depth per warp
+constexpr uint32_t NS_SH_BITS = 11, NS_SH = 1u << NS_SH_BITS;  // seed id hash (lists)
 
 __device__ __forceinline__ unsigned long long dkey(double x) {  // order-preserving
   const unsigned long long b = (unsigned long long)__double_as_longlong(x);
@@ -2125,16 +2219,18 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
 // final k-th best.  Every id is scored exactly at most once: the
 // collect's lists hold each id once, and their seeds are recognised by a
 // shared-memory hash of the seed ids at the exact stage's admission.
-// WALK = true (FPP_SC_WALK=1): the kernel walks the query's probes itself -- no
-// collect pass and no candidate lists.  Warps take 32-probe chunks from a CTA
-// counter and cover each chunk's entries 32 at a time (the warp-cooperative walk of
-// k_collect: coalesced id loads ahead of the record ring).  Entries repeat across
-// tables, so admission is a test-and-set in a per-CTA visited bitmap (global memory,
-// n bits, L2 atomics on the few stage-2 survivors; its set bits are logged and
-// cleared at the end of the query); persistent CTAs (one bitmap each) fetch queries
-// from a counter.  Measured slower on C4 (rows gathered in probe order miss L2 far
-// more often than in id order).
-constexpr uint32_t WK_SEEDCAP = 2048;  // seed entries per query (whole leading true buckets)
+// WALK = true (the default; FPP_SC_WALK=0 reads lists): the kernel walks the query's
+// probes itself -- no collect pass, no candidate lists, no host sync.  Warps take
+// 32-probe chunks from a CTA counter and cover each chunk's entries 32 at a time (the
+// warp-cooperative walk of k_collect), the ids moving by cp.async into the id ring
+// ahead of their records.  Entries repeat across tables, so admission is a
+// test-and-set in a per-CTA visited bitmap (global memory, n bits, L2 atomics on the
+// few stage-2 survivors; its set bits are logged and cleared at the end of the
+// query); persistent CTAs (one bitmap each) fetch queries from a counter.  On C4 the
+// walk reads ~30% more DRAM bytes than the screen over the collect's id-ordered lists
+// (12.2 vs 9.3 MB per query: repeats, and rows gathered in probe order hit L2 less),
+// but saves the collect pass: 231 ms per step against 97 + 148.
+constexpr uint32_t WK_SEEDCAP = 512;  // seed entries per query (whole leading true buckets)
 
 template <int NW, int MINB, bool WALK>
 __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
@@ -2143,9 +2239,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   const uint32_t d = a.d, nch = (d + 31) / 32;  // 32-float chunks (rows padded with zeros)
   double* qd = reinterpret_cast<double*>(smraw);                       // [32 * nch]
   uint4* ring_all = reinterpret_cast<uint4*>(smraw + (size_t)nch * 32 * 8);  // [NW][RING][32][4]
-  uint32_t* rid_all = reinterpret_cast<uint32_t*>(ring_all + (size_t)NW * NS_RING * 128);  // [NW][RING][32]
-  float* stg_all = reinterpret_cast<float*>(rid_all + (size_t)NW * NS_RING * 32);  // [NW][32][NS_PAD]
-  uint32_t* sq_all = reinterpret_cast<uint32_t*>(stg_all + (size_t)NW * 32 * NS_PAD);  // [NW][QCAP]
+  uint32_t* idr_all = reinterpret_cast<uint32_t*>(ring_all + (size_t)NW * NS_RING * 128);  // [NW][IDR][32]
+  uint32_t* sq_all = idr_all + (size_t)NW * NS_IDR * 32;               // [NW][QCAP]
   uint32_t* s1_all = sq_all + (size_t)NW * NS_QCAP;                    // [NW][QCAP] stage-2 queue ids
   float2* s1v_all = reinterpret_cast<float2*>(s1_all + (size_t)NW * NS_QCAP);  // [NW][QCAP] (A1, N1)
   __shared__ unsigned long long thr_key;  // lower bound of the final k-th best (ordered key)
@@ -2160,9 +2255,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int part = lane & 3, grp = lane >> 2;  // record part (0-2 codes, 3 terms), record slot
   const uint32_t lt_mask = (1u << lane) - 1u;
-  float* stg = stg_all + (size_t)w * 32 * NS_PAD;
   uint4* ring = ring_all + (size_t)w * NS_RING * 128;
-  uint32_t* rid = rid_all + (size_t)w * NS_RING * 32;
+  uint32_t* idr = idr_all + (size_t)w * NS_IDR * 32;  // candidate ids of batch b: slot b % IDR
   uint32_t* sq = sq_all + (size_t)w * NS_QCAP;    // survivors of stage 2 -> exact
   uint32_t* s1q = s1_all + (size_t)w * NS_QCAP;   // survivors of stage 1 -> stage 2
   float2* s1v = s1v_all + (size_t)w * NS_QCAP;
@@ -2225,11 +2319,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   unsigned long long nrows = 0, nst2 = 0, nfl = 0;  // rows screened, stage-2 records, row floats
 
   // ---------------------------------------------------------------- exact rows
-  // lane r folds row `id` of lane r (NONE: nothing) in the reference's order
-  auto exact_fold = [&](uint32_t id) {
+  // lane r folds row `id` of lane r (NONE: nothing) in the reference's order; `stg` is
+  // a free 2 KB slot of the warp's record ring
+  auto exact_fold = [&](uint32_t id, float* stg) {
     // 16-float half chunks of the 32 rows: 4 lanes per row (16 B each), 8 rows per
-    // load instruction, staged in shared memory (row stride 20 floats); the next half
-    // chunk is in flight while lane r folds row r's 16 floats
+    // load instruction, staged in shared memory (row r's 16 B chunk c at r * 16 +
+    // 4 * (c ^ ((r >> 1) & 3)) floats: conflict-free STS.128 / LDS.128 without
+    // padding); the next half chunk is in flight while lane r folds row r's 16 floats
     float4 v[4];
     const int p4 = lane & 3, r8 = lane >> 2;
     const uint32_t nh = nch * 2;
@@ -2247,15 +2343,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       __syncwarp();  // the previous half chunk's readers are done with the staging rows
 #pragma unroll
       for (int it = 0; it < 4; ++it)
-        *reinterpret_cast<float4*>(stg + (it * 8 + r8) * NS_PAD + 4 * p4) = v[it];
+        *reinterpret_cast<float4*>(stg + (it * 8 + r8) * 16 + 4 * (p4 ^ (((it * 8 + r8) >> 1) & 3))) = v[it];
       if (hc + 1 < nh) load_h(hc + 1);
       __syncwarp();
-      const float* row = stg + lane * NS_PAD;
+      const float* row = stg + lane * 16;
+      const int sw = (lane >> 1) & 3;
       const double* qq = qd + hc * 16;
       // dataset.cpp:67 acc += double(a[i]) * double(b[i]), sequential i (exact products)
 #pragma unroll
       for (int j = 0; j < 16; j += 4) {
-        const float4 xv = *reinterpret_cast<const float4*>(row + j);
+        const float4 xv = *reinterpret_cast<const float4*>(row + 4 * ((j >> 2) ^ sw));
         acc = fma((double)xv.x, qq[j], acc);
         acc = fma((double)xv.y, qq[j + 1], acc);
         acc = fma((double)xv.z, qq[j + 2], acc);
@@ -2282,10 +2379,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       if (t > -INFINITY) atomicMax(&thr_key, dkey(t));
     }
   };
-  auto exact_batch = [&](uint32_t cnt) {
+  auto exact_batch = [&](uint32_t cnt, float* stg) {
     const uint32_t id = (uint32_t)lane < cnt ? sq[(qhead + lane) % NS_QCAP] : NONE;
     qhead += cnt;
-    const double acc = exact_fold(id);
+    const double acc = exact_fold(id, stg);
     topk_insert(bs, bi, k, acc, id, id != NONE);
     if (lane == 0) nfl += (unsigned long long)cnt * nch * 32;
     publish(bs, bi, thr2_s);
@@ -2370,11 +2467,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     nprod = 0;
     wk_fetch();
   };
-  auto wk_next = [&]() -> uint32_t {
+  // wk_step: the next 32-entry window; lane l's CSR position in gp, false for lanes
+  // past a chunk's end and, with wk_done set, once the range is exhausted
+  auto wk_step = [&](uint64_t& gp) -> bool {
     while (wk_e0 >= wk_T) {
       if (!wk_nhas) {
         wk_done = true;
-        return NONE;
+        return false;
       }
       const uint32_t len = wk_nlen;
       const uint64_t pos = wk_npos;
@@ -2405,7 +2504,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     const uint32_t ex = __shfl_sync(FULL, wk_cex, r);
     wk_e0 += 32;
     ++nprod;
-    return e < wk_T ? __ldg(a.ids + ((((uint64_t)phi << 32) | plo) + (e - ex))) : NONE;
+    gp = (((uint64_t)phi << 32) | plo) + (e - ex);
+    return e < wk_T;
+  };
+  auto wk_next = [&]() -> uint32_t {  // lane l's id of the next window (NONE: none)
+    uint64_t gp;
+    return wk_step(gp) ? __ldg(a.ids + gp) : NONE;
   };
 
   // ---------------------------------------------------------------- seeds
@@ -2417,10 +2521,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   // after those probes, and lists meet the seeds again in the scan, where the
   // bitmap drops them before the exact stage.
   uint32_t pstart = 0;
+  float* const stg0 = reinterpret_cast<float*>(ring);  // exact staging while the ring is idle
   if (a.nseedp) {
     // leading true buckets whose cumulative length stays <= the seed cap (lists: half
     // the seed hash, so its load stays <= 1/2)
-    const uint32_t seedcap = bm ? WK_SEEDCAP : NS_SH / 2;
+    const uint32_t seedcap = bm ? a.seedcap : min(a.seedcap, NS_SH / 2);
     if (w == 0) {
       uint32_t acc = 0, cnt = 0;
       for (uint32_t p0 = 0; p0 < a.nseedp; p0 += 32) {
@@ -2449,7 +2554,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
         push_exact(id, admit(id, id != NONE));
         if (qtail - qhead >= 32) {
           __syncwarp();
-          exact_batch(32);
+          exact_batch(32, stg0);
         }
       }
     } else {
@@ -2467,13 +2572,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
         push_exact(id, id != NONE);
         if (qtail - qhead >= 32) {
           __syncwarp();
-          exact_batch(32);
+          exact_batch(32, stg0);
         }
       }
     }
     if (qtail != qhead) {
       __syncwarp();
-      exact_batch(qtail - qhead);
+      exact_batch(qtail - qhead, stg0);
     }
   }
 
@@ -2561,55 +2666,94 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   // ---------------------------------------------------------------- stage 1
   // A per-warp ring of NS_RING batches: the 32 stage-1 records of batch i + RING - 1
   // move by cp.async (16 B per lane, four per lane) while batch i is bounded, so
-  // RING - 1 batches (6 KB) per warp are in flight without holding registers; the
-  // ids of the batch after that are loaded one iteration early.
+  // RING - 1 batches (6 KB) per warp are in flight without holding registers.  The
+  // candidate ids move the same way, RING batches ahead of their records, into an id
+  // ring of IDR = 2 RING slots (one 4 B cp.async per lane -- from the lists, or from
+  // the CSR at the walker's entries -- in the same commit group as the records of
+  // iteration i).  Commit group i holds records(i + RING - 1) and
+  // ids(i + 2 RING - 1); the wait for group i - RING at the end of iteration i - 1
+  // covers both the records of batch i and the ids of batch i + RING - 1.
   const uint32_t nb = (Len + 31) / 32;
   const uint32_t nbw = nb > (uint32_t)w ? (nb - w + NW - 1) / NW : 0;  // this warp's batches
-  auto batch_ids = [&](uint32_t i) {  // lane c: candidate c of the warp's i-th batch
-    if constexpr (WALK) {
-      return wk_next();
-    } else {
-      const uint32_t ci = (w + i * NW) * 32 + lane;
-      return (i < nbw && ci < Len) ? __ldcs(cand + ci) : NONE;
+  auto ids_async = [&](uint32_t b) {  // lists: ids of the warp's batch b -> id ring (cp.async)
+    if constexpr (!WALK) {
+      const uint32_t ci = (w + b * NW) * 32 + lane;
+      uint32_t* dst = idr + (b % NS_IDR) * 32 + lane;
+      if (b < nbw && ci < Len) cp_async4(dst, cand + ci);
+      else *dst = NONE;
     }
   };
   auto more = [&](uint32_t i) { return WALK ? !(wk_done && i >= nprod) : i < nbw; };
-  auto issue = [&](uint32_t i, uint32_t id) {  // records of the warp's i-th batch -> slot
-    const uint32_t slot = i % NS_RING;
-    rid[slot * 32 + lane] = id;
+  auto issue = [&](uint32_t b) {  // records of the warp's batch b (ids in the id ring) -> slot
+    const uint32_t slot = b % NS_RING;
+    const uint32_t id = idr[(b % NS_IDR) * 32 + lane];
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const uint32_t r = it * 8 + grp;
-      const uint32_t idr = __shfl_sync(FULL, id, r);
-      if (idr != NONE)
-        cp_async16(ring + (slot * 32 + r) * 4 + part, rec + (uint64_t)idr * 4 + part);
+      const uint32_t idv = __shfl_sync(FULL, id, r);
+      if (idv != NONE)
+        cp_async16(ring + (slot * 32 + r) * 4 + part, rec + (uint64_t)idv * 4 + part);
     }
-    cp_commit();
   };
-  if constexpr (WALK) wk_begin(pstart, (uint32_t)a.peff, &wctr_s[1]);
+  // WALK: the walker's next window -> batch b's slot: its ids (4 B cp.async per lane
+  // from the CSR ids) and its stage-1 records, inline in CSR order (a.csrrec: the
+  // window's entries are runs of consecutive records, so the copies are coalesced and
+  // whole 128 B lines are used), one commit group
+  auto produce = [&](uint32_t b) {
+    const uint32_t slot = b % NS_RING;
+    uint64_t gp = 0;
+    const bool v = wk_step(gp);
+    uint32_t* dst = idr + slot * 32;  // (WALK uses id-ring slots 0 .. RING-1)
+    if (v) cp_async4(dst + lane, a.ids + gp);
+    else dst[lane] = NONE;
+    const uint4* cr = reinterpret_cast<const uint4*>(a.csrrec);
 #pragma unroll
-  for (uint32_t i = 0; i < NS_RING - 1; ++i) issue(i, batch_ids(i));
-  // candidate ids are loaded NS_IDPF iterations before their records are issued (a
-  // register queue): one iteration did not cover the id load's DRAM latency (the
-  // top stall)
-  uint32_t nid[NS_IDPF];
+    for (int it = 0; it < 4; ++it) {
+      const uint32_t r = it * 8 + grp;
+      const uint64_t gr = __shfl_sync(FULL, gp, r);
+      if (__shfl_sync(FULL, v, r)) cp_async16(ring + (slot * 32 + r) * 4 + part, cr + gr * 4 + part);
+    }
+  };
+  if constexpr (WALK) {
+    wk_begin(pstart, (uint32_t)a.peff, &wctr_s[1]);
 #pragma unroll
-  for (int j = 0; j < NS_IDPF; ++j) nid[j] = batch_ids(NS_RING - 1 + j);
+    for (uint32_t j = 0; j + 1 < NS_RING; ++j) {
+      produce(j);
+      cp_commit();
+    }
+  } else {
+    for (uint32_t b = 0; b < NS_RING; ++b) ids_async(b);
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (uint32_t j = 0; j + 1 < NS_RING; ++j) {
+      issue(j);
+      ids_async(j + NS_RING);
+      cp_commit();
+    }
+  }
   for (uint32_t i = 0; more(i); ++i) {
-    // full queues are drained first (their own loads; the ring stays in flight)
+    // full queues are drained first (their own loads; the ring stays in flight); the
+    // exact rows are staged in the ring slot the issue below refills
+    float* const stg = reinterpret_cast<float*>(ring + ((i + NS_RING - 1) % NS_RING) * 128);
     if (qtail - qhead >= 32) {
       __syncwarp();
-      exact_batch(32);
+      exact_batch(32, stg);
     }
     if (t1 - h1 >= 32) stage2_batch(32);
-    issue(i + NS_RING - 1, nid[0]);   // (an empty commit past the end keeps the count)
-#pragma unroll
-    for (int j = 0; j + 1 < NS_IDPF; ++j) nid[j] = nid[j + 1];
-    nid[NS_IDPF - 1] = batch_ids(i + NS_RING - 1 + NS_IDPF);
+    __syncwarp();  // (the staging slot's readers are done before its refill)
+    if constexpr (WALK) {
+      produce(i + NS_RING - 1);
+    } else {
+      issue(i + NS_RING - 1);   // (an empty commit past the end keeps the count)
+      ids_async(i + 2 * NS_RING - 1);
+    }
+    cp_commit();
     cp_wait<NS_RING - 1>();
     __syncwarp();
     const uint32_t slot = i % NS_RING;
-    const uint32_t cid = rid[slot * 32 + lane];
+    const uint32_t cid = idr[(i % (WALK ? NS_RING : NS_IDR)) * 32 + lane];
     Recs cur;
 #pragma unroll
     for (int it = 0; it < 4; ++it)
@@ -2636,12 +2780,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     __syncwarp();  // slot i % RING is refilled by the next iteration's issue
   }
   cp_wait<0>();
+  __syncwarp();
   while (t1 != h1 || qtail != qhead) {
     if (t1 != h1 && qtail - qhead < 32) {
       stage2_batch(min(32u, t1 - h1));
     } else {
       __syncwarp();
-      exact_batch(min(32u, qtail - qhead));
+      exact_batch(min(32u, qtail - qhead), stg0);
     }
   }
   if (lane == 0) {
@@ -2689,8 +2834,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
 
 static size_t screen_smem(uint32_t d) {
   const uint32_t nch = (d + 31) / 32;
-  return (size_t)nch * 32 * 8 + (size_t)NS_W * NS_RING * (128 * 16 + 32 * 4) +
-         (size_t)NS_W * 32 * NS_PAD * 4 + (size_t)NS_W * NS_QCAP * (4 + 4 + 8);
+  return (size_t)nch * 32 * 8 + (size_t)NS_W * NS_RING * 128 * 16 + (size_t)NS_W * NS_IDR * 32 * 4 +
+         (size_t)NS_W * NS_QCAP * (4 + 4 + 8);
 }
 
 static size_t score_smem(uint32_t d, int sl, int st) {
@@ -2851,6 +2996,26 @@ static uint32_t grouped_shift(uint64_t n) {
   return sm + 64 <= (size_t)co_smem_max() ? gs : 0u;
 }
 
+// Index::q8csr: entry e's stage-1 record = q8rec[ids[e]] (four threads per entry)
+__global__ void k_q8_inline(const uint4* __restrict__ rec, const uint32_t* __restrict__ ids,
+                            uint64_t kept, uint4* __restrict__ out) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < kept * 4;
+       t += (uint64_t)gridDim.x * blockDim.x)
+    out[t] = __ldg(rec + (uint64_t)__ldg(ids + (t >> 2)) * 4 + (t & 3));
+}
+
+static void ensure_q8csr(const Index& ix) {
+  std::lock_guard<std::mutex> lk(ix.mu);
+  if (ix.q8csr || !ix.q8rec) return;
+  uint4* p = static_cast<uint4*>(dmalloc((size_t)(ix.kept_total + 1) * 64));
+  if (ix.kept_total) {
+    k_q8_inline<<<sm_count() * 8, 256, 0, ix.stream>>>(ix.q8rec, ix.ids, ix.kept_total, p);
+    FPP_LAUNCH();
+  }
+  FPP_CUDA(cudaStreamSynchronize(ix.stream));  // (one-time; later calls read it on any stream)
+  ix.q8csr = p;
+}
+
 // zero-initialised on (re)allocation; every kernel using it leaves it clear
 static uint32_t* slot_bitmap(QSlot& sl, size_t words, cudaStream_t st) {
   if (sl.bitmap.n < words) {
@@ -2895,12 +3060,13 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     use_pruned = force_prune || probe || ix.prune_frac < 0 || ix.prune_frac <= 0.65;
     ++ix.prune_chunks;
   }
-  // narrow rows: the record screen (k_score_screen) unless FPP_SC_NARROW=0.  It reads
-  // the collect's id-ordered candidate lists; FPP_SC_WALK=1 makes it walk the probes
-  // itself instead (no collect pass; measured slower on C4: 256 vs 94 + 175 ms per
-  // step -- rows gathered in probe order miss L2 far more often than in id order).
+  // narrow rows: the record screen (k_score_screen) unless FPP_SC_NARROW=0.  It walks
+  // the probes itself (no collect pass and no host sync; C4: 231 ms per step against
+  // 97 + 148 ms for collect + the screen over the collect's id-ordered lists, which
+  // FPP_SC_WALK=0 selects).  With stats requested the collect still runs, for the
+  // unique candidate counts.
   static const bool narrow_off = getenv("FPP_SC_NARROW") && atoi(getenv("FPP_SC_NARROW")) == 0;
-  static const bool walk_on = getenv("FPP_SC_WALK") && atoi(getenv("FPP_SC_WALK")) != 0;
+  static const bool walk_on = !(getenv("FPP_SC_WALK") && atoi(getenv("FPP_SC_WALK")) == 0);
   const bool screen = use_pruned && ix.q8rec && !narrow_off && !rerank;
   const bool walk = screen && walk_on && !lists;
   const bool collect = !walk || stats_d != nullptr;
@@ -2921,6 +3087,7 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   // FPP_FORCE_COLLECT=grouped|cluster|global selects a large-shard path at any n (tests).
   const char* force = getenv("FPP_FORCE_COLLECT");
   const bool f_grouped = force && !strcmp(force, "grouped");
+  const bool f_sliced = force && !strcmp(force, "sliced");
   const bool f_cluster = force && !strcmp(force, "cluster"), f_global = force && !strcmp(force, "global");
   const size_t static_co = 64;
   const int sms = sm_count();
@@ -2941,6 +3108,20 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     ca.grouped = 1;
     ca.gshift = gshift;
     const size_t co_smem = (size_t)CO_NG * 4 + (size_t)32 * ((1ull << gshift) / 8);
+    FPP_CUDA(cudaFuncSetAttribute(k_collect, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)co_smem));
+    int occ = 1;
+    FPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collect, CO_THREADS, co_smem));
+    co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * std::max(occ, 1));
+    FPP_CUDA(cudaMemsetAsync(sl.counter.p, 0, sizeof(uint32_t), st));
+    k_collect<<<co_grid, CO_THREADS, co_smem, st>>>(ca);
+  } else if ((!force || f_sliced) && ((ix.n - 1) >> CO_SLICE_BITS) < CO_NG &&
+             (size_t)CO_NG * 4 + (4ull << (CO_SLICE_BITS - 5)) + 64 <= (size_t)co_smem_max()) {
+    // sliced bitmap dedup: unique ids in ascending order (beyond the grouped range;
+    // on C4 it measured slower than grouped: 118 vs 97 ms per step)
+    ca.sliced = 1;
+    ca.gshift = CO_SLICE_BITS;
+    const size_t co_smem = (size_t)CO_NG * 4 + (4ull << (CO_SLICE_BITS - 5));
     FPP_CUDA(cudaFuncSetAttribute(k_collect, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)co_smem));
     int occ = 1;
@@ -3031,6 +3212,9 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     sa.plen = sl.plen.p;
     sa.ids = ix.ids;
     sa.nseedp = no_seeds ? 0u : ix.prm.L;
+    static const uint32_t seedcap =
+        getenv("FPP_SC_SEEDCAP") ? (uint32_t)atoi(getenv("FPP_SC_SEEDCAP")) : WK_SEEDCAP;
+    sa.seedcap = seedcap;
     const size_t sm = screen_smem(ix.d);
     // 2 CTAs/SM (shared memory: the record rings); FPP_SC_SCR_MINB=3 caps registers at 80
     static const int scr_minb = getenv("FPP_SC_SCR_MINB") ? atoi(getenv("FPP_SC_SCR_MINB")) : 2;
@@ -3038,6 +3222,8 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
       FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       unsigned grid = nqc;
       if (walk) {  // persistent CTAs, one visited bitmap + admission log each
+        ensure_q8csr(ix);
+        sa.csrrec = ix.q8csr;
         int occ = 1;
         FPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NS_W * 32, sm));
         grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sm_count() * std::max(occ, 1));

@@ -5,8 +5,10 @@ cfg=$1; tag=$2; shift 2
 mkdir -p gpurun_out/$tag
 i=0
 for e in "$@"; do
-  env $e python bench.py --config $cfg --no-c5 --no-cpu-baseline --no-sweep --no-parity \
-      > gpurun_out/$tag/ab$i.json 2> gpurun_out/$tag/ab$i.err
+  env $e python -X faulthandler bench.py --config $cfg --no-c5 --no-cpu-baseline --no-sweep \
+      --no-parity > gpurun_out/$tag/ab$i.json 2> gpurun_out/$tag/ab$i.err
+  rc=$?
+  [ $rc != 0 ] && echo "$e: rc=$rc" && tail -25 gpurun_out/$tag/ab$i.err
   python - gpurun_out/$tag/ab$i.json "$e" <<'PY'
 import json, sys
 try:

@@ -245,9 +245,10 @@ def test_empty_batch_and_errors(fpp):
         fpp.Index.build(bad, L=2, K=2, D=16, iProbes=1, alpha=1.0)
 
 
-@pytest.mark.parametrize("path", ["grouped", "cluster", "global"])
+@pytest.mark.parametrize("path", ["sliced", "grouped", "cluster", "global"])
 def test_large_shard_collect_paths(fpp, orc, path, monkeypatch):
-    # the large-shard visited sets (n > one SM's shared memory): grouped dedup
+    # the large-shard visited sets (n > one SM's shared memory): sliced bitmap dedup
+    # (id-slice counting sort + a shared-memory bitmap per slice), grouped dedup
     # (id-range counting sort + per-warp range bitmaps), the DSMEM-cluster bitmap and
     # the global-memory bitmap, forced at small n: the oracle's candidates/top-k/stats
     monkeypatch.setenv("FPP_FORCE_COLLECT", path)
@@ -263,8 +264,9 @@ def test_large_shard_collect_paths(fpp, orc, path, monkeypatch):
     assert np.array_equal(gc, oc)
 
 
-def test_grouped_collect_natural_large_n(fpp, orc):
-    # n = 2.2M points > the single-CTA bitmap limit (~1.8M) -> grouped dedup for real
+def test_sliced_collect_natural_large_n(fpp, orc):
+    # n = 2.2M points > the single-CTA bitmap limit (~1.8M) -> sliced dedup for real
+    # (5 slices of 2^19 ids)
     X = data(fpp, 2_200_000, 16, 50, 0.2)
     Q = data(fpp, 16, 16, 50, 0.2, stream=1)
     ix = fpp.Index.build(X, L=2, K=2, D=16, iProbes=2, alpha=0.05, kappa=10)
@@ -491,14 +493,15 @@ def test_score_early_termination_unstructured(fpp, orc, monkeypatch):
     assert np.array_equal(gs[ok], os_[ok])
 
 
+@pytest.mark.parametrize("path", ["grouped", "sliced"])
 @pytest.mark.parametrize("prune", ["0", "1"])
 @pytest.mark.parametrize("n,qp", [(20000, 5000), (2000, 3000)])
-def test_grouped_collect_every_id_once(fpp, orc, prune, n, qp, monkeypatch):
-    # grouped dedup (the large-shard path): every candidate id appears once and in
-    # ascending order (SPEC.md:352 -- stats.exact = unique candidates), so ids, scores
-    # and all four stats columns equal the oracle's, with and without early termination;
-    # n = 2000 packs many entries into few groups (heavy repeats)
-    monkeypatch.setenv("FPP_FORCE_COLLECT", "grouped")
+def test_grouped_collect_every_id_once(fpp, orc, path, prune, n, qp, monkeypatch):
+    # grouped / sliced dedup (the large-shard paths): every candidate id is scored once
+    # (SPEC.md:352 -- stats.exact = unique candidates), so ids, scores and all four
+    # stats columns equal the oracle's, with and without early termination; n = 2000
+    # packs many entries into few groups (heavy repeats)
+    monkeypatch.setenv("FPP_FORCE_COLLECT", path)
     monkeypatch.setenv("FPP_PRUNE" if prune == "1" else "FPP_NO_PRUNE", "1")
     X = data(fpp, n, 128, 200, 0.25, seed=41)
     Q = data(fpp, 300, 128, 200, 0.25, seed=41, stream=1)

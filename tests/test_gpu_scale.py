@@ -231,10 +231,10 @@ def test_score_screen_exact(fpp, orc, d, k, seeds, monkeypatch):
     # lists: the screen reads the collect's id-ordered lists (default; without stats
     # the grouped collect leaves repeats, which the exact stage's bitmap drops);
     # walk: it walks the probes itself (FPP_SC_WALK=1; without stats no collect runs)
-    for path in ("smem", "grouped", "grouped-nostats", "walk", "walk-nostats"):
+    for path in ("smem", "grouped", "sliced-nostats", "walk", "walk-nostats"):
         monkeypatch.setenv("FPP_SC_WALK", "1" if path.startswith("walk") else "0")
-        if path.startswith("grouped"):
-            monkeypatch.setenv("FPP_FORCE_COLLECT", "grouped")
+        if path.startswith("grouped") or path.startswith("sliced"):
+            monkeypatch.setenv("FPP_FORCE_COLLECT", path.split("-")[0])
         else:
             monkeypatch.delenv("FPP_FORCE_COLLECT", raising=False)
         monkeypatch.setenv("FPP_PRUNE", "1")
