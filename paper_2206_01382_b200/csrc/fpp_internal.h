@@ -175,7 +175,7 @@ struct QueryCtx {
   DBuf<double> ord_sc;
   DBuf<fpp_query_stats> ord_st;
   // k_score_pruned read-fraction probe (async readback into the index policy)
-  unsigned long long* prune_h = nullptr;  // pinned [2]: rows, row slices read
+  unsigned long long* prune_h = nullptr;  // pinned [4]: rows, row floats read, stage-2, exact rows
   DBuf<unsigned long long> prune_d;
   cudaEvent_t prune_ev = nullptr;
   bool prune_pending = false;

@@ -2203,7 +2203,9 @@ constexpr uint32_t NS_QCAP = 64;   // survivor queue per warp (<= 31 + 32 queued
 #endif
 constexpr int NS_RING = FPP_NS_RING;  // stage-1 record ring depth per warp (cp.async)
 constexpr int NS_IDR = 2 * NS_RING;   // candidate-id ring depth per warp
-constexpr uint32_t NS_SH_BITS = 11, NS_SH = 1u << NS_SH_BITS;  // seed id hash (lists)
+constexpr uint32_t NS_SH_BITS = 12, NS_SH = 1u << NS_SH_BITS;  // seed id hash (lists) /
+                                                                // admission hash (WALK)
+constexpr int WK_HPROBE = 32;  // admission hash: probes before the bitmap takes an id
 
 __device__ __forceinline__ unsigned long long dkey(double x) {  // order-preserving
   const unsigned long long b = (unsigned long long)__double_as_longlong(x);
@@ -2388,8 +2390,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     publish(bs, bi, thr2_s);
   };
   // admission to the exact stage (lanes with `want`): true for an id not scored exactly
-  // before in this query.  WALK: a test-and-set in the CTA's visited bitmap (logged
-  // for the clear).
+  // before in this query.  WALK: a shared-memory hash of the admitted ids, backed by a
+  // test-and-set in the CTA's visited bitmap for the ids the hash cannot hold.
   // Lists (deduplicated by the collect) meet only the seeds again: an id found in the
   // seed hash is not admitted (the seeds are scored from the hash itself).
   auto hslot = [](uint32_t id) { return (id * 2654435761u) >> (32 - NS_SH_BITS); };
@@ -2410,16 +2412,33 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   auto admit = [&](uint32_t id, bool want) {
     bool fresh = false;
     if (bm) {  // WALK: lists repeat ids
+      // first the shared-memory hash (a CAS on the first empty slot of the id's probe
+      // sequence; slots only fill, so an id whose sequence is full of other ids can
+      // never enter later either): 1 = inserted, 0 = present; ids with a full
+      // sequence (-1) take the visited bitmap, whose set bits are logged
+      int res = -1;
       if (want) {
-        const uint32_t bit = 1u << (id & 31);
-        fresh = !(atomicOr(bm + (id >> 5), bit) & bit);
+        uint32_t h = hslot(id);
+        for (int t = 0; t < WK_HPROBE; ++t, h = (h + 1) & (NS_SH - 1)) {
+          const uint32_t old = atomicCAS(&seedh[h], NONE, id);
+          if (old == NONE || old == id) {
+            res = old == NONE;
+            break;
+          }
+        }
       }
-      const uint32_t bal = __ballot_sync(FULL, fresh);
+      bool viab = false;
+      if (want && res < 0) {
+        const uint32_t bit = 1u << (id & 31);
+        viab = !(atomicOr(bm + (id >> 5), bit) & bit);
+      }
+      fresh = res == 1 || viab;
+      const uint32_t bal = __ballot_sync(FULL, viab);
       if (bal) {
         uint32_t base = 0;
         if (lane == 0) base = atomicAdd(&logn_s, (uint32_t)__popc(bal));
         base = __shfl_sync(FULL, base, 0) + __popc(bal & lt_mask);
-        if (fresh && base < a.logcap) wlog[base] = id;
+        if (viab && base < a.logcap) wlog[base] = id;
       }
     } else {
       fresh = want && !seed_has(id);
@@ -2796,6 +2815,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     if (a.dbg) {  // read fraction in row floats: a record counts as 16 floats
       atomicAdd(a.dbg, nrows);
       atomicAdd(a.dbg + 1, (nrows + nst2) * 16ull + nfl);
+      atomicAdd(a.dbg + 2, nst2);
+      atomicAdd(a.dbg + 3, nfl / (nch * 32));
     }
   }
   // CTA merge of the warp lists
@@ -3199,11 +3220,11 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     sa.n = ix.n;
     if (probe) {
       if (!cx.prune_h) {
-        FPP_CUDA(cudaMallocHost(&cx.prune_h, 16));
+        FPP_CUDA(cudaMallocHost(&cx.prune_h, 32));
         FPP_CUDA(cudaEventCreateWithFlags(&cx.prune_ev, cudaEventDisableTiming));
-        cx.prune_d.alloc(2);
+        cx.prune_d.alloc(4);
       }
-      FPP_CUDA(cudaMemsetAsync(cx.prune_d.p, 0, 16, st));
+      FPP_CUDA(cudaMemsetAsync(cx.prune_d.p, 0, 32, st));
       sa.dbg = cx.prune_d.p;
     }
     // seeds: the true buckets (the first L probes); FPP_SC_SEEDS=0 disables
@@ -3245,14 +3266,16 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
       else launch_scr(k_score_screen<NS_W, 3, false>);
     }
     if (probe) {
-      FPP_CUDA(cudaMemcpyAsync(cx.prune_h, cx.prune_d.p, 16, cudaMemcpyDeviceToHost, st));
+      FPP_CUDA(cudaMemcpyAsync(cx.prune_h, cx.prune_d.p, 32, cudaMemcpyDeviceToHost, st));
       FPP_CUDA(cudaEventRecord(cx.prune_ev, st));
       cx.prune_pending = true;
       if (dbg) {
         FPP_CUDA(cudaEventSynchronize(cx.prune_ev));
         const unsigned long long* h = cx.prune_h;
-        fprintf(stderr, "[prune dbg] screen: rows %llu, floats read per row %.1f of %u (%.1f%% of row bytes)\n",
-                h[0], h[0] ? (double)h[1] / h[0] : 0.0, ix.d, h[0] ? 100.0 * h[1] / h[0] / ix.d : 0.0);
+        fprintf(stderr, "[prune dbg] screen: rows %llu, floats read per row %.1f of %u (%.1f%% of row bytes); "
+                "stage-2 records %llu (%.2f%%), exact rows %llu (%.2f%%)\n",
+                h[0], h[0] ? (double)h[1] / h[0] : 0.0, ix.d, h[0] ? 100.0 * h[1] / h[0] / ix.d : 0.0,
+                h[2], h[0] ? 100.0 * h[2] / h[0] : 0.0, h[3], h[0] ? 100.0 * h[3] / h[0] : 0.0);
       }
     }
   } else if (use_pruned) {
@@ -3262,11 +3285,11 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     sa.n = ix.n;
     if (probe) {
       if (!cx.prune_h) {
-        FPP_CUDA(cudaMallocHost(&cx.prune_h, 16));
+        FPP_CUDA(cudaMallocHost(&cx.prune_h, 32));
         FPP_CUDA(cudaEventCreateWithFlags(&cx.prune_ev, cudaEventDisableTiming));
-        cx.prune_d.alloc(2);
+        cx.prune_d.alloc(4);
       }
-      FPP_CUDA(cudaMemsetAsync(cx.prune_d.p, 0, 16, st));
+      FPP_CUDA(cudaMemsetAsync(cx.prune_d.p, 0, 32, st));
       sa.dbg = cx.prune_d.p;
     }
     // ring geometry (FPP_SC_PR = NW,ST,MINB digits; default 4 warps x 2 stages, 3 CTAs/SM:
@@ -3305,7 +3328,7 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     }
 #undef FPP_PR_CASE
     if (probe) {
-      FPP_CUDA(cudaMemcpyAsync(cx.prune_h, cx.prune_d.p, 16, cudaMemcpyDeviceToHost, st));
+      FPP_CUDA(cudaMemcpyAsync(cx.prune_h, cx.prune_d.p, 32, cudaMemcpyDeviceToHost, st));
       FPP_CUDA(cudaEventRecord(cx.prune_ev, st));
       cx.prune_pending = true;
       if (dbg) {
