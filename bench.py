@@ -690,12 +690,17 @@ def run_query_bench(args, cfg, qprobes):
             "algorithmic_bytes_per_launch": score_bytes_full / score_launches,
             "algorithmic_gbs": score_bytes_full / score_launches / launch_s / 1e9}
     if tr:
-        roof.update(achieved=tr["dram_bytes_per_launch"] / launch_s / 1e9,
-                    traffic=tr["dram_bytes_per_launch"],
-                    frac=tr["dram_bytes_per_launch"] / launch_s / 1e9 / hbm,
-                    frac_basis="ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
-                               f"({tr.get('source', 'profiles/dram_traffic.json')}) / CUDA-event "
-                               "launch time (this run) / measured HBM peak")
+        # the captured launch's DRAM bytes per query, times this run's queries per launch
+        # (chunks differ in size), over this run's CUDA-event launch time
+        per_q = tr["dram_bytes_per_launch"] / tr.get("queries_per_launch", 8192)
+        bytes_launch = per_q * nq / score_launches
+        roof.update(achieved=bytes_launch / launch_s / 1e9,
+                    traffic=bytes_launch, traffic_per_query=per_q,
+                    frac=bytes_launch / launch_s / 1e9 / hbm,
+                    frac_basis="ncu dram__bytes_read.sum + dram__bytes_write.sum per query of the "
+                               f"captured launch ({tr.get('source', 'profiles/dram_traffic.json')}) "
+                               "x queries per launch / CUDA-event launch time (this run) / measured "
+                               "HBM peak")
     else:
         roof.update(achieved=roof["requested_gbs"], traffic=None, frac=roof["requested_frac"],
                     frac_basis="requested row bytes (no ncu DRAM capture for this config/qProbes "

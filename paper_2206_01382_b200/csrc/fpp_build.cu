@@ -30,6 +30,36 @@ namespace fpp {
 // ------------------------------------------------------------------ K1 build
 constexpr int HB_SEL = 32;  // keys sorted after the threshold preselection
 
+// Rank pairs (a, b) with (a + 1)(b + 1) <= R: the only candidates for the top ip <= R
+// pairs (every pair with a' <= a, b' <= b strictly precedes (a, b)); D(R) = sum_a
+// floor(R / (a + 1)) of them (8, 20, 50 for R = 4, 8, 16) instead of R^2 slots.
+template <int R>
+struct PairList {
+  static constexpr int N = [] {
+    int n = 0;
+    for (int a = 0; a < R; ++a) n += R / (a + 1);
+    return n;
+  }();
+  uint16_t ab[N];  // a << 8 | b
+};
+template <int R>
+constexpr PairList<R> make_pairs() {
+  PairList<R> p{};
+  int i = 0;
+  for (int a = 0; a < R; ++a)
+    for (int b = 0; b < R / (a + 1); ++b) p.ab[i++] = (uint16_t)(a << 8 | b);
+  return p;
+}
+__constant__ PairList<4> c_pairs4 = make_pairs<4>();
+__constant__ PairList<8> c_pairs8 = make_pairs<8>();
+__constant__ PairList<16> c_pairs16 = make_pairs<16>();
+template <int R>
+__device__ __forceinline__ uint32_t pair_ab(int i) {
+  if constexpr (R == 4) return c_pairs4.ab[i];
+  else if constexpr (R == 8) return c_pairs8.ab[i];
+  else return c_pairs16.ab[i];
+}
+
 // k_hash_build shared memory: NGRP transpose buffers (TS >= P floats, reused
 // for the v dump of the preselection) + per group HB_SEL scratch keys and the
 // two sorted top-R lists
@@ -169,7 +199,10 @@ __device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], in
 }
 
 template <int P, int R>
-__global__ void __launch_bounds__(256, 3)
+#ifndef FPP_HB_MINB
+#define FPP_HB_MINB 3
+#endif
+__global__ void __launch_bounds__(256, FPP_HB_MINB)
 k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx, uint32_t D,
              uint32_t K,
              const uint32_t* __restrict__ signs, uint32_t t0, uint32_t T, uint32_t ip,
@@ -197,8 +230,8 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx, 
   const uint32_t r = ip < D ? ip : D;  // ranks needed per function (host ensures <= R)
   const uint32_t twoD = 2 * D;
   // candidate pairs: (a+1)(b+1) <= ip (every pair with a' <= a, b' <= b strictly
-  // precedes (a, b), so no other pair can be among the top ip)
-  constexpr int NPL = (R * R + S::G - 1) / S::G;
+  // precedes (a, b), so no other pair can be among the top ip): PairList<R>
+  constexpr int NPL = (PairList<R>::N + S::G - 1) / S::G;
   for (uint32_t tt = 0; tt < T; ++tt) {
     const uint32_t t = t0 + tt;
 #pragma unroll 1
@@ -233,9 +266,10 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx, 
 #pragma unroll
     for (int k = 0; k < NPL; ++k) {
       const uint32_t pi = (uint32_t)g + (uint32_t)k * S::G;
-      const uint32_t a = pi / R, b = pi % R;
+      const uint32_t ab = pi < (uint32_t)PairList<R>::N ? pair_ab<R>((int)pi) : 0xffffu;
+      const uint32_t a = ab >> 8, b = ab & 0xffu;
       pk[k] = 0;
-      if (pi < (uint32_t)(R * R) && a < r && b < r && (a + 1) * (b + 1) <= ip) {
+      if (pi < (uint32_t)PairList<R>::N && a < r && b < r && (a + 1) * (b + 1) <= ip) {
         const float sc = rank_val(sel0[a]) + rank_val(sel1[b]);
         pk[k] = ((uint64_t)ord_key(sc) << 32) | ((uint64_t)(0xffffu - a) << 16) | (0xffffu - b);
       }

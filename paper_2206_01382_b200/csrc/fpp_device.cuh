@@ -95,6 +95,48 @@ __device__ __forceinline__ void spinner_project(float (&v)[FhtShape<P>::EPT], co
   for (int e = 0; e < S::EPT; ++e) v[e] = v[e] * scale;
 }
 
+// ------------------------------------------------- packed FP32 butterflies
+// Two butterflies in one FADD2 pair (add/sub.rn.f32x2, sm_100a): (a0, a1) <- (a0 + b0,
+// a1 + b1) and (b0, b1) <- (a0 - b0, a1 - b1).  Each lane of the packed op is the IEEE
+// round-to-nearest add / subtract of the scalar code (same operands, same order), so
+// results are bit-identical; the FP32 instruction count of the FHT halves.
+__device__ __forceinline__ void bfly2(float& a0, float& a1, float& b0, float& b1) {
+  asm("{.reg .b64 ra, rb, rs, rd;\n\t"
+      "mov.b64 ra, {%0, %1};\n\tmov.b64 rb, {%2, %3};\n\t"
+      "add.rn.f32x2 rs, ra, rb;\n\tsub.rn.f32x2 rd, ra, rb;\n\t"
+      "mov.b64 {%0, %1}, rs;\n\tmov.b64 {%2, %3}, rd;\n\t}"
+      : "+f"(a0), "+f"(a1), "+f"(b0), "+f"(b1));
+}
+
+// one in-register butterfly stage of stride `len` over 32 registers (reference
+// operand order x + y low, x - y high); strides >= 2 pair neighbouring butterflies
+// (j, j + 1) into one FADD2
+template <int len>
+__device__ __forceinline__ void fht_stage32(float (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 2 * len) {
+    if constexpr (len >= 2) {
+#pragma unroll
+      for (int j = i; j < i + len; j += 2) bfly2(v[j], v[j + 1], v[j + len], v[j + len + 1]);
+    } else {
+      const float x = v[i], y = v[i + 1];
+      v[i] = x + y;
+      v[i + 1] = x - y;
+    }
+  }
+}
+
+// x * s for 32 registers, two per FMUL2 (mul.rn.f32x2: per-lane IEEE products)
+__device__ __forceinline__ void scale32(float (&v)[32], float s) {
+#pragma unroll
+  for (int e = 0; e < 32; e += 2)
+    asm("{.reg .b64 ra, rs, rd;\n\t"
+        "mov.b64 ra, {%0, %1};\n\tmov.b64 rs, {%2, %2};\n\t"
+        "mul.rn.f32x2 rd, ra, rs;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "+f"(v[e]), "+f"(v[e + 1])
+        : "f"(s));
+}
+
 // ------------------------------------------------ transpose FHT (P >= 64)
 // Same butterfly graph as fht_group, but the cross-lane stages run in
 // registers after one shared-memory transpose per round instead of log2(G)
@@ -116,18 +158,11 @@ __device__ __forceinline__ int tpad(int j) { return j + ((j >> 5) << 2); }
 template <int P>
 __device__ __forceinline__ void fht_regs_B(float (&v)[32]) {
   constexpr int G = P / 32;
-#pragma unroll
-  for (int len = 32 / G; len < 32; len <<= 1) {
-#pragma unroll
-    for (int i = 0; i < 32; i += 2 * len) {
-#pragma unroll
-      for (int j = i; j < i + len; ++j) {
-        const float x = v[j], y = v[j + len];
-        v[j] = x + y;
-        v[j + len] = x - y;
-      }
-    }
-  }
+  if constexpr (32 / G <= 1) fht_stage32<1>(v);
+  if constexpr (32 / G <= 2) fht_stage32<2>(v);
+  if constexpr (32 / G <= 4) fht_stage32<4>(v);
+  if constexpr (32 / G <= 8) fht_stage32<8>(v);
+  fht_stage32<16>(v);
 }
 
 // e*G + g stays in the 32-block of e*G (G | 32, g < G), so tpad(e*G + g) =
@@ -179,24 +214,15 @@ __device__ __forceinline__ void spinner_project_T(float (&v)[32], const uint32_t
   for (int stage = 0; stage < 3; ++stage) {
     if (stage) transpose_B_to_A<P>(v, g, buf);
     apply_signs<32>(v, stage == 0 ? w0 : (stage == 1 ? w1 : w2));
-#pragma unroll
-    for (int len = 1; len < 32; len <<= 1) {
-#pragma unroll
-      for (int i = 0; i < 32; i += 2 * len) {
-#pragma unroll
-        for (int j = i; j < i + len; ++j) {
-          const float x = v[j], y = v[j + len];
-          v[j] = x + y;
-          v[j + len] = x - y;
-        }
-      }
-    }
+    fht_stage32<1>(v);
+    fht_stage32<2>(v);
+    fht_stage32<4>(v);
+    fht_stage32<8>(v);
+    fht_stage32<16>(v);
     transpose_A_to_B<P>(v, g, buf);
     fht_regs_B<P>(v);
   }
-  const float scale = 1.0f / (float)P;
-#pragma unroll
-  for (int e = 0; e < 32; ++e) v[e] = v[e] * scale;
+  scale32(v, 1.0f / (float)P);
 }
 
 // Load row x[0..d) into the group layout, zero-padded to P (rotation.cpp:88-89).

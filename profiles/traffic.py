@@ -1,6 +1,7 @@
 """Write the DRAM traffic of the dominant query kernel into profiles/dram_traffic.json.
 
 usage: python profiles/traffic.py <report.ncu-rep> <config> <qprobes> <kernel-substring> <source-note>
+                                  [queries-per-launch (default 8192)]
 
 Reads one `ncu --set full` capture (dram__bytes_read.sum + dram__bytes_write.sum and
 gpu__time_duration.sum of the first launch whose name contains <kernel-substring>) and
@@ -14,6 +15,7 @@ import subprocess
 import sys
 
 rep, config, qprobes, kname, note = sys.argv[1:6]
+qpl = int(sys.argv[6]) if len(sys.argv) > 6 else 8192
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True, check=True).stdout
 rr = list(csv.reader(raw.splitlines()))
@@ -35,6 +37,7 @@ ent = {"qprobes": int(qprobes), "kernel": row[H.index("Kernel Name")][:80],
        "dram_write_bytes": val(row, "dram__bytes_write.sum"),
        "gpu_time_ms": val(row, "gpu__time_duration.sum"),
        "grid": row[H.index("launch__grid_size")],
+       "queries_per_launch": qpl,
        "source": note}
 ent["ncu_gbs"] = ent["dram_bytes_per_launch"] / ent["gpu_time_ms"] / 1e6
 p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "dram_traffic.json")
