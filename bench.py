@@ -628,6 +628,11 @@ def run_query_bench(args, cfg, qprobes):
     merged = {}
 
     def step(qp, stats=None):
+        if world > 1 and not args.replicate_stage_a:
+            # stage A split across the ranks, probe sets all-gathered
+            merged["s"], merged["i"] = fdist.sharded_query(ix, Qd, ids_d, sc_d, K_TOP, qp,
+                                                           stream=stream, stats=stats)
+            return
         ix.query_device(Qd, ids_d, sc_d, K_TOP, qp, stats=stats, stream=stream)
         if world > 1:
             merged["s"], merged["i"] = fdist.allgather_merge(sc_d, ids_d, K_TOP)
@@ -894,6 +899,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--qprobes", type=int, default=0)
+    ap.add_argument("--replicate-stage-a", action="store_true",
+                    help="N>1: every rank hashes and probe-selects the whole batch (the "
+                         "round-1 path) instead of its slice + an all-gather of probe sets")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")

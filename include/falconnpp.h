@@ -30,7 +30,8 @@ extern "C" {
 
 #define FPP_ABI_VERSION 5  /* 2: fpp_query_stats.exact, SimHash rerank; 3: fpp_timings.score_bytes;
                               4: fpp_synth_rows, fpp_merge_topk, per-call query contexts;
-                              5: fpp_timings.score_launches */
+                              5: fpp_timings.score_launches, fpp_query_probe_sets_device,
+                                 fpp_query_from_probe_sets_device */
 
 /* error classes ("one exit code per error class") */
 #define FPP_OK 0
@@ -120,11 +121,26 @@ int fpp_query(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uin
               uint32_t* ids, double* scores, fpp_query_stats* stats);
 /* device-resident variant: Q_dev, ids_dev, scores_dev, stats_dev on the index device;
    stream is a cudaStream_t (NULL = the call context's stream), asynchronous w.r.t.
-   the host except for one small readback per query chunk (the chunk's candidate
-   total, which sizes its candidate buffer). */
+   the host on the walking-screen path (narrow rows, no stats); the collect path
+   (other rows, or stats requested) reads back one small word per query chunk (the
+   chunk's candidate total, which sizes its candidate buffer). */
 int fpp_query_device(const fpp_index* idx, const float* Q_dev, uint64_t nq, uint32_t k,
                      uint32_t qprobes, uint32_t* ids_dev, double* scores_dev,
                      fpp_query_stats* stats_dev, void* stream);
+
+/* Multi-GPU query split.  Stage A alone: the
+   probe sets of nq queries as global bucket ids t * num_buckets + b, probes_dev
+   [nq][fpp_query_probes(qprobes)] u32 in probe order (the L true buckets first).
+   They depend only on the queries and the hash functions (parameters + seed), so a
+   rank computes them for its slice of a batch and every shard resolves them. */
+int fpp_query_probe_sets_device(const fpp_index* idx, const float* Q_dev, uint64_t nq,
+                                uint32_t qprobes, uint32_t* probes_dev, void* stream);
+/* Stage B from such probe sets (computed by any index with the same parameters and
+   seed), resolved in this index's tables: equals fpp_query_device on the same Q. */
+int fpp_query_from_probe_sets_device(const fpp_index* idx, const float* Q_dev, uint64_t nq,
+                                     const uint32_t* probes_dev, uint32_t k, uint32_t qprobes,
+                                     uint32_t* ids_dev, double* scores_dev,
+                                     fpp_query_stats* stats_dev, void* stream);
 
 /* search with a SimHash rerank budget B (SPEC.md:311-314 QueryParams, :330-338
  * simhash_screen): the collected candidates are screened to the B with the most

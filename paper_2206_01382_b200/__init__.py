@@ -139,6 +139,8 @@ SIGNATURES = [
     ("fpp_free", None, [vp]),
     ("fpp_query", C.c_int, [vp, vp, u64, u32, u32, vp, vp, vp]),
     ("fpp_query_device", C.c_int, [vp, vp, u64, u32, u32, vp, vp, vp, vp]),
+    ("fpp_query_probe_sets_device", C.c_int, [vp, vp, u64, u32, vp, vp]),
+    ("fpp_query_from_probe_sets_device", C.c_int, [vp, vp, u64, vp, u32, u32, vp, vp, vp, vp]),
     ("fpp_query_rerank", C.c_int, [vp, vp, u64, u32, u32, u32, vp, vp, vp]),
     ("fpp_query_rerank_device", C.c_int, [vp, vp, u64, u32, u32, u32, vp, vp, vp, vp]),
     ("fpp_signatures", C.c_int, [vp, vp, u64, vp]),
@@ -472,6 +474,46 @@ class Index:
         else:
             _check(lib().fpp_query_device(self._h, C.c_void_p(Q.data_ptr()), nq, k,
                                           qProbes, *args))
+
+    def query_probe_sets_device(self, Q, qProbes: int, probes=None, stream=None):
+        """Stage A alone (multi-GPU split): the probe sets of the
+        queries Q (float32 [nq, d] on the index device) as global bucket ids, int32
+        (uint32 bits) [nq, P_eff] -- resolvable by any shard with the same parameters
+        and seed (query_from_probe_sets_device)."""
+        import torch
+        dev = self.device_obj()
+        _require_tensor(Q, "Q", ("torch.float32",), dev, ndim=2)
+        if Q.shape[1] != self.d:
+            raise FppDimensionError(f"search: query dim {Q.shape[1]} != index dim {self.d}")
+        nq, pe = Q.shape[0], self.peff(qProbes)
+        if probes is None:
+            probes = torch.empty((nq, pe), dtype=torch.int32, device=dev)
+        _require_tensor(probes, "probes", ("torch.int32", "torch.uint32"), dev, shape=(nq, pe))
+        _check(lib().fpp_query_probe_sets_device(self._h, C.c_void_p(Q.data_ptr()), nq, qProbes,
+                                                 C.c_void_p(probes.data_ptr()),
+                                                 C.c_void_p(stream) if stream else None))
+        return probes
+
+    def query_from_probe_sets_device(self, Q, probes, ids, scores, k: int, qProbes: int,
+                                     stats=None, stream=None):
+        """Stage B from probe sets (query_probe_sets_device of any shard) resolved in
+        this index's tables; the same answers as query_device on Q."""
+        dev = self.device_obj()
+        _require_tensor(Q, "Q", ("torch.float32",), dev, ndim=2)
+        if Q.shape[1] != self.d:
+            raise FppDimensionError(f"search: query dim {Q.shape[1]} != index dim {self.d}")
+        nq = Q.shape[0]
+        _require_tensor(probes, "probes", ("torch.int32", "torch.uint32"), dev,
+                        shape=(nq, self.peff(qProbes)))
+        _require_tensor(ids, "ids", ("torch.int32", "torch.uint32"), dev, shape=(nq, k))
+        _require_tensor(scores, "scores", ("torch.float64",), dev, shape=(nq, k))
+        if stats is not None:
+            _require_tensor(stats, "stats", ("torch.int64",), dev, shape=(nq, 4))
+        _check(lib().fpp_query_from_probe_sets_device(
+            self._h, C.c_void_p(Q.data_ptr()), nq, C.c_void_p(probes.data_ptr()), k, qProbes,
+            C.c_void_p(ids.data_ptr()), C.c_void_p(scores.data_ptr()),
+            C.c_void_p(stats.data_ptr()) if stats is not None else None,
+            C.c_void_p(stream) if stream else None))
 
     def device_obj(self):
         import torch

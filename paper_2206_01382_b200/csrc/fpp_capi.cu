@@ -682,6 +682,36 @@ int fpp_query_device(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t
   return guarded([&] { query_dev(idx, Q, nq, k, qprobes, 0, ids, scores, stats, stream); });
 }
 
+int fpp_query_probe_sets_device(const fpp_index* idx, const float* Q, uint64_t nq,
+                                uint32_t qprobes, uint32_t* probes, void* stream) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    if (nq && (!Q || !probes)) fail(FPP_ERR_INVALID_ARGUMENT, "query_probe_sets: NULL buffer");
+    validate_query(ix, nq, 1, qprobes, Q, probes, probes);
+    if (!nq) return;
+    DeviceGuard dg(ix.device);
+    CtxLease cx(ix);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : cx->own;
+    run_query_probes(ix, *cx, Q, nq, qprobes, probes, s);
+  });
+}
+
+int fpp_query_from_probe_sets_device(const fpp_index* idx, const float* Q, uint64_t nq,
+                                     const uint32_t* probes, uint32_t k, uint32_t qprobes,
+                                     uint32_t* ids, double* scores, fpp_query_stats* stats,
+                                     void* stream) {
+  return guarded([&] {
+    const Index& ix = IX(idx);
+    validate_query(ix, nq, k, qprobes, Q, ids, scores);
+    if (nq && !probes) fail(FPP_ERR_INVALID_ARGUMENT, "query_from_probe_sets: NULL probes");
+    if (!nq) return;
+    DeviceGuard dg(ix.device);
+    CtxLease cx(ix);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : cx->own;
+    run_query_from_probes(ix, *cx, Q, nq, probes, k, qprobes, ids, scores, stats, s);
+  });
+}
+
 int fpp_query_rerank(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k,
                      uint32_t qprobes, uint32_t rerank, uint32_t* ids, double* scores,
                      fpp_query_stats* stats) {

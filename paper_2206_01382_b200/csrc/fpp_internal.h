@@ -249,6 +249,11 @@ void run_query(const Index& ix, QueryCtx& cx, const float* Qd, uint64_t nq, uint
 void launch_query_lists(const Index& ix, const float* Qd, uint64_t nq, uint32_t s_cap,
                         float* vals, uint32_t* codes, cudaStream_t s, uint64_t lstride = 0);
 // probes (t*NB+b) and candidates of query 0 of Qd (debug/parity)
+void run_query_probes(const Index& ix, QueryCtx& cx, const float* Qd, uint64_t nq, uint32_t qprobes,
+                  uint32_t* probes_d, cudaStream_t s);
+void run_query_from_probes(const Index& ix, QueryCtx& cx, const float* Qd, uint64_t nq,
+                       const uint32_t* probes_d, uint32_t k, uint32_t qprobes, uint32_t* ids_d,
+                       double* scores_d, fpp_query_stats* stats_d, cudaStream_t s);
 void query_debug(const Index& ix, QueryCtx& cx, const float* qd, uint32_t qprobes,
                  std::vector<uint64_t>& probes, std::vector<uint32_t>& cands);
 // k-way merge of `lists` per-shard top-k lists [lists][nq][k] (each sorted by score

@@ -320,6 +320,8 @@ struct ProbeArgs {
   uint32_t ccap;
   uint32_t beta_q8;       // first T_lo attempt at arm rank beta * m (beta = beta_q8 / 256)
   uint32_t rank_order;    // 1: keep the selection's emission order (no table-major sort)
+  uint32_t* pout;         // != nullptr: write the probes as global bucket ids t * NB + b
+                          // ([nq][peff], no directory reads) instead of (pos, len)
 };
 
 __device__ const float g_zero_row[1] = {0.0f};
@@ -927,9 +929,23 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
     for (int u = 0; u < UR; ++u) {
       const uint32_t t = pr[u] >> 22;
       c1[u] = K == 2 ? c1[u] * twoD + c2[u] : c1[u];  // bucket within table t
-      const uint32_t* of = a.offs + (uint64_t)t * (NB + 1) + c1[u];
-      o0[u] = __ldg(of);
-      o1[u] = __ldg(of + 1);
+      if (!a.pout) {
+        const uint32_t* of = a.offs + (uint64_t)t * (NB + 1) + c1[u];
+        o0[u] = __ldg(of);
+        o1[u] = __ldg(of + 1);
+      }
+    }
+    if (a.pout) {  // probe sets only (multi-GPU split: resolved by each shard)
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        const uint32_t pp = p0 + u * blockDim.x;
+        if (pp < P) {
+          const uint32_t t = pr[u] >> 22;
+          const uint32_t dst = (tmajor && pp >= L) ? atomicAdd(&tcur[t], 1u) : pp;
+          a.pout[(uint64_t)q * a.peff + dst] = t * NB + c1[u];
+        }
+      }
+      continue;
     }
 #pragma unroll
     for (int u = 0; u < UR; ++u) {
@@ -957,6 +973,32 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
       d[11] = refalls;
     }
   }
+}
+
+// Probe sets given as global bucket ids (fpp_query_from_probes: computed by any index
+// with the same parameters and seed, e.g. another shard's) -> this index's CSR
+// (pos, len) and the entries per query; CTA per query.
+__global__ void __launch_bounds__(256) k_resolve_probes(const uint32_t* __restrict__ probes, uint64_t peff,
+                                                        uint64_t NB, const uint32_t* __restrict__ offs,
+                                                        const uint64_t* __restrict__ tbase,
+                                                        uint64_t* __restrict__ ppos,
+                                                        uint32_t* __restrict__ plen,
+                                                        uint32_t* __restrict__ eq) {
+  __shared__ uint64_t red[8];
+  const uint32_t q = blockIdx.x;
+  const uint32_t* pb = probes + (uint64_t)q * peff;
+  uint64_t esum = 0;
+  for (uint64_t p = threadIdx.x; p < peff; p += blockDim.x) {
+    const uint32_t gb = __ldg(pb + p);
+    const uint32_t t = (uint32_t)(gb / NB), b = (uint32_t)(gb - (uint64_t)t * NB);
+    const uint32_t* of = offs + (uint64_t)t * (NB + 1) + b;
+    const uint32_t o0 = __ldg(of), o1 = __ldg(of + 1);
+    ppos[(uint64_t)q * peff + p] = __ldg(tbase + t) + o0;
+    plen[(uint64_t)q * peff + p] = o1 - o0;
+    esum += o1 - o0;
+  }
+  esum = block_sum_u64(esum, red);
+  if (threadIdx.x == 0) eq[q] = (uint32_t)esum;
 }
 
 // exclusive scan of eq[nq] -> coff[nq+1] (single CTA)
@@ -2951,7 +2993,8 @@ static void prepare_slot(const Index& ix, QSlot& sl, uint32_t nqc, uint32_t qpro
 }
 
 static void stage_a(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, uint32_t nqc,
-                    uint32_t qprobes, cudaStream_t st, uint64_t* dbg_probes) {
+                    uint32_t qprobes, cudaStream_t st, uint64_t* dbg_probes,
+                    uint32_t* probes_out = nullptr) {
   const uint32_t L = ix.prm.L, K = ix.prm.K;
   const uint32_t scap = query_cap(ix, qprobes);
   const uint64_t peff = query_probes(ix, qprobes);
@@ -2975,6 +3018,7 @@ static void stage_a(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   pa.beta_q8 = beta_env ? (uint32_t)(atof(beta_env) * 256) : 179u;
   static const bool rank_order = getenv("FPP_PROBE_RANKORDER") != nullptr;
   pa.rank_order = rank_order ? 1u : 0u;
+  pa.pout = probes_out;
   static const bool dbg_probe = getenv("FPP_DEBUG_PROBE") != nullptr;
   if (dbg_probe) {
     sl.dbgclk.ensure((size_t)nqc * 16);
@@ -3500,10 +3544,7 @@ __global__ void __launch_bounds__(1024) k_order_sort(const uint64_t* __restrict_
 // the caller's order; FPP_NO_REORDER=1 keeps the input order.  Results are
 // identical either way (every query is independent).  The context's previous
 // call (possibly on another stream) completes before its scratch is reused.
-void run_query(const Index& ix, QueryCtx& cx, const float* Qd, uint64_t nq, uint32_t k,
-               uint32_t qprobes, uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d,
-               cudaStream_t s, uint32_t rerank) {
-  if (cx.done_recorded) FPP_CUDA(cudaStreamWaitEvent(s, cx.ev_done, 0));
+static void ensure_score_bytes(const Index& ix) {
   if (!ix.score_bytes_d.p) {
     std::lock_guard<std::mutex> lk(ix.mu);
     if (!ix.score_bytes_d.p) {
@@ -3511,6 +3552,61 @@ void run_query(const Index& ix, QueryCtx& cx, const float* Qd, uint64_t nq, uint
       FPP_CUDA(cudaMemset(ix.score_bytes_d.p, 0, 8));
     }
   }
+}
+
+// Multi-GPU query split: stage A alone for a
+// slice of the batch -- the probe sets as global bucket ids, [nq][P_eff] in probe
+// order (the L true buckets first).  They depend on the queries and the hash
+// functions only, so any shard's index (same parameters and seed) can resolve them.
+void run_query_probes(const Index& ix, QueryCtx& cx, const float* Qd, uint64_t nq, uint32_t qprobes,
+                  uint32_t* probes_d, cudaStream_t s) {
+  if (cx.done_recorded) FPP_CUDA(cudaStreamWaitEvent(s, cx.ev_done, 0));
+  const uint32_t cs = chunk_size(ix, qprobes, nq);
+  const uint64_t peff = query_probes(ix, qprobes);
+  for (uint64_t q0 = 0; q0 < nq; q0 += cs) {
+    const uint32_t n = (uint32_t)std::min<uint64_t>(cs, nq - q0);
+    stage_a(ix, cx, cx.slot[0], Qd + q0 * ix.d, n, qprobes, s, nullptr, probes_d + q0 * peff);
+  }
+  FPP_CUDA(cudaEventRecord(cx.ev_done, s));
+  cx.done_recorded = true;
+}
+
+// ... and stage B from such probe sets: resolved in this index's tables
+// (k_resolve_probes), then the same collect / score path as run_query.
+void run_query_from_probes(const Index& ix, QueryCtx& cx, const float* Qd, uint64_t nq,
+                       const uint32_t* probes_d, uint32_t k, uint32_t qprobes, uint32_t* ids_d,
+                       double* scores_d, fpp_query_stats* stats_d, cudaStream_t s) {
+  if (cx.done_recorded) FPP_CUDA(cudaStreamWaitEvent(s, cx.ev_done, 0));
+  ensure_score_bytes(ix);
+  const uint32_t cs = chunk_size(ix, qprobes, nq);
+  const uint64_t peff = query_probes(ix, qprobes);
+  QSlot& sl = cx.slot[0];
+  for (uint64_t q0 = 0; q0 < nq; q0 += cs) {
+    const uint32_t n = (uint32_t)std::min<uint64_t>(cs, nq - q0);
+    prepare_slot(ix, sl, n, qprobes);
+    cudaEvent_t e0;
+    cx.timer.begin(PH_PROBE, s, &e0);
+    k_resolve_probes<<<n, 256, 0, s>>>(probes_d + q0 * peff, peff, ix.NB, ix.offsets, ix.table_base,
+                                       sl.ppos.p, sl.plen.p, sl.eq.p);
+    FPP_LAUNCH();
+    k_scan_eq<<<1, 1024, 0, s>>>(sl.eq.p, n, sl.coff.p);
+    FPP_LAUNCH();
+    FPP_CUDA(cudaMemcpyAsync(sl.pinned, sl.coff.p + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    cx.timer.end(PH_PROBE, e0, s);
+    cx.acc.launches += 2;
+    FPP_CUDA(cudaEventRecord(sl.ev_probe, s));
+    stage_b(ix, cx, sl, Qd + q0 * ix.d, n, k, qprobes, ids_d + q0 * k, scores_d + q0 * k,
+            stats_d ? stats_d + q0 : nullptr, s);
+  }
+  FPP_CUDA(cudaEventRecord(cx.ev_done, s));
+  cx.done_recorded = true;
+}
+
+void run_query(const Index& ix, QueryCtx& cx, const float* Qd, uint64_t nq, uint32_t k,
+               uint32_t qprobes, uint32_t* ids_d, double* scores_d, fpp_query_stats* stats_d,
+               cudaStream_t s, uint32_t rerank) {
+  if (cx.done_recorded) FPP_CUDA(cudaStreamWaitEvent(s, cx.ev_done, 0));
+  ensure_score_bytes(ix);
   static const bool no_reorder = getenv("FPP_NO_REORDER") != nullptr;
   // the reorder costs a fixed ~35 us plus a gather of Q; its gain scales with the
   // score gather (C1, 1000 x 128 i.i.d.: -5%; C3, 1000 x 960 clustered: +4%)

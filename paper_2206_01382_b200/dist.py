@@ -4,10 +4,11 @@ One process per GPU, torch.distributed for the plumbing (NCCL on GPUs, gloo in
 the CPU tests).  Shard g owns the contiguous global ids [g*n/G, (g+1)*n/G) and
 builds its own index with ``id_offset`` so the ids it returns are global; every
 GPU holds the same sign bitmasks (same seeds).  A query batch is replicated to
-every rank, each rank answers from its shard, and the per-shard top-k lists are
-merged after one all-gather with the reference's key order (score desc, id
-asc) by the library's k-way merge kernel (fpp_merge_topk), so ties still resolve
-to the lower global id.
+every rank; stage A (hashing + probe selection) is split across the ranks and
+the probe sets all-gathered (sharded_query), each rank answers from its shard,
+and the per-shard top-k lists are merged after one all-gather with the
+reference's key order (score desc, id asc) by the library's k-way merge kernel
+(fpp_merge_topk), so ties still resolve to the lower global id.
 
 Filter scope: ``per_shard`` applies the alpha/kappa filter inside each shard
 (SURVEY 8(e) option A, the literal north-star reading); results then equal the
@@ -102,6 +103,68 @@ def allgather_merge(scores: torch.Tensor, ids: torch.Tensor, k: int, group=None)
     dist.all_gather(s_all, scores.contiguous(), group=group)
     dist.all_gather(i_all, ids64.contiguous(), group=group)
     return merge_topk(torch.cat(s_all, dim=1), torch.cat(i_all, dim=1), k)
+
+
+def query_slice(nq: int, world: int, rank: int) -> tuple[int, int]:
+    """Rank `rank`'s slice of a query batch for the stage-A split: equal slices of
+    ceil(nq / world) rows (the last ones shorter or empty), so the gathered
+    [world, per, P_eff] probe sets viewed as [world * per, P_eff] start with the
+    batch's [nq, P_eff] in order."""
+    per = -(-nq // world) if nq else 0
+    return min(nq, rank * per), min(nq, (rank + 1) * per)
+
+
+class GpuQueryEngine:
+    """The rank's GPU index as a stage-A / stage-B engine (tensors on its device)."""
+
+    def __init__(self, ix, stream=None):
+        self.ix, self.stream = ix, stream
+
+    def peff(self, qprobes: int) -> int:
+        return self.ix.peff(qprobes)
+
+    def probe_sets(self, Q, qprobes, out):
+        self.ix.query_probe_sets_device(Q, qprobes, probes=out, stream=self.stream)
+
+    def from_probe_sets(self, Q, probes, k, qprobes, ids, scores, stats=None):
+        self.ix.query_from_probe_sets_device(Q, probes, ids, scores, k, qprobes, stats=stats,
+                                             stream=self.stream)
+
+
+def sharded_query_engine(engine, Q: torch.Tensor, ids: torch.Tensor, scores: torch.Tensor, k: int,
+                         qprobes: int, group=None, stats=None):
+    """Sharded batch query with stage A split across the ranks.
+
+    Every rank holds the whole (replicated) batch Q and one shard.  Rank r computes the
+    probe sets of its slice only (hashing and probe selection: the part of the query
+    that does not depend on the shard); one all-gather gives every rank all probe sets
+    (u32 bucket ids, P_eff per query); each rank resolves them in its own tables and
+    runs stage B on the whole batch into ids/scores; the per-rank top-k lists are
+    merged after an all-gather (score desc, id asc).  Returns the merged (scores, ids)
+    on every rank.  Equals the replicated path (every rank running the whole query)
+    because probe sets depend only on the queries and the hash functions, which all
+    shards share.  `engine`: GpuQueryEngine, or the oracle engine of the CPU tests."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    nq = Q.shape[0]
+    pe = engine.peff(qprobes)
+    per = -(-nq // world) if nq else 0
+    lo, hi = query_slice(nq, world, rank)
+    mine = torch.zeros((per, pe), dtype=torch.int32, device=Q.device)
+    if hi > lo:
+        engine.probe_sets(Q[lo:hi], qprobes, mine[:hi - lo])
+    if world > 1:
+        allp = all_gather_stacked(mine, group).view(world * per, pe)[:nq]
+    else:
+        allp = mine[:nq]
+    engine.from_probe_sets(Q, allp, k, qprobes, ids, scores, stats)
+    return allgather_merge(scores, ids, k, group)
+
+
+def sharded_query(ix, Qd, ids, scores, k: int, qprobes: int, group=None, stream=None, stats=None):
+    """sharded_query_engine on the rank's GPU index (bench.py --gpus N)."""
+    return sharded_query_engine(GpuQueryEngine(ix, stream), Qd, ids, scores, k, qprobes, group,
+                                stats)
 
 
 # ---------------------------------------------------------------------------

@@ -87,6 +87,89 @@ def test_two_rank_merge(tmp_path, name):
         assert np.array_equal(got["scores"], bs)
 
 
+class OracleQueryEngine:
+    """CPU stand-in for dist.GpuQueryEngine (test infrastructure): probe sets from the
+    oracle's query_debug, stage B as the oracle's search restricted to given probe
+    sets (union of the buckets' kept entries, exact sequential fp64 inner products,
+    top-k by score desc / id asc)."""
+
+    def __init__(self, X, lo, cfg):
+        from oracle import oracle as orc
+        self.orc, self.X, self.lo = orc, X, lo
+        self.ox = orc.Index(X, **cfg["index"])
+        self.tabs = [self.ox.table(t) for t in range(cfg["index"]["L"])]
+
+    def peff(self, qprobes):
+        return int(self.ox.peff(qprobes))
+
+    def probe_sets(self, Q, qprobes, out):
+        for i, q in enumerate(Q.numpy()):
+            p, _ = self.ox.query_debug(q, qprobes)
+            assert len(p) == out.shape[1]
+            out[i] = torch.from_numpy(p.astype(np.uint32).view(np.int32).copy())
+
+    def from_probe_sets(self, Q, probes, k, qprobes, ids, scores, stats=None):
+        L = self.orc.lib()
+        NB = int(self.ox.NB)
+        for i, q in enumerate(Q.numpy()):
+            pb = probes[i].numpy().view(np.uint32).astype(np.int64)
+            cand = set()
+            for gb in pb.tolist():
+                off, tid, _ = self.tabs[gb // NB]
+                b = gb % NB
+                cand.update(tid[off[b]:off[b + 1]].tolist())
+            res = sorted(((-L.orc_inner_product(self.X[c], q, self.X.shape[1]), c) for c in cand))[:k]
+            ids[i] = 0xFFFFFFFF
+            scores[i] = -np.inf
+            for j, (ns, c) in enumerate(res):
+                ids[i, j] = c + self.lo
+                scores[i, j] = -ns
+
+
+def split_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n, d, nq, k = 1501, 32, 37, 10
+    X, Q = make(n, d, nq)
+    lo, hi = fdist.shard_range(n, world, rank)
+    cfg = CFGS["filtered"]
+    eng = OracleQueryEngine(np.ascontiguousarray(X[lo:hi]), lo, cfg)
+    ids = torch.empty((nq, k), dtype=torch.int64)
+    sc = torch.empty((nq, k), dtype=torch.float64)
+    ms, mi = fdist.sharded_query_engine(eng, torch.from_numpy(Q), ids, sc, k, cfg["qprobes"])
+    if rank == 0:
+        np.savez(out, scores=ms.numpy(), ids=mi.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_stage_a_split_equals_replicated(tmp_path, world):
+    """dist.sharded_query_engine (stage A on each rank's slice of the batch, probe sets
+    all-gathered, stage B per shard from the gathered probe sets, top-k merge) equals
+    the replicated path (every rank answering the whole batch, merge) on the same
+    shards; nq = 37 does not divide by the world size (a short / empty last slice)."""
+    out = str(tmp_path / "split.npz")
+    mp.spawn(split_worker, args=(world, free_port(), out), nprocs=world, join=True)
+    got = np.load(out)
+    n, d, nq, k = 1501, 32, 37, 10
+    X, Q = make(n, d, nq)
+    parts = [shard_answer(X, Q, *fdist.shard_range(n, world, r), CFGS["filtered"], k)
+             for r in range(world)]
+    es, ei = fdist.merge_topk(torch.from_numpy(np.concatenate([p[0] for p in parts], 1)),
+                              torch.from_numpy(np.concatenate([p[1] for p in parts], 1)), k)
+    assert np.array_equal(got["ids"], ei.numpy())
+    assert np.array_equal(got["scores"], es.numpy())
+
+
+def test_query_slices_cover():
+    for nq in (0, 1, 5, 37, 100):
+        for w in (1, 2, 3, 8):
+            rs = [fdist.query_slice(nq, w, r) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == nq
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(w - 1))
+
+
 def test_shard_ranges_cover():
     for n in (1, 7, 100, 1501):
         for w in (1, 2, 3, 8):

@@ -365,3 +365,84 @@ def test_bench_two_ranks_gloo_equals_single_rank():
     assert line["n_gpus"] == 2 and line["dist_backend"] == "gloo"
     assert line["parity"]["merged_equals_single"] is True
     assert line["parity"]["e2e_equals_device"] is True
+
+
+# -------------------------------------- multi-GPU stage-A split (probe sets)
+@pytest.mark.parametrize("d,L,qp", [(128, 12, 3000), (300, 8, 1500)])
+def test_probe_sets_split_equals_query(fpp, orc, d, L, qp):
+    """fpp_query_probe_sets_device + fpp_query_from_probe_sets_device equal
+    fpp_query_device (ids, scores, stats) -- d=128 takes the walking screen, d=300
+    the collect + pruned gather; the probe sets equal the oracle's (the L true
+    buckets first, then the rest of the probe set in table-major order)."""
+    import torch
+    X = data(fpp, 20000, d, 80, 0.3, seed=51)
+    Q = data(fpp, 300, d, 80, 0.3, seed=51, stream=1)
+    prm = dict(L=L, K=2, D=128 if d <= 128 else 256, iProbes=3, alpha=0.2)
+    ix = fpp.Index.build(X, **prm)
+    Qd = torch.from_numpy(Q).cuda()
+    k = 20
+    ids = torch.empty((len(Q), k), dtype=torch.int32, device="cuda")
+    sc = torch.empty((len(Q), k), dtype=torch.float64, device="cuda")
+    st = torch.empty((len(Q), 4), dtype=torch.int64, device="cuda")
+    ix.query_device(Qd, ids, sc, k, qp, stats=st)
+    probes = ix.query_probe_sets_device(Qd, qp)
+    ids2, sc2, st2 = torch.empty_like(ids), torch.empty_like(sc), torch.empty_like(st)
+    ix.query_from_probe_sets_device(Qd, probes, ids2, sc2, k, qp, stats=st2)
+    torch.cuda.synchronize()
+    assert torch.equal(ids, ids2) and torch.equal(sc, sc2) and torch.equal(st, st2)
+    ids3, sc3 = torch.empty_like(ids), torch.empty_like(sc)
+    ix.query_from_probe_sets_device(Qd, probes, ids3, sc3, k, qp)  # (no stats: no collect)
+    torch.cuda.synchronize()
+    assert torch.equal(ids, ids3) and torch.equal(sc, sc3)
+    # probe sets vs the oracle's (sorted bucket ids t * NB + b); true buckets first
+    ox = orc.Index(X, L=L, K=2, D=prm["D"], iprobes=3, alpha=0.2)
+    pb = probes.cpu().numpy().view(np.uint32)
+    nb = ix.info()["num_buckets"]
+    for qi in (0, 7, 299):
+        op, _ = ox.query_debug(Q[qi], qp)
+        assert np.array_equal(np.sort(pb[qi].astype(np.uint64)), np.sort(op.astype(np.uint64)))
+        assert sorted((pb[qi, :L] // nb).tolist()) == list(range(L))  # one per table
+        assert (np.diff(pb[qi, L:] // nb) >= 0).all()                 # table-major after
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_stage_a_split_over_shards_equals_single_index(fpp, world):
+    """DESIGN.md section 9 on one GPU: `world` global-filter shards; shard r computes the
+    probe sets of its slice of the batch only, the slices are concatenated (the
+    all-gather), every shard resolves all of them in its own tables, and the merged
+    top-k equals the 1-GPU index's -- dist.sharded_query's data flow, in process."""
+    import torch
+    from paper_2206_01382_b200 import dist as fdist
+    X = data(fpp, 24007, 128, 60, 0.3, seed=53)
+    Q = data(fpp, 201, 128, 60, 0.3, seed=53, stream=1)
+    prm = dict(L=8, K=2, D=128, iProbes=3, alpha=0.1, kappa=20)
+    n = len(X)
+    ranges = [fdist.shard_range(n, world, r) for r in range(world)]
+    engines = [fdist.GpuShardEngine(X[lo:hi], lo, device=0, **prm) for lo, hi in ranges]
+    gh = sum(e.hist() for e in engines)
+    slots = [e.slots(gh) for e in engines][0]
+    allp = torch.cat([e.prefix(gh, slots) for e in engines])
+    shards = [e.finish(gh, allp, world) for e in engines]
+    full = fpp.Index.build(X, **prm)
+    k, qp = 20, 2000
+    Qd = torch.from_numpy(Q).cuda()
+    nq = len(Q)
+    parts = []
+    for r, ix in enumerate(shards):
+        lo, hi = fdist.query_slice(nq, world, r)
+        if hi > lo:
+            parts.append(ix.query_probe_sets_device(Qd[lo:hi].contiguous(), qp))
+    torch.cuda.synchronize()  # (the library runs on its own streams here: stream=None)
+    probes = torch.cat(parts)
+    outs_s, outs_i = [], []
+    for ix in shards:
+        ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+        sc = torch.empty((nq, k), dtype=torch.float64, device="cuda")
+        ix.query_from_probe_sets_device(Qd, probes, ids, sc, k, qp)
+        outs_s.append(sc)
+        outs_i.append(ids)
+    torch.cuda.synchronize()
+    ms, mi = fdist.merge_lists(torch.stack(outs_s), torch.stack(outs_i), k)
+    fi, fs = full.query(Q, k, qp)
+    assert np.array_equal(mi.cpu().numpy().view(np.uint32), fi)
+    assert np.array_equal(ms.cpu().numpy(), fs)
