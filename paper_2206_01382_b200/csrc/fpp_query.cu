@@ -1636,6 +1636,9 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async16s(uint32_t sa, const void* gmem) {  // shared address
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
@@ -2301,6 +2304,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint4* ring = ring_all + (size_t)w * NS_RING * 128;
   uint32_t* idr = idr_all + (size_t)w * NS_IDR * 32;  // candidate ids of batch b: slot b % IDR
+  const uint32_t ring_sa = (uint32_t)__cvta_generic_to_shared(ring);
   uint32_t* sq = sq_all + (size_t)w * NS_QCAP;    // survivors of stage 2 -> exact
   uint32_t* s1q = s1_all + (size_t)w * NS_QCAP;   // survivors of stage 1 -> stage 2
   float2* s1v = s1v_all + (size_t)w * NS_QCAP;
@@ -2664,9 +2668,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
                                          : make_uint4(0, 0, 0, 0);
     }
   };
-  auto stage_bound = [&](const Recs& R, uint32_t stage, float& tx, float& nx) {
-    const int4 qw = part < 3 ? *reinterpret_cast<const int4*>(&q8_s[stage][4 * part])
-                             : make_int4(0, 0, 0, 0);
+  // the query's stage codes for this lane's 16 B part (zero for the terms part, so the
+  // terms bytes a part-3 lane holds in R.r[] add nothing to the dot product)
+  auto stage_qw = [&](uint32_t stage) {
+    return part < 3 ? *reinterpret_cast<const int4*>(&q8_s[stage][4 * part]) : make_int4(0, 0, 0, 0);
+  };
+  auto stage_bound = [&](const Recs& R, uint32_t stage, float& tx, float& nx, const int4 qw) {
     // integer dot products of the 4 rounds' records, then a transposing reduction
     // over the 4 lanes of a record group: lane grp * 4 + p ends with round p's total
     int dt[4];
@@ -2711,7 +2718,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     Recs R;
     load_recs(id, 1, R);
     float tx, nx;
-    const float A2 = stage_bound(R, 1, tx, nx);
+    const float A2 = stage_bound(R, 1, tx, nx, stage_qw(1));
     bool live = false;
     if (id != NONE) {
       const float A = __fadd_ru(an.x, A2);
@@ -2753,7 +2760,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       const uint32_t r = it * 8 + grp;
       const uint32_t idv = __shfl_sync(FULL, id, r);
       if (idv != NONE)
-        cp_async16(ring + (slot * 32 + r) * 4 + part, rec + (uint64_t)idv * 4 + part);
+        cp_async16s(ring_sa + ((slot * 32 + r) * 4 + part) * 16, rec + (uint64_t)idv * 4 + part);
     }
   };
   // WALK: the walker's next window -> batch b's slot: its ids (4 B cp.async per lane
@@ -2772,7 +2779,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     for (int it = 0; it < 4; ++it) {
       const uint32_t r = it * 8 + grp;
       const uint64_t gr = __shfl_sync(FULL, gp, r);
-      if (__shfl_sync(FULL, v, r)) cp_async16(ring + (slot * 32 + r) * 4 + part, cr + gr * 4 + part);
+      if (__shfl_sync(FULL, v, r)) cp_async16s(ring_sa + ((slot * 32 + r) * 4 + part) * 16, cr + gr * 4 + part);
     }
   };
   if constexpr (WALK) {
@@ -2794,6 +2801,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       cp_commit();
     }
   }
+  const int4 qw1 = stage_qw(0);  // (loop-invariant: hoisted out of the bound)
   for (uint32_t i = 0; more(i); ++i) {
     // full queues are drained first (their own loads; the ring stays in flight); the
     // exact rows are staged in the ring slot the issue below refills
@@ -2818,10 +2826,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     Recs cur;
 #pragma unroll
     for (int it = 0; it < 4; ++it)
-      cur.r[it] = part < 3 ? ring[(slot * 32 + it * 8 + grp) * 4 + part] : make_uint4(0, 0, 0, 0);
+      cur.r[it] = ring[(slot * 32 + it * 8 + grp) * 4 + part];  // (part 3: terms, times qw = 0)
     cur.m = ring[(slot * 32 + lane) * 4 + 3];
     float tx, nx;
-    const float A1 = stage_bound(cur, 0, tx, nx);
+    const float A1 = stage_bound(cur, 0, tx, nx, qw1);
     bool live = false;
     float N1 = 0.f;
     if (cid != NONE) {
