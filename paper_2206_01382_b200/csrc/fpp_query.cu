@@ -2244,11 +2244,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
 constexpr int NS_W = 8;            // warps per CTA
 constexpr uint32_t NS_QCAP = 64;   // survivor queue per warp (<= 31 + 32 queued)
 #ifndef FPP_NS_RING
-#define FPP_NS_RING 4
+#define FPP_NS_RING 3  // (3 CTAs per SM fit: 63 KB dynamic + 12 KB static shared memory)
 #endif
 constexpr int NS_RING = FPP_NS_RING;  // stage-1 record ring depth per warp (cp.async)
 constexpr int NS_IDR = 2 * NS_RING;   // candidate-id ring depth per warp
-constexpr uint32_t NS_SH_BITS = 12, NS_SH = 1u << NS_SH_BITS;  // seed id hash (lists) /
+#ifndef FPP_NS_SH_BITS
+#define FPP_NS_SH_BITS 11
+#endif
+constexpr uint32_t NS_SH_BITS = FPP_NS_SH_BITS, NS_SH = 1u << NS_SH_BITS;  // seed id hash (lists) /
                                                                 // admission hash (WALK)
 constexpr int WK_HPROBE = 32;  // admission hash: probes before the bitmap takes an id
 
@@ -3289,8 +3292,10 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
         getenv("FPP_SC_SEEDCAP") ? (uint32_t)atoi(getenv("FPP_SC_SEEDCAP")) : WK_SEEDCAP;
     sa.seedcap = seedcap;
     const size_t sm = screen_smem(ix.d);
-    // 2 CTAs/SM (shared memory: the record rings); FPP_SC_SCR_MINB=3 caps registers at 80
-    static const int scr_minb = getenv("FPP_SC_SCR_MINB") ? atoi(getenv("FPP_SC_SCR_MINB")) : 2;
+    // 3 CTAs/SM (24 warps: 80 registers, a 3-batch ring and a 2048-slot admission hash
+    // so three CTAs' shared memory fits): C4 533 vs 522 k q/s for 2 CTAs/SM with a
+    // 4-batch ring; FPP_SC_SCR_MINB=2 selects the 2-CTA register budget
+    static const int scr_minb = getenv("FPP_SC_SCR_MINB") ? atoi(getenv("FPP_SC_SCR_MINB")) : 3;
     auto launch_scr = [&](auto kern) {
       FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       unsigned grid = nqc;
