@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "fpp_internal.h"
 
 namespace fpp {
@@ -327,7 +329,10 @@ __global__ void k_q8_records(const float* __restrict__ X, uint64_t n, uint32_t d
       const float x1 = (lane < 16 && j1 < min(d, hi)) ? r[j1] : 0.f;
       float mx = fmaxf(fabsf(x0), fabsf(x1));
       for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const float sc = mx / 127.0f;
+      // stage 1's scale is rounded up to an fp16-exact value (the inline CSR-order
+      // records keep it in fp16, k_q8_inline), so the codes below are computed with the
+      // scale the bound uses; stage 2 keeps the fp32 scale
+      const float sc = stage == 0 ? __half2float(__float2half_ru(mx / 127.0f)) : mx / 127.0f;
       const int c0 = sc > 0.f ? max(-127, min(127, __float2int_rn(x0 / sc))) : 0;
       const int c1 = sc > 0.f ? max(-127, min(127, __float2int_rn(x1 / sc))) : 0;
       const double e0 = (double)x0 - (double)sc * c0, e1 = (double)x1 - (double)sc * c1;

@@ -34,6 +34,7 @@
 #include <cstring>
 
 #include <cooperative_groups.h>
+#include <cuda_fp16.h>
 
 #include "fpp_device.cuh"
 #include "fpp_internal.h"
@@ -2676,7 +2677,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   auto stage_qw = [&](uint32_t stage) {
     return part < 3 ? *reinterpret_cast<const int4*>(&q8_s[stage][4 * part]) : make_int4(0, 0, 0, 0);
   };
-  auto stage_bound = [&](const Recs& R, uint32_t stage, float& tx, float& nx, const int4 qw) {
+  // h16: the terms word is the inline (CSR-order) record's {s, r | m, t} as half2 pairs
+  // (s exact, the norms rounded up: k_q8_inline) instead of four fp32
+  auto stage_bound = [&](const Recs& R, uint32_t stage, float& tx, float& nx, const int4 qw,
+                         bool h16) {
     // integer dot products of the 4 rounds' records, then a transposing reduction
     // over the 4 lanes of a record group: lane grp * 4 + p ends with round p's total
     int dt[4];
@@ -2699,9 +2703,20 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     // candidate c = round (c >> 3), group (c & 7): held by lane (c & 7) * 4 + (c >> 3)
     const int dot = __shfl_sync(FULL, d1, (lane & 7) * 4 + (lane >> 3));
     const float qs = qn_s[stage][0], qh = qn_s[stage][1], qr = qn_s[stage][2];
-    const float sx = __uint_as_float(R.m.x), rx = __uint_as_float(R.m.y);
-    const float mxn = __uint_as_float(R.m.z);
-    tx = __uint_as_float(R.m.w);
+    float sx, rx, mxn;
+    if (h16) {
+      const __half2 sr = *reinterpret_cast<const __half2*>(&R.m.x);
+      const __half2 mt = *reinterpret_cast<const __half2*>(&R.m.y);
+      sx = __low2float(sr);
+      rx = __high2float(sr);
+      mxn = __low2float(mt);
+      tx = __high2float(mt);
+    } else {
+      sx = __uint_as_float(R.m.x);
+      rx = __uint_as_float(R.m.y);
+      mxn = __uint_as_float(R.m.z);
+      tx = __uint_as_float(R.m.w);
+    }
     nx = __fadd_ru(mxn, rx);  // >= ||x_h||
     const float If = (float)dot;  // |I| <= 48 * 127^2: exact in fp32
     // s_x s_q I rounded up: round the scale product toward the side that raises it
@@ -2721,7 +2736,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     Recs R;
     load_recs(id, 1, R);
     float tx, nx;
-    const float A2 = stage_bound(R, 1, tx, nx, stage_qw(1));
+    const float A2 = stage_bound(R, 1, tx, nx, stage_qw(1), false);
     bool live = false;
     if (id != NONE) {
       const float A = __fadd_ru(an.x, A2);
@@ -2746,18 +2761,20 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   // covers both the records of batch i and the ids of batch i + RING - 1.
   const uint32_t nb = (Len + 31) / 32;
   const uint32_t nbw = nb > (uint32_t)w ? (nb - w + NW - 1) / NW : 0;  // this warp's batches
-  auto ids_async = [&](uint32_t b) {  // lists: ids of the warp's batch b -> id ring (cp.async)
+  // Slots are kept as wrapping counters (NS_RING = 3 is not a power of two: a modulo
+  // per use was a multiply-shift sequence).  islot: an id-ring slot, rslot: a ring slot.
+  auto ids_async = [&](uint32_t b, uint32_t islot) {  // lists: ids of batch b -> id ring
     if constexpr (!WALK) {
       const uint32_t ci = (w + b * NW) * 32 + lane;
-      uint32_t* dst = idr + (b % NS_IDR) * 32 + lane;
+      uint32_t* dst = idr + islot * 32 + lane;
       if (b < nbw && ci < Len) cp_async4(dst, cand + ci);
       else *dst = NONE;
     }
   };
   auto more = [&](uint32_t i) { return WALK ? !(wk_done && i >= nprod) : i < nbw; };
-  auto issue = [&](uint32_t b) {  // records of the warp's batch b (ids in the id ring) -> slot
-    const uint32_t slot = b % NS_RING;
-    const uint32_t id = idr[(b % NS_IDR) * 32 + lane];
+  auto issue = [&](uint32_t rslot, uint32_t islot) {  // records of a batch (ids in the id ring)
+    const uint32_t slot = rslot;
+    const uint32_t id = idr[islot * 32 + lane];
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const uint32_t r = it * 8 + grp;
@@ -2770,13 +2787,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   // from the CSR ids) and its stage-1 records, inline in CSR order (a.csrrec: the
   // window's entries are runs of consecutive records, so the copies are coalesced and
   // whole 128 B lines are used), one commit group
-  auto produce = [&](uint32_t b) {
-    const uint32_t slot = b % NS_RING;
+  auto produce = [&](uint32_t slot) {
     uint64_t gp = 0;
     const bool v = wk_step(gp);
-    uint32_t* dst = idr + slot * 32;  // (WALK uses id-ring slots 0 .. RING-1)
-    if (v) cp_async4(dst + lane, a.ids + gp);
-    else dst[lane] = NONE;
+    const uint32_t vm = __ballot_sync(FULL, v);  // lanes with an entry (the record holds the id)
+    if (lane == 0) idr[slot * 32] = vm;          // (WALK: word 0 of id-ring slot `slot`)
     const uint4* cr = reinterpret_cast<const uint4*>(a.csrrec);
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
@@ -2793,22 +2808,28 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       cp_commit();
     }
   } else {
-    for (uint32_t b = 0; b < NS_RING; ++b) ids_async(b);
+    for (uint32_t b = 0; b < NS_RING; ++b) ids_async(b, b);
     cp_commit();
     cp_wait<0>();
     __syncwarp();
 #pragma unroll
     for (uint32_t j = 0; j + 1 < NS_RING; ++j) {
-      issue(j);
-      ids_async(j + NS_RING);
+      issue(j, j);
+      ids_async(j + NS_RING, j + NS_RING);
       cp_commit();
     }
   }
   const int4 qw1 = stage_qw(0);  // (loop-invariant: hoisted out of the bound)
+  // batch i: ring slot cs = i % RING, id-ring slot ci = i % IDR; the refill of this
+  // iteration goes to ring slot (i + RING - 1) % RING (the slot consumed last), its ids
+  // from id-ring slot (i + RING - 1) % IDR, and the ids of batch i + 2 RING - 1 to
+  // id-ring slot (i - 1) % IDR
+  uint32_t cs = 0, ci = 0;
   for (uint32_t i = 0; more(i); ++i) {
+    const uint32_t ps = cs == 0 ? NS_RING - 1 : cs - 1;
     // full queues are drained first (their own loads; the ring stays in flight); the
     // exact rows are staged in the ring slot the issue below refills
-    float* const stg = reinterpret_cast<float*>(ring + ((i + NS_RING - 1) % NS_RING) * 128);
+    float* const stg = reinterpret_cast<float*>(ring + ps * 128);
     if (qtail - qhead >= 32) {
       __syncwarp();
       exact_batch(32, stg);
@@ -2816,23 +2837,28 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     if (t1 - h1 >= 32) stage2_batch(32);
     __syncwarp();  // (the staging slot's readers are done before its refill)
     if constexpr (WALK) {
-      produce(i + NS_RING - 1);
+      produce(ps);
     } else {
-      issue(i + NS_RING - 1);   // (an empty commit past the end keeps the count)
-      ids_async(i + 2 * NS_RING - 1);
+      const uint32_t pi = ci + NS_RING - 1 < NS_IDR ? ci + NS_RING - 1 : ci + NS_RING - 1 - NS_IDR;
+      issue(ps, pi);   // (an empty commit past the end keeps the count)
+      ids_async(i + 2 * NS_RING - 1, ci == 0 ? NS_IDR - 1 : ci - 1);
     }
     cp_commit();
     cp_wait<NS_RING - 1>();
     __syncwarp();
-    const uint32_t slot = i % NS_RING;
-    const uint32_t cid = idr[(i % (WALK ? NS_RING : NS_IDR)) * 32 + lane];
+    const uint32_t slot = cs;
+    const uint32_t cid =
+        WALK ? (((idr[slot * 32] >> lane) & 1u) ? ring[(slot * 32 + lane) * 4 + 3].z : NONE)
+             : idr[ci * 32 + lane];
+    cs = cs + 1 == NS_RING ? 0 : cs + 1;
+    ci = ci + 1 == NS_IDR ? 0 : ci + 1;
     Recs cur;
 #pragma unroll
     for (int it = 0; it < 4; ++it)
       cur.r[it] = ring[(slot * 32 + it * 8 + grp) * 4 + part];  // (part 3: terms, times qw = 0)
     cur.m = ring[(slot * 32 + lane) * 4 + 3];
     float tx, nx;
-    const float A1 = stage_bound(cur, 0, tx, nx, qw1);
+    const float A1 = stage_bound(cur, 0, tx, nx, qw1, WALK);
     bool live = false;
     float N1 = 0.f;
     if (cid != NONE) {
@@ -3072,12 +3098,27 @@ static uint32_t grouped_shift(uint64_t n) {
   return sm + 64 <= (size_t)co_smem_max() ? gs : 0u;
 }
 
-// Index::q8csr: entry e's stage-1 record = q8rec[ids[e]] (four threads per entry)
+// Index::q8csr: entry e's stage-1 record = q8rec[ids[e]] (four threads per entry) with
+// the terms part repacked as {s, r | m, t} half2 pairs + the entry's id: the scale is
+// fp16-exact (k_q8_records rounds it up to fp16 before quantizing), the norms are
+// rounded up (still upper bounds), so the walking screen reads the id with the record
+// and no separate ids stream
 __global__ void k_q8_inline(const uint4* __restrict__ rec, const uint32_t* __restrict__ ids,
                             uint64_t kept, uint4* __restrict__ out) {
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < kept * 4;
-       t += (uint64_t)gridDim.x * blockDim.x)
-    out[t] = __ldg(rec + (uint64_t)__ldg(ids + (t >> 2)) * 4 + (t & 3));
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t id = __ldg(ids + (t >> 2));
+    uint4 v = __ldg(rec + (uint64_t)id * 4 + (t & 3));
+    if ((t & 3) == 3) {
+      const __half2 sr = __halves2half2(__float2half_ru(__uint_as_float(v.x)),
+                                        __float2half_ru(__uint_as_float(v.y)));
+      const __half2 mt = __halves2half2(__float2half_ru(__uint_as_float(v.z)),
+                                        __float2half_ru(__uint_as_float(v.w)));
+      v = make_uint4(*reinterpret_cast<const uint32_t*>(&sr), *reinterpret_cast<const uint32_t*>(&mt),
+                     id, 0u);
+    }
+    out[t] = v;
+  }
 }
 
 static void ensure_q8csr(const Index& ix) {
