@@ -2249,6 +2249,10 @@ constexpr uint32_t NS_QCAP = 64;   // survivor queue per warp (<= 31 + 32 queued
 #endif
 constexpr int NS_RING = FPP_NS_RING;  // stage-1 record ring depth per warp (cp.async)
 constexpr int NS_IDR = 2 * NS_RING;   // candidate-id ring depth per warp
+#ifndef FPP_NS_TMA
+#define FPP_NS_TMA 0  // measured: C4 511 vs 538 k q/s with the cp.async ring
+#endif
+constexpr int NS_TMA = FPP_NS_TMA;    // WALK: stage-1 records by TMA bulk copies per run
 #ifndef FPP_NS_SH_BITS
 #define FPP_NS_SH_BITS 11
 #endif
@@ -2303,6 +2307,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   __shared__ uint32_t mg_i[NW][32];
   __shared__ uint32_t q_s, wctr_s[2], logn_s;  // query, walker chunk counters, log length
   __shared__ uint32_t seedh[NS_SH];     // lists: the seeds' ids (open addressing)
+  __shared__ __align__(8) uint64_t smbar[WALK && NS_TMA ? NW : 1][NS_RING];  // TMA: per ring slot
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int part = lane & 3, grp = lane >> 2;  // record part (0-2 codes, 3 terms), record slot
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -2316,6 +2321,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   uint32_t* const bm = a.gbm ? a.gbm + (size_t)blockIdx.x * a.nwords : nullptr;
   uint32_t* const wlog = a.gbm ? a.wlog + (size_t)blockIdx.x * a.logcap : nullptr;
   const uint4* rec = reinterpret_cast<const uint4*>(a.xtail);  // [stages][n][4] 16 B parts
+  uint32_t mph = 0;  // TMA: parity of each ring slot's next completion (bit per slot)
+  if constexpr (WALK && NS_TMA) {
+    if (lane == 0)
+      for (int i = 0; i < NS_RING; ++i) mbar_init(&smbar[w][i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncwarp();
+  }
   const float* X = a.X;
   const uint32_t ldx = a.ldx;
   const uint32_t k = a.k;
@@ -2793,6 +2805,23 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     const uint32_t vm = __ballot_sync(FULL, v);  // lanes with an entry (the record holds the id)
     if (lane == 0) idr[slot * 32] = vm;          // (WALK: word 0 of id-ring slot `slot`)
     const uint4* cr = reinterpret_cast<const uint4*>(a.csrrec);
+    if constexpr (NS_TMA) {
+      // the window's valid lanes are a prefix, split into runs of consecutive CSR
+      // entries (one bucket each): one bulk copy per run (TMA), completing on the
+      // slot's mbarrier; the slot's previous generic-proxy use (exact staging) is
+      // fenced first
+      const uint64_t gprev = __shfl_up_sync(FULL, gp, 1);
+      const uint32_t starts = __ballot_sync(FULL, v && (lane == 0 || gp != gprev + 1));
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      if (lane == 0) mbar_arrive_tx(&smbar[w][slot], (uint32_t)__popc(vm) * 64u);
+      __syncwarp();
+      if ((starts >> lane) & 1u) {
+        const uint32_t after = starts & ~((2u << lane) - 1u);  // later run starts
+        const uint32_t end = after ? (uint32_t)(__ffs(after) - 1) : (uint32_t)__popc(vm);
+        bulk_g2s(ring + (slot * 32 + lane) * 4, cr + gp * 4, (end - lane) * 64u, &smbar[w][slot]);
+      }
+      return;
+    }
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const uint32_t r = it * 8 + grp;
@@ -2843,9 +2872,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       issue(ps, pi);   // (an empty commit past the end keeps the count)
       ids_async(i + 2 * NS_RING - 1, ci == 0 ? NS_IDR - 1 : ci - 1);
     }
-    cp_commit();
-    cp_wait<NS_RING - 1>();
-    __syncwarp();
+    if constexpr (WALK && NS_TMA) {
+      mbar_wait(&smbar[w][cs], (mph >> cs) & 1u);
+      mph ^= 1u << cs;
+    } else {
+      cp_commit();
+      cp_wait<NS_RING - 1>();
+      __syncwarp();
+    }
     const uint32_t slot = cs;
     const uint32_t cid =
         WALK ? (((idr[slot * 32] >> lane) & 1u) ? ring[(slot * 32 + lane) * 4 + 3].z : NONE)
@@ -2876,6 +2910,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     t1 += __popc(live_m);
     nrows += __popc(__ballot_sync(FULL, cid != NONE));
     __syncwarp();  // slot i % RING is refilled by the next iteration's issue
+  }
+  if constexpr (WALK && NS_TMA) {  // the RING - 1 windows produced past the end (empty)
+#pragma unroll
+    for (int j = 0; j + 1 < NS_RING; ++j) {
+      mbar_wait(&smbar[w][cs], (mph >> cs) & 1u);
+      mph ^= 1u << cs;
+      cs = cs + 1 == NS_RING ? 0 : cs + 1;
+    }
   }
   cp_wait<0>();
   __syncwarp();
