@@ -307,12 +307,12 @@ __global__ void k_tail_norms(const float* __restrict__ X, uint64_t n, uint32_t d
   }
 }
 
-// Screening records for k_score_screen (warp per row): two 64-byte stages per row.
-// Stage j covers dims [48 j, 48 j + 48): int8 codes with the stage's scale
-// s = max|x_i| / 127 (fp32), codes rint(x_i / s); then, in fp64 and rounded up to
-// fp32 (x 1+1e-12): r = ||x_h - s code|| (quantization error), m = ||s code|| and
-// t = ||x[48 j + 48 : d)|| (everything after the stage).  Record = 48 code bytes +
-// {s, r, m, t}.  The score kernel bounds the stage's part of x.q by
+// Screening records for k_score_screen (warp per row; layout: fpp_internal.h Q8A/Q8B).
+// Stage A covers dims [0, 20), stage B dims [20, 116): int8 codes with the stage's
+// scale s = max|x_i| / 127 (stage A: rounded up to an fp16-exact value, the records
+// keep it in fp16), codes rint(x_i / s); then, in fp64 and rounded up (x 1+1e-12):
+// r = ||x_h - s code|| (quantization error), m = ||s code|| and t = ||x[hi : d)||
+// (everything after the stage).  The score kernel bounds the stage's part of x.q by
 // s_q s I + r ||q_h|| + m ||q_h - q~_h|| (I = the integer dot product of the codes)
 // and the rest by t ||q_t|| (Cauchy-Schwarz).
 __global__ void k_q8_records(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx,
@@ -322,41 +322,53 @@ __global__ void k_q8_records(const float* __restrict__ X, uint64_t n, uint32_t d
   for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
     const float* r = X + i * ldx;
 #pragma unroll
-    for (uint32_t stage = 0; stage < Q8_STAGES; ++stage) {
-      const uint32_t lo = stage * Q8_DIMS, hi = lo + Q8_DIMS;
-      const uint32_t j0 = lo + lane, j1 = lo + lane + 32;
-      const float x0 = j0 < min(d, hi) ? r[j0] : 0.f;
-      const float x1 = (lane < 16 && j1 < min(d, hi)) ? r[j1] : 0.f;
-      float mx = fmaxf(fabsf(x0), fabsf(x1));
+    for (uint32_t stage = 0; stage < 2; ++stage) {
+      const uint32_t W = stage ? Q8B_DIMS : Q8A_DIMS;  // code bytes
+      const uint32_t lo = stage ? Q8A_DIMS : 0u, hi = min(d, lo + W);
+      float x[3];
+      float mx = 0.f;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const uint32_t k = lane + 32 * j;
+        x[j] = (k < W && lo + k < hi) ? r[lo + k] : 0.f;
+        mx = fmaxf(mx, fabsf(x[j]));
+      }
       for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      // stage 1's scale is rounded up to an fp16-exact value (the inline CSR-order
-      // records keep it in fp16, k_q8_inline), so the codes below are computed with the
-      // scale the bound uses; stage 2 keeps the fp32 scale
       const float sc = stage == 0 ? __half2float(__float2half_ru(mx / 127.0f)) : mx / 127.0f;
-      const int c0 = sc > 0.f ? max(-127, min(127, __float2int_rn(x0 / sc))) : 0;
-      const int c1 = sc > 0.f ? max(-127, min(127, __float2int_rn(x1 / sc))) : 0;
-      const double e0 = (double)x0 - (double)sc * c0, e1 = (double)x1 - (double)sc * c1;
-      const double m0 = (double)sc * c0, m1 = (double)sc * c1;
-      double er = e0 * e0 + e1 * e1, mm = m0 * m0 + m1 * m1, tt = 0.0;
-      for (uint32_t j = hi + lane; j < d; j += 32) tt = fma((double)r[j], (double)r[j], tt);
+      double er = 0.0, mm = 0.0, tt = 0.0;
+      int c[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        c[j] = sc > 0.f ? max(-127, min(127, __float2int_rn(x[j] / sc))) : 0;
+        const double e = (double)x[j] - (double)sc * c[j], m = (double)sc * c[j];
+        er = fma(e, e, er);
+        mm = fma(m, m, mm);
+      }
+      for (uint32_t j = lo + W + lane; j < d; j += 32) tt = fma((double)r[j], (double)r[j], tt);
       for (int o = 16; o; o >>= 1) {
         er += __shfl_xor_sync(0xffffffffu, er, o);
         mm += __shfl_xor_sync(0xffffffffu, mm, o);
         tt += __shfl_xor_sync(0xffffffffu, tt, o);
       }
-      // byte b of the stage record = code of dim lo + b (lanes: b = lane, lane + 32 < 48)
-      // stage tables are separate ([stage][n] records): a stage-1 read never drags the
-      // stage-2 record of the row into L2
-      unsigned char* rb = reinterpret_cast<unsigned char*>(rec + ((uint64_t)stage * n + i) * 4);
-      rb[lane] = (unsigned char)(signed char)c0;
-      if (lane < 16) rb[lane + 32] = (unsigned char)(signed char)c1;
+      unsigned char* rb = reinterpret_cast<unsigned char*>(stage ? rec + (uint64_t)n * 2 + i * 8 : rec + i * 2);
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (lane + 32 * j < (int)W) rb[lane + 32 * j] = (unsigned char)(signed char)c[j];
       if (lane == 0) {
-        float4 m;
-        m.x = sc;
-        m.y = __double2float_ru(__dsqrt_ru(er) * (1.0 + 1e-12));
-        m.z = __double2float_ru(__dsqrt_ru(mm) * (1.0 + 1e-12));
-        m.w = __double2float_ru(__dsqrt_ru(tt) * (1.0 + 1e-12));
-        *reinterpret_cast<float4*>(rb + Q8_DIMS) = m;
+        const float rr = __double2float_ru(__dsqrt_ru(er) * (1.0 + 1e-12));
+        const float m2 = __double2float_ru(__dsqrt_ru(mm) * (1.0 + 1e-12));
+        const float t2 = __double2float_ru(__dsqrt_ru(tt) * (1.0 + 1e-12));
+        if (stage == 0) {  // bytes 20..31: id slot, {s, r}, {m, t} half2
+          const __half2 sr = __halves2half2(__float2half_ru(sc), __float2half_ru(rr));
+          const __half2 mt = __halves2half2(__float2half_ru(m2), __float2half_ru(t2));
+          uint32_t* w32 = reinterpret_cast<uint32_t*>(rb + Q8A_DIMS);
+          w32[0] = 0u;
+          w32[1] = *reinterpret_cast<const uint32_t*>(&sr);
+          w32[2] = *reinterpret_cast<const uint32_t*>(&mt);
+        } else {
+          *reinterpret_cast<float4*>(rb + Q8B_DIMS) = make_float4(sc, rr, m2, t2);
+          *reinterpret_cast<float4*>(rb + Q8B_DIMS + 16) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
     }
   }
@@ -366,7 +378,7 @@ void launch_tail_norms(Index& ix) {
   // FPP_L2_FETCH=32|64|128: cudaLimitMaxL2FetchGranularity hint (experiments)
   if (getenv("FPP_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(getenv("FPP_L2_FETCH")));
   if (ix.d >= 64 && ix.d <= 256 && ix.d % 4 == 0) {  // k_score_screen's records
-    ix.q8rec = static_cast<uint4*>(dmalloc((size_t)ix.n * 64 * Q8_STAGES));
+    ix.q8rec = static_cast<uint4*>(dmalloc((size_t)ix.n * (32 + 128)));
     k_q8_records<<<sm_count() * 8, 256, 0, ix.stream>>>(ix.X, ix.n, ix.d, ix.ldx, ix.q8rec);
     FPP_LAUNCH();
   }

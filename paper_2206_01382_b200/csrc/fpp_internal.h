@@ -93,9 +93,9 @@ struct Index {
   // ||X[i][(j+1)*XT_SLICE:d)||, rounded up to fp32, checkpoints j < xt_n
   float* xtail = nullptr;
   uint32_t xt_n = 0;
-  // narrow rows (64 <= d <= 256, d % 4 == 0; k_score_screen): Q8_STAGES 64 B
-  // screening records per row -- Q8_DIMS dims each as int8 codes with a per-row
-  // scale, plus the error / norm terms of the bound (k_q8_records)
+  // narrow rows (64 <= d <= 256, d % 4 == 0; k_score_screen): a 32 B and a 128 B
+  // screening record per row -- int8 codes with a per-row scale, plus the error /
+  // norm terms of the bound (k_q8_records)
   uint4* q8rec = nullptr;
   // the stage-1 records again, in CSR entry order ([kept_total][4] uint4: entry e's
   // record is q8rec[ids[e]]), so the walking screen streams them with its bucket walk
@@ -211,10 +211,18 @@ uint64_t content_hash(const float* X, uint64_t n, uint32_t d);
 void save_index(const Index& ix, const char* path, const float* X_host);
 void launch_signatures(const Index& ix, const float* Xd, uint64_t n, uint32_t ld, uint64_t* out,
                        cudaStream_t s);
-// k_score_screen record: int8 codes of dims [0, Q8_DIMS) (48 B) + {scale, ||x_h - x~_h||,
-// ||x~_h||, ||x[Q8_DIMS:d)||} as fp32 rounded up (16 B) = 64 B per row
-constexpr uint32_t Q8_DIMS = 48;
-constexpr uint32_t Q8_STAGES = 2;  // record tables [stage][n]: dims [0,48) and [48,96)
+// k_score_screen records (k_q8_records), two per row:
+//   stage A, 32 B: int8 codes of dims [0, Q8A_DIMS) (20 B), a 4 B id slot (the inline
+//     CSR-order copy stores the entry's id there), {scale, ||x_h - x~_h||, ||x~_h||,
+//     ||x[Q8A_DIMS:d)||} as half2 pairs (8 B: the scale fp16-exact, the norms rounded
+//     up);
+//   stage B, 128 B (a random access costs a 128 B DRAM line anyway): codes of dims
+//     [Q8A_DIMS, Q8A_DIMS + Q8B_DIMS) (96 B) + the same four terms in fp32 (16 B) +
+//     16 B padding.
+// Tables: [n][32 B] (A), then [n][128 B] (B).
+constexpr uint32_t Q8A_DIMS = 20;
+constexpr uint32_t Q8B_DIMS = 96;
+constexpr uint32_t Q8_STAGES = 2;
 constexpr uint32_t XT_SLICE = 64;  // = the score ring's row-slice width for d >= 64
 constexpr uint32_t XT_MAX = 4;     // tail-norm checkpoints per row
 // score-gather slices of a d-wide row: a head [0, h) (h = Index::xt_head, 32 or 64),

@@ -2302,14 +2302,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   __shared__ double thr2_s[NW];          // per warp: its ceil(k/NW)-th best
   __shared__ uint32_t nseed_s;
   __shared__ float qn_s[Q8_STAGES][4];   // per stage: s_q, ||q_h||, r_q, ||q after the stage||
-  __shared__ __align__(16) int32_t q8_s[Q8_STAGES][Q8_DIMS / 4];  // the query's stage codes
+  __shared__ __align__(16) int32_t q8_s[Q8_STAGES][Q8B_DIMS / 4];  // the query's stage codes
   __shared__ double mg_s[NW][32];
   __shared__ uint32_t mg_i[NW][32];
   __shared__ uint32_t q_s, wctr_s[2], logn_s;  // query, walker chunk counters, log length
   __shared__ uint32_t seedh[NS_SH];     // lists: the seeds' ids (open addressing)
   __shared__ __align__(8) uint64_t smbar[WALK && NS_TMA ? NW : 1][NS_RING];  // TMA: per ring slot
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int part = lane & 3, grp = lane >> 2;  // record part (0-2 codes, 3 terms), record slot
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint4* ring = ring_all + (size_t)w * NS_RING * 128;
   uint32_t* idr = idr_all + (size_t)w * NS_IDR * 32;  // candidate ids of batch b: slot b % IDR
@@ -2347,26 +2346,37 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   if (threadIdx.x == 0) thr_key = dkey(-INFINITY);
   if (threadIdx.x < NW) thr2_s[threadIdx.x] = -INFINITY;
   if ((uint32_t)w < Q8_STAGES) {  // quantize the query like the records (k_q8_records)
-    const uint32_t lo = w * Q8_DIMS, hi = lo + Q8_DIMS;
-    const uint32_t j0 = lo + lane, j1 = lo + lane + 32;
-    const float x0 = j0 < min(d, hi) ? Qr[j0] : 0.f;
-    const float x1 = (lane < 16 && j1 < min(d, hi)) ? Qr[j1] : 0.f;
-    float mx = fmaxf(fabsf(x0), fabsf(x1));
+    const uint32_t W = w ? Q8B_DIMS : Q8A_DIMS;
+    const uint32_t lo = w ? Q8A_DIMS : 0u, hi = min(d, lo + W);
+    float x[3];
+    float mx = 0.f;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const uint32_t kk = lane + 32 * j;
+      x[j] = (kk < W && lo + kk < hi) ? Qr[lo + kk] : 0.f;
+      mx = fmaxf(mx, fabsf(x[j]));
+    }
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
     const float sc = mx / 127.0f;
-    const int c0 = sc > 0.f ? max(-127, min(127, __float2int_rn(x0 / sc))) : 0;
-    const int c1 = sc > 0.f ? max(-127, min(127, __float2int_rn(x1 / sc))) : 0;
-    const double e0 = (double)x0 - (double)sc * c0, e1 = (double)x1 - (double)sc * c1;
-    double er = e0 * e0 + e1 * e1, hh = (double)x0 * x0 + (double)x1 * x1, tt = 0.0;
-    for (uint32_t j = hi + lane; j < d; j += 32) tt = fma((double)Qr[j], (double)Qr[j], tt);
+    double er = 0.0, hh = 0.0, tt = 0.0;
+    int c[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      c[j] = sc > 0.f ? max(-127, min(127, __float2int_rn(x[j] / sc))) : 0;
+      const double e = (double)x[j] - (double)sc * c[j];
+      er = fma(e, e, er);
+      hh = fma((double)x[j], (double)x[j], hh);
+    }
+    for (uint32_t j = lo + W + lane; j < d; j += 32) tt = fma((double)Qr[j], (double)Qr[j], tt);
     for (int o = 16; o; o >>= 1) {
       er += __shfl_xor_sync(FULL, er, o);
       hh += __shfl_xor_sync(FULL, hh, o);
       tt += __shfl_xor_sync(FULL, tt, o);
     }
     unsigned char* qb = reinterpret_cast<unsigned char*>(q8_s[w]);
-    qb[lane] = (unsigned char)(signed char)c0;
-    if (lane < 16) qb[lane + 32] = (unsigned char)(signed char)c1;
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      if (lane + 32 * j < (int)Q8B_DIMS) qb[lane + 32 * j] = (unsigned char)(signed char)c[j];
     if (lane == 0) {
       qn_s[w][0] = sc;
       qn_s[w][1] = __double2float_ru(__dsqrt_ru(hh) * (1.0 + 1e-12));
@@ -2663,77 +2673,82 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     }
   }
 
-  // -------------------------------------------------------- record stage bound
-  // 32 candidates, lane c <-> candidate c (id NONE = none).  Round it (0-3) reads
-  // stage records it * 8 + grp, 16 B part `part` per lane (code parts 0-2; the terms
-  // part 3 is loaded by the candidate's own lane).  Returns the stage's part bound
-  // A = s_x s_q I + r_x ||q_h|| + m_x r_q (rounded up) and, in `tx`, the norm of the
-  // row after the stage.
+  // -------------------------------------------------------- record stage bounds
+  // Stage A (32 B records, two 16 B parts): 32 candidates, lane c <-> candidate c (id
+  // NONE = none).  Round it (0-1) holds part p2 of record it * 16 + g16 per lane (part
+  // 0: codes 0-15; part 1: codes 16-19, the id slot and the half2 terms -- the query
+  // weights of its last three words are zero).  Per-candidate terms come from the
+  // candidate's own part 1 (R.m).  Returns A = s_x s_q I + r_x ||q_h|| + m_x r_q
+  // (rounded up) and, in `tx`, the norm of the row after the stage.
   struct Recs {
-    uint4 r[4];
+    uint4 r[2];
     uint4 m;
   };
-  auto load_recs = [&](uint32_t id, uint32_t stage, Recs& R) {
-    // L2-only loads (ld.global.cg): sector-granular, no L1 line fills
-    const uint4* rs = rec + (uint64_t)stage * a.n * 4;  // this stage's table
-    R.m = id != NONE ? __ldcg(rs + (uint64_t)id * 4 + 3) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const uint32_t idr = __shfl_sync(FULL, id, it * 8 + grp);
-      R.r[it] = (idr != NONE && part < 3) ? __ldcg(rs + (uint64_t)idr * 4 + part)
-                                         : make_uint4(0, 0, 0, 0);
-    }
+  const int p2 = lane & 1, g16 = lane >> 1;
+  auto stageA_qw = [&] {
+    return p2 == 0 ? *reinterpret_cast<const int4*>(&q8_s[0][0]) : make_int4(q8_s[0][4], 0, 0, 0);
   };
-  // the query's stage codes for this lane's 16 B part (zero for the terms part, so the
-  // terms bytes a part-3 lane holds in R.r[] add nothing to the dot product)
-  auto stage_qw = [&](uint32_t stage) {
-    return part < 3 ? *reinterpret_cast<const int4*>(&q8_s[stage][4 * part]) : make_int4(0, 0, 0, 0);
-  };
-  // h16: the terms word is the inline (CSR-order) record's {s, r | m, t} as half2 pairs
-  // (s exact, the norms rounded up: k_q8_inline) instead of four fp32
-  auto stage_bound = [&](const Recs& R, uint32_t stage, float& tx, float& nx, const int4 qw,
-                         bool h16) {
-    // integer dot products of the 4 rounds' records, then a transposing reduction
-    // over the 4 lanes of a record group: lane grp * 4 + p ends with round p's total
-    int dt[4];
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      int t = __dp4a((int)R.r[it].x, qw.x, 0);
-      t = __dp4a((int)R.r[it].y, qw.y, t);
-      t = __dp4a((int)R.r[it].z, qw.z, t);
-      dt[it] = __dp4a((int)R.r[it].w, qw.w, t);
-    }
-    const bool hb = part & 2, lb = part & 1;
-    int d2[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int snd = hb ? dt[j] : dt[j + 2];
-      d2[j] = (hb ? dt[j + 2] : dt[j]) + __shfl_xor_sync(FULL, snd, 2);
-    }
-    const int snd = lb ? d2[0] : d2[1];
-    const int d1 = (lb ? d2[1] : d2[0]) + __shfl_xor_sync(FULL, snd, 1);
-    // candidate c = round (c >> 3), group (c & 7): held by lane (c & 7) * 4 + (c >> 3)
-    const int dot = __shfl_sync(FULL, d1, (lane & 7) * 4 + (lane >> 3));
+  auto terms_bound = [&](int dot, float sx, float rx, float mxn, uint32_t stage) {
     const float qs = qn_s[stage][0], qh = qn_s[stage][1], qr = qn_s[stage][2];
-    float sx, rx, mxn;
-    if (h16) {
-      const __half2 sr = *reinterpret_cast<const __half2*>(&R.m.x);
-      const __half2 mt = *reinterpret_cast<const __half2*>(&R.m.y);
-      sx = __low2float(sr);
-      rx = __high2float(sr);
-      mxn = __low2float(mt);
-      tx = __high2float(mt);
-    } else {
-      sx = __uint_as_float(R.m.x);
-      rx = __uint_as_float(R.m.y);
-      mxn = __uint_as_float(R.m.z);
-      tx = __uint_as_float(R.m.w);
-    }
-    nx = __fadd_ru(mxn, rx);  // >= ||x_h||
-    const float If = (float)dot;  // |I| <= 48 * 127^2: exact in fp32
+    const float If = (float)dot;  // |I| <= 96 * 127^2 < 2^24: exact in fp32
     // s_x s_q I rounded up: round the scale product toward the side that raises it
     const float sp = dot >= 0 ? __fmul_ru(sx, qs) : __fmul_rd(sx, qs);
     return __fadd_ru(__fmul_ru(sp, If), __fmaf_ru(rx, qh, __fmul_ru(mxn, qr)));
+  };
+  auto stageA_bound = [&](const Recs& R, float& tx, float& nx, const int4 qw) {
+    int dt[2];
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      int t = __dp4a((int)R.r[it].x, qw.x, 0);
+      t = __dp4a((int)R.r[it].y, qw.y, t);
+      t = __dp4a((int)R.r[it].z, qw.z, t);
+      t = __dp4a((int)R.r[it].w, qw.w, t);
+      dt[it] = t + __shfl_xor_sync(FULL, t, 1);  // the record's two parts
+    }
+    // candidate c = round (c >> 4), record slot (c & 15): held by lane (c & 15) * 2
+    const int d0 = __shfl_sync(FULL, dt[0], (lane & 15) * 2);
+    const int d1 = __shfl_sync(FULL, dt[1], (lane & 15) * 2);
+    const int dot = lane < 16 ? d0 : d1;
+    const __half2 sr = *reinterpret_cast<const __half2*>(&R.m.z);
+    const __half2 mt = *reinterpret_cast<const __half2*>(&R.m.w);
+    const float sx = __low2float(sr), rx = __high2float(sr), mxn = __low2float(mt);
+    tx = __high2float(mt);
+    nx = __fadd_ru(mxn, rx);  // >= ||x_h||
+    return terms_bound(dot, sx, rx, mxn, 0);
+  };
+  // Stage B (128 B records by id): eight lanes per record (parts 0-5 codes, 6 the fp32
+  // terms, 7 padding), four records per round, eight rounds; each round's integer
+  // dot is reduced over its 8-lane group and handed to the candidate's lane.
+  auto stageB_bound = [&](uint32_t id, float& tx) {
+    const int p8 = lane & 7, g8 = lane >> 3;
+    const uint4* rs = rec + (uint64_t)a.n * 2;  // [n][8] uint4
+    const uint4 m = id != NONE ? __ldcg(rs + (uint64_t)id * 8 + 6) : make_uint4(0, 0, 0, 0);
+    const int4 qw = p8 < 6 ? *reinterpret_cast<const int4*>(&q8_s[1][4 * p8]) : make_int4(0, 0, 0, 0);
+    int dot = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // two halves of four rounds (register budget)
+      uint4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t idr = __shfl_sync(FULL, id, (h * 4 + j) * 4 + g8);
+        v[j] = (idr != NONE && p8 < 6) ? __ldcg(rs + (uint64_t)idr * 8 + p8) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int it = h * 4 + j;
+        int t = __dp4a((int)v[j].x, qw.x, 0);
+        t = __dp4a((int)v[j].y, qw.y, t);
+        t = __dp4a((int)v[j].z, qw.z, t);
+        t = __dp4a((int)v[j].w, qw.w, t);
+        t += __shfl_xor_sync(FULL, t, 4);
+        t += __shfl_xor_sync(FULL, t, 2);
+        t += __shfl_xor_sync(FULL, t, 1);
+        const int got = __shfl_sync(FULL, t, (lane & 3) * 8);  // candidate it * 4 + (lane & 3)
+        if ((lane >> 2) == it) dot = got;
+      }
+    }
+    tx = __uint_as_float(m.w);
+    return terms_bound(dot, __uint_as_float(m.x), __uint_as_float(m.y), __uint_as_float(m.z), 1);
   };
   const float qt1 = qn_s[0][3], qt2 = qn_s[1][3];
   const float qnorm = __fadd_ru(qn_s[0][1], qt1);  // >= ||q||
@@ -2745,10 +2760,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     const uint32_t id = (uint32_t)lane < cnt ? s1q[slot] : NONE;
     const float2 an = (uint32_t)lane < cnt ? s1v[slot] : make_float2(0.f, 0.f);
     h1 += cnt;
-    Recs R;
-    load_recs(id, 1, R);
-    float tx, nx;
-    const float A2 = stage_bound(R, 1, tx, nx, stage_qw(1), false);
+    float tx;
+    const float A2 = stageB_bound(id, tx);
     bool live = false;
     if (id != NONE) {
       const float A = __fadd_ru(an.x, A2);
@@ -2788,11 +2801,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     const uint32_t slot = rslot;
     const uint32_t id = idr[islot * 32 + lane];
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const uint32_t r = it * 8 + grp;
+    for (int it = 0; it < 2; ++it) {  // record r = it * 16 + g16, 16 B part p2 per lane
+      const uint32_t r = it * 16 + g16;
       const uint32_t idv = __shfl_sync(FULL, id, r);
       if (idv != NONE)
-        cp_async16s(ring_sa + ((slot * 32 + r) * 4 + part) * 16, rec + (uint64_t)idv * 4 + part);
+        cp_async16s(ring_sa + (slot * 128 + r * 2 + p2) * 16, rec + (uint64_t)idv * 2 + p2);
     }
   };
   // WALK: the walker's next window -> batch b's slot: its ids (4 B cp.async per lane
@@ -2813,20 +2826,20 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       const uint64_t gprev = __shfl_up_sync(FULL, gp, 1);
       const uint32_t starts = __ballot_sync(FULL, v && (lane == 0 || gp != gprev + 1));
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      if (lane == 0) mbar_arrive_tx(&smbar[w][slot], (uint32_t)__popc(vm) * 64u);
+      if (lane == 0) mbar_arrive_tx(&smbar[w][slot], (uint32_t)__popc(vm) * 32u);
       __syncwarp();
       if ((starts >> lane) & 1u) {
         const uint32_t after = starts & ~((2u << lane) - 1u);  // later run starts
         const uint32_t end = after ? (uint32_t)(__ffs(after) - 1) : (uint32_t)__popc(vm);
-        bulk_g2s(ring + (slot * 32 + lane) * 4, cr + gp * 4, (end - lane) * 64u, &smbar[w][slot]);
+        bulk_g2s(ring + slot * 128 + lane * 2, cr + gp * 2, (end - lane) * 32u, &smbar[w][slot]);
       }
       return;
     }
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const uint32_t r = it * 8 + grp;
+    for (int it = 0; it < 2; ++it) {  // record r = it * 16 + g16, 16 B part p2 per lane
+      const uint32_t r = it * 16 + g16;
       const uint64_t gr = __shfl_sync(FULL, gp, r);
-      if (__shfl_sync(FULL, v, r)) cp_async16s(ring_sa + ((slot * 32 + r) * 4 + part) * 16, cr + gr * 4 + part);
+      if (__shfl_sync(FULL, v, r)) cp_async16s(ring_sa + (slot * 128 + r * 2 + p2) * 16, cr + gr * 2 + p2);
     }
   };
   if constexpr (WALK) {
@@ -2848,7 +2861,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       cp_commit();
     }
   }
-  const int4 qw1 = stage_qw(0);  // (loop-invariant: hoisted out of the bound)
+  const int4 qw1 = stageA_qw();  // (loop-invariant: hoisted out of the bound)
   // batch i: ring slot cs = i % RING, id-ring slot ci = i % IDR; the refill of this
   // iteration goes to ring slot (i + RING - 1) % RING (the slot consumed last), its ids
   // from id-ring slot (i + RING - 1) % IDR, and the ids of batch i + 2 RING - 1 to
@@ -2882,17 +2895,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     }
     const uint32_t slot = cs;
     const uint32_t cid =
-        WALK ? (((idr[slot * 32] >> lane) & 1u) ? ring[(slot * 32 + lane) * 4 + 3].z : NONE)
+        WALK ? (((idr[slot * 32] >> lane) & 1u) ? ring[slot * 128 + lane * 2 + 1].y : NONE)
              : idr[ci * 32 + lane];
     cs = cs + 1 == NS_RING ? 0 : cs + 1;
     ci = ci + 1 == NS_IDR ? 0 : ci + 1;
     Recs cur;
 #pragma unroll
-    for (int it = 0; it < 4; ++it)
-      cur.r[it] = ring[(slot * 32 + it * 8 + grp) * 4 + part];  // (part 3: terms, times qw = 0)
-    cur.m = ring[(slot * 32 + lane) * 4 + 3];
+    for (int it = 0; it < 2; ++it) cur.r[it] = ring[slot * 128 + (it * 16 + g16) * 2 + p2];
+    cur.m = ring[slot * 128 + lane * 2 + 1];
     float tx, nx;
-    const float A1 = stage_bound(cur, 0, tx, nx, qw1, WALK);
+    const float A1 = stageA_bound(cur, tx, nx, qw1);
     bool live = false;
     float N1 = 0.f;
     if (cid != NONE) {
@@ -2930,12 +2942,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     }
   }
   if (lane == 0) {
-    // bytes read: 64 B stage-1 record per candidate, 64 B stage-2 record per stage-1
+    // bytes read: 32 B stage-A record per candidate, 128 B stage-B record per stage-A
     // survivor, and the exact rows
-    if (a.rbytes) atomicAdd(a.rbytes, (nrows + nst2) * 64ull + nfl * 4ull);
-    if (a.dbg) {  // read fraction in row floats: a record counts as 16 floats
+    if (a.rbytes) atomicAdd(a.rbytes, nrows * 32ull + nst2 * 128ull + nfl * 4ull);
+    if (a.dbg) {  // read fraction in row floats: records count as 8 and 32 floats
       atomicAdd(a.dbg, nrows);
-      atomicAdd(a.dbg + 1, (nrows + nst2) * 16ull + nfl);
+      atomicAdd(a.dbg + 1, nrows * 8ull + nst2 * 32ull + nfl);
       atomicAdd(a.dbg + 2, nst2);
       atomicAdd(a.dbg + 3, nfl / (nch * 32));
     }
@@ -3140,25 +3152,16 @@ static uint32_t grouped_shift(uint64_t n) {
   return sm + 64 <= (size_t)co_smem_max() ? gs : 0u;
 }
 
-// Index::q8csr: entry e's stage-1 record = q8rec[ids[e]] (four threads per entry) with
-// the terms part repacked as {s, r | m, t} half2 pairs + the entry's id: the scale is
-// fp16-exact (k_q8_records rounds it up to fp16 before quantizing), the norms are
-// rounded up (still upper bounds), so the walking screen reads the id with the record
-// and no separate ids stream
+// Index::q8csr: entry e's stage-A record = q8rec[ids[e]] (two threads per entry, 16 B
+// each) with the entry's id in the id slot, so the walking screen reads the id with
+// the record and no separate ids stream
 __global__ void k_q8_inline(const uint4* __restrict__ rec, const uint32_t* __restrict__ ids,
                             uint64_t kept, uint4* __restrict__ out) {
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < kept * 4;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < kept * 2;
        t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t id = __ldg(ids + (t >> 2));
-    uint4 v = __ldg(rec + (uint64_t)id * 4 + (t & 3));
-    if ((t & 3) == 3) {
-      const __half2 sr = __halves2half2(__float2half_ru(__uint_as_float(v.x)),
-                                        __float2half_ru(__uint_as_float(v.y)));
-      const __half2 mt = __halves2half2(__float2half_ru(__uint_as_float(v.z)),
-                                        __float2half_ru(__uint_as_float(v.w)));
-      v = make_uint4(*reinterpret_cast<const uint32_t*>(&sr), *reinterpret_cast<const uint32_t*>(&mt),
-                     id, 0u);
-    }
+    const uint32_t id = __ldg(ids + (t >> 1));
+    uint4 v = __ldg(rec + (uint64_t)id * 2 + (t & 1));
+    if (t & 1) v.y = id;
     out[t] = v;
   }
 }
@@ -3166,7 +3169,7 @@ __global__ void k_q8_inline(const uint4* __restrict__ rec, const uint32_t* __res
 static void ensure_q8csr(const Index& ix) {
   std::lock_guard<std::mutex> lk(ix.mu);
   if (ix.q8csr || !ix.q8rec) return;
-  uint4* p = static_cast<uint4*>(dmalloc((size_t)(ix.kept_total + 1) * 64));
+  uint4* p = static_cast<uint4*>(dmalloc((size_t)(ix.kept_total + 1) * 32));
   if (ix.kept_total) {
     k_q8_inline<<<sm_count() * 8, 256, 0, ix.stream>>>(ix.q8rec, ix.ids, ix.kept_total, p);
     FPP_LAUNCH();
