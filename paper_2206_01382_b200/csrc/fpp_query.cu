@@ -2292,12 +2292,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr uint32_t NONE = 0xffffffffu;
   const uint32_t d = a.d, nch = (d + 31) / 32;  // 32-float chunks (rows padded with zeros)
-  double* qd = reinterpret_cast<double*>(smraw);                       // [32 * nch]
-  uint4* ring_all = reinterpret_cast<uint4*>(smraw + (size_t)nch * 32 * 8);  // [NW][RING][32][4]
+  // fixed-size parts first (compile-time offsets: the compiler rematerialises these
+  // addresses under the register cap), the d-dependent query copy last
+  uint4* ring_all = reinterpret_cast<uint4*>(smraw);                   // [NW][RING][2 KB]
   uint32_t* idr_all = reinterpret_cast<uint32_t*>(ring_all + (size_t)NW * NS_RING * 128);  // [NW][IDR][32]
   uint32_t* sq_all = idr_all + (size_t)NW * NS_IDR * 32;               // [NW][QCAP]
   uint32_t* s1_all = sq_all + (size_t)NW * NS_QCAP;                    // [NW][QCAP] stage-2 queue ids
   float2* s1v_all = reinterpret_cast<float2*>(s1_all + (size_t)NW * NS_QCAP);  // [NW][QCAP] (A1, N1)
+  double* qd = reinterpret_cast<double*>(s1v_all + (size_t)NW * NS_QCAP);  // [32 * nch]
   __shared__ unsigned long long thr_key;  // lower bound of the final k-th best (ordered key)
   __shared__ double thr2_s[NW];          // per warp: its ceil(k/NW)-th best
   __shared__ uint32_t nseed_s;
