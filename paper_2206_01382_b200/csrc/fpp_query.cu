@@ -2837,11 +2837,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       }
       return;
     }
-#pragma unroll
-    for (int it = 0; it < 2; ++it) {  // record r = it * 16 + g16, 16 B part p2 per lane
-      const uint32_t r = it * 16 + g16;
-      const uint64_t gr = __shfl_sync(FULL, gp, r);
-      if (__shfl_sync(FULL, v, r)) cp_async16s(ring_sa + (slot * 128 + r * 2 + p2) * 16, cr + gr * 2 + p2);
+    if (v) {  // each lane copies its own record (2 x 16 B: no address shuffles)
+      const uint32_t sa = ring_sa + (slot * 128 + lane * 2) * 16;
+      cp_async16s(sa, cr + gp * 2);
+      cp_async16s(sa + 16, cr + gp * 2 + 1);
     }
   };
   if constexpr (WALK) {
