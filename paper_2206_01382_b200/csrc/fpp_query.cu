@@ -2909,9 +2909,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     bool live = false;
     float N1 = 0.f;
     if (cid != NONE) {
-      N1 = __fmul_ru(__fadd_ru(nx, tx), qnorm);  // >= ||x|| ||q||
+      // (||q|| terms re-read from shared memory: kept in registers they were spilled)
+      const float qh1 = *(volatile float*)&qn_s[0][1], qt1v = *(volatile float*)&qn_s[0][3];
+      N1 = __fmul_ru(__fadd_ru(nx, tx), __fadd_ru(qh1, qt1v));  // >= ||x|| ||q||
       const float mag = __fadd_ru(fabsf(A1), N1);
-      const float ub = __fadd_ru(__fmaf_ru(tx, qt1, A1), __fmul_ru(mag, 1e-6f));
+      const float ub = __fadd_ru(__fmaf_ru(tx, qt1v, A1), __fmul_ru(mag, 1e-6f));
       live = (double)ub >= thr_now();
     }
     const uint32_t live_m = __ballot_sync(FULL, live);
