@@ -713,26 +713,44 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
           }
           pb = npb;
         }
+        // thin tail: lane l takes row r1 + l and finds its prefix length by a binary
+        // search below the previous bound (the staircase is non-increasing), then the
+        // block's pairs are emitted as one flat range, 32 per round (lane f finds its
+        // row by a 5-step search over the rows' exclusive offsets): coalesced stores,
+        // one counter atomic per block
         for (; r1 < g.na && pb > 0; r1 += 32) {
           const uint32_t my = r1 + lane;
-          bool alive = my < g.na;
-          const float x = alive ? g.va[my] : 0.0f;
-          uint32_t cnt = 0;
-          for (uint32_t c0 = 0; c0 < pb; c0 += 4) {
-            float y[4];
-  #pragma unroll
-            for (int u = 0; u < 4; ++u) y[u] = c0 + u < pb ? g.vb[c0 + u] : 0.0f;
-            uint32_t any = 0;
-  #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const uint32_t c = c0 + u;
-              const uint32_t key = pk(x, y[u]);
-              alive = alive && c < pb && key >= Tlo;
-              cnt += alive;
-              any |= __ballot_sync(FULL, alive);
-              emit(alive && !(g.forced && my == 0 && c == 0), key, pack(g.t, g.oa + my, g.ob + c));
+          const float x = my < g.na ? g.va[my] : 0.0f;
+          const uint32_t cnt = my < g.na ? prefix_bs(pk, x, g.vb, pb, Tlo) : 0u;
+          uint32_t incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const uint32_t excl = incl - cnt, tot = __shfl_sync(FULL, incl, 31);
+          // the forced pair (0, 0) is counted in the staircase but never emitted
+          const uint32_t skip0 = (g.forced && r1 == 0 && __shfl_sync(FULL, cnt, 0) > 0) ? 1u : 0u;
+          uint32_t base = 0;
+          if (lane == 0 && tot > skip0) base = smem_fetch_add(&n_cand, tot - skip0);
+          base = __shfl_sync(FULL, base, 0);
+          for (uint32_t f0 = 0; f0 < tot; f0 += 32) {
+            const uint32_t f = f0 + lane;
+            uint32_t l = 0;
+#pragma unroll
+            for (int sft = 16; sft; sft >>= 1) {
+              const uint32_t e = __shfl_sync(FULL, excl, l + sft);
+              if (e <= f) l += sft;
             }
-            if (!any) break;
+            const uint32_t c = f - __shfl_sync(FULL, excl, l);
+            const float xr = __shfl_sync(FULL, x, l);
+            if (f < tot && f >= skip0) {
+              const uint32_t at = base + f - skip0;
+              if (at < a.ccap) {
+                ckey[at] = pk(xr, g.vb[c]);
+                cpair[at] = pack(g.t, g.oa + r1 + l, g.ob + c);
+              }
+            }
           }
           pb = __shfl_sync(FULL, cnt, 31);  // the next block's rows lie below row r1 + 31
         }
