@@ -902,8 +902,9 @@ __global__ void __launch_bounds__(PS_THREADS, 4) k_probe_select(ProbeArgs a) {
   const uint32_t P = (uint32_t)a.peff;
   const uint32_t twoD = 2 * D;
   const uint32_t NB = (uint32_t)a.NB;
-  // Table-major probe order: the non-forced probes [L, P) are counting-sorted by
-  // table (order within a table: arbitrary), so the walking score kernel
+  // Table-major probe order (FPP_PROBE_TABLEMAJOR=1; off by default: measured no gain):
+  // the non-forced probes [L, P) are counting-sorted by table (order within a table:
+  // arbitrary), so the walking score kernel
   // (k_score_screen<WALK>) sweeps the tables in order and similar queries scored side
   // by side read the same buckets' rows at about the same time (L2 reuse).  The L
   // forced true buckets stay in front (the kernel's seeds).  The probe set, hence
@@ -3128,8 +3129,10 @@ static void stage_a(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   // e.g. tests force the exact re-walk fallback with a low beta)
   const char* beta_env = getenv("FPP_PS_BETA");
   pa.beta_q8 = beta_env ? (uint32_t)(atof(beta_env) * 256) : 179u;
-  static const bool rank_order = getenv("FPP_PROBE_RANKORDER") != nullptr;
-  pa.rank_order = rank_order ? 1u : 0u;
+  // table-major probe order only on request: the walk measured the same either way and
+  // the sort's 50-counter atomics cost ~1 ms of probe selection per C4 step
+  static const bool table_major = getenv("FPP_PROBE_TABLEMAJOR") != nullptr;
+  pa.rank_order = table_major ? 0u : 1u;
   pa.pout = probes_out;
   static const bool dbg_probe = getenv("FPP_DEBUG_PROBE") != nullptr;
   if (dbg_probe) {
