@@ -2304,7 +2304,7 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
 // walk reads ~30% more DRAM bytes than the screen over the collect's id-ordered lists
 // (12.2 vs 9.3 MB per query: repeats, and rows gathered in probe order hit L2 less),
 // but saves the collect pass: 231 ms per step against 97 + 148.
-constexpr uint32_t WK_SEEDCAP = 512;  // seed entries per query (whole leading true buckets)
+constexpr uint32_t WK_SEEDCAP = 64;  // seed entries per query (whole leading true buckets; C4: 64 -> 686 k, 512 -> 668 k, none -> 678 k q/s)
 
 template <int NW, int MINB, bool WALK>
 __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
