@@ -2695,20 +2695,17 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   }
 
   // -------------------------------------------------------- record stage bounds
-  // Stage A (32 B records, two 16 B parts): 32 candidates, lane c <-> candidate c (id
-  // NONE = none).  Round it (0-1) holds part p2 of record it * 16 + g16 per lane (part
-  // 0: codes 0-15; part 1: codes 16-19, the id slot and the half2 terms -- the query
-  // weights of its last three words are zero).  Per-candidate terms come from the
-  // candidate's own part 1 (R.m).  Returns A = s_x s_q I + r_x ||q_h|| + m_x r_q
-  // (rounded up) and, in `tx`, the norm of the row after the stage.
+  // Stage A (32 B records, two 16 B parts: codes 0-15 | codes 16-19, the id slot and
+  // the half2 terms): 32 candidates, lane c <-> candidate c (id NONE = none), each lane
+  // reading its own record.  Returns A = s_x s_q I + r_x ||q_h|| + m_x r_q (rounded
+  // up) and, in `tx`, the norm of the row after the stage.
   struct Recs {
-    uint4 r[2];
-    uint4 m;
+    uint4 r[1];  // part 0
+    uint4 m;     // part 1
   };
   const int p2 = lane & 1, g16 = lane >> 1;
-  auto stageA_qw = [&] {
-    return p2 == 0 ? *reinterpret_cast<const int4*>(&q8_s[0][0]) : make_int4(q8_s[0][4], 0, 0, 0);
-  };
+  // lane c bounds its own candidate: the record's 20 codes are part 0 (16 B) and the
+  // first word of part 1 (R.m), five DP4A against the query's codes (qa, qa4)
   auto terms_bound = [&](int dot, float sx, float rx, float mxn, uint32_t stage) {
     const float qs = qn_s[stage][0], qh = qn_s[stage][1], qr = qn_s[stage][2];
     const float If = (float)dot;  // |I| <= 96 * 127^2 < 2^24: exact in fp32
@@ -2716,20 +2713,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     const float sp = dot >= 0 ? __fmul_ru(sx, qs) : __fmul_rd(sx, qs);
     return __fadd_ru(__fmul_ru(sp, If), __fmaf_ru(rx, qh, __fmul_ru(mxn, qr)));
   };
-  auto stageA_bound = [&](const Recs& R, float& tx, float& nx, const int4 qw) {
-    int dt[2];
-#pragma unroll
-    for (int it = 0; it < 2; ++it) {
-      int t = __dp4a((int)R.r[it].x, qw.x, 0);
-      t = __dp4a((int)R.r[it].y, qw.y, t);
-      t = __dp4a((int)R.r[it].z, qw.z, t);
-      t = __dp4a((int)R.r[it].w, qw.w, t);
-      dt[it] = t + __shfl_xor_sync(FULL, t, 1);  // the record's two parts
-    }
-    // candidate c = round (c >> 4), record slot (c & 15): held by lane (c & 15) * 2
-    const int d0 = __shfl_sync(FULL, dt[0], (lane & 15) * 2);
-    const int d1 = __shfl_sync(FULL, dt[1], (lane & 15) * 2);
-    const int dot = lane < 16 ? d0 : d1;
+  auto stageA_bound = [&](const Recs& R, float& tx, float& nx, const int4 qa, const int qa4) {
+    int dot = __dp4a((int)R.r[0].x, qa.x, 0);
+    dot = __dp4a((int)R.r[0].y, qa.y, dot);
+    dot = __dp4a((int)R.r[0].z, qa.z, dot);
+    dot = __dp4a((int)R.r[0].w, qa.w, dot);
+    dot = __dp4a((int)R.m.x, qa4, dot);
     const __half2 sr = *reinterpret_cast<const __half2*>(&R.m.z);
     const __half2 mt = *reinterpret_cast<const __half2*>(&R.m.w);
     const float sx = __low2float(sr), rx = __high2float(sr), mxn = __low2float(mt);
@@ -2881,7 +2870,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       cp_commit();
     }
   }
-  const int4 qw1 = stageA_qw();  // (loop-invariant: hoisted out of the bound)
+  const int4 qa = *reinterpret_cast<const int4*>(&q8_s[0][0]);  // (loop-invariant)
+  const int qa4 = q8_s[0][4];
   // batch i: ring slot cs = i % RING, id-ring slot ci = i % IDR; the refill of this
   // iteration goes to ring slot (i + RING - 1) % RING (the slot consumed last), its ids
   // from id-ring slot (i + RING - 1) % IDR, and the ids of batch i + 2 RING - 1 to
@@ -2920,11 +2910,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     cs = cs + 1 == NS_RING ? 0 : cs + 1;
     ci = ci + 1 == NS_IDR ? 0 : ci + 1;
     Recs cur;
-#pragma unroll
-    for (int it = 0; it < 2; ++it) cur.r[it] = ring[slot * 128 + (it * 16 + g16) * 2 + p2];
+    cur.r[0] = ring[slot * 128 + lane * 2];
     cur.m = ring[slot * 128 + lane * 2 + 1];
     float tx, nx;
-    const float A1 = stageA_bound(cur, tx, nx, qw1);
+    const float A1 = stageA_bound(cur, tx, nx, qa, qa4);
     bool live = false;
     float N1 = 0.f;
     if (cid != NONE) {
