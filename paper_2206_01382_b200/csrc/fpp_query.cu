@@ -2287,6 +2287,10 @@ __device__ __forceinline__ double dkey_inv(unsigned long long k) {
   const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double((long long)b);
 }
+__device__ __forceinline__ int fkey(float x) {  // order-preserving (signed compare)
+  const int b = __float_as_int(x);
+  return b ^ ((b >> 31) & 0x7fffffff);
+}
 
 // Seeds: all entries of the leading true buckets (whole buckets, up to a cap) are
 // scored exactly first, straight into the warps' lists, so the scan starts near the
@@ -2320,6 +2324,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   float2* s1v_all = reinterpret_cast<float2*>(s1_all + (size_t)NW * NS_QCAP);  // [NW][QCAP] (A1, N1)
   double* qd = reinterpret_cast<double*>(s1v_all + (size_t)NW * NS_QCAP);  // [32 * nch]
   __shared__ unsigned long long thr_key;  // lower bound of the final k-th best (ordered key)
+  __shared__ int thr_fk;  // the same bound rounded down to fp32, as an ordered int key (fkey)
   __shared__ double thr2_s[NW];          // per warp: its ceil(k/NW)-th best
   __shared__ uint32_t nseed_s;
   __shared__ float qn_s[Q8_STAGES][4];   // per stage: s_q, ||q_h||, r_q, ||q after the stage||
@@ -2364,7 +2369,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   if (q >= a.nq) break;
   const float* Qr = a.Q + (uint64_t)q * d;
   for (uint32_t j = threadIdx.x; j < nch * 32; j += blockDim.x) qd[j] = j < d ? (double)Qr[j] : 0.0;
-  if (threadIdx.x == 0) thr_key = dkey(-INFINITY);
+  if (threadIdx.x == 0) {
+    thr_key = dkey(-INFINITY);
+    thr_fk = fkey(-INFINITY);
+  }
   if (threadIdx.x < NW) thr2_s[threadIdx.x] = -INFINITY;
   if ((uint32_t)w < Q8_STAGES) {  // quantize the query like the records (k_q8_records)
     const uint32_t W = w ? Q8B_DIMS : Q8A_DIMS;
@@ -2411,8 +2419,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   double bs = -INFINITY;
   uint32_t bi = NONE;
   uint32_t qhead = 0, qtail = 0, h1 = 0, t1 = 0;  // exact queue, stage-2 queue
-  unsigned long long nrows = 0, nst2 = 0, nfl = 0;  // rows screened, stage-2 records, row floats
+  uint32_t nrows = 0, nst2 = 0, nex = 0;  // rows screened, stage-2 records, exact rows
 
+  auto thr_now = [&] { return dkey_inv(*(volatile unsigned long long*)&thr_key); };
   // ---------------------------------------------------------------- exact rows
   // lane r folds row `id` of lane r (NONE: nothing) in the reference's order; `stg` is
   // a free 2 KB slot of the warp's record ring
@@ -2471,15 +2480,25 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
 #pragma unroll
       for (int i = 0; i < NW; ++i) t2 = fmin(t2, lb[i]);
       const double t = kid != NONE ? fmax(kth, t2) : t2;
-      if (t > -INFINITY) atomicMax(&thr_key, dkey(t));
+      if (t > -INFINITY) {
+        atomicMax(&thr_key, dkey(t));
+        // fp32 copy for the record screens: rounded down (a lower bound still), zeros as
+        // -0 (the smallest key of the two zeros, so ub = +-0 >= thr compares as floats do)
+        float tf = __double2float_rd(t);
+        if (tf == 0.f) tf = -0.f;
+        atomicMax(&thr_fk, fkey(tf));
+      }
     }
   };
   auto exact_batch = [&](uint32_t cnt, float* stg) {
     const uint32_t id = (uint32_t)lane < cnt ? sq[(qhead + lane) % NS_QCAP] : NONE;
     qhead += cnt;
     const double acc = exact_fold(id, stg);
-    topk_insert(bs, bi, k, acc, id, id != NONE);
-    if (lane == 0) nfl += (unsigned long long)cnt * nch * 32;
+    // rows below the CTA's lower bound of the final k-th best cannot enter the top-k
+    // nor tie: kept out of the warp list (its entries stay distinct real candidates,
+    // so the bounds published from it stay valid), fewer insertions
+    topk_insert(bs, bi, k, acc, id, id != NONE && acc >= thr_now());
+    nex += cnt;
     publish(bs, bi, thr2_s);
   };
   // admission to the exact stage (lanes with `want`): true for an id not scored exactly
@@ -2553,7 +2572,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
   const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
   uint32_t wk_p0 = 0, wk_p1 = 0, wk_T = 0, wk_e0 = 0, wk_nc = 0, wk_cex = 0, wk_plo = 0, wk_phi = 0;
-  uint32_t wk_nlen = 0, nprod = 0;
+  uint32_t wk_nlen = 0, nprod = 0, wk_tot = 0;  // wk_tot: entries walked
   uint64_t wk_npos = 0;
   bool wk_nhas = false, wk_done = true;
   uint32_t* wk_ctr = nullptr;
@@ -2597,6 +2616,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
         if (lane >= o) incl += y;
       }
       wk_T = __shfl_sync(FULL, incl, 31);
+      wk_tot += wk_T;
       const uint32_t ne = __ballot_sync(FULL, len > 0);
       wk_nc = __popc(ne);
       const uint32_t src = (uint32_t)lane < wk_nc ? __fns(ne, 0, lane + 1) : 0u;
@@ -2762,7 +2782,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   };
   const float qt1 = qn_s[0][3], qt2 = qn_s[1][3];
   const float qnorm = __fadd_ru(qn_s[0][1], qt1);  // >= ||q||
-  auto thr_now = [&] { return dkey_inv(*(volatile unsigned long long*)&thr_key); };
+  // the threshold as an fp32 ordered key (one LDS + integer compare per lane)
+  auto thr_fnow = [&] { return *(volatile int*)&thr_fk; };
 
   // stage 2 of 32 stage-1 survivors: bound A1 + A2 + t2 ||q after stage 2||
   auto stage2_batch = [&](uint32_t cnt) {
@@ -2777,7 +2798,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       const float A = __fadd_ru(an.x, A2);
       const float mag = __fadd_ru(__fadd_ru(fabsf(an.x), fabsf(A2)), an.y);
       const float ub = __fadd_ru(__fmaf_ru(tx, qt2, A), __fmul_ru(mag, 1e-6f));
-      live = (double)ub >= thr_now();
+      live = fkey(ub) >= thr_fnow();
     }
     live = admit(id, live);  // every id scored exactly at most once
     push_exact(id, live);
@@ -2853,6 +2874,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   };
   if constexpr (WALK) {
     wk_begin(pstart, (uint32_t)a.peff, &wctr_s[1]);
+    nrows = wk_tot;  // (the seeds' entries; subtracted below)
 #pragma unroll
     for (uint32_t j = 0; j + 1 < NS_RING; ++j) {
       produce(j);
@@ -2870,8 +2892,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       cp_commit();
     }
   }
-  const int4 qa = *reinterpret_cast<const int4*>(&q8_s[0][0]);  // (loop-invariant)
-  const int qa4 = q8_s[0][4];
   // batch i: ring slot cs = i % RING, id-ring slot ci = i % IDR; the refill of this
   // iteration goes to ring slot (i + RING - 1) % RING (the slot consumed last), its ids
   // from id-ring slot (i + RING - 1) % IDR, and the ids of batch i + 2 RING - 1 to
@@ -2913,6 +2933,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     cur.r[0] = ring[slot * 128 + lane * 2];
     cur.m = ring[slot * 128 + lane * 2 + 1];
     float tx, nx;
+    // the query codes re-read from shared memory per batch (a broadcast LDS.128 + LDS:
+    // hoisted into registers they were spilled under the 80-register cap)
+    int4 qa;
+    int qa4;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%5];\n\tld.shared.s32 %4, [%5+16];"
+                 : "=r"(qa.x), "=r"(qa.y), "=r"(qa.z), "=r"(qa.w), "=r"(qa4)
+                 : "r"((uint32_t)__cvta_generic_to_shared(&q8_s[0][0])));
     const float A1 = stageA_bound(cur, tx, nx, qa, qa4);
     bool live = false;
     float N1 = 0.f;
@@ -2922,7 +2949,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       N1 = __fmul_ru(__fadd_ru(nx, tx), __fadd_ru(qh1, qt1v));  // >= ||x|| ||q||
       const float mag = __fadd_ru(fabsf(A1), N1);
       const float ub = __fadd_ru(__fmaf_ru(tx, qt1v, A1), __fmul_ru(mag, 1e-6f));
-      live = (double)ub >= thr_now();
+      live = fkey(ub) >= thr_fnow();
     }
     const uint32_t live_m = __ballot_sync(FULL, live);
     if (live) {
@@ -2931,7 +2958,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       s1v[pos] = make_float2(A1, N1);
     }
     t1 += __popc(live_m);
-    nrows += __popc(__ballot_sync(FULL, cid != NONE));
+    if constexpr (!WALK) nrows += __popc(__ballot_sync(FULL, cid != NONE));  // (WALK: chunk totals)
     __syncwarp();  // slot i % RING is refilled by the next iteration's issue
   }
   if constexpr (WALK && NS_TMA) {  // the RING - 1 windows produced past the end (empty)
@@ -2944,6 +2971,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   }
   cp_wait<0>();
   __syncwarp();
+  if constexpr (WALK) nrows = wk_tot - nrows;
   while (t1 != h1 || qtail != qhead) {
     if (t1 != h1 && qtail - qhead < 32) {
       stage2_batch(min(32u, t1 - h1));
@@ -2955,12 +2983,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   if (lane == 0) {
     // bytes read: 32 B stage-A record per candidate, 128 B stage-B record per stage-A
     // survivor, and the exact rows
+    const unsigned long long nfl = (unsigned long long)nex * nch * 32;  // exact row floats
     if (a.rbytes) atomicAdd(a.rbytes, nrows * 32ull + nst2 * 128ull + nfl * 4ull);
     if (a.dbg) {  // read fraction in row floats: records count as 8 and 32 floats
-      atomicAdd(a.dbg, nrows);
+      atomicAdd(a.dbg, (unsigned long long)nrows);
       atomicAdd(a.dbg + 1, nrows * 8ull + nst2 * 32ull + nfl);
-      atomicAdd(a.dbg + 2, nst2);
-      atomicAdd(a.dbg + 3, nfl / (nch * 32));
+      atomicAdd(a.dbg + 2, (unsigned long long)nst2);
+      atomicAdd(a.dbg + 3, (unsigned long long)nex);
     }
   }
   // CTA merge of the warp lists
