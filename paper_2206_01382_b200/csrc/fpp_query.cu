@@ -2332,6 +2332,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   __shared__ double mg_s[NW][32];
   __shared__ uint32_t mg_i[NW][32];
   __shared__ uint32_t q_s, wctr_s[2], logn_s;  // query, walker chunk counters, log length
+  __shared__ uint32_t wk_rng_s[2][2];          // walker ranges: seeds, main walk
+  __shared__ uint32_t cnt_s[NW][2];            // per warp: stage-2 records, exact rows
   __shared__ uint32_t seedh[NS_SH];     // lists: the seeds' ids (open addressing)
   __shared__ __align__(8) uint64_t smbar[WALK && NS_TMA ? NW : 1][NS_RING];  // TMA: per ring slot
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -2343,8 +2345,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   uint32_t* s1q = s1_all + (size_t)w * NS_QCAP;   // survivors of stage 1 -> stage 2
   float2* s1v = s1v_all + (size_t)w * NS_QCAP;
   // WALK: the CTA's visited bitmap (exact-stage admission, every id scored once)
-  uint32_t* const bm = a.gbm ? a.gbm + (size_t)blockIdx.x * a.nwords : nullptr;
-  uint32_t* const wlog = a.gbm ? a.wlog + (size_t)blockIdx.x * a.logcap : nullptr;
+  // (the visited bitmap / log pointers are formed where used, from the parameters:
+  // no registers held across the hot loop)
+  auto bm_of = [&] { return a.gbm + (size_t)blockIdx.x * a.nwords; };
+  auto wlog_of = [&] { return a.wlog + (size_t)blockIdx.x * a.logcap; };
   const uint4* rec = reinterpret_cast<const uint4*>(a.xtail);  // [stages][n][4] 16 B parts
   uint32_t mph = 0;  // TMA: parity of each ring slot's next completion (bit per slot)
   if constexpr (WALK && NS_TMA) {
@@ -2361,6 +2365,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   if (threadIdx.x == 0) {  // persistent CTAs fetch queries from a counter
     q_s = a.qctr ? atomicAdd(a.qctr, 1u) : blockIdx.x;
     wctr_s[0] = wctr_s[1] = 0;
+    wk_rng_s[0][0] = wk_rng_s[0][1] = wk_rng_s[1][0] = 0;
+    wk_rng_s[1][1] = (uint32_t)a.peff;
     logn_s = 0;
   }
   for (uint32_t i = threadIdx.x; i < NS_SH; i += blockDim.x) seedh[i] = NONE;
@@ -2373,7 +2379,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     thr_key = dkey(-INFINITY);
     thr_fk = fkey(-INFINITY);
   }
-  if (threadIdx.x < NW) thr2_s[threadIdx.x] = -INFINITY;
+  if (threadIdx.x < NW) {
+    thr2_s[threadIdx.x] = -INFINITY;
+    cnt_s[threadIdx.x][0] = cnt_s[threadIdx.x][1] = 0;
+  }
   if ((uint32_t)w < Q8_STAGES) {  // quantize the query like the records (k_q8_records)
     const uint32_t W = w ? Q8B_DIMS : Q8A_DIMS;
     const uint32_t lo = w ? Q8A_DIMS : 0u, hi = min(d, lo + W);
@@ -2419,7 +2428,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   double bs = -INFINITY;
   uint32_t bi = NONE;
   uint32_t qhead = 0, qtail = 0, h1 = 0, t1 = 0;  // exact queue, stage-2 queue
-  uint32_t nrows = 0, nst2 = 0, nex = 0;  // rows screened, stage-2 records, exact rows
+  uint32_t nrows = 0;  // rows screened (stage-2 records and exact rows: cnt_s)
 
   auto thr_now = [&] { return dkey_inv(*(volatile unsigned long long*)&thr_key); };
   // ---------------------------------------------------------------- exact rows
@@ -2498,7 +2507,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     // nor tie: kept out of the warp list (its entries stay distinct real candidates,
     // so the bounds published from it stay valid), fewer insertions
     topk_insert(bs, bi, k, acc, id, id != NONE && acc >= thr_now());
-    nex += cnt;
+    if (lane == 0) cnt_s[w][1] += cnt;
     publish(bs, bi, thr2_s);
   };
   // admission to the exact stage (lanes with `want`): true for an id not scored exactly
@@ -2523,7 +2532,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   };
   auto admit = [&](uint32_t id, bool want) {
     bool fresh = false;
-    if (bm) {  // WALK: lists repeat ids
+    if (a.gbm) {  // WALK: lists repeat ids
       // first the shared-memory hash (a CAS on the first empty slot of the id's probe
       // sequence; slots only fill, so an id whose sequence is full of other ids can
       // never enter later either): 1 = inserted, 0 = present; ids with a full
@@ -2542,7 +2551,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       bool viab = false;
       if (want && res < 0) {
         const uint32_t bit = 1u << (id & 31);
-        viab = !(atomicOr(bm + (id >> 5), bit) & bit);
+        viab = !(atomicOr(bm_of() + (id >> 5), bit) & bit);
       }
       fresh = res == 1 || viab;
       const uint32_t bal = __ballot_sync(FULL, viab);
@@ -2550,7 +2559,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
         uint32_t base = 0;
         if (lane == 0) base = atomicAdd(&logn_s, (uint32_t)__popc(bal));
         base = __shfl_sync(FULL, base, 0) + __popc(bal & lt_mask);
-        if (viab && base < a.logcap) wlog[base] = id;
+        if (viab && base < a.logcap) wlog_of()[base] = id;
       }
     } else {
       fresh = want && !seed_has(id);
@@ -2569,30 +2578,30 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   // counter (the next chunk's (pos, len) loads in flight while the current one is
   // walked); wk_next() returns lane l's id of the next 32-entry window (NONE past a
   // chunk's end) and sets wk_done, with NONE, once the range is exhausted.
-  const uint64_t* pp = a.ppos + (uint64_t)q * a.peff;
+  // (the walk's range and chunk counter live in shared memory, wk_rng_s[phase]: read
+  // once per 32-probe chunk, they need no registers in the hot loop)
   const uint32_t* pl = a.plen + (uint64_t)q * a.peff;
-  uint32_t wk_p0 = 0, wk_p1 = 0, wk_T = 0, wk_e0 = 0, wk_nc = 0, wk_cex = 0, wk_plo = 0, wk_phi = 0;
-  uint32_t wk_nlen = 0, nprod = 0, wk_tot = 0;  // wk_tot: entries walked
+  uint32_t wk_T = 0, wk_e0 = 0, wk_nc = 0, wk_cex = 0, wk_plo = 0, wk_phi = 0;
+  uint32_t wk_nlen = 0, nprod = 0, wk_tot = 0, wk_ph = 0;  // wk_tot: entries walked
   uint64_t wk_npos = 0;
   bool wk_nhas = false, wk_done = true;
-  uint32_t* wk_ctr = nullptr;
   auto wk_fetch = [&] {
     uint32_t c = 0;
-    if (lane == 0) c = atomicAdd(wk_ctr, 1u);
+    if (lane == 0) c = atomicAdd(&wctr_s[wk_ph], 1u);
     c = __shfl_sync(FULL, c, 0);
-    const uint32_t p = wk_p0 + c * 32 + lane;
-    wk_nhas = wk_p0 + c * 32 < wk_p1;
+    const uint32_t p0 = wk_rng_s[wk_ph][0], p1 = wk_rng_s[wk_ph][1];
+    const uint32_t p = p0 + c * 32 + lane;
+    wk_nhas = p0 + c * 32 < p1;
     wk_nlen = 0;
     wk_npos = 0;
-    if (p < wk_p1) {
-      wk_nlen = pl[p];
-      wk_npos = pp[p];
+    if (p < p1) {
+      const uint64_t o = (uint64_t)q_s * a.peff + p;
+      wk_nlen = __ldg(a.plen + o);
+      wk_npos = __ldg(a.ppos + o);
     }
   };
-  auto wk_begin = [&](uint32_t p0, uint32_t p1, uint32_t* ctr) {
-    wk_p0 = p0;
-    wk_p1 = p1;
-    wk_ctr = ctr;
+  auto wk_begin = [&](uint32_t ph) {
+    wk_ph = ph;
     wk_T = wk_e0 = 0;
     wk_done = false;
     nprod = 0;
@@ -2657,7 +2666,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   if (a.nseedp) {
     // leading true buckets whose cumulative length stays <= the seed cap (lists: half
     // the seed hash, so its load stays <= 1/2)
-    const uint32_t seedcap = bm ? a.seedcap : min(a.seedcap, NS_SH / 2);
+    const uint32_t seedcap = a.gbm ? a.seedcap : min(a.seedcap, NS_SH / 2);
     if (w == 0) {
       uint32_t acc = 0, cnt = 0;
       for (uint32_t p0 = 0; p0 < a.nseedp; p0 += 32) {
@@ -2674,12 +2683,15 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
         if (ok != FULL) break;
         acc += __shfl_sync(FULL, incl, 31);
       }
-      if (lane == 0) nseed_s = cnt;
+      if (lane == 0) {
+        nseed_s = cnt;
+        wk_rng_s[0][1] = wk_rng_s[1][0] = cnt;
+      }
     }
     __syncthreads();
     pstart = nseed_s;
-    wk_begin(0, pstart, &wctr_s[0]);
-    if (bm) {  // WALK: admitted through the bitmap and scored as they come
+    wk_begin(0);
+    if (a.gbm) {  // WALK: admitted through the bitmap and scored as they come
       for (;;) {
         const uint32_t id = wk_next();
         if (wk_done) break;
@@ -2734,11 +2746,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     return __fadd_ru(__fmul_ru(sp, If), __fmaf_ru(rx, qh, __fmul_ru(mxn, qr)));
   };
   auto stageA_bound = [&](const Recs& R, float& tx, float& nx, const int4 qa, const int qa4) {
-    int dot = __dp4a((int)R.r[0].x, qa.x, 0);
-    dot = __dp4a((int)R.r[0].y, qa.y, dot);
-    dot = __dp4a((int)R.r[0].z, qa.z, dot);
-    dot = __dp4a((int)R.r[0].w, qa.w, dot);
-    dot = __dp4a((int)R.m.x, qa4, dot);
+    int d0 = __dp4a((int)R.r[0].x, qa.x, 0);  // (two chains: shorter dependency)
+    int d1 = __dp4a((int)R.r[0].z, qa.z, 0);
+    d0 = __dp4a((int)R.r[0].y, qa.y, d0);
+    d1 = __dp4a((int)R.r[0].w, qa.w, d1);
+    d0 = __dp4a((int)R.m.x, qa4, d0);
+    const int dot = d0 + d1;
     const __half2 sr = *reinterpret_cast<const __half2*>(&R.m.z);
     const __half2 mt = *reinterpret_cast<const __half2*>(&R.m.w);
     const float sx = __low2float(sr), rx = __high2float(sr), mxn = __low2float(mt);
@@ -2802,7 +2815,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     }
     live = admit(id, live);  // every id scored exactly at most once
     push_exact(id, live);
-    nst2 += cnt;
+    if (lane == 0) cnt_s[w][0] += cnt;
   };
 
   // ---------------------------------------------------------------- stage 1
@@ -2846,8 +2859,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   auto produce = [&](uint32_t slot) {
     uint64_t gp = 0;
     const bool v = wk_step(gp);
-    const uint32_t vm = __ballot_sync(FULL, v);  // lanes with an entry (the record holds the id)
-    if (lane == 0) idr[slot * 32] = vm;          // (WALK: word 0 of id-ring slot `slot`)
+    // a lane without an entry marks its own record slot empty (id NONE; the lane reads
+    // it back itself, so no ordering beyond program order is needed)
+    if (!v) ring[slot * 128 + lane * 2 + 1] = make_uint4(0u, NONE, 0u, 0u);
     const uint4* cr = reinterpret_cast<const uint4*>(a.csrrec);
     if constexpr (NS_TMA) {
       // the window's valid lanes are a prefix, split into runs of consecutive CSR
@@ -2857,6 +2871,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       const uint64_t gprev = __shfl_up_sync(FULL, gp, 1);
       const uint32_t starts = __ballot_sync(FULL, v && (lane == 0 || gp != gprev + 1));
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      const uint32_t vm = __ballot_sync(FULL, v);
       if (lane == 0) mbar_arrive_tx(&smbar[w][slot], (uint32_t)__popc(vm) * 32u);
       __syncwarp();
       if ((starts >> lane) & 1u) {
@@ -2873,7 +2888,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     }
   };
   if constexpr (WALK) {
-    wk_begin(pstart, (uint32_t)a.peff, &wctr_s[1]);
+    wk_begin(1);
     nrows = wk_tot;  // (the seeds' entries; subtracted below)
 #pragma unroll
     for (uint32_t j = 0; j + 1 < NS_RING; ++j) {
@@ -2924,14 +2939,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       __syncwarp();
     }
     const uint32_t slot = cs;
-    const uint32_t cid =
-        WALK ? (((idr[slot * 32] >> lane) & 1u) ? ring[slot * 128 + lane * 2 + 1].y : NONE)
-             : idr[ci * 32 + lane];
-    cs = cs + 1 == NS_RING ? 0 : cs + 1;
-    ci = ci + 1 == NS_IDR ? 0 : ci + 1;
     Recs cur;
     cur.r[0] = ring[slot * 128 + lane * 2];
     cur.m = ring[slot * 128 + lane * 2 + 1];
+    const uint32_t cid = WALK ? cur.m.y : idr[ci * 32 + lane];  // (WALK: the record's id)
+    cs = cs + 1 == NS_RING ? 0 : cs + 1;
+    ci = ci + 1 == NS_IDR ? 0 : ci + 1;
     float tx, nx;
     // the query codes re-read from shared memory per batch (a broadcast LDS.128 + LDS:
     // hoisted into registers they were spilled under the 80-register cap)
@@ -2941,16 +2954,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
                  : "=r"(qa.x), "=r"(qa.y), "=r"(qa.z), "=r"(qa.w), "=r"(qa4)
                  : "r"((uint32_t)__cvta_generic_to_shared(&q8_s[0][0])));
     const float A1 = stageA_bound(cur, tx, nx, qa, qa4);
-    bool live = false;
-    float N1 = 0.f;
-    if (cid != NONE) {
-      // (||q|| terms re-read from shared memory: kept in registers they were spilled)
-      const float qh1 = *(volatile float*)&qn_s[0][1], qt1v = *(volatile float*)&qn_s[0][3];
-      N1 = __fmul_ru(__fadd_ru(nx, tx), __fadd_ru(qh1, qt1v));  // >= ||x|| ||q||
-      const float mag = __fadd_ru(fabsf(A1), N1);
-      const float ub = __fadd_ru(__fmaf_ru(tx, qt1v, A1), __fmul_ru(mag, 1e-6f));
-      live = fkey(ub) >= thr_fnow();
-    }
+    // (branch-free: lanes without an entry compute on the empty record and drop out
+    // at the compare; ||q|| terms re-read from shared memory: kept in registers they
+    // were spilled)
+    const float qh1 = *(volatile float*)&qn_s[0][1], qt1v = *(volatile float*)&qn_s[0][3];
+    const float N1 = __fmul_ru(__fadd_ru(nx, tx), __fadd_ru(qh1, qt1v));  // >= ||x|| ||q||
+    const float mag = __fadd_ru(fabsf(A1), N1);
+    const float ub = __fadd_ru(__fmaf_ru(tx, qt1v, A1), __fmul_ru(mag, 1e-6f));
+    const bool live = cid != NONE && fkey(ub) >= thr_fnow();
     const uint32_t live_m = __ballot_sync(FULL, live);
     if (live) {
       const uint32_t pos = (t1 + __popc(live_m & lt_mask)) % NS_QCAP;
@@ -2983,6 +2994,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   if (lane == 0) {
     // bytes read: 32 B stage-A record per candidate, 128 B stage-B record per stage-A
     // survivor, and the exact rows
+    const uint32_t nst2 = cnt_s[w][0], nex = cnt_s[w][1];
     const unsigned long long nfl = (unsigned long long)nex * nch * 32;  // exact row floats
     if (a.rbytes) atomicAdd(a.rbytes, nrows * 32ull + nst2 * 128ull + nfl * 4ull);
     if (a.dbg) {  // read fraction in row floats: records count as 8 and 32 floats
@@ -3013,7 +3025,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       a.stats[q].exact = a.uq_all ? a.uq_all[q] : Len;
     }
   }
-  if (bm) {  // leave the visited bitmap clear for the next query
+  if (a.gbm) {  // leave the visited bitmap clear for the next query
+    uint32_t* const bm = bm_of();
+    const uint32_t* const wlog = wlog_of();
     __syncthreads();
     const uint32_t nl = logn_s;
     if (nl > a.logcap) {  // log overflow (pathological survivor counts): clear it all
