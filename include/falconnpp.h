@@ -28,10 +28,11 @@
 extern "C" {
 #endif
 
-#define FPP_ABI_VERSION 5  /* 2: fpp_query_stats.exact, SimHash rerank; 3: fpp_timings.score_bytes;
+#define FPP_ABI_VERSION 6  /* 2: fpp_query_stats.exact, SimHash rerank; 3: fpp_timings.score_bytes;
                               4: fpp_synth_rows, fpp_merge_topk, per-call query contexts;
                               5: fpp_timings.score_launches, fpp_query_probe_sets_device,
-                                 fpp_query_from_probe_sets_device */
+                                 fpp_query_from_probe_sets_device;
+                              6: fpp_multi_* (single-process multi-GPU index) */
 
 /* error classes ("one exit code per error class") */
 #define FPP_OK 0
@@ -215,6 +216,32 @@ int fpp_shard_slots(fpp_index* idx, const uint32_t* global_hist_dev, uint64_t* s
 int fpp_shard_prefix(fpp_index* idx, const uint32_t* global_hist_dev, uint64_t* prefix_dev);
 int fpp_shard_finish(fpp_index* idx, const uint32_t* global_hist_dev,
                      const uint64_t* all_prefix_dev, uint32_t world);
+
+/* ------------------------- multi-GPU index in one process (SURVEY 8(b) num_gpus, 8(e))
+ * build(dataset, config) over num_gpus devices and search
+ * over the sharded index.  Shard g holds the contiguous global ids
+ * [g*n/G, (g+1)*n/G) on devices[g] (NULL = devices 0..num_gpus-1; an ordinal may
+ * repeat, the shards then share that device) and is built by the global-filter
+ * protocol above, so the union of the shards equals the 1-GPU index and every answer
+ * (ids, scores, stats) is identical for every num_gpus.  A query batch
+ * is sent to every device; hashing + probe selection are split across the shards and
+ * the probe sets all-gathered; every shard scores its own candidates; shard g merges
+ * the G top-k lists of its slice of the batch (score desc, id asc) and writes that
+ * slice of ids/scores.  Exchanges are device-to-device copies (NVLink peer access is
+ * enabled between the devices at build).  X, Q, ids, scores, stats are host buffers
+ * as in fpp_build / fpp_query; p->device and p->id_offset are ignored / must be 0;
+ * centering is FPP_ERR_UNSUPPORTED (center X first).  Calls on one fpp_multi
+ * serialise. */
+typedef struct fpp_multi fpp_multi;
+int fpp_multi_build(const float* X, uint64_t n, uint32_t d, const fpp_params* p, uint32_t num_gpus,
+                    const int32_t* devices, fpp_multi** out);
+int fpp_multi_query(const fpp_multi* m, const float* Q, uint64_t nq, uint32_t k, uint32_t qprobes,
+                    uint32_t* ids, double* scores, fpp_query_stats* stats);
+uint32_t fpp_multi_shards(const fpp_multi* m);
+/* shard g as a plain index (introspection: fpp_index_info_get, fpp_table_csr, ...);
+   owned by the fpp_multi */
+const fpp_index* fpp_multi_shard(const fpp_multi* m, uint32_t g);
+void fpp_multi_free(fpp_multi* m);
 
 /* -------------------------------------------------------------- host helpers */
 /* ---- multi-GPU query merge: after an all-gather of the G shards'

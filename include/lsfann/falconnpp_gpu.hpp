@@ -124,4 +124,60 @@ class Index {
   fpp_index* h_ = nullptr;
 };
 
+// build(X, L, K, D, iProbes, alpha, ..., num_gpus) / query over num_gpus devices of one
+// process (fpp_multi_*): contiguous id shards with the global alpha/kappa filter, so
+// the answers equal Index's for every num_gpus.  devices: one CUDA
+// ordinal per shard (empty = 0..num_gpus-1; ordinals may repeat).
+class MultiIndex {
+ public:
+  static MultiIndex build(std::span<const float> X, std::size_t n, std::size_t d, uint32_t L,
+                          uint32_t K, uint32_t D, uint32_t iProbes, float alpha,
+                          uint32_t num_gpus, std::span<const int32_t> devices = {},
+                          uint32_t kappa = 20, uint64_t seed = 1,
+                          uint32_t mode = FPP_MODE_FALCONNPP) {
+    if (X.size() != n * d) throw std::invalid_argument("build: X.size() != n*d");
+    if (!devices.empty() && devices.size() != num_gpus)
+      throw std::invalid_argument("build: devices.size() != num_gpus");
+    fpp_params p;
+    fpp_default_params(&p);
+    p.L = L; p.K = K; p.D = D; p.iprobes = iProbes; p.alpha = alpha; p.kappa = kappa;
+    p.seed = seed; p.mode = mode;
+    fpp_multi* h = nullptr;
+    check(fpp_multi_build(X.data(), n, static_cast<uint32_t>(d), &p, num_gpus,
+                          devices.empty() ? nullptr : devices.data(), &h));
+    return MultiIndex(h);
+  }
+
+  QueryResult query(std::span<const float> Q, std::size_t nq, uint32_t k, uint32_t qProbes,
+                    bool with_stats = false) const {
+    QueryResult r;
+    r.ids.resize(nq * k);
+    r.scores.resize(nq * k);
+    if (with_stats) r.stats.resize(nq);
+    check(fpp_multi_query(h_, Q.data(), nq, k, qProbes, r.ids.data(), r.scores.data(),
+                          with_stats ? r.stats.data() : nullptr));
+    return r;
+  }
+
+  uint32_t num_shards() const { return fpp_multi_shards(h_); }
+  fpp_index_info shard_info(uint32_t g) const {
+    fpp_index_info i;
+    check(fpp_index_info_get(fpp_multi_shard(h_, g), &i));
+    return i;
+  }
+
+  MultiIndex(MultiIndex&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  MultiIndex& operator=(MultiIndex&& o) noexcept {
+    if (this != &o) { fpp_multi_free(h_); h_ = std::exchange(o.h_, nullptr); }
+    return *this;
+  }
+  MultiIndex(const MultiIndex&) = delete;
+  MultiIndex& operator=(const MultiIndex&) = delete;
+  ~MultiIndex() { fpp_multi_free(h_); }
+
+ private:
+  explicit MultiIndex(fpp_multi* h) : h_(h) {}
+  fpp_multi* h_ = nullptr;
+};
+
 }  // namespace lsfann::gpu

@@ -32,7 +32,7 @@ LIB_PATH = os.environ.get("FPP_LIB_PATH") or _build.LIB
 
 FPP_OK = 0
 MODES = {"falconnpp": 0, "falconn_baseline": 1}
-ABI_VERSION = 5  # include/falconnpp.h FPP_ABI_VERSION this binding was written against
+ABI_VERSION = 6  # include/falconnpp.h FPP_ABI_VERSION this binding was written against
 ERRORS = {1: "INVALID_ARGUMENT", 2: "EMPTY_DATASET", 3: "DIMENSION", 4: "OUT_OF_RANGE",
           5: "NON_FINITE", 6: "ZERO_NORM", 7: "CUDA", 8: "OUT_OF_MEMORY", 9: "UNSUPPORTED",
           10: "FORMAT", 11: "IO"}
@@ -174,6 +174,11 @@ SIGNATURES = [
     ("fpp_synth", C.c_int, [vp, u64, u32, u32, f32, u64, u32, i32]),
     ("fpp_synth_rows", C.c_int, [vp, u64, u64, u32, u32, f32, u64, u32, i32]),
     ("fpp_merge_topk", C.c_int, [vp, vp, u32, u64, u32, vp, vp, i32, vp]),
+    ("fpp_multi_build", C.c_int, [vp, u64, u32, C.POINTER(Params), u32, vp, C.POINTER(vp)]),
+    ("fpp_multi_query", C.c_int, [vp, vp, u64, u32, u32, vp, vp, vp]),
+    ("fpp_multi_shards", u32, [vp]),
+    ("fpp_multi_shard", vp, [vp, u32]),
+    ("fpp_multi_free", None, [vp]),
 ]
 
 _lib = None
@@ -405,9 +410,9 @@ class Index:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and _lib is not None:
+        if h and _lib is not None and getattr(self, "_borrowed", None) is None:
             _lib.fpp_free(h)
-            self._h = None
+        self._h = None
 
     def close(self):
         self.__del__()
@@ -594,6 +599,77 @@ class Index:
 
     def reset_timings(self) -> None:
         _check(lib().fpp_timings_reset(self._h))
+
+
+class MultiIndex:
+    """build(X, config) / query(Q, k, qProbes) over num_gpus devices in one process
+    (fpp_multi_*, include/falconnpp.h): contiguous id shards built by the global-filter
+    protocol, so every answer equals the 1-GPU index's for every num_gpus.
+    devices: one CUDA ordinal per shard (default 0..num_gpus-1; ordinals may repeat)."""
+
+    def __init__(self, handle, params: Params, n: int, d: int):
+        self._h = handle
+        self.params = params
+        self.n, self.d = n, d
+
+    @classmethod
+    def build(cls, X, L: int, K: int, D: int, iProbes: int, alpha: float, kappa: int = 20,
+              seed: int = 1, num_gpus: int = 1, devices=None, mode: str = "falconnpp"):
+        p = Params(L, K, D, iProbes, kappa, alpha, seed, -1, 0, 0, 0,
+                   MODES[mode] if isinstance(mode, str) else int(mode))
+        X = _f32(X)
+        n, d = X.shape
+        dv = None
+        if devices is not None:
+            if len(devices) != num_gpus:
+                raise FppInvalidArgument("build: len(devices) != num_gpus")
+            dv = (C.c_int32 * num_gpus)(*[int(x) for x in devices])
+        h = C.c_void_p()
+        _check(lib().fpp_multi_build(_ptr(X), n, d, C.byref(p), num_gpus,
+                                     C.cast(dv, C.c_void_p) if dv is not None else None,
+                                     C.byref(h)))
+        return cls(h, p, n, d)
+
+    @property
+    def num_shards(self) -> int:
+        return lib().fpp_multi_shards(self._h)
+
+    def shard(self, g: int) -> "Index":
+        """Shard g as a borrowed Index (introspection; owned by this MultiIndex)."""
+        h = lib().fpp_multi_shard(self._h, g)
+        if not h:
+            raise FppOutOfRange(f"shard {g} of {self.num_shards}")
+        ix = Index(None, self.params, 0, self.d)
+        ix._h = C.c_void_p(h)
+        ix._borrowed = self  # keeps the owner alive; Index.__del__ must not free it
+        inf = ix.info()
+        ix.n = inf["n"]
+        return ix
+
+    def query(self, Q, k: int, qProbes: int, return_stats: bool = False):
+        Q = _f32(Q)
+        if Q.shape[1] != self.d:
+            raise FppDimensionError(f"search: query dim {Q.shape[1]} != index dim {self.d}")
+        nq = Q.shape[0]
+        ids = np.empty((nq, k), np.uint32)
+        sc = np.empty((nq, k), np.float64)
+        st = (QueryStats * max(nq, 1))() if return_stats else None
+        stp = C.cast(st, C.c_void_p) if st is not None else None
+        _check(lib().fpp_multi_query(self._h, _ptr(Q), nq, k, qProbes, _ptr(ids), _ptr(sc), stp))
+        if return_stats:
+            stats = np.array([(s.probes, s.entries, s.candidates, s.exact) for s in st[:nq]],
+                             dtype=np.uint64).reshape(nq, 4)
+            return ids, sc, stats
+        return ids, sc
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.fpp_multi_free(h)
+            self._h = None
+
+    def close(self):
+        self.__del__()
 
 
 def center(X):

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <new>
 #include <string>
 #include <vector>
@@ -607,6 +608,10 @@ static int guarded(F&& f) {
     return FPP_ERR_CUDA;
   }
 }
+
+namespace fpp {
+int guarded_call(const std::function<void()>& f) { return guarded(f); }
+}  // namespace fpp
 
 extern "C" {
 

@@ -36,6 +36,15 @@ int main() {
   auto r2 = iy.query(Q, nq, 10, 64, true);
   if (r2.ids != r.ids || r2.scores != r.scores) return 1;
   std::remove(path);
+  // the same index over three shards of one process (all on device 0 here)
+  const int32_t devs[3] = {0, 0, 0};
+  auto mx = lsfann::gpu::MultiIndex::build(X, n, d, 4, 2, 32, 3, 0.1f, 3, devs);
+  auto r3 = mx.query(Q, nq, 10, 64, true);
+  if (mx.num_shards() != 3 || r3.ids != r.ids || r3.scores != r.scores) return 1;
+  for (std::size_t i = 0; i < nq; ++i)
+    if (r3.stats[i].probes != r.stats[i].probes || r3.stats[i].entries != r.stats[i].entries ||
+        r3.stats[i].candidates != r.stats[i].candidates)
+      return 1;
   std::printf("cpp ok: kept %llu, top1 %u (gt %u)\n", (unsigned long long)ix.info().kept_total,
               r.ids[0], gt.ids[0]);
   return 0;

@@ -138,3 +138,27 @@ def test_cpp_wrapper_runs_on_gpu(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, (r.stdout, r.stderr)
     assert "cpp ok" in r.stdout
+
+
+def test_multi_build_validation(fpp):
+    """fpp_multi_build: argument errors before any device work; config errors are the
+    single-index build's classes; no CPU fallback."""
+    X = np.zeros((10, 32), np.float32)
+    X[:, 0] = 1
+    h = C.c_void_p()
+    L = fpp.lib()
+    p = P(fpp, D=32)
+    assert L.fpp_multi_build(X.ctypes.data, 10, 32, C.byref(p), 0, None, C.byref(h)) == 1
+    assert L.fpp_multi_build(X.ctypes.data, 10, 32, C.byref(p), 33, None, C.byref(h)) == 1
+    assert L.fpp_multi_build(None, 0, 32, C.byref(p), 2, None, C.byref(h)) == 2
+    assert L.fpp_multi_build(X.ctypes.data, 10, 32, C.byref(p), 11, None, C.byref(h)) == 1
+    assert L.fpp_multi_build(X.ctypes.data, 10, 32, C.byref(p), 2, None, None) == 1
+    assert L.fpp_multi_shards(None) == 0 and not L.fpp_multi_shard(None, 0)
+    L.fpp_multi_free(None)
+    assert L.fpp_multi_query(None, X.ctypes.data, 1, 1, 1, None, None, None) == 1
+    if not gpu_available():
+        p = P(fpp, D=32, K=3)
+        assert L.fpp_multi_build(X.ctypes.data, 10, 32, C.byref(p), 2, None, C.byref(h)) == 1
+        p = P(fpp, D=32)
+        assert L.fpp_multi_build(X.ctypes.data, 10, 32, C.byref(p), 2, None, C.byref(h)) == 7
+        assert b"no CPU fallback" in L.fpp_last_error()

@@ -445,3 +445,73 @@ def test_stage_a_split_over_shards_equals_single_index(fpp, world):
     fi, fs = full.query(Q, k, qp)
     assert np.array_equal(mi.cpu().numpy().view(np.uint32), fi)
     assert np.array_equal(ms.cpu().numpy(), fs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G,d,L,D,qp,n", [(2, 128, 6, 128, 600, 30011), (3, 128, 6, 128, 600, 30011),
+                                          (3, 300, 4, 512, 800, 9001), (4, 20, 5, 32, 200, 5003)])
+def test_multi_index_equals_single_index(fpp, orc, G, d, L, D, qp, n, monkeypatch):
+    """fpp_multi_build / fpp_multi_query (one process, G shards; here all on device 0):
+    every shard's tables partition the 1-GPU index's and ids, scores and stats equal the
+    single index's and the oracle's for every G, also when the batch is
+    cut into several chunks with ragged slices."""
+    X = fpp.normalize(fpp.synth(n, d, clusters=40, sigma=0.3, seed=5))
+    Q = fpp.normalize(fpp.synth(203, d, clusters=40, sigma=0.3, seed=5, stream=1))
+    prm = dict(L=L, K=2, D=D, iProbes=3, alpha=0.05, kappa=20, seed=9)
+    one = fpp.Index.build(X, device=0, **prm)
+    mx = fpp.MultiIndex.build(X, num_gpus=G, devices=[0] * G, **prm)
+    assert mx.num_shards == G
+    kept = 0
+    for g in range(G):
+        sh = mx.shard(g)
+        inf = sh.info()
+        kept += inf["kept_total"]
+        lo = g * (n // G) + min(g, n % G)
+        assert inf["id_offset"] == lo
+    assert kept == one.info()["kept_total"]
+    # table 0: the shards' buckets, concatenated in shard order, are the single index's
+    off1, ids1, sc1 = one.table(0)
+    parts = [mx.shard(g).table(0) for g in range(G)]
+    offs = [mx.shard(g).info()["id_offset"] for g in range(G)]
+    for b in np.flatnonzero(np.diff(off1))[:400]:
+        want = set(zip(ids1[off1[b]:off1[b + 1]].tolist(), sc1[off1[b]:off1[b + 1]].tolist()))
+        got = set()
+        for (o, i, s), base in zip(parts, offs):
+            got |= set(zip((i[o[b]:o[b + 1]] + base).tolist(), s[o[b]:o[b + 1]].tolist()))
+        assert got == want
+    ids1, s1, st1 = one.query(Q, 20, qp, return_stats=True)
+    for chunk in (None, "37"):
+        if chunk:
+            monkeypatch.setenv("FPP_MULTI_CHUNK", chunk)
+        idsm, sm, stm = mx.query(Q, 20, qp, return_stats=True)
+        assert np.array_equal(idsm, ids1)
+        assert np.array_equal(sm, s1)
+        assert np.array_equal(stm[:, :3], st1[:, :3])
+        idsn, sn = mx.query(Q, 20, qp)  # the timed path: no stats (walking screen for d = 128)
+        assert np.array_equal(idsn, ids1) and np.array_equal(sn, s1)
+    ox = orc.Index(X, iprobes=3, **{k: v for k, v in prm.items() if k != "iProbes"})
+    oid, osc, ost = ox.query(Q[:64], 20, qp)
+    assert np.array_equal(idsm[:64], oid) and np.array_equal(stm[:64, :3], ost[:, :3])
+
+
+@pytest.mark.gpu
+def test_multi_index_errors(fpp):
+    X = fpp.normalize(fpp.synth(500, 32, seed=3))
+    prm = dict(L=2, K=2, D=32, iProbes=3, alpha=0.1)
+    with pytest.raises(fpp.FppInvalidArgument):
+        fpp.MultiIndex.build(X, num_gpus=0, **prm)
+    with pytest.raises(fpp.FppInvalidArgument):
+        fpp.MultiIndex.build(X, num_gpus=2, devices=[0, 99], **prm)
+    with pytest.raises(fpp.FppInvalidArgument):  # K = 3: the reference's config error
+        fpp.MultiIndex.build(X, num_gpus=2, devices=[0, 0], **{**prm, "K": 3})
+    mx = fpp.MultiIndex.build(X, num_gpus=2, devices=[0, 0], **prm)
+    with pytest.raises(fpp.FppDimensionError):
+        mx.query(np.zeros((1, 31), np.float32), 5, 16)
+    with pytest.raises(fpp.FppOutOfRange):
+        mx.query(X[:2], 5, 1)  # qProbes < L
+    ids, sc = mx.query(X[:0], 5, 16)
+    assert ids.shape == (0, 5)
+    one = fpp.MultiIndex.build(X, num_gpus=1, **prm)  # G = 1 is the plain index
+    a = one.query(X[:10], 5, 16)
+    b = mx.query(X[:10], 5, 16)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
