@@ -2278,6 +2278,12 @@ constexpr int NS_TMA = FPP_NS_TMA;    // WALK: stage-1 records by TMA bulk copie
 constexpr uint32_t NS_SH_BITS = FPP_NS_SH_BITS, NS_SH = 1u << NS_SH_BITS;  // seed id hash (lists) /
                                                                 // admission hash (WALK)
 constexpr int WK_HPROBE = 32;  // admission hash: probes before the bitmap takes an id
+#ifndef FPP_NS_PF
+#define FPP_NS_PF 0  // (measured on C4: each bit costs ~2 ms of 100: the kernel is issue-bound) bit 0: stage-A survivors prefetch their stage-B record into L2;
+#endif               // bit 1: rows admitted to the exact stage prefetch their lines
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
 
 __device__ __forceinline__ unsigned long long dkey(double x) {  // order-preserving
   const unsigned long long b = (unsigned long long)__double_as_longlong(x);
@@ -2814,6 +2820,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       live = fkey(ub) >= thr_fnow();
     }
     live = admit(id, live);  // every id scored exactly at most once
+    if constexpr ((FPP_NS_PF & 2) != 0) {  // the row's lines on their way to L2 before exact_fold
+      if (live)
+        for (uint32_t c = 0; c < nch; ++c) prefetch_l2(X + (uint64_t)id * ldx + c * 32);
+    }
     push_exact(id, live);
     if (lane == 0) cnt_s[w][0] += cnt;
   };
@@ -2967,6 +2977,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       const uint32_t pos = (t1 + __popc(live_m & lt_mask)) % NS_QCAP;
       s1q[pos] = cid;
       s1v[pos] = make_float2(A1, N1);
+      // its stage-B record (one 128 B line) on its way to L2 before stage2_batch reads it
+      if constexpr ((FPP_NS_PF & 1) != 0) prefetch_l2(rec + ((uint64_t)a.n * 2 + (uint64_t)cid * 8));
     }
     t1 += __popc(live_m);
     if constexpr (!WALK) nrows += __popc(__ballot_sync(FULL, cid != NONE));  // (WALK: chunk totals)
