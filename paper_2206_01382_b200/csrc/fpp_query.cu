@@ -2264,10 +2264,12 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
 constexpr int NS_W = 8;            // warps per CTA
 constexpr uint32_t NS_QCAP = 64;   // survivor queue per warp (<= 31 + 32 queued)
 #ifndef FPP_NS_RING
-#define FPP_NS_RING 3  // (3 CTAs per SM fit: 63 KB dynamic + 12 KB static shared memory)
+#define FPP_NS_RING 3  // (1 KB slots + a 2 KB exact staging buffer per warp; C4 screen 95.3 ms, depth 4: 97.5)
 #endif
 constexpr int NS_RING = FPP_NS_RING;  // stage-1 record ring depth per warp (cp.async)
-constexpr int NS_IDR = 2 * NS_RING;   // candidate-id ring depth per warp
+constexpr int NS_IDR = 2 * NS_RING;   // candidate-id ring depth per warp (lists mode only)
+constexpr int NS_SLOT = 64;           // uint4 per ring slot: 32 records of 32 B
+constexpr int NS_STG = 128;           // uint4 of the per-warp exact staging buffer (32 rows x 16 floats)
 #ifndef FPP_NS_TMA
 #define FPP_NS_TMA 0  // measured: C4 511 vs 538 k q/s with the cp.async ring
 #endif
@@ -2323,9 +2325,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   const uint32_t d = a.d, nch = (d + 31) / 32;  // 32-float chunks (rows padded with zeros)
   // fixed-size parts first (compile-time offsets: the compiler rematerialises these
   // addresses under the register cap), the d-dependent query copy last
-  uint4* ring_all = reinterpret_cast<uint4*>(smraw);                   // [NW][RING][2 KB]
-  uint32_t* idr_all = reinterpret_cast<uint32_t*>(ring_all + (size_t)NW * NS_RING * 128);  // [NW][IDR][32]
-  uint32_t* sq_all = idr_all + (size_t)NW * NS_IDR * 32;               // [NW][QCAP]
+  uint4* ring_all = reinterpret_cast<uint4*>(smraw);                   // [NW][RING][1 KB]
+  uint4* stg_all = ring_all + (size_t)NW * NS_RING * NS_SLOT;          // [NW][2 KB] exact staging
+  uint32_t* idr_all = reinterpret_cast<uint32_t*>(stg_all + (size_t)NW * NS_STG);  // lists: [NW][IDR][32]
+  uint32_t* sq_all = idr_all + (WALK ? (size_t)0 : (size_t)NW * NS_IDR * 32);  // [NW][QCAP]
   uint32_t* s1_all = sq_all + (size_t)NW * NS_QCAP;                    // [NW][QCAP] stage-2 queue ids
   float2* s1v_all = reinterpret_cast<float2*>(s1_all + (size_t)NW * NS_QCAP);  // [NW][QCAP] (A1, N1)
   double* qd = reinterpret_cast<double*>(s1v_all + (size_t)NW * NS_QCAP);  // [32 * nch]
@@ -2344,7 +2347,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   __shared__ __align__(8) uint64_t smbar[WALK && NS_TMA ? NW : 1][NS_RING];  // TMA: per ring slot
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  uint4* ring = ring_all + (size_t)w * NS_RING * 128;
+  uint4* ring = ring_all + (size_t)w * NS_RING * NS_SLOT;
   uint32_t* idr = idr_all + (size_t)w * NS_IDR * 32;  // candidate ids of batch b: slot b % IDR
   const uint32_t ring_sa = (uint32_t)__cvta_generic_to_shared(ring);
   uint32_t* sq = sq_all + (size_t)w * NS_QCAP;    // survivors of stage 2 -> exact
@@ -2668,7 +2671,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   // after those probes, and lists meet the seeds again in the scan, where the
   // bitmap drops them before the exact stage.
   uint32_t pstart = 0;
-  float* const stg0 = reinterpret_cast<float*>(ring);  // exact staging while the ring is idle
+  float* const stg0 = reinterpret_cast<float*>(stg_all + (size_t)w * NS_STG);  // exact staging rows
   if (a.nseedp) {
     // leading true buckets whose cumulative length stays <= the seed cap (lists: half
     // the seed hash, so its load stays <= 1/2)
@@ -2859,19 +2862,23 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       const uint32_t r = it * 16 + g16;
       const uint32_t idv = __shfl_sync(FULL, id, r);
       if (idv != NONE)
-        cp_async16s(ring_sa + (slot * 128 + r * 2 + p2) * 16, rec + (uint64_t)idv * 2 + p2);
+        cp_async16s(ring_sa + (slot * NS_SLOT + r * 2 + p2) * 16, rec + (uint64_t)idv * 2 + p2);
     }
   };
   // WALK: the walker's next window -> batch b's slot: its ids (4 B cp.async per lane
   // from the CSR ids) and its stage-1 records, inline in CSR order (a.csrrec: the
   // window's entries are runs of consecutive records, so the copies are coalesced and
   // whole 128 B lines are used), one commit group
+  // this lane's record address in ring slot 0 (shared window); kept opaque per iteration
+  // so it stays in a register instead of being rebuilt from tid / the window base
+  uint32_t my_sa = ring_sa + lane * 32;
   auto produce = [&](uint32_t slot) {
     uint64_t gp = 0;
     const bool v = wk_step(gp);
     // a lane without an entry marks its own record slot empty (id NONE; the lane reads
     // it back itself, so no ordering beyond program order is needed)
-    if (!v) ring[slot * 128 + lane * 2 + 1] = make_uint4(0u, NONE, 0u, 0u);
+    const uint32_t sa = my_sa + slot * (NS_SLOT * 16);  // this lane's record in the slot
+    if (!v) asm volatile("st.shared.v4.u32 [%0+16], {%1, %2, %1, %1};" ::"r"(sa), "r"(0u), "r"(NONE) : "memory");
     const uint4* cr = reinterpret_cast<const uint4*>(a.csrrec);
     if constexpr (NS_TMA) {
       // the window's valid lanes are a prefix, split into runs of consecutive CSR
@@ -2887,12 +2894,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
       if ((starts >> lane) & 1u) {
         const uint32_t after = starts & ~((2u << lane) - 1u);  // later run starts
         const uint32_t end = after ? (uint32_t)(__ffs(after) - 1) : (uint32_t)__popc(vm);
-        bulk_g2s(ring + slot * 128 + lane * 2, cr + gp * 2, (end - lane) * 32u, &smbar[w][slot]);
+        bulk_g2s(ring + slot * NS_SLOT + lane * 2, cr + gp * 2, (end - lane) * 32u, &smbar[w][slot]);
       }
       return;
     }
     if (v) {  // each lane copies its own record (2 x 16 B: no address shuffles)
-      const uint32_t sa = ring_sa + (slot * 128 + lane * 2) * 16;
       cp_async16s(sa, cr + gp * 2);
       cp_async16s(sa + 16, cr + gp * 2 + 1);
     }
@@ -2923,10 +2929,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   // id-ring slot (i - 1) % IDR
   uint32_t cs = 0, ci = 0;
   for (uint32_t i = 0; more(i); ++i) {
+    asm volatile("" : "+r"(my_sa));
     const uint32_t ps = cs == 0 ? NS_RING - 1 : cs - 1;
-    // full queues are drained first (their own loads; the ring stays in flight); the
-    // exact rows are staged in the ring slot the issue below refills
-    float* const stg = reinterpret_cast<float*>(ring + ps * 128);
+    // full queues are drained first (their own loads; the ring stays in flight)
+    float* const stg = stg0;
     if (qtail - qhead >= 32) {
       __syncwarp();
       exact_batch(32, stg);
@@ -2950,8 +2956,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
     }
     const uint32_t slot = cs;
     Recs cur;
-    cur.r[0] = ring[slot * 128 + lane * 2];
-    cur.m = ring[slot * 128 + lane * 2 + 1];
+    if constexpr (WALK) {
+      const uint32_t ca = my_sa + slot * (NS_SLOT * 16);
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(cur.r[0].x), "=r"(cur.r[0].y), "=r"(cur.r[0].z), "=r"(cur.r[0].w) : "r"(ca));
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+16];"
+                   : "=r"(cur.m.x), "=r"(cur.m.y), "=r"(cur.m.z), "=r"(cur.m.w) : "r"(ca));
+    } else {
+      cur.r[0] = ring[slot * NS_SLOT + lane * 2];
+      cur.m = ring[slot * NS_SLOT + lane * 2 + 1];
+    }
     const uint32_t cid = WALK ? cur.m.y : idr[ci * 32 + lane];  // (WALK: the record's id)
     cs = cs + 1 == NS_RING ? 0 : cs + 1;
     ci = ci + 1 == NS_IDR ? 0 : ci + 1;
@@ -3052,10 +3066,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_screen(ScoreArgs a) {
   }  // queries
 }
 
-static size_t screen_smem(uint32_t d) {
+static size_t screen_smem(uint32_t d, bool walk) {
   const uint32_t nch = (d + 31) / 32;
-  return (size_t)nch * 32 * 8 + (size_t)NS_W * NS_RING * 128 * 16 + (size_t)NS_W * NS_IDR * 32 * 4 +
-         (size_t)NS_W * NS_QCAP * (4 + 4 + 8);
+  return (size_t)nch * 32 * 8 + (size_t)NS_W * (NS_RING * NS_SLOT + NS_STG) * 16 +
+         (walk ? (size_t)0 : (size_t)NS_W * NS_IDR * 32 * 4) + (size_t)NS_W * NS_QCAP * (4 + 4 + 8);
 }
 
 static size_t score_smem(uint32_t d, int sl, int st) {
@@ -3445,7 +3459,7 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     static const uint32_t seedcap =
         getenv("FPP_SC_SEEDCAP") ? (uint32_t)atoi(getenv("FPP_SC_SEEDCAP")) : WK_SEEDCAP;
     sa.seedcap = seedcap;
-    const size_t sm = screen_smem(ix.d);
+    const size_t sm = screen_smem(ix.d, walk);
     // 3 CTAs/SM (24 warps: 80 registers, a 3-batch ring and a 2048-slot admission hash
     // so three CTAs' shared memory fits): C4 533 vs 522 k q/s for 2 CTAs/SM with a
     // 4-batch ring; FPP_SC_SCR_MINB=2 selects the 2-CTA register budget
