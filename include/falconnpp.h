@@ -248,7 +248,7 @@ void fpp_multi_free(fpp_multi* m);
  * per-query top-k lists, scores/ids [lists][nq][k] on `device` (each list sorted by
  * score desc, id asc; empty slots id 0xFFFFFFFF / -inf) are merged into
  * out [nq][k] by the same key order on the device (k-way merge kernel).  The shard
- * lists must hold disjoint (global) ids.  lists, k <= 32.  Asynchronous on stream. */
+ * lists must hold disjoint (global) ids.  lists <= 32, any k >= 1.  Asynchronous on stream. */
 int fpp_merge_topk(const double* scores_dev, const uint32_t* ids_dev, uint32_t lists, uint64_t nq,
                    uint32_t k, double* out_scores_dev, uint32_t* out_ids_dev, int device,
                    void* stream);
@@ -256,7 +256,8 @@ int fpp_merge_topk(const double* scores_dev, const uint32_t* ids_dev, uint32_t l
 /* ---- exact brute force over the index's dataset: the recall ground truth
  * (SPEC.md:490-503 brute_force_topk).  Scores are inner_product (dataset.cpp:61-69)
  * bit for bit; top-k by (score desc, id asc), ids global (id_offset added).
- * Errors as fpp_query (k <= 32, k <= n, dimension, finite Q). */
+ * Errors as fpp_query (k <= n, dimension, finite Q).  k > 32 takes one pass over X per
+ * 32 ranks. */
 int fpp_brute_force(const fpp_index* idx, const float* Q, uint64_t nq, uint32_t k, uint32_t* ids,
                     double* scores);
 int fpp_brute_force_device(const fpp_index* idx, const float* Q_dev, uint64_t nq, uint32_t k,

@@ -72,6 +72,11 @@ struct BruteArgs {
   uint64_t rows_per_split;
   uint32_t* part_ids;     // [split][nq][k]
   double* part_scores;
+  // k > 32: pass p keeps ranks [32p, 32p + k) -- the k best rows that come strictly
+  // after the previous pass's last answer entry (the cursor) in (score desc, id asc)
+  const uint32_t* cur_ids;  // answer rows [nq][ostride] (global ids); nullptr on pass 0
+  const double* cur_scores;
+  uint32_t ostride, ooff, id_offset;
 };
 
 template <bool VEC>
@@ -86,6 +91,21 @@ __global__ void __launch_bounds__(BF_WARPS * 32) k_brute(BruteArgs a) {
   for (uint32_t i = threadIdx.x; i < d * BF_QT; i += blockDim.x) {
     const uint32_t j = i / BF_QT, qi = i - j * BF_QT;
     qd[i] = qi < nqt ? (double)a.Q[(uint64_t)(q0 + qi) * d + j] : 0.0;
+  }
+  // per-query cursor: (+inf, 0) admits every row (pass 0), (-inf, 0) none (the rows ran out)
+  __shared__ double cur_s[BF_QT];
+  __shared__ uint32_t cur_i[BF_QT];
+  if (threadIdx.x < BF_QT) {
+    double cs = INFINITY;
+    uint32_t ci = 0;
+    if (a.cur_ids && threadIdx.x < nqt) {
+      const uint64_t o = (uint64_t)(q0 + threadIdx.x) * a.ostride + a.ooff - 1;
+      const uint32_t g = a.cur_ids[o];
+      cs = g == 0xffffffffu ? -INFINITY : a.cur_scores[o];
+      ci = g == 0xffffffffu ? 0u : g - a.id_offset;
+    }
+    cur_s[threadIdx.x] = cs;
+    cur_i[threadIdx.x] = ci;
   }
   __syncthreads();
   const uint64_t r_begin = (uint64_t)split * a.rows_per_split;
@@ -165,7 +185,9 @@ __global__ void __launch_bounds__(BF_WARPS * 32) k_brute(BruteArgs a) {
       const bool valid = rid < r_end;
 #pragma unroll
       for (int qi = 0; qi < BF_QT; ++qi) {
-        bf_insert(bs[qi], bi[qi], k, acc[qi], (uint32_t)rid, valid && (uint32_t)qi < nqt);
+        const double cs = cur_s[qi];
+        const bool after = cs > acc[qi] || (cs == acc[qi] && cur_i[qi] < (uint32_t)rid);
+        bf_insert(bs[qi], bi[qi], k, acc[qi], (uint32_t)rid, valid && (uint32_t)qi < nqt && after);
         acc[qi] = 0.0;
       }
       cc = 0;
@@ -202,7 +224,8 @@ __global__ void __launch_bounds__(256) k_brute_merge(const uint32_t* __restrict_
                                                      const double* __restrict__ part_scores,
                                                      uint32_t splits, uint32_t nq, uint32_t k,
                                                      uint32_t id_offset, uint32_t* out_ids,
-                                                     double* out_scores) {
+                                                     double* out_scores, uint32_t ostride,
+                                                     uint32_t ooff) {
   const int lane = threadIdx.x & 31;
   const uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
@@ -217,8 +240,8 @@ __global__ void __launch_bounds__(256) k_brute_merge(const uint32_t* __restrict_
   }
   if ((uint32_t)lane < k) {
     const bool ok = bi != 0xffffffffu;
-    out_ids[(uint64_t)q * k + lane] = ok ? bi + id_offset : 0xffffffffu;
-    out_scores[(uint64_t)q * k + lane] = ok ? bs : -INFINITY;
+    out_ids[(uint64_t)q * ostride + ooff + lane] = ok ? bi + id_offset : 0xffffffffu;
+    out_scores[(uint64_t)q * ostride + ooff + lane] = ok ? bs : -INFINITY;
   }
 }
 
@@ -233,27 +256,33 @@ void run_brute_force(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, 
   splits = std::min<uint64_t>(splits, (ix.n + 1023) / 1024);
   splits = std::max<uint64_t>(splits, 1);
   const uint64_t rows_per_split = (ix.n + splits - 1) / splits;
-  DBuf<uint32_t> pids((size_t)splits * nq * k);
-  DBuf<double> psc((size_t)splits * nq * k);
-  BruteArgs a{ix.X, ix.n, d, ix.ldx, Qd, (uint32_t)nq, k, rows_per_split, pids.p, psc.p};
+  const uint32_t kp_max = std::min<uint32_t>(k, 32);
+  DBuf<uint32_t> pids((size_t)splits * nq * kp_max);
+  DBuf<double> psc((size_t)splits * nq * kp_max);
   static_assert(BF_WARPS * BF_QT * 32 * 12 <= BF_WARPS * BF_STAGES * BF_STAGE_FLOATS * 4,
                 "merge lists must fit in the ring");
   const size_t smem = (size_t)d * BF_QT * 8 + (size_t)BF_WARPS * BF_STAGES * BF_STAGE_FLOATS * 4;
   const dim3 grid((unsigned)splits, tiles);
-  if ((d & 3u) == 0) {
-    FPP_CUDA(cudaFuncSetAttribute(k_brute<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    k_brute<true><<<grid, BF_WARPS * 32, smem, s>>>(a);
-  } else {
-    FPP_CUDA(cudaFuncSetAttribute(k_brute<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    k_brute<false><<<grid, BF_WARPS * 32, smem, s>>>(a);
+  // k > 32: one pass over X per 32 ranks (the warp lists hold 32 entries)
+  for (uint32_t off = 0; off < k; off += 32) {
+    const uint32_t kp = std::min<uint32_t>(32, k - off);
+    BruteArgs a{ix.X, ix.n, d, ix.ldx, Qd, (uint32_t)nq, kp, rows_per_split, pids.p, psc.p,
+                off ? ids_d : nullptr, scores_d, k, off, ix.prm.id_offset};
+    if ((d & 3u) == 0) {
+      FPP_CUDA(cudaFuncSetAttribute(k_brute<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      k_brute<true><<<grid, BF_WARPS * 32, smem, s>>>(a);
+    } else {
+      FPP_CUDA(cudaFuncSetAttribute(k_brute<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      k_brute<false><<<grid, BF_WARPS * 32, smem, s>>>(a);
+    }
+    FPP_LAUNCH();
+    k_brute_merge<<<(unsigned)((nq + 7) / 8), 256, 0, s>>>(pids.p, psc.p, (uint32_t)splits,
+                                                            (uint32_t)nq, kp, ix.prm.id_offset, ids_d,
+                                                            scores_d, k, off);
+    FPP_LAUNCH();
   }
-  FPP_LAUNCH();
-  k_brute_merge<<<(unsigned)((nq + 7) / 8), 256, 0, s>>>(pids.p, psc.p, (uint32_t)splits,
-                                                          (uint32_t)nq, k, ix.prm.id_offset, ids_d,
-                                                          scores_d);
-  FPP_LAUNCH();
   FPP_CUDA(cudaStreamSynchronize(s));  // scratch is freed on return
 }
 

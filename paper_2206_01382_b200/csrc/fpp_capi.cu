@@ -111,7 +111,7 @@ void QueryCtx::QSlot::release() {
   vals.release(); codes.release(); ppos.release(); plen.release(); gbuf.release();
   ckey.release(); cpair.release(); dbgclk.release(); eq.release(); coff.release();
   uq.release(); uniq.release(); cands.release(); bitmap.release(); counter.release();
-  qsig.release(); cands2.release(); uq2.release(); wlog.release();
+  qsig.release(); cands2.release(); uq2.release(); wlog.release(); allsc.release();
   if (pinned) cudaFreeHost(pinned);
   if (ev_probe) cudaEventDestroy(ev_probe);
   if (ev_bdone) cudaEventDestroy(ev_bdone);
@@ -569,7 +569,6 @@ static void validate_query(const Index& ix, uint64_t nq, uint32_t k, uint32_t qp
   if (!ix.offsets) fail(FPP_ERR_INVALID_ARGUMENT, "search: sharded build not finished (fpp_shard_finish)");
   if (k == 0) fail(FPP_ERR_INVALID_ARGUMENT, "search: k must be >= 1");
   if (k > ix.n) fail(FPP_ERR_OUT_OF_RANGE, "search: k > n");
-  if (k > 32) fail(FPP_ERR_UNSUPPORTED, "GPU path: k must be <= 32");
   if (qprobes < ix.prm.L || (uint64_t)qprobes > (uint64_t)ix.prm.L * ix.NB)
     fail(FPP_ERR_OUT_OF_RANGE, "query_probe_sequence: qProbes must be in [L, L*NB]");
   if (nq && (!Q || !ids || !scores)) fail(FPP_ERR_INVALID_ARGUMENT, "search: NULL buffer");
@@ -978,7 +977,6 @@ static void validate_brute(const Index& ix, uint64_t nq, uint32_t k, const void*
                            const void* ids, const void* scores) {
   if (k == 0) fail(FPP_ERR_INVALID_ARGUMENT, "brute_force_topk: k must be >= 1");
   if (k > ix.n) fail(FPP_ERR_OUT_OF_RANGE, "brute_force_topk: k > n");
-  if (k > 32) fail(FPP_ERR_UNSUPPORTED, "GPU path: k must be <= 32");
   if (nq && (!Q || !ids || !scores)) fail(FPP_ERR_INVALID_ARGUMENT, "brute_force_topk: NULL buffer");
 }
 
@@ -1132,7 +1130,7 @@ int fpp_merge_topk(const double* scores_dev, const uint32_t* ids_dev, uint32_t l
                    void* stream) {
   return guarded([&] {
     if (lists == 0 || lists > 32) fail(FPP_ERR_INVALID_ARGUMENT, "merge_topk: lists must be in [1, 32]");
-    if (k == 0 || k > 32) fail(FPP_ERR_INVALID_ARGUMENT, "merge_topk: k must be in [1, 32]");
+    if (k == 0) fail(FPP_ERR_INVALID_ARGUMENT, "merge_topk: k must be >= 1");
     if (nq && (!scores_dev || !ids_dev || !out_scores_dev || !out_ids_dev))
       fail(FPP_ERR_INVALID_ARGUMENT, "merge_topk: NULL buffer");
     if (!nq) return;

@@ -153,6 +153,7 @@ struct QueryCtx {
     DBuf<uint32_t> cands2;  // rerank: screened candidates [nqc][B]
     DBuf<uint32_t> uq2;
     DBuf<uint32_t> wlog;    // walking screen: per-CTA log of admitted ids
+    DBuf<double> allsc;     // k > 32: every candidate's exact score (k_topk_more)
     uint64_t* pinned = nullptr;     // etot readback
     cudaEvent_t ev_probe = nullptr; // stage A (hash + probe select) done
     cudaEvent_t ev_bdone = nullptr; // stage B (collect + score) done

@@ -259,7 +259,6 @@ void multi_query(const Multi& m, const float* Q, uint64_t nq, uint32_t k, uint32
   }
   if (k == 0) fail(FPP_ERR_INVALID_ARGUMENT, "search: k must be >= 1");
   if (k > m.n) fail(FPP_ERR_OUT_OF_RANGE, "search: k > n");
-  if (k > 32) fail(FPP_ERR_UNSUPPORTED, "GPU path: k must be <= 32");
   if (nq && (!Q || !ids || !scores)) fail(FPP_ERR_INVALID_ARGUMENT, "search: NULL buffer");
   const uint64_t pe = fpp_query_probes(m.sh[0].ix, qprobes);
   if (qprobes < m.prm.L || pe == 0)

@@ -1650,6 +1650,11 @@ struct ScoreArgs {
   uint32_t logcap;
   uint32_t seedcap;  // k_score_screen: seed entries per query (whole leading true buckets)
   const uint4* csrrec;  // WALK: stage-1 records in CSR entry order [kept_total][4] (Index::q8csr)
+  // k > 32 (k_score + k_topk_more): the kernel keeps ranks [0, k) of an answer row of
+  // `ostride` slots (0: = k) and dumps every candidate's exact score to allsc (same
+  // offsets as the candidate lists), from which k_topk_more selects the later ranks
+  uint32_t ostride;
+  double* allsc;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1840,6 +1845,7 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
     if (++cc == nsl) {
       const uint32_t ci = cb * 32 + lane;
       const uint32_t id = ci < U ? __ldg(cand + ci) : 0xffffffffu;
+      if (a.allsc && ci < U) a.allsc[(cand - a.cands) + ci] = acc;
       topk_insert(bs, bi, k, acc, id, id != 0xffffffffu);  // (grouped lists carry holes)
       acc = 0.0;
       cc = 0;
@@ -1858,8 +1864,9 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
     }
     if ((uint32_t)lane < k) {
       const bool ok = bi != 0xffffffffu;
-      a.out_ids[(uint64_t)q * k + lane] = ok ? bi + a.id_offset : 0xffffffffu;
-      a.out_scores[(uint64_t)q * k + lane] = ok ? bs : -INFINITY;
+      const uint64_t o = (uint64_t)q * (a.ostride ? a.ostride : k) + lane;
+      a.out_ids[o] = ok ? bi + a.id_offset : 0xffffffffu;
+      a.out_scores[o] = ok ? bs : -INFINITY;
     }
     // unique candidates scored: the list length, or (grouped lists with holes) the
     // collect's unique count; with a SimHash screen the screened list
@@ -1874,6 +1881,62 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
   }
   if (!a.qctr) return;
   __syncthreads();  // qd, mg_* and q_sh are reused by the next query
+  }
+}
+
+// Ranks [32, k) of an answer (k > 32).  k_score kept ranks [0, 32) in its warp lists
+// and dumped every candidate's exact score (ScoreArgs::allsc), so every exact score is
+// computed once.  Pass p streams the query's (score, id) pairs again and
+// keeps the 32 best that come strictly after the previous pass's last entry (the
+// cursor) in the answer order (score desc, id asc): ranks [32p, 32p + 32).  A pass
+// that ends short (cursor = none) leaves the rest of the row empty.
+constexpr int TM_WARPS = 8;
+__global__ void __launch_bounds__(TM_WARPS * 32) k_topk_more(ScoreArgs a) {
+  __shared__ double mg_s[TM_WARPS][32];
+  __shared__ uint32_t mg_i[TM_WARPS][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t q = blockIdx.x;
+  const uint32_t U = a.uq[q];
+  const uint64_t base = a.cstride ? (uint64_t)q * a.cstride : a.coff[q];
+  const uint32_t* cand = a.cands + base;
+  const double* sc = a.allsc + base;
+  const uint32_t K = a.ostride;
+  uint32_t* oid = a.out_ids + (uint64_t)q * K;
+  double* osc = a.out_scores + (uint64_t)q * K;
+  for (uint32_t off = 32; off < K; off += 32) {
+    const uint32_t k = min(32u, K - off);
+    const uint32_t cg = oid[off - 1];  // the cursor (a global id)
+    const double cs = osc[off - 1];
+    if (cg == 0xffffffffu) {  // the candidates ran out (uniform over the CTA)
+      for (uint32_t i = off + threadIdx.x; i < K; i += blockDim.x) {
+        oid[i] = 0xffffffffu;
+        osc[i] = -INFINITY;
+      }
+      return;
+    }
+    const uint32_t ci = cg - a.id_offset;
+    double bs = -INFINITY;
+    uint32_t bi = 0xffffffffu;
+    for (uint32_t c0 = (uint32_t)w * 32; c0 < U; c0 += TM_WARPS * 32) {
+      const uint32_t c = c0 + lane;
+      const uint32_t id = c < U ? __ldg(cand + c) : 0xffffffffu;
+      const double s = c < U ? sc[c] : 0.0;
+      topk_insert(bs, bi, k, s, id, id != 0xffffffffu && sbetter(cs, ci, s, id));
+    }
+    mg_s[w][lane] = bs;
+    mg_i[w][lane] = bi;
+    __syncthreads();
+    if (w == 0) {
+      for (int w2 = 1; w2 < TM_WARPS; ++w2)
+        topk_insert(bs, bi, k, mg_s[w2][lane], mg_i[w2][lane],
+                    (uint32_t)lane < k && mg_i[w2][lane] != 0xffffffffu);
+      if ((uint32_t)lane < k) {
+        const bool ok = bi != 0xffffffffu;
+        oid[off + lane] = ok ? bi + a.id_offset : 0xffffffffu;
+        osc[off + lane] = ok ? bs : -INFINITY;
+      }
+    }
+    __syncthreads();  // the next pass reads this pass's last entry and reuses mg_*
   }
 }
 
@@ -3294,7 +3357,10 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   const bool force_prune = getenv("FPP_PRUNE") != nullptr;
   const bool dbg = getenv("FPP_DEBUG_PRUNE") != nullptr;
   bool use_pruned = false, probe = false;
-  if (ix.xt_n && !no_prune) {
+  // k > 32: the warp lists hold 32 ranks, so k_score keeps ranks [0, 32), dumps every
+  // exact score, and k_topk_more selects the later ranks from the dump
+  const bool bigk = k > 32;
+  if (ix.xt_n && !no_prune && !bigk) {
     std::lock_guard<std::mutex> lk(ix.mu);  // the index-wide policy (concurrent calls)
     if (cx.prune_pending && cudaEventQuery(cx.prune_ev) == cudaSuccess) {
       if (cx.prune_h[0]) ix.prune_frac = (double)cx.prune_h[1] / ((double)cx.prune_h[0] * ix.d);
@@ -3318,9 +3384,10 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   sl.uniq.ensure(nqc);
   CollectArgs ca{sl.ppos.p, sl.plen.p, peff, ix.ids, sl.coff.p, sl.cands.p, sl.uq.p,
                  nqc, nwords, nullptr, sl.counter.p, 0, 0, sl.uniq.p, ix.n};
+  uint64_t etot = 0;
   if (collect) {
   FPP_CUDA(cudaEventSynchronize(sl.ev_probe));  // the candidate total (stage A readback)
-  const uint64_t etot = sl.pinned[0];
+  etot = sl.pinned[0];
   sl.cands.ensure(etot + 1);
   ca.cands = sl.cands.p;
   cx.timer.begin(PH_COLLECT, st, &e0);
@@ -3423,6 +3490,12 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   // so the remaining SM resources stay free for the next chunk's stage A
   static const int sc_ctas = getenv("FPP_SC_CTAS") ? atoi(getenv("FPP_SC_CTAS")) : 0;
   sa.nq = nqc;
+  if (bigk) {
+    sl.allsc.ensure(rerank ? (size_t)nqc * rerank : (size_t)etot + 1);
+    sa.allsc = sl.allsc.p;
+    sa.ostride = k;
+    sa.k = 32;
+  }
   auto launch_score = [&](auto kern, int slice, int stg) {
     const size_t sm = score_smem(ix.d, slice, stg);
     FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -3571,6 +3644,11 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     else launch_score(k_score<false, 32, 4>, 32, 4);
   }
   FPP_LAUNCH();
+  if (bigk) {
+    k_topk_more<<<nqc, TM_WARPS * 32, 0, st>>>(sa);
+    FPP_LAUNCH();
+    cx.acc.launches += 1;
+  }
   cx.timer.end(PH_SCORE, e0, st);
   cx.acc.launches += 1;  // score (stage A: lists, probe_select, scan_eq)
   cx.acc.score_launches += 1;

@@ -515,3 +515,53 @@ def test_multi_index_errors(fpp):
     a = one.query(X[:10], 5, 16)
     b = mx.query(X[:10], 5, 16)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,clusters,D", [(128, 30, 128), (300, 30, 512), (17, 0, 32)])
+def test_k_above_32_equals_oracle(fpp, orc, d, clusters, D):
+    """SPEC.md:312 only requires k >= 1.  Above the 32-entry warp lists k_score keeps
+    ranks [0, 32) and dumps every exact score; k_topk_more selects ranks [32, k) from
+    the dump, 32 per pass.  ids, scores and stats equal the oracle's for k = 33 ... 200,
+    also when a query has fewer than k candidates, through the reordered batch path,
+    the SimHash rerank and the brute force."""
+    n = 6000
+    X = fpp.normalize(fpp.synth(n, d, clusters=clusters, sigma=0.3, seed=11))
+    Q = fpp.normalize(fpp.synth(70, d, clusters=clusters, sigma=0.3, seed=11, stream=1))
+    X[100:140] = X[7]  # 41 equal scores straddle a pass boundary: ties go to the lower id
+    prm = dict(L=6, K=2, D=D, alpha=0.2, kappa=20, seed=3)
+    ix = fpp.Index.build(X, iProbes=3, **prm)
+    ox = orc.Index(X, iprobes=3, **prm)
+    Q[0] = X[7]
+    short = False
+    for k, qp in [(33, 600), (64, 600), (100, 2000), (200, 6), (1000, 2000)]:
+        gi, gs, gst = ix.query(Q, k, qp, return_stats=True)
+        oi, os_, ost = ox.query(Q, k, qp)
+        assert np.array_equal(gst, ost), (k, qp)
+        assert np.array_equal(gi, oi), (k, qp)
+        assert np.array_equal(gs, os_), (k, qp)
+        gi2, gs2 = ix.query(Q, k, qp)  # the timed path (no stats)
+        assert np.array_equal(gi2, oi) and np.array_equal(gs2, os_)
+        short |= bool((oi == 0xFFFFFFFF).any())
+    assert short or d == 17  # some rows end before k entries (fewer candidates than k)
+    # SimHash rerank with B >= k > 32
+    gi, gs, gst = ix.query(Q, 40, 2000, return_stats=True, rerank=300)
+    oi, os_, ost = ox.query(Q, 40, 2000, rerank=300)
+    assert np.array_equal(gi, oi) and np.array_equal(gs, os_) and np.array_equal(gst, ost)
+    # brute force: one pass over X per 32 ranks
+    for k in (33, 100):
+        bi, bs = ix.brute_force(Q[:20], k)
+        ri, rs = orc.brute_force(X, Q[:20], k)
+        assert np.array_equal(bi, ri) and np.array_equal(bs, rs)
+
+
+@pytest.mark.gpu
+def test_k_above_32_multi_index(fpp):
+    X = fpp.normalize(fpp.synth(9000, 128, clusters=40, sigma=0.3, seed=5))
+    Q = fpp.normalize(fpp.synth(50, 128, clusters=40, sigma=0.3, seed=5, stream=1))
+    prm = dict(L=6, K=2, D=128, iProbes=3, alpha=0.1, kappa=20, seed=9)
+    one = fpp.Index.build(X, device=0, **prm)
+    mx = fpp.MultiIndex.build(X, num_gpus=3, devices=[0] * 3, **prm)
+    i1, s1 = one.query(Q, 70, 900)
+    im, sm = mx.query(Q, 70, 900)
+    assert np.array_equal(im, i1) and np.array_equal(sm, s1)
