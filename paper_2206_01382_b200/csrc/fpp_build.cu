@@ -86,7 +86,10 @@ __device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], in
   using S = FhtShape<P>;
   constexpr bool TR = P >= 64;
   const bool full = D >= (uint32_t)P;  // no truncation: skip the j < D test
-  auto jof = [&](int e) -> uint32_t { return TR ? (uint32_t)e * S::G + g : (uint32_t)g * S::EPT + e; };
+  auto jof = [&](int e) -> uint32_t {
+    if constexpr (TR) return jB<P>(e, g);
+    else return (uint32_t)g * S::EPT + e;
+  };
   bool fast = false;
   if constexpr (TR) {
     float amax = 0.0f;
@@ -121,8 +124,7 @@ __device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], in
     if (fast) {
       // v -> shared memory in natural order (the lane reads back only its own
       // entries), then each lane appends its kept keys at its exclusive offset
-#pragma unroll
-      for (int e = 0; e < S::EPT; ++e) vbuf[jof(e)] = v[e];
+      store_B_natural<P>(v, g, vbuf);
       const uint32_t cl = __popc(macc);
       uint32_t x = cl;
 #pragma unroll
@@ -240,7 +242,7 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx, 
 #pragma unroll
       for (int e = 0; e < S::EPT; ++e) v[e] = x[e];
       const uint32_t* sw = signs + ((uint64_t)t * K + f) * 3 * S::W;
-      if constexpr (TR) spinner_project_T<P>(v, sw, g, buf);  // layout B: j = e*G + g
+      if constexpr (TR) spinner_project_T<P>(v, sw, g, buf);  // layout B: j = jB<P>(e, g)
       else spinner_project<P>(v, sw, g);                      // layout A: j = g*EPT + e
       hb_select<P, R>(v, g, D, r, buf, scratch, f == 0 ? sel0 : sel1);
       __syncwarp();  // the v dump aliases the next projection's transpose buffer
@@ -318,7 +320,7 @@ k_project(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D,
   if (!active) return;
 #pragma unroll
   for (int e = 0; e < S::EPT; ++e) {
-    const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * S::EPT + e;
+    const uint32_t j = layout_index<P>(e, g);
     if (j < D) out[i * D + j] = v[e];
   }
 }
@@ -348,7 +350,7 @@ k_signatures(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ld, u
   uint64_t sig = 0;
 #pragma unroll
   for (int e = 0; e < S::EPT; ++e) {
-    const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * S::EPT + e;
+    const uint32_t j = layout_index<P>(e, g);
     if (j < m && v[e] >= 0.0f) sig |= 1ull << j;
   }
 #pragma unroll
@@ -405,7 +407,7 @@ k_order_keys(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t D, ui
     uint64_t best = 0;
 #pragma unroll
     for (int e = 0; e < S::EPT; ++e) {
-      const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * S::EPT + e;
+      const uint32_t j = layout_index<P>(e, g);
       if (j < D) {
         const uint64_t c = ((uint64_t)ord_key(fabsf(v[e])) << 32) |
                            ((uint64_t)(0x7fffffffu - j) << 1) | (v[e] < 0.0f ? 1u : 0u);

@@ -141,11 +141,16 @@ __device__ __forceinline__ void scale32(float (&v)[32], float s) {
 // Same butterfly graph as fht_group, but the cross-lane stages run in
 // registers after one shared-memory transpose per round instead of log2(G)
 // shuffle stages:
-//   layout A: lane g holds j = g*32 + e  (bits 0..4 in registers)
-//   layout B: lane g holds j = e*G + g   (bits lgG..lgG+4 in registers)
+//   layout A: lane g holds j = g*32 + e              (index bits 0..4 in registers)
+//   layout B: lane g holds j = (e / RUN)*32 + g*RUN + (e % RUN), RUN = 32/G
+//             (index bits 0..lgRUN-1 and 5..5+lgG-1 in registers: runs of RUN
+//             contiguous elements, so both sides of the transpose move 16-byte
+//             vectors for P <= 256, 8-byte for P = 512; P = 1024: RUN = 1)
+// Register stride RUN*2^m is index bit 5 + m in layout B, so the cross-lane stages are
+// the in-register strides RUN .. 16 (fht_regs_B).
 // Per-group scratch: TransposeShape<P>::STRIDE floats (16-byte aligned), padded
-// (4 floats per 32) so the vectorised A writes and the strided B reads are free
-// of bank conflicts, and group regions are offset to different banks.
+// (4 floats per 32) so the vectorised A rows (36 floats apart) and the B runs are
+// free of bank conflicts, and group regions are offset to different banks.
 template <int P>
 struct TransposeShape {
   static constexpr int G = P / 32;
@@ -153,8 +158,15 @@ struct TransposeShape {
 };
 __device__ __forceinline__ int tpad(int j) { return j + ((j >> 5) << 2); }
 
-// in-register butterflies of layout B: register bit k <-> index bit lgG + k;
-// run the stages of index bits 5 .. 5+lgG-1 (register strides 32/G .. 16)
+// layout B: the index held by register e of lane g
+template <int P>
+__host__ __device__ constexpr uint32_t jB(int e, int g) {
+  constexpr int RUN = 32 / (P / 32);
+  return (uint32_t)((e / RUN) * 32 + g * RUN + (e % RUN));
+}
+
+// in-register butterflies of layout B: run the stages of index bits 5 .. 5+lgG-1
+// (register strides 32/G .. 16)
 template <int P>
 __device__ __forceinline__ void fht_regs_B(float (&v)[32]) {
   constexpr int G = P / 32;
@@ -165,34 +177,59 @@ __device__ __forceinline__ void fht_regs_B(float (&v)[32]) {
   fht_stage32<16>(v);
 }
 
-// e*G + g stays in the 32-block of e*G (G | 32, g < G), so tpad(e*G + g) =
-// C(e) + g with C(e) = e*G + 4*((e*G) >> 5) a compile-time offset; the A rows
-// start at 36*g.  Every access is base register + immediate.
-template <int G>
-__host__ __device__ constexpr int tB(int e) { return e * G + 4 * ((e * G) >> 5); }
+// Layout-B registers <-> the padded buffer: register e = c*RUN + r lives at float
+// offset 36*c + g*RUN + r (tpad of jB: the run stays inside one 32-block).  Every
+// access is base register + immediate.
+template <int P, bool LOAD>
+__device__ __forceinline__ void move_B(float (&v)[32], float* rb) {
+  constexpr int G = P / 32, RUN = 32 / G;
+#pragma unroll
+  for (int c = 0; c < G; ++c) {
+    if constexpr (RUN >= 4) {
+#pragma unroll
+      for (int i = 0; i < RUN; i += 4) {
+        float4* p4 = reinterpret_cast<float4*>(rb + 36 * c + i);
+        const int e = c * RUN + i;
+        if constexpr (LOAD) {
+          const float4 q = *p4;
+          v[e] = q.x; v[e + 1] = q.y; v[e + 2] = q.z; v[e + 3] = q.w;
+        } else {
+          *p4 = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        }
+      }
+    } else if constexpr (RUN == 2) {
+      float2* p2 = reinterpret_cast<float2*>(rb + 36 * c);
+      if constexpr (LOAD) {
+        const float2 q = *p2;
+        v[2 * c] = q.x; v[2 * c + 1] = q.y;
+      } else {
+        *p2 = make_float2(v[2 * c], v[2 * c + 1]);
+      }
+    } else {
+      if constexpr (LOAD) v[c] = rb[36 * c];
+      else rb[36 * c] = v[c];
+    }
+  }
+}
 
 template <int P>
 __device__ __forceinline__ void transpose_A_to_B(float (&v)[32], int g, float* buf) {
-  constexpr int G = P / 32;
+  constexpr int RUN = 32 / (P / 32);
   float* ra = buf + 36 * g;
-  float* rb = buf + g;
 #pragma unroll
   for (int k = 0; k < 8; ++k)
     *reinterpret_cast<float4*>(ra + 4 * k) =
         make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
   __syncwarp();
-#pragma unroll
-  for (int e = 0; e < 32; ++e) v[e] = rb[tB<G>(e)];
+  move_B<P, true>(v, buf + g * RUN);
   __syncwarp();
 }
 
 template <int P>
 __device__ __forceinline__ void transpose_B_to_A(float (&v)[32], int g, float* buf) {
-  constexpr int G = P / 32;
+  constexpr int RUN = 32 / (P / 32);
   float* ra = buf + 36 * g;
-  float* rb = buf + g;
-#pragma unroll
-  for (int e = 0; e < 32; ++e) rb[tB<G>(e)] = v[e];
+  move_B<P, false>(v, buf + g * RUN);
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -202,8 +239,38 @@ __device__ __forceinline__ void transpose_B_to_A(float (&v)[32], int g, float* b
   __syncwarp();
 }
 
+// The index held by register e of lane g after a projection: layout B after the
+// transpose FHT (P >= 64), layout A (j = g*EPT + e) after the shuffle FHT.
+template <int P>
+__host__ __device__ constexpr uint32_t layout_index(int e, int g) {
+  if constexpr (P >= 64) return jB<P>(e, g);
+  else return (uint32_t)(g * (P < 32 ? P : 32) + e);
+}
+
+// Layout-B registers to an UNPADDED natural-order buffer (nat[j] = value of index j),
+// vectorised by runs (16-byte aligned buffer).
+template <int P>
+__device__ __forceinline__ void store_B_natural(const float (&v)[32], int g, float* nat) {
+  constexpr int G = P / 32, RUN = 32 / G;
+  float* rb = nat + g * RUN;
+#pragma unroll
+  for (int c = 0; c < G; ++c) {
+    if constexpr (RUN >= 4) {
+#pragma unroll
+      for (int i = 0; i < RUN; i += 4) {
+        const int e = c * RUN + i;
+        *reinterpret_cast<float4*>(rb + 32 * c + i) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+      }
+    } else if constexpr (RUN == 2) {
+      *reinterpret_cast<float2*>(rb + 32 * c) = make_float2(v[2 * c], v[2 * c + 1]);
+    } else {
+      rb[32 * c] = v[c];
+    }
+  }
+}
+
 // SpinnerStack::project with transpose FHTs: input in layout A, output in
-// layout B (element e of lane g is index e*G + g), scaled by 1/P.
+// layout B (element e of lane g is index jB<P>(e, g)), scaled by 1/P.
 template <int P>
 __device__ __forceinline__ void spinner_project_T(float (&v)[32], const uint32_t* sw, int g,
                                                   float* buf) {

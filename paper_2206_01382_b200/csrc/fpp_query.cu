@@ -193,10 +193,11 @@ k_query_lists(const float* __restrict__ Q, uint64_t nq, uint32_t d, uint32_t D, 
   for (int m = 1; m < S::G; m <<= 1) amax = fmaxf(amax, __shfl_xor_sync(FULL, amax, m));
   const float qs = amax > 0.0f ? 4194303.0f / amax : 0.0f;
   uint32_t kk[EPT];
+  if constexpr (TR) store_B_natural<P>(v, g, pv);
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
-    const uint32_t j = TR ? (uint32_t)e * S::G + g : (uint32_t)g * EPT + e;  // layout B / A
-    pv[j] = v[e];
+    const uint32_t j = layout_index<P>(e, g);  // layout B / A
+    if constexpr (!TR) pv[j] = v[e];
     // round(|p| * qs) via the 2^23 magic-number trick (FFMA + LOP on the FMA/ALU
     // pipes instead of F2I); monotone in |p| like the floor it replaces
     const uint32_t qv = min(__float_as_uint(fmaf(fabsf(v[e]), qs, 8388608.0f)) & 0x7fffffu, 4194303u);
