@@ -475,6 +475,11 @@ def build_block(cfg, name, steps, warmup, dd, check_tables, threads):
     mhz = clocks["sm_mhz"] or 1965.0
     adds = (hi - lo) * cfg["L"] * cfg["K"] * 3 * cfg["D"] * int(np.log2(cfg["D"]))
     fp32_peak = SM_COUNT * FP32_LANES * mhz * 1e6
+    # shared-memory crossbar (128 B/clk/SM): the five layout transposes of a projection
+    # write and read the padded vector once each
+    P = 1 << max(int(d - 1).bit_length(), 0)
+    smem_tr_bytes = (hi - lo) * cfg["L"] * cfg["K"] * 5 * 2 * P * 4
+    smem_peak = SM_COUNT * 128 * mhz * 1e6
     bytes_build = (4 * (hi - lo) * d + 24 * (hi - lo) * cfg["L"] * cfg["iprobes"]
                    + 8 * info["kept_total"] + 4 * cfg["L"] * (info["num_buckets"] + 1))
     hbm, peak_kind = peaks()
@@ -491,6 +496,13 @@ def build_block(cfg, name, steps, warmup, dd, check_tables, threads):
                                f"(median SM clock under load)",
             "fp32_frac_hash_kernel": adds / (hash_ms / 1e3) / fp32_peak,
             "fp32_frac_build": adds / step_s / fp32_peak,
+            "smem_transpose_bytes_per_build": smem_tr_bytes,
+            "smem_peak_bytes_per_s": smem_peak,
+            "smem_frac_hash_kernel_transposes": smem_tr_bytes / (hash_ms / 1e3) / smem_peak,
+            "smem_note": "k_hash_build is bound by shared-memory wavefronts, not FP32 issue: ncu "
+                         "l1tex__data_pipe_lsu_wavefronts 83.6% of peak (transposes ~60% of them, the "
+                         "top-r selection and spills the rest), issue-active 73%, FMA pipe 42% "
+                         "(profiles/r02_c5_hash_build.json)",
             "hbm_algorithmic_bytes": bytes_build, "hbm_achieved_gbs": bytes_build / step_s / 1e9,
             "hbm_peak": hbm, "peak_kind": peak_kind, "hbm_frac": bytes_build / step_s / 1e9 / hbm,
             "hash_ms": hash_ms, "sort_ms": sort_ms},
