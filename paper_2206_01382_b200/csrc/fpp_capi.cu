@@ -15,6 +15,7 @@
 
 #include <cuda_fp16.h>
 
+#include "fpp_device.cuh"
 #include "fpp_internal.h"
 
 namespace fpp {
@@ -205,8 +206,20 @@ uint64_t host_derive_seed(uint64_t m, uint64_t a, uint64_t b, uint64_t c) {  // 
   return h;
 }
 
-// Sign bitmasks [L][K][3][W]: bit e of word w of stage s is sign index
-// s*P + 32w + e of the stack's stream (rotation.cpp:55-67; bit = 1 -> +1).
+// Sign bitmasks [L][K][3][W]: bit e of word g of round s is the sign of index
+// sign_index<P>(s, e, g) of that round's P signs of the stack's stream (rotation.cpp:55-67;
+// bit = 1 -> +1): layout A (index 32g + e), except rounds 1 and 2 of the shuffle FHT plan,
+// whose words are in layout B (fpp_device.cuh).
+template <int P>
+static void pack_words(const std::vector<uint8_t>& bits, uint32_t* out) {
+  constexpr uint32_t W = P < 32 ? 1 : P / 32;
+  constexpr int EPT = P < 32 ? P : 32;
+  for (int s = 0; s < 3; ++s)
+    for (int g = 0; g < (int)W; ++g)
+      for (int e = 0; e < EPT; ++e)
+        if (bits[(size_t)s * P + sign_index<P>(s, e, g)]) out[s * W + g] |= 1u << e;
+}
+
 void pack_signs(const fpp_params& p, uint32_t P, std::vector<uint32_t>& words) {
   const uint32_t W = P < 32 ? 1 : P / 32;
   words.assign((size_t)p.L * p.K * 3 * W, 0u);
@@ -222,9 +235,20 @@ void pack_signs(const fpp_params& p, uint32_t P, std::vector<uint32_t>& words) {
         --left;
       }
       uint32_t* out = words.data() + ((size_t)t * p.K + f) * 3 * W;
-      for (uint32_t s = 0; s < 3; ++s)
-        for (uint32_t j = 0; j < P; ++j)
-          if (bits[(size_t)s * P + j]) out[s * W + j / 32] |= 1u << (j % 32);
+      switch (P) {
+        case 1: pack_words<1>(bits, out); break;
+        case 2: pack_words<2>(bits, out); break;
+        case 4: pack_words<4>(bits, out); break;
+        case 8: pack_words<8>(bits, out); break;
+        case 16: pack_words<16>(bits, out); break;
+        case 32: pack_words<32>(bits, out); break;
+        case 64: pack_words<64>(bits, out); break;
+        case 128: pack_words<128>(bits, out); break;
+        case 256: pack_words<256>(bits, out); break;
+        case 512: pack_words<512>(bits, out); break;
+        case 1024: pack_words<1024>(bits, out); break;
+        default: fail(FPP_ERR_UNSUPPORTED, "pack_signs: padded dimension > 1024 not supported on GPU");
+      }
     }
 }
 

@@ -269,6 +269,57 @@ __device__ __forceinline__ void store_B_natural(const float (&v)[32], int g, flo
   }
 }
 
+// Rounds 2 and 3 of the transpose FHT without leaving layout B (P <= 128, FPP_FHT_SHFL):
+// k_hash_build is bound by shared-memory wavefronts, and the B->A->B transposes of a
+// round cost 2 x 2 x P x 4 bytes of them.  Layout B already holds index bits
+// 0..lgRUN-1 and 5.. in registers; the lgG bits in between live in the lane id, so
+// their stages are a shuffle plus one FMA per element,
+//   lower lane:  x + y = fma(v, +1, o)      upper lane:  x - y = o - v = fma(v, -1, o)
+// (the product is exact, so the FMA is the IEEE add / subtract of the reference
+// butterfly, operands in its order).  The stage order stays len ascending.
+// Measured (B200): shuffles load the same crossbar as shared memory, so the plan pays
+// while lgG shuffle stages (32 SHFL each) cost less than the two transposes (128
+// wavefronts): P = 128 query hashing 8.2 -> 7.4 ms (C4), P = 256 build hashing 3.70 ->
+// 3.86 s (C5, three stages: kept on the transposes).
+#ifndef FPP_FHT_SHFL
+#define FPP_FHT_SHFL 1
+#endif
+template <int P>
+struct FhtPlan {
+  static constexpr int G = P / 32;
+  static constexpr bool SHFL = FPP_FHT_SHFL && P >= 64 && P <= 128;
+};
+
+// index of the sign bit that bit e of lane g's word of round `round` holds (host packing
+// and device use must agree): layout A, except rounds 1 and 2 of the shuffle plan (B)
+template <int P>
+__host__ __device__ constexpr uint32_t sign_index(int round, int e, int g) {
+  if constexpr (P >= 64) {
+    if (FhtPlan<P>::SHFL && round > 0) return jB<P>(e, g);
+  }
+  return (uint32_t)(g * (P < 32 ? P : 32) + e);
+}
+
+__device__ __forceinline__ void fma2_lane(float& a0, float& a1, float s, float o0, float o1) {
+  asm("{.reg .b64 ra, rs, ro, rd;\n\t"
+      "mov.b64 ra, {%0, %1};\n\tmov.b64 rs, {%2, %2};\n\tmov.b64 ro, {%3, %4};\n\t"
+      "fma.rn.f32x2 rd, ra, rs, ro;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(s), "f"(o0), "f"(o1));
+}
+
+// one cross-lane butterfly stage (lane bit m): every register of the lane pairs with
+// the same register of lane g ^ m
+__device__ __forceinline__ void fht_stage_lane(float (&v)[32], int g, int m) {
+  const float sg = (g & m) ? -1.0f : 1.0f;
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    const float o0 = __shfl_xor_sync(FULL, v[e], m);
+    const float o1 = __shfl_xor_sync(FULL, v[e + 1], m);
+    fma2_lane(v[e], v[e + 1], sg, o0, o1);
+  }
+}
+
 // SpinnerStack::project with transpose FHTs: input in layout A, output in
 // layout B (element e of lane g is index jB<P>(e, g)), scaled by 1/P.
 template <int P>
@@ -277,10 +328,9 @@ __device__ __forceinline__ void spinner_project_T(float (&v)[32], const uint32_t
   constexpr int G = P / 32;
   // the three rounds' sign words are loaded up front (one latency, not three)
   const uint32_t w0 = __ldg(sw + g), w1 = __ldg(sw + G + g), w2 = __ldg(sw + 2 * G + g);
-#pragma unroll 1
-  for (int stage = 0; stage < 3; ++stage) {
-    if (stage) transpose_B_to_A<P>(v, g, buf);
-    apply_signs<32>(v, stage == 0 ? w0 : (stage == 1 ? w1 : w2));
+  if constexpr (FhtPlan<P>::SHFL) {
+    constexpr int RUN = 32 / G;
+    apply_signs<32>(v, w0);
     fht_stage32<1>(v);
     fht_stage32<2>(v);
     fht_stage32<4>(v);
@@ -288,6 +338,33 @@ __device__ __forceinline__ void spinner_project_T(float (&v)[32], const uint32_t
     fht_stage32<16>(v);
     transpose_A_to_B<P>(v, g, buf);
     fht_regs_B<P>(v);
+#pragma unroll 1
+    for (int stage = 1; stage < 3; ++stage) {
+      apply_signs<32>(v, stage == 1 ? w1 : w2);  // words packed in layout B (sign_index)
+      // index bits 0 .. lgRUN-1: register strides 1 .. RUN/2
+      fht_stage32<1>(v);
+      if constexpr (RUN > 2) fht_stage32<2>(v);
+      if constexpr (RUN > 4) fht_stage32<4>(v);
+      if constexpr (RUN > 8) fht_stage32<8>(v);
+      // index bits lgRUN .. 4: lane bits 0 .. lgG-1
+#pragma unroll
+      for (int m = 1; m < G; m <<= 1) fht_stage_lane(v, g, m);
+      // index bits 5 ..: register strides RUN .. 16
+      fht_regs_B<P>(v);
+    }
+  } else {
+#pragma unroll 1
+    for (int stage = 0; stage < 3; ++stage) {
+      if (stage) transpose_B_to_A<P>(v, g, buf);
+      apply_signs<32>(v, stage == 0 ? w0 : (stage == 1 ? w1 : w2));
+      fht_stage32<1>(v);
+      fht_stage32<2>(v);
+      fht_stage32<4>(v);
+      fht_stage32<8>(v);
+      fht_stage32<16>(v);
+      transpose_A_to_B<P>(v, g, buf);
+      fht_regs_B<P>(v);
+    }
   }
   scale32(v, 1.0f / (float)P);
 }
