@@ -1769,16 +1769,24 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
   const float* X = a.X;
   // issue cursor
   uint32_t ib = w, ic = 0, nissued = 0;
-  const float* rp[8];
+  // Copy mapping (VEC): with 64-float slices an instruction covers 2 rows x 256 contiguous
+  // bytes (16 lanes per row); with 32-float slices 4 rows x 128 bytes.  B200 serves random
+  // 256-byte row segments requested by ONE instruction at 6.0-6.2 TB/s, the same bytes as
+  // two 128-byte halves from two instructions at 4.7-4.8 (profiles/probes/gather4_probe.cu;
+  // TMA tile::gather4 with a 64-float box: 6.2-6.4)
+  constexpr int LPR = SC_SLICE >= 64 ? 16 : 8;  // lanes per row
+  constexpr int RPI = 32 / LPR;                 // rows per instruction
+  constexpr int NIT = 32 / RPI;
+  const float* rp[NIT];
   uint32_t my_id = 0xffffffffu;
-  const int kk = lane & 7, rbase = lane >> 3;
+  const int kk = lane % LPR, rbase = lane / LPR;
   auto load_batch = [&](uint32_t bidx) {
     const uint32_t ci = bidx * 32 + lane;
     my_id = ci < U ? __ldg(cand + ci) : 0xffffffffu;
     if (VEC) {
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const uint32_t idr = __shfl_sync(FULL, my_id, rbase + 4 * it);
+      for (int it = 0; it < NIT; ++it) {
+        const uint32_t idr = __shfl_sync(FULL, my_id, rbase + RPI * it);
         rp[it] = idr != 0xffffffffu ? X + (uint64_t)idr * a.ldx : nullptr;
       }
     }
@@ -1790,12 +1798,12 @@ __global__ void __launch_bounds__(SC_WARPS * 32, MINB) k_score(ScoreArgs a) {
       const uint32_t len = min((uint32_t)SC_SLICE, d - col0);
       if (VEC) {
 #pragma unroll
-        for (int h = 0; h < SC_SLICE / 32; ++h) {  // 16 B chunks kk + 8h of each row
-          const uint32_t ch = kk + 8 * h;
+        for (int h = 0; h < SC_SLICE / (4 * LPR); ++h) {  // 16 B chunks kk + LPR*h of each row
+          const uint32_t ch = kk + LPR * h;
           if (ch < (len >> 2)) {
 #pragma unroll
-            for (int it = 0; it < 8; ++it)
-              if (rp[it]) cp_async16(buf + (rbase + 4 * it) * SC_ROWPAD + ch * 4, rp[it] + col0 + ch * 4);
+            for (int it = 0; it < NIT; ++it)
+              if (rp[it]) cp_async16(buf + (rbase + RPI * it) * SC_ROWPAD + ch * 4, rp[it] + col0 + ch * 4);
           }
         }
       } else {
@@ -2101,6 +2109,8 @@ __global__ void __launch_bounds__(NW * 32, MINB) k_score_pruned(ScoreArgs a) {
             bulk_g2s(dst + rot * 4, src, n1 * 16, &mbar[w][islot]);
             if (nch > n1) bulk_g2s(dst, src + n1 * 4, (nch - n1) * 16, &mbar[w][islot]);
           }
+        // (4 rows x 128 B per instruction; the 2 rows x 256 B mapping of k_score measured
+        // slower here: C2 2.76 vs 2.64 ms per launch -- this kernel is bound by job latency)
         } else if (VEC) {
 #pragma unroll
           for (int it = 0; it < 8; ++it) {
