@@ -907,7 +907,9 @@ def run_query_bench(args, cfg, qprobes):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=0,
+                    help="timed steps (default: 5; the short c1-c3 steps default to enough "
+                         "steps for about a second, so the clock sampler sees the timed region)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--qprobes", type=int, default=0)
@@ -927,6 +929,9 @@ def main():
                     help="query (default for c1-c4) or build-only throughput (default for c5)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.steps <= 0:
+        args.steps = ({"c1": 1000, "c2": 60, "c3": 400}.get(args.config, 5)
+                      if args.impl == "ours" else 5)
     cfg = CONFIGS[args.config]
     qprobes = args.qprobes or cfg["qprobes"]
     mode = args.mode or ("build" if args.config == "c5" else "query")
