@@ -29,6 +29,14 @@ namespace fpp {
 
 // ------------------------------------------------------------------ K1 build
 constexpr int HB_SEL = 32;  // keys sorted after the threshold preselection
+// k_hash_build CTA size and CTAs per SM (FPP_HB_THREADS x FPP_HB_MINB warps resident)
+#ifndef FPP_HB_THREADS
+#define FPP_HB_THREADS 256
+#endif
+#ifndef FPP_HB_MINB
+#define FPP_HB_MINB 3
+#endif
+constexpr int HB_THREADS = FPP_HB_THREADS;
 
 // Rank pairs (a, b) with (a + 1)(b + 1) <= R: the only candidates for the top ip <= R
 // pairs (every pair with a' <= a, b' <= b strictly precedes (a, b)); D(R) = sum_a
@@ -65,11 +73,11 @@ __device__ __forceinline__ uint32_t pair_ab(int i) {
 // two sorted top-R lists
 template <int P>
 __host__ __device__ constexpr int hb_tbuf_bytes() {
-  return (256 / (P < 32 ? 1 : P / 32)) * (P >= 64 ? TransposeShape<P>::STRIDE : 4) * 4;
+  return (HB_THREADS / (P < 32 ? 1 : P / 32)) * (P >= 64 ? TransposeShape<P>::STRIDE : 4) * 4;
 }
 template <int P, int R>
 constexpr int hb_smem_bytes() {
-  return hb_tbuf_bytes<P>() + (256 / (P < 32 ? 1 : P / 32)) * (HB_SEL + 2 * R) * 8;
+  return hb_tbuf_bytes<P>() + (HB_THREADS / (P < 32 ? 1 : P / 32)) * (HB_SEL + 2 * R) * 8;
 }
 
 // Top-r selection of one projection (r = min(iProbes, D) <= R), exact order
@@ -201,10 +209,7 @@ __device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], in
 }
 
 template <int P, int R>
-#ifndef FPP_HB_MINB
-#define FPP_HB_MINB 3
-#endif
-__global__ void __launch_bounds__(256, FPP_HB_MINB)
+__global__ void __launch_bounds__(HB_THREADS, FPP_HB_MINB)
 k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx, uint32_t D,
              uint32_t K,
              const uint32_t* __restrict__ signs, uint32_t t0, uint32_t T, uint32_t ip,
@@ -216,7 +221,7 @@ k_hash_build(const float* __restrict__ X, uint64_t n, uint32_t d, uint32_t ldx, 
   // floats (reused as the 32-key sort scratch once the FHT is done), then per
   // group the sorted top-R lists of the K functions
   extern __shared__ __align__(16) unsigned char hb_smem[];
-  constexpr int NGRP = 256 / S::G;
+  constexpr int NGRP = HB_THREADS / S::G;
   const int lane = threadIdx.x & 31;
   const int g = lane % S::G;
   const int grp = threadIdx.x / S::G;
@@ -808,7 +813,7 @@ static void launch_hash_R(const Index& ix, const float* X, uint32_t ld, uint64_t
   const uint32_t P = ix.P;
   uint32_t G = P < 32 ? 1 : P / 32;
   const uint64_t threads = n * G;
-  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  const unsigned blocks = (unsigned)((threads + HB_THREADS - 1) / HB_THREADS);
   const uint32_t K = ix.prm.K, D = ix.prm.D, ip = ix.prm.iprobes;
 #define FPP_HASH_CASE(PP)                                                                      \
   case PP: {                                                                                   \
@@ -816,7 +821,7 @@ static void launch_hash_R(const Index& ix, const float* X, uint32_t ld, uint64_t
     if (sm > 48 * 1024)                                                                        \
       FPP_CUDA(cudaFuncSetAttribute(k_hash_build<PP, R>,                                       \
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, sm));         \
-    k_hash_build<PP, R><<<blocks, 256, sm, s>>>(X, n, ix.d, ld, D, K, ix.signs, t0, T, ip, ent, \
+    k_hash_build<PP, R><<<blocks, HB_THREADS, sm, s>>>(X, n, ix.d, ld, D, K, ix.signs, t0, T, ip, ent, \
                                                 counts, ix.NB);                                \
     break;                                                                                     \
   }
