@@ -26,7 +26,7 @@ def bits(a):
     return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
 
 
-@pytest.mark.parametrize("d", [2, 5, 17, 32, 100, 128, 256, 300, 960])
+@pytest.mark.parametrize("d", [2, 5, 17, 32, 48, 64, 100, 128, 256, 300, 960])
 def test_projection_bitexact(fpp, orc, d):
     X = data(fpp, 257, d)
     P = orc.lib().orc_pad_dimension(d)
@@ -535,3 +535,22 @@ def test_query_out_buffers(fpp, orc):
     assert np.array_equal(oi, gi) and np.array_equal(os_, gs)
     with pytest.raises(ValueError):
         ix.query(Q, 10, 300, out=(np.zeros((50, 9), np.uint32), os_))
+
+
+@pytest.mark.parametrize("d,D,ip", [(64, 64, 5), (128, 128, 3), (256, 256, 5)])
+def test_index_probes_equal_magnitudes(fpp, orc, d, D, ip):
+    # rows with six non-zeros: a projection takes at most 32 distinct |p| values, each at
+    # several coordinates, so the top-r selection meets exact |p| ties among its kept keys
+    # (the high-word group minimum must fall back to the low words: j ascending)
+    rng = np.random.default_rng(7)
+    X = np.zeros((300, d), np.float32)
+    for i in range(300):
+        X[i, rng.choice(d, 6, replace=False)] = rng.standard_normal(6).astype(np.float32)
+    X = fpp.normalize(X)
+    ix = fpp.Index.build(X, L=3, K=2, D=D, iProbes=ip, alpha=0.5)
+    ox = orc.Index(X, L=3, K=2, D=D, iprobes=ip, alpha=0.5)
+    for t in range(3):
+        gb, gs = ix.index_probes(X, t)
+        ob, os_ = ox.index_probes(X, t)
+        assert np.array_equal(gb, ob), (d, t)
+        assert np.array_equal(bits(gs), bits(os_)), (d, t)
