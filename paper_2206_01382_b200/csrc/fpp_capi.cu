@@ -402,7 +402,9 @@ __global__ void k_q8_records(const float* __restrict__ X, uint64_t n, uint32_t d
 void launch_tail_norms(Index& ix) {
   // FPP_L2_FETCH=32|64|128: cudaLimitMaxL2FetchGranularity hint (experiments)
   if (getenv("FPP_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(getenv("FPP_L2_FETCH")));
-  if (ix.d >= 64 && ix.d <= 256 && ix.d % 4 == 0) {  // k_score_screen's records
+  // FPP_SC_DMAX: widest rows that get screening records (default 256; experiments)
+  static const uint32_t sc_dmax = getenv("FPP_SC_DMAX") ? (uint32_t)atoi(getenv("FPP_SC_DMAX")) : 256u;
+  if (ix.d >= 64 && ix.d <= sc_dmax && ix.d % 4 == 0) {  // k_score_screen's records
     ix.q8rec = static_cast<uint4*>(dmalloc((size_t)ix.n * (32 + 128)));
     k_q8_records<<<sm_count() * 8, 256, 0, ix.stream>>>(ix.X, ix.n, ix.d, ix.ldx, ix.q8rec);
     FPP_LAUNCH();
