@@ -3670,8 +3670,11 @@ static uint32_t chunk_size(const Index& ix, uint32_t qprobes, uint64_t nq) {
   const uint64_t LKs = (uint64_t)ix.prm.L * ix.prm.K * query_cap(ix, qprobes);
   const uint64_t pe = query_probes(ix, qprobes);
   const uint64_t per_q = LKs * 8 + pe * 16 + (4 * pe + 16384) * 8 + 64;
-  uint64_t c = (4ull << 30) / per_q;  // ~4 GB of per-chunk scratch per slot
-  c = std::max<uint64_t>(1, std::min<uint64_t>(c, 8192));
+  // ~4 GB of per-chunk scratch per slot, at most 8192 queries (FPP_CHUNK_GB / FPP_CHUNK_MAX)
+  static const uint64_t cgb = getenv("FPP_CHUNK_GB") ? std::max(1, atoi(getenv("FPP_CHUNK_GB"))) : 4;
+  static const uint64_t cmax = getenv("FPP_CHUNK_MAX") ? std::max(1, atoi(getenv("FPP_CHUNK_MAX"))) : 8192;
+  uint64_t c = (cgb << 30) / per_q;
+  c = std::max<uint64_t>(1, std::min<uint64_t>(c, cmax));
   // at least 3 chunks when the batch allows, so the two-stream pipeline overlaps
   // (C2 sweep: 2 chunks 288k, 3 -> 300k, 4 -> 295k, 6 -> 290k, 8 -> 275k q/s);
   // FPP_CHUNKS overrides
