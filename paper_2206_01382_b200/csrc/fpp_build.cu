@@ -186,12 +186,17 @@ __device__ __forceinline__ void hb_select(const float (&v)[FhtShape<P>::EPT], in
       if ((full || j < D) && a > thr) {
         float cp = v[e];
         uint32_t cj = j;
+        bool shift = false;
 #pragma unroll
         for (int q = 0; q < R; ++q) {  // insert, shifting the tail down
-          const bool ins = tj[q] == 0xffffffffu || fabsf(cp) > fabsf(tp[q]);
+          // once the new entry is placed every later slot shifts unconditionally: a
+          // displaced entry must stay AHEAD of the entries it was ahead of, also of those
+          // with an equal |p| (j ascending among ties) -- a strict compare here would
+          // let a displaced entry slip behind its tied successor
+          const bool ins = shift || tj[q] == 0xffffffffu || fabsf(cp) > fabsf(tp[q]);
           const float op = tp[q];
           const uint32_t oj = tj[q];
-          if (ins) { tp[q] = cp; tj[q] = cj; cp = op; cj = oj; }
+          if (ins) { tp[q] = cp; tj[q] = cj; cp = op; cj = oj; shift = true; }
         }
         thr = tj[R - 1] == 0xffffffffu ? -1.0f : fabsf(tp[R - 1]);
       }

@@ -1,0 +1,51 @@
+"""Randomised GPU-vs-oracle soak (not a pytest module): random small configurations for
+a bounded time; ids, scores and stats must equal the oracle's.
+usage: python profiles/soak_parity.py [seconds] [seed]"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+import paper_2206_01382_b200 as fpp
+from oracle import oracle as orc
+
+budget = float(sys.argv[1]) if len(sys.argv) > 1 else 240.0
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
+t0, cases = time.time(), 0
+while time.time() - t0 < budget:
+    d = int(rng.choice([8, 17, 32, 48, 64, 100, 128, 200, 256, 300, 320, 512, 960]))
+    n = int(rng.integers(500, 12000))
+    K = int(rng.choice([1, 2, 2, 2]))
+    P = 1 << max(int(d - 1).bit_length(), 0)
+    D = int(rng.choice([P, P, max(P // 2, 2)]))
+    ip = int(rng.integers(1, min(D, 8) + 1))
+    L = int(rng.integers(1, 7))
+    alpha = float(rng.choice([1.0, 0.5, 0.1, 0.02]))
+    kappa = int(rng.choice([0, 5, 20]))
+    clusters = int(rng.choice([0, 5, 40]))
+    seed = int(rng.integers(1, 1 << 30))
+    X = fpp.normalize(fpp.synth(n, d, clusters, 0.3, seed=seed))
+    Q = fpp.normalize(fpp.synth(int(rng.integers(1, 90)), d, clusters, 0.3, seed=seed, stream=1))
+    prm = dict(L=L, K=K, D=D, alpha=alpha, kappa=kappa, seed=seed)
+    ix = fpp.Index.build(X, iProbes=ip, **prm)
+    ox = orc.Index(X, iprobes=ip, **prm)
+    NB = (2 * D) ** K
+    for _ in range(3):
+        k = int(rng.choice([1, 7, 20, 32, 33, 50, 100]))
+        k = min(k, n)
+        qp = int(rng.integers(L, min(L * NB, 30000) + 1))
+        stats = bool(rng.integers(0, 2))
+        if stats:
+            gi, gs, gst = ix.query(Q, k, qp, return_stats=True)
+        else:
+            gi, gs = ix.query(Q, k, qp)
+        oi, os_, ost = ox.query(Q, k, qp)
+        ok = np.array_equal(gi, oi) and np.array_equal(gs, os_) and (not stats or np.array_equal(gst, ost))
+        if not ok:
+            print("MISMATCH", dict(n=n, d=d, ip=ip, k=k, qp=qp, stats=stats, clusters=clusters, **prm), flush=True)
+            sys.exit(1)
+    ix.close()
+    cases += 1
+print(f"soak ok: {cases} random configurations x 3 queries batches in {time.time() - t0:.0f} s")

@@ -554,3 +554,57 @@ def test_index_probes_equal_magnitudes(fpp, orc, d, D, ip):
         ob, os_ = ox.index_probes(X, t)
         assert np.array_equal(gb, ob), (d, t)
         assert np.array_equal(bits(gs), bits(os_)), (d, t)
+
+
+def test_top_r_insertion_keeps_tie_order(fpp, orc):
+    # regression (found by profiles/soak_parity.py): the lane-local top-R insertion of the
+    # shuffle-FHT path (d_pad < 64, and the tie fallback above) must shift the displaced
+    # entries unconditionally -- with a strict compare a displaced entry slipped behind a
+    # successor of equal |p| (here j = 2 and j = 22 of row 18, table 2), swapping two index
+    # probes and so the kept set of four buckets
+    X = data(fpp, 10205, 17, clusters=5, sigma=0.3, seed=850085278)
+    prm = dict(L=3, K=1, D=32, alpha=1.0, kappa=5, seed=850085278)
+    ix = fpp.Index.build(X, iProbes=8, **prm)
+    ox = orc.Index(X, iprobes=8, **prm)
+    for t in range(3):
+        gb, gs = ix.index_probes(X, t)
+        ob, os_ = ox.index_probes(X, t)
+        assert np.array_equal(gb, ob), t
+        assert np.array_equal(bits(gs), bits(os_)), t
+        go, gi, gsc = ix.table(t)
+        oo, oi, osc = ox.table(t)
+        assert np.array_equal(go, oo) and np.array_equal(gi, oi) and np.array_equal(bits(gsc), bits(osc))
+
+
+def test_random_configurations_equal_oracle(fpp, orc):
+    # a short, seeded run of profiles/soak_parity.py's generator: random (n, d, K, D, iProbes,
+    # L, alpha, kappa, clusters, k, qProbes, stats on/off); ids, scores, stats = the oracle's
+    rng = np.random.default_rng(20260121)
+    for _ in range(60):
+        d = int(rng.choice([8, 17, 32, 48, 64, 100, 128, 200, 256, 300, 320, 512, 960]))
+        n = int(rng.integers(500, 6000))
+        K = int(rng.choice([1, 2, 2, 2]))
+        P = int(orc.lib().orc_pad_dimension(d))
+        D = int(rng.choice([P, P, max(P // 2, 2)]))
+        ip = int(rng.integers(1, min(D, 8) + 1))
+        L = int(rng.integers(1, 6))
+        prm = dict(L=L, K=K, D=D, alpha=float(rng.choice([1.0, 0.5, 0.1, 0.02])),
+                   kappa=int(rng.choice([0, 5, 20])), seed=int(rng.integers(1, 1 << 30)))
+        clusters = int(rng.choice([0, 5, 40]))
+        X = data(fpp, n, d, clusters, 0.3, seed=prm["seed"])
+        Q = data(fpp, int(rng.integers(1, 70)), d, clusters, 0.3, seed=prm["seed"], stream=1)
+        ix = fpp.Index.build(X, iProbes=ip, **prm)
+        ox = orc.Index(X, iprobes=ip, **prm)
+        NB = (2 * D) ** K
+        for _ in range(2):
+            k = min(int(rng.choice([1, 7, 20, 32, 33, 50, 100])), n)
+            qp = int(rng.integers(L, min(L * NB, 20000) + 1))
+            gi, gs, gst = ix.query(Q, k, qp, return_stats=True)
+            oi, os_, ost = ox.query(Q, k, qp)
+            case = dict(n=n, d=d, ip=ip, k=k, qp=qp, clusters=clusters, **prm)
+            assert np.array_equal(gi, oi), case
+            assert np.array_equal(gs, os_), case
+            assert np.array_equal(gst, ost), case
+            gi2, gs2 = ix.query(Q, k, qp)  # the stats-off (timed) path
+            assert np.array_equal(gi2, oi) and np.array_equal(gs2, os_), case
+        ix.close()
