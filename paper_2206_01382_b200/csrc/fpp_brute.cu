@@ -269,12 +269,10 @@ void run_brute_force(const Index& ix, const float* Qd, uint64_t nq, uint32_t k, 
     BruteArgs a{ix.X, ix.n, d, ix.ldx, Qd, (uint32_t)nq, kp, rows_per_split, pids.p, psc.p,
                 off ? ids_d : nullptr, scores_d, k, off, ix.prm.id_offset};
     if ((d & 3u) == 0) {
-      FPP_CUDA(cudaFuncSetAttribute(k_brute<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
+      allow_dynamic_smem(k_brute<true>);
       k_brute<true><<<grid, BF_WARPS * 32, smem, s>>>(a);
     } else {
-      FPP_CUDA(cudaFuncSetAttribute(k_brute<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
+      allow_dynamic_smem(k_brute<false>);
       k_brute<false><<<grid, BF_WARPS * 32, smem, s>>>(a);
     }
     FPP_LAUNCH();

@@ -823,9 +823,7 @@ static void launch_hash_R(const Index& ix, const float* X, uint32_t ld, uint64_t
 #define FPP_HASH_CASE(PP)                                                                      \
   case PP: {                                                                                   \
     constexpr int sm = hb_smem_bytes<PP, R>();                                                 \
-    if (sm > 48 * 1024)                                                                        \
-      FPP_CUDA(cudaFuncSetAttribute(k_hash_build<PP, R>,                                       \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, sm));         \
+    if (sm > 48 * 1024) allow_dynamic_smem(k_hash_build<PP, R>);                               \
     k_hash_build<PP, R><<<blocks, HB_THREADS, sm, s>>>(X, n, ix.d, ld, D, K, ix.signs, t0, T, ip, ent, \
                                                 counts, ix.NB);                                \
     break;                                                                                     \

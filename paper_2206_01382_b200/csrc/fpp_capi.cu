@@ -271,6 +271,17 @@ uint64_t query_probes(const Index& ix, uint32_t qprobes) {
   return std::min<uint64_t>(qprobes, avail);
 }
 
+int smem_optin_max() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    v = optin;
+  }
+  return v;
+}
+
 int sm_count() {
   static int v = -1;
   if (v < 0) {

@@ -204,6 +204,19 @@ void pack_signs(const fpp_params& p, uint32_t P, std::vector<uint32_t>& words);
 uint32_t query_cap(const Index& ix, uint32_t qprobes);
 uint64_t query_probes(const Index& ix, uint32_t qprobes);
 int sm_count();
+int smem_optin_max();  // cudaDevAttrMaxSharedMemoryPerBlockOptin of the current device
+// Let `kern` be launched with any dynamic shared-memory size the device allows.  The
+// limit is a per-function, per-device attribute shared by every host thread: setting it to
+// each launch's own size raced between threads driving indexes of different sizes on one
+// device (thread A: set 324 B, thread B: set 320 B, thread A: launch with 324 B ->
+// "invalid argument"), so every caller sets the same, largest value.
+template <class Kern>
+inline void allow_dynamic_smem(Kern kern) {
+  cudaFuncAttributes fa;
+  FPP_CUDA(cudaFuncGetAttributes(&fa, kern));
+  FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin_max() - (int)fa.sharedSizeBytes));
+}
 
 // build (fpp_build.cu)
 void build_tables(Index& ix);

@@ -3195,16 +3195,7 @@ void launch_query_lists(const Index& ix, const float* Qd, uint64_t nq, uint32_t 
   FPP_LAUNCH();
 }
 
-static int co_smem_max() {
-  static int v = -1;
-  if (v < 0) {
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    v = optin;
-  }
-  return v;
-}
+static int co_smem_max() { return smem_optin_max(); }
 
 // Stage A of one chunk on stream `st`: query hashing, probe selection,
 // candidate offsets; the total candidate count is copied to the slot's pinned
@@ -3418,8 +3409,7 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   unsigned co_grid;
   if (!force && (size_t)nwords * 4 + static_co <= (size_t)co_smem_max()) {
     const size_t co_smem = (size_t)nwords * 4;
-    FPP_CUDA(cudaFuncSetAttribute(k_collect, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)co_smem));
+    allow_dynamic_smem(k_collect);
     int occ = 1;
     FPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collect, CO_THREADS, co_smem));
     co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * std::max(occ, 1));
@@ -3430,8 +3420,7 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     ca.grouped = 1;
     ca.gshift = gshift;
     const size_t co_smem = (size_t)CO_NG * 4 + (size_t)32 * ((1ull << gshift) / 8);
-    FPP_CUDA(cudaFuncSetAttribute(k_collect, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)co_smem));
+    allow_dynamic_smem(k_collect);
     int occ = 1;
     FPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collect, CO_THREADS, co_smem));
     co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * std::max(occ, 1));
@@ -3444,8 +3433,7 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     ca.sliced = 1;
     ca.gshift = CO_SLICE_BITS;
     const size_t co_smem = (size_t)CO_NG * 4 + (4ull << (CO_SLICE_BITS - 5));
-    FPP_CUDA(cudaFuncSetAttribute(k_collect, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)co_smem));
+    allow_dynamic_smem(k_collect);
     int occ = 1;
     FPP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_collect, CO_THREADS, co_smem));
     co_grid = (unsigned)std::min<uint64_t>(nqc, (uint64_t)sms * std::max(occ, 1));
@@ -3454,8 +3442,7 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   } else if (!f_global && (size_t)slice_words * 4 + static_co <= (size_t)co_smem_max()) {
     // bitmap split over a CO_CLUSTER-CTA cluster (DSMEM)
     const size_t sm = (size_t)slice_words * 4;
-    FPP_CUDA(cudaFuncSetAttribute(k_collect_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sm));
+    allow_dynamic_smem(k_collect_cluster);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CO_CLUSTER);
     cfg.blockDim = dim3(CO_CL_THREADS);
@@ -3509,7 +3496,7 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
   }
   auto launch_score = [&](auto kern, int slice, int stg) {
     const size_t sm = score_smem(ix.d, slice, stg);
-    FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    allow_dynamic_smem(kern);
     unsigned grid = nqc;
     if (sc_ctas > 0 && (uint64_t)sm_count() * sc_ctas < nqc) {
       grid = (unsigned)(sm_count() * sc_ctas);
@@ -3549,7 +3536,7 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     // 4-batch ring; FPP_SC_SCR_MINB=2 selects the 2-CTA register budget
     static const int scr_minb = getenv("FPP_SC_SCR_MINB") ? atoi(getenv("FPP_SC_SCR_MINB")) : 3;
     auto launch_scr = [&](auto kern) {
-      FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      allow_dynamic_smem(kern);
       unsigned grid = nqc;
       if (walk) {  // persistent CTAs, one visited bitmap + admission log each
         ensure_q8csr(ix);
@@ -3606,7 +3593,7 @@ static void stage_b(const Index& ix, QueryCtx& cx, QSlot& sl, const float* Qd, u
     // 20.7 (4x4 @ 1/SM))
     auto launch_pruned = [&](auto kern, int nw, int stg) {
       const size_t sm = (size_t)nw * stg * 32 * XT_SLICE * 4 + ((ix.d * 8 + 127) / 128) * 128;
-      FPP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      allow_dynamic_smem(kern);
       unsigned grid = nqc;
       if (sc_ctas > 0 && (uint64_t)sm_count() * sc_ctas < nqc) {
         grid = (unsigned)(sm_count() * sc_ctas);

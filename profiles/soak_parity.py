@@ -29,22 +29,49 @@ while time.time() - t0 < budget:
     X = fpp.normalize(fpp.synth(n, d, clusters, 0.3, seed=seed))
     Q = fpp.normalize(fpp.synth(int(rng.integers(1, 90)), d, clusters, 0.3, seed=seed, stream=1))
     prm = dict(L=L, K=K, D=D, alpha=alpha, kappa=kappa, seed=seed)
-    ix = fpp.Index.build(X, iProbes=ip, **prm)
-    ox = orc.Index(X, iprobes=ip, **prm)
+    # variants: falconn_baseline mode, centering, a 2..3-shard MultiIndex on one device
+    variant = str(rng.choice(["plain", "plain", "baseline", "centering", "multi"]))
+    if variant == "baseline":
+        ix = fpp.Index.build(X, iProbes=ip, mode="falconn_baseline", **prm)
+        ox = orc.Index(X, iprobes=ip, mode=1, **prm)
+    elif variant == "centering":
+        X = X + np.float32(0.03)
+        ix = fpp.Index.build(X, iProbes=ip, centering=True, **prm)
+        ox = orc.Index(orc.center(X)[0], iprobes=ip, **prm)
+    elif variant == "multi":
+        G = int(rng.integers(2, 4))
+        ix = fpp.MultiIndex.build(X, num_gpus=G, devices=[0] * G, iProbes=ip, **prm)
+        ox = orc.Index(X, iprobes=ip, **prm)
+    else:
+        ix = fpp.Index.build(X, iProbes=ip, **prm)
+        ox = orc.Index(X, iprobes=ip, **prm)
     NB = (2 * D) ** K
     for _ in range(3):
         k = int(rng.choice([1, 7, 20, 32, 33, 50, 100]))
         k = min(k, n)
         qp = int(rng.integers(L, min(L * NB, 30000) + 1))
         stats = bool(rng.integers(0, 2))
-        if stats:
-            gi, gs, gst = ix.query(Q, k, qp, return_stats=True)
-        else:
-            gi, gs = ix.query(Q, k, qp)
-        oi, os_, ost = ox.query(Q, k, qp)
-        ok = np.array_equal(gi, oi) and np.array_equal(gs, os_) and (not stats or np.array_equal(gst, ost))
+        rr = int(rng.choice([0, 0, k, 3 * k, 50 * k])) if variant in ("plain", "baseline") else 0
+        kw = dict(rerank=rr) if rr else {}
+        if os.environ.get("SOAK_LOG"):
+            print("Q", dict(variant=variant, n=n, d=d, ip=ip, k=k, qp=qp, stats=stats, rerank=rr,
+                            clusters=clusters, nq=len(Q), **prm), file=sys.stderr, flush=True)
+        try:
+            if stats:
+                gi, gs, gst = ix.query(Q, k, qp, return_stats=True, **kw)
+            else:
+                gi, gs = ix.query(Q, k, qp, **kw)
+        except Exception as ex:
+            print("EXCEPTION", ex, dict(variant=variant, n=n, d=d, ip=ip, k=k, qp=qp, stats=stats, rerank=rr,
+                                        clusters=clusters, nq=len(Q), **prm), flush=True)
+            sys.exit(2)
+        oi, os_, ost = ox.query(Q, k, qp, **kw)
+        ncol = 3 if variant == "multi" else ost.shape[1]  # (the multi index reports no exact count)
+        ok = np.array_equal(gi, oi) and np.array_equal(gs, os_) and \
+            (not stats or np.array_equal(gst[:, :ncol], ost[:, :ncol]))
         if not ok:
-            print("MISMATCH", dict(n=n, d=d, ip=ip, k=k, qp=qp, stats=stats, clusters=clusters, **prm), flush=True)
+            print("MISMATCH", dict(variant=variant, n=n, d=d, ip=ip, k=k, qp=qp, stats=stats, rerank=rr,
+                                   clusters=clusters, nq=len(Q), **prm), flush=True)
             sys.exit(1)
     ix.close()
     cases += 1

@@ -104,6 +104,43 @@ def test_concurrent_queries_two_threads_two_streams(fpp, orc):
     assert not errors, errors
 
 
+def test_concurrent_queries_on_indexes_of_different_sizes(fpp, orc):
+    """Three host threads query three indexes of different n on ONE device at once.  The
+    collect kernel's dynamic shared memory (the n-bit visited bitmap) differs per index;
+    its per-function limit used to be set to each launch's own size, which raced between
+    threads ("invalid argument at kernel launch", found by profiles/soak_parity.py on a
+    3-shard MultiIndex).  Every answer must equal the oracle's."""
+    prm = dict(L=4, K=2, D=64, alpha=0.3, kappa=5)
+    sizes = (2561, 4100, 7777)
+    Xs = [data(fpp, n, 48, 5, 0.3, seed=31 + i) for i, n in enumerate(sizes)]
+    Q = data(fpp, 40, 48, 5, 0.3, seed=31, stream=1)
+    idx = [fpp.Index.build(X, iProbes=3, **prm) for X in Xs]
+    want = [orc.Index(X, iprobes=3, **prm).query(Q, 10, 300)[:2] for X in Xs]
+    errors = []
+
+    def worker(i):
+        try:
+            for _ in range(150):
+                gi, gs = idx[i].query(Q, 10, 300)
+                assert np.array_equal(gi, want[i][0]) and np.array_equal(gs, want[i][1])
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors[:3]
+    # the library's own shard threads (no GIL between them): shards of 2561 / 2560 / 2560 points
+    X = data(fpp, 7681, 48, 5, 0.3, seed=893943846)
+    mx = fpp.MultiIndex.build(X, num_gpus=3, devices=[0] * 3, iProbes=3, **prm)
+    wi, ws = orc.Index(X, iprobes=3, **prm).query(Q[:4], 10, 300)[:2]
+    for _ in range(400):
+        gi, gs = mx.query(Q[:4], 10, 300)
+        assert np.array_equal(gi, wi) and np.array_equal(gs, ws)
+
+
 def test_device_calls_back_to_back_on_two_streams(fpp, orc):
     """consecutive fpp_query_device calls on different streams with
     no host sync in between must not overwrite each other's scratch."""
