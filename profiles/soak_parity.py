@@ -26,8 +26,16 @@ while time.time() - t0 < budget:
     kappa = int(rng.choice([0, 5, 20]))
     clusters = int(rng.choice([0, 5, 40]))
     seed = int(rng.integers(1, 1 << 30))
+    if rng.random() < 0.1:
+        n = int(rng.integers(20000, 60000))  # (a few larger shards)
     X = fpp.normalize(fpp.synth(n, d, clusters, 0.3, seed=seed))
-    Q = fpp.normalize(fpp.synth(int(rng.integers(1, 90)), d, clusters, 0.3, seed=seed, stream=1))
+    if rng.random() < 0.3:  # exact duplicates: equal scores, ties to the lower id
+        src = rng.integers(0, n, size=max(1, n // 50))
+        X[rng.integers(0, n, size=len(src))] = X[src]
+    nq = int(rng.integers(1, 90)) if rng.random() < 0.85 else int(rng.integers(600, 2500))
+    Q = fpp.normalize(fpp.synth(nq, d, clusters, 0.3, seed=seed, stream=1))
+    if rng.random() < 0.3:
+        Q[: min(nq, 5)] = X[: min(nq, 5)]  # queries that are data points
     prm = dict(L=L, K=K, D=D, alpha=alpha, kappa=kappa, seed=seed)
     # variants: falconn_baseline mode, centering, a 2..3-shard MultiIndex on one device
     variant = str(rng.choice(["plain", "plain", "baseline", "centering", "multi"]))
@@ -53,6 +61,19 @@ while time.time() - t0 < budget:
         stats = bool(rng.integers(0, 2))
         rr = int(rng.choice([0, 0, k, 3 * k, 50 * k])) if variant in ("plain", "baseline") else 0
         kw = dict(rerank=rr) if rr else {}
+        # scheduling / path switches (none may change a result)
+        for var in ("FPP_FORCE_COLLECT", "FPP_PRUNE", "FPP_NO_PRUNE", "FPP_NO_REORDER", "FPP_SERIAL"):
+            os.environ.pop(var, None)
+        env = {}
+        if rng.random() < 0.3:
+            env["FPP_FORCE_COLLECT"] = str(rng.choice(["grouped", "sliced", "cluster", "global"]))
+        if rng.random() < 0.3:
+            env[str(rng.choice(["FPP_PRUNE", "FPP_NO_PRUNE"]))] = "1"
+        if rng.random() < 0.2:
+            env["FPP_NO_REORDER"] = "1"
+        if rng.random() < 0.2:
+            env["FPP_SERIAL"] = "1"
+        os.environ.update(env)
         if os.environ.get("SOAK_LOG"):
             print("Q", dict(variant=variant, n=n, d=d, ip=ip, k=k, qp=qp, stats=stats, rerank=rr,
                             clusters=clusters, nq=len(Q), **prm), file=sys.stderr, flush=True)
@@ -62,7 +83,7 @@ while time.time() - t0 < budget:
             else:
                 gi, gs = ix.query(Q, k, qp, **kw)
         except Exception as ex:
-            print("EXCEPTION", ex, dict(variant=variant, n=n, d=d, ip=ip, k=k, qp=qp, stats=stats, rerank=rr,
+            print("EXCEPTION", ex, env, dict(variant=variant, n=n, d=d, ip=ip, k=k, qp=qp, stats=stats, rerank=rr,
                                         clusters=clusters, nq=len(Q), **prm), flush=True)
             sys.exit(2)
         oi, os_, ost = ox.query(Q, k, qp, **kw)
@@ -70,7 +91,7 @@ while time.time() - t0 < budget:
         ok = np.array_equal(gi, oi) and np.array_equal(gs, os_) and \
             (not stats or np.array_equal(gst[:, :ncol], ost[:, :ncol]))
         if not ok:
-            print("MISMATCH", dict(variant=variant, n=n, d=d, ip=ip, k=k, qp=qp, stats=stats, rerank=rr,
+            print("MISMATCH", env, dict(variant=variant, n=n, d=d, ip=ip, k=k, qp=qp, stats=stats, rerank=rr,
                                    clusters=clusters, nq=len(Q), **prm), flush=True)
             sys.exit(1)
     ix.close()
