@@ -28,11 +28,21 @@ while time.time() - t0 < budget:
     seed = int(rng.integers(1, 1 << 30))
     if rng.random() < 0.1:
         n = int(rng.integers(20000, 60000))  # (a few larger shards)
+    if os.environ.get("SOAK_BIG"):  # the walking screen at scale: admission hash / bitmap / log paths
+        d = int(rng.choice([64, 128, 128, 256]))
+        n = int(rng.integers(200_000, 1_500_000))
+        K, P = 2, d
+        D = d
+        ip, L = 3, int(rng.integers(4, 10))
+        alpha, kappa = float(rng.choice([0.01, 0.05, 0.3])), 20
+        clusters = int(rng.choice([100, 2000]))
     X = fpp.normalize(fpp.synth(n, d, clusters, 0.3, seed=seed))
     if rng.random() < 0.3:  # exact duplicates: equal scores, ties to the lower id
         src = rng.integers(0, n, size=max(1, n // 50))
         X[rng.integers(0, n, size=len(src))] = X[src]
     nq = int(rng.integers(1, 90)) if rng.random() < 0.85 else int(rng.integers(600, 2500))
+    if os.environ.get("SOAK_BIG"):
+        nq = 150
     Q = fpp.normalize(fpp.synth(nq, d, clusters, 0.3, seed=seed, stream=1))
     if rng.random() < 0.3:
         Q[: min(nq, 5)] = X[: min(nq, 5)]  # queries that are data points
