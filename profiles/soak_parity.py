@@ -37,6 +37,14 @@ while time.time() - t0 < budget:
         alpha, kappa = float(rng.choice([0.01, 0.05, 0.3])), 20
         clusters = int(rng.choice([100, 2000]))
     X = fpp.normalize(fpp.synth(n, d, clusters, 0.3, seed=seed))
+    if rng.random() < 0.15 and not os.environ.get("SOAK_BIG"):
+        # sparse rows (1-6 non-zeros): projections with many equal |p| -- tie order everywhere
+        m = int(rng.choice([1, 2, 3, 6]))
+        X = np.zeros((n, d), np.float32)
+        for i in range(n):
+            X[i, rng.choice(d, min(m, d), replace=False)] = rng.standard_normal(min(m, d)).astype(np.float32)
+        X[np.abs(X).sum(axis=1) == 0, 0] = 1.0
+        X = fpp.normalize(X)
     if rng.random() < 0.3:  # exact duplicates: equal scores, ties to the lower id
         src = rng.integers(0, n, size=max(1, n // 50))
         X[rng.integers(0, n, size=len(src))] = X[src]
